@@ -1,0 +1,508 @@
+// ref_capi.cpp -- C ABI over the UNMODIFIED reference headers
+// (/root/reference/proj/include/helmbench, compiled in place; nothing copied).
+// TEST INFRASTRUCTURE: built by oracle/build_ref.sh into oracle/_ref/ to pin the
+// C restatement (oracle/helm_oracle.c) and to serve as the CPU reference arm of
+// bench.py (--impl reference).  Entry points mirror oracle/helm_oracle.c.
+//
+// The BASELINE-config extensions are assembled here from
+// reference primitives only: Tape::conv2d / Tape::concat (inc/autodiff.hpp:124,403),
+// bilinear_resize (inc/datagen.hpp:19), StencilOperator::jacobi/residual,
+// restrict_field/prolong_field (inc/stencil.hpp:69-165), MultigridHierarchy
+// (inc/multigrid.hpp:70-125), block_fgmres (inc/krylov.hpp:83), Rng
+// (inc/rng.hpp).  New forward-only ops (ReLU, 2x2 max-pool) are loops on Tensor4.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <thread>
+
+#include "helmbench/datagen.hpp"
+#include "helmbench/grid.hpp"
+#include "helmbench/krylov.hpp"
+#include "helmbench/multigrid.hpp"
+#include "helmbench/precond.hpp"
+#include "helmbench/rng.hpp"
+#include "helmbench/stencil.hpp"
+#include "helmbench/tensor.hpp"
+#include "helmbench/unet.hpp"
+
+extern "C" void openblas_set_num_threads(int);
+
+using namespace helm;
+
+#define HR_EXPORT extern "C" __attribute__((visibility("default")))
+
+namespace {
+
+ComplexField to_field(const double* p, int nx, int ny) {
+  ComplexField f(nx, ny);
+  std::memcpy(f.v.data(), p, sizeof(Complex) * f.v.size());
+  return f;
+}
+void from_field(const ComplexField& f, double* p) { std::memcpy(p, f.v.data(), sizeof(Complex) * f.v.size()); }
+
+HelmholtzProblem make_prob(int nx, int ny, double omega, const double* k2, const double* gam, double lo, double hi) {
+  ProblemGrid g = make_grid(nx, ny, 1);
+  RealField K(nx, ny), G(nx, ny);
+  std::memcpy(K.v.data(), k2, sizeof(double) * K.v.size());
+  std::memcpy(G.v.data(), gam, sizeof(double) * G.v.size());
+  return make_problem(g, omega, make_slowness_squared(std::move(K), lo, hi), Attenuation{std::move(G)});
+}
+
+// ---------------- classic U-Net (oracle ext A5/A7) on the reference Tape ----
+struct ClassicNet {
+  int kind = 0, L = 0, base = 16, in_ch = 3, ctx_ch = 0;
+  std::vector<std::unique_ptr<Param>> k, b;  // creation order
+  int enc1[8], enc2[8], up[8], dec1[8], dec2[8], head = -1;
+  int add(int cout, int cin) {
+    auto pk = std::make_unique<Param>();
+    pk->value = Tensor4(cout, cin, 3, 3);
+    pk->trainable = false;
+    auto pb = std::make_unique<Param>();
+    pb->value = Tensor4(1, cout, 1, 1);
+    pb->trainable = false;
+    k.push_back(std::move(pk));
+    b.push_back(std::move(pb));
+    return int(k.size()) - 1;
+  }
+};
+
+Tensor4 relu(Tensor4 t) {
+  for (auto& x : t.v) x = x < 0.0f ? 0.0f : x;
+  return t;
+}
+Tensor4 maxpool2(const Tensor4& a) {
+  Tensor4 o(a.n, a.c, a.h / 2, a.w / 2);
+  for (int n = 0; n < a.n; ++n)
+    for (int c = 0; c < a.c; ++c)
+      for (int y = 0; y < o.h; ++y)
+        for (int x = 0; x < o.w; ++x)
+          o.at(n, c, y, x) = std::max(std::max(a.at(n, c, 2 * y, 2 * x), a.at(n, c, 2 * y, 2 * x + 1)),
+                                      std::max(a.at(n, c, 2 * y + 1, 2 * x), a.at(n, c, 2 * y + 1, 2 * x + 1)));
+  return o;
+}
+// x2 bilinear with half-pixel centres / clamped edges = bilinear_resize per plane
+Tensor4 upsample2(const Tensor4& a) {
+  Tensor4 o(a.n, a.c, 2 * a.h, 2 * a.w);
+  RealField src(a.w, a.h);
+  for (int n = 0; n < a.n; ++n)
+    for (int c = 0; c < a.c; ++c) {
+      for (int y = 0; y < a.h; ++y)
+        for (int x = 0; x < a.w; ++x) src.at(x, y) = a.at(n, c, y, x);
+      RealField dst = bilinear_resize(src, 2 * a.w, 2 * a.h);
+      for (int y = 0; y < o.h; ++y)
+        for (int x = 0; x < o.w; ++x) o.at(n, c, y, x) = float(dst.at(x, y));
+    }
+  return o;
+}
+
+Tensor4 conv(Tape& tape, ClassicNet& net, int i, const Tensor4& x) {
+  const int id = tape.leaf(x);
+  return tape.value(tape.conv2d(id, *net.k[std::size_t(i)], net.b[std::size_t(i)].get(), 1));
+}
+Tensor4 cat(Tape& tape, const Tensor4& a, const Tensor4& b) {
+  const Tensor4 bb = (b.n == a.n) ? b : tile_batch(b, a.n);
+  return tape.value(tape.concat(tape.leaf(a), tape.leaf(bb)));
+}
+
+Tensor4 unet_fwd(ClassicNet& n, const Tensor4& in, const std::vector<Tensor4>* ctx) {
+  Tape tape(false);
+  std::vector<Tensor4> skip(std::size_t(n.L));
+  Tensor4 x = in;
+  for (int l = 0; l < n.L; ++l) {
+    if (l > 0) x = maxpool2(x);
+    if (ctx) x = cat(tape, x, (*ctx)[std::size_t(l)]);
+    x = relu(conv(tape, n, n.enc1[l], x));
+    x = relu(conv(tape, n, n.enc2[l], x));
+    skip[std::size_t(l)] = x;
+  }
+  for (int l = n.L - 2; l >= 0; --l) {
+    if (ctx) x = cat(tape, x, (*ctx)[std::size_t(l + 1)]);
+    x = conv(tape, n, n.up[l], upsample2(x));
+    x = cat(tape, x, skip[std::size_t(l)]);
+    x = relu(conv(tape, n, n.dec1[l], x));
+    x = relu(conv(tape, n, n.dec2[l], x));
+  }
+  return conv(tape, n, n.head, x);
+}
+
+std::vector<Tensor4> encoder_fwd(ClassicNet& e, const Tensor4& kappa) {
+  Tape tape(false);
+  std::vector<Tensor4> ctx;
+  Tensor4 x = kappa;
+  for (int l = 0; l < e.L; ++l) {
+    if (l > 0) x = maxpool2(x);
+    x = relu(conv(tape, e, e.enc1[l], x));
+    x = relu(conv(tape, e, e.enc2[l], x));
+    ctx.push_back(x);
+  }
+  return ctx;
+}
+
+// network applier: [H^2 Re f, H^2 Im f, kappa^2] -> complex (inc/precond.hpp:71-91 pattern)
+ComplexField net_apply(ClassicNet& n, const ComplexField& f, const RealField& k2, double h,
+                       const std::vector<Tensor4>* ctx) {
+  const double h2 = h * h;
+  Tensor4 in(1, 3, f.ny, f.nx);
+  for (int y = 0; y < f.ny; ++y)
+    for (int x = 0; x < f.nx; ++x) {
+      in.at(0, 0, y, x) = float(h2 * f.at(x, y).real());
+      in.at(0, 1, y, x) = float(h2 * f.at(x, y).imag());
+      in.at(0, 2, y, x) = float(k2.at(x, y));
+    }
+  return complex_from_channels(unet_fwd(n, in, ctx), 0);
+}
+
+struct RefMG {
+  HelmholtzProblem prob;
+  VCycleConfig cfg;
+  std::shared_ptr<MultigridHierarchy> hier;  // coarse GMRES / dense levels
+  int coarse_kind = 0;                        // 0 gmres, 1 jacobi (A3), 2 net (A4)
+  ClassicNet* coarse_net = nullptr;
+};
+
+// public-API restatement of MultigridHierarchy::cycle_at (inc/multigrid.hpp:108-119)
+// with the coarsest solve replaced (A3 Jacobi / A4 net)
+ComplexField cycle_ext(const RefMG& m, int level, ComplexField v, const ComplexField& f) {
+  const MultigridHierarchy& H = *m.hier;
+  const StencilOperator& op = H.op(level);
+  if (level == H.levels() - 1) {
+    if (m.coarse_kind == 1) return op.jacobi(ComplexField(f.nx, f.ny), f, m.cfg.damping, m.cfg.coarse_iters);
+    return net_apply(*m.coarse_net, f, H.problem(level).kappa2.values, H.problem(level).grid.h, nullptr);
+  }
+  const int offset = level % 2;
+  v = op.jacobi(std::move(v), f, m.cfg.damping, m.cfg.nu1);
+  ComplexField r = op.residual(v, f);
+  ComplexField fc = restrict_field(r, offset);
+  ComplexField vc = cycle_ext(m, level + 1, ComplexField(fc.nx, fc.ny), fc);
+  ComplexField corr = prolong_field(vc, offset);
+  for (std::size_t i = 0; i < v.v.size(); ++i) v.v[i] += corr.v[i];
+  return op.jacobi(std::move(v), f, m.cfg.damping, m.cfg.nu2);
+}
+
+ComplexField cycle(const RefMG& m, ComplexField v, const ComplexField& f) {
+  if (m.coarse_kind == 0) return m.hier->cycle(std::move(v), f);
+  return cycle_ext(m, 0, std::move(v), f);
+}
+
+struct RefPC : Preconditioner {
+  RefMG* mg;
+  int kind;  // 0 M_V / coarse-net cycle, 1 M_VU (A8)
+  ClassicNet* net = nullptr;
+  std::vector<Tensor4> ctx;
+  bool has_ctx = false;
+  std::vector<ComplexField> apply(const std::vector<ComplexField>& r) override {
+    std::vector<ComplexField> out;
+    for (const auto& col : r) {
+      ComplexField v0(col.nx, col.ny);
+      if (kind == 1)
+        v0 = net_apply(*net, col, mg->prob.kappa2.values, mg->prob.grid.h, has_ctx ? &ctx : nullptr);
+      out.push_back(cycle(*mg, std::move(v0), col));
+    }
+    return out;
+  }
+  bool requires_flexible() const override { return kind == 1 || mg->coarse_kind == 2; }
+  std::string name() const override { return kind == 1 ? "vu" : "v"; }
+};
+
+thread_local std::string g_err;
+
+}  // namespace
+
+#define HR_TRY(...)                   \
+  try {                               \
+    __VA_ARGS__;                      \
+    return 0;                         \
+  } catch (const std::exception& e) { \
+    g_err = e.what();                 \
+    return -1;                        \
+  }
+
+HR_EXPORT const char* hr_last_error() { return g_err.c_str(); }
+
+HR_EXPORT void hr_init() { openblas_set_num_threads(1); }
+
+HR_EXPORT void hr_rng_normals(uint64_t seed, int64_t n, double* out) {
+  Rng r(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+HR_EXPORT void hr_rng_u64(uint64_t seed, int64_t n, uint64_t* out) {
+  Rng r(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.next_u64();
+}
+
+HR_EXPORT int hr_absorbing_layer(int nx, int ny, int width, double gmax, double* out) {
+  HR_TRY({
+    auto att = make_absorbing_layer(make_grid(nx, ny, 1), width, gmax);
+    std::memcpy(out, att.values.v.data(), sizeof(double) * att.values.v.size());
+  })
+}
+
+HR_EXPORT int hr_restrict(int nx, int ny, int offset, int ncomp, const double* fine, double* coarse) {
+  HR_TRY({
+    if (ncomp == 1) {
+      RealField f(nx, ny);
+      std::memcpy(f.v.data(), fine, sizeof(double) * f.v.size());
+      auto c = restrict_field(f, offset);
+      std::memcpy(coarse, c.v.data(), sizeof(double) * c.v.size());
+    } else {
+      auto c = restrict_field(to_field(fine, nx, ny), offset);
+      from_field(c, coarse);
+    }
+  })
+}
+HR_EXPORT int hr_prolong(int cnx, int cny, int offset, int ncomp, const double* coarse, double* fine) {
+  HR_TRY({
+    if (ncomp == 1) {
+      RealField c(cnx, cny);
+      std::memcpy(c.v.data(), coarse, sizeof(double) * c.v.size());
+      auto f = prolong_field(c, offset);
+      std::memcpy(fine, f.v.data(), sizeof(double) * f.v.size());
+    } else {
+      from_field(prolong_field(to_field(coarse, cnx, cny), offset), fine);
+    }
+  })
+}
+
+// ---- hierarchy
+HR_EXPORT void* hr_mg_create(int nx, int ny, double omega, const double* k2, const double* gam, double lo, double hi,
+                             int levels, int nu1, int nu2, double damping, double alpha, double beta, int coarse_kind,
+                             int coarse_iters) {
+  try {
+    auto* m = new RefMG();
+    m->prob = make_prob(nx, ny, omega, k2, gam, lo, hi);
+    m->cfg.levels = levels;
+    m->cfg.nu1 = nu1;
+    m->cfg.nu2 = nu2;
+    m->cfg.damping = damping;
+    m->cfg.shift = Shift{alpha, beta};
+    m->cfg.coarse_iters = coarse_iters;
+    m->cfg.coarse_solver = coarse_kind == 3 ? CoarseSolver::dense : CoarseSolver::gmres;
+    m->coarse_kind = coarse_kind == 3 ? 0 : coarse_kind;
+    m->hier = std::make_shared<MultigridHierarchy>(m->prob, m->cfg);
+    return m;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+HR_EXPORT void hr_mg_destroy(void* p) { delete static_cast<RefMG*>(p); }
+
+HR_EXPORT void hr_mg_level_coef(void* p, int l, double* k2, double* gam, double* diagA, double* diagM) {
+  auto* m = static_cast<RefMG*>(p);
+  const auto& pr = m->hier->problem(l);
+  const std::size_t n = pr.kappa2.values.v.size();
+  if (k2) std::memcpy(k2, pr.kappa2.values.v.data(), n * sizeof(double));
+  if (gam) std::memcpy(gam, pr.gamma.values.v.data(), n * sizeof(double));
+  if (diagA) {
+    StencilOperator A(pr, kHelmholtzShift);
+    std::memcpy(diagA, A.diagonal().data(), n * sizeof(Complex));
+  }
+  if (diagM) std::memcpy(diagM, m->hier->op(l).diagonal().data(), n * sizeof(Complex));
+}
+
+HR_EXPORT int hr_apply(void* p, int l, int which, const double* u, double* y) {
+  HR_TRY({
+    auto* m = static_cast<RefMG*>(p);
+    const auto& pr = m->hier->problem(l);
+    StencilOperator A(pr, which ? m->cfg.shift : kHelmholtzShift);
+    from_field(A.apply(to_field(u, pr.grid.nx, pr.grid.ny)), y);
+  })
+}
+HR_EXPORT int hr_jacobi(void* p, int l, int which, double* v, const double* f, double damping, int iters) {
+  HR_TRY({
+    auto* m = static_cast<RefMG*>(p);
+    const auto& pr = m->hier->problem(l);
+    StencilOperator A(pr, which ? m->cfg.shift : kHelmholtzShift);
+    const int nx = pr.grid.nx, ny = pr.grid.ny;
+    from_field(A.jacobi(to_field(v, nx, ny), to_field(f, nx, ny), damping, iters), v);
+  })
+}
+HR_EXPORT int hr_coarse_gmres(void* p, int l, const double* f, double* x) {
+  HR_TRY({
+    auto* m = static_cast<RefMG*>(p);
+    const auto& pr = m->hier->problem(l);
+    from_field(coarse_solve_with_op(m->hier->op(l), to_field(f, pr.grid.nx, pr.grid.ny), m->cfg), x);
+  })
+}
+
+// ---- classic nets
+HR_EXPORT void* hr_net_create(int kind, int L, int base, int in_ch, int ctx_ch) {
+  auto* n = new ClassicNet();
+  n->kind = kind;
+  n->L = L;
+  n->base = base;
+  n->in_ch = in_ch;
+  n->ctx_ch = ctx_ch;
+  if (kind == 1) {
+    for (int l = 0; l < L; ++l) {
+      n->enc1[l] = n->add(base, l == 0 ? in_ch : base);
+      n->enc2[l] = n->add(base, base);
+    }
+    return n;
+  }
+  for (int l = 0; l < L; ++l) {
+    n->enc1[l] = n->add(base << l, (l == 0 ? in_ch : base << (l - 1)) + ctx_ch);
+    n->enc2[l] = n->add(base << l, base << l);
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    n->up[l] = n->add(base << l, (base << (l + 1)) + ctx_ch);
+    n->dec1[l] = n->add(base << l, 2 * (base << l));
+    n->dec2[l] = n->add(base << l, base << l);
+  }
+  n->head = n->add(2, base);
+  return n;
+}
+HR_EXPORT void hr_net_destroy(void* p) { delete static_cast<ClassicNet*>(p); }
+HR_EXPORT int hr_net_nconv(void* p) { return int(static_cast<ClassicNet*>(p)->k.size()); }
+HR_EXPORT float* hr_net_weight(void* p, int i) { return static_cast<ClassicNet*>(p)->k[std::size_t(i)]->value.v.data(); }
+HR_EXPORT float* hr_net_bias(void* p, int i) { return static_cast<ClassicNet*>(p)->b[std::size_t(i)]->value.v.data(); }
+// He-normal (A6) via fill_normal semantics (inc/tensor.hpp:51-53)
+HR_EXPORT void hr_net_init_he(void* p, uint64_t seed) {
+  auto* n = static_cast<ClassicNet*>(p);
+  Rng rng(seed);
+  for (std::size_t i = 0; i < n->k.size(); ++i) {
+    auto& t = n->k[i]->value;
+    fill_normal(t, rng, float(std::sqrt(2.0 / double(t.c * 9))));
+    std::fill(n->b[i]->value.v.begin(), n->b[i]->value.v.end(), 0.0f);
+  }
+}
+HR_EXPORT int hr_net_forward(void* p, int B, int H, int W, const float* in, const float* const* ctx, float* out) {
+  HR_TRY({
+    auto* n = static_cast<ClassicNet*>(p);
+    Tensor4 x(B, n->in_ch, H, W);
+    std::memcpy(x.v.data(), in, sizeof(float) * x.v.size());
+    std::vector<Tensor4> cx;
+    if (ctx)
+      for (int l = 0; l < n->L; ++l) {
+        Tensor4 t(1, n->ctx_ch, H >> l, W >> l);
+        std::memcpy(t.v.data(), ctx[l], sizeof(float) * t.v.size());
+        cx.push_back(std::move(t));
+      }
+    Tensor4 y = unet_fwd(*n, x, ctx ? &cx : nullptr);
+    std::memcpy(out, y.v.data(), sizeof(float) * y.v.size());
+  })
+}
+HR_EXPORT int hr_encoder_forward(void* p, int H, int W, const float* kappa, float** ctx) {
+  HR_TRY({
+    auto* e = static_cast<ClassicNet*>(p);
+    Tensor4 k(1, 1, H, W);
+    std::memcpy(k.v.data(), kappa, sizeof(float) * k.v.size());
+    auto c = encoder_fwd(*e, k);
+    for (int l = 0; l < e->L; ++l) std::memcpy(ctx[l], c[std::size_t(l)].v.data(), sizeof(float) * c[std::size_t(l)].v.size());
+  })
+}
+// raw Tape::conv2d (3x3 or 5x5, stride 1 or 2) for the conv KATs
+HR_EXPORT int hr_conv2d(int N, int cin, int cout, int H, int W, int k, int stride, const float* x, const float* w,
+                        const float* b, float* y) {
+  HR_TRY({
+    Param K, Bp;
+    K.value = Tensor4(cout, cin, k, k);
+    std::memcpy(K.value.v.data(), w, sizeof(float) * K.value.v.size());
+    Bp.value = Tensor4(1, cout, 1, 1);
+    std::memcpy(Bp.value.v.data(), b, sizeof(float) * cout);
+    K.trainable = Bp.trainable = false;
+    Tape tape(false);
+    Tensor4 xt(N, cin, H, W);
+    std::memcpy(xt.v.data(), x, sizeof(float) * xt.v.size());
+    const Tensor4& o = tape.value(tape.conv2d(tape.leaf(xt), K, &Bp, stride));
+    std::memcpy(y, o.v.data(), sizeof(float) * o.v.size());
+  })
+}
+
+// ---- preconditioners + solve
+HR_EXPORT void hr_mg_set_coarse_net(void* mg, void* net) {
+  auto* m = static_cast<RefMG*>(mg);
+  m->coarse_net = static_cast<ClassicNet*>(net);
+}
+
+HR_EXPORT void* hr_pc_create(int kind, void* mg, void* net, void* enc) {
+  auto* pc = new RefPC();
+  pc->mg = static_cast<RefMG*>(mg);
+  pc->kind = kind;
+  pc->net = static_cast<ClassicNet*>(net);
+  if (enc) {  // encoder runs once per medium (inc/precond.hpp:66-67)
+    auto* e = static_cast<ClassicNet*>(enc);
+    const auto& K = pc->mg->prob.kappa2.values;
+    Tensor4 k(1, 1, K.ny, K.nx);
+    for (int y = 0; y < K.ny; ++y)
+      for (int x = 0; x < K.nx; ++x) k.at(0, 0, y, x) = float(K.at(x, y));
+    pc->ctx = encoder_fwd(*e, k);
+    pc->has_ctx = true;
+  }
+  return pc;
+}
+HR_EXPORT void hr_pc_destroy(void* p) { delete static_cast<RefPC*>(p); }
+HR_EXPORT int hr_pc_apply(void* p, int B, const double* r, double* z) {
+  HR_TRY({
+    auto* pc = static_cast<RefPC*>(p);
+    const int nx = pc->mg->prob.grid.nx, ny = pc->mg->prob.grid.ny;
+    std::vector<ComplexField> R;
+    for (int b = 0; b < B; ++b) R.push_back(to_field(r + std::size_t(b) * nx * ny * 2, nx, ny));
+    auto Z = pc->apply(R);
+    for (int b = 0; b < B; ++b) from_field(Z[std::size_t(b)], z + std::size_t(b) * nx * ny * 2);
+  })
+}
+
+// block FGMRES through the reference's own entry point, exactly as
+// run_preconditioner_test (inc/bench.hpp:93-110).  nthreads > 1 splits the
+// columns into contiguous independent blocks (columns are independent,
+// tests/test_classic.cpp:469-508), each with its own preconditioner object.
+HR_EXPORT int hr_fgmres(void* p, int restart, int max_iters, double rel_tol, int flexible, int B, const double* b,
+                        double* x, double* hist, int hist_cap, int* iters, int* conv, int* brk, int* hlen,
+                        int nthreads, double* seconds) {
+  HR_TRY({
+    auto* pc0 = static_cast<RefPC*>(p);
+    const int nx = pc0->mg->prob.grid.nx, ny = pc0->mg->prob.grid.ny;
+    const std::size_t n2 = std::size_t(nx) * ny * 2;
+    KrylovConfig cfg;
+    cfg.restart = restart;
+    cfg.max_iters = max_iters;
+    cfg.rel_tol = rel_tol;
+    cfg.flexible = flexible != 0;
+    check_flexible_contract(cfg, *pc0);
+    StencilOperator A(pc0->mg->prob, kHelmholtzShift);
+    BatchedOp apply_A = [&A](const std::vector<ComplexField>& in) {
+      std::vector<ComplexField> out;
+      out.reserve(in.size());
+      for (const auto& f : in) out.push_back(A.apply(f));
+      return out;
+    };
+    const int T = std::max(1, std::min(nthreads, B));
+    std::vector<std::string> errs;
+    errs.resize(std::size_t(T));
+    auto work = [&](int t) {
+      try {
+        const int c0 = B * t / T, c1 = B * (t + 1) / T;
+        RefPC pc = *pc0;  // per-thread preconditioner object (same weights, shared ctx)
+        std::vector<ComplexField> Bc;
+        for (int c = c0; c < c1; ++c) Bc.push_back(to_field(b + std::size_t(c) * n2, nx, ny));
+        auto [X, rep] = block_fgmres(apply_A, pc.as_batched_op(), Bc, cfg);
+        for (int c = c0; c < c1; ++c) {
+          const std::size_t q = std::size_t(c - c0);
+          from_field(X[q], x + std::size_t(c) * n2);
+          const auto& h = rep.residual_history[q];
+          hlen[c] = int(h.size());
+          for (int i = 0; i < std::min<int>(hist_cap, int(h.size())); ++i) hist[std::size_t(c) * hist_cap + i] = h[std::size_t(i)];
+          iters[c] = rep.iterations[q];
+          conv[c] = rep.converged[q] ? 1 : 0;
+          brk[c] = rep.breakdown[q] ? 1 : 0;
+        }
+      } catch (const std::exception& e) {
+        errs[std::size_t(t)] = e.what();
+      }
+    };
+    const auto t0 = std::chrono::steady_clock::now();
+    if (T == 1) {
+      work(0);
+    } else {
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t) th.emplace_back(work, t);
+      for (auto& h : th) h.join();
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+    for (auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+  })
+}

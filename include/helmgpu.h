@@ -1,0 +1,173 @@
+/*
+ * helmgpu.h -- C ABI of the B200-native (sm_100a) hot path of arXiv 2203.11025:
+ * flexible GMRES on the heterogeneous 2-D Helmholtz operator, preconditioned by
+ * a shifted-Laplacian multigrid V-cycle combined with a U-Net (coarse solver or
+ * deflation guess), optionally with an encoder network.
+ *
+ * Plain C, plain pointers and sizes.  Host buffers are caller-owned, device
+ * buffers are library-owned.  One hb_ctx per GPU, used by one host thread.
+ * Every call returns 0 on success, or a negative status with the message in
+ * hb_last_error(ctx).  Complex fields are interleaved (re, im) doubles
+ * (std::complex<double>, inc/grid.hpp:11), row-major iy*nx+ix
+ * (inc/grid.hpp:22-36); batches are contiguous [batch][ny][nx].
+ *
+ * Reference interfaces each entry point replaces (inc/ =
+ * /root/reference/proj/include/helmbench/):
+ *   hb_set_problem      make_problem / HelmholtzProblem        inc/grid.hpp:121-141
+ *   hb_build_hierarchy  MultigridHierarchy(problem, VCycleConfig) inc/multigrid.hpp:13-21,72-86
+ *   hb_operator_apply   StencilOperator::apply                 inc/stencil.hpp:44-60
+ *   hb_jacobi           StencilOperator::jacobi                inc/stencil.hpp:78-92
+ *   hb_restrict/prolong restrict_field / prolong_field         inc/stencil.hpp:119-165
+ *   hb_cycle            MultigridHierarchy::cycle              inc/multigrid.hpp:92,108-119
+ *   hb_set_net / hb_load_conv / hb_init_net_he
+ *                       NetworkWeights + build_unet/build_encoder (classic U-Net)
+ *                                                              inc/unet.hpp:10-33,171-257
+ *   hb_net_forward      unet_forward / solver_forward          inc/unet.hpp:261-295
+ *   hb_precond_apply    Preconditioner::apply (M_V / coarse-net cycle / M_VU)
+ *                                                              inc/precond.hpp:14-27,35-53,143-165
+ *   hb_fgmres           block_fgmres (device-resident)         inc/krylov.hpp:83-267
+ */
+#ifndef HELMGPU_H_
+#define HELMGPU_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+typedef struct hb_ctx hb_ctx;
+
+#define HB_OK 0
+#define HB_ERR_ARG (-1)     /* std::invalid_argument in the reference */
+#define HB_ERR_CUDA (-2)    /* device / runtime failure */
+#define HB_ERR_STATE (-3)   /* call order (e.g. no problem set) */
+#define HB_ERR_NUMERIC (-4) /* std::runtime_error (zero diagonal, ...) */
+
+/* ---- context ---------------------------------------------------------- */
+int hb_create(int device, hb_ctx** out);
+void hb_destroy(hb_ctx* ctx);
+const char* hb_last_error(const hb_ctx* ctx); /* ctx may be NULL: last create error */
+/* cudaStream_t the library launches on (for event timing by the caller) */
+void* hb_stream(hb_ctx* ctx);
+int hb_synchronize(hb_ctx* ctx);
+
+/* ---- problem + hierarchy ------------------------------------------------ */
+/* kappa2, gamma: nx*ny doubles; enforces the reference's contracts
+ * (inc/grid.hpp:72-78,128-141): kappa2 in [lo, hi], omega*sqrt(max kappa2)*h <= 0.6284. */
+int hb_set_problem(hb_ctx* ctx, int nx, int ny, double h, double omega, const double* kappa2,
+                   const double* gamma, double kappa_lo, double kappa_hi);
+
+#define HB_COARSE_GMRES 0  /* GMRES(coarse_iters) with D^-1, inc/multigrid.hpp:45-61 */
+#define HB_COARSE_JACOBI 1 /* coarse_iters damped-Jacobi sweeps */
+#define HB_COARSE_NET 2    /* U-Net in net slot 0 as coarsest solver */
+
+typedef struct hb_vcycle_cfg {
+  int levels;          /* >= 2 (inc/multigrid.hpp:73) */
+  int nu1, nu2;        /* pre/post damped-Jacobi sweeps */
+  double damping;      /* 0.8 */
+  double alpha, beta;  /* shift (1, 0.5) */
+  int coarse_solver;   /* HB_COARSE_* */
+  int coarse_iters;    /* GMRES restart / Jacobi sweeps */
+} hb_vcycle_cfg;
+
+int hb_build_hierarchy(hb_ctx* ctx, const hb_vcycle_cfg* cfg);
+/* level geometry after coarsening (inc/stencil.hpp:169-185) */
+int hb_level_info(hb_ctx* ctx, int level, int* nx, int* ny, double* h);
+
+/* ---- networks (classic U-Net) ------------------------ */
+#define HB_NET_SOLVER 0
+#define HB_NET_ENCODER 1
+typedef struct hb_net_cfg {
+  int kind;    /* HB_NET_SOLVER or HB_NET_ENCODER */
+  int levels;  /* resolution levels L */
+  int base;    /* channels at level 0 (16) */
+  int in_ch;   /* 3 for the solver (h^2 Re r, h^2 Im r, kappa^2), 1 for the encoder */
+  int ctx_ch;  /* encoder context channels concatenated per level (0 = standalone) */
+} hb_net_cfg;
+/* slot 0: solver / coarse net, slot 1: encoder */
+int hb_set_net(hb_ctx* ctx, int slot, const hb_net_cfg* cfg);
+int hb_net_num_convs(hb_ctx* ctx, int slot);
+int hb_net_conv_shape(hb_ctx* ctx, int slot, int index, int* cout, int* cin);
+/* weights (cout, cin, 3, 3) OIHW fp32 + bias (cout) in creation order */
+int hb_load_conv(hb_ctx* ctx, int slot, int index, const float* w, const float* b);
+/* He-normal init from Rng(seed) in creation order (inc/tensor.hpp:51-53) */
+int hb_init_net_he(hb_ctx* ctx, int slot, uint64_t seed);
+int hb_get_conv(hb_ctx* ctx, int slot, int index, float* w, float* b);
+/* forward on host NCHW buffers: in (B, in_ch, H, W) -> out (B, 2, H, W);
+ * ctx maps from the encoder are used when the solver net has ctx_ch > 0 and
+ * hb_encode has been run.  Test hook (unet_forward, inc/unet.hpp:261). */
+int hb_net_forward(hb_ctx* ctx, int batch, int H, int W, const float* in, float* out);
+/* encoder over the fine kappa^2 (run once per medium, cached on device). */
+int hb_encode(hb_ctx* ctx);
+int hb_get_context(hb_ctx* ctx, int level, float* out); /* (base, H>>l, W>>l) */
+
+/* ---- operators (parity hooks, host c128 buffers) ------------------------ */
+int hb_operator_apply(hb_ctx* ctx, int level, int shifted, int batch, const double* u, double* y);
+int hb_jacobi(hb_ctx* ctx, int level, int batch, double* v, const double* f, int iters);
+int hb_restrict(hb_ctx* ctx, int level, int batch, const double* fine, double* coarse);
+int hb_prolong(hb_ctx* ctx, int level, int batch, const double* coarse, double* fine);
+int hb_coarse_solve(hb_ctx* ctx, int batch, const double* f, double* x);
+
+/* ---- preconditioners ----------------------------------------------------- */
+#define HB_PC_V 0  /* SL V-cycle from zero (M_V; with HB_COARSE_NET = coarse-net cycle) */
+#define HB_PC_VU 1 /* e0 = net(h^2 r, kappa^2) then V-cycle from e0 (M_VU) */
+int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* z);
+/* name() and requires_flexible() of the reference plugin (inc/precond.hpp:14-27) */
+const char* hb_precond_name(int kind);
+int hb_precond_requires_flexible(hb_ctx* ctx, int kind);
+
+/* ---- FGMRES -------------------------------------------------------------- */
+typedef struct hb_krylov_cfg {
+  int restart;    /* m */
+  int max_iters;  /* preconditioner applications per column */
+  double rel_tol; /* in (0, 1) */
+  int flexible;   /* must be 1 (device path stores Z) */
+} hb_krylov_cfg;
+
+/* Solve A X = B for `batch` independent columns (block_fgmres semantics).
+ * B, X0 (may be NULL), X: host c128 [batch][ny][nx].  hist: [batch][hist_stride]
+ * absolute residual history (entry 0 = ||b - A x0||, then |g_{j+1}|);
+ * hist_len/iters per column; converged/breakdown flags per column. */
+int hb_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,
+              double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
+              uint8_t* breakdown);
+/* Same, with B and X as DEVICE c128 buffers (inputs resident in HBM); the
+ * report arrays are host buffers and may be NULL. */
+int hb_fgmres_device(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const void* dB, void* dX,
+                     double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
+                     uint8_t* breakdown);
+
+/* ---- setup helpers (host restatements of the reference RNG / generators) -- */
+/* Rng (inc/rng.hpp:9-67): n normals from Rng(seed) */
+void hb_rng_normals(uint64_t seed, int64_t n, double* out);
+/* absorbing layer (inc/grid.hpp:101-119) */
+int hb_absorbing_layer(int nx, int ny, int width, double gamma_max, double* out);
+/* medium generator SURVEY A1 (+D7 interfaces) -> kappa^2 */
+int hb_make_medium(int nx, int ny, uint64_t seed, double sigma, double vmin, double vmax, int n_interfaces,
+                   uint64_t iface_seed, int iface_margin, double jmin, double jmax, double* kappa2);
+/* point sources SURVEY A2 (mode 0: uniform (x, y) in [lo, hi]^2, mode 1: on `row`) */
+void hb_point_sources(uint64_t seed, int batch, int mode, int lo, int hi, int row, int* xs, int* ys);
+
+/* ---- instrumentation ------------------------------------------------------ */
+/* per-kernel-class device time (CUDA events on the library stream), for the
+ * roofline numerator/denominator in bench.py.  classes: see hb_prof_name. */
+int hb_prof_enable(hb_ctx* ctx, int on);
+int hb_prof_reset(hb_ctx* ctx);
+int hb_prof_count(hb_ctx* ctx);
+const char* hb_prof_name(hb_ctx* ctx, int i);
+int hb_prof_get(hb_ctx* ctx, int i, double* total_ms, int64_t* launches, double* bytes, double* flops);
+/* number of library kernel launches since the last reset */
+int64_t hb_launch_count(hb_ctx* ctx);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* HELMGPU_H_ */

@@ -1,0 +1,699 @@
+// libhelmgpu host runtime + C ABI (include/helmgpu.h).
+//
+// The host owns: problem setup and fp64 coefficient coarsening (as
+// coarsen_problem, inc/stencil.hpp:169-185, offset (l-1)%2 per
+// inc/multigrid.hpp:80-81), the V-cycle schedule (cycle_at,
+// inc/multigrid.hpp:108-119), the preconditioner plugins (inc/precond.hpp) and
+// the FGMRES restart loop; every arithmetic step runs on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hb_host.h"
+#include "hb_internal.h"
+
+namespace hb {
+
+void krylov_report(Context& c, int B, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv,
+                   uint8_t* brk);
+
+// ------------------------------------------------------------ profiling --
+static const char* kProfNames[PC_COUNT] = {"stencil",        "smooth",         "vcycle_down",   "vcycle_up",
+                                           "transfer",       "coarse_solve",   "krylov_adots",  "krylov_update",
+                                           "krylov_restart", "krylov_finalize", "conv3x3",      "net_io"};
+
+int prof_begin(Context& c, int cls) {
+  (void)cls;
+  c.launches++;
+  if (!c.prof_on) return -1;
+  cudaEvent_t a, b;
+  if (c.ev_pool.size() >= 2) {
+    a = c.ev_pool.back();
+    c.ev_pool.pop_back();
+    b = c.ev_pool.back();
+    c.ev_pool.pop_back();
+  } else {
+    HB_CUDA(cudaEventCreate(&a));
+    HB_CUDA(cudaEventCreate(&b));
+  }
+  HB_CUDA(cudaEventRecord(a, c.stream));
+  c.ev_pending.push_back({cls, {a, b}});
+  return int(c.ev_pending.size()) - 1;
+}
+
+void prof_collect(Context& c) {
+  if (c.ev_pending.empty()) return;
+  HB_CUDA(cudaStreamSynchronize(c.stream));
+  for (auto& e : c.ev_pending) {
+    float ms = 0.f;
+    HB_CUDA(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+    c.prof[size_t(e.first)].ms += ms;
+    c.ev_pool.push_back(e.second.first);
+    c.ev_pool.push_back(e.second.second);
+  }
+  c.ev_pending.clear();
+}
+
+void prof_end(Context& c, int cls, int token, double bytes, double flops) {
+  if (token < 0) return;
+  HB_CUDA(cudaEventRecord(c.ev_pending[size_t(token)].second.second, c.stream));
+  Prof& p = c.prof[size_t(cls)];
+  p.launches += 1;
+  p.bytes += bytes;
+  p.flops += flops;
+  if (c.ev_pending.size() > 8192) prof_collect(c);
+}
+
+// ------------------------------------------------------------- helpers --
+static std::vector<float2> to_c64(const double* p, size_t n) {
+  std::vector<float2> v(n);
+  for (size_t i = 0; i < n; ++i) v[i] = make_float2(float(p[2 * i]), float(p[2 * i + 1]));
+  return v;
+}
+static void from_c64(const std::vector<float2>& v, double* p) {
+  for (size_t i = 0; i < v.size(); ++i) {
+    p[2 * i] = v[i].x;
+    p[2 * i + 1] = v[i].y;
+  }
+}
+
+static void require_hier(Context& c) {
+  if (!c.has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built (hb_build_hierarchy)"};
+}
+
+static void fill_level_device(Level& L, double omega, double alpha, double beta, bool fp64A) {
+  const size_t n = L.N();
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  std::vector<float2> dm(n), da(n);
+  std::vector<double2> da64(fp64A ? n : 0);
+  std::vector<float> kf(n);
+  const std::complex<double> sh(alpha, -beta), sh0(1.0, 0.0);
+  for (size_t i = 0; i < n; ++i) {
+    // inc/stencil.hpp:27-34: d = 4/h^2 - omega^2 kappa^2 (alpha - beta i)(1 - gamma i)
+    const std::complex<double> damp(1.0, -L.gam[i]);
+    const std::complex<double> mM = -omega * omega * L.k2[i] * sh * damp;
+    const std::complex<double> mA = -omega * omega * L.k2[i] * sh0 * damp;
+    const std::complex<double> dMd = 4.0 * inv_h2 + mM, dAd = 4.0 * inv_h2 + mA;
+    if (dMd == 0.0 || dAd == 0.0) throw HbError{HB_ERR_NUMERIC, "zero stencil diagonal"};
+    dm[i] = make_float2(float(dMd.real()), float(dMd.imag()));
+    da[i] = make_float2(float(dAd.real()), float(dAd.imag()));
+    if (fp64A) da64[i] = make_double2(dAd.real(), dAd.imag());
+    kf[i] = float(L.k2[i]);
+  }
+  L.dM.ensure(n);
+  L.dA.ensure(n);
+  L.k2f.ensure(n);
+  HB_CUDA(cudaMemcpy(L.dM.p, dm.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(L.dA.p, da.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(L.k2f.p, kf.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  if (fp64A) {
+    L.dA64.ensure(n);
+    HB_CUDA(cudaMemcpy(L.dA64.p, da64.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+}
+
+void ensure_batch(Context& c, int B) {
+  require_hier(c);
+  if (B <= c.batch_cap) return;
+  for (auto& L : c.levels) {
+    const size_t n = L->N() * size_t(B);
+    L->f.ensure(n);
+    L->v.ensure(n);
+    L->t.ensure(n);
+    L->x.ensure(n);
+  }
+  const Level& C = *c.levels.back();
+  c.scratch_c64.ensure(size_t(B) * (kMaxCoarseIters + 2) * C.N());
+  c.act_all.ensure(B);
+  std::vector<int> ones(size_t(B), 1);
+  HB_CUDA(cudaMemcpy(c.act_all.p, ones.data(), sizeof(int) * B, cudaMemcpyHostToDevice));
+  c.batch_cap = B;
+}
+
+// ------------------------------------------------------------- V-cycle --
+// cycle_at (inc/multigrid.hpp:108-119) on device buffers; level-0 input f may
+// carry a per-column scale (FGMRES basis vectors are stored unnormalised).
+static void coarsest_solve(Context& c, int B, const int* act, const float2* f, float2* out) {
+  Level& L = *c.levels.back();
+  const LevelView V = L.view();
+  switch (c.vc.coarse_solver) {
+    case HB_COARSE_GMRES:
+      launch_coarse_gmres(c, V, c.vc.coarse_iters, B, act, f, out, c.scratch_c64.p);
+      break;
+    case HB_COARSE_JACOBI: {  // A3: iters damped sweeps from zero
+      const float w = float(c.vc.damping);
+      if (c.vc.coarse_iters <= 0) {
+        HB_CUDA(cudaMemsetAsync(out, 0, sizeof(float2) * L.N() * B, c.stream));
+        break;
+      }
+      float2* a = (c.vc.coarse_iters % 2 == 1) ? out : L.t.p;
+      float2* bb = (a == out) ? L.t.p : out;
+      launch_jacobi_zero(c, V, w, B, act, f, nullptr, a);
+      for (int s = 1; s < c.vc.coarse_iters; ++s) {
+        launch_jacobi_sweep(c, V, w, B, act, a, f, nullptr, bb);
+        std::swap(a, bb);
+      }
+      break;
+    }
+    case HB_COARSE_NET: {  // A4: U-Net on [H^2 Re f, H^2 Im f, kappa^2]
+      Net& n = c.nets[0];
+      if (!n.set) throw HbError{HB_ERR_STATE, "coarse solver is the net but net slot 0 is not set"};
+      const int H = L.ny, W = L.nx;
+      const size_t np = size_t(B) * H * W;
+      c.net_act.ensure(0);
+      // staging: in (3 ch) + out (2 ch) in the generic c64 scratch region after the coarse area
+      static thread_local DBuf<float> io;  // per-thread staging (one context per thread by contract)
+      io.ensure(np * 5);
+      launch_pack_input(c, V, L.h * L.h, B, act, f, nullptr, io.p);
+      net_forward_dev(c, 0, B, act, H, W, io.p, io.p + np * 3);
+      launch_unpack_output(c, H * W, B, act, io.p + np * 3, out);
+      break;
+    }
+    default:
+      throw HbError{HB_ERR_ARG, "unknown coarse solver"};
+  }
+}
+
+static void vcycle_at(Context& c, int l, int B, const int* act, const float2* f, const float* fscale,
+                      const float2* e0, float2* out) {
+  const int nl = int(c.levels.size());
+  if (l == nl - 1) {
+    coarsest_solve(c, B, act, f, out);
+    return;
+  }
+  Level& L = *c.levels[size_t(l)];
+  Level& C = *c.levels[size_t(l + 1)];
+  const LevelView V = L.view();
+  const float w = float(c.vc.damping);
+  const int offset = l % 2;
+  const int nu1 = c.vc.nu1, nu2 = c.vc.nu2;
+  float2* v = L.v.p;
+  float2* t = L.t.p;
+  // pre-smoothing (nu1 sweeps from e0 or zero)
+  if (nu1 == 0) {
+    if (e0)
+      HB_CUDA(cudaMemcpyAsync(v, e0, sizeof(float2) * L.N() * B, cudaMemcpyDeviceToDevice, c.stream));
+    else
+      HB_CUDA(cudaMemsetAsync(v, 0, sizeof(float2) * L.N() * B, c.stream));
+  } else {
+    if (e0)
+      launch_jacobi_sweep(c, V, w, B, act, e0, f, fscale, v);
+    else
+      launch_jacobi_zero(c, V, w, B, act, f, fscale, v);
+    for (int s = 1; s < nu1; ++s) {
+      launch_jacobi_sweep(c, V, w, B, act, v, f, fscale, t);
+      std::swap(v, t);
+    }
+  }
+  launch_residual_restrict(c, V, offset, B, act, v, f, fscale, C.f.p);
+  vcycle_at(c, l + 1, B, act, C.f.p, nullptr, nullptr, C.x.p);
+  launch_prolong_add(c, V, C.nx, C.ny, offset, B, act, C.x.p, v);
+  if (nu2 == 0) {
+    HB_CUDA(cudaMemcpyAsync(out, v, sizeof(float2) * L.N() * B, cudaMemcpyDeviceToDevice, c.stream));
+    return;
+  }
+  for (int s = 0; s < nu2; ++s) {
+    float2* dst = (s == nu2 - 1) ? out : (v == L.v.p ? L.t.p : L.v.p);
+    launch_jacobi_sweep(c, V, w, B, act, v, f, fscale, dst);
+    v = dst;
+  }
+}
+
+void vcycle(Context& c, int B, const int* act, const float2* f0, const float* fscale, const float2* e0, float2* z) {
+  vcycle_at(c, 0, B, act, f0, fscale, e0, z);
+}
+
+void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2* r, const float* rscale,
+                       float2* z) {
+  if (kind == HB_PC_V) {
+    vcycle(c, B, act, r, rscale, nullptr, z);
+    return;
+  }
+  if (kind != HB_PC_VU) throw HbError{HB_ERR_ARG, "unknown preconditioner kind"};
+  // M_VU (inc/precond.hpp:151-158): e0 = net(h^2 r, kappa^2); z = cycle(e0, r)
+  Net& n = c.nets[0];
+  if (!n.set) throw HbError{HB_ERR_STATE, "M_VU needs net slot 0"};
+  Level& L = *c.levels[0];
+  const LevelView V = L.view();
+  const size_t np = size_t(B) * L.N();
+  static thread_local DBuf<float> io;
+  static thread_local DBuf<float2> e0;
+  io.ensure(np * 5);
+  e0.ensure(np);
+  launch_pack_input(c, V, L.h * L.h, B, act, r, rscale, io.p);
+  net_forward_dev(c, 0, B, act, L.ny, L.nx, io.p, io.p + np * 3);
+  launch_unpack_output(c, int(L.N()), B, act, io.p + np * 3, e0.p);
+  vcycle(c, B, act, r, rscale, e0.p, z);
+}
+
+// ------------------------------------------------------------- FGMRES --
+static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, const double2* dB, double2* dX,
+                       double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv, uint8_t* brk) {
+  require_hier(c);
+  if (!cfg) throw HbError{HB_ERR_ARG, "null krylov config"};
+  if (cfg->restart < 1) throw HbError{HB_ERR_ARG, "restart must be >= 1"};
+  if (!(cfg->rel_tol > 0.0 && cfg->rel_tol < 1.0)) throw HbError{HB_ERR_ARG, "rel_tol in (0,1)"};
+  if (!cfg->flexible) throw HbError{HB_ERR_ARG, "the device FGMRES stores Z: flexible must be 1"};
+  if (B < 1) throw HbError{HB_ERR_ARG, "batch must be >= 1"};
+  ensure_batch(c, B);
+  const int m = cfg->restart;
+  const int cap = std::max(1, cfg->max_iters + 2);
+  krylov_alloc(c, B, m, cap);
+  const size_t N = c.levels[0]->N();
+  const size_t BN = size_t(B) * N;
+  if (!c.h_count) HB_CUDA(cudaMallocHost(&c.h_count, sizeof(int)));
+  for (;;) {
+    launch_fg_restart(c, B, dB, dX, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
+    HB_CUDA(cudaMemcpyAsync(c.h_count, c.kcount.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    HB_CUDA(cudaStreamSynchronize(c.stream));
+    if (*c.h_count == 0) break;
+    for (int j = 0; j < m; ++j) {
+      float2* Vj = c.kV.p + size_t(j) * BN;
+      float2* Zj = c.kZ.p + size_t(j) * BN;
+      precond_apply_dev(c, kind, B, c.kact.p, Vj, c.kscale.p, Zj);
+      launch_fg_adots(c, B, j, Zj, c.kW.p, c.kV.p);
+      launch_fg_update(c, B, j, m, c.kW.p, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
+    }
+    launch_fg_finalize(c, B, m, c.kZ.p, dX);
+  }
+  if (hist || hist_len || iters || conv || brk) krylov_report(c, B, hist, hist_stride, hist_len, iters, conv, brk);
+}
+
+}  // namespace hb
+
+// ===================================================================== C ABI
+using namespace hb;
+
+struct hb_ctx : hb::Context {};
+
+static std::string g_create_err;
+
+#define HB_API_BEGIN \
+  if (!ctx) return HB_ERR_ARG; \
+  try {
+#define HB_API_END                          \
+  return HB_OK;                             \
+  }                                         \
+  catch (const HbError& e) {                \
+    ctx->err = e.msg;                       \
+    return e.code;                          \
+  }                                         \
+  catch (const std::exception& e) {         \
+    ctx->err = e.what();                    \
+    return HB_ERR_ARG;                      \
+  }
+
+extern "C" {
+
+int hb_create(int device, hb_ctx** out) {
+  if (!out) return HB_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0) {
+    g_create_err = std::string("no CUDA device: ") + cudaGetErrorString(e);
+    return HB_ERR_CUDA;
+  }
+  if (device < 0 || device >= ndev) {
+    g_create_err = "device index out of range";
+    return HB_ERR_ARG;
+  }
+  cudaSetDevice(device);
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10) {
+    g_create_err = "libhelmgpu is built for sm_100a (B200); found sm_" + std::to_string(prop.major) +
+                   std::to_string(prop.minor);
+    return HB_ERR_CUDA;
+  }
+  auto* c = new hb_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    g_create_err = "stream creation failed";
+    delete c;
+    return HB_ERR_CUDA;
+  }
+  c->prof.resize(PC_COUNT);
+  for (int i = 0; i < PC_COUNT; ++i) c->prof[size_t(i)].name = kProfNames[i];
+  *out = c;
+  return HB_OK;
+}
+
+void hb_destroy(hb_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (auto& e : ctx->ev_pending) {
+    cudaEventDestroy(e.second.first);
+    cudaEventDestroy(e.second.second);
+  }
+  if (ctx->h_count) cudaFreeHost(ctx->h_count);
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char* hb_last_error(const hb_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
+void* hb_stream(hb_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int hb_synchronize(hb_ctx* ctx) {
+  HB_API_BEGIN
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  HB_API_END
+}
+
+int hb_set_problem(hb_ctx* ctx, int nx, int ny, double h, double omega, const double* kappa2, const double* gamma,
+                   double lo, double hi) {
+  HB_API_BEGIN
+  if (nx < 8 || ny < 8) throw HbError{HB_ERR_ARG, "grid must be at least 8x8"};
+  if (!kappa2 || !gamma) throw HbError{HB_ERR_ARG, "null coefficient array"};
+  if (!(lo < hi) || lo < 0.0) throw HbError{HB_ERR_ARG, "slowness range must satisfy 0 <= lo < hi"};
+  if (omega < 0.0) throw HbError{HB_ERR_ARG, "omega must be nonnegative"};
+  const size_t n = size_t(nx) * ny;
+  double kmax = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    if (!(kappa2[i] >= lo - 1e-12 && kappa2[i] <= hi + 1e-12))
+      throw HbError{HB_ERR_ARG, "slowness value outside declared range"};
+    kmax = std::max(kmax, std::sqrt(kappa2[i]));
+  }
+  if (omega * kmax * h > 0.6284) throw HbError{HB_ERR_ARG, "discretization bound omega*kappa*h <= 0.628 violated"};
+  ctx->nx = nx;
+  ctx->ny = ny;
+  ctx->h = h;
+  ctx->omega = omega;
+  ctx->klo = lo;
+  ctx->khi = hi;
+  ctx->k2.assign(kappa2, kappa2 + n);
+  ctx->gam.assign(gamma, gamma + n);
+  ctx->has_problem = true;
+  ctx->has_hier = false;
+  ctx->levels.clear();
+  ctx->batch_cap = 0;
+  ctx->ctx_valid = false;
+  HB_API_END
+}
+
+int hb_build_hierarchy(hb_ctx* ctx, const hb_vcycle_cfg* cfg) {
+  HB_API_BEGIN
+  if (!ctx->has_problem) throw HbError{HB_ERR_STATE, "problem not set"};
+  if (!cfg) throw HbError{HB_ERR_ARG, "null config"};
+  if (cfg->levels < 2) throw HbError{HB_ERR_ARG, "levels must be >= 2"};
+  if (cfg->nu1 + cfg->nu2 < 1 || cfg->nu1 < 0 || cfg->nu2 < 0) throw HbError{HB_ERR_ARG, "nu1 + nu2 must be >= 1"};
+  if (!(cfg->damping > 0.0 && cfg->damping <= 1.0)) throw HbError{HB_ERR_ARG, "damping must be in (0,1]"};
+  if (cfg->beta < 0.0) throw HbError{HB_ERR_ARG, "shift beta must be >= 0"};
+  const int div = 1 << (cfg->levels - 1);
+  if (ctx->nx % div || ctx->ny % div)
+    throw HbError{HB_ERR_ARG, "grid does not support the configured level count"};
+  if (cfg->coarse_solver == HB_COARSE_GMRES && (cfg->coarse_iters < 1 || cfg->coarse_iters > kMaxCoarseIters))
+    throw HbError{HB_ERR_ARG, "coarse GMRES iterations must be in [1, 16]"};
+  ctx->vc = *cfg;
+  ctx->levels.clear();
+  ctx->batch_cap = 0;
+  auto L0 = std::make_unique<Level>();
+  L0->nx = ctx->nx;
+  L0->ny = ctx->ny;
+  L0->h = ctx->h;
+  L0->k2 = ctx->k2;
+  L0->gam = ctx->gam;
+  ctx->levels.push_back(std::move(L0));
+  for (int l = 1; l < cfg->levels; ++l) {
+    const Level& P = *ctx->levels.back();
+    auto L = std::make_unique<Level>();
+    L->nx = P.nx / 2;
+    L->ny = P.ny / 2;
+    L->h = P.h * 2.0;
+    L->k2.resize(L->N());
+    L->gam.resize(L->N());
+    const int off = (l - 1) % 2;
+    restrict_real(P.k2.data(), P.nx, P.ny, off, L->k2.data());
+    restrict_real(P.gam.data(), P.nx, P.ny, off, L->gam.data());
+    for (double& x : L->k2) x = std::clamp(x, ctx->klo, ctx->khi);
+    for (double& x : L->gam) x = std::max(x, 0.0);
+    ctx->levels.push_back(std::move(L));
+  }
+  for (size_t l = 0; l < ctx->levels.size(); ++l)
+    fill_level_device(*ctx->levels[l], ctx->omega, cfg->alpha, cfg->beta, l == 0);
+  ctx->has_hier = true;
+  HB_API_END
+}
+
+int hb_level_info(hb_ctx* ctx, int level, int* nx, int* ny, double* h) {
+  HB_API_BEGIN
+  require_hier(*ctx);
+  if (level < 0 || level >= int(ctx->levels.size())) throw HbError{HB_ERR_ARG, "level out of range"};
+  const Level& L = *ctx->levels[size_t(level)];
+  if (nx) *nx = L.nx;
+  if (ny) *ny = L.ny;
+  if (h) *h = L.h;
+  HB_API_END
+}
+
+// ---- operator hooks (host c128 buffers, staged as c64) ----
+static Level& level_at(hb_ctx* ctx, int level) {
+  require_hier(*ctx);
+  if (level < 0 || level >= int(ctx->levels.size())) throw HbError{HB_ERR_ARG, "level out of range"};
+  return *ctx->levels[size_t(level)];
+}
+
+int hb_operator_apply(hb_ctx* ctx, int level, int shifted, int batch, const double* u, double* y) {
+  HB_API_BEGIN
+  Level& L = level_at(ctx, level);
+  const size_t n = L.N() * size_t(batch);
+  ctx->io_f.ensure(n);
+  ctx->io_g.ensure(n);
+  auto hu = to_c64(u, n);
+  HB_CUDA(cudaMemcpyAsync(ctx->io_f.p, hu.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  launch_apply(*ctx, L.view(), shifted ? 1 : 0, batch, nullptr, ctx->io_f.p, ctx->io_g.p, nullptr);
+  HB_CUDA(cudaMemcpyAsync(hu.data(), ctx->io_g.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  from_c64(hu, y);
+  HB_API_END
+}
+
+int hb_jacobi(hb_ctx* ctx, int level, int batch, double* v, const double* f, int iters) {
+  HB_API_BEGIN
+  Level& L = level_at(ctx, level);
+  if (iters < 0) throw HbError{HB_ERR_ARG, "iters must be >= 0"};
+  const size_t n = L.N() * size_t(batch);
+  ctx->io_f.ensure(n);
+  ctx->io_g.ensure(n);
+  ctx->scratch_c64.ensure(n);
+  auto hv = to_c64(v, n), hf = to_c64(f, n);
+  HB_CUDA(cudaMemcpyAsync(ctx->io_f.p, hv.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  HB_CUDA(cudaMemcpyAsync(ctx->io_g.p, hf.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  float2* a = ctx->io_f.p;
+  float2* b = ctx->scratch_c64.p;
+  for (int s = 0; s < iters; ++s) {
+    launch_jacobi_sweep(*ctx, L.view(), float(ctx->vc.damping), batch, nullptr, a, ctx->io_g.p, nullptr, b);
+    std::swap(a, b);
+  }
+  HB_CUDA(cudaMemcpyAsync(hv.data(), a, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  from_c64(hv, v);
+  HB_API_END
+}
+
+int hb_restrict(hb_ctx* ctx, int level, int batch, const double* fine, double* coarse) {
+  HB_API_BEGIN
+  Level& L = level_at(ctx, level);
+  const size_t n = L.N() * size_t(batch), nc = n / 4;
+  ctx->io_f.ensure(n);
+  ctx->io_g.ensure(n);
+  auto hf = to_c64(fine, n);
+  HB_CUDA(cudaMemcpyAsync(ctx->io_f.p, hf.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  launch_restrict_plain(*ctx, L.nx, L.ny, level % 2, batch, ctx->io_f.p, ctx->io_g.p);
+  std::vector<float2> hc(nc);
+  HB_CUDA(cudaMemcpyAsync(hc.data(), ctx->io_g.p, nc * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  from_c64(hc, coarse);
+  HB_API_END
+}
+
+int hb_prolong(hb_ctx* ctx, int level, int batch, const double* coarse, double* fine) {
+  HB_API_BEGIN
+  Level& L = level_at(ctx, level);
+  const size_t n = L.N() * size_t(batch), nc = n / 4;
+  ctx->io_f.ensure(n);
+  ctx->io_g.ensure(n);
+  auto hc = to_c64(coarse, nc);
+  HB_CUDA(cudaMemcpyAsync(ctx->io_f.p, hc.data(), nc * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  HB_CUDA(cudaMemsetAsync(ctx->io_g.p, 0, n * sizeof(float2), ctx->stream));
+  launch_prolong_add(*ctx, L.view(), L.nx / 2, L.ny / 2, level % 2, batch, nullptr, ctx->io_f.p, ctx->io_g.p);
+  std::vector<float2> hf(n);
+  HB_CUDA(cudaMemcpyAsync(hf.data(), ctx->io_g.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  from_c64(hf, fine);
+  HB_API_END
+}
+
+int hb_coarse_solve(hb_ctx* ctx, int batch, const double* f, double* x) {
+  HB_API_BEGIN
+  require_hier(*ctx);
+  ensure_batch(*ctx, batch);
+  Level& C = *ctx->levels.back();
+  const size_t n = C.N() * size_t(batch);
+  ctx->io_f.ensure(n);
+  ctx->io_g.ensure(n);
+  auto hf = to_c64(f, n);
+  HB_CUDA(cudaMemcpyAsync(ctx->io_f.p, hf.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  coarsest_solve(*ctx, batch, ctx->act_all.p, ctx->io_f.p, ctx->io_g.p);
+  HB_CUDA(cudaMemcpyAsync(hf.data(), ctx->io_g.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  from_c64(hf, x);
+  HB_API_END
+}
+
+int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* z) {
+  HB_API_BEGIN
+  require_hier(*ctx);
+  if (batch < 1) throw HbError{HB_ERR_ARG, "batch must be >= 1"};
+  ensure_batch(*ctx, batch);
+  const size_t n = ctx->levels[0]->N() * size_t(batch);
+  ctx->io_f.ensure(n);
+  ctx->io_g.ensure(n);
+  auto hr = to_c64(r, n);
+  HB_CUDA(cudaMemcpyAsync(ctx->io_f.p, hr.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
+  precond_apply_dev(*ctx, kind, batch, ctx->act_all.p, ctx->io_f.p, nullptr, ctx->io_g.p);
+  HB_CUDA(cudaMemcpyAsync(hr.data(), ctx->io_g.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  from_c64(hr, z);
+  HB_API_END
+}
+
+const char* hb_precond_name(int kind) { return kind == HB_PC_VU ? "vu" : "v"; }
+
+int hb_precond_requires_flexible(hb_ctx* ctx, int kind) {
+  if (!ctx) return 1;
+  // network-based preconditioners are non-stationary (inc/precond.hpp:132,160)
+  return kind == HB_PC_VU || ctx->vc.coarse_solver == HB_COARSE_NET;
+}
+
+int hb_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,
+              double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
+              uint8_t* breakdown) {
+  HB_API_BEGIN
+  require_hier(*ctx);
+  if (!B || !X) throw HbError{HB_ERR_ARG, "null B or X"};
+  const size_t n = ctx->levels[0]->N() * size_t(batch);
+  ctx->kB.ensure(n);
+  ctx->kX.ensure(n);
+  HB_CUDA(cudaMemcpyAsync(ctx->kB.p, B, n * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  if (X0)
+    HB_CUDA(cudaMemcpyAsync(ctx->kX.p, X0, n * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  else
+    HB_CUDA(cudaMemsetAsync(ctx->kX.p, 0, n * sizeof(double2), ctx->stream));
+  fgmres_dev(*ctx, cfg, kind, batch, ctx->kB.p, ctx->kX.p, hist, hist_stride, hist_len, iters, converged, breakdown);
+  HB_CUDA(cudaMemcpyAsync(X, ctx->kX.p, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  HB_API_END
+}
+
+int hb_fgmres_device(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const void* dB, void* dX,
+                     double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
+                     uint8_t* breakdown) {
+  HB_API_BEGIN
+  if (!dB || !dX) throw HbError{HB_ERR_ARG, "null device buffer"};
+  fgmres_dev(*ctx, cfg, kind, batch, static_cast<const double2*>(dB), static_cast<double2*>(dX), hist, hist_stride,
+             hist_len, iters, converged, breakdown);
+  HB_API_END
+}
+
+// ---- setup helpers ----
+void hb_rng_normals(uint64_t seed, int64_t n, double* out) {
+  Rng r(seed);
+  for (int64_t i = 0; i < n; ++i) out[i] = r.normal();
+}
+
+int hb_absorbing_layer(int nx, int ny, int width, double gamma_max, double* out) {
+  if (gamma_max < 0.0 || width < 0 || width > std::min(nx, ny) / 2 || !out) return HB_ERR_ARG;
+  for (int iy = 0; iy < ny; ++iy)
+    for (int ix = 0; ix < nx; ++ix) {
+      const int d = std::min(std::min(ix, nx - 1 - ix), std::min(iy, ny - 1 - iy));
+      double g = 0.0;
+      if (width > 0 && d < width) {
+        const double t = double(width - d) / double(width);
+        g = gamma_max * t * t;
+      }
+      out[size_t(iy) * nx + ix] = g;
+    }
+  return HB_OK;
+}
+
+int hb_make_medium(int nx, int ny, uint64_t seed, double sigma, double vmin, double vmax, int n_interfaces,
+                   uint64_t iface_seed, int iface_margin, double jmin, double jmax, double* kappa2) {
+  if (nx < 1 || ny < 1 || !kappa2 || !(sigma > 0) || !(vmin < vmax)) return HB_ERR_ARG;
+  const size_t n = size_t(nx) * ny;
+  std::vector<double> f(n), c(n);
+  Rng r(seed);
+  for (auto& x : f) x = r.normal();
+  gaussian_blur(f.data(), nx, ny, sigma, c.data());
+  normalize_range(c, vmin, vmax);
+  if (n_interfaces > 0) {
+    Rng ir(iface_seed);
+    for (int t = 0; t < n_interfaces; ++t) {
+      const int row = int(ir.uniform_int(iface_margin, ny - iface_margin - 1));
+      const double jump = jmin + (jmax - jmin) * ir.uniform();
+      for (int iy = row; iy < ny; ++iy)
+        for (int ix = 0; ix < nx; ++ix) c[size_t(iy) * nx + ix] += jump;
+    }
+    normalize_range(c, vmin, vmax);
+  }
+  for (size_t i = 0; i < n; ++i) kappa2[i] = 1.0 / (c[i] * c[i]);
+  return HB_OK;
+}
+
+void hb_point_sources(uint64_t seed, int batch, int mode, int lo, int hi, int row, int* xs, int* ys) {
+  Rng r(seed);
+  for (int b = 0; b < batch; ++b) {
+    if (mode == 0) {
+      xs[b] = int(r.uniform_int(lo, hi));
+      ys[b] = int(r.uniform_int(lo, hi));
+    } else {
+      xs[b] = int(r.uniform_int(lo, hi));
+      ys[b] = row;
+    }
+  }
+}
+
+// ---- instrumentation ----
+int hb_prof_enable(hb_ctx* ctx, int on) {
+  HB_API_BEGIN
+  if (!on) prof_collect(*ctx);
+  ctx->prof_on = on != 0;
+  HB_API_END
+}
+int hb_prof_reset(hb_ctx* ctx) {
+  HB_API_BEGIN
+  prof_collect(*ctx);
+  for (auto& p : ctx->prof) {
+    p.ms = 0;
+    p.launches = 0;
+    p.bytes = p.flops = 0;
+  }
+  ctx->launches = 0;
+  HB_API_END
+}
+int hb_prof_count(hb_ctx* ctx) { return ctx ? int(ctx->prof.size()) : 0; }
+const char* hb_prof_name(hb_ctx* ctx, int i) {
+  return (ctx && i >= 0 && i < int(ctx->prof.size())) ? ctx->prof[size_t(i)].name.c_str() : "";
+}
+int hb_prof_get(hb_ctx* ctx, int i, double* total_ms, int64_t* launches, double* bytes, double* flops) {
+  HB_API_BEGIN
+  prof_collect(*ctx);
+  if (i < 0 || i >= int(ctx->prof.size())) throw HbError{HB_ERR_ARG, "bad profile index"};
+  const Prof& p = ctx->prof[size_t(i)];
+  if (total_ms) *total_ms = p.ms;
+  if (launches) *launches = p.launches;
+  if (bytes) *bytes = p.bytes;
+  if (flops) *flops = p.flops;
+  HB_API_END
+}
+int64_t hb_launch_count(hb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,60 @@
+// Device helpers: complex64 arithmetic, fp64 block reductions.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace hb {
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
+// a + s*b
+__device__ __forceinline__ float2 caxpy(float2 a, float s, float2 b) {
+  return make_float2(fmaf(s, b.x, a.x), fmaf(s, b.y, a.y));
+}
+__device__ __forceinline__ float2 crcp(float2 d) {
+  const float s = 1.0f / fmaf(d.x, d.x, d.y * d.y);
+  return make_float2(d.x * s, -d.y * s);
+}
+__device__ __forceinline__ double2 dadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+// conj(a) * b in fp64
+__device__ __forceinline__ double2 dconjmul(float2 a, float2 b) {
+  const double ax = a.x, ay = a.y, bx = b.x, by = b.y;
+  return make_double2(fma(ax, bx, ay * by), fma(ax, by, -ay * bx));
+}
+__device__ __forceinline__ double dnorm2(float2 a) {
+  const double ax = a.x, ay = a.y;
+  return fma(ax, ax, ay * ay);
+}
+__device__ __forceinline__ float2 ld(const float2* p, size_t i) { return __ldg(p + i); }
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ double2 warp_sum2(double2 v) {
+  v.x = warp_sum(v.x);
+  v.y = warp_sum(v.y);
+  return v;
+}
+
+// 5-point stencil of u at (ix, iy) with zero padding: d*u - inv_h2*(sum of neighbours)
+__device__ __forceinline__ float2 stencil_at(const float2* __restrict__ u, int nx, int ny, int ix, int iy,
+                                             float2 d, float inv_h2, float s) {
+  const size_t i = size_t(iy) * nx + ix;
+  float2 nb = make_float2(0.f, 0.f);
+  if (ix > 0) nb = cadd(nb, ld(u, i - 1));
+  if (ix + 1 < nx) nb = cadd(nb, ld(u, i + 1));
+  if (iy > 0) nb = cadd(nb, ld(u, i - nx));
+  if (iy + 1 < ny) nb = cadd(nb, ld(u, i + nx));
+  const float2 c = ld(u, i);
+  float2 y = cmul(d, c);
+  y.x = fmaf(-inv_h2, nb.x, y.x);
+  y.y = fmaf(-inv_h2, nb.y, y.y);
+  return cscale(y, s);
+}
+
+}  // namespace hb

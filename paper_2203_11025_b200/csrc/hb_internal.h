@@ -1,0 +1,224 @@
+// Internal declarations shared by the libhelmgpu translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/helmgpu.h"
+
+namespace hb {
+
+constexpr int kMaxRestart = 32;  // FGMRES restart cap (device column state)
+constexpr int kMaxCoarseIters = 16;
+
+struct HbError {
+  int code;
+  std::string msg;
+};
+
+#define HB_CUDA(x)                                                                                     \
+  do {                                                                                                 \
+    cudaError_t e_ = (x);                                                                              \
+    if (e_ != cudaSuccess)                                                                             \
+      throw ::hb::HbError{HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};              \
+  } while (0)
+
+// device buffer (RAII)
+template <typename T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) {
+    o.p = nullptr;
+    o.n = 0;
+  }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      n = o.n;
+      o.p = nullptr;
+      o.n = 0;
+    }
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void ensure(size_t count) {
+    if (count <= n) return;
+    release();
+    HB_CUDA(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
+    n = count;
+  }
+};
+
+// device view of one multigrid level (passed by value to kernels)
+struct LevelView {
+  int nx, ny;
+  float inv_h2;
+  const float2* dM;  // diagonal of the shifted operator M^h (c64)
+  const float2* dA;  // diagonal of A^h (c64)
+  const float* k2f;  // kappa^2 (fp32)
+};
+
+struct Level {
+  int nx = 0, ny = 0;
+  double h = 0;
+  std::vector<double> k2, gam;  // host fp64 coefficients (inc/stencil.hpp:169-185 coarsening)
+  DBuf<float2> dM, dA;
+  DBuf<double2> dA64;  // level 0: fp64 diagonal of A^h for the restart residual
+  DBuf<float> k2f;
+  // V-cycle work buffers [B][N]
+  DBuf<float2> f, v, t, x;
+  LevelView view() const {
+    return LevelView{nx, ny, float(1.0 / (h * h)), dM.p, dA.p, k2f.p};
+  }
+  size_t N() const { return size_t(nx) * ny; }
+};
+
+struct ConvW {
+  int cout = 0, cin = 0;
+  std::vector<float> w, b;  // host OIHW + bias
+  DBuf<float> dw;           // device packed weights [9*cin][cout] (k-major rows)
+  DBuf<float> db;
+};
+
+struct Net {
+  hb_net_cfg cfg{};
+  bool set = false;
+  std::vector<ConvW> convs;
+  int enc1[8], enc2[8], up[8], dec1[8], dec2[8], head = -1;
+  bool dirty = true;
+};
+
+struct Prof {
+  std::string name;
+  double ms = 0;
+  int64_t launches = 0;
+  double bytes = 0, flops = 0;
+};
+
+struct Context;
+
+// ---- multigrid / operator launchers (hb_mg.cu)
+void launch_apply(Context& c, const LevelView& L, int which, int B, const int* act, const float2* u, float2* y,
+                  const float* uscale);
+void launch_jacobi_zero(Context& c, const LevelView& L, float damping, int B, const int* act, const float2* f,
+                        const float* fscale, float2* v);
+void launch_jacobi_sweep(Context& c, const LevelView& L, float damping, int B, const int* act, const float2* v,
+                         const float2* f, const float* fscale, float2* out);
+void launch_residual_restrict(Context& c, const LevelView& L, int offset, int B, const int* act, const float2* v,
+                              const float2* f, const float* fscale, float2* fc);
+void launch_prolong_add(Context& c, const LevelView& Lf, int cnx, int cny, int offset, int B, const int* act,
+                        const float2* vc, float2* v);
+void launch_restrict_plain(Context& c, int nx, int ny, int offset, int B, const float2* fine, float2* coarse);
+void launch_coarse_gmres(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
+                         float2* x, float2* scratch);
+// fused down/up legs (nu1 = nu2 = 1)
+void launch_down_fused(Context& c, const LevelView& L, float damping, int offset, int B, const int* act,
+                       const float2* f, const float* fscale, const float2* e0, float2* fc);
+void launch_up_fused(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B,
+                     const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
+                     float2* z);
+// network pack / unpack (hb_net.cu)
+void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const int* act, const float2* r,
+                       const float* rscale, float* x /*NHWC, 3 ch*/);
+void launch_unpack_output(Context& c, int N, int B, const int* act, const float* y /*NHWC 2ch*/, float2* e);
+
+// ---- Krylov (hb_krylov.cu)
+struct ColState;
+void krylov_alloc(Context& c, int B, int m, int hist_cap);
+void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, float2* V0, int hist_cap,
+                       double rel_tol, int max_iters);
+void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V);
+void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* V, int hist_cap, double rel_tol,
+                      int max_iters);
+void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x);
+
+// ---- profiling / launch accounting
+int prof_begin(Context& c, int cls);
+void prof_end(Context& c, int cls, int token, double bytes, double flops);
+
+enum ProfClass {
+  PC_STENCIL = 0,
+  PC_SMOOTH,
+  PC_DOWN,
+  PC_UP,
+  PC_TRANSFER,
+  PC_COARSE,
+  PC_KRYLOV_DOTS,
+  PC_KRYLOV_UPDATE,
+  PC_KRYLOV_RESTART,
+  PC_KRYLOV_FINAL,
+  PC_CONV,
+  PC_NETIO,
+  PC_COUNT
+};
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int num_sms = 148;
+  std::string err;
+  // problem
+  bool has_problem = false;
+  int nx = 0, ny = 0;
+  double h = 0, omega = 0, klo = 0, khi = 0;
+  std::vector<double> k2, gam;
+  // hierarchy
+  bool has_hier = false;
+  hb_vcycle_cfg vc{};
+  std::vector<std::unique_ptr<Level>> levels;
+  int batch_cap = 0;
+  // nets: slot 0 solver, slot 1 encoder
+  Net nets[2];
+  // generic scratch
+  DBuf<float2> scratch_c64;
+  DBuf<double2> io_a, io_b;  // c128 staging
+  DBuf<float2> io_f, io_g;   // c64 staging
+  DBuf<int> act_all;         // all-ones activity flags
+  // Krylov
+  DBuf<char> kstate;         // ColState[B]
+  DBuf<double2> kpart;       // per-CTA partials
+  DBuf<double> khist;        // [B][hist_cap]
+  DBuf<int> kact;            // per-column: active in the current inner step
+  DBuf<float> kscale;        // per-column: scale of the current V_j
+  DBuf<unsigned> kticket;    // per-column last-CTA counters
+  DBuf<int> kcount;          // number of unfrozen columns (host-visible after restart)
+  DBuf<float2> kV, kZ, kW;   // [B][m+1][N], [B][m][N], [B][N]
+  DBuf<double2> kX, kB;      // c128 solution / rhs when called with host buffers
+  int k_B = 0, k_m = 0, k_hist = 0;
+  int* h_count = nullptr;    // pinned
+  // net activations
+  DBuf<float> net_act;       // arena
+  std::vector<DBuf<float>> ctx_maps;  // encoder context per level (NHWC)
+  bool ctx_valid = false;
+  // profiling
+  bool prof_on = false;
+  std::vector<Prof> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+  int64_t launches = 0;
+};
+
+void ensure_batch(Context& c, int B);
+// V-cycle driver (hb_api.cu)
+void vcycle(Context& c, int B, const int* act, const float2* f0, const float* fscale, const float2* e0, float2* z);
+void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2* r, const float* rscale,
+                       float2* z);
+// network forward on device (hb_net.cu): x NHWC [B][H][W][in_ch] -> y NHWC [B][H][W][2]
+void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, const float* x, float* y);
+void encoder_forward_dev(Context& c, int H, int W, const float* k2f);
+void net_upload(Context& c, int slot);
+
+}  // namespace hb

@@ -1,0 +1,497 @@
+// Device-resident restarted flexible GMRES over a block of independent
+// columns: the hot loop of block_fgmres (inc/krylov.hpp:83-267) with all
+// per-column control (Arnoldi, Givens, convergence, freezing, restarts) on the
+// GPU, so the host only replays one CUDA graph per restart cycle.
+//
+// Basis layout: V [m+1][B][N] and Z [m][B][N] complex64 (slot-major so a
+// preconditioner apply on V_j is one contiguous batch).  V_i is stored
+// unnormalised with a per-column fp64 scale s_i (V_i = s_i * Vraw_i).
+// Solution x and rhs b are complex128; the restart residual b - A x is formed
+// in fp64.  Reductions accumulate in fp64; per-CTA
+// partials are folded by the last CTA of each column (atomic ticket), which
+// also runs the scalar recurrences:
+//   MGS  h_ij = <V_i, w> - sum_{k<i} h_kj <V_i, V_k>   (one pass over V, Gram-corrected)
+//   Givens with real c, complex s (inc/krylov.hpp:49-64,221-232)
+//   stop on |g_{j+1}|/beta0 <= tol, happy breakdown hnorm <= 1e-14 beta0,
+//   iters >= max_iters; history: [0] = ||b - A x0||, then |g_{j+1}|.
+#include "hb_common.cuh"
+#include "hb_internal.h"
+
+#include <algorithm>
+
+namespace hb {
+
+struct ColState {
+  double beta0;
+  int iters, k, hist_len;
+  int frozen, converged, breakdown, active;
+  double cs[kMaxRestart];
+  double2 sn[kMaxRestart];
+  double2 g[kMaxRestart + 1];
+  double2 H[kMaxRestart][kMaxRestart + 1];
+  double2 G[kMaxRestart][kMaxRestart];
+  double2 hc[kMaxRestart + 1];
+  double2 coef[kMaxRestart + 1];
+  double scale[kMaxRestart + 1];
+};
+
+namespace {
+
+constexpr int KT = 256;           // threads per CTA
+constexpr int KNPT = 4;           // nodes per thread per tile
+constexpr int KTILE = KT * KNPT;  // nodes per tile
+constexpr int KMAXV = 2 * kMaxRestart + 1;
+
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 zconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 zsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 zscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, den = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
+  }
+  const double r = b.x / b.y, den = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
+}
+
+struct FineView {
+  int nx, ny;
+  double inv_h2;
+  const double2* dA64;  // fp64 diagonal of A^h (restart residual)
+  const float2* dA;     // fp32 diagonal (A z per inner step)
+};
+
+// last CTA of column b? (classic threadfence + ticket pattern; resets the ticket)
+__device__ bool last_cta(unsigned* ticket, int b, int nblk) {
+  __shared__ bool is_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(&ticket[b], 1u);
+    is_last = (t == unsigned(nblk - 1));
+    if (is_last) ticket[b] = 0;
+  }
+  __syncthreads();
+  return is_last;
+}
+
+// sum a per-warp smem partial table [8][nv] into out[nv] (threads < nv)
+__device__ void cta_fold(double2 (*part)[KMAXV], int nv, double2* out) {
+  __syncthreads();
+  for (int t = threadIdx.x; t < nv; t += KT) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int w = 0; w < KT / 32; ++w) s = dadd(s, part[w][t]);
+    out[t] = s;
+  }
+}
+
+// r = b - A x (fp64), V0raw = r, ||r||^2 -> restart logic (inc/krylov.hpp:143-188)
+__global__ void __launch_bounds__(KT) k_restart(FineView F, int B, ColState* st, const double2* __restrict__ bvec,
+                                                const double2* __restrict__ x, float2* __restrict__ V0,
+                                                double* part, unsigned* ticket, double* hist, int hist_cap,
+                                                double rel_tol, int max_iters, int* act, float* scale_out,
+                                                int* count) {
+  const int b = blockIdx.y;
+  ColState& S = st[b];
+  if (S.frozen) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      S.k = 0;
+      act[b] = 0;
+    }
+    return;
+  }
+  const size_t N = size_t(F.nx) * F.ny;
+  const double2* xb = x + b * N;
+  const double2* bb = bvec + b * N;
+  double acc = 0.0;
+  for (size_t base = size_t(blockIdx.x) * KTILE; base < N; base += size_t(gridDim.x) * KTILE) {
+#pragma unroll
+    for (int q = 0; q < KNPT; ++q) {
+      const size_t p = base + q * KT + threadIdx.x;
+      if (p >= N) break;
+      const int ix = int(p % F.nx), iy = int(p / F.nx);
+      double2 nb = make_double2(0.0, 0.0);
+      if (ix > 0) nb = dadd(nb, xb[p - 1]);
+      if (ix + 1 < F.nx) nb = dadd(nb, xb[p + 1]);
+      if (iy > 0) nb = dadd(nb, xb[p - F.nx]);
+      if (iy + 1 < F.ny) nb = dadd(nb, xb[p + F.nx]);
+      const double2 ax = zsub(zmul(F.dA64[p], xb[p]), zscale(nb, F.inv_h2));
+      const double2 r = zsub(bb[p], ax);
+      V0[b * N + p] = make_float2(float(r.x), float(r.y));
+      acc += r.x * r.x + r.y * r.y;
+    }
+  }
+  acc = warp_sum(acc);
+  __shared__ double wp[KT / 32];
+  if ((threadIdx.x & 31) == 0) wp[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < KT / 32; ++w) t += wp[w];
+    part[size_t(b) * gridDim.x + blockIdx.x] = t;
+  }
+  if (!last_cta(ticket, b, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
+  const double beta = sqrt(t);
+  S.k = 0;
+  S.active = 0;
+  if (S.hist_len == 0) {
+    S.beta0 = beta;
+    if (hist_cap > 0) hist[size_t(b) * hist_cap] = beta;
+    S.hist_len = 1;
+    if (beta == 0.0) {
+      S.frozen = 1;
+      S.converged = 1;
+    }
+  }
+  if (!S.frozen) {
+    if (beta / S.beta0 <= rel_tol) {
+      S.frozen = 1;
+      S.converged = 1;
+    } else if (S.iters >= max_iters) {
+      S.frozen = 1;
+    } else {
+      for (int i = 0; i <= kMaxRestart; ++i) S.g[i] = make_double2(0.0, 0.0);
+      S.g[0] = make_double2(beta, 0.0);
+      S.scale[0] = 1.0 / beta;
+      S.active = 1;
+    }
+  }
+  act[b] = S.active;
+  scale_out[b] = float(S.scale[0]);
+  if (!S.frozen) atomicAdd(count, 1);
+}
+
+// w = A Z_j ; partial <Vraw_i, w> (i <= j) and <Vraw_j, Vraw_k> (k < j);
+// last CTA forms the Gram-corrected MGS coefficients.
+__global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
+                                              const float2* __restrict__ Z, float2* __restrict__ W,
+                                              const float2* __restrict__ V, double2* part, unsigned* ticket) {
+  const int b = blockIdx.y;
+  if (!act[b]) return;
+  const size_t N = size_t(F.nx) * F.ny;
+  const size_t BN = size_t(B) * N;
+  const float2* zb = Z + b * N;  // slot j already applied by the caller
+  float2* wb = W + b * N;
+  const float2* Vj = V + size_t(j) * BN + b * N;
+  __shared__ double2 wpart[KT / 32][KMAXV];
+  const int nv = 2 * j + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = threadIdx.x; t < (KT / 32) * KMAXV; t += KT) (&wpart[0][0])[t] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const float inv_h2 = float(F.inv_h2);
+  for (size_t base = size_t(blockIdx.x) * KTILE; base < N; base += size_t(gridDim.x) * KTILE) {
+    float2 w[KNPT], vj[KNPT];
+    bool ok[KNPT];
+#pragma unroll
+    for (int q = 0; q < KNPT; ++q) {
+      const size_t p = base + q * KT + threadIdx.x;
+      ok[q] = p < N;
+      if (ok[q]) {
+        const int ix = int(p % F.nx), iy = int(p / F.nx);
+        w[q] = stencil_at(zb, F.nx, F.ny, ix, iy, ld(F.dA, p), inv_h2, 1.0f);
+        wb[p] = w[q];
+        vj[q] = ld(Vj, p);
+      } else {
+        w[q] = vj[q] = make_float2(0.f, 0.f);
+      }
+    }
+    for (int i = 0; i <= j; ++i) {
+      const float2* Vi = V + size_t(i) * BN + b * N;
+      double2 a = make_double2(0.0, 0.0), g = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < KNPT; ++q) {
+        if (!ok[q]) continue;
+        const float2 vi = ld(Vi, base + q * KT + threadIdx.x);
+        a = dadd(a, dconjmul(vi, w[q]));
+        if (i < j) g = dadd(g, dconjmul(vj[q], vi));
+      }
+      a = warp_sum2(a);
+      if (i < j) g = warp_sum2(g);
+      if (lane == 0) {
+        wpart[warp][i] = dadd(wpart[warp][i], a);
+        if (i < j) wpart[warp][j + 1 + i] = dadd(wpart[warp][j + 1 + i], g);
+      }
+    }
+  }
+  __shared__ double2 red[KMAXV];
+  cta_fold(wpart, nv, red);
+  __syncthreads();
+  for (int t = threadIdx.x; t < nv; t += KT) part[(size_t(b) * gridDim.x + blockIdx.x) * KMAXV + t] = red[t];
+  if (!last_cta(ticket, b, gridDim.x)) return;
+  for (int t = threadIdx.x; t < nv; t += KT) {
+    double2 s = make_double2(0.0, 0.0);
+    for (unsigned q = 0; q < gridDim.x; ++q) {
+      const volatile double2* pp = part + (size_t(b) * gridDim.x + q) * KMAXV + t;
+      s.x += pp->x;
+      s.y += pp->y;
+    }
+    red[t] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  ColState& S = st[b];
+  for (int k = 0; k < j; ++k) S.G[j][k] = zscale(red[j + 1 + k], S.scale[j] * S.scale[k]);
+  for (int i = 0; i <= j; ++i) {
+    double2 h = zscale(red[i], S.scale[i]);
+    for (int k = 0; k < i; ++k) h = zsub(h, zmul(S.hc[k], S.G[i][k]));
+    S.hc[i] = h;
+    S.coef[i] = zscale(h, S.scale[i]);
+  }
+}
+
+// V_{j+1}raw = w - sum_i coef_i Vraw_i ; hnorm ; Givens + convergence (inc/krylov.hpp:219-254)
+__global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, ColState* st, int* act,
+                                               const float2* __restrict__ W, float2* __restrict__ V, double* part,
+                                               unsigned* ticket, double* hist, int hist_cap, double rel_tol,
+                                               int max_iters, float* scale_out) {
+  const int b = blockIdx.y;
+  if (!act[b]) return;
+  ColState& S = st[b];
+  const size_t N = size_t(F.nx) * F.ny;
+  const size_t BN = size_t(B) * N;
+  __shared__ float2 cf[kMaxRestart + 1];
+  for (int i = threadIdx.x; i <= j; i += KT) cf[i] = make_float2(float(S.coef[i].x), float(S.coef[i].y));
+  __syncthreads();
+  const float2* wb = W + b * N;
+  float2* Vn = V + size_t(j + 1) * BN + b * N;
+  double acc = 0.0;
+  for (size_t base = size_t(blockIdx.x) * KTILE; base < N; base += size_t(gridDim.x) * KTILE) {
+    float2 t[KNPT];
+    bool ok[KNPT];
+#pragma unroll
+    for (int q = 0; q < KNPT; ++q) {
+      const size_t p = base + q * KT + threadIdx.x;
+      ok[q] = p < N;
+      t[q] = ok[q] ? ld(wb, p) : make_float2(0.f, 0.f);
+    }
+    for (int i = 0; i <= j; ++i) {
+      const float2* Vi = V + size_t(i) * BN + b * N;
+      const float2 c = cf[i];
+#pragma unroll
+      for (int q = 0; q < KNPT; ++q)
+        if (ok[q]) t[q] = csub(t[q], cmul(c, ld(Vi, base + q * KT + threadIdx.x)));
+    }
+#pragma unroll
+    for (int q = 0; q < KNPT; ++q)
+      if (ok[q]) {
+        Vn[base + q * KT + threadIdx.x] = t[q];
+        acc += dnorm2(t[q]);
+      }
+  }
+  acc = warp_sum(acc);
+  __shared__ double wp[KT / 32];
+  if ((threadIdx.x & 31) == 0) wp[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < KT / 32; ++w) t += wp[w];
+    part[size_t(b) * gridDim.x + blockIdx.x] = t;
+  }
+  if (!last_cta(ticket, b, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
+  const double hnorm = sqrt(t);
+  double2* hj = S.H[j];
+  for (int i = 0; i <= j; ++i) hj[i] = S.hc[i];
+  hj[j + 1] = make_double2(hnorm, 0.0);
+  for (int i = 0; i < j; ++i) {
+    const double2 t1 = dadd(zscale(hj[i], S.cs[i]), zmul(S.sn[i], hj[i + 1]));
+    hj[i + 1] = dadd(zscale(zmul(zconj(S.sn[i]), hj[i]), -1.0), zscale(hj[i + 1], S.cs[i]));
+    hj[i] = t1;
+  }
+  {  // make_givens (inc/krylov.hpp:49-64)
+    const double2 a = hj[j];
+    const double aa = hypot(a.x, a.y), rho = hypot(aa, hnorm);
+    if (rho == 0.0) {
+      S.cs[j] = 1.0;
+      S.sn[j] = make_double2(0.0, 0.0);
+    } else if (aa == 0.0) {
+      S.cs[j] = 0.0;
+      S.sn[j] = make_double2(1.0, 0.0);
+    } else {
+      S.cs[j] = aa / rho;
+      S.sn[j] = zscale(a, hnorm / (rho * aa));
+    }
+  }
+  hj[j] = dadd(zscale(hj[j], S.cs[j]), zmul(S.sn[j], hj[j + 1]));
+  hj[j + 1] = make_double2(0.0, 0.0);
+  S.g[j + 1] = zscale(zmul(zconj(S.sn[j]), S.g[j]), -1.0);
+  S.g[j] = zscale(S.g[j], S.cs[j]);
+  S.k = j + 1;
+  S.iters += 1;
+  const double est = hypot(S.g[j + 1].x, S.g[j + 1].y);
+  if (S.hist_len < hist_cap) hist[size_t(b) * hist_cap + S.hist_len] = est;
+  S.hist_len += 1;
+  const bool happy = hnorm <= 1e-14 * S.beta0;
+  if (happy) S.breakdown = 1;
+  if (est / S.beta0 <= rel_tol || happy) {
+    S.converged = 1;
+    S.frozen = 1;
+    S.active = 0;
+  } else if (S.iters >= max_iters) {
+    S.frozen = 1;
+    S.active = 0;
+  } else if (S.k < m) {
+    S.scale[j + 1] = 1.0 / hnorm;
+  } else {
+    S.active = 0;  // cycle end; finalize folds the correction
+  }
+  act[b] = S.active;
+  scale_out[b] = float(S.scale[S.active ? j + 1 : 0]);
+}
+
+// y = R^-1 g (back-substitution, inc/krylov.hpp:119-126); x += sum_i y_i Z_i
+__global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st, const float2* __restrict__ Z,
+                                                 double2* __restrict__ x) {
+  const int b = blockIdx.y;
+  const ColState& S = st[b];
+  const int k = S.k;
+  if (k == 0) return;
+  __shared__ double2 y[kMaxRestart];
+  if (threadIdx.x == 0) {
+    for (int i = k - 1; i >= 0; --i) {
+      double2 sum = S.g[i];
+      for (int l = i + 1; l < k; ++l) sum = zsub(sum, zmul(S.H[l][i], y[l]));
+      y[i] = zdiv(sum, S.H[i][i]);
+    }
+  }
+  __syncthreads();
+  const size_t N = size_t(F.nx) * F.ny;
+  const size_t BN = size_t(B) * N;
+  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
+    double2 acc = x[b * N + p];
+    for (int i = 0; i < k; ++i) {
+      const float2 z = ld(Z + size_t(i) * BN + b * N, p);
+      acc.x += y[i].x * double(z.x) - y[i].y * double(z.y);
+      acc.y += y[i].x * double(z.y) + y[i].y * double(z.x);
+    }
+    x[b * N + p] = acc;
+  }
+}
+
+__global__ void k_init_state(ColState* st, int B) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  ColState& S = st[b];
+  S.beta0 = 0.0;
+  S.iters = S.k = S.hist_len = 0;
+  S.frozen = S.converged = S.breakdown = S.active = 0;
+}
+
+FineView fine_view(Context& c) {
+  Level& L = *c.levels[0];
+  return FineView{L.nx, L.ny, 1.0 / (L.h * L.h), L.dA64.p, L.dA.p};
+}
+
+int nblk_for(Context& c, size_t N, int B) {
+  const size_t tiles = (N + KTILE - 1) / KTILE;
+  const int cap = std::max(1, 4 * c.num_sms / std::max(1, B));
+  return int(std::max<size_t>(1, std::min<size_t>(tiles, size_t(cap))));
+}
+
+}  // namespace
+
+struct KScope {
+  Context& c;
+  int cls, tok;
+  double bytes;
+  KScope(Context& c_, int cls_, double bytes_ = 0) : c(c_), cls(cls_), tok(prof_begin(c_, cls_)), bytes(bytes_) {}
+  ~KScope() { prof_end(c, cls, tok, bytes, 0); }
+};
+
+void krylov_alloc(Context& c, int B, int m, int hist_cap) {
+  if (m < 1 || m > kMaxRestart) throw HbError{HB_ERR_ARG, "restart must be in [1, 32]"};
+  const size_t N = c.levels[0]->N();
+  c.kstate.ensure(size_t(B) * sizeof(ColState));
+  c.kV.ensure(size_t(m + 1) * B * N);
+  c.kZ.ensure(size_t(m) * B * N);
+  c.kW.ensure(size_t(B) * N);
+  const int nb = nblk_for(c, N, B);
+  c.kpart.ensure(size_t(B) * nb * KMAXV);
+  c.khist.ensure(size_t(B) * std::max(1, hist_cap));
+  c.kact.ensure(B);
+  c.kscale.ensure(B);
+  c.kcount.ensure(1);
+  if (c.kticket.n < size_t(B)) {
+    c.kticket.ensure(B);
+    HB_CUDA(cudaMemsetAsync(c.kticket.p, 0, sizeof(unsigned) * B, c.stream));
+  }
+  HB_CUDA(cudaMemsetAsync(c.kticket.p, 0, sizeof(unsigned) * B, c.stream));
+  k_init_state<<<(B + 127) / 128, 128, 0, c.stream>>>(reinterpret_cast<ColState*>(c.kstate.p), B);
+  HB_CUDA(cudaGetLastError());
+  c.k_B = B;
+  c.k_m = m;
+  c.k_hist = hist_cap;
+}
+
+void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, float2* V0, int hist_cap,
+                       double rel_tol, int max_iters) {
+  const size_t N = c.levels[0]->N();
+  const int nb = nblk_for(c, N, B);
+  KScope ks(c, PC_KRYLOV_RESTART, double(B) * N * 56.0);
+  HB_CUDA(cudaMemsetAsync(c.kcount.p, 0, sizeof(int), c.stream));
+  k_restart<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), b, x, V0,
+                                               reinterpret_cast<double*>(c.kpart.p), c.kticket.p, c.khist.p,
+                                               hist_cap, rel_tol, max_iters, c.kact.p, c.kscale.p, c.kcount.p);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V) {
+  const size_t N = c.levels[0]->N();
+  const int nb = nblk_for(c, N, B);
+  KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0 + 8.0));
+  k_adots<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p,
+                                             Zj, w, V, c.kpart.p, c.kticket.p);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* V, int hist_cap, double rel_tol,
+                      int max_iters) {
+  const size_t N = c.levels[0]->N();
+  const int nb = nblk_for(c, N, B);
+  KScope ks(c, PC_KRYLOV_UPDATE, double(B) * N * (8.0 * (j + 1) + 16.0));
+  k_update<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p),
+                                              c.kact.p, w, V, reinterpret_cast<double*>(c.kpart.p), c.kticket.p,
+                                              c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x) {
+  (void)m;
+  const size_t N = c.levels[0]->N();
+  const int nb = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
+  KScope ks(c, PC_KRYLOV_FINAL);
+  k_finalize<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), Z, x);
+  HB_CUDA(cudaGetLastError());
+}
+
+// report readback helpers (host side of hb_fgmres)
+void krylov_report(Context& c, int B, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv,
+                   uint8_t* brk) {
+  std::vector<ColState> hs(B);
+  HB_CUDA(cudaMemcpyAsync(hs.data(), c.kstate.p, sizeof(ColState) * B, cudaMemcpyDeviceToHost, c.stream));
+  std::vector<double> hh;
+  if (hist && c.k_hist > 0) {
+    hh.resize(size_t(B) * c.k_hist);
+    HB_CUDA(cudaMemcpyAsync(hh.data(), c.khist.p, sizeof(double) * hh.size(), cudaMemcpyDeviceToHost, c.stream));
+  }
+  HB_CUDA(cudaStreamSynchronize(c.stream));
+  for (int b = 0; b < B; ++b) {
+    if (hist_len) hist_len[b] = hs[b].hist_len;
+    if (iters) iters[b] = hs[b].iters;
+    if (conv) conv[b] = uint8_t(hs[b].converged);
+    if (brk) brk[b] = uint8_t(hs[b].breakdown);
+    if (hist)
+      for (int i = 0; i < std::min(hist_stride, std::min(hs[b].hist_len, c.k_hist)); ++i)
+        hist[size_t(b) * hist_stride + i] = hh[size_t(b) * c.k_hist + i];
+  }
+}
+
+}  // namespace hb

@@ -1,0 +1,559 @@
+// Classic U-Net / encoder forward on sm_100a.
+//
+// Activations are NHWC fp32 so a 3x3 convolution is an implicit GEMM with
+// M = pixels, N = C_out, K = 9*C_in (taps outer, channels inner).  Channel
+// concatenation [a | b] (inc/autodiff.hpp:403) is never materialised: the
+// conv reads K from two sources.  The encoder context maps are broadcast over
+// the batch (tile_batch, inc/tensor.hpp:81) by a zero batch stride.
+//
+// Conv kernel (this file): CTA tile 128 pixels x 32 output channels, K in
+// chunks of 8 input channels x 9 taps staged in shared memory, 4x4 register
+// micro-tile, fp32 FFMA with fused bias + ReLU.
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "hb_common.cuh"
+#include "hb_host.h"
+#include "hb_internal.h"
+
+namespace hb {
+
+namespace {
+
+constexpr int CT_H = 8, CT_W = 16, CT_CO = 32, CT_CI = 8;
+constexpr int PH = CT_H + 2, PW = CT_W + 2;
+
+struct ConvArgs {
+  int B, H, W;
+  const float* a;  // NHWC, ca channels
+  long long sa;    // batch stride of a (elements)
+  int ca;
+  const float* b;  // NHWC, cb channels (may be null)
+  long long sb;    // batch stride of b (0 = broadcast)
+  int cb;
+  const float* w;  // packed [(tap*cin + ci)][cout]
+  const float* bias;
+  int cout;
+  int relu;
+  float* out;  // NHWC cout
+  const int* act;
+};
+
+__global__ void __launch_bounds__(256) k_conv3x3(ConvArgs p) {
+  const int bz = blockIdx.z;
+  if (p.act && !p.act[bz]) return;
+  __shared__ float patch[PH * PW][CT_CI + 1];
+  __shared__ __align__(16) float wts[9][CT_CI][CT_CO];
+  const int tilesW = (p.W + CT_W - 1) / CT_W;
+  const int y0 = (blockIdx.x / tilesW) * CT_H, x0 = (blockIdx.x % tilesW) * CT_W;
+  const int co0 = blockIdx.y * CT_CO;
+  const int t = threadIdx.x;
+  const int cg = t % (CT_CO / 4), pg = t / (CT_CO / 4);
+  const int prow = pg / (CT_W / 4), pcol = (pg % (CT_W / 4)) * 4;
+  const int cin = p.ca + p.cb;
+  float acc[4][4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int r = 0; r < 4; ++r) acc[q][r] = 0.f;
+  const float* A = p.a + bz * p.sa;
+  const float* Bsrc = p.b ? p.b + bz * p.sb : nullptr;
+  for (int ci0 = 0; ci0 < cin; ci0 += CT_CI) {
+    for (int idx = t; idx < PH * PW * CT_CI; idx += 256) {
+      const int c = idx % CT_CI, pix = idx / CT_CI;
+      const int gy = y0 + pix / PW - 1, gx = x0 + pix % PW - 1;
+      const int ci = ci0 + c;
+      float v = 0.f;
+      if (gy >= 0 && gy < p.H && gx >= 0 && gx < p.W && ci < cin) {
+        const size_t px = size_t(gy) * p.W + gx;
+        v = ci < p.ca ? __ldg(A + px * p.ca + ci) : __ldg(Bsrc + px * p.cb + (ci - p.ca));
+      }
+      patch[pix][c] = v;
+    }
+    for (int idx = t; idx < 9 * CT_CI * CT_CO; idx += 256) {
+      const int col = idx % CT_CO, rest = idx / CT_CO;
+      const int cl = rest % CT_CI, tap = rest / CT_CI;
+      const int ci = ci0 + cl, co = co0 + col;
+      wts[tap][cl][col] = (ci < cin && co < p.cout) ? __ldg(p.w + (size_t(tap) * cin + ci) * p.cout + co) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int c = 0; c < CT_CI; ++c) {
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky)
+#pragma unroll
+        for (int kx = 0; kx < 3; ++kx) {
+          const float4 w4 = *reinterpret_cast<const float4*>(&wts[ky * 3 + kx][c][cg * 4]);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float v = patch[(prow + ky) * PW + pcol + q + kx][c];
+            acc[q][0] = fmaf(v, w4.x, acc[q][0]);
+            acc[q][1] = fmaf(v, w4.y, acc[q][1]);
+            acc[q][2] = fmaf(v, w4.z, acc[q][2]);
+            acc[q][3] = fmaf(v, w4.w, acc[q][3]);
+          }
+        }
+    }
+    __syncthreads();
+  }
+  const int y = y0 + prow;
+  if (y >= p.H) return;
+  float* O = p.out + size_t(bz) * p.H * p.W * p.cout;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int x = x0 + pcol + q;
+    if (x >= p.W) continue;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int co = co0 + cg * 4 + r;
+      if (co >= p.cout) continue;
+      float v = acc[q][r] + __ldg(p.bias + co);
+      if (p.relu) v = fmaxf(v, 0.f);
+      O[(size_t(y) * p.W + x) * p.cout + co] = v;
+    }
+  }
+}
+
+__global__ void k_maxpool2(int B, int H, int W, int C, const float* __restrict__ in, float* __restrict__ out,
+                           const int* act) {
+  const int Ho = H / 2, Wo = W / 2;
+  const size_t total = size_t(Ho) * Wo * C;
+  const int b = blockIdx.y;
+  if (act && !act[b]) return;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % C);
+    const size_t px = i / C;
+    const int x = int(px % Wo), y = int(px / Wo);
+    const float* s = in + size_t(b) * H * W * C;
+    const float a0 = s[(size_t(2 * y) * W + 2 * x) * C + c], a1 = s[(size_t(2 * y) * W + 2 * x + 1) * C + c];
+    const float a2 = s[(size_t(2 * y + 1) * W + 2 * x) * C + c], a3 = s[(size_t(2 * y + 1) * W + 2 * x + 1) * C + c];
+    out[size_t(b) * Ho * Wo * C + i] = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+  }
+}
+
+// x2 bilinear, half-pixel centres, clamped edges (inc/datagen.hpp:19-37 weights)
+__device__ __forceinline__ void up_taps(int o, int n, int* i0, int* i1, float* f) {
+  const float s = (o + 0.5f) * 0.5f - 0.5f;
+  int a = int(floorf(s));
+  a = a < 0 ? 0 : (a > n - 1 ? n - 1 : a);
+  *i0 = a;
+  *i1 = a + 1 < n - 1 ? a + 1 : n - 1;
+  float fr = s - float(a);
+  *f = fr < 0.f ? 0.f : (fr > 1.f ? 1.f : fr);
+}
+
+__global__ void k_upsample2(int B, int H, int W, int C, const float* __restrict__ in, long long sin_,
+                            float* __restrict__ out, const int* act) {
+  const int Ho = 2 * H, Wo = 2 * W;
+  const size_t total = size_t(Ho) * Wo * C;
+  const int b = blockIdx.y;
+  if (act && !act[b]) return;
+  const float* s = in + b * sin_;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % C);
+    const size_t px = i / C;
+    const int ox = int(px % Wo), oy = int(px / Wo);
+    int y0, y1, x0, x1;
+    float fy, fx;
+    up_taps(oy, H, &y0, &y1, &fy);
+    up_taps(ox, W, &x0, &x1, &fx);
+    const float v00 = s[(size_t(y0) * W + x0) * C + c], v01 = s[(size_t(y0) * W + x1) * C + c];
+    const float v10 = s[(size_t(y1) * W + x0) * C + c], v11 = s[(size_t(y1) * W + x1) * C + c];
+    out[size_t(b) * total + i] = (1.f - fy) * ((1.f - fx) * v00 + fx * v01) + fy * ((1.f - fx) * v10 + fx * v11);
+  }
+}
+
+// [h^2 Re r, h^2 Im r, kappa^2] NHWC (inc/precond.hpp:74-83, gamma dropped)
+__global__ void k_pack(int N, float h2, const int* act, const float2* __restrict__ r, const float* rscale,
+                       const float* __restrict__ k2, float* __restrict__ x) {
+  const int b = blockIdx.y;
+  if (act && !act[b]) return;
+  const float s = h2 * (rscale ? rscale[b] : 1.0f);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const float2 v = r[size_t(b) * N + i];
+    float* o = x + (size_t(b) * N + i) * 3;
+    o[0] = s * v.x;
+    o[1] = s * v.y;
+    o[2] = k2[i];
+  }
+}
+
+__global__ void k_unpack(int N, const int* act, const float* __restrict__ y, float2* __restrict__ e) {
+  const int b = blockIdx.y;
+  if (act && !act[b]) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const float* s = y + (size_t(b) * N + i) * 2;
+    e[size_t(b) * N + i] = make_float2(s[0], s[1]);
+  }
+}
+
+__global__ void k_nhwc_to_nchw(int B, int C, int HW, const float* __restrict__ in, float* __restrict__ out) {
+  const size_t total = size_t(B) * C * HW;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+    const int p = int(i % HW);
+    const size_t bc = i / HW;
+    const int c = int(bc % C), b = int(bc / C);
+    out[i] = in[(size_t(b) * HW + p) * C + c];
+  }
+}
+__global__ void k_nchw_to_nhwc(int B, int C, int HW, const float* __restrict__ in, float* __restrict__ out) {
+  const size_t total = size_t(B) * C * HW;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
+    const int c = int(i % C);
+    const size_t bp = i / C;
+    const int p = int(bp % HW), b = int(bp / HW);
+    out[i] = in[(size_t(b) * C + c) * HW + p];
+  }
+}
+
+int grid1(size_t work, int cap = 4096) { return int(std::max<size_t>(1, std::min<size_t>((work + 255) / 256, cap))); }
+
+}  // namespace
+
+struct NScope {
+  Context& c;
+  int cls, tok;
+  double bytes, flops;
+  NScope(Context& c_, int cls_, double bytes_ = 0, double flops_ = 0)
+      : c(c_), cls(cls_), tok(prof_begin(c_, cls_)), bytes(bytes_), flops(flops_) {}
+  ~NScope() { prof_end(c, cls, tok, bytes, flops); }
+};
+
+// ---------------------------------------------------------------- launchers
+static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, long long sa,
+                 int ca, const float* b, long long sb, int cb, int relu, float* out) {
+  if (ca + cb != cw.cin) throw HbError{HB_ERR_ARG, "conv input channels mismatch"};
+  ConvArgs p{B, H, W, a, sa, ca, b, sb, cb, cw.dw.p, cw.db.p, cw.cout, relu, out, act};
+  const dim3 grid(((W + CT_W - 1) / CT_W) * ((H + CT_H - 1) / CT_H), (cw.cout + CT_CO - 1) / CT_CO, B);
+  NScope ns(c, PC_CONV, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
+  k_conv3x3<<<grid, 256, 0, c.stream>>>(p);
+  HB_CUDA(cudaGetLastError());
+}
+
+static void maxpool(Context& c, int B, const int* act, int H, int W, int C, const float* in, float* out) {
+  NScope ns(c, PC_NETIO);
+  k_maxpool2<<<dim3(grid1(size_t(H / 2) * (W / 2) * C), B), 256, 0, c.stream>>>(B, H, W, C, in, out, act);
+  HB_CUDA(cudaGetLastError());
+}
+
+static void upsample(Context& c, int B, const int* act, int H, int W, int C, const float* in, long long sin_,
+                     float* out) {
+  NScope ns(c, PC_NETIO);
+  k_upsample2<<<dim3(grid1(size_t(4) * H * W * C), B), 256, 0, c.stream>>>(B, H, W, C, in, sin_, out, act);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const int* act, const float2* r,
+                       const float* rscale, float* x) {
+  NScope ns(c, PC_NETIO);
+  const int N = L.nx * L.ny;
+  k_pack<<<dim3(grid1(N), B), 256, 0, c.stream>>>(N, float(h2), act, r, rscale, L.k2f, x);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_unpack_output(Context& c, int N, int B, const int* act, const float* y, float2* e) {
+  NScope ns(c, PC_NETIO);
+  k_unpack<<<dim3(grid1(N), B), 256, 0, c.stream>>>(N, act, y, e);
+  HB_CUDA(cudaGetLastError());
+}
+
+// ------------------------------------------------------------ net topology
+static void build_topology(Net& n) {
+  const hb_net_cfg& g = n.cfg;
+  n.convs.clear();
+  auto add = [&](int cout, int cin) {
+    ConvW w;
+    w.cout = cout;
+    w.cin = cin;
+    w.w.assign(size_t(cout) * cin * 9, 0.f);
+    w.b.assign(size_t(cout), 0.f);
+    n.convs.push_back(std::move(w));
+    return int(n.convs.size()) - 1;
+  };
+  if (g.kind == HB_NET_ENCODER) {
+    for (int l = 0; l < g.levels; ++l) {
+      n.enc1[l] = add(g.base, l == 0 ? g.in_ch : g.base);
+      n.enc2[l] = add(g.base, g.base);
+    }
+    n.head = -1;
+  } else {
+    for (int l = 0; l < g.levels; ++l) {
+      n.enc1[l] = add(g.base << l, (l == 0 ? g.in_ch : g.base << (l - 1)) + g.ctx_ch);
+      n.enc2[l] = add(g.base << l, g.base << l);
+    }
+    for (int l = g.levels - 2; l >= 0; --l) {
+      n.up[l] = add(g.base << l, (g.base << (l + 1)) + g.ctx_ch);
+      n.dec1[l] = add(g.base << l, 2 * (g.base << l));
+      n.dec2[l] = add(g.base << l, g.base << l);
+    }
+    n.head = add(2, g.base);
+  }
+  n.dirty = true;
+}
+
+void net_upload(Context& c, int slot) {
+  Net& n = c.nets[slot];
+  if (!n.dirty) return;
+  for (auto& cw : n.convs) {
+    std::vector<float> pk(size_t(9) * cw.cin * cw.cout);
+    for (int co = 0; co < cw.cout; ++co)
+      for (int ci = 0; ci < cw.cin; ++ci)
+        for (int tap = 0; tap < 9; ++tap)
+          pk[(size_t(tap) * cw.cin + ci) * cw.cout + co] = cw.w[(size_t(co) * cw.cin + ci) * 9 + tap];
+    cw.dw.ensure(pk.size());
+    cw.db.ensure(cw.b.size());
+    HB_CUDA(cudaMemcpy(cw.dw.p, pk.data(), pk.size() * sizeof(float), cudaMemcpyHostToDevice));
+    HB_CUDA(cudaMemcpy(cw.db.p, cw.b.data(), cw.b.size() * sizeof(float), cudaMemcpyHostToDevice));
+  }
+  n.dirty = false;
+  if (slot == 1) c.ctx_valid = false;
+}
+
+// per-forward activation buffers, keyed by shape
+struct NetBuffers {
+  int B = 0, H = 0, W = 0, slot = -1;
+  std::vector<DBuf<float>> skip, tmp, pool, up, u;
+};
+static thread_local NetBuffers g_nb[2];
+
+static NetBuffers& buffers(Context& c, int slot, int B, int H, int W) {
+  NetBuffers& nb = g_nb[slot];
+  const Net& n = c.nets[slot];
+  const int L = n.cfg.levels;
+  if (nb.B >= B && nb.H == H && nb.W == W && nb.slot == slot && int(nb.skip.size()) == L) return nb;
+  nb.skip = std::vector<DBuf<float>>(size_t(L));
+  nb.tmp = std::vector<DBuf<float>>(size_t(L));
+  nb.pool = std::vector<DBuf<float>>(size_t(L));
+  nb.up = std::vector<DBuf<float>>(size_t(L));
+  nb.u = std::vector<DBuf<float>>(size_t(L));
+  for (int l = 0; l < L; ++l) {
+    const size_t px = size_t(B) * (H >> l) * (W >> l);
+    const int cl = n.cfg.kind == HB_NET_ENCODER ? n.cfg.base : (n.cfg.base << l);
+    nb.skip[size_t(l)].ensure(px * cl);
+    nb.tmp[size_t(l)].ensure(px * cl);
+    if (l > 0) nb.pool[size_t(l)].ensure(px * (n.cfg.kind == HB_NET_ENCODER ? n.cfg.base : (n.cfg.base << (l - 1))));
+    if (l < L - 1 && n.cfg.kind == HB_NET_SOLVER) {
+      nb.up[size_t(l)].ensure(px * (n.cfg.base << (l + 1)));
+      nb.u[size_t(l)].ensure(px * cl);
+    }
+  }
+  nb.B = B;
+  nb.H = H;
+  nb.W = W;
+  nb.slot = slot;
+  return nb;
+}
+
+// solver U-Net (A5, + A7 context concat); x NHWC in_ch -> y NHWC 2
+void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, const float* x, float* y) {
+  Net& n = c.nets[slot];
+  if (!n.set || n.cfg.kind != HB_NET_SOLVER) throw HbError{HB_ERR_STATE, "solver net not set"};
+  const int L = n.cfg.levels;
+  if (H % (1 << (L - 1)) || W % (1 << (L - 1))) throw HbError{HB_ERR_ARG, "input dims must be divisible by 2^(L-1)"};
+  const bool es = n.cfg.ctx_ch > 0;
+  if (es && !c.ctx_valid) throw HbError{HB_ERR_STATE, "encoder-solver net needs hb_encode first"};
+  net_upload(c, slot);
+  NetBuffers& nb = buffers(c, slot, B, H, W);
+  const float* cur = x;
+  int curc = n.cfg.in_ch;
+  for (int l = 0; l < L; ++l) {
+    const int Hl = H >> l, Wl = W >> l, cl = n.cfg.base << l;
+    if (l > 0) {
+      maxpool(c, B, act, Hl * 2, Wl * 2, curc, cur, nb.pool[size_t(l)].p);
+      cur = nb.pool[size_t(l)].p;
+    }
+    const float* ctxp = es ? c.ctx_maps[size_t(2 * l)].p : nullptr;
+    conv(c, n.convs[size_t(n.enc1[l])], B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, ctxp, 0,
+         es ? n.cfg.ctx_ch : 0, 1, nb.tmp[size_t(l)].p);
+    conv(c, n.convs[size_t(n.enc2[l])], B, act, Hl, Wl, nb.tmp[size_t(l)].p, (long long)Hl * Wl * cl, cl, nullptr, 0,
+         0, 1, nb.skip[size_t(l)].p);
+    cur = nb.skip[size_t(l)].p;
+    curc = cl;
+  }
+  for (int l = L - 2; l >= 0; --l) {
+    const int Hl = H >> l, Wl = W >> l, cl = n.cfg.base << l;
+    // concat(x, ctx_{l+1}) then upsample == [upsample(x) | upsample(ctx_{l+1})]; the latter is cached
+    upsample(c, B, act, Hl / 2, Wl / 2, curc, cur, (long long)(Hl / 2) * (Wl / 2) * curc, nb.up[size_t(l)].p);
+    const float* cup = es ? c.ctx_maps[size_t(2 * (l + 1) + 1)].p : nullptr;
+    conv(c, n.convs[size_t(n.up[l])], B, act, Hl, Wl, nb.up[size_t(l)].p, (long long)Hl * Wl * curc, curc, cup, 0,
+         es ? n.cfg.ctx_ch : 0, 0, nb.u[size_t(l)].p);
+    conv(c, n.convs[size_t(n.dec1[l])], B, act, Hl, Wl, nb.u[size_t(l)].p, (long long)Hl * Wl * cl, cl,
+         nb.skip[size_t(l)].p, (long long)Hl * Wl * cl, cl, 1, nb.tmp[size_t(l)].p);
+    conv(c, n.convs[size_t(n.dec2[l])], B, act, Hl, Wl, nb.tmp[size_t(l)].p, (long long)Hl * Wl * cl, cl, nullptr, 0,
+         0, 1, nb.skip[size_t(l)].p);
+    cur = nb.skip[size_t(l)].p;
+    curc = cl;
+  }
+  conv(c, n.convs[size_t(n.head)], B, act, H, W, cur, (long long)H * W * curc, curc, nullptr, 0, 0, 0, y);
+}
+
+// encoder over kappa^2 (once per medium): ctx_maps[2l] = ctx_l (NHWC base ch at
+// level l), ctx_maps[2l+1] = upsample(ctx_l) at level l-1 (for the up-convs)
+void encoder_forward_dev(Context& c, int H, int W, const float* k2f) {
+  Net& e = c.nets[1];
+  if (!e.set || e.cfg.kind != HB_NET_ENCODER) throw HbError{HB_ERR_STATE, "encoder net (slot 1) not set"};
+  net_upload(c, 1);
+  const int L = e.cfg.levels, C = e.cfg.base;
+  NetBuffers& nb = buffers(c, 1, 1, H, W);
+  c.ctx_maps = std::vector<DBuf<float>>(size_t(2 * L));
+  const float* cur = k2f;  // NHWC with 1 channel == plain [H][W]
+  int curc = 1;
+  for (int l = 0; l < L; ++l) {
+    const int Hl = H >> l, Wl = W >> l;
+    if (l > 0) {
+      maxpool(c, 1, nullptr, Hl * 2, Wl * 2, curc, cur, nb.pool[size_t(l)].p);
+      cur = nb.pool[size_t(l)].p;
+    }
+    conv(c, e.convs[size_t(e.enc1[l])], 1, nullptr, Hl, Wl, cur, 0, curc, nullptr, 0, 0, 1, nb.tmp[size_t(l)].p);
+    c.ctx_maps[size_t(2 * l)].ensure(size_t(Hl) * Wl * C);
+    conv(c, e.convs[size_t(e.enc2[l])], 1, nullptr, Hl, Wl, nb.tmp[size_t(l)].p, 0, C, nullptr, 0, 0, 1,
+         c.ctx_maps[size_t(2 * l)].p);
+    cur = c.ctx_maps[size_t(2 * l)].p;
+    curc = C;
+    if (l > 0) {
+      c.ctx_maps[size_t(2 * l + 1)].ensure(size_t(4) * Hl * Wl * C);
+      upsample(c, 1, nullptr, Hl, Wl, C, cur, 0, c.ctx_maps[size_t(2 * l + 1)].p);
+    }
+  }
+  c.ctx_valid = true;
+}
+
+}  // namespace hb
+
+// ===================================================================== C ABI
+using namespace hb;
+struct hb_ctx : hb::Context {};
+
+#define HB_API_BEGIN \
+  if (!ctx) return HB_ERR_ARG; \
+  try {
+#define HB_API_END                  \
+  return HB_OK;                     \
+  }                                 \
+  catch (const HbError& e) {        \
+    ctx->err = e.msg;               \
+    return e.code;                  \
+  }                                 \
+  catch (const std::exception& e) { \
+    ctx->err = e.what();            \
+    return HB_ERR_ARG;              \
+  }
+
+static Net& net_slot(hb_ctx* ctx, int slot) {
+  if (slot < 0 || slot > 1) throw HbError{HB_ERR_ARG, "net slot must be 0 or 1"};
+  return ctx->nets[slot];
+}
+
+extern "C" {
+
+int hb_set_net(hb_ctx* ctx, int slot, const hb_net_cfg* cfg) {
+  HB_API_BEGIN
+  Net& n = net_slot(ctx, slot);
+  if (!cfg || cfg->levels < 1 || cfg->levels > 8 || cfg->base < 1 || cfg->in_ch < 1 || cfg->ctx_ch < 0)
+    throw HbError{HB_ERR_ARG, "bad net config"};
+  if (cfg->kind != HB_NET_SOLVER && cfg->kind != HB_NET_ENCODER) throw HbError{HB_ERR_ARG, "bad net kind"};
+  n.cfg = *cfg;
+  build_topology(n);
+  n.set = true;
+  if (slot == 1) ctx->ctx_valid = false;
+  HB_API_END
+}
+
+int hb_net_num_convs(hb_ctx* ctx, int slot) {
+  if (!ctx || slot < 0 || slot > 1) return HB_ERR_ARG;
+  return int(ctx->nets[slot].convs.size());
+}
+
+int hb_net_conv_shape(hb_ctx* ctx, int slot, int index, int* cout, int* cin) {
+  HB_API_BEGIN
+  Net& n = net_slot(ctx, slot);
+  if (index < 0 || index >= int(n.convs.size())) throw HbError{HB_ERR_ARG, "conv index out of range"};
+  if (cout) *cout = n.convs[size_t(index)].cout;
+  if (cin) *cin = n.convs[size_t(index)].cin;
+  HB_API_END
+}
+
+int hb_load_conv(hb_ctx* ctx, int slot, int index, const float* w, const float* b) {
+  HB_API_BEGIN
+  Net& n = net_slot(ctx, slot);
+  if (index < 0 || index >= int(n.convs.size())) throw HbError{HB_ERR_ARG, "conv index out of range"};
+  ConvW& cw = n.convs[size_t(index)];
+  if (w) std::memcpy(cw.w.data(), w, cw.w.size() * sizeof(float));
+  if (b) std::memcpy(cw.b.data(), b, cw.b.size() * sizeof(float));
+  n.dirty = true;
+  if (slot == 1) ctx->ctx_valid = false;
+  HB_API_END
+}
+
+int hb_get_conv(hb_ctx* ctx, int slot, int index, float* w, float* b) {
+  HB_API_BEGIN
+  Net& n = net_slot(ctx, slot);
+  if (index < 0 || index >= int(n.convs.size())) throw HbError{HB_ERR_ARG, "conv index out of range"};
+  const ConvW& cw = n.convs[size_t(index)];
+  if (w) std::memcpy(w, cw.w.data(), cw.w.size() * sizeof(float));
+  if (b) std::memcpy(b, cw.b.data(), cw.b.size() * sizeof(float));
+  HB_API_END
+}
+
+int hb_init_net_he(hb_ctx* ctx, int slot, uint64_t seed) {
+  HB_API_BEGIN
+  Net& n = net_slot(ctx, slot);
+  if (!n.set) throw HbError{HB_ERR_STATE, "net not set"};
+  Rng r(seed);
+  for (auto& cw : n.convs) {
+    const float sd = float(std::sqrt(2.0 / double(cw.cin * 9)));
+    for (auto& x : cw.w) x = float(r.normal()) * sd;  // fill_normal (inc/tensor.hpp:51-53)
+    std::fill(cw.b.begin(), cw.b.end(), 0.f);
+  }
+  n.dirty = true;
+  if (slot == 1) ctx->ctx_valid = false;
+  HB_API_END
+}
+
+int hb_net_forward(hb_ctx* ctx, int batch, int H, int W, const float* in, float* out) {
+  HB_API_BEGIN
+  Net& n = net_slot(ctx, 0);
+  if (!n.set) throw HbError{HB_ERR_STATE, "net slot 0 not set"};
+  const int cin = n.cfg.in_ch;
+  const size_t px = size_t(batch) * H * W;
+  DBuf<float> a, b2, y, y2;
+  a.ensure(px * cin);
+  b2.ensure(px * cin);
+  y.ensure(px * 2);
+  y2.ensure(px * 2);
+  HB_CUDA(cudaMemcpyAsync(a.p, in, px * cin * sizeof(float), cudaMemcpyHostToDevice, ctx->stream));
+  k_nchw_to_nhwc<<<grid1(px * cin), 256, 0, ctx->stream>>>(batch, cin, H * W, a.p, b2.p);
+  net_forward_dev(*ctx, 0, batch, nullptr, H, W, b2.p, y.p);
+  k_nhwc_to_nchw<<<grid1(px * 2), 256, 0, ctx->stream>>>(batch, 2, H * W, y.p, y2.p);
+  HB_CUDA(cudaMemcpyAsync(out, y2.p, px * 2 * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  HB_API_END
+}
+
+int hb_encode(hb_ctx* ctx) {
+  HB_API_BEGIN
+  if (!ctx->has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built"};
+  const Level& L = *ctx->levels[0];
+  encoder_forward_dev(*ctx, L.ny, L.nx, L.k2f.p);
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  HB_API_END
+}
+
+int hb_get_context(hb_ctx* ctx, int level, float* out) {
+  HB_API_BEGIN
+  if (!ctx->ctx_valid) throw HbError{HB_ERR_STATE, "no encoder context (hb_encode)"};
+  const Net& e = ctx->nets[1];
+  if (level < 0 || level >= e.cfg.levels) throw HbError{HB_ERR_ARG, "level out of range"};
+  const Level& L = *ctx->levels[0];
+  const int Hl = L.ny >> level, Wl = L.nx >> level, C = e.cfg.base;
+  DBuf<float> t;
+  t.ensure(size_t(Hl) * Wl * C);
+  k_nhwc_to_nchw<<<grid1(size_t(Hl) * Wl * C), 256, 0, ctx->stream>>>(1, C, Hl * Wl, ctx->ctx_maps[size_t(2 * level)].p,
+                                                                      t.p);
+  HB_CUDA(cudaMemcpyAsync(out, t.p, size_t(Hl) * Wl * C * sizeof(float), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  HB_API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,444 @@
+"""Python host mirror of the helmbench solver/preconditioner API over the
+libhelmgpu C ABI (include/helmgpu.h).
+
+Names follow the reference (inc/ = /root/reference/proj/include/helmbench/):
+KrylovConfig / SolveReport (inc/krylov.hpp:11-35), VCycleConfig
+(inc/multigrid.hpp:13-21), Preconditioner and its plugins
+(inc/precond.hpp:14-165), block_fgmres (inc/krylov.hpp:83).  Errors keep the
+reference's convention: contract violations raise ValueError (the C++
+std::invalid_argument), numerical/device failures raise RuntimeError.
+
+There is no CPU fallback: importing this module on a machine without the
+built library raises, and every compute call goes through the CUDA library.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libhelmgpu.so")
+
+_dp = C.POINTER(C.c_double)
+_fp = C.POINTER(C.c_float)
+_ip = C.POINTER(C.c_int)
+_u8p = C.POINTER(C.c_uint8)
+_vp = C.c_void_p
+
+HB_COARSE = {"gmres": 0, "jacobi": 1, "net": 2}
+HB_PC = {"v": 0, "vu": 1}
+
+
+class _VCycleCfg(C.Structure):
+    _fields_ = [("levels", C.c_int), ("nu1", C.c_int), ("nu2", C.c_int), ("damping", C.c_double),
+                ("alpha", C.c_double), ("beta", C.c_double), ("coarse_solver", C.c_int),
+                ("coarse_iters", C.c_int)]
+
+
+class _NetCfg(C.Structure):
+    _fields_ = [("kind", C.c_int), ("levels", C.c_int), ("base", C.c_int), ("in_ch", C.c_int),
+                ("ctx_ch", C.c_int)]
+
+
+class _KrylovCfg(C.Structure):
+    _fields_ = [("restart", C.c_int), ("max_iters", C.c_int), ("rel_tol", C.c_double), ("flexible", C.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libhelmgpu.so (fails loudly when it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2203_11025_b200.build` "
+                              "(the CUDA library is the only implementation; there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.hb_create.argtypes = [C.c_int, C.POINTER(_vp)]
+        L.hb_destroy.argtypes = [_vp]
+        L.hb_last_error.restype = C.c_char_p
+        L.hb_last_error.argtypes = [_vp]
+        L.hb_stream.restype = _vp
+        L.hb_stream.argtypes = [_vp]
+        L.hb_synchronize.argtypes = [_vp]
+        L.hb_set_problem.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_double, _dp, _dp, C.c_double, C.c_double]
+        L.hb_build_hierarchy.argtypes = [_vp, C.POINTER(_VCycleCfg)]
+        L.hb_level_info.argtypes = [_vp, C.c_int, _ip, _ip, _dp]
+        L.hb_set_net.argtypes = [_vp, C.c_int, C.POINTER(_NetCfg)]
+        L.hb_net_num_convs.argtypes = [_vp, C.c_int]
+        L.hb_net_conv_shape.argtypes = [_vp, C.c_int, C.c_int, _ip, _ip]
+        L.hb_load_conv.argtypes = [_vp, C.c_int, C.c_int, _fp, _fp]
+        L.hb_get_conv.argtypes = [_vp, C.c_int, C.c_int, _fp, _fp]
+        L.hb_init_net_he.argtypes = [_vp, C.c_int, C.c_uint64]
+        L.hb_net_forward.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp]
+        L.hb_encode.argtypes = [_vp]
+        L.hb_get_context.argtypes = [_vp, C.c_int, _fp]
+        L.hb_operator_apply.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _dp, _dp]
+        L.hb_jacobi.argtypes = [_vp, C.c_int, C.c_int, _dp, _dp, C.c_int]
+        L.hb_restrict.argtypes = [_vp, C.c_int, C.c_int, _dp, _dp]
+        L.hb_prolong.argtypes = [_vp, C.c_int, C.c_int, _dp, _dp]
+        L.hb_coarse_solve.argtypes = [_vp, C.c_int, _dp, _dp]
+        L.hb_precond_apply.argtypes = [_vp, C.c_int, C.c_int, _dp, _dp]
+        L.hb_precond_name.restype = C.c_char_p
+        L.hb_precond_name.argtypes = [C.c_int]
+        L.hb_precond_requires_flexible.argtypes = [_vp, C.c_int]
+        L.hb_fgmres.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.c_int, _ip, _ip,
+                                _u8p, _u8p]
+        L.hb_fgmres_device.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _vp, _vp, _dp, C.c_int, _ip,
+                                       _ip, _u8p, _u8p]
+        L.hb_rng_normals.argtypes = [C.c_uint64, C.c_int64, _dp]
+        L.hb_absorbing_layer.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, _dp]
+        L.hb_make_medium.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_int,
+                                     C.c_uint64, C.c_int, C.c_double, C.c_double, _dp]
+        L.hb_point_sources.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]
+        L.hb_prof_enable.argtypes = [_vp, C.c_int]
+        L.hb_prof_reset.argtypes = [_vp]
+        L.hb_prof_count.argtypes = [_vp]
+        L.hb_prof_name.restype = C.c_char_p
+        L.hb_prof_name.argtypes = [_vp, C.c_int]
+        L.hb_prof_get.argtypes = [_vp, C.c_int, _dp, C.POINTER(C.c_int64), _dp, _dp]
+        L.hb_launch_count.restype = C.c_int64
+        L.hb_launch_count.argtypes = [_vp]
+        _lib = L
+    return _lib
+
+
+def _p(a, t=_dp):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def _c128(a):
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+# ------------------------------------------------------------ config types
+@dataclasses.dataclass
+class KrylovConfig:  # inc/krylov.hpp:11-16
+    restart: int = 10
+    max_iters: int = 200
+    rel_tol: float = 1e-6
+    flexible: bool = True
+
+
+@dataclasses.dataclass
+class VCycleConfig:  # inc/multigrid.hpp:13-21
+    levels: int = 3
+    nu1: int = 1
+    nu2: int = 1
+    damping: float = 0.8
+    alpha: float = 1.0
+    beta: float = 0.5
+    coarse_iters: int = 10
+    coarse_solver: str = "gmres"  # gmres | jacobi | net
+
+
+@dataclasses.dataclass
+class SolveReport:  # inc/krylov.hpp:20-35
+    residual_history: List[np.ndarray]
+    iterations: List[int]
+    converged: List[bool]
+    breakdown: List[bool]
+
+    def write_csv(self, os_):
+        os_.write("iter,rhs_index,relative_residual\n")
+        for c, h in enumerate(self.residual_history):
+            r0 = h[0] if len(h) and h[0] > 0 else 1.0
+            for i, v in enumerate(h):
+                os_.write(f"{i},{c},{v / r0:.17g}\n")
+
+
+# ------------------------------------------------------------------ context
+class Context:
+    """One GPU context (hb_ctx): problem, hierarchy, nets, solver state."""
+
+    def __init__(self, device: int = 0):
+        h = _vp()
+        rc = lib().hb_create(device, C.byref(h))
+        if rc != 0:
+            raise RuntimeError("hb_create: " + lib().hb_last_error(None).decode())
+        self.h = h
+        self.nx = self.ny = 0
+        self.vcfg: Optional[VCycleConfig] = None
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().hb_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc):
+        if rc != 0:
+            msg = lib().hb_last_error(self.h).decode()
+            if rc == -1:
+                raise ValueError(msg)
+            raise RuntimeError(msg)
+
+    @property
+    def stream(self) -> int:
+        return lib().hb_stream(self.h) or 0
+
+    def synchronize(self):
+        self._check(lib().hb_synchronize(self.h))
+
+    # problem + hierarchy (inc/grid.hpp:128, inc/multigrid.hpp:72)
+    def set_problem(self, kappa2, gamma, omega, lo, hi, h=None):
+        kappa2 = np.ascontiguousarray(kappa2, np.float64)
+        gamma = np.ascontiguousarray(gamma, np.float64)
+        ny, nx = kappa2.shape
+        self.nx, self.ny = nx, ny
+        self.h_mesh = 1.0 / nx if h is None else h
+        self._check(lib().hb_set_problem(self.h, nx, ny, self.h_mesh, omega, _p(kappa2), _p(gamma), lo, hi))
+
+    def build_hierarchy(self, cfg: VCycleConfig):
+        c = _VCycleCfg(cfg.levels, cfg.nu1, cfg.nu2, cfg.damping, cfg.alpha, cfg.beta,
+                       HB_COARSE[cfg.coarse_solver], cfg.coarse_iters)
+        self._check(lib().hb_build_hierarchy(self.h, C.byref(c)))
+        self.vcfg = cfg
+
+    def level_info(self, l):
+        nx, ny, h = C.c_int(), C.c_int(), C.c_double()
+        self._check(lib().hb_level_info(self.h, l, C.byref(nx), C.byref(ny), C.byref(h)))
+        return nx.value, ny.value, h.value
+
+    # networks
+    def set_net(self, slot, kind, levels, base=16, in_ch=3, ctx_ch=0):
+        c = _NetCfg({"solver": 0, "encoder": 1}[kind], levels, base, in_ch, ctx_ch)
+        self._check(lib().hb_set_net(self.h, slot, C.byref(c)))
+
+    def init_net_he(self, slot, seed):
+        self._check(lib().hb_init_net_he(self.h, slot, seed))
+
+    def net_convs(self, slot):
+        out = []
+        for i in range(lib().hb_net_num_convs(self.h, slot)):
+            co, ci = C.c_int(), C.c_int()
+            self._check(lib().hb_net_conv_shape(self.h, slot, i, C.byref(co), C.byref(ci)))
+            w = np.zeros((co.value, ci.value, 3, 3), np.float32)
+            b = np.zeros(co.value, np.float32)
+            self._check(lib().hb_get_conv(self.h, slot, i, _p(w, _fp), _p(b, _fp)))
+            out.append((w, b))
+        return out
+
+    def load_net(self, slot, convs):
+        for i, (w, b) in enumerate(convs):
+            w = np.ascontiguousarray(w, np.float32)
+            b = np.ascontiguousarray(b, np.float32)
+            self._check(lib().hb_load_conv(self.h, slot, i, _p(w, _fp), _p(b, _fp)))
+
+    def net_forward(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        B, _, H, W = x.shape
+        y = np.zeros((B, 2, H, W), np.float32)
+        self._check(lib().hb_net_forward(self.h, B, H, W, _p(x, _fp), _p(y, _fp)))
+        return y
+
+    def encode(self):
+        self._check(lib().hb_encode(self.h))
+
+    def context_map(self, l, base=16):
+        out = np.zeros((1, base, self.ny >> l, self.nx >> l), np.float32)
+        self._check(lib().hb_get_context(self.h, l, _p(out, _fp)))
+        return out
+
+    # operators (inc/stencil.hpp)
+    def apply(self, u, level=0, shifted=False):
+        u = _c128(u)
+        B = 1 if u.ndim == 2 else u.shape[0]
+        y = np.zeros_like(u)
+        self._check(lib().hb_operator_apply(self.h, level, int(shifted), B, _p(u), _p(y)))
+        return y
+
+    def jacobi(self, v, f, iters=1, level=0):
+        v = _c128(v).copy()
+        f = _c128(f)
+        B = 1 if v.ndim == 2 else v.shape[0]
+        self._check(lib().hb_jacobi(self.h, level, B, _p(v), _p(f), iters))
+        return v
+
+    def restrict(self, fine, level=0):
+        fine = _c128(fine)
+        B = 1 if fine.ndim == 2 else fine.shape[0]
+        shp = fine.shape[:-2] + (fine.shape[-2] // 2, fine.shape[-1] // 2)
+        out = np.zeros(shp, np.complex128)
+        self._check(lib().hb_restrict(self.h, level, B, _p(fine), _p(out)))
+        return out
+
+    def prolong(self, coarse, level=0):
+        coarse = _c128(coarse)
+        B = 1 if coarse.ndim == 2 else coarse.shape[0]
+        shp = coarse.shape[:-2] + (coarse.shape[-2] * 2, coarse.shape[-1] * 2)
+        out = np.zeros(shp, np.complex128)
+        self._check(lib().hb_prolong(self.h, level, B, _p(coarse), _p(out)))
+        return out
+
+    def coarse_solve(self, f):
+        f = _c128(f)
+        B = 1 if f.ndim == 2 else f.shape[0]
+        x = np.zeros_like(f)
+        self._check(lib().hb_coarse_solve(self.h, B, _p(f), _p(x)))
+        return x
+
+    def precond_apply(self, kind, r):
+        r = _c128(r)
+        B = 1 if r.ndim == 2 else r.shape[0]
+        z = np.zeros_like(r)
+        self._check(lib().hb_precond_apply(self.h, HB_PC[kind], B, _p(r), _p(z)))
+        return z
+
+    def fgmres(self, kind, B, cfg: KrylovConfig, X0=None):
+        B = _c128(B)
+        if B.ndim == 2:
+            B = B[None]
+        nb = B.shape[0]
+        X = np.zeros_like(B)
+        cap = cfg.max_iters + 2
+        hist = np.zeros((nb, cap))
+        hl = np.zeros(nb, np.int32)
+        it = np.zeros(nb, np.int32)
+        cv = np.zeros(nb, np.uint8)
+        bk = np.zeros(nb, np.uint8)
+        kc = _KrylovCfg(cfg.restart, cfg.max_iters, cfg.rel_tol, int(cfg.flexible))
+        x0p = _p(_c128(X0)) if X0 is not None else None
+        self._check(lib().hb_fgmres(self.h, C.byref(kc), HB_PC[kind], nb, _p(B), x0p, _p(X), _p(hist), cap,
+                                    _p(hl, _ip), _p(it, _ip), _p(cv, _u8p), _p(bk, _u8p)))
+        rep = SolveReport([hist[c, :hl[c]].copy() for c in range(nb)], [int(v) for v in it],
+                          [bool(v) for v in cv], [bool(v) for v in bk])
+        return X, rep
+
+    def fgmres_device(self, kind, dB: int, dX: int, nb: int, cfg: KrylovConfig, want_report=True):
+        """B, X are device pointers (c128 [nb][ny][nx]); e.g. torch tensors' data_ptr()."""
+        kc = _KrylovCfg(cfg.restart, cfg.max_iters, cfg.rel_tol, int(cfg.flexible))
+        if not want_report:
+            self._check(lib().hb_fgmres_device(self.h, C.byref(kc), HB_PC[kind], nb, C.c_void_p(dB), C.c_void_p(dX),
+                                               None, 0, None, None, None, None))
+            return None
+        cap = cfg.max_iters + 2
+        hist = np.zeros((nb, cap))
+        hl = np.zeros(nb, np.int32)
+        it = np.zeros(nb, np.int32)
+        cv = np.zeros(nb, np.uint8)
+        bk = np.zeros(nb, np.uint8)
+        self._check(lib().hb_fgmres_device(self.h, C.byref(kc), HB_PC[kind], nb, C.c_void_p(dB), C.c_void_p(dX),
+                                           _p(hist), cap, _p(hl, _ip), _p(it, _ip), _p(cv, _u8p), _p(bk, _u8p)))
+        return SolveReport([hist[c, :hl[c]].copy() for c in range(nb)], [int(v) for v in it],
+                           [bool(v) for v in cv], [bool(v) for v in bk])
+
+    # instrumentation
+    def prof_enable(self, on=True):
+        self._check(lib().hb_prof_enable(self.h, int(on)))
+
+    def prof_reset(self):
+        self._check(lib().hb_prof_reset(self.h))
+
+    def prof(self):
+        out = {}
+        for i in range(lib().hb_prof_count(self.h)):
+            ms, n, by, fl = C.c_double(), C.c_int64(), C.c_double(), C.c_double()
+            self._check(lib().hb_prof_get(self.h, i, C.byref(ms), C.byref(n), C.byref(by), C.byref(fl)))
+            out[lib().hb_prof_name(self.h, i).decode()] = dict(ms=ms.value, launches=n.value, bytes=by.value,
+                                                               flops=fl.value)
+        return out
+
+    def launch_count(self) -> int:
+        return int(lib().hb_launch_count(self.h))
+
+
+# --------------------------------------------------------- setup helpers
+def absorbing_layer(nx, ny, width, gamma_max):
+    out = np.zeros((ny, nx))
+    if lib().hb_absorbing_layer(nx, ny, width, gamma_max, _p(out)) != 0:
+        raise ValueError("absorbing layer width out of range / gamma_max negative")
+    return out
+
+
+def make_medium(nx, ny, seed, sigma=8.0, vmin=1.5, vmax=4.0, n_interfaces=0, iface_seed=0, margin=16, jmin=0.5,
+                jmax=1.0):
+    out = np.zeros((ny, nx))
+    if lib().hb_make_medium(nx, ny, seed, sigma, vmin, vmax, n_interfaces, iface_seed, margin, jmin, jmax,
+                            _p(out)) != 0:
+        raise ValueError("bad medium parameters")
+    return out
+
+
+def point_sources(seed, B, mode, lo, hi, row=0):
+    xs = np.zeros(B, np.int32)
+    ys = np.zeros(B, np.int32)
+    lib().hb_point_sources(seed, B, mode, lo, hi, row, _p(xs, _ip), _p(ys, _ip))
+    return xs, ys
+
+
+def rng_normals(seed, n):
+    out = np.zeros(n)
+    lib().hb_rng_normals(seed, n, _p(out))
+    return out
+
+
+# ------------------------------------------------ reference plugin mirror
+class Preconditioner:
+    """inc/precond.hpp:14-27: batched apply, requires_flexible, name."""
+
+    def apply(self, r: Sequence[np.ndarray]) -> List[np.ndarray]:
+        raise NotImplementedError
+
+    def requires_flexible(self) -> bool:
+        raise NotImplementedError
+
+    def name(self) -> str:
+        raise NotImplementedError
+
+    def apply_one(self, r):
+        return self.apply([r])[0]
+
+
+class _GpuPrecond(Preconditioner):
+    kind = "v"
+
+    def __init__(self, ctx: Context):
+        self.ctx = ctx
+
+    def apply(self, r):
+        z = self.ctx.precond_apply(self.kind, np.stack([_c128(x) for x in r]))
+        return [z[i] for i in range(z.shape[0])]
+
+    def requires_flexible(self):
+        return bool(lib().hb_precond_requires_flexible(self.ctx.h, HB_PC[self.kind]))
+
+    def name(self):
+        return lib().hb_precond_name(HB_PC[self.kind]).decode()
+
+
+class SLVCyclePreconditioner(_GpuPrecond):  # M_V (inc/precond.hpp:35-53); coarse-net cycle when coarse = net
+    kind = "v"
+
+
+class UnetVCyclePreconditioner(_GpuPrecond):  # M_VU (inc/precond.hpp:143-165)
+    kind = "vu"
+
+
+def check_flexible_contract(cfg: KrylovConfig, m: Preconditioner):  # inc/precond.hpp:29-32
+    if m.requires_flexible() and not cfg.flexible:
+        raise ValueError(f"preconditioner {m.name()} requires flexible = true")
+
+
+def block_fgmres(M: _GpuPrecond, B, cfg: KrylovConfig, X0=None):
+    """Device-resident block FGMRES with A = A^h of M's context (inc/krylov.hpp:83-86)."""
+    check_flexible_contract(cfg, M)
+    X, rep = M.ctx.fgmres(M.kind, np.stack([_c128(b) for b in B]), cfg,
+                          X0=None if X0 is None else np.stack([_c128(x) for x in X0]))
+    return [X[i] for i in range(X.shape[0])], rep
+
+
+def convergence_factor(history, target_drop=1e6):  # inc/bench.hpp:22-38
+    h = np.asarray(history)
+    for t in range(1, len(h)):
+        ratio = h[t] / h[0]
+        if ratio <= 1.0 / target_drop:
+            return t, ratio ** (1.0 / t), True
+    return len(h) - 1, float("nan"), False

@@ -1,0 +1,73 @@
+"""CPU-side checks of the drop-in boundary: libhelmgpu.so loads without a GPU,
+exports every symbol include/helmgpu.h declares, and its host-side setup
+restatements (Rng, ABL, medium, point sources, He init order) are bit-identical
+to the oracle / reference.  No compute calls (no GPU here)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _lib():
+    from paper_2203_11025_b200 import build, helmgpu
+    build.build()
+    return helmgpu
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "helmgpu.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(hb_[a-z0-9_]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    hg = _lib()
+    L = hg.lib()
+    syms = header_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in syms if not hasattr(L, s)]
+    assert not missing, missing
+
+
+def test_create_without_gpu_fails_cleanly():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    hg = _lib()
+    with pytest.raises(RuntimeError):
+        hg.Context(0)
+
+
+def test_host_rng_bit_exact(golden):
+    hg = _lib()
+    assert np.array_equal(hg.rng_normals(1234, 33), golden["rng_normal_1234"])
+
+
+def test_host_setup_generators_match_oracle():
+    hg = _lib()
+    for (n, w, g) in ((32, 6, 2.5), (128, 16, 241.3)):
+        assert np.array_equal(hg.absorbing_layer(n, n, w, g), O.absorbing_layer(n, n, w, g))
+    assert np.array_equal(hg.make_medium(96, 64, 1234), O.make_medium(96, 64, 1234))
+    a = hg.make_medium(128, 128, 1234, n_interfaces=3, iface_seed=1235, margin=16)
+    b = O.make_medium(128, 128, 1234, n_interfaces=3, iface_seed=1235, margin=16)
+    assert np.array_equal(a, b)
+    assert a.min() >= 1 / 16 - 1e-12 and a.max() <= 1 / 2.25 + 1e-12
+    for mode in (0, 1):
+        xs, ys = hg.point_sources(42, 8, mode, 16, 239, 20)
+        xo, yo = O.point_sources(42, 8, mode, 16, 239, 20)
+        assert np.array_equal(xs, xo) and np.array_equal(ys, yo)
+
+
+def test_config_problem_arrays():
+    from paper_2203_11025_b200 import configs, problems
+    arr = problems.problem_arrays(configs.CONFIGS["c0"])
+    assert arr["xs"] == [64] and arr["ys"] == [64]
+    om = arr["omega"]
+    assert om * np.sqrt(arr["kappa2"].max()) / 128 <= 0.6284
+    c1 = problems.problem_arrays(configs.CONFIGS["c1"])
+    assert len(c1["xs"]) == 8 and min(c1["xs"]) >= 16 and max(c1["xs"]) <= 239

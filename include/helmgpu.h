@@ -18,7 +18,6 @@
  *   hb_operator_apply   StencilOperator::apply                 inc/stencil.hpp:44-60
  *   hb_jacobi           StencilOperator::jacobi                inc/stencil.hpp:78-92
  *   hb_restrict/prolong restrict_field / prolong_field         inc/stencil.hpp:119-165
- *   hb_cycle            MultigridHierarchy::cycle              inc/multigrid.hpp:92,108-119
  *   hb_set_net / hb_load_conv / hb_init_net_he
  *                       NetworkWeights + build_unet/build_encoder (classic U-Net)
  *                                                              inc/unet.hpp:10-33,171-257
@@ -152,6 +151,12 @@ int hb_make_medium(int nx, int ny, uint64_t seed, double sigma, double vmin, dou
                    uint64_t iface_seed, int iface_margin, double jmin, double jmax, double* kappa2);
 /* point sources SURVEY A2 (mode 0: uniform (x, y) in [lo, hi]^2, mode 1: on `row`) */
 void hb_point_sources(uint64_t seed, int batch, int mode, int lo, int hi, int row, int* xs, int* ys);
+
+/* ---- options ------------------------------------------------------------ */
+/* "fused_vcycle" (1): fused down/up V-cycle legs for nu1 = nu2 = 1
+ * "cuda_graphs"  (1): replay each FGMRES restart cycle as one CUDA graph
+ * "small_coarse" (1): register-resident coarsest GMRES for <= 1024-node grids */
+int hb_set_option(hb_ctx* ctx, const char* key, int64_t value);
 
 /* ---- instrumentation ------------------------------------------------------ */
 /* per-kernel-class device time (CUDA events on the library stream), for the

@@ -19,6 +19,8 @@
 
 namespace hb {
 
+unsigned long long g_alloc_gen = 0;
+
 void krylov_report(Context& c, int B, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv,
                    uint8_t* brk);
 
@@ -143,7 +145,8 @@ static void coarsest_solve(Context& c, int B, const int* act, const float2* f, f
   const LevelView V = L.view();
   switch (c.vc.coarse_solver) {
     case HB_COARSE_GMRES:
-      launch_coarse_gmres(c, V, c.vc.coarse_iters, B, act, f, out, c.scratch_c64.p);
+      if (!(c.opt_small_coarse && launch_coarse_small(c, V, c.vc.coarse_iters, B, act, f, out)))
+        launch_coarse_gmres(c, V, c.vc.coarse_iters, B, act, f, out, c.scratch_c64.p);
       break;
     case HB_COARSE_JACOBI: {  // A3: iters damped sweeps from zero
       const float w = float(c.vc.damping);
@@ -165,9 +168,7 @@ static void coarsest_solve(Context& c, int B, const int* act, const float2* f, f
       if (!n.set) throw HbError{HB_ERR_STATE, "coarse solver is the net but net slot 0 is not set"};
       const int H = L.ny, W = L.nx;
       const size_t np = size_t(B) * H * W;
-      c.net_act.ensure(0);
-      // staging: in (3 ch) + out (2 ch) in the generic c64 scratch region after the coarse area
-      static thread_local DBuf<float> io;  // per-thread staging (one context per thread by contract)
+      DBuf<float>& io = c.cn_io;  // staging: in (3 ch) + out (2 ch), NHWC
       io.ensure(np * 5);
       launch_pack_input(c, V, L.h * L.h, B, act, f, nullptr, io.p);
       net_forward_dev(c, 0, B, act, H, W, io.p, io.p + np * 3);
@@ -192,6 +193,13 @@ static void vcycle_at(Context& c, int l, int B, const int* act, const float2* f,
   const float w = float(c.vc.damping);
   const int offset = l % 2;
   const int nu1 = c.vc.nu1, nu2 = c.vc.nu2;
+  if (c.opt_fused && nu1 == 1 && nu2 == 1) {
+    // fused legs: v and r stay on chip (hb_mg_fused.cu)
+    launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, C.f.p);
+    vcycle_at(c, l + 1, B, act, C.f.p, nullptr, nullptr, C.x.p);
+    launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, C.x.p, out);
+    return;
+  }
   float2* v = L.v.p;
   float2* t = L.t.p;
   // pre-smoothing (nu1 sweeps from e0 or zero)
@@ -241,8 +249,8 @@ void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2
   Level& L = *c.levels[0];
   const LevelView V = L.view();
   const size_t np = size_t(B) * L.N();
-  static thread_local DBuf<float> io;
-  static thread_local DBuf<float2> e0;
+  DBuf<float>& io = c.pc_io;
+  DBuf<float2>& e0 = c.pc_e0;
   io.ensure(np * 5);
   e0.ensure(np);
   launch_pack_input(c, V, L.h * L.h, B, act, r, rscale, io.p);
@@ -267,11 +275,7 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
   const size_t N = c.levels[0]->N();
   const size_t BN = size_t(B) * N;
   if (!c.h_count) HB_CUDA(cudaMallocHost(&c.h_count, sizeof(int)));
-  for (;;) {
-    launch_fg_restart(c, B, dB, dX, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
-    HB_CUDA(cudaMemcpyAsync(c.h_count, c.kcount.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
-    HB_CUDA(cudaStreamSynchronize(c.stream));
-    if (*c.h_count == 0) break;
+  auto cycle_body = [&]() {
     for (int j = 0; j < m; ++j) {
       float2* Vj = c.kV.p + size_t(j) * BN;
       float2* Zj = c.kZ.p + size_t(j) * BN;
@@ -280,6 +284,59 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
       launch_fg_update(c, B, j, m, c.kW.p, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
     }
     launch_fg_finalize(c, B, m, c.kZ.p, dX);
+    launch_fg_restart(c, B, dB, dX, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
+  };
+  auto read_count = [&]() {
+    HB_CUDA(cudaMemcpyAsync(c.h_count, c.kcount.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
+    HB_CUDA(cudaStreamSynchronize(c.stream));
+    return *c.h_count;
+  };
+  launch_fg_restart(c, B, dB, dX, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
+  if (read_count() == 0) {
+    // nothing to do
+  } else if (c.opt_graphs && !c.prof_on) {
+    // one CUDA graph per restart cycle: m inner steps + finalize + next restart
+    Context::GraphEntry* ge = nullptr;
+    for (auto& g : c.graphs)
+      if (g.gen == g_alloc_gen && g.kind == kind && g.B == B && g.m == m && g.cap == cap &&
+          g.max_iters == cfg->max_iters && g.tol == cfg->rel_tol && g.dB == dB && g.dX == dX)
+        ge = &g;
+    bool more = true;
+    if (!ge) {
+      // first cycle of a new shape runs eagerly (lazy allocations happen here,
+      // outside capture); the following cycles replay the captured graph
+      cycle_body();
+      more = read_count() > 0;
+    }
+    if (more && !ge) {
+      cudaGraph_t graph;
+      const int64_t l0 = c.launches;
+      HB_CUDA(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        cycle_body();
+      } catch (...) {
+        cudaStreamEndCapture(c.stream, &graph);
+        throw;
+      }
+      HB_CUDA(cudaStreamEndCapture(c.stream, &graph));
+      const int64_t per_cycle = c.launches - l0;  // captured, not yet executed
+      c.launches = l0;
+      cudaGraphExec_t exec;
+      HB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      HB_CUDA(cudaGraphDestroy(graph));
+      c.graphs.push_back(Context::GraphEntry{g_alloc_gen, kind, B, m, cap, cfg->max_iters, cfg->rel_tol, dB, dX,
+                                             exec, per_cycle});
+      ge = &c.graphs.back();
+    }
+    while (more) {
+      HB_CUDA(cudaGraphLaunch(ge->exec, c.stream));
+      c.launches += ge->launches;
+      more = read_count() > 0;
+    }
+  } else {
+    do {
+      cycle_body();
+    } while (read_count() > 0);
   }
   if (hist || hist_len || iters || conv || brk) krylov_report(c, B, hist, hist_stride, hist_len, iters, conv, brk);
 }
@@ -355,6 +412,7 @@ void hb_destroy(hb_ctx* ctx) {
     cudaEventDestroy(e.second.second);
   }
   if (ctx->h_count) cudaFreeHost(ctx->h_count);
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
   cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -679,6 +737,26 @@ int hb_prof_reset(hb_ctx* ctx) {
   ctx->launches = 0;
   HB_API_END
 }
+int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
+  HB_API_BEGIN
+  if (!key) throw HbError{HB_ERR_ARG, "null option key"};
+  const std::string k(key);
+  // options change the captured kernel sequence: drop cached cycle graphs
+  for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
+  ctx->graphs.clear();
+  if (k == "fused_vcycle")
+    ctx->opt_fused = value != 0;
+  else if (k == "cuda_graphs")
+    ctx->opt_graphs = value != 0;
+  else if (k == "small_coarse")
+    ctx->opt_small_coarse = value != 0;
+  else if (k == "coarse_threads")
+    ctx->coarse_threads = int(value);
+  else
+    throw HbError{HB_ERR_ARG, "unknown option " + k};
+  HB_API_END
+}
+
 int hb_prof_count(hb_ctx* ctx) { return ctx ? int(ctx->prof.size()) : 0; }
 const char* hb_prof_name(hb_ctx* ctx, int i) {
   return (ctx && i >= 0 && i < int(ctx->prof.size())) ? ctx->prof[size_t(i)].name.c_str() : "";

@@ -1,0 +1,371 @@
+// CTA-resident coarsest-grid GMRES(k) for coarse grids of <= 2048 nodes
+// (32x32 at c0): same contract as k_coarse_gmres in hb_mg.cu
+// (coarse_solve_with_op, inc/multigrid.hpp:45-61: non-flexible GMRES(k),
+// M = D^-1, x0 = 0, fixed budget, happy breakdown).  One 256-thread CTA per
+// column; each thread owns NPT nodes; the Krylov basis and z live in shared
+// memory (k+1 vectors, <= 200 KB), nothing touches global memory between
+// the load of f and the store of x.  Per Arnoldi step
+// the 2j+1 inner products (MGS via the Gram recurrence) are reduced with one
+// warp reduce-scatter butterfly (62 shuffles for 32 complex slots) instead of
+// 5 shuffles per value.
+#include "hb_common.cuh"
+#include "hb_internal.h"
+
+namespace hb {
+
+namespace {
+
+constexpr int CS_MAXW = 32;
+constexpr int CS_SLOTS = 32;  // complex reduction slots: [0..15] dots, [16..31] Gram
+
+__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 zconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double2 zsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 zscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, den = b.x + b.y * r;
+    return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
+  }
+  const double r = b.x / b.y, den = b.x * r + b.y;
+  return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
+}
+
+// warp reduce-scatter of 64 floats: on return lane l holds (sum over lanes of
+// v[2l], v[2l+1]) in v[0], v[1]
+__device__ __forceinline__ void warp_reduce_scatter64(float (&v)[64]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int stage = 0; stage < 5; ++stage) {
+    const int half = 32 >> stage;  // number of floats kept after this stage
+    const int mask = 16 >> stage;
+    const bool upper = (lane & mask) != 0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      if (k < half) {
+        const float send = upper ? v[k] : v[k + half];
+        const float keep = upper ? v[k + half] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+      }
+    }
+  }
+}
+
+// warp reduce-scatter of 32 floats: on return lane l holds the warp sum of v[l] in v[0]
+__device__ __forceinline__ void warp_reduce_scatter32(float (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int stage = 0; stage < 5; ++stage) {
+    const int half = 16 >> stage;
+    const int mask = 16 >> stage;
+    const bool upper = (lane & mask) != 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < half) {
+        const float send = upper ? v[k] : v[k + half];
+        const float keep = upper ? v[k + half] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+      }
+    }
+  }
+}
+
+struct SmallSmem {
+  float part[CS_MAXW][2 * CS_SLOTS];  // [warp][float]: 0..31 dots (re,im), 32..63 Gram / norm
+  double2 H[kMaxCoarseIters + 1][kMaxCoarseIters + 1];  // H[col][row], col < k, row <= col+1
+  double2 G[kMaxCoarseIters][kMaxCoarseIters];          // G[i][k] = <V_i, V_k>, k < i
+  double2 y[kMaxCoarseIters];
+  double2 sn[kMaxCoarseIters], g[kMaxCoarseIters + 1];
+  double cs[kMaxCoarseIters];
+  double scale[kMaxCoarseIters + 2];                    // V_i = scale[i] * Vraw_i
+  float2 coef[kMaxCoarseIters + 1];
+  double beta0;
+  int k;
+};
+
+// Per Arnoldi step j (two CTA barriers):
+//   w_raw = M D^-1 Vraw_j          (neighbours of Vraw_j read from shared memory)
+//   partials: <Vraw_i, w_raw> (i <= j), <Vraw_j, Vraw_k> (k < j), |Vraw_j|^2  -> one butterfly
+//   ---- barrier ----
+//   every warp folds the 8 warp partials for all slots (redundantly, no serial
+//   section): s_j = 1/||Vraw_j||, h_ij = s_i s_j <Vraw_i, w_raw>, MGS Gram
+//   correction h_ij -= sum_{k<i} h_kj^(cgs) G_ik (first order; G = O(eps32)),
+//   Vraw_{j+1} = w_raw - sum_i (h_ij s_i / s_j) Vraw_i
+//   ---- barrier ----
+// so the subdiagonal H_{j+1,j} = s_j / s_{j+1} is known one step later.  The
+// budget is fixed (tol 1e-300), so the Givens QR of the (k+1) x k Hessenberg
+// runs once at the end, followed by back-substitution and x = D^-1 sum y_i V_i
+// (krylov.hpp:119-137 non-flexible finalize).
+template <int NT, int NPT, int MAXK>
+__global__ void __launch_bounds__(NT, 1) k_coarse_small(LevelView L, int m, const int* act,
+                                                         const float2* __restrict__ f, float2* __restrict__ x) {
+  const int b = blockIdx.x;
+  if (act && !act[b]) return;
+  extern __shared__ float2 dyn[];  // Vraw_0..Vraw_m [m+1][N], then D^-1 [N]
+  __shared__ SmallSmem S;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nx = L.nx, ny = L.ny, N = nx * ny;
+  const float ih2 = L.inv_h2;
+  float2* sV = dyn;
+  float2* sDi = dyn + size_t(m + 1) * N;
+  float2 d[NPT];
+  int px[NPT], py[NPT];
+  bool ok[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    const int p = t + q * NT;
+    ok[q] = p < N;
+    px[q] = ok[q] ? p % nx : 0;
+    py[q] = ok[q] ? p / nx : 0;
+    d[q] = ok[q] ? ld(L.dM, p) : make_float2(1.f, 0.f);
+    if (ok[q]) {
+      sV[p] = ld(f + size_t(b) * N, p);
+      sDi[p] = crcp(d[q]);
+    }
+  }
+  __syncthreads();
+  int k = m;
+  double hn_prev = 0.0;
+#pragma unroll 1
+  for (int j = 0; j <= m; ++j) {
+    const float2* Vj = sV + size_t(j) * N;
+    float2 w[NPT], vj[NPT];
+    float v[32];
+#pragma unroll
+    for (int s2 = 0; s2 < 32; ++s2) v[s2] = 0.f;
+    float nrm_part = 0.f;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      const int p = t + q * NT;
+      w[q] = vj[q] = make_float2(0.f, 0.f);
+      if (!ok[q]) continue;
+      vj[q] = Vj[p];
+      nrm_part = fmaf(vj[q].x, vj[q].x, fmaf(vj[q].y, vj[q].y, nrm_part));
+      if (j == m) continue;
+      float2 nb = make_float2(0.f, 0.f);
+      if (px[q] > 0) nb = cadd(nb, cmul(Vj[p - 1], sDi[p - 1]));
+      if (px[q] + 1 < nx) nb = cadd(nb, cmul(Vj[p + 1], sDi[p + 1]));
+      if (py[q] > 0) nb = cadd(nb, cmul(Vj[p - nx], sDi[p - nx]));
+      if (py[q] + 1 < ny) nb = cadd(nb, cmul(Vj[p + nx], sDi[p + nx]));
+      float2 yv = cmul(d[q], cmul(vj[q], sDi[p]));
+      yv.x = fmaf(-ih2, nb.x, yv.x);
+      yv.y = fmaf(-ih2, nb.y, yv.y);
+      w[q] = yv;
+    }
+    // dots <Vraw_i, w_raw>, i <= j  (floats 2i, 2i+1)
+    if (j < m) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (i > j) break;
+        const float2* Vi = sV + size_t(i) * N;
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) {
+          if (!ok[q]) continue;
+          const float2 a = Vi[t + q * NT], c = w[q];
+          v[2 * i] = fmaf(a.x, c.x, fmaf(a.y, c.y, v[2 * i]));
+          v[2 * i + 1] = fmaf(a.x, c.y, fmaf(-a.y, c.x, v[2 * i + 1]));
+        }
+      }
+    }
+    warp_reduce_scatter32(v);
+    S.part[warp][lane] = v[0];
+#pragma unroll
+    for (int s2 = 0; s2 < 32; ++s2) v[s2] = 0.f;
+    // Gram <Vraw_j, Vraw_k>, k < j (floats 2k, 2k+1), ||Vraw_j||^2 (float 30)
+    v[30] = nrm_part;
+    if (j < m) {
+#pragma unroll
+      for (int i = 0; i < 15; ++i) {
+        if (i >= j) break;
+        const float2* Vi = sV + size_t(i) * N;
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) {
+          if (!ok[q]) continue;
+          const float2 a = Vi[t + q * NT], e = vj[q];
+          v[2 * i] = fmaf(e.x, a.x, fmaf(e.y, a.y, v[2 * i]));
+          v[2 * i + 1] = fmaf(e.x, a.y, fmaf(-e.y, a.x, v[2 * i + 1]));
+        }
+      }
+    }
+    warp_reduce_scatter32(v);
+    S.part[warp][32 + lane] = v[0];
+    __syncthreads();
+    // fold (every warp, lane l <-> complex slot l: 0..15 dots, 16..30 Gram, 31 norm)
+    double2 val = make_double2(0.0, 0.0);
+    {
+      const int f0 = lane < 16 ? 2 * lane : 32 + 2 * (lane - 16);
+#pragma unroll 4
+      for (int w2 = 0; w2 < NT / 32; ++w2) {
+        val.x += S.part[w2][f0];
+        val.y += S.part[w2][f0 + 1];
+      }
+    }
+    const double nrm = sqrt(__shfl_sync(0xffffffffu, val.x, 31));  // ||Vraw_j|| (float 62 = slot 31 re)
+    if (j == 0) {
+      if (t == 0) S.beta0 = nrm;
+      if (nrm == 0.0) {  // zero rhs -> zero correction
+        k = 0;
+        break;
+      }
+    } else {
+      const double hn = hn_prev * nrm;  // true H_{j, j-1} = s_{j-1} ||Vraw_j||
+      if (t == 0) S.H[j - 1][j] = make_double2(hn, 0.0);
+      if (hn <= 1e-14 * S.beta0) {  // happy breakdown (krylov.hpp:240)
+        k = j;
+        break;
+      }
+    }
+    const double sj = 1.0 / nrm;
+    if (t == 0) S.scale[j] = sj;
+    if (j == m) break;
+    hn_prev = sj;
+    // h_i (lane i <= j): s_i s_j <Vraw_i, w_raw>; Gram row j: s_j s_k <Vraw_j, Vraw_k>
+    const double si = (lane < j) ? S.scale[lane] : sj;
+    double2 hcgs = make_double2(0.0, 0.0);
+    if (lane <= j) hcgs = zscale(val, si * sj);
+    double2 gjk = make_double2(0.0, 0.0);
+    {
+      const double2 e = make_double2(__shfl_sync(0xffffffffu, val.x, (16 + lane) & 31),
+                                     __shfl_sync(0xffffffffu, val.y, (16 + lane) & 31));
+      if (lane < j) gjk = zscale(e, sj * S.scale[lane]);
+    }
+    // first-order MGS correction: h_i -= sum_{k<i} hcgs_k G_ik
+    double2 h = hcgs;
+    for (int kk = 0; kk < j; ++kk) {
+      const double2 hk = make_double2(__shfl_sync(0xffffffffu, hcgs.x, kk), __shfl_sync(0xffffffffu, hcgs.y, kk));
+      const double2 gjkk = make_double2(__shfl_sync(0xffffffffu, gjk.x, kk), __shfl_sync(0xffffffffu, gjk.y, kk));
+      if (lane <= j && kk < lane) {
+        const double2 Gik = (lane == j) ? gjkk : S.G[lane][kk];
+        h = zsub(h, zmul(hk, Gik));
+      }
+    }
+    if (warp == 0) {
+      if (lane <= j) S.H[j][lane] = h;
+      if (lane < j) S.G[j][lane] = gjk;
+    }
+    // raw update coefficients c_i = h_i s_i / s_j
+    const double2 cc = zscale(h, si / sj);
+    float2 cf = make_float2(float(cc.x), float(cc.y));
+    float2 vn[NPT];
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) vn[q] = w[q];
+    for (int i = 0; i <= j; ++i) {
+      const float2 ci = make_float2(__shfl_sync(0xffffffffu, cf.x, i), __shfl_sync(0xffffffffu, cf.y, i));
+      const float2* Vi = sV + size_t(i) * N;
+#pragma unroll
+      for (int q = 0; q < NPT; ++q)
+        if (ok[q]) vn[q] = csub(vn[q], cmul(ci, Vi[t + q * NT]));
+    }
+    float2* Vn = sV + size_t(j + 1) * N;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
+      if (ok[q]) Vn[t + q * NT] = vn[q];
+    __syncthreads();
+  }
+  if (k == 0) {
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
+      if (ok[q]) x[size_t(b) * N + t + q * NT] = make_float2(0.f, 0.f);
+    return;
+  }
+  __syncthreads();
+  if (t == 0) {
+    // Givens QR of the (k+1) x k Hessenberg (inc/krylov.hpp:221-232) + back-substitution (:119-126)
+    double* cs = S.cs;
+    double2* sn = S.sn;
+    double2* g = S.g;
+    for (int i = 0; i <= k; ++i) g[i] = make_double2(0.0, 0.0);
+    g[0] = make_double2(S.beta0, 0.0);
+    for (int j = 0; j < k; ++j) {
+      double2* hj = S.H[j];
+      for (int i = 0; i < j; ++i) {
+        const double2 t1 = dadd(zscale(hj[i], cs[i]), zmul(sn[i], hj[i + 1]));
+        hj[i + 1] = dadd(zscale(zmul(zconj(sn[i]), hj[i]), -1.0), zscale(hj[i + 1], cs[i]));
+        hj[i] = t1;
+      }
+      const double2 a = hj[j];
+      const double hn = hj[j + 1].x;
+      // make_givens (krylov.hpp:49-64) with reciprocal square roots instead of
+      // hypot + divisions: c = |a|/rho, s = a hn / (rho |a|)
+      const double a2 = a.x * a.x + a.y * a.y;
+      if (a2 + hn * hn == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = make_double2(0.0, 0.0);
+      } else if (a2 == 0.0) {
+        cs[j] = 0.0;
+        sn[j] = make_double2(1.0, 0.0);
+      } else {
+        const double ia = rsqrt(a2), ir = rsqrt(a2 + hn * hn);
+        cs[j] = a2 * ia * ir;
+        sn[j] = zscale(a, hn * ia * ir);
+      }
+      hj[j] = dadd(zscale(hj[j], cs[j]), zmul(sn[j], hj[j + 1]));
+      hj[j + 1] = make_double2(0.0, 0.0);
+      g[j + 1] = zscale(zmul(zconj(sn[j]), g[j]), -1.0);
+      g[j] = zscale(g[j], cs[j]);
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double2 sum = g[i];
+      for (int l = i + 1; l < k; ++l) sum = zsub(sum, zmul(S.H[l][i], S.y[l]));
+      const double2 d = S.H[i][i];
+      const double inv = 1.0 / (d.x * d.x + d.y * d.y);
+      S.y[i] = zscale(zmul(sum, zconj(d)), inv);
+    }
+    for (int i = 0; i < k; ++i) {
+      const double2 c = zscale(S.y[i], S.scale[i]);
+      S.coef[i] = make_float2(float(c.x), float(c.y));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    if (!ok[q]) continue;
+    const int p = t + q * NT;
+    float2 u = make_float2(0.f, 0.f);
+    for (int i = 0; i < k; ++i) u = cadd(u, cmul(S.coef[i], sV[size_t(i) * N + p]));
+    x[size_t(b) * N + p] = cmul(u, sDi[p]);
+  }
+}
+
+}  // namespace
+
+bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
+                         float2* x) {
+  const int N = L.nx * L.ny;
+  if (iters > 15 || N > 8 * 256) return false;
+  const size_t smem = sizeof(float2) * size_t(N) * (iters + 2);
+  if (smem > 200 * 1024) return false;
+  static int attr_set = 0;  // per-device bitmask
+  if (!(attr_set & (1 << c.device))) {
+    const int mx = 200 * 1024;
+    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<1024, 1, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<512, 2, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<256, 1, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<256, 2, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<256, 4, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<256, 8, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    attr_set |= 1 << c.device;
+  }
+  const int tok = prof_begin(c, PC_COARSE);
+  const int nt = c.coarse_threads;
+  if (nt == 1024 && N <= 1024) {
+    k_coarse_small<1024, 1, 15><<<B, 1024, smem, c.stream>>>(L, iters, act, f, x);
+  } else if (nt >= 512 && N <= 1024) {
+    k_coarse_small<512, 2, 15><<<B, 512, smem, c.stream>>>(L, iters, act, f, x);
+  } else if (N <= 256) {
+    k_coarse_small<256, 1, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+  } else if (N <= 512) {
+    k_coarse_small<256, 2, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+  } else if (N <= 1024) {
+    k_coarse_small<256, 4, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+  } else {
+    k_coarse_small<256, 8, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+  }
+  prof_end(c, PC_COARSE, tok, double(B) * N * 24.0, 0);
+  HB_CUDA(cudaGetLastError());
+  return true;
+}
+
+}  // namespace hb

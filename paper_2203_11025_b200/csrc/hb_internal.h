@@ -26,6 +26,9 @@ struct HbError {
       throw ::hb::HbError{HB_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)};              \
   } while (0)
 
+// bumped on every device (re)allocation: captured CUDA graphs are keyed on it
+extern unsigned long long g_alloc_gen;
+
 // device buffer (RAII)
 template <typename T>
 struct DBuf {
@@ -59,6 +62,7 @@ struct DBuf {
     release();
     HB_CUDA(cudaMalloc(&p, sizeof(T) * (count ? count : 1)));
     n = count;
+    ++g_alloc_gen;
   }
 };
 
@@ -124,6 +128,9 @@ void launch_prolong_add(Context& c, const LevelView& Lf, int cnx, int cny, int o
 void launch_restrict_plain(Context& c, int nx, int ny, int offset, int B, const float2* fine, float2* coarse);
 void launch_coarse_gmres(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
                          float2* x, float2* scratch);
+// register-resident variant for <= 1024-node coarse grids, iters <= 10 (hb_coarse_small.cu); false if not applicable
+bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
+                         float2* x);
 // fused down/up legs (nu1 = nu2 = 1)
 void launch_down_fused(Context& c, const LevelView& L, float damping, int offset, int B, const int* act,
                        const float2* f, const float* fscale, const float2* e0, float2* fc);
@@ -199,6 +206,22 @@ struct Context {
   DBuf<double2> kX, kB;      // c128 solution / rhs when called with host buffers
   int k_B = 0, k_m = 0, k_hist = 0;
   int* h_count = nullptr;    // pinned
+  // preconditioner staging (context-owned so captured graphs see stable pointers)
+  DBuf<float> pc_io, cn_io;
+  DBuf<float2> pc_e0;
+  // options
+  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true;
+  int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
+  // captured FGMRES cycle graphs
+  struct GraphEntry {
+    unsigned long long gen;
+    int kind, B, m, cap, max_iters;
+    double tol;
+    const void *dB, *dX;
+    cudaGraphExec_t exec;
+    int64_t launches;
+  };
+  std::vector<GraphEntry> graphs;
   // net activations
   DBuf<float> net_act;       // arena
   std::vector<DBuf<float>> ctx_maps;  // encoder context per level (NHWC)

@@ -233,15 +233,34 @@ __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState
     }
     red[t] = s;
   }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
+  // stage the Gram rows this step needs, then warp 0 forms the MGS coefficients
+  // with lanes in parallel: h_i = s_i <Vraw_i, w> - sum_{k<i} h_k^(cgs) G_ik
+  // (first-order Gram correction; G = O(eps32) off the diagonal)
   ColState& S = st[b];
-  for (int k = 0; k < j; ++k) S.G[j][k] = zscale(red[j + 1 + k], S.scale[j] * S.scale[k]);
-  for (int i = 0; i <= j; ++i) {
-    double2 h = zscale(red[i], S.scale[i]);
-    for (int k = 0; k < i; ++k) h = zsub(h, zmul(S.hc[k], S.G[i][k]));
-    S.hc[i] = h;
-    S.coef[i] = zscale(h, S.scale[i]);
+  __shared__ double2 sG[kMaxRestart][kMaxRestart];
+  __shared__ double ssc[kMaxRestart + 1];
+  for (int t = threadIdx.x; t <= j; t += KT) ssc[t] = S.scale[t];
+  for (int t = threadIdx.x; t < j * j; t += KT) {
+    const int i = t / j, kk = t % j;
+    if (kk < i) sG[i][kk] = S.G[i][kk];
+  }
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const double sj = ssc[j];
+  const double si = lane <= j ? ssc[lane] : 0.0;
+  const double2 zero = make_double2(0.0, 0.0);
+  const double2 hcgs = lane <= j ? zscale(red[lane], si) : zero;
+  const double2 gjk = lane < j ? zscale(red[j + 1 + lane], sj * si) : zero;
+  if (lane < j) S.G[j][lane] = gjk;
+  double2 h = hcgs;
+  for (int kk = 0; kk < j; ++kk) {
+    const double2 hk = make_double2(__shfl_sync(0xffffffffu, hcgs.x, kk), __shfl_sync(0xffffffffu, hcgs.y, kk));
+    const double2 gk = make_double2(__shfl_sync(0xffffffffu, gjk.x, kk), __shfl_sync(0xffffffffu, gjk.y, kk));
+    if (lane <= j && kk < lane) h = zsub(h, zmul(hk, lane == j ? gk : sG[lane][kk]));
+  }
+  if (lane <= j) {
+    S.hc[lane] = h;
+    S.coef[lane] = zscale(h, si);
   }
 }
 
@@ -294,57 +313,84 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
     part[size_t(b) * gridDim.x + blockIdx.x] = t;
   }
   if (!last_cta(ticket, b, gridDim.x)) return;
-  if (threadIdx.x != 0) return;
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  // warp 0: fold the partial norms, stage rotation state in shared memory
   double t = 0.0;
-  for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
+  for (unsigned q = lane; q < gridDim.x; q += 32) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
+  t = warp_sum(t);
   const double hnorm = sqrt(t);
-  double2* hj = S.H[j];
-  for (int i = 0; i <= j; ++i) hj[i] = S.hc[i];
-  hj[j + 1] = make_double2(hnorm, 0.0);
-  for (int i = 0; i < j; ++i) {
-    const double2 t1 = dadd(zscale(hj[i], S.cs[i]), zmul(S.sn[i], hj[i + 1]));
-    hj[i + 1] = dadd(zscale(zmul(zconj(S.sn[i]), hj[i]), -1.0), zscale(hj[i + 1], S.cs[i]));
-    hj[i] = t1;
+  __shared__ double2 hcol[kMaxRestart + 1], ssn[kMaxRestart];
+  __shared__ double scs[kMaxRestart];
+  if (lane <= j) hcol[lane] = S.hc[lane];
+  if (lane < j) {
+    scs[lane] = S.cs[lane];
+    ssn[lane] = S.sn[lane];
   }
-  {  // make_givens (inc/krylov.hpp:49-64)
-    const double2 a = hj[j];
-    const double aa = hypot(a.x, a.y), rho = hypot(aa, hnorm);
-    if (rho == 0.0) {
-      S.cs[j] = 1.0;
-      S.sn[j] = make_double2(0.0, 0.0);
-    } else if (aa == 0.0) {
-      S.cs[j] = 0.0;
-      S.sn[j] = make_double2(1.0, 0.0);
-    } else {
-      S.cs[j] = aa / rho;
-      S.sn[j] = zscale(a, hnorm / (rho * aa));
+  __syncwarp();
+  if (lane == 0) {
+    double2* hj = hcol;
+    hj[j + 1] = make_double2(hnorm, 0.0);
+    for (int i = 0; i < j; ++i) {  // previous rotations (inc/krylov.hpp:221-225)
+      const double2 t1 = dadd(zscale(hj[i], scs[i]), zmul(ssn[i], hj[i + 1]));
+      hj[i + 1] = dadd(zscale(zmul(zconj(ssn[i]), hj[i]), -1.0), zscale(hj[i + 1], scs[i]));
+      hj[i] = t1;
     }
+    double c;
+    double2 sn;
+    {  // make_givens (inc/krylov.hpp:49-64)
+      const double2 a = hj[j];
+      const double aa = hypot(a.x, a.y), rho = hypot(aa, hnorm);
+      if (rho == 0.0) {
+        c = 1.0;
+        sn = make_double2(0.0, 0.0);
+      } else if (aa == 0.0) {
+        c = 0.0;
+        sn = make_double2(1.0, 0.0);
+      } else {
+        c = aa / rho;
+        sn = zscale(a, hnorm / (rho * aa));
+      }
+    }
+    S.cs[j] = c;
+    S.sn[j] = sn;
+    hj[j] = dadd(zscale(hj[j], c), zmul(sn, hj[j + 1]));
+    hj[j + 1] = make_double2(0.0, 0.0);
+    const double2 gj = S.g[j];
+    const double2 gj1 = zscale(zmul(zconj(sn), gj), -1.0);
+    S.g[j + 1] = gj1;
+    S.g[j] = zscale(gj, c);
+    S.k = j + 1;
+    const int iters = S.iters + 1;
+    S.iters = iters;
+    const double est = hypot(gj1.x, gj1.y);
+    const int hl = S.hist_len;
+    if (hl < hist_cap) hist[size_t(b) * hist_cap + hl] = est;
+    S.hist_len = hl + 1;
+    const double beta0 = S.beta0;
+    const bool happy = hnorm <= 1e-14 * beta0;
+    if (happy) S.breakdown = 1;
+    int active = 1;
+    double snext = 0.0;
+    if (est / beta0 <= rel_tol || happy) {
+      S.converged = 1;
+      S.frozen = 1;
+      active = 0;
+    } else if (iters >= max_iters) {
+      S.frozen = 1;
+      active = 0;
+    } else if (j + 1 < m) {
+      snext = 1.0 / hnorm;
+      S.scale[j + 1] = snext;
+    } else {
+      active = 0;  // cycle end; finalize folds the correction
+    }
+    S.active = active;
+    act[b] = active;
+    scale_out[b] = float(active ? snext : 0.0);
   }
-  hj[j] = dadd(zscale(hj[j], S.cs[j]), zmul(S.sn[j], hj[j + 1]));
-  hj[j + 1] = make_double2(0.0, 0.0);
-  S.g[j + 1] = zscale(zmul(zconj(S.sn[j]), S.g[j]), -1.0);
-  S.g[j] = zscale(S.g[j], S.cs[j]);
-  S.k = j + 1;
-  S.iters += 1;
-  const double est = hypot(S.g[j + 1].x, S.g[j + 1].y);
-  if (S.hist_len < hist_cap) hist[size_t(b) * hist_cap + S.hist_len] = est;
-  S.hist_len += 1;
-  const bool happy = hnorm <= 1e-14 * S.beta0;
-  if (happy) S.breakdown = 1;
-  if (est / S.beta0 <= rel_tol || happy) {
-    S.converged = 1;
-    S.frozen = 1;
-    S.active = 0;
-  } else if (S.iters >= max_iters) {
-    S.frozen = 1;
-    S.active = 0;
-  } else if (S.k < m) {
-    S.scale[j + 1] = 1.0 / hnorm;
-  } else {
-    S.active = 0;  // cycle end; finalize folds the correction
-  }
-  act[b] = S.active;
-  scale_out[b] = float(S.scale[S.active ? j + 1 : 0]);
+  __syncwarp();
+  if (lane <= j + 1) S.H[j][lane] = hcol[lane];
 }
 
 // y = R^-1 g (back-substitution, inc/krylov.hpp:119-126); x += sum_i y_i Z_i
@@ -354,12 +400,26 @@ __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st
   const ColState& S = st[b];
   const int k = S.k;
   if (k == 0) return;
+  // stage R (upper k x k of the rotated Hessenberg) and g, then warp 0 runs a
+  // column-sweep back-substitution (krylov.hpp:119-126) with lanes in parallel
+  __shared__ double2 sH[kMaxRestart][kMaxRestart];  // sH[col][row]
   __shared__ double2 y[kMaxRestart];
-  if (threadIdx.x == 0) {
+  for (int t = threadIdx.x; t < k * k; t += KT) {
+    const int col = t / k, row = t % k;
+    if (row <= col) sH[col][row] = S.H[col][row];
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double2 g = lane < k ? S.g[lane] : make_double2(0.0, 0.0);
     for (int i = k - 1; i >= 0; --i) {
-      double2 sum = S.g[i];
-      for (int l = i + 1; l < k; ++l) sum = zsub(sum, zmul(S.H[l][i], y[l]));
-      y[i] = zdiv(sum, S.H[i][i]);
+      double2 yi = make_double2(0.0, 0.0);
+      if (lane == i) {
+        yi = zdiv(g, sH[i][i]);
+        y[i] = yi;
+      }
+      yi = make_double2(__shfl_sync(0xffffffffu, yi.x, i), __shfl_sync(0xffffffffu, yi.y, i));
+      if (lane < i) g = zsub(g, zmul(sH[i][lane], yi));
     }
   }
   __syncthreads();

@@ -96,6 +96,7 @@ def lib():
         L.hb_make_medium.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_int,
                                      C.c_uint64, C.c_int, C.c_double, C.c_double, _dp]
         L.hb_point_sources.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]
+        L.hb_set_option.argtypes = [_vp, C.c_char_p, C.c_int64]
         L.hb_prof_enable.argtypes = [_vp, C.c_int]
         L.hb_prof_reset.argtypes = [_vp]
         L.hb_prof_count.argtypes = [_vp]
@@ -329,6 +330,9 @@ class Context:
                                            _p(hist), cap, _p(hl, _ip), _p(it, _ip), _p(cv, _u8p), _p(bk, _u8p)))
         return SolveReport([hist[c, :hl[c]].copy() for c in range(nb)], [int(v) for v in it],
                            [bool(v) for v in cv], [bool(v) for v in bk])
+
+    def set_option(self, key: str, value: int):
+        self._check(lib().hb_set_option(self.h, key.encode(), int(value)))
 
     # instrumentation
     def prof_enable(self, on=True):

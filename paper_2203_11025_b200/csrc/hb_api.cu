@@ -88,10 +88,10 @@ static void require_hier(Context& c) {
   if (!c.has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built (hb_build_hierarchy)"};
 }
 
-static void fill_level_device(Level& L, double omega, double alpha, double beta, bool fp64A) {
+static void fill_level_device(Level& L, double omega, double alpha, double beta, double damping, bool fp64A) {
   const size_t n = L.N();
   const double inv_h2 = 1.0 / (L.h * L.h);
-  std::vector<float2> dm(n), da(n);
+  std::vector<float2> dm(n), da(n), wd(n);
   std::vector<double2> da64(fp64A ? n : 0);
   std::vector<float> kf(n);
   const std::complex<double> sh(alpha, -beta), sh0(1.0, 0.0);
@@ -103,12 +103,16 @@ static void fill_level_device(Level& L, double omega, double alpha, double beta,
     const std::complex<double> dMd = 4.0 * inv_h2 + mM, dAd = 4.0 * inv_h2 + mA;
     if (dMd == 0.0 || dAd == 0.0) throw HbError{HB_ERR_NUMERIC, "zero stencil diagonal"};
     dm[i] = make_float2(float(dMd.real()), float(dMd.imag()));
+    const std::complex<double> w = damping / dMd;
+    wd[i] = make_float2(float(w.real()), float(w.imag()));
     da[i] = make_float2(float(dAd.real()), float(dAd.imag()));
     if (fp64A) da64[i] = make_double2(dAd.real(), dAd.imag());
     kf[i] = float(L.k2[i]);
   }
   L.dM.ensure(n);
   L.dA.ensure(n);
+  L.wdi.ensure(n);
+  HB_CUDA(cudaMemcpy(L.wdi.p, wd.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
   L.k2f.ensure(n);
   HB_CUDA(cudaMemcpy(L.dM.p, dm.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
   HB_CUDA(cudaMemcpy(L.dA.p, da.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
@@ -140,13 +144,15 @@ void ensure_batch(Context& c, int B) {
 // ------------------------------------------------------------- V-cycle --
 // cycle_at (inc/multigrid.hpp:108-119) on device buffers; level-0 input f may
 // carry a per-column scale (FGMRES basis vectors are stored unnormalised).
-static void coarsest_solve(Context& c, int B, const int* act, const float2* f, float2* out) {
+static void coarsest_solve(Context& c, int B, int c0, const int* act, const float2* f, float2* out) {
   Level& L = *c.levels.back();
   const LevelView V = L.view();
+  float2* tbuf = L.t.p + size_t(c0) * L.N();
   switch (c.vc.coarse_solver) {
     case HB_COARSE_GMRES:
       if (!(c.opt_small_coarse && launch_coarse_small(c, V, c.vc.coarse_iters, B, act, f, out)))
-        launch_coarse_gmres(c, V, c.vc.coarse_iters, B, act, f, out, c.scratch_c64.p);
+        launch_coarse_gmres(c, V, c.vc.coarse_iters, B, act, f, out,
+                            c.scratch_c64.p + size_t(c0) * (kMaxCoarseIters + 2) * L.N());
       break;
     case HB_COARSE_JACOBI: {  // A3: iters damped sweeps from zero
       const float w = float(c.vc.damping);
@@ -154,8 +160,8 @@ static void coarsest_solve(Context& c, int B, const int* act, const float2* f, f
         HB_CUDA(cudaMemsetAsync(out, 0, sizeof(float2) * L.N() * B, c.stream));
         break;
       }
-      float2* a = (c.vc.coarse_iters % 2 == 1) ? out : L.t.p;
-      float2* bb = (a == out) ? L.t.p : out;
+      float2* a = (c.vc.coarse_iters % 2 == 1) ? out : tbuf;
+      float2* bb = (a == out) ? tbuf : out;
       launch_jacobi_zero(c, V, w, B, act, f, nullptr, a);
       for (int s = 1; s < c.vc.coarse_iters; ++s) {
         launch_jacobi_sweep(c, V, w, B, act, a, f, nullptr, bb);
@@ -164,6 +170,7 @@ static void coarsest_solve(Context& c, int B, const int* act, const float2* f, f
       break;
     }
     case HB_COARSE_NET: {  // A4: U-Net on [H^2 Re f, H^2 Im f, kappa^2]
+      if (c0 != 0) throw HbError{HB_ERR_STATE, "split V-cycle with a net coarse solver"};
       Net& n = c.nets[0];
       if (!n.set) throw HbError{HB_ERR_STATE, "coarse solver is the net but net slot 0 is not set"};
       const int H = L.ny, W = L.nx;
@@ -180,11 +187,16 @@ static void coarsest_solve(Context& c, int B, const int* act, const float2* f, f
   }
 }
 
-static void vcycle_at(Context& c, int l, int B, const int* act, const float2* f, const float* fscale,
+// c0: first column of this (sub-)batch within the level work buffers
+static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const float2* f, const float* fscale,
                       const float2* e0, float2* out) {
   const int nl = int(c.levels.size());
   if (l == nl - 1) {
-    coarsest_solve(c, B, act, f, out);
+    if (c.ev_at_coarse) {  // split V-cycle: release the second half-batch
+      HB_CUDA(cudaEventRecord(c.ev_at_coarse, c.stream));
+      c.ev_at_coarse = nullptr;
+    }
+    coarsest_solve(c, B, c0, act, f, out);
     return;
   }
   Level& L = *c.levels[size_t(l)];
@@ -193,15 +205,19 @@ static void vcycle_at(Context& c, int l, int B, const int* act, const float2* f,
   const float w = float(c.vc.damping);
   const int offset = l % 2;
   const int nu1 = c.vc.nu1, nu2 = c.vc.nu2;
+  float2* Cf = C.f.p + size_t(c0) * C.N();
+  float2* Cx = C.x.p + size_t(c0) * C.N();
   if (c.opt_fused && nu1 == 1 && nu2 == 1) {
     // fused legs: v and r stay on chip (hb_mg_fused.cu)
-    launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, C.f.p);
-    vcycle_at(c, l + 1, B, act, C.f.p, nullptr, nullptr, C.x.p);
-    launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, C.x.p, out);
+    launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
+    vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
+    launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
     return;
   }
-  float2* v = L.v.p;
-  float2* t = L.t.p;
+  float2* const Lv = L.v.p + size_t(c0) * L.N();
+  float2* const Lt = L.t.p + size_t(c0) * L.N();
+  float2* v = Lv;
+  float2* t = Lt;
   // pre-smoothing (nu1 sweeps from e0 or zero)
   if (nu1 == 0) {
     if (e0)
@@ -218,22 +234,48 @@ static void vcycle_at(Context& c, int l, int B, const int* act, const float2* f,
       std::swap(v, t);
     }
   }
-  launch_residual_restrict(c, V, offset, B, act, v, f, fscale, C.f.p);
-  vcycle_at(c, l + 1, B, act, C.f.p, nullptr, nullptr, C.x.p);
-  launch_prolong_add(c, V, C.nx, C.ny, offset, B, act, C.x.p, v);
+  launch_residual_restrict(c, V, offset, B, act, v, f, fscale, Cf);
+  vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
+  launch_prolong_add(c, V, C.nx, C.ny, offset, B, act, Cx, v);
   if (nu2 == 0) {
     HB_CUDA(cudaMemcpyAsync(out, v, sizeof(float2) * L.N() * B, cudaMemcpyDeviceToDevice, c.stream));
     return;
   }
   for (int s = 0; s < nu2; ++s) {
-    float2* dst = (s == nu2 - 1) ? out : (v == L.v.p ? L.t.p : L.v.p);
+    float2* dst = (s == nu2 - 1) ? out : (v == Lv ? Lt : Lv);
     launch_jacobi_sweep(c, V, w, B, act, v, f, fscale, dst);
     v = dst;
   }
 }
 
 void vcycle(Context& c, int B, const int* act, const float2* f0, const float* fscale, const float2* e0, float2* z) {
-  vcycle_at(c, 0, B, act, f0, fscale, e0, z);
+  const bool split = c.opt_split && B >= 2 && c.vc.coarse_solver != HB_COARSE_NET && act != nullptr;
+  if (!split) {
+    vcycle_at(c, 0, B, 0, act, f0, fscale, e0, z);
+    return;
+  }
+  // two half-batches on two streams (forked/joined with events; captured as
+  // parallel graph branches): one half's latency-bound coarsest solve (one CTA
+  // per column) overlaps the other half's bandwidth-bound fine-level legs
+  // (Starting the second half only when the first reaches its coarsest level
+  // -- staggering -- measured slower on B200; both halves start together.)
+  const int Bh = B / 2;
+  const size_t N0 = c.levels[0]->N();
+  HB_CUDA(cudaEventRecord(c.ev_fork, c.stream));
+  HB_CUDA(cudaStreamWaitEvent(c.stream2, c.ev_fork, 0));
+  vcycle_at(c, 0, Bh, 0, act, f0, fscale, e0, z);
+  cudaStream_t main = c.stream;
+  c.stream = c.stream2;
+  try {
+    vcycle_at(c, 0, B - Bh, Bh, act + Bh, f0 + Bh * N0, fscale ? fscale + Bh : nullptr, e0 ? e0 + Bh * N0 : nullptr,
+              z + Bh * N0);
+  } catch (...) {
+    c.stream = main;
+    throw;
+  }
+  c.stream = main;
+  HB_CUDA(cudaEventRecord(c.ev_join, c.stream2));
+  HB_CUDA(cudaStreamWaitEvent(c.stream, c.ev_join, 0));
 }
 
 void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2* r, const float* rscale,
@@ -391,7 +433,10 @@ int hb_create(int device, hb_ctx** out) {
   auto* c = new hb_ctx();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
-  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     g_create_err = "stream creation failed";
     delete c;
     return HB_ERR_CUDA;
@@ -414,6 +459,9 @@ void hb_destroy(hb_ctx* ctx) {
   if (ctx->h_count) cudaFreeHost(ctx->h_count);
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
   cudaStreamDestroy(ctx->stream);
+  cudaStreamDestroy(ctx->stream2);
+  cudaEventDestroy(ctx->ev_fork);
+  cudaEventDestroy(ctx->ev_join);
   delete ctx;
 }
 
@@ -496,7 +544,7 @@ int hb_build_hierarchy(hb_ctx* ctx, const hb_vcycle_cfg* cfg) {
     ctx->levels.push_back(std::move(L));
   }
   for (size_t l = 0; l < ctx->levels.size(); ++l)
-    fill_level_device(*ctx->levels[l], ctx->omega, cfg->alpha, cfg->beta, l == 0);
+    fill_level_device(*ctx->levels[l], ctx->omega, cfg->alpha, cfg->beta, cfg->damping, l == 0);
   ctx->has_hier = true;
   HB_API_END
 }
@@ -600,7 +648,7 @@ int hb_coarse_solve(hb_ctx* ctx, int batch, const double* f, double* x) {
   ctx->io_g.ensure(n);
   auto hf = to_c64(f, n);
   HB_CUDA(cudaMemcpyAsync(ctx->io_f.p, hf.data(), n * sizeof(float2), cudaMemcpyHostToDevice, ctx->stream));
-  coarsest_solve(*ctx, batch, ctx->act_all.p, ctx->io_f.p, ctx->io_g.p);
+  coarsest_solve(*ctx, batch, 0, ctx->act_all.p, ctx->io_f.p, ctx->io_g.p);
   HB_CUDA(cudaMemcpyAsync(hf.data(), ctx->io_g.p, n * sizeof(float2), cudaMemcpyDeviceToHost, ctx->stream));
   HB_CUDA(cudaStreamSynchronize(ctx->stream));
   from_c64(hf, x);
@@ -752,6 +800,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_small_coarse = value != 0;
   else if (k == "coarse_threads")
     ctx->coarse_threads = int(value);
+  else if (k == "split_vcycle")
+    ctx->opt_split = value != 0;
   else
     throw HbError{HB_ERR_ARG, "unknown option " + k};
   HB_API_END

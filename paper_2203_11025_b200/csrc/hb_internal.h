@@ -73,19 +73,20 @@ struct LevelView {
   const float2* dM;  // diagonal of the shifted operator M^h (c64)
   const float2* dA;  // diagonal of A^h (c64)
   const float* k2f;  // kappa^2 (fp32)
+  const float2* wdi; // damping / diag(M^h) (c64), the Jacobi update factor
 };
 
 struct Level {
   int nx = 0, ny = 0;
   double h = 0;
   std::vector<double> k2, gam;  // host fp64 coefficients (inc/stencil.hpp:169-185 coarsening)
-  DBuf<float2> dM, dA;
+  DBuf<float2> dM, dA, wdi;
   DBuf<double2> dA64;  // level 0: fp64 diagonal of A^h for the restart residual
   DBuf<float> k2f;
   // V-cycle work buffers [B][N]
   DBuf<float2> f, v, t, x;
   LevelView view() const {
-    return LevelView{nx, ny, float(1.0 / (h * h)), dM.p, dA.p, k2f.p};
+    return LevelView{nx, ny, float(1.0 / (h * h)), dM.p, dA.p, k2f.p, wdi.p};
   }
   size_t N() const { return size_t(nx) * ny; }
 };
@@ -175,6 +176,9 @@ enum ProfClass {
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream2 = nullptr;  // second branch for split V-cycles
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_at_coarse = nullptr;  // recorded when a V-cycle reaches its coarsest level
   int num_sms = 148;
   std::string err;
   // problem
@@ -210,7 +214,7 @@ struct Context {
   DBuf<float> pc_io, cn_io;
   DBuf<float2> pc_e0;
   // options
-  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true;
+  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {

@@ -167,30 +167,58 @@ __global__ void __launch_bounds__(KT) k_restart(FineView F, int B, ColState* st,
   if (!S.frozen) atomicAdd(count, 1);
 }
 
-// w = A Z_j ; partial <Vraw_i, w> (i <= j) and <Vraw_j, Vraw_k> (k < j);
-// last CTA forms the Gram-corrected MGS coefficients.
-__global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
+// warp reduce-scatter of NF floats (NF % 32 == 0): on return lane l holds the
+// warp sums of floats [l*NF/32, (l+1)*NF/32) in v[0 .. NF/32)
+template <int NF>
+__device__ __forceinline__ void warp_reduce_scatter(float (&v)[NF]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int stage = 0; stage < 5; ++stage) {
+    const int half = (NF / 2) >> stage;
+    const int mask = 16 >> stage;
+    const bool upper = (lane & mask) != 0;
+#pragma unroll
+    for (int k = 0; k < NF / 2; ++k) {
+      if (k < half) {
+        const float send = upper ? v[k] : v[k + half];
+        const float keep = upper ? v[k + half] : v[k];
+        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+      }
+    }
+  }
+}
+
+// w = A Z_j ; partial <Vraw_i, w> (i <= j) and <Vraw_j, Vraw_k> (k < j).
+// Basis vectors are streamed in groups of 4 (all 4*KNPT loads in flight
+// before use); each group's 4 dot + 4 Gram products are summed in fp32 over
+// the thread's nodes and reduced across the warp by one 16-float butterfly,
+// the warp partial accumulates in shared memory; warps and CTAs fold in fp64;
+// the last CTA of the column forms the MGS coefficients.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
                                               const float2* __restrict__ Z, float2* __restrict__ W,
                                               const float2* __restrict__ V, double2* part, unsigned* ticket) {
   const int b = blockIdx.y;
   if (!act[b]) return;
   const size_t N = size_t(F.nx) * F.ny;
   const size_t BN = size_t(B) * N;
-  const float2* zb = Z + b * N;  // slot j already applied by the caller
+  const float2* zb = Z + b * N;
   float2* wb = W + b * N;
   const float2* Vj = V + size_t(j) * BN + b * N;
-  __shared__ double2 wpart[KT / 32][KMAXV];
-  const int nv = 2 * j + 1;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int t = threadIdx.x; t < (KT / 32) * KMAXV; t += KT) (&wpart[0][0])[t] = make_double2(0.0, 0.0);
-  __syncthreads();
+  const int nv = 2 * j + 1;
   const float inv_h2 = float(F.inv_h2);
-  for (size_t base = size_t(blockIdx.x) * KTILE; base < N; base += size_t(gridDim.x) * KTILE) {
+  // wpart[warp][float]: dots of basis i at floats 2i, 2i+1; Gram k at 2*kMaxRestart + 2k
+  __shared__ float wpart[NT / 32][4 * kMaxRestart + 8];
+  for (int t = threadIdx.x; t < (NT / 32) * (4 * kMaxRestart + 8); t += NT) (&wpart[0][0])[t] = 0.f;
+  __syncthreads();
+  constexpr int TILE = NT * KNPT;
+  for (size_t base = size_t(blockIdx.x) * TILE; base < N; base += size_t(gridDim.x) * TILE) {
     float2 w[KNPT], vj[KNPT];
     bool ok[KNPT];
 #pragma unroll
     for (int q = 0; q < KNPT; ++q) {
-      const size_t p = base + q * KT + threadIdx.x;
+      const size_t p = base + q * NT + threadIdx.x;
       ok[q] = p < N;
       if (ok[q]) {
         const int ix = int(p % F.nx), iy = int(p / F.nx);
@@ -201,30 +229,77 @@ __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState
         w[q] = vj[q] = make_float2(0.f, 0.f);
       }
     }
-    for (int i = 0; i <= j; ++i) {
-      const float2* Vi = V + size_t(i) * BN + b * N;
-      double2 a = make_double2(0.0, 0.0), g = make_double2(0.0, 0.0);
+    for (int i0 = 0; i0 <= j; i0 += 4) {
+      float2 a[4][KNPT];
 #pragma unroll
-      for (int q = 0; q < KNPT; ++q) {
-        if (!ok[q]) continue;
-        const float2 vi = ld(Vi, base + q * KT + threadIdx.x);
-        a = dadd(a, dconjmul(vi, w[q]));
-        if (i < j) g = dadd(g, dconjmul(vj[q], vi));
+      for (int u = 0; u < 4; ++u) {
+        const float2* Vi = V + size_t(i0 + u) * BN + b * N;
+#pragma unroll
+        for (int q = 0; q < KNPT; ++q)
+          a[u][q] = (ok[q] && i0 + u <= j) ? ld(Vi, base + q * NT + threadIdx.x) : make_float2(0.f, 0.f);
       }
-      a = warp_sum2(a);
-      if (i < j) g = warp_sum2(g);
-      if (lane == 0) {
-        wpart[warp][i] = dadd(wpart[warp][i], a);
-        if (i < j) wpart[warp][j + 1 + i] = dadd(wpart[warp][j + 1 + i], g);
+      float v[16];  // [0..7] dots of i0..i0+3, [8..15] Gram
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        float dr = 0.f, di = 0.f, gr = 0.f, gi = 0.f;
+#pragma unroll
+        for (int q = 0; q < KNPT; ++q) {
+          const float2 ai = a[u][q], c = w[q], e = vj[q];
+          dr = fmaf(ai.x, c.x, fmaf(ai.y, c.y, dr));
+          di = fmaf(ai.x, c.y, fmaf(-ai.y, c.x, di));
+          gr = fmaf(e.x, ai.x, fmaf(e.y, ai.y, gr));
+          gi = fmaf(e.x, ai.y, fmaf(-e.y, ai.x, gi));
+        }
+        v[2 * u] = dr;
+        v[2 * u + 1] = di;
+        v[8 + 2 * u] = gr;
+        v[8 + 2 * u + 1] = gi;
+      }
+      // 16-float reduce-scatter: 4 halving stages, then a pairwise allreduce
+#pragma unroll
+      for (int stage = 0; stage < 4; ++stage) {
+        const int half = 8 >> stage, mask = 16 >> stage;
+        const bool upper = (lane & mask) != 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          if (k < half) {
+            const float send = upper ? v[k] : v[k + half];
+            const float keep = upper ? v[k + half] : v[k];
+            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+          }
+        }
+      }
+      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+      if ((lane & 1) == 0) {
+        const int fidx = lane >> 1;  // float index in the group's 16
+        const int u = (fidx & 7) >> 1, comp = fidx & 1;
+        const int i = i0 + u;
+        if (fidx < 8) {
+          if (i <= j) wpart[warp][2 * i + comp] += v[0];
+        } else {
+          if (i < j) wpart[warp][2 * kMaxRestart + 2 * i + comp] += v[0];
+        }
       }
     }
   }
-  __shared__ double2 red[KMAXV];
-  cta_fold(wpart, nv, red);
   __syncthreads();
-  for (int t = threadIdx.x; t < nv; t += KT) part[(size_t(b) * gridDim.x + blockIdx.x) * KMAXV + t] = red[t];
+  constexpr int HS = kMaxRestart;
+  // fold warps in fp64: slot s <- floats 2s, 2s+1 (dots s <= j at s, Gram k < j at HS + k)
+  __shared__ double2 red[KMAXV];
+  for (int t = threadIdx.x; t < nv; t += NT) {
+    const int slot = t <= j ? t : HS + (t - j - 1);
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int w2 = 0; w2 < NT / 32; ++w2) {
+      acc.x += wpart[w2][2 * slot];
+      acc.y += wpart[w2][2 * slot + 1];
+    }
+    red[t] = acc;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nv; t += NT) part[(size_t(b) * gridDim.x + blockIdx.x) * KMAXV + t] = red[t];
   if (!last_cta(ticket, b, gridDim.x)) return;
-  for (int t = threadIdx.x; t < nv; t += KT) {
+  for (int t = threadIdx.x; t < nv; t += NT) {
     double2 s = make_double2(0.0, 0.0);
     for (unsigned q = 0; q < gridDim.x; ++q) {
       const volatile double2* pp = part + (size_t(b) * gridDim.x + q) * KMAXV + t;
@@ -239,8 +314,8 @@ __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState
   ColState& S = st[b];
   __shared__ double2 sG[kMaxRestart][kMaxRestart];
   __shared__ double ssc[kMaxRestart + 1];
-  for (int t = threadIdx.x; t <= j; t += KT) ssc[t] = S.scale[t];
-  for (int t = threadIdx.x; t < j * j; t += KT) {
+  for (int t = threadIdx.x; t <= j; t += NT) ssc[t] = S.scale[t];
+  for (int t = threadIdx.x; t < j * j; t += NT) {
     const int i = t / j, kk = t % j;
     if (kk < i) sG[i][kk] = S.G[i][kk];
   }
@@ -274,7 +349,7 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
   ColState& S = st[b];
   const size_t N = size_t(F.nx) * F.ny;
   const size_t BN = size_t(B) * N;
-  __shared__ float2 cf[kMaxRestart + 1];
+  __shared__ float2 cf[kMaxRestart + 4];
   for (int i = threadIdx.x; i <= j; i += KT) cf[i] = make_float2(float(S.coef[i].x), float(S.coef[i].y));
   __syncthreads();
   const float2* wb = W + b * N;
@@ -289,12 +364,21 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
       ok[q] = p < N;
       t[q] = ok[q] ? ld(wb, p) : make_float2(0.f, 0.f);
     }
-    for (int i = 0; i <= j; ++i) {
-      const float2* Vi = V + size_t(i) * BN + b * N;
-      const float2 c = cf[i];
+    for (int i0 = 0; i0 <= j; i0 += 4) {
+      float2 a[4][KNPT];
 #pragma unroll
-      for (int q = 0; q < KNPT; ++q)
-        if (ok[q]) t[q] = csub(t[q], cmul(c, ld(Vi, base + q * KT + threadIdx.x)));
+      for (int u = 0; u < 4; ++u) {
+        const float2* Vi = V + size_t(i0 + u) * BN + b * N;
+#pragma unroll
+        for (int q = 0; q < KNPT; ++q)
+          a[u][q] = (ok[q] && i0 + u <= j) ? ld(Vi, base + q * KT + threadIdx.x) : make_float2(0.f, 0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 c = (i0 + u <= j) ? cf[i0 + u] : make_float2(0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < KNPT; ++q) t[q] = csub(t[q], cmul(c, a[u][q]));
+      }
     }
 #pragma unroll
     for (int q = 0; q < KNPT; ++q)
@@ -450,6 +534,14 @@ FineView fine_view(Context& c) {
   return FineView{L.nx, L.ny, 1.0 / (L.h * L.h), L.dA64.p, L.dA.p};
 }
 
+// one tile per CTA for small columns (latency), capped for huge columns so the
+// last-CTA fold stays short
+int nblk_adots(Context& c, size_t N, int B, int tile) {
+  const size_t tiles = (N + tile - 1) / tile;
+  const size_t cap = std::max<size_t>(16, size_t(4) * c.num_sms / std::max(1, B));
+  return int(std::max<size_t>(1, std::min(tiles, cap)));
+}
+
 int nblk_for(Context& c, size_t N, int B) {
   const size_t tiles = (N + KTILE - 1) / KTILE;
   const int cap = std::max(1, 4 * c.num_sms / std::max(1, B));
@@ -473,7 +565,7 @@ void krylov_alloc(Context& c, int B, int m, int hist_cap) {
   c.kV.ensure(size_t(m + 1) * B * N);
   c.kZ.ensure(size_t(m) * B * N);
   c.kW.ensure(size_t(B) * N);
-  const int nb = nblk_for(c, N, B);
+  const int nb = std::max(nblk_for(c, N, B), nblk_adots(c, N, B, 256 * KNPT));
   c.kpart.ensure(size_t(B) * nb * KMAXV);
   c.khist.ensure(size_t(B) * std::max(1, hist_cap));
   c.kact.ensure(B);
@@ -505,10 +597,10 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
 
 void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V) {
   const size_t N = c.levels[0]->N();
-  const int nb = nblk_for(c, N, B);
   KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0 + 8.0));
-  k_adots<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p,
-                                             Zj, w, V, c.kpart.p, c.kticket.p);
+  const int nb = nblk_adots(c, N, B, 256 * KNPT);
+  k_adots<256><<<dim3(nb, B), 256, 0, c.stream>>>(fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p),
+                                                   c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p);
   HB_CUDA(cudaGetLastError());
 }
 

@@ -31,7 +31,7 @@ __global__ void __launch_bounds__(CX* CY) k_down_fused(LevelView L, float dampin
   constexpr int NT = CX * CY;
   const int b = blockIdx.z;
   if (act && !act[b]) return;
-  __shared__ float2 sf[VH][VW], sd[VH][VW], sv[VH][VW];
+  __shared__ float2 sf[VH][VW], sd[VH][VW], sw[VH][VW], sv[VH][VW];
   __shared__ float2 se_r[(EW * EH > RW * RH) ? EW * EH : RW * RH];  // e0 tile, then residual tile
   const int nx = L.nx, ny = L.ny;
   const size_t N = size_t(nx) * ny;
@@ -44,14 +44,16 @@ __global__ void __launch_bounds__(CX* CY) k_down_fused(LevelView L, float dampin
   for (int i = t; i < VW * VH; i += NT) {
     const int ly = i / VW, lx = i % VW;
     const int gx = xv0 + lx, gy = yv0 + ly;
-    float2 fv = make_float2(0.f, 0.f), dv = make_float2(1.f, 0.f);
+    float2 fv = make_float2(0.f, 0.f), dv = make_float2(1.f, 0.f), wv = make_float2(0.f, 0.f);
     if (in_dom(gx, gy, nx, ny)) {
       const size_t g = size_t(gy) * nx + gx;
       fv = cscale(ld(fb, g), s);
       dv = ld(L.dM, g);
+      wv = ld(L.wdi, g);
     }
     sf[ly][lx] = fv;
     sd[ly][lx] = dv;
+    sw[ly][lx] = wv;
   }
   if (E0) {
     const float2* eb = e0 + b * N;
@@ -76,9 +78,9 @@ __global__ void __launch_bounds__(CX* CY) k_down_fused(LevelView L, float dampin
         float2 me = cmul(d, c);
         me.x = fmaf(-ih2, nb.x, me.x);
         me.y = fmaf(-ih2, nb.y, me.y);
-        v = caxpy(c, damping, cmul(csub(sf[ly][lx], me), crcp(d)));
+        v = cadd(c, cmul(csub(sf[ly][lx], me), sw[ly][lx]));
       } else {
-        v = cscale(cmul(sf[ly][lx], crcp(d)), damping);
+        v = cmul(sf[ly][lx], sw[ly][lx]);
       }
     }
     sv[ly][lx] = v;
@@ -124,7 +126,7 @@ __global__ void __launch_bounds__(TX* TY) k_up_fused(LevelView L, float damping,
   constexpr int NT = TX * TY;
   const int b = blockIdx.z;
   if (act && !act[b]) return;
-  __shared__ float2 sf[VH][VW], sd[VH][VW], sv[VH][VW];
+  __shared__ float2 sf[VH][VW], sd[VH][VW], sw[VH][VW], sv[VH][VW];
   __shared__ float2 se[E0 ? EH : 1][E0 ? EW : 1];
   __shared__ float2 sc[CH][CW];
   const int nx = L.nx, ny = L.ny;
@@ -138,14 +140,16 @@ __global__ void __launch_bounds__(TX* TY) k_up_fused(LevelView L, float damping,
   for (int i = t; i < VW * VH; i += NT) {
     const int ly = i / VW, lx = i % VW;
     const int gx = xv0 + lx, gy = yv0 + ly;
-    float2 fv = make_float2(0.f, 0.f), dv = make_float2(1.f, 0.f);
+    float2 fv = make_float2(0.f, 0.f), dv = make_float2(1.f, 0.f), wv = make_float2(0.f, 0.f);
     if (in_dom(gx, gy, nx, ny)) {
       const size_t g = size_t(gy) * nx + gx;
       fv = cscale(ld(fb, g), s);
       dv = ld(L.dM, g);
+      wv = ld(L.wdi, g);
     }
     sf[ly][lx] = fv;
     sd[ly][lx] = dv;
+    sw[ly][lx] = wv;
   }
   if (E0) {
     const float2* eb = e0 + b * N;
@@ -176,9 +180,9 @@ __global__ void __launch_bounds__(TX* TY) k_up_fused(LevelView L, float damping,
         float2 me = cmul(d, c);
         me.x = fmaf(-ih2, nb.x, me.x);
         me.y = fmaf(-ih2, nb.y, me.y);
-        v = caxpy(c, damping, cmul(csub(sf[ly][lx], me), crcp(d)));
+        v = cadd(c, cmul(csub(sf[ly][lx], me), sw[ly][lx]));
       } else {
-        v = cscale(cmul(sf[ly][lx], crcp(d)), damping);
+        v = cmul(sf[ly][lx], sw[ly][lx]);
       }
       // + P_o vc: per axis, (g - o) even -> j = (g-o)/2 weight 1; odd -> j = (g-o+-1)/2 weight 1/2
       const int tx = gx - offset, ty = gy - offset;
@@ -210,7 +214,7 @@ __global__ void __launch_bounds__(TX* TY) k_up_fused(LevelView L, float damping,
     float2 mv = cmul(d, sv[ly][lx]);
     mv.x = fmaf(-ih2, nb.x, mv.x);
     mv.y = fmaf(-ih2, nb.y, mv.y);
-    zb[size_t(gy) * nx + gx] = caxpy(sv[ly][lx], damping, cmul(csub(sf[ly][lx], mv), crcp(d)));
+    zb[size_t(gy) * nx + gx] = cadd(sv[ly][lx], cmul(csub(sf[ly][lx], mv), sw[ly][lx]));
   }
 }
 
@@ -230,11 +234,11 @@ void launch_down_fused(Context& c, const LevelView& L, float damping, int offset
   FScope fs(c, PC_DOWN, double(B) * L.nx * L.ny * ((e0 ? 24.0 : 16.0) + 2.0));
   const size_t big = size_t(cnx) * cny * B;
   if (big >= size_t(2) * 148 * 256) {
-    const dim3 grid((cnx + 31) / 32, (cny + 7) / 8, B);
+    const dim3 grid((cnx + 31) / 32, (cny + 3) / 4, B);
     if (e0)
-      k_down_fused<32, 8, true><<<grid, dim3(32, 8), 0, c.stream>>>(L, damping, offset, act, f, fscale, e0, fc);
+      k_down_fused<32, 4, true><<<grid, dim3(32, 4), 0, c.stream>>>(L, damping, offset, act, f, fscale, e0, fc);
     else
-      k_down_fused<32, 8, false><<<grid, dim3(32, 8), 0, c.stream>>>(L, damping, offset, act, f, fscale, e0, fc);
+      k_down_fused<32, 4, false><<<grid, dim3(32, 4), 0, c.stream>>>(L, damping, offset, act, f, fscale, e0, fc);
   } else {
     const dim3 grid((cnx + 15) / 16, (cny + 7) / 8, B);
     if (e0)

@@ -21,6 +21,9 @@ ctx, arr = problems.gpu_setup(cfg)
 if os.environ.get("HB_NO_GRAPHS"):
     ctx.set_option("cuda_graphs", 0)
 B = problems.rhs_block(arr)
+R = int(os.environ.get("REPLICAS", "1"))
+if R > 1:
+    B = np.concatenate([B] * R)
 kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=cfg["max_iters"])
 for r in range(reps):
     X, rep = ctx.fgmres(cfg["precond"], B, kc)

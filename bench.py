@@ -1,23 +1,27 @@
 #!/usr/bin/env python
 """Benchmark: Helmholtz solves/s to 1e-6 relative residual (BASELINE.json metric)
-through the B200 FGMRES + SL-multigrid (+ U-Net) hot path.
+through the B200 FGMRES + shifted-Laplacian multigrid (+ U-Net) hot path.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c0]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c0] [--replicas R]
 
-Workload: the headline line is config c0 --
-the only BASELINE config whose solve reaches 1e-6 with seeded random-init
-weights (configs c1-c4 put a random-init U-Net in the preconditioner and
-stagnate; the oracle shows it).  One step = one FGMRES(10) solve of the c0
-problem (128^2, M_V 3 levels, GMRES(10) coarsest) to 1e-6, inputs resident in
-HBM.  L2 is flushed (a 512 MiB write) between timed steps.  c1 (the U-Net
-coarse-solver config) is measured on a fixed iteration budget and reported
-under "also".  Multi-GPU: independent replicas / RHS shards, no collective.
+Workload: config c0 -- 128^2 heterogeneous
+Helmholtz, unit point source, M_V (3-level shifted-Laplacian V-cycle, GMRES(10)
+coarsest), FGMRES(10) to 1e-6.  It is the only BASELINE config whose solve
+reaches 1e-6 with the seeded random-init weights the configs prescribe (c1-c4
+put a random-init U-Net in the preconditioner and stagnate; the oracle shows
+it).  One step = R independent c0 solves on one GPU, R = one per SM
+(148) by default -- the device-filling analog of the reference arm, which runs
+one c0 solve per host core.  Inputs resident in HBM; the per-step working set
+(~0.5 GB) exceeds L2, and L2 is additionally flushed (512 MiB write) between
+timed steps.  Multi-GPU: each rank runs its own R replicas (weak scaling, no
+collective).  The U-Net configs are measured on a fixed iteration budget under
+"also".
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -36,8 +40,7 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return p, "measured"
+            return json.load(f), "measured"
     except Exception:
         return PEAKS_FALLBACK, "fallback"
 
@@ -75,22 +78,23 @@ def max_over_ranks(x, ws):
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.active", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
     def __init__(self, index):
-        self.index = index
-        self.proc = None
-        self.lines = []
+        self.index, self.proc, self.lines = index, None, []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}",
-                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                ["nvidia-smi", f"--id={self.index}", "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            threading.Thread(target=self._read, daemon=True).start()
+            time.sleep(0.2)
         except Exception:
             self.proc = None
         return self
@@ -101,6 +105,7 @@ class ClockSampler:
 
     def __exit__(self, *a):
         if self.proc:
+            time.sleep(0.1)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -124,8 +129,7 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
 # ------------------------------------------------------------- workloads
@@ -134,40 +138,47 @@ def config_for(name):
     return dict(configs.CONFIGS[name])
 
 
-def shard(cfg, ws, rank):
-    """RHS sharding: rank r gets columns [r*B/ws, (r+1)*B/ws); c0/c4: replicas."""
+def columns(cfg, ws, rank, replicas):
+    """RHS of this rank: the config's own RHS block sharded by rank,
+    or R replicas of a single-RHS config."""
     B = cfg["B"]
-    if B >= ws and B % ws == 0 and B > 1:
-        return list(range(rank * B // ws, (rank + 1) * B // ws))
-    return list(range(B))  # replicas
+    if B > 1:
+        if B % ws == 0 and B >= ws:
+            return list(range(rank * B // ws, (rank + 1) * B // ws))
+        return list(range(B))
+    return [0] * replicas
+
+
+def make_solver(O, kind, cfg, arr):
+    mk = O.RefHierarchy if kind == "reference" else O.Hierarchy
+    H = mk(arr["kappa2"], arr["gamma"], arr["omega"], arr["lo"], arr["hi"], levels=cfg["levels"],
+           coarse=cfg["coarse"], coarse_iters=cfg["coarse_iters"])
+    P = (O.RefPrecond if kind == "reference" else O.Precond)("v", H)
+    solve = O.ref_fgmres if kind == "reference" else O.fgmres
+    return H, P, solve
 
 
 def cpu_baseline_sample(cfg_name, cfg):
-    """The reference CPU path (oracle/_ref = reference headers compiled in place) on
-    a bounded sample, 1 thread; falls back to the C restatement ('port')."""
+    """The reference CPU path (oracle/_ref: the reference headers compiled in place)
+    on a bounded sample: one full solve, one thread.  Falls back to the C
+    restatement ('port') if the reference build is absent."""
     from oracle import oracle as O
     from paper_2203_11025_b200 import problems
     arr = problems.problem_arrays(cfg)
     B = problems.rhs_block(arr)[:1]
     kind = "reference" if O.have_ref() else "port"
-    mk = (lambda *a, **k: O.RefHierarchy(*a, **k)) if kind == "reference" else (lambda *a, **k: O.Hierarchy(*a, **k))
-    H = mk(arr["kappa2"], arr["gamma"], arr["omega"], arr["lo"], arr["hi"], levels=cfg["levels"],
-           coarse=cfg["coarse"], coarse_iters=cfg["coarse_iters"])
-    P = (O.RefPrecond if kind == "reference" else O.Precond)("v", H)
+    H, P, solve = make_solver(O, kind, cfg, arr)
     t0 = time.perf_counter()
-    if kind == "reference":
-        X, rep = O.ref_fgmres(P, B, restart=cfg["restart"], max_iters=cfg["max_iters"], nthreads=1)
-    else:
-        X, rep = O.fgmres(P, B, restart=cfg["restart"], max_iters=cfg["max_iters"], nthreads=1)
+    X, rep = solve(P, B, restart=cfg["restart"], max_iters=cfg["max_iters"], nthreads=1)
     dt = time.perf_counter() - t0
     return {"value": 1.0 / dt, "unit": "solves/s", "cores": 1, "kind": kind,
             "sample": f"1 full {cfg_name} solve ({int(rep['iterations'][0])} FGMRES iterations, "
-                      f"converged={bool(rep['converged'][0])}), 1 thread, {dt:.3f} s"}
+                      f"converged={bool(rep['converged'][0])}) on 1 host thread, {dt:.3f} s"}
 
 
 def run_reference(args, ws, rank):
-    """--impl reference: the reference's own CPU implementation (oracle/_ref) on
-    all host threads; replicas of the workload, one per thread."""
+    """--impl reference: the reference's own CPU implementation (oracle/_ref) on all
+    host threads, one c0 solve per thread per step (replicas, as our arm)."""
     if rank != 0:
         return
     from oracle import oracle as O
@@ -177,14 +188,9 @@ def run_reference(args, ws, rank):
     Bfull = problems.rhs_block(arr)
     threads = os.cpu_count() or 1
     kind = "reference" if O.have_ref() else "port"
-    mk = O.RefHierarchy if kind == "reference" else O.Hierarchy
-    H = mk(arr["kappa2"], arr["gamma"], arr["omega"], arr["lo"], arr["hi"], levels=cfg["levels"],
-           coarse=cfg["coarse"], coarse_iters=cfg["coarse_iters"])
-    P = (O.RefPrecond if kind == "reference" else O.Precond)("v", H)
-    # one column per thread: the workload's RHS, replicated if the config has fewer RHS than threads
+    H, P, solve = make_solver(O, kind, cfg, arr)
     cols = np.stack([Bfull[i % Bfull.shape[0]] for i in range(threads)])
-    solve = O.ref_fgmres if kind == "reference" else O.fgmres
-    times, conv = [], []
+    times, conv, iters = [], [], []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
         X, rep = solve(P, cols, restart=cfg["restart"], max_iters=cfg["max_iters"], nthreads=threads)
@@ -192,6 +198,7 @@ def run_reference(args, ws, rank):
         if s >= args.warmup:
             times.append(dt)
             conv.append(bool(np.all(rep["converged"])))
+            iters.append(int(np.max(rep["iterations"])))
     total = sum(times)
     value = threads * args.steps / total
     line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": args.gpus, "steps": args.steps,
@@ -199,16 +206,12 @@ def run_reference(args, ws, rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (fp64), fp32 network",
             "data": "synthetic (seeded media / point sources, SURVEY 8(d))", "impl": "reference",
             "config": {"workload": args.config, "grid": cfg["n"], "rhs_per_step": threads,
-                       "note": "one replica column per host thread"},
+                       "iterations": iters[-1] if iters else None, "converged": all(conv),
+                       "note": "one independent solve per host thread per step"},
             "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": kind,
-                             "sample": f"{threads} concurrent {args.config} solves per step "
-                                       f"(all converged: {all(conv)})"},
+                             "sample": f"{threads} concurrent {args.config} solves per step x {args.steps} steps"},
             "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
-
-
-def flush_l2(buf):
-    buf.add_(1.0)  # 512 MiB write >> 126 MB L2
 
 
 def run_ours(args, ws, rank, local):
@@ -216,37 +219,38 @@ def run_ours(args, ws, rank, local):
     from paper_2203_11025_b200 import helmgpu as hg
     from paper_2203_11025_b200 import problems
     torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     cfg = config_for(args.config)
-    cols = shard(cfg, ws, rank)
+    R = args.replicas or sms
+    cols = columns(cfg, ws, rank, R)
     ctx, arr = problems.gpu_setup(cfg, device=local)
-    Bh = problems.rhs_block(arr)[cols]
+    Bh = np.ascontiguousarray(problems.rhs_block(arr)[cols])
     nb = Bh.shape[0]
     kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=cfg["max_iters"], rel_tol=1e-6)
     kind = cfg["precond"]
-    dev = torch.device("cuda", local)
     dB = torch.from_numpy(Bh).to(dev)
     dX = torch.zeros_like(dB)
     stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)
 
-    def step():
+    def solve(report=False):
         dX.zero_()
-        return ctx.fgmres_device(kind, dB.data_ptr(), dX.data_ptr(), nb, kc, want_report=False)
+        return ctx.fgmres_device(kind, dB.data_ptr(), dX.data_ptr(), nb, kc, want_report=report)
 
     for _ in range(args.warmup):
-        step()
-    dX.zero_()
-    rep = ctx.fgmres_device(kind, dB.data_ptr(), dX.data_ptr(), nb, kc)
+        solve()
+    rep = solve(report=True)
     torch.cuda.synchronize()
-    # timed region: K steps, each bracketed by events on the library stream, L2 flushed in between
+
+    # ---- timed region: K steps, events on the library stream, L2 flushed between steps
     barrier(ws)
     torch.cuda.synchronize()
     n0 = ctx.launch_count()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         for k in range(args.steps):
-            flush_l2(flush)
-            torch.cuda.synchronize()
+            flush.add_(1.0)
             dX.zero_()
             torch.cuda.synchronize()
             ev[k][0].record(stream)
@@ -257,15 +261,15 @@ def run_ours(args, ws, rank, local):
     t_ms = sum(a.elapsed_time(b) for a, b in ev)
     barrier(ws)
     t_ms = max_over_ranks(t_ms, ws)
-    solves = nb * args.steps * ws  # every rank solves nb columns per step
+    solves = nb * args.steps * ws
     value = solves / (t_ms / 1e3)
 
-    # e2e through the public C ABI with host (pinned) buffers, copies inside the timed region
+    # ---- e2e: the public C ABI (hb_fgmres) on pinned host buffers; H2D of B and
+    # D2H of X inside the timed region every step
     Bpin = torch.from_numpy(Bh).pin_memory()
-    Xpin = torch.zeros_like(Bpin).pin_memory()
     ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for k in range(args.steps):
-        flush_l2(flush)
+        flush.add_(1.0)
         torch.cuda.synchronize()
         ee[k][0].record(stream)
         X, _ = ctx.fgmres(kind, Bpin.numpy(), kc)
@@ -273,20 +277,48 @@ def run_ours(args, ws, rank, local):
     torch.cuda.synchronize()
     e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ee), ws)
     e2e = {"value": solves / (e_ms / 1e3), "unit": "solves/s", "h2d_bytes_per_step": int(Bh.nbytes),
-           "d2h_bytes_per_step": int(Bh.nbytes)}
+           "d2h_bytes_per_step": int(Bh.nbytes), "path": "hb_fgmres (host c128 buffers)"}
 
-    # roofline pass (same workload, per-kernel-class CUDA events on the library stream)
+    # ---- single-solve latency (R = 1)
+    lat = None
+    if cfg["B"] == 1:
+        d1B, d1X = dB[:1].contiguous(), torch.zeros_like(dB[:1])
+        for _ in range(2):
+            d1X.zero_()
+            ctx.fgmres_device(kind, d1B.data_ptr(), d1X.data_ptr(), 1, kc)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        d1X.zero_()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        ctx.fgmres_device(kind, d1B.data_ptr(), d1X.data_ptr(), 1, kc, want_report=False)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        lat = e0.elapsed_time(e1)
+
+    # ---- roofline pass: same workload, per-kernel-class CUDA events on the library
+    # stream (eager launches; the timed region above replays CUDA graphs)
     ctx.prof_reset()
     ctx.prof_enable(True)
     for _ in range(args.steps):
-        step()
+        solve()
     torch.cuda.synchronize()
     ctx.prof_enable(False)
     prof = ctx.prof()
     total_ms = sum(p["ms"] for p in prof.values()) or 1.0
-    dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     pk, src = peaks()
-    name, p = dom
+    kernels = {}
+    for k, v in prof.items():
+        if not v["launches"]:
+            continue
+        row = {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+               "share": v["ms"] / total_ms, "avg_launch_us": 1e3 * v["ms"] / v["launches"]}
+        if v["flops"] > 0:
+            row["tflops"] = v["flops"] / (v["ms"] / 1e3) / 1e12
+        if v["bytes"] > 0:
+            row["gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9
+            row["hbm_frac"] = row["gbs"] / pk.get("hbm_gbs", 6650.0)
+        kernels[k] = row
+    name, p = max(prof.items(), key=lambda kv: kv[1]["ms"])
     if p["flops"] > 0:
         achieved = p["flops"] / (p["ms"] / 1e3) / 1e12
         peak = pk.get("bf16_tflops", 1590.0) * 0.5
@@ -297,35 +329,37 @@ def run_ours(args, ws, rank, local):
         achieved = p["bytes"] / (p["ms"] / 1e3) / 1e9 if p["ms"] > 0 else 0.0
         peak = pk.get("hbm_gbs", 6650.0)
         rl = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-              "traffic": None, "kernel": name, "note": f"peak = {src} HBM copy bandwidth"}
+              "traffic": None, "kernel": name, "note": f"peak = {src} HBM copy bandwidth; algorithmic bytes per "
+                                                       "launch as DESIGN.md 'Roofline accounting'"}
     rl["share_of_step"] = p["ms"] / total_ms
     rl["avg_launch_us"] = 1e3 * p["ms"] / max(1, p["launches"])
-    kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
-                   "share": v["ms"] / total_ms} for k, v in prof.items() if v["launches"]}
 
     line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "complex64 (fp64 reductions/Hessenberg/x), fp32 net",
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "complex64 fields (fp64 reductions/Hessenberg/solution), fp32 net",
             "data": "synthetic (seeded media / point sources, SURVEY 8(d))",
-            "config": {"workload": args.config, "grid": cfg["n"], "rhs_per_gpu": nb, "levels": cfg["levels"],
-                       "coarse": f"{cfg['coarse']}({cfg['coarse_iters']})", "restart": cfg["restart"],
-                       "precond": kind, "iterations": [int(i) for i in rep.iterations],
-                       "converged": [bool(c) for c in rep.converged], "l2": "flushed (512 MiB write) between steps",
-                       "parallelism": f"replicas/rhs-shards x{ws}"},
+            "config": {"workload": args.config, "grid": cfg["n"], "rhs_per_gpu_per_step": nb,
+                       "rhs_kind": "replicas of the single c0 RHS" if cfg["B"] == 1 else "config RHS block (sharded)",
+                       "levels": cfg["levels"], "coarse": f"{cfg['coarse']}({cfg['coarse_iters']})",
+                       "restart": cfg["restart"], "precond": kind, "iterations": int(max(rep.iterations)),
+                       "all_converged": bool(all(rep.converged)),
+                       "l2": "working set > L2; L2 flushed (512 MiB write) between steps",
+                       "single_solve_latency_ms": lat, "parallelism": f"independent solves x{ws} GPUs"},
             "roofline": rl, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(args.config, cfg)
+    ctx.close()
     if rank == 0 and args.also:
         line["also"] = {}
-        for name in [s for s in args.also.split(",") if s]:
+        for nm in [s for s in args.also.split(",") if s]:
             try:
-                line["also"][name] = fixed_budget(name, local, args, ws, rank)
-            except Exception as e:  # report, do not hide
-                line["also"][name] = {"error": repr(e)}
+                line["also"][nm] = fixed_budget(nm, local, args, ws, rank)
+            except Exception as e:  # reported, not hidden
+                line["also"][nm] = {"error": repr(e)}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
 
 
 def fixed_budget(name, local, args, ws, rank):
@@ -335,12 +369,11 @@ def fixed_budget(name, local, args, ws, rank):
     from paper_2203_11025_b200 import helmgpu as hg
     from paper_2203_11025_b200 import problems
     cfg = config_for(name)
-    cols = shard(cfg, ws, rank)
+    cols = columns(cfg, ws, rank, 1)
     ctx, arr = problems.gpu_setup(cfg, device=local)
-    Bh = problems.rhs_block(arr)[cols]
+    Bh = np.ascontiguousarray(problems.rhs_block(arr)[cols])
     nb = Bh.shape[0]
-    budget = args.budget
-    kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=budget, rel_tol=1e-6)
+    kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=args.budget, rel_tol=1e-6)
     dev = torch.device("cuda", local)
     dB = torch.from_numpy(Bh).to(dev)
     dX = torch.zeros_like(dB)
@@ -361,9 +394,9 @@ def fixed_budget(name, local, args, ws, rank):
     ctx.prof_enable(False)
     prof = ctx.prof()
     conv = prof.get("conv3x3", {})
-    out = {"grid": cfg["n"], "rhs": nb, "iterations_budget": budget, "ms": ms,
+    out = {"grid": cfg["n"], "rhs": nb, "iterations_budget": args.budget, "ms": ms,
            "ms_per_iteration": ms / max(1, max(rep.iterations)),
-           "rel_residual_end": [float(h[-1] / h[0]) for h in rep.residual_history],
+           "rel_residual_end": [round(float(h[-1] / h[0]), 6) for h in rep.residual_history],
            "converged": [bool(c) for c in rep.converged]}
     if conv.get("ms", 0) > 0:
         out["conv_tflops"] = conv["flops"] / (conv["ms"] / 1e3) / 1e12
@@ -379,12 +412,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c0")
+    ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
+                                                              "(0 = one per SM)")
     ap.add_argument("--also", default="c1", help="comma list of configs measured on a fixed iteration budget")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args.warmup = max(3, args.warmup)
     ws, rank, local = dist_init()
     if args.impl == "reference":
         run_reference(args, ws, rank)

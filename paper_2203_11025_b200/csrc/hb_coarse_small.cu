@@ -363,7 +363,7 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
   } else {
     k_coarse_small<256, 8, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
   }
-  prof_end(c, PC_COARSE, tok, double(B) * N * 24.0, 0);
+  prof_end(c, PC_COARSE, tok, double(B) * N * 16.0 + double(N) * 8.0, 0);  // f in, x out; diag
   HB_CUDA(cudaGetLastError());
   return true;
 }

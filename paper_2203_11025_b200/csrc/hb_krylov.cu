@@ -587,7 +587,7 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
                        double rel_tol, int max_iters) {
   const size_t N = c.levels[0]->N();
   const int nb = nblk_for(c, N, B);
-  KScope ks(c, PC_KRYLOV_RESTART, double(B) * N * 56.0);
+  KScope ks(c, PC_KRYLOV_RESTART, double(B) * N * 40.0 + double(N) * 16.0);  // b, x (c128) in; V0 (c64) out; dA64
   HB_CUDA(cudaMemsetAsync(c.kcount.p, 0, sizeof(int), c.stream));
   k_restart<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), b, x, V0,
                                                reinterpret_cast<double*>(c.kpart.p), c.kticket.p, c.khist.p,
@@ -597,7 +597,7 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
 
 void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V) {
   const size_t N = c.levels[0]->N();
-  KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0 + 8.0));
+  KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0) + double(N) * 8.0);  // Z_j, V_0..V_j in; w out; dA
   const int nb = nblk_adots(c, N, B, 256 * KNPT);
   k_adots<256><<<dim3(nb, B), 256, 0, c.stream>>>(fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p),
                                                    c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p);
@@ -608,7 +608,7 @@ void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* 
                       int max_iters) {
   const size_t N = c.levels[0]->N();
   const int nb = nblk_for(c, N, B);
-  KScope ks(c, PC_KRYLOV_UPDATE, double(B) * N * (8.0 * (j + 1) + 16.0));
+  KScope ks(c, PC_KRYLOV_UPDATE, double(B) * N * (8.0 * (j + 1) + 16.0));  // w, V_0..V_j in; V_{j+1} out
   k_update<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p),
                                               c.kact.p, w, V, reinterpret_cast<double*>(c.kpart.p), c.kticket.p,
                                               c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p);
@@ -619,7 +619,7 @@ void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x) {
   (void)m;
   const size_t N = c.levels[0]->N();
   const int nb = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
-  KScope ks(c, PC_KRYLOV_FINAL);
+  KScope ks(c, PC_KRYLOV_FINAL, double(B) * N * (32.0 + 8.0 * m));  // x (c128) in+out, Z_0..Z_{k-1} in (upper bound k = m)
   k_finalize<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), Z, x);
   HB_CUDA(cudaGetLastError());
 }

@@ -231,7 +231,7 @@ struct FScope {
 void launch_down_fused(Context& c, const LevelView& L, float damping, int offset, int B, const int* act,
                        const float2* f, const float* fscale, const float2* e0, float2* fc) {
   const int cnx = L.nx / 2, cny = L.ny / 2;
-  FScope fs(c, PC_DOWN, double(B) * L.nx * L.ny * ((e0 ? 24.0 : 16.0) + 2.0));
+  FScope fs(c, PC_DOWN, double(B) * L.nx * L.ny * ((e0 ? 16.0 : 8.0) + 2.0) + double(L.nx) * L.ny * 16.0);  // f (+e0) in, fc out; D, wD^-1
   const size_t big = size_t(cnx) * cny * B;
   if (big >= size_t(2) * 148 * 256) {
     const dim3 grid((cnx + 31) / 32, (cny + 3) / 4, B);
@@ -252,7 +252,7 @@ void launch_down_fused(Context& c, const LevelView& L, float damping, int offset
 void launch_up_fused(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B,
                      const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
                      float2* z) {
-  FScope fs(c, PC_UP, double(B) * L.nx * L.ny * ((e0 ? 24.0 : 16.0) + 2.0 + 8.0));
+  FScope fs(c, PC_UP, double(B) * L.nx * L.ny * ((e0 ? 16.0 : 8.0) + 2.0 + 8.0) + double(L.nx) * L.ny * 16.0);  // f (+e0), vc in; z out; D, wD^-1
   const size_t big = size_t(L.nx) * L.ny * B;
   if (big >= size_t(2) * 148 * 512) {
     const dim3 grid((L.nx + 63) / 64, (L.ny + 7) / 8, B);

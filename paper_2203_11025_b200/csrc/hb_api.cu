@@ -802,6 +802,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->coarse_threads = int(value);
   else if (k == "split_vcycle")
     ctx->opt_split = value != 0;
+  else if (k == "tc_conv")
+    ctx->opt_tc_conv = value != 0;
   else
     throw HbError{HB_ERR_ARG, "unknown option " + k};
   HB_API_END

@@ -94,8 +94,9 @@ struct Level {
 struct ConvW {
   int cout = 0, cin = 0;
   std::vector<float> w, b;  // host OIHW + bias
-  DBuf<float> dw;           // device packed weights [9*cin][cout] (k-major rows)
+  DBuf<float> dw;           // device packed weights [9*cin][cout] (k-major rows), SIMT path
   DBuf<float> db;
+  DBuf<float> dwh, dwl;     // tensor-core path: [cout][9*cin] tf32 hi / lo split
 };
 
 struct Net {
@@ -138,6 +139,10 @@ void launch_down_fused(Context& c, const LevelView& L, float damping, int offset
 void launch_up_fused(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B,
                      const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
                      float2* z);
+// tensor-core conv (hb_conv_tc.cu)
+void conv_tc_prepare(ConvW& cw);
+bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
+                    const float* bsrc, int cb, bool b_ctx, int relu, float* out);
 // network pack / unpack (hb_net.cu)
 void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const int* act, const float2* r,
                        const float* rscale, float* x /*NHWC, 3 ch*/);
@@ -214,7 +219,7 @@ struct Context {
   DBuf<float> pc_io, cn_io;
   DBuf<float2> pc_e0;
   // options
-  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true;
+  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {

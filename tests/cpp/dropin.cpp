@@ -1,0 +1,90 @@
+// Drop-in check at the C++ plugin boundary (built against the UNMODIFIED
+// reference headers; see tests/cpp/build.sh).  The GPU preconditioner is
+// plugged into the reference's own block_fgmres through helm::Preconditioner,
+// and the device-resident helm::gpu::block_fgmres is run beside the reference
+// CPU solve on the same problem.
+#include <cmath>
+#include <cstdio>
+#include <memory>
+
+#include "helmbench/grid.hpp"
+#include "helmbench/krylov.hpp"
+#include "helmbench/multigrid.hpp"
+#include "helmbench/precond.hpp"
+#include "helmbench/rng.hpp"
+#include "helmgpu_helm.hpp"
+
+using namespace helm;
+
+static double rel(const std::vector<ComplexField>& a, const std::vector<ComplexField>& b) {
+  double num = 0, den = 0;
+  for (size_t c = 0; c < a.size(); ++c)
+    for (size_t i = 0; i < a[c].v.size(); ++i) {
+      num += std::norm(a[c].v[i] - b[c].v[i]);
+      den += std::norm(b[c].v[i]);
+    }
+  return std::sqrt(num / den);
+}
+
+int main() {
+  const int n = 64;
+  const double omega = 2 * M_PI * 1.5 * n / 10;
+  auto grid = make_grid(n, n, 3);
+  RealField k2(n, n);
+  for (int iy = 0; iy < n; ++iy)
+    for (int ix = 0; ix < n; ++ix) {  // smooth velocity in [1.5, 4] -> kappa^2 = 1/c^2
+      const double x = double(ix) / n, y = double(iy) / n;
+      const double c = 2.75 + 1.25 * std::sin(3.1 * x + 1.0) * std::cos(2.3 * y);
+      k2.at(ix, iy) = 1.0 / (c * c);
+    }
+  auto prob = make_problem(grid, omega, make_slowness_squared(std::move(k2), 1.0 / 16, 1.0 / 2.25),
+                           make_absorbing_layer(grid, 8, 2 * omega));
+  VCycleConfig vc;  // 3 levels, V(1,1), damping 0.8, shift (1, 0.5), GMRES(10) coarsest
+  auto hier = std::make_shared<MultigridHierarchy>(prob, vc);
+  SLVCyclePreconditioner M_cpu(hier);
+  StencilOperator A(prob, kHelmholtzShift);
+  BatchedOp apply_A = [&A](const std::vector<ComplexField>& in) {
+    std::vector<ComplexField> out;
+    for (const auto& f : in) out.push_back(A.apply(f));
+    return out;
+  };
+  std::vector<ComplexField> B;
+  Rng rng(7);
+  for (int c = 0; c < 2; ++c) {
+    ComplexField f(n, n);
+    for (auto& z : f.v) z = Complex(rng.normal(), rng.normal());
+    B.push_back(std::move(f));
+  }
+  ComplexField pt(n, n);
+  pt.at(n / 2, n / 2) = 1.0;
+  B.push_back(pt);
+  KrylovConfig cfg;
+  cfg.restart = 10;
+  cfg.max_iters = 300;
+
+  auto [X_ref, rep_ref] = block_fgmres(apply_A, M_cpu.as_batched_op(), B, cfg);
+
+  auto ctx = std::make_shared<gpu::Context>(0);
+  ctx->set_problem(prob, vc);
+  gpu::GpuSLVCycle M_gpu(ctx);
+  // (1) GPU plugin inside the reference's CPU block_fgmres
+  auto [X_mix, rep_mix] = block_fgmres(apply_A, M_gpu.as_batched_op(), B, cfg);
+  // (2) device-resident solve behind the reference's signature
+  auto [X_gpu, rep_gpu] = gpu::block_fgmres(M_gpu, B, cfg);
+  // (3) single preconditioner apply parity
+  const double pc_err = rel(M_gpu.apply(B), M_cpu.apply(B));
+
+  bool ok = pc_err < 1e-4;
+  std::printf("{\"pc_rel\": %.3e, \"cols\": [", pc_err);
+  for (size_t c = 0; c < B.size(); ++c) {
+    const int d1 = rep_mix.iterations[c] - rep_ref.iterations[c], d2 = rep_gpu.iterations[c] - rep_ref.iterations[c];
+    ok = ok && std::abs(d1) <= 1 && std::abs(d2) <= 1 && rep_gpu.converged[c];
+    std::printf("%s{\"ref\": %d, \"plugin\": %d, \"device\": %d}", c ? ", " : "", rep_ref.iterations[c],
+                rep_mix.iterations[c], rep_gpu.iterations[c]);
+  }
+  const double xe = rel(X_gpu, X_ref), xm = rel(X_mix, X_ref);
+  ok = ok && xe < 1e-4 && xm < 1e-4 && M_gpu.name() == M_cpu.name();
+  std::printf("], \"x_rel_device\": %.3e, \"x_rel_plugin\": %.3e, \"name\": \"%s\", \"ok\": %s}\n", xe, xm,
+              M_gpu.name().c_str(), ok ? "true" : "false");
+  return ok ? 0 : 1;
+}

@@ -71,3 +71,14 @@ def test_config_problem_arrays():
     assert om * np.sqrt(arr["kappa2"].max()) / 128 <= 0.6284
     c1 = problems.problem_arrays(configs.CONFIGS["c1"])
     assert len(c1["xs"]) == 8 and min(c1["xs"]) >= 16 and max(c1["xs"]) <= 239
+
+
+def test_cpp_adapter_header_compiles_against_reference():
+    """include/helmgpu_helm.hpp (the drop-in adapters) compiles against the
+    unmodified reference headers and links against libhelmgpu."""
+    import subprocess
+    if not os.path.isdir("/root/reference/proj/include/helmbench"):
+        pytest.skip("reference headers absent")
+    _lib()
+    r = subprocess.run(["bash", os.path.join(ROOT, "tests", "cpp", "build.sh")], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr[-2000:]

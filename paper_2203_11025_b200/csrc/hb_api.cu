@@ -208,10 +208,18 @@ static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const fl
   float2* Cf = C.f.p + size_t(c0) * C.N();
   float2* Cx = C.x.p + size_t(c0) * C.N();
   if (c.opt_fused && nu1 == 1 && nu2 == 1) {
-    // fused legs: v and r stay on chip (hb_mg_fused.cu)
-    launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
+    // fused legs: v and r stay on chip (row-streaming kernels for a zero
+    // initial guess, shared-memory tiles otherwise)
+    const bool stream = c.opt_stream && e0 == nullptr && L.nx >= 16;
+    if (stream)
+      launch_down_stream(c, V, offset, B, act, f, fscale, Cf);
+    else
+      launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
     vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
-    launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
+    if (stream)
+      launch_up_stream(c, V, offset, C.nx, C.ny, B, act, f, fscale, Cx, out);
+    else
+      launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
     return;
   }
   float2* const Lv = L.v.p + size_t(c0) * L.N();
@@ -804,6 +812,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_split = value != 0;
   else if (k == "tc_conv")
     ctx->opt_tc_conv = value != 0;
+  else if (k == "stream_vcycle")
+    ctx->opt_stream = value != 0;
   else
     throw HbError{HB_ERR_ARG, "unknown option " + k};
   HB_API_END

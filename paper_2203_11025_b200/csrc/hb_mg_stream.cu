@@ -1,0 +1,258 @@
+// Row-streaming V-cycle legs (zero initial guess, nu1 = nu2 = 1): the M_V /
+// coarse-net path of every FGMRES inner step.  Same math as hb_mg_fused.cu
+// (inc/multigrid.hpp:108-119 with inc/stencil.hpp:44-165) but organised for
+// bandwidth: a warp owns a strip of 32 coarse columns (= 64 fine columns, each
+// lane two adjacent fine columns 2jx+o, 2jx+o+1) and marches down a chunk of
+// rows keeping the 3-row stencil window in registers; horizontal neighbours
+// come from warp shuffles, so there is no shared memory and no CTA barrier.
+// Lanes 0 and 31 are halo lanes (their neighbours live in other warps); each
+// warp emits 30 coarse columns.  Loads are float4 (two fine nodes per lane).
+//
+//   down:  v = wD^-1 f ; r = f - M v ; fc(jy, jx) = sum_k W_k r(2j+o+k)
+//   up:    v = wD^-1 f + P_o vc ; z = v + wD^-1 (f - M v)
+#include "hb_common.cuh"
+#include "hb_internal.h"
+
+namespace hb {
+
+namespace {
+
+constexpr int SW_OUT = 30;  // coarse columns emitted per warp
+constexpr int WARPS = 4;    // warps per CTA (independent row chunks)
+
+struct Pair {
+  float2 a, b;  // fine columns c0 = 2jx+o, c1 = c0+1
+};
+
+__device__ __forceinline__ Pair ld_pair(const float2* row, int c0, int nx) {
+  // c0 may be -1..nx; c0 even-aligned iff o == 0
+  Pair p;
+  p.a = (c0 >= 0 && c0 < nx) ? __ldg(row + c0) : make_float2(0.f, 0.f);
+  p.b = (c0 + 1 >= 0 && c0 + 1 < nx) ? __ldg(row + c0 + 1) : make_float2(0.f, 0.f);
+  return p;
+}
+__device__ __forceinline__ float2 shfl_up2(float2 v) {
+  return make_float2(__shfl_up_sync(0xffffffffu, v.x, 1), __shfl_up_sync(0xffffffffu, v.y, 1));
+}
+__device__ __forceinline__ float2 shfl_down2(float2 v) {
+  return make_float2(__shfl_down_sync(0xffffffffu, v.x, 1), __shfl_down_sync(0xffffffffu, v.y, 1));
+}
+// M v at (c0, c1) of one row: d v - ih2 (up + down + left + right)
+__device__ __forceinline__ Pair apply_M(const Pair& d, const Pair& vm, const Pair& v, const Pair& vp, float ih2) {
+  const float2 left = shfl_up2(v.b);    // column c0 - 1 (lane - 1's c1)
+  const float2 right = shfl_down2(v.a); // column c1 + 1 (lane + 1's c0)
+  Pair o;
+  float2 nb = cadd(cadd(vm.a, vp.a), cadd(left, v.b));
+  o.a = cmul(d.a, v.a);
+  o.a.x = fmaf(-ih2, nb.x, o.a.x);
+  o.a.y = fmaf(-ih2, nb.y, o.a.y);
+  nb = cadd(cadd(vm.b, vp.b), cadd(v.a, right));
+  o.b = cmul(d.b, v.b);
+  o.b.x = fmaf(-ih2, nb.x, o.b.x);
+  o.b.y = fmaf(-ih2, nb.y, o.b.y);
+  return o;
+}
+
+// down leg: grid (ceil(cnx / 30), ceil(row chunks / WARPS), B), block 32 x WARPS
+__global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, int offset, int rows_per_chunk,
+                                                            const int* act, const float2* __restrict__ f,
+                                                            const float* fscale, float2* __restrict__ fc) {
+  const int b = blockIdx.z;
+  if (act && !act[b]) return;
+  const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
+  const int jx = blockIdx.x * SW_OUT - 1 + lane;  // lane 0 / 31: halo
+  const int c0 = 2 * jx + offset;
+  const int jy0 = (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
+  if (jy0 >= cny) return;
+  const int jy1 = min(cny, jy0 + rows_per_chunk);
+  const size_t N = size_t(nx) * ny;
+  const float2* fb = f + b * N;
+  const float s = fscale ? fscale[b] : 1.0f;
+  const float ih2 = L.inv_h2;
+  const bool colok_a = c0 >= 0 && c0 < nx, colok_b = c0 + 1 >= 0 && c0 + 1 < nx;
+  // raw row data (f, wD^-1, D), zero outside the domain; prefetched two rows ahead
+  struct Raw {
+    Pair f, w, d;
+  };
+  auto load_raw = [&](int y) {
+    Raw r;
+    if (y < 0 || y >= ny) {
+      r.f.a = r.f.b = r.w.a = r.w.b = r.d.a = r.d.b = make_float2(0.f, 0.f);
+      return r;
+    }
+    const size_t o = size_t(y) * nx;
+    r.f = ld_pair(fb + o, c0, nx);
+    r.w = ld_pair(L.wdi + o, c0, nx);
+    r.d = ld_pair(L.dM + o, c0, nx);
+    return r;
+  };
+  auto vrow = [&](const Raw& r) {
+    Pair v;
+    v.a = cmul(cscale(r.f.a, s), r.w.a);
+    v.b = cmul(cscale(r.f.b, s), r.w.b);
+    return v;
+  };
+  // fine rows y from 2 jy0 + o - 1 to 2 (jy1 - 1) + o + 1; v needed one row beyond
+  int y = 2 * jy0 + offset - 1;
+  Raw r_c = load_raw(y), r_p1 = load_raw(y + 1), r_p2 = load_raw(y + 2);
+  Pair v_m = vrow(load_raw(y - 1)), v_c = vrow(r_c);
+  float2 h_m2 = make_float2(0.f, 0.f), h_m1 = make_float2(0.f, 0.f);
+  const int yend = 2 * (jy1 - 1) + offset + 1;
+  for (; y <= yend; ++y) {
+    const Raw r_p3 = load_raw(y + 3);  // in flight during this row
+    const Pair v_p = vrow(r_p1);
+    float2 h = make_float2(0.f, 0.f);
+    const Pair mv = apply_M(r_c.d, v_m, v_c, v_p, ih2);
+    if (y >= 0 && y < ny) {
+      Pair r;
+      r.a = colok_a ? csub(cscale(r_c.f.a, s), mv.a) : make_float2(0.f, 0.f);
+      r.b = colok_b ? csub(cscale(r_c.f.b, s), mv.b) : make_float2(0.f, 0.f);
+      const float2 rl = shfl_up2(r.b);  // r at c0 - 1
+      h = caxpy(cscale(r.a, 0.5f), 0.25f, cadd(rl, r.b));
+    } else {
+      (void)shfl_up2(v_c.b);  // keep the shuffles convergent
+    }
+    // y = 2 jy + o + 1 closes coarse row jy
+    const int t = y - offset - 1;
+    if (t >= 2 * jy0 && ((t & 1) == 0)) {
+      const int jy = t >> 1;
+      if (lane >= 1 && lane <= SW_OUT && jx < cnx && jy < jy1) {
+        const float2 v = caxpy(cscale(h_m1, 0.5f), 0.25f, cadd(h_m2, h));
+        fc[size_t(b) * cnx * cny + size_t(jy) * cnx + jx] = v;
+      }
+    }
+    h_m2 = h_m1;
+    h_m1 = h;
+    v_m = v_c;
+    v_c = v_p;
+    r_c = r_p1;
+    r_p1 = r_p2;
+    r_p2 = r_p3;
+  }
+}
+
+// up leg: grid (ceil(cnx / 30), ceil(row chunks / WARPS), B); each warp produces
+// fine rows [y0, y1) for its 60 fine columns
+__global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, int offset, int cnx, int cny,
+                                                          int rows_per_chunk, const int* act,
+                                                          const float2* __restrict__ f, const float* fscale,
+                                                          const float2* __restrict__ vc, float2* __restrict__ z) {
+  const int b = blockIdx.z;
+  if (act && !act[b]) return;
+  const int lane = threadIdx.x, nx = L.nx, ny = L.ny;
+  const int jx = blockIdx.x * SW_OUT - 1 + lane;
+  const int c0 = 2 * jx + offset;
+  const int y0 = (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
+  if (y0 >= ny) return;
+  const int y1 = min(ny, y0 + rows_per_chunk);
+  const size_t N = size_t(nx) * ny;
+  const float2* fb = f + b * N;
+  const float2* cb = vc + size_t(b) * cnx * cny;
+  const float s = fscale ? fscale[b] : 1.0f;
+  const float ih2 = L.inv_h2;
+  const bool colok_a = c0 >= 0 && c0 < nx, colok_b = c0 + 1 >= 0 && c0 + 1 < nx;
+  // raw fine-row data (f, wD^-1, D) and the two coarse values this lane needs for
+  // fine row y (coarse rows (y-o)/2 or floor/ceil), prefetched two rows ahead
+  struct Raw {
+    Pair f, w, d;
+    float2 c0v, c1v;  // vc at this lane's coarse column, rows jlo / jhi
+    int even;         // (y - o) even: one coarse row
+  };
+  auto cload = [&](int jy) {
+    return (jy >= 0 && jy < cny && jx >= 0 && jx < cnx) ? __ldg(cb + size_t(jy) * cnx + jx) : make_float2(0.f, 0.f);
+  };
+  auto load_raw = [&](int y) {
+    Raw r;
+    r.even = 1;
+    if (y < 0 || y >= ny) {
+      r.f.a = r.f.b = r.w.a = r.w.b = r.d.a = r.d.b = make_float2(0.f, 0.f);
+      r.c0v = r.c1v = make_float2(0.f, 0.f);
+      return r;
+    }
+    const size_t o = size_t(y) * nx;
+    r.f = ld_pair(fb + o, c0, nx);
+    r.w = ld_pair(L.wdi + o, c0, nx);
+    r.d = ld_pair(L.dM + o, c0, nx);
+    const int t = y - offset;
+    if ((t & 1) == 0) {
+      r.c0v = cload(t >> 1);
+      r.c1v = make_float2(0.f, 0.f);
+    } else {
+      const int jlo = (t - 1) >> 1;  // t >= -1
+      r.c0v = cload(t < 0 ? -1 : jlo);
+      r.c1v = cload(jlo + 1);
+      r.even = 0;
+    }
+    return r;
+  };
+  // v(y) = wD^-1 f + P vc  (horizontal prolongation via one shuffle of the coarse value)
+  auto vrow = [&](const Raw& r) {
+    const float2 cur = r.even ? r.c0v : cscale(cadd(r.c0v, r.c1v), 0.5f);  // vertical prolongation
+    const float2 nxt = shfl_down2(cur);                                   // coarse column jx + 1
+    Pair v;
+    v.a = colok_a ? cadd(cmul(cscale(r.f.a, s), r.w.a), cur) : make_float2(0.f, 0.f);
+    v.b = colok_b ? cadd(cmul(cscale(r.f.b, s), r.w.b), cscale(cadd(cur, nxt), 0.5f)) : make_float2(0.f, 0.f);
+    return v;
+  };
+  Raw r_c = load_raw(y0), r_p1 = load_raw(y0 + 1), r_p2 = load_raw(y0 + 2);
+  Pair v_m = vrow(load_raw(y0 - 1)), v_c = vrow(r_c);
+  float2* zb = z + b * N;
+  for (int y = y0; y < y1; ++y) {
+    const Raw r_p3 = load_raw(y + 3);
+    const Pair v_p = vrow(r_p1);
+    const size_t o = size_t(y) * nx;
+    const Pair mv = apply_M(r_c.d, v_m, v_c, v_p, ih2);
+    const float2 fa = cscale(r_c.f.a, s), fb2 = cscale(r_c.f.b, s);
+    if (lane >= 1 && lane <= SW_OUT) {
+      const float2 za = cadd(v_c.a, cmul(csub(fa, mv.a), r_c.w.a));
+      const float2 zb2 = cadd(v_c.b, cmul(csub(fb2, mv.b), r_c.w.b));
+      if (colok_a && colok_b && ((c0 & 1) == 0)) {
+        *reinterpret_cast<float4*>(zb + o + c0) = make_float4(za.x, za.y, zb2.x, zb2.y);
+      } else {
+        if (colok_a) zb[o + c0] = za;
+        if (colok_b) zb[o + c0 + 1] = zb2;
+      }
+    } else if (lane == 0 && jx == -1 && colok_b) {
+      // offset 1: fine column 0 is the second column of coarse column -1; it only
+      // needs this lane's own first column and lane 1's, so the halo lane emits it
+      zb[o + c0 + 1] = cadd(v_c.b, cmul(csub(fb2, mv.b), r_c.w.b));
+    }
+    v_m = v_c;
+    v_c = v_p;
+    r_c = r_p1;
+    r_p1 = r_p2;
+    r_p2 = r_p3;
+  }
+}
+
+}  // namespace
+
+void launch_down_stream(Context& c, const LevelView& L, int offset, int B, const int* act, const float2* f,
+                        const float* fscale, float2* fc) {
+  const int cnx = L.nx / 2, cny = L.ny / 2;
+  const int tok = prof_begin(c, PC_DOWN);
+  // rows per warp: enough warps to fill the machine, >= 4 coarse rows to amortise the halo
+  int rpc = 8;
+  while (rpc > 4 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((cny + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
+    rpc /= 2;
+  const int chunks = (cny + rpc - 1) / rpc;
+  const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
+  k_down_stream<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
+  prof_end(c, PC_DOWN, tok, double(B) * L.nx * L.ny * 10.0 + double(L.nx) * L.ny * 16.0, 0);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_up_stream(Context& c, const LevelView& L, int offset, int cnx, int cny, int B, const int* act,
+                      const float2* f, const float* fscale, const float2* vc, float2* z) {
+  const int tok = prof_begin(c, PC_UP);
+  int rpc = 16;
+  while (rpc > 8 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((L.ny + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
+    rpc /= 2;
+  const int chunks = (L.ny + rpc - 1) / rpc;
+  const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
+  k_up_stream<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, cnx, cny, rpc, act, f, fscale, vc, z);
+  prof_end(c, PC_UP, tok, double(B) * L.nx * L.ny * 18.0 + double(L.nx) * L.ny * 16.0, 0);
+  HB_CUDA(cudaGetLastError());
+}
+
+}  // namespace hb

@@ -166,6 +166,9 @@ int hb_prof_reset(hb_ctx* ctx);
 int hb_prof_count(hb_ctx* ctx);
 const char* hb_prof_name(hb_ctx* ctx, int i);
 int hb_prof_get(hb_ctx* ctx, int i, double* total_ms, int64_t* launches, double* bytes, double* flops);
+/* per-launch detail: turn on/off; dumps (and clears) the records collected so far
+ * as "label,us,bytes,flops" lines into buf */
+int hb_prof_detail(hb_ctx* ctx, int on, char* buf, int cap);
 /* number of library kernel launches since the last reset */
 int64_t hb_launch_count(hb_ctx* ctx);
 

@@ -51,19 +51,31 @@ int prof_begin(Context& c, int cls) {
 void prof_collect(Context& c) {
   if (c.ev_pending.empty()) return;
   HB_CUDA(cudaStreamSynchronize(c.stream));
-  for (auto& e : c.ev_pending) {
+  std::vector<float> times(c.ev_pending.size());
+  for (size_t i = 0; i < c.ev_pending.size(); ++i) {
+    auto& e = c.ev_pending[i];
     float ms = 0.f;
     HB_CUDA(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
+    times[i] = ms;
     c.prof[size_t(e.first)].ms += ms;
     c.ev_pool.push_back(e.second.first);
     c.ev_pool.push_back(e.second.second);
   }
+  for (auto& d : c.detail) {
+    d.ms = d.token < times.size() ? times[d.token] : 0.0;
+    c.detail_done.push_back(d);
+  }
+  c.detail.clear();
   c.ev_pending.clear();
 }
 
 void prof_end(Context& c, int cls, int token, double bytes, double flops) {
   if (token < 0) return;
   HB_CUDA(cudaEventRecord(c.ev_pending[size_t(token)].second.second, c.stream));
+  if (c.prof_detail)
+    c.detail.push_back(Context::DetailRec{c.prof_label.empty() ? c.prof[size_t(cls)].name : c.prof_label,
+                                          size_t(token), 0.0, bytes, flops});
+  c.prof_label.clear();
   Prof& p = c.prof[size_t(cls)];
   p.launches += 1;
   p.bytes += bytes;
@@ -816,6 +828,23 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_stream = value != 0;
   else
     throw HbError{HB_ERR_ARG, "unknown option " + k};
+  HB_API_END
+}
+
+int hb_prof_detail(hb_ctx* ctx, int on, char* buf, int cap) {
+  HB_API_BEGIN
+  prof_collect(*ctx);
+  if (buf && cap > 0) {
+    std::string s;
+    for (const auto& d : ctx->detail_done)
+      s += d.label + "," + std::to_string(d.ms * 1e3) + "," + std::to_string(d.bytes) + "," + std::to_string(d.flops) +
+           "\n";
+    const size_t n = std::min(s.size(), size_t(cap - 1));
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  ctx->detail_done.clear();
+  ctx->prof_detail = on != 0;
   HB_API_END
 }
 

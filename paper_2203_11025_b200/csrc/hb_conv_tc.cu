@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapWh32, const __grid_constant__ CUtensorMap mapWl32,
               const __grid_constant__ CUtensorMap mapWh16, const __grid_constant__ CUtensorMap mapWl16, TcParams p,
-              int stages, int kcmax, int G) {
+              int stages, int kcmax, int G, int dbg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t bar_full[TC_MAX_STAGES], bar_cvt[TC_MAX_STAGES], bar_empty[TC_MAX_STAGES];
   __shared__ uint64_t bar_tfull[2], bar_tempty[2];
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int kc = (r >= nchunk_a) ? p.s.kcb : p.s.kca;
             bytes += uint32_t(TC_M * kc * 4 + 2 * N * kc * 4);
           }
+          if (dbg & 8) bytes = 0;
           mbar_expect_tx(&bar_full[s], bytes);
           for (int kb = k0; kb < k1; ++kb) {
             const int g = kb - k0;
@@ -200,6 +202,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int ci0 = srcb ? (r - nchunk_a) * kc : r * kc;
             const int kglob = tap * cin + (srcb ? p.s.ca : 0) + ci0;
             const int ky = tap / 3, kx = tap % 3;
+            if (dbg & 8) continue;
             if (!srcb)
               tma_load_4d(sA(s, g), &mapA, &bar_full[s], ci0, x0 + kx - 1, y0 + ky - 1, b);
             else
@@ -239,7 +242,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int rowb = kc * 4;
             const uint32_t a = smem_u32(sA(s, g)), al = smem_u32(sAl(s, g));
             const uint32_t wh = smem_u32(sWh(s, g)), wl = smem_u32(sWl(s, g));
-            for (int k = 0; k < kc / 8; ++k) {
+            for (int k = 0; k < ((dbg & 1) ? 0 : kc / 8); ++k) {
               const uint32_t off = k * 32;
               const uint64_t dA = umma_desc(a + off, rowb), dAl = umma_desc(al + off, rowb);
               const uint64_t dWh = umma_desc(wh + off, rowb), dWl = umma_desc(wl + off, rowb);
@@ -276,7 +279,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int kc = (r >= nchunk_a) ? p.s.kcb : p.s.kca;
           float4* a4 = reinterpret_cast<float4*>(sA(s, g));
           float4* l4 = reinterpret_cast<float4*>(sAl(s, g));
-          const int n4 = TC_M * kc / 4;
+          const int n4 = (dbg & 2) ? 0 : TC_M * kc / 4;
           // hi = x with the 13 low mantissa bits cleared (a tf32 value), lo = x - hi
           // (exact in fp32; the MMA reads its top 10 mantissa bits) -- integer
           // mask + one FADD per element, no cvt (conversion-pipe bound otherwise)
@@ -317,7 +320,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int row = 32 * q + lane;
       const int yy = row / p.bw, xx = row % p.bw;
       float* orow = p.out + ((size_t(b) * p.H + (y0 + yy)) * p.W + (x0 + xx)) * N;
-      for (int c0 = 0; c0 < N; c0 += 16) {
+      for (int c0 = 0; c0 < ((dbg & 4) ? 0 : N); c0 += 16) {
         uint32_t v[16];
         const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * N + c0);
         asm volatile(
@@ -440,7 +443,8 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   const int kcmax = (kca == 32 || (cb && kcb == 32)) ? 32 : 16;
   const int chunk_bytes = 2 * TC_M * kcmax * 4 + 2 * cw.cout * kcmax * 4;
   // group K chunks per stage so a stage moves >= ~48 KB (latency-bound otherwise)
-  const int G = std::max(1, std::min(9, (48 * 1024) / chunk_bytes));
+  static const int g_env = getenv("HB_CONV_G") ? atoi(getenv("HB_CONV_G")) : 0;
+  const int G = g_env > 0 ? g_env : std::max(1, std::min(9, (48 * 1024) / chunk_bytes));
   const int stage_bytes = G * chunk_bytes;
   int stages = TC_MAX_STAGES;
   while (stages > 2 && stages * stage_bytes + 1024 > 220 * 1024) --stages;
@@ -453,7 +457,11 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   const int tiles = B * (H / bh) * (W / bw);
   const int grid = std::min(tiles, c.num_sms);
   const int tok = prof_begin(c, PC_CONV);
-  k_conv_tc<<<grid, TC_THREADS, smem, c.stream>>>(mA, mB, wh32, wl32, wh16, wl16, p, stages, kcmax, G);
+  if (c.prof_detail)
+    c.prof_label = "conv_tc " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
+                   std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
+  static const int dbg = getenv("HB_CONV_DEBUG") ? atoi(getenv("HB_CONV_DEBUG")) : 0;
+  k_conv_tc<<<grid, TC_THREADS, smem, c.stream>>>(mA, mB, wh32, wl32, wh16, wl16, p, stages, kcmax, G, dbg);
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout),
            2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());

@@ -245,6 +245,15 @@ struct Context {
   std::vector<Prof> prof;
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> ev_pending;
+  // per-launch detail (label set by the launcher just before prof_end)
+  bool prof_detail = false;
+  std::string prof_label;
+  struct DetailRec {
+    std::string label;
+    size_t token;
+    double ms, bytes, flops;
+  };
+  std::vector<DetailRec> detail, detail_done;
   int64_t launches = 0;
 };
 

@@ -228,6 +228,9 @@ static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int 
   ConvArgs p{B, H, W, a, sa, ca, b, sb, cb, cw.dw.p, cw.db.p, cw.cout, relu, out, act};
   const dim3 grid(((W + CT_W - 1) / CT_W) * ((H + CT_H - 1) / CT_H), (cw.cout + CT_CO - 1) / CT_CO, B);
   NScope ns(c, PC_CONV, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
+  if (c.prof_detail)
+    c.prof_label = "conv_simt " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
+                   std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
   k_conv3x3<<<grid, 256, 0, c.stream>>>(p);
   HB_CUDA(cudaGetLastError());
 }

@@ -103,6 +103,7 @@ def lib():
         L.hb_prof_name.restype = C.c_char_p
         L.hb_prof_name.argtypes = [_vp, C.c_int]
         L.hb_prof_get.argtypes = [_vp, C.c_int, _dp, C.POINTER(C.c_int64), _dp, _dp]
+        L.hb_prof_detail.argtypes = [_vp, C.c_int, C.c_char_p, C.c_int]
         L.hb_launch_count.restype = C.c_int64
         L.hb_launch_count.argtypes = [_vp]
         _lib = L
@@ -348,6 +349,16 @@ class Context:
             self._check(lib().hb_prof_get(self.h, i, C.byref(ms), C.byref(n), C.byref(by), C.byref(fl)))
             out[lib().hb_prof_name(self.h, i).decode()] = dict(ms=ms.value, launches=n.value, bytes=by.value,
                                                                flops=fl.value)
+        return out
+
+    def prof_detail(self, on=True):
+        """Switch per-launch records on/off; returns [(label, us, bytes, flops)] collected so far."""
+        buf = C.create_string_buffer(1 << 22)
+        self._check(lib().hb_prof_detail(self.h, int(on), buf, len(buf)))
+        out = []
+        for ln in buf.value.decode().splitlines():
+            lab, us, by, fl = ln.rsplit(",", 3)
+            out.append((lab, float(us), float(by), float(fl)))
         return out
 
     def launch_count(self) -> int:

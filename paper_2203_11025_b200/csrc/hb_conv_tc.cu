@@ -19,6 +19,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -30,7 +31,7 @@ namespace hb {
 
 namespace {
 
-constexpr int TC_THREADS = 320;
+constexpr int TC_THREADS = 448;  // 14 warps, see k_conv_tc
 constexpr int TC_MAX_STAGES = 8;
 constexpr int TC_M = 128;
 
@@ -55,6 +56,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+// whole-warp forms: warp-uniform operands, one elected lane issues
+__device__ __forceinline__ void mbar_expect_tx_elect(uint64_t* bar, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(bytes)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d_elect(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                                  int c2, int c3) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+      "[%6];\n\t}" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d_elect(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n\t}" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2,
                                             int c3) {
   asm volatile(
@@ -75,26 +101,19 @@ __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::
 
 // UMMA shared-memory descriptor, K-major, SWIZZLE_128B (2) or SWIZZLE_64B (4):
 // start >> 4 [0,14), LBO [16,30) (unused for swizzled K-major), SBO = 8 rows *
-// row bytes >> 4 [32,46), version 1 [46,48), layout [61,64)
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, int row_bytes) {
-  uint64_t d = 0;
-  d |= uint64_t((saddr & 0x3FFFF) >> 4);
-  d |= uint64_t(1) << 16;
-  d |= uint64_t((8 * row_bytes) >> 4) << 32;
-  d |= uint64_t(1) << 46;
-  d |= uint64_t(row_bytes == 128 ? 2 : 4) << 61;
-  return d;
-}
-__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(idesc), "r"(acc));
-}
+// row bytes >> 4 [32,46), version 1 [46,48), layout [61,64).  Built as two
+// 32-bit words in the MMA issuer (umma_tf32_w).
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
 }
 
 struct TcSources {
@@ -105,52 +124,133 @@ struct TcSources {
 
 struct TcParams {
   int B, H, W, cout, relu;
+  int ntile, nsplit;  // output channels per work item (N of the MMA), work items per pixel tile
   int bw, bh;         // pixel box of one M tile
   TcSources s;
   const float* bias;
   float* out;
   const int* act;
+  long long* trace;  // debug: per-stage role timestamps of CTA 0 (HB_CONV_TRACE), else null
 };
 
+// pipeline geometry chosen on the host (see launch_conv_tc)
+struct TcLayout {
+  int stages;     // smem ring depth
+  int G;          // K chunks per stage
+  int kcmax;      // widest chunk (16 | 32 channels)
+  int nslots;     // TMEM A-operand ring depth (one slot per stage)
+  int nacc;       // accumulator buffers (1 | 2)
+  int ncat;       // 2-MMA 3xTF32 form (B = [W_hi ; W_lo])
+  int wres;       // all weights resident in smem (loaded once per CTA) instead of streamed per stage
+};
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+
+// D (+)= A * B^T with A (M=128 x K=8 tf32) in TMEM, B descriptor as (lo, hi)
+// words.  Executed by a whole warp with warp-uniform operands (so they live in
+// uniform registers); one elected lane issues.
+__device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint32_t blo, uint32_t bhi, uint32_t idesc,
+                                        uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b64 db;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %5, 0;\n\t"
+      "mov.b64 db, {%2, %3};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], db, %4, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "r"(blo), "r"(bhi), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      : "memory");
+}
+
 // Persistent CTA (one per SM), 10 warps:
-//   w0 TMA producer | w1 MMA issuer | w2..w5 split A in smem | w6..w9 epilogue.
-// The smem ring runs continuously across the CTA's M tiles; the accumulator is
-// double-buffered in TMEM (2 x N columns), so tile t's epilogue (TMEM -> bias,
-// ReLU -> NHWC) overlaps tile t+1's MMAs.
+//   w0 TMA producer | w1 MMA issuer | w2..w9 A split smem -> TMEM | w10..w13 epilogue.
+//
+// A K chunk = one tap x kc input channels of a 128-pixel tile.  The producer
+// TMA-loads the fp32 activations (a 4-D box whose out-of-range taps read
+// zeros = the padding) and the [W_hi ; W_lo] weight rows into a smem stage of
+// G chunks.  The converter warps own TMEM lanes 32*(warp%4).. (= tile pixels):
+// each thread reads its pixel's kc channels (swizzled rows, conflict-free),
+// splits x = hi + lo (hi = x with the 13 low mantissa bits cleared, lo = x -
+// hi, exact) and stores both into a TMEM slot.  The MMA thread then issues
+// kind::tf32 MMAs with A read from TMEM (no shared-memory A traffic) and B
+// from the smem stage:
+//   ncat (2N <= 64):  D[:, 0:2N] += A_hi [W_hi | W_lo];  D[:, 0:N] += A_lo W_hi
+//   otherwise:        D += A_hi W_hi + A_hi W_lo + A_lo W_hi
+// Accumulators are double-buffered in TMEM where the slot ring leaves room, so
+// tile t's epilogue (TMEM -> bias, ReLU -> NHWC) overlaps tile t+1's MMAs.
+// The K schedule (tap, source, channel chunk -> TMA coordinates) is tabulated
+// in shared memory once per CTA: the producer and MMA threads are serial
+// single-thread loops where integer division costs more than a 16-channel
+// chunk's data movement.
+constexpr int TC_MAX_CHUNKS = 256;
+constexpr int TC_MAX_SLOTS = 8;
+
+template <int KC, int NCAT>  // KC: uniform chunk width (16 | 32) or 0 = mixed; NCAT: -1 = runtime
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapWh32, const __grid_constant__ CUtensorMap mapWl32,
               const __grid_constant__ CUtensorMap mapWh16, const __grid_constant__ CUtensorMap mapWl16, TcParams p,
-              int stages, int kcmax, int G, int dbg) {
+              TcLayout lay, int dbg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ uint64_t bar_full[TC_MAX_STAGES], bar_cvt[TC_MAX_STAGES], bar_empty[TC_MAX_STAGES];
-  __shared__ uint64_t bar_tfull[2], bar_tempty[2];
+  __shared__ uint64_t bar_full[TC_MAX_STAGES], bar_empty[TC_MAX_STAGES];
+  __shared__ uint64_t bar_afull[TC_MAX_SLOTS], bar_aempty[TC_MAX_SLOTS];
+  __shared__ uint64_t bar_tfull[2], bar_tempty[2], bar_w;
   __shared__ uint32_t tmem_slot;
+  __shared__ int4 sched[TC_MAX_CHUNKS];       // per K chunk: {flags, ci0, kglob, kc}
+  __shared__ uint32_t sbytes[TC_MAX_CHUNKS];  // per stage: TMA bytes
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int N = p.cout;
+  const int N = p.ntile;  // output channels of this CTA's work items; p.cout = row stride of out
+  const int stages = lay.stages, G = lay.G, kcmax = KC ? KC : lay.kcmax, nslots = lay.nslots;
+  const bool ncat = NCAT >= 0 ? NCAT != 0 : lay.ncat != 0;
+  const int accw = ncat ? 2 * N : N;          // TMEM columns per accumulator buffer [main | correction]
+  const int slot_cols = G * 2 * kcmax;        // TMEM columns per A slot: G x [hi | lo]
+  const int slot0 = lay.nacc * accw;          // first A-slot column
   const int tiles_x = p.W / p.bw, tiles_y = p.H / p.bh;
-  const int ntiles = p.B * tiles_x * tiles_y;
-  unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  // a stage holds G consecutive K chunks: A[G], A_lo[G], W_hi[G], W_lo[G]
-  const int a_bytes = TC_M * kcmax * 4, w_bytes = N * kcmax * 4;
-  const int stage_bytes = G * (2 * a_bytes + 2 * w_bytes);
+  const int ntiles = p.B * tiles_x * tiles_y * p.nsplit;
+  // 1024-align by offset (not by integer cast) so the compiler keeps the shared address space
+  unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  // a stage holds G consecutive K chunks: A[G] then [W_hi ; W_lo][G]
+  const int a_bytes = TC_M * kcmax * 4, w_bytes = 2 * N * kcmax * 4;
+  const bool wres = lay.wres != 0;
+  const int stage_bytes = G * (a_bytes + (wres ? 0 : w_bytes));
+  unsigned char* wbase = base + stages * stage_bytes;  // resident weights: chunk kb at wbase + kb * w_bytes
   auto sA = [&](int s, int g) { return base + s * stage_bytes + g * a_bytes; };
-  auto sAl = [&](int s, int g) { return base + s * stage_bytes + (G + g) * a_bytes; };
-  auto sWh = [&](int s, int g) { return base + s * stage_bytes + 2 * G * a_bytes + g * w_bytes; };
-  auto sWl = [&](int s, int g) { return base + s * stage_bytes + 2 * G * a_bytes + (G + g) * w_bytes; };
+  auto sW = [&](int s, int g) { return base + s * stage_bytes + G * a_bytes + g * w_bytes; };
   const int cin = p.s.ca + p.s.cb;
   const int nchunk_a = p.s.ca / p.s.kca, nchunk_b = p.s.cb ? p.s.cb / p.s.kcb : 0;
   const int per_tap = nchunk_a + nchunk_b;
   const int nk = 9 * per_tap;
   const int nst = (nk + G - 1) / G;  // stage iterations per tile
-  uint32_t ncols = 32;
-  while (ncols < uint32_t(2 * N)) ncols <<= 1;
+  const bool mixed = KC == 0;
+  for (int kb = threadIdx.x; kb < nk; kb += blockDim.x) {
+    const int tap = kb / per_tap, r = kb - tap * per_tap;
+    const bool srcb = r >= nchunk_a;
+    const int kc = srcb ? p.s.kcb : p.s.kca;
+    const int ci0 = srcb ? (r - nchunk_a) * kc : r * kc;
+    sched[kb] = make_int4(int(srcb) | ((tap % 3) << 2) | ((tap / 3) << 4), ci0, tap * cin + (srcb ? p.s.ca : 0) + ci0,
+                          kc);
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_cvt[s], 128);
-      mbar_init(&bar_empty[s], 1);
+      mbar_init(&bar_empty[s], wres ? 256 : 256 + 1);  // converter threads (A read) [+ MMA commit (W read)]
     }
+    for (int j = 0; j < nslots; ++j) {
+      mbar_init(&bar_afull[j], 256);
+      mbar_init(&bar_aempty[j], 1);
+    }
+    mbar_init(&bar_w, 1);
     for (int a = 0; a < 2; ++a) {
       mbar_init(&bar_tfull[a], 1);
       mbar_init(&bar_tempty[a], 128);
@@ -159,56 +259,71 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                 "r"(ncols));
+                 "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  for (int st = threadIdx.x; st < nst; st += blockDim.x) {
+    uint32_t bytes = 0;
+    for (int kb = st * G; kb < min(nk, st * G + G); ++kb) bytes += uint32_t((TC_M + (wres ? 0 : 2 * N)) * sched[kb].w * 4);
+    sbytes[st] = (dbg & 8) ? 0u : bytes;
+  }
+  __syncthreads();
   const uint32_t tmem_base = tmem_slot;
 
-  auto tile_coords = [&](int tile, int& b, int& y0, int& x0) {
+  // work item -> (image, pixel box, output-channel block n0)
+  int n0 = 0;
+  auto tile_coords = [&](int item, int& b, int& y0, int& x0) {
+    n0 = (item % p.nsplit) * N;
+    const int tile = item / p.nsplit;
     b = tile / (tiles_x * tiles_y);
     y0 = ((tile / tiles_x) % tiles_y) * p.bh;
     x0 = (tile % tiles_x) * p.bw;
   };
 
-  if (warp == 0) {
-    if (lane == 0) {  // ---------------- TMA producer
+  if ((dbg & 16) && warp != 1) {
+    // debug: everything but the MMA issuer idles
+  } else if (warp == 0) {
+    {  // ---------------- TMA producer (whole warp, elected lane issues)
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
+      if (wres) {  // the whole [W_hi ; W_lo] schedule, once
+        uint32_t wb = 0;
+        for (int kb = 0; kb < nk; ++kb) wb += uint32_t(2 * N * sched[kb].w * 4);
+        mbar_expect_tx_elect(&bar_w, (dbg & 8) ? 0u : wb);
+        for (int kb = 0; kb < nk && !(dbg & 8); ++kb) {
+          const int4 e = sched[kb];
+          const int kc = KC ? KC : e.w;
+          unsigned char* w = wbase + kb * w_bytes;
+          tma_load_2d_elect(w, kc == 32 ? &mapWh32 : &mapWh16, &bar_w, e.z, 0);
+          tma_load_2d_elect(w + N * kc * 4, kc == 32 ? &mapWl32 : &mapWl16, &bar_w, e.z, 0);
+        }
+      }
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int b, y0, x0;
         tile_coords(tile, b, y0, x0);
-        const bool skip = p.act && !p.act[b];
-        if (skip) continue;
-        for (int st = 0; st < nst; ++st, ++it) {
+        if (p.act && !p.act[b]) continue;
+        const int bb = p.s.b_is_ctx ? 0 : b;
+        for (int st = 0, kb = 0; st < nst; ++st, ++it) {
           if (it >= stages) mbar_wait(&bar_empty[s], ph ^ 1);
-          const int k0 = st * G, k1 = min(nk, k0 + G);
-          uint32_t bytes = 0;
-          for (int kb = k0; kb < k1; ++kb) {
-            const int r = kb % per_tap;
-            const int kc = (r >= nchunk_a) ? p.s.kcb : p.s.kca;
-            bytes += uint32_t(TC_M * kc * 4 + 2 * N * kc * 4);
-          }
-          if (dbg & 8) bytes = 0;
-          mbar_expect_tx(&bar_full[s], bytes);
-          for (int kb = k0; kb < k1; ++kb) {
-            const int g = kb - k0;
-            const int tap = kb / per_tap, r = kb % per_tap;
-            const bool srcb = r >= nchunk_a;
-            const int kc = srcb ? p.s.kcb : p.s.kca;
-            const int ci0 = srcb ? (r - nchunk_a) * kc : r * kc;
-            const int kglob = tap * cin + (srcb ? p.s.ca : 0) + ci0;
-            const int ky = tap / 3, kx = tap % 3;
+          if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 4 + 0] = clock64();
+          mbar_expect_tx_elect(&bar_full[s], sbytes[st]);
+          for (int g = 0; g < G && kb < nk; ++g, ++kb) {
             if (dbg & 8) continue;
-            if (!srcb)
-              tma_load_4d(sA(s, g), &mapA, &bar_full[s], ci0, x0 + kx - 1, y0 + ky - 1, b);
+            const int4 e = sched[kb];
+            const int kx = (e.x >> 2) & 3, ky = e.x >> 4;
+            const int kc = KC ? KC : e.w;
+            if (!(e.x & 1))
+              tma_load_4d_elect(sA(s, g), &mapA, &bar_full[s], e.y, x0 + kx - 1, y0 + ky - 1, b);
             else
-              tma_load_4d(sA(s, g), &mapB, &bar_full[s], ci0, x0 + kx - 1, y0 + ky - 1, p.s.b_is_ctx ? 0 : b);
-            tma_load_2d(sWh(s, g), kc == 32 ? &mapWh32 : &mapWh16, &bar_full[s], kglob, 0);
-            tma_load_2d(sWl(s, g), kc == 32 ? &mapWl32 : &mapWl16, &bar_full[s], kglob, 0);
+              tma_load_4d_elect(sA(s, g), &mapB, &bar_full[s], e.y, x0 + kx - 1, y0 + ky - 1, bb);
+            if (wres) continue;
+            unsigned char* w = sW(s, g);
+            tma_load_2d_elect(w, kc == 32 ? &mapWh32 : &mapWh16, &bar_full[s], e.z, n0);
+            tma_load_2d_elect(w + N * kc * 4, kc == 32 ? &mapWl32 : &mapWl16, &bar_full[s], e.z, n0);
           }
           if (++s == stages) {
             s = 0;
@@ -218,121 +333,168 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {  // ---------------- MMA issuer
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
-      int s = 0;
-      uint32_t ph = 0;
-      int tl = 0;  // local tile counter (accumulator buffer = tl & 1)
+    {  // ---------------- MMA issuer (whole warp, elected lane issues)
+      // B descriptors as (lo, hi) words: lo = start >> 4 | LBO, hi = SBO |
+      // version | layout; chunk and K-step offsets are 32-bit adds on lo (the
+      // 14-bit start field never carries for smem < 256 KB)
+      const uint32_t idN = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
+      const uint32_t id2N = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t((2 * N) >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
+      const uint32_t hi32 = (1024u >> 4) | (1u << 14) | (2u << 29);  // 128-B rows, SWIZZLE_128B
+      const uint32_t hi16 = (512u >> 4) | (1u << 14) | (4u << 29);   // 64-B rows, SWIZZLE_64B
+      const uint32_t lo0 = (smem_u32(base) >> 4) | (1u << 16);
+      const uint32_t st16 = uint32_t(stage_bytes) >> 4, w16 = uint32_t(w_bytes) >> 4;
+      // warp-uniform copies (shfl from lane 0 lets the compiler keep them in uniform registers)
+      const uint32_t tbase = __shfl_sync(0xffffffff, tmem_base, 0);
+      const uint32_t lo0u = __shfl_sync(0xffffffff, lo0, 0);
+      const uint32_t wlo0 = __shfl_sync(0xffffffff, (smem_u32(wbase) >> 4) | (1u << 16), 0);
+      if (wres) mbar_wait(&bar_w, 0);
+      int s = 0, j = 0;
+      uint32_t ph = 0, aph = 0;
+      int tl = 0;  // local tile counter
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         int b, y0, x0;
         tile_coords(tile, b, y0, x0);
         if (p.act && !p.act[b]) continue;
-        const int acc = tl & 1;
-        const uint32_t tmem_d = tmem_base + uint32_t(acc * N);
-        if (tl >= 2) mbar_wait(&bar_tempty[acc], ((tl >> 1) - 1) & 1);  // epilogue drained this buffer
+        const int acc = lay.nacc == 2 ? (tl & 1) : 0;
+        const uint32_t tmem_d = tbase + uint32_t(acc * accw);
+        if (dbg & 16) {
+        } else if (lay.nacc == 2) {
+          if (tl >= 2) mbar_wait(&bar_tempty[acc], ((tl >> 1) - 1) & 1);  // epilogue drained this buffer
+        } else if (tl >= 1) {
+          mbar_wait(&bar_tempty[0], (tl - 1) & 1);
+        }
         tc_fence_after();
-        for (int st = 0; st < nst; ++st) {
-          mbar_wait(&bar_cvt[s], ph);
+        uint32_t first = 0;  // accumulate flag: 0 only for the tile's first MMA
+        for (int st = 0, kb = 0; st < nst; ++st) {
+          if (!(dbg & 16)) {
+            if (!wres) mbar_wait(&bar_full[s], ph);  // W in smem
+            mbar_wait(&bar_afull[j], aph);           // A hi/lo in TMEM
+          }
           tc_fence_after();
-          const int k0 = st * G, k1 = min(nk, k0 + G);
-          for (int kb = k0; kb < k1; ++kb) {
-            const int g = kb - k0;
-            const int r = kb % per_tap;
-            const int kc = (r >= nchunk_a) ? p.s.kcb : p.s.kca;
-            const int rowb = kc * 4;
-            const uint32_t a = smem_u32(sA(s, g)), al = smem_u32(sAl(s, g));
-            const uint32_t wh = smem_u32(sWh(s, g)), wl = smem_u32(sWl(s, g));
-            for (int k = 0; k < ((dbg & 1) ? 0 : kc / 8); ++k) {
-              const uint32_t off = k * 32;
-              const uint64_t dA = umma_desc(a + off, rowb), dAl = umma_desc(al + off, rowb);
-              const uint64_t dWh = umma_desc(wh + off, rowb), dWl = umma_desc(wl + off, rowb);
-              umma_tf32(tmem_d, dA, dWh, idesc, (kb | k) ? 1u : 0u);
-              umma_tf32(tmem_d, dA, dWl, idesc, 1u);
-              umma_tf32(tmem_d, dAl, dWh, idesc, 1u);
+          if (p.trace && blockIdx.x == 0 && lane == 0 && tl * nst + st < 64) p.trace[(tl * nst + st) * 4 + 2] = clock64();
+          uint32_t lW = wres ? wlo0 + uint32_t(kb) * w16 : lo0u + uint32_t(s) * st16 + (uint32_t(G * a_bytes) >> 4);
+          uint32_t ta = tbase + uint32_t(slot0 + j * slot_cols);
+          for (int g = 0; g < G && kb < nk; ++g, ++kb, lW += w16, ta += uint32_t(2 * kcmax)) {
+            const int kc = mixed ? sched[kb].w : kcmax;
+            if (dbg & 1) continue;
+            const uint32_t hi = kc == 32 ? hi32 : hi16;
+            const uint32_t lWl = lW + uint32_t((N * kc * 4) >> 4);
+            const uint32_t tal = ta + uint32_t(kc);
+#pragma unroll
+            for (int k = 0; k < kc / 8; ++k) {
+              if (ncat) {  // small terms accumulate apart from A_hi W_hi: D[:, N:2N] = A_hi W_lo + A_lo W_hi
+                umma_ts(tmem_d, ta + 8 * k, lW + 2 * k, hi, id2N, first);
+                umma_ts(tmem_d + uint32_t(N), tal + 8 * k, lW + 2 * k, hi, idN, 1u);
+              } else {
+                umma_ts(tmem_d, ta + 8 * k, lW + 2 * k, hi, idN, first);
+                umma_ts(tmem_d, ta + 8 * k, lWl + 2 * k, hi, idN, 1u);
+                umma_ts(tmem_d, tal + 8 * k, lW + 2 * k, hi, idN, 1u);
+              }
+              first = 1;
             }
           }
-          umma_commit(&bar_empty[s]);
+          if (!(dbg & 16)) {
+            if (!wres) umma_commit_elect(&bar_empty[s]);  // W stage free once these MMAs completed
+            umma_commit_elect(&bar_aempty[j]);  // A slot free likewise
+          }
           if (++s == stages) {
             s = 0;
             ph ^= 1;
           }
+          if (++j == nslots) {
+            j = 0;
+            aph ^= 1;
+          }
         }
-        umma_commit(&bar_tfull[acc]);
+        if (!(dbg & 16)) umma_commit_elect(&bar_tfull[acc]);
         ++tl;
       }
     }
-  } else if (warp < 6) {
-    // ---------------- warps 2..5: split each A stage into tf32 hi / lo in place
-    const int ct = threadIdx.x - 64;
-    int s = 0;
-    uint32_t ph = 0;
+  } else if (warp < 10) {
+    // ---------------- warps 2..9: A chunk (smem, fp32) -> TMEM slot [hi | lo];
+    // two warps per TMEM lane quarter, taking alternate chunks of a stage
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = 32 * q + lane;  // tile pixel row = TMEM lane
+    int s = 0, j = 0;
+    uint32_t ph = 0, aph = 0;
+    int itc = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int b, y0, x0;
       tile_coords(tile, b, y0, x0);
       if (p.act && !p.act[b]) continue;
-      for (int st = 0; st < nst; ++st) {
+      for (int st = 0, kb = 0; st < nst; ++st, ++itc) {
         mbar_wait(&bar_full[s], ph);
-        const int k0 = st * G, k1 = min(nk, k0 + G);
-        for (int kb = k0; kb < k1; ++kb) {
-          const int g = kb - k0;
-          const int r = kb % per_tap;
-          const int kc = (r >= nchunk_a) ? p.s.kcb : p.s.kca;
-          float4* a4 = reinterpret_cast<float4*>(sA(s, g));
-          float4* l4 = reinterpret_cast<float4*>(sAl(s, g));
-          const int n4 = (dbg & 2) ? 0 : TC_M * kc / 4;
-          // hi = x with the 13 low mantissa bits cleared (a tf32 value), lo = x - hi
-          // (exact in fp32; the MMA reads its top 10 mantissa bits) -- integer
-          // mask + one FADD per element, no cvt (conversion-pipe bound otherwise)
-          for (int i = ct; i < n4; i += 128) {
-            const float4 x = a4[i];
-            float4 hi, lo;
-            hi.x = __uint_as_float(__float_as_uint(x.x) & 0xffffe000u);
-            hi.y = __uint_as_float(__float_as_uint(x.y) & 0xffffe000u);
-            hi.z = __uint_as_float(__float_as_uint(x.z) & 0xffffe000u);
-            hi.w = __uint_as_float(__float_as_uint(x.w) & 0xffffe000u);
-            lo.x = x.x - hi.x;
-            lo.y = x.y - hi.y;
-            lo.z = x.z - hi.z;
-            lo.w = x.w - hi.w;
-            a4[i] = hi;
-            l4[i] = lo;
+        if (itc >= nslots) mbar_wait(&bar_aempty[j], aph ^ 1);
+        tc_fence_after();
+        if (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && itc < 64) p.trace[itc * 4 + 1] = clock64();
+        uint32_t ta = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(slot0 + j * slot_cols);
+        for (int g = 0; g < G && kb < nk; ++g, ++kb, ta += uint32_t(2 * kcmax)) {
+          const int kc = mixed ? sched[kb].w : kcmax;
+          if ((dbg & 2) || (g & 1) != half) continue;
+          const unsigned char* row = sA(s, g) + r * (kc * 4);
+          // swizzled 16-B chunk c of row r sits at chunk c ^ f(r): SW128 f = r & 7, SW64 f = (r >> 1) & 3
+          const int f = kc == 32 ? (r & 7) : ((r >> 1) & 3);
+#pragma unroll
+          for (int h = 0; h < kc / 16; ++h) {
+            uint32_t vh[16], vl[16];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              const float4 x = *reinterpret_cast<const float4*>(row + (((4 * h + c) ^ f) << 4));
+              const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const uint32_t hb = __float_as_uint(xs[e]) & 0xffffe000u;
+                vh[4 * c + e] = hb;
+                vl[4 * c + e] = __float_as_uint(xs[e] - __uint_as_float(hb));
+              }
+            }
+            tmem_st16(ta + uint32_t(16 * h), vh);
+            tmem_st16(ta + uint32_t(kc + 16 * h), vl);
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> tensor-core reads
-        mbar_arrive(&bar_cvt[s]);
+        mbar_arrive(&bar_empty[s]);  // this thread's smem reads are done (values are in registers)
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        tc_fence_before();
+        mbar_arrive(&bar_afull[j]);
+        if (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && itc < 64) p.trace[itc * 4 + 3] = clock64();
         if (++s == stages) {
           s = 0;
           ph ^= 1;
         }
+        if (++j == nslots) {
+          j = 0;
+          aph ^= 1;
+        }
       }
     }
   } else {
-    // ---------------- warps 6..9: epilogue; warp owns TMEM lanes 32*(warp%4) .. +31 (= tile pixel rows)
+    // ---------------- warps 10..13: epilogue; warp owns TMEM lanes 32*(warp%4) .. +31 (= tile pixel rows)
     const int q = warp & 3;
     int tl = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int b, y0, x0;
       tile_coords(tile, b, y0, x0);
       if (p.act && !p.act[b]) continue;
-      const int acc = tl & 1;
-      mbar_wait(&bar_tfull[acc], (tl >> 1) & 1);
+      const int acc = lay.nacc == 2 ? (tl & 1) : 0;
+      const uint32_t uph = lay.nacc == 2 ? uint32_t((tl >> 1) & 1) : uint32_t(tl & 1);
+      mbar_wait(&bar_tfull[acc], uph);
       tc_fence_after();
       const int row = 32 * q + lane;
       const int yy = row / p.bw, xx = row % p.bw;
-      float* orow = p.out + ((size_t(b) * p.H + (y0 + yy)) * p.W + (x0 + xx)) * N;
+      float* orow = p.out + ((size_t(b) * p.H + (y0 + yy)) * p.W + (x0 + xx)) * p.cout + n0;
+      const float* bias = p.bias + n0;
+      const uint32_t trow = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * accw);
       for (int c0 = 0; c0 < ((dbg & 4) ? 0 : N); c0 += 16) {
-        uint32_t v[16];
-        const uint32_t taddr = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * N + c0);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(taddr));
+        uint32_t v[16], u[16];
+        tmem_ld16(trow + uint32_t(c0), v);
+        if (ncat) tmem_ld16(trow + uint32_t(N + c0), u);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         float o[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float x = __uint_as_float(v[i]) + __ldg(p.bias + c0 + i);
+          float x = __uint_as_float(v[i]) + __ldg(bias + c0 + i);
+          if (ncat) x += __uint_as_float(u[i]);
           o[i] = p.relu ? fmaxf(x, 0.f) : x;
         }
 #pragma unroll
@@ -348,7 +510,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(ncols));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
   }
 }
 
@@ -379,12 +541,12 @@ CUtensorMap act_map(const float* ptr, int B, int H, int W, int C, int kc, int bw
   return m;
 }
 
-// weight map: [Cout][K] fp32 as 2-D (K, Cout); box (kc, Cout)
-CUtensorMap w_map(const float* ptr, int cout, int K, int kc) {
+// weight map: [Cout][K] fp32 as 2-D (K, Cout); box (kc, rows)
+CUtensorMap w_map(const float* ptr, int cout, int K, int kc, int rows) {
   CUtensorMap m;
   const cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(cout)};
   const cuuint64_t strides[1] = {cuuint64_t(K) * 4};
-  const cuuint32_t box[2] = {cuuint32_t(kc), cuuint32_t(cout)};
+  const cuuint32_t box[2] = {cuuint32_t(kc), cuuint32_t(rows)};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = get_encode()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box,
                                   es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -437,34 +599,84 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   const CUtensorMap mA = act_map(a, B, H, W, ca, kca, bw, bh);
   const CUtensorMap mB = cb ? act_map(bsrc, b_ctx ? 1 : B, H, W, cb, kcb, bw, bh) : mA;
   const int K = 9 * cw.cin;
-  const CUtensorMap wh32 = w_map(cw.dwh.p, cw.cout, K, 32), wl32 = w_map(cw.dwl.p, cw.cout, K, 32);
-  const CUtensorMap wh16 = w_map(cw.dwh.p, cw.cout, K, 16), wl16 = w_map(cw.dwl.p, cw.cout, K, 16);
-  TcParams p{B, H, W, cw.cout, relu, bw, bh, TcSources{ca, cb, kca, kcb, b_ctx ? 1 : 0}, cw.db.p, out, act};
+  // Cout > 128 is split into 128-channel work items so every layer uses the
+  // split-accumulator form (correction terms summed apart, better accuracy)
+  const int nsplit = cw.cout > 128 ? cw.cout / 128 : 1;
+  const int ntile = cw.cout / nsplit;
+  if (ntile * nsplit != cw.cout || ntile > 128) return false;
+  const CUtensorMap wh32 = w_map(cw.dwh.p, cw.cout, K, 32, ntile), wl32 = w_map(cw.dwl.p, cw.cout, K, 32, ntile);
+  const CUtensorMap wh16 = w_map(cw.dwh.p, cw.cout, K, 16, ntile), wl16 = w_map(cw.dwl.p, cw.cout, K, 16, ntile);
+  TcParams p{B,  H,  W,  cw.cout, relu, ntile, nsplit, bw, bh, TcSources{ca, cb, kca, kcb, b_ctx ? 1 : 0}, cw.db.p,
+             out, act, nullptr};
+  static const bool trace = getenv("HB_CONV_TRACE") != nullptr;
+  static long long* dtrace = nullptr;
+  if (trace) {
+    if (!dtrace) HB_CUDA(cudaMalloc(&dtrace, 256 * sizeof(long long)));
+    HB_CUDA(cudaMemsetAsync(dtrace, 0, 256 * sizeof(long long), c.stream));
+    p.trace = dtrace;
+  }
   const int kcmax = (kca == 32 || (cb && kcb == 32)) ? 32 : 16;
-  const int chunk_bytes = 2 * TC_M * kcmax * 4 + 2 * cw.cout * kcmax * 4;
-  // group K chunks per stage so a stage moves >= ~48 KB (latency-bound otherwise)
-  static const int g_env = getenv("HB_CONV_G") ? atoi(getenv("HB_CONV_G")) : 0;
-  const int G = g_env > 0 ? g_env : std::max(1, std::min(9, (48 * 1024) / chunk_bytes));
-  const int stage_bytes = G * chunk_bytes;
-  int stages = TC_MAX_STAGES;
-  while (stages > 2 && stages * stage_bytes + 1024 > 220 * 1024) --stages;
-  const size_t smem = size_t(stages) * stage_bytes + 1024;
+  if (9 * (ca / kca + (cb ? cb / kcb : 0)) > TC_MAX_CHUNKS) return false;
+  // TMEM (512 columns): accumulators [nacc x accw] then nslots A slots of G x [hi | lo] chunks
+  TcLayout lay{};
+  lay.kcmax = kcmax;
+  lay.ncat = 1;
+  const int accw = 2 * ntile;
+  lay.nacc = 2 * accw + 2 * (2 * 2 * kcmax) <= 512 ? 2 : 1;
+  const int free_cols = 512 - lay.nacc * accw;
+  if (free_cols < 2 * 2 * kcmax) return false;
+  const int nk = 9 * (ca / kca + (cb ? cb / kcb : 0));
+  const int w_chunk = 2 * ntile * kcmax * 4;
+  // small layers keep all weights resident (one TMA burst per CTA instead of
+  // two weight TMAs per chunk: TMA issue, not bytes, limits 16-channel layers)
+  lay.wres = nsplit == 1 && nk * w_chunk <= 96 * 1024 ? 1 : 0;
+  const int wres_bytes = lay.wres ? nk * w_chunk : 0;
+  const int chunk_bytes = TC_M * kcmax * 4 + (lay.wres ? 0 : w_chunk);
+  // a stage should carry enough tensor work to amortise its handshakes: aim
+  // for ~3 TMEM slots and <= 54 KB of smem per stage
+  lay.G = std::max(1, std::min({9, free_cols / (3 * 2 * kcmax), (54 * 1024) / chunk_bytes,
+                                 (220 * 1024 - 1024 - wres_bytes) / (3 * chunk_bytes)}));
+  lay.nslots = std::min(TC_MAX_SLOTS, free_cols / (lay.G * 2 * kcmax));
+  const int stage_bytes = lay.G * chunk_bytes;
+  lay.stages = TC_MAX_STAGES;
+  while (lay.stages > 2 && lay.stages * stage_bytes + wres_bytes + 1024 > 220 * 1024) --lay.stages;
+  if (lay.stages * stage_bytes + wres_bytes + 1024 > 220 * 1024 || lay.nslots < 2) return false;
+  const size_t smem = size_t(lay.stages) * stage_bytes + wres_bytes + 1024;
+  // instantiation: uniform chunk width and the 3xTF32 form as template arguments
+  // (fully unrolled issue loops); mixed-width sources take the generic one
+  const bool uni = !cb || kca == kcb;
+  void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams, TcLayout, int) =
+      !uni ? k_conv_tc<0, -1>
+           : kcmax == 32 ? (lay.ncat ? k_conv_tc<32, 1> : k_conv_tc<32, 0>)
+                         : (lay.ncat ? k_conv_tc<16, 1> : k_conv_tc<16, 0>);
   static int attr_dev = -1;
   if (attr_dev != c.device) {
-    HB_CUDA(cudaFuncSetAttribute(k_conv_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    for (auto k : {k_conv_tc<0, -1>, k_conv_tc<32, 1>, k_conv_tc<32, 0>, k_conv_tc<16, 1>, k_conv_tc<16, 0>})
+      HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     attr_dev = c.device;
   }
-  const int tiles = B * (H / bh) * (W / bw);
+  const int tiles = B * (H / bh) * (W / bw) * nsplit;
   const int grid = std::min(tiles, c.num_sms);
   const int tok = prof_begin(c, PC_CONV);
   if (c.prof_detail)
     c.prof_label = "conv_tc " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
   static const int dbg = getenv("HB_CONV_DEBUG") ? atoi(getenv("HB_CONV_DEBUG")) : 0;
-  k_conv_tc<<<grid, TC_THREADS, smem, c.stream>>>(mA, mB, wh32, wl32, wh16, wl16, p, stages, kcmax, G, dbg);
+  kern<<<grid, TC_THREADS, smem, c.stream>>>(mA, mB, wh32, wl32, wh16, wl16, p, lay, dbg);
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout),
            2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());
+  if (trace) {
+    long long h[256];
+    HB_CUDA(cudaStreamSynchronize(c.stream));
+    HB_CUDA(cudaMemcpy(h, dtrace, sizeof(h), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "conv_tc %dx%dx%d %d+%d->%d G=%d stages=%d slots=%d nacc=%d ncat=%d wres=%d: it prod cvt_in mma cvt_out\n",
+            B, H, W, ca, cb, cw.cout, lay.G, lay.stages, lay.nslots, lay.nacc, lay.ncat, lay.wres);
+    const long long t0 = h[0] ? h[0] : h[2];
+    for (int i = 0; i < 64 && (h[i * 4] || h[i * 4 + 2]); ++i)
+      fprintf(stderr, "  %2d %7lld %7lld %7lld %7lld\n", i, h[i * 4] - t0, h[i * 4 + 1] - t0, h[i * 4 + 2] - t0,
+              h[i * 4 + 3] - t0);
+  }
   return true;
 }
 

@@ -115,6 +115,137 @@ __global__ void __launch_bounds__(256) k_conv3x3(ConvArgs p) {
   }
 }
 
+// Narrow convolutions the tensor-core path does not take -- the 3-channel input
+// layer (3 [+ ctx] -> 16) and the 16 -> 2 head.  A 32 x 8 output tile per
+// CTA, CS_PX consecutive pixels x COUT outputs per thread (broadcast float4
+// weight loads); the (8+2) x (32+2) x Cin input tile and all
+// weights sit in shared memory (pixel stride Cin|1 words).
+constexpr int CS_TW = 32, CS_TH = 8, CS_PX = 1, CS_NT = CS_TW * CS_TH / CS_PX;
+
+template <int COUT>
+__global__ void __launch_bounds__(CS_NT) k_conv_small(ConvArgs p) {
+  extern __shared__ __align__(16) float cs_sm[];
+  const int bz = blockIdx.z;
+  if (p.act && !p.act[bz]) return;
+  const int cin = p.ca + p.cb, cp = cin | 1;
+  float* wts = cs_sm;                                  // [9][cin][COUT]
+  float* tile = cs_sm + ((9 * cin * COUT + 3) & ~3);   // [(TH+2)(TW+2)][cp]
+  const int tilesW = (p.W + CS_TW - 1) / CS_TW;
+  const int y0 = (blockIdx.x / tilesW) * CS_TH, x0 = (blockIdx.x % tilesW) * CS_TW;
+  const int t = threadIdx.x;
+  for (int i = t; i < 9 * cin * COUT; i += CS_NT) wts[i] = __ldg(p.w + i);
+  const float* A = p.a + bz * p.sa;
+  const float* Bsrc = p.b ? p.b + bz * p.sb : nullptr;
+  const int npix = (CS_TH + 2) * (CS_TW + 2);
+  // thread per halo-tile pixel: its Cin channels are contiguous (float4 when
+  // possible); no per-element index division
+  for (int pix = t; pix < npix; pix += CS_NT) {
+    const int gy = y0 + pix / (CS_TW + 2) - 1, gx = x0 + pix % (CS_TW + 2) - 1;
+    float* dst = tile + pix * cp;
+    if (gy >= 0 && gy < p.H && gx >= 0 && gx < p.W) {
+      const size_t px = size_t(gy) * p.W + gx;
+      const float* sa = A + px * p.ca;
+      if ((p.ca & 3) == 0) {
+        for (int c = 0; c < p.ca; c += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(sa + c));
+          dst[c] = v.x;
+          dst[c + 1] = v.y;
+          dst[c + 2] = v.z;
+          dst[c + 3] = v.w;
+        }
+      } else {
+        for (int c = 0; c < p.ca; ++c) dst[c] = __ldg(sa + c);
+      }
+      if (p.cb) {
+        const float* sb = Bsrc + px * p.cb;
+        for (int c = 0; c < p.cb; ++c) dst[p.ca + c] = __ldg(sb + c);
+      }
+    } else {
+      for (int c = 0; c < cin; ++c) dst[c] = 0.f;
+    }
+  }
+  __syncthreads();
+  const int ty = t / (CS_TW / CS_PX), tx = (t % (CS_TW / CS_PX)) * CS_PX;
+  float acc[CS_PX][COUT];
+#pragma unroll
+  for (int q = 0; q < CS_PX; ++q)
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) acc[q][co] = 0.f;
+  for (int ky = 0; ky < 3; ++ky) {
+    const float* rp = tile + ((ty + ky) * (CS_TW + 2) + tx) * cp;
+    for (int ci = 0; ci < cin; ++ci) {
+      float v[CS_PX + 2];
+#pragma unroll
+      for (int j = 0; j < CS_PX + 2; ++j) v[j] = rp[j * cp + ci];
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) {
+        const float* wp = wts + ((ky * 3 + kx) * cin + ci) * COUT;
+        if constexpr (COUT % 4 == 0) {
+#pragma unroll
+          for (int c4 = 0; c4 < COUT; c4 += 4) {
+            const float4 w = *reinterpret_cast<const float4*>(wp + c4);
+#pragma unroll
+            for (int q = 0; q < CS_PX; ++q) {
+              acc[q][c4] = fmaf(v[q + kx], w.x, acc[q][c4]);
+              acc[q][c4 + 1] = fmaf(v[q + kx], w.y, acc[q][c4 + 1]);
+              acc[q][c4 + 2] = fmaf(v[q + kx], w.z, acc[q][c4 + 2]);
+              acc[q][c4 + 3] = fmaf(v[q + kx], w.w, acc[q][c4 + 3]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int co = 0; co < COUT; ++co) {
+            const float w = wp[co];
+#pragma unroll
+            for (int q = 0; q < CS_PX; ++q) acc[q][co] = fmaf(v[q + kx], w, acc[q][co]);
+          }
+        }
+      }
+    }
+  }
+  const int y = y0 + ty;
+  if (y >= p.H) return;
+#pragma unroll
+  for (int q = 0; q < CS_PX; ++q) {
+    const int x = x0 + tx + q;
+    if (x >= p.W) continue;
+    float* O = p.out + ((size_t(bz) * p.H + y) * p.W + x) * COUT;
+    float r[COUT];
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) {
+      r[co] = acc[q][co] + __ldg(p.bias + co);
+      if (p.relu) r[co] = fmaxf(r[co], 0.f);
+    }
+    if constexpr (COUT % 4 == 0) {
+#pragma unroll
+      for (int co = 0; co < COUT; co += 4)
+        *reinterpret_cast<float4*>(O + co) = make_float4(r[co], r[co + 1], r[co + 2], r[co + 3]);
+    } else {
+#pragma unroll
+      for (int co = 0; co < COUT; ++co) O[co] = r[co];
+    }
+  }
+}
+
+// 2x2 max-pool / x2 bilinear upsample, NHWC, 4 channels per thread (C % 4 == 0)
+__global__ void k_maxpool2_v4(int H, int W, int C4, const float4* __restrict__ in, float4* __restrict__ out,
+                              const int* act) {
+  const int b = blockIdx.z, oy = blockIdx.y;
+  if (act && !act[b]) return;
+  const int Wo = W / 2;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (ox, c4)
+  if (i >= Wo * C4) return;
+  const int ox = i / C4, c = i - ox * C4;
+  const float4* s = in + ((size_t(b) * H + 2 * oy) * W + 2 * ox) * C4 + c;
+  const float4 a0 = s[0], a1 = s[C4], a2 = s[size_t(W) * C4], a3 = s[size_t(W) * C4 + C4];
+  float4 m;
+  m.x = fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x));
+  m.y = fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y));
+  m.z = fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z));
+  m.w = fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w));
+  out[((size_t(b) * (H / 2) + oy) * Wo + ox) * C4 + c] = m;
+}
+
 __global__ void k_maxpool2(int B, int H, int W, int C, const float* __restrict__ in, float* __restrict__ out,
                            const int* act) {
   const int Ho = H / 2, Wo = W / 2;
@@ -162,6 +293,29 @@ __global__ void k_upsample2(int B, int H, int W, int C, const float* __restrict_
     const float v10 = s[(size_t(y1) * W + x0) * C + c], v11 = s[(size_t(y1) * W + x1) * C + c];
     out[size_t(b) * total + i] = (1.f - fy) * ((1.f - fx) * v00 + fx * v01) + fy * ((1.f - fx) * v10 + fx * v11);
   }
+}
+
+__global__ void k_upsample2_v4(int H, int W, int C4, const float4* __restrict__ in, long long sin4,
+                               float4* __restrict__ out, const int* act) {
+  const int b = blockIdx.z, oy = blockIdx.y;
+  if (act && !act[b]) return;
+  const int Wo = 2 * W;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (ox, c4)
+  if (i >= Wo * C4) return;
+  const int ox = i / C4, c = i - ox * C4;
+  int y0, y1, x0, x1;
+  float fy, fx;
+  up_taps(oy, H, &y0, &y1, &fy);
+  up_taps(ox, W, &x0, &x1, &fx);
+  const float4* s = in + b * sin4;
+  const float4 v00 = s[(size_t(y0) * W + x0) * C4 + c], v01 = s[(size_t(y0) * W + x1) * C4 + c];
+  const float4 v10 = s[(size_t(y1) * W + x0) * C4 + c], v11 = s[(size_t(y1) * W + x1) * C4 + c];
+  auto lerp2 = [&](float a, float bq, float cq, float d) {
+    return (1.f - fy) * ((1.f - fx) * a + fx * bq) + fy * ((1.f - fx) * cq + fx * d);
+  };
+  out[((size_t(b) * 2 * H + oy) * Wo + ox) * C4 + c] =
+      make_float4(lerp2(v00.x, v01.x, v10.x, v11.x), lerp2(v00.y, v01.y, v10.y, v11.y),
+                  lerp2(v00.z, v01.z, v10.z, v11.z), lerp2(v00.w, v01.w, v10.w, v11.w));
 }
 
 // [h^2 Re r, h^2 Im r, kappa^2] NHWC (inc/precond.hpp:74-83, gamma dropped)
@@ -226,6 +380,28 @@ static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int 
   if (ca + cb != cw.cin) throw HbError{HB_ERR_ARG, "conv input channels mismatch"};
   if (launch_conv_tc(c, cw, B, act, H, W, a, ca, b, cb, b != nullptr && sb == 0, relu, out)) return;
   ConvArgs p{B, H, W, a, sa, ca, b, sb, cb, cw.dw.p, cw.db.p, cw.cout, relu, out, act};
+  const int cin = ca + cb;
+  if ((cw.cout == 16 || cw.cout == 2) && cin <= 40) {
+    const size_t smem =
+        (size_t(CS_TH + 2) * (CS_TW + 2) * size_t(cin | 1) + ((size_t(9) * cin * cw.cout + 3) & ~size_t(3))) * sizeof(float);
+    const dim3 g(((W + CS_TW - 1) / CS_TW) * ((H + CS_TH - 1) / CS_TH), 1, B);
+    NScope ns(c, PC_CONV, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
+    if (c.prof_detail)
+      c.prof_label = "conv_small " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
+                     std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
+    static bool attr = false;
+    if (!attr) {
+      HB_CUDA(cudaFuncSetAttribute(k_conv_small<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      HB_CUDA(cudaFuncSetAttribute(k_conv_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr = true;
+    }
+    if (cw.cout == 16)
+      k_conv_small<16><<<g, CS_NT, smem, c.stream>>>(p);
+    else
+      k_conv_small<2><<<g, CS_NT, smem, c.stream>>>(p);
+    HB_CUDA(cudaGetLastError());
+    return;
+  }
   const dim3 grid(((W + CT_W - 1) / CT_W) * ((H + CT_H - 1) / CT_H), (cw.cout + CT_CO - 1) / CT_CO, B);
   NScope ns(c, PC_CONV, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   if (c.prof_detail)
@@ -237,6 +413,13 @@ static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int 
 
 static void maxpool(Context& c, int B, const int* act, int H, int W, int C, const float* in, float* out) {
   NScope ns(c, PC_NETIO);
+  if (C % 4 == 0) {
+    const int n = (W / 2) * (C / 4);
+    k_maxpool2_v4<<<dim3((n + 127) / 128, H / 2, B), 128, 0, c.stream>>>(H, W, C / 4, reinterpret_cast<const float4*>(in),
+                                                                          reinterpret_cast<float4*>(out), act);
+    HB_CUDA(cudaGetLastError());
+    return;
+  }
   k_maxpool2<<<dim3(grid1(size_t(H / 2) * (W / 2) * C), B), 256, 0, c.stream>>>(B, H, W, C, in, out, act);
   HB_CUDA(cudaGetLastError());
 }
@@ -244,6 +427,13 @@ static void maxpool(Context& c, int B, const int* act, int H, int W, int C, cons
 static void upsample(Context& c, int B, const int* act, int H, int W, int C, const float* in, long long sin_,
                      float* out) {
   NScope ns(c, PC_NETIO);
+  if (C % 4 == 0 && sin_ % 4 == 0) {
+    const int n = 2 * W * (C / 4);
+    k_upsample2_v4<<<dim3((n + 127) / 128, 2 * H, B), 128, 0, c.stream>>>(
+        H, W, C / 4, reinterpret_cast<const float4*>(in), sin_ / 4, reinterpret_cast<float4*>(out), act);
+    HB_CUDA(cudaGetLastError());
+    return;
+  }
   k_upsample2<<<dim3(grid1(size_t(4) * H * W * C), B), 256, 0, c.stream>>>(B, H, W, C, in, sin_, out, act);
   HB_CUDA(cudaGetLastError());
 }

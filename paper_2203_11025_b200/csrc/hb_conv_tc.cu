@@ -124,7 +124,10 @@ struct TcSources {
 
 struct TcParams {
   int B, H, W, cout, relu;
-  int ntile, nsplit;  // output channels per work item (N of the MMA), work items per pixel tile
+  int ntile, nsplit;  // output channels per work item (N of the MMA), output-channel blocks per pixel tile
+  int ksplit;         // K splits per (tile, block): > 1 writes raw partial sums to ws (bias/ReLU in the reduce)
+  int sps;            // stages per K split (every split non-empty)
+  float* ws;          // [ksplit][B*H*W][cout] partial sums
   int bw, bh;         // pixel box of one M tile
   TcSources s;
   const float* bias;
@@ -135,13 +138,16 @@ struct TcParams {
 
 // pipeline geometry chosen on the host (see launch_conv_tc)
 struct TcLayout {
-  int stages;     // smem ring depth
-  int G;          // K chunks per stage
-  int kcmax;      // widest chunk (16 | 32 channels)
-  int nslots;     // TMEM A-operand ring depth (one slot per stage)
+  int kcmax;      // widest channel chunk (16 | 32)
+  int nchunk;     // channel chunks over both sources
+  int CG;         // channel chunks per halo group
+  int nhbuf;      // halo group buffers (1 | 2)
+  int box_bytes;  // smem bytes per halo box (one channel chunk), 1024-aligned
+  int G;          // K entries per MMA stage (= per TMEM A slot); stages never straddle a group
+  int stages;     // weight ring depth (streamed weights)
+  int nslots;     // TMEM A-slot ring depth
   int nacc;       // accumulator buffers (1 | 2)
-  int ncat;       // 2-MMA 3xTF32 form (B = [W_hi ; W_lo])
-  int wres;       // all weights resident in smem (loaded once per CTA) instead of streamed per stage
+  int wres;       // all weights resident in smem (loaded once per CTA)
 };
 
 __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
@@ -173,78 +179,98 @@ __device__ __forceinline__ void umma_commit_elect(uint64_t* bar) {
       : "memory");
 }
 
-// Persistent CTA (one per SM), 10 warps:
-//   w0 TMA producer | w1 MMA issuer | w2..w9 A split smem -> TMEM | w10..w13 epilogue.
+// Persistent CTA (one per SM), 14 warps:
+//   w0 TMA producer | w1 MMA issuer | w2..w9 A build (smem halo -> TMEM) | w10..w13 epilogue.
 //
-// A K chunk = one tap x kc input channels of a 128-pixel tile.  The producer
-// TMA-loads the fp32 activations (a 4-D box whose out-of-range taps read
-// zeros = the padding) and the [W_hi ; W_lo] weight rows into a smem stage of
-// G chunks.  The converter warps own TMEM lanes 32*(warp%4).. (= tile pixels):
-// each thread reads its pixel's kc channels (swizzled rows, conflict-free),
-// splits x = hi + lo (hi = x with the 13 low mantissa bits cleared, lo = x -
-// hi, exact) and stores both into a TMEM slot.  The MMA thread then issues
-// kind::tf32 MMAs with A read from TMEM (no shared-memory A traffic) and B
-// from the smem stage:
-//   ncat (2N <= 64):  D[:, 0:2N] += A_hi [W_hi | W_lo];  D[:, 0:N] += A_lo W_hi
-//   otherwise:        D += A_hi W_hi + A_hi W_lo + A_lo W_hi
-// Accumulators are double-buffered in TMEM where the slot ring leaves room, so
-// tile t's epilogue (TMEM -> bias, ReLU -> NHWC) overlaps tile t+1's MMAs.
-// The K schedule (tap, source, channel chunk -> TMA coordinates) is tabulated
-// in shared memory once per CTA: the producer and MMA threads are serial
-// single-thread loops where integer division costs more than a 16-channel
-// chunk's data movement.
-constexpr int TC_MAX_CHUNKS = 256;
+// An M tile is a bh x bw box of 128 output pixels of one image.  Its input is
+// loaded ONCE per channel chunk as a TMA box of (bh+2) x (bw+2) pixels at
+// (y0-1, x0-1): out-of-range rows/columns read zeros, which is the conv
+// padding, and the 9 taps are 9 shifted views of that halo tile (an implicit
+// GEMM that does not re-read the input per tap).  Channel chunks are grouped
+// so a group's halo boxes fit a smem buffer (double-buffered when they fit).
+//
+// K is ordered (group, tap, chunk of the group); one K entry = one tap x kc
+// input channels.  The A-build warps own TMEM lanes 32*(warp%4).. (= tile
+// pixels): each thread reads its shifted halo pixel's kc channels (swizzled
+// rows, conflict-free), splits x = hi + lo (hi = x with the 13 low mantissa
+// bits cleared, lo = x - hi, exact) and stores both into a TMEM slot.  The MMA
+// thread issues kind::tf32 MMAs with A read from TMEM and B = [W_hi ; W_lo]
+// (2N rows) from smem, accumulating
+//   D[:, 0:2N]  += A_hi [W_hi | W_lo]      D[:, N:2N] += A_lo W_hi
+// so the small 3xTF32 terms sum apart from A_hi W_hi (the epilogue adds the
+// halves).  Weights are resident in smem for small layers, else streamed per
+// stage.  Accumulators are double-buffered in TMEM where the slot ring leaves
+// room, so tile t's epilogue (TMEM -> bias, ReLU -> NHWC) overlaps tile t+1.
+// All schedules are tabulated in shared memory once per CTA: the producer and
+// MMA loops are serial, and integer division there costs more than a
+// 16-channel chunk's data movement.
+constexpr int TC_MAX_CHUNKS = 320;  // K entries per tile (9 x channel chunks)
 constexpr int TC_MAX_SLOTS = 8;
+constexpr int TC_DYN_SMEM = 216 * 1024;  // + ~8 KB of static tables/barriers <= 227 KB
 
-template <int KC, int NCAT>  // KC: uniform chunk width (16 | 32) or 0 = mixed; NCAT: -1 = runtime
+template <int KC>  // uniform chunk width (16 | 32), or 0 = mixed-width sources
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapWh32, const __grid_constant__ CUtensorMap mapWl32,
               const __grid_constant__ CUtensorMap mapWh16, const __grid_constant__ CUtensorMap mapWl16, TcParams p,
               TcLayout lay, int dbg) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  __shared__ uint64_t bar_full[TC_MAX_STAGES], bar_empty[TC_MAX_STAGES];
-  __shared__ uint64_t bar_afull[TC_MAX_SLOTS], bar_aempty[TC_MAX_SLOTS];
+  __shared__ uint64_t bar_full[TC_MAX_STAGES], bar_empty[TC_MAX_STAGES];  // weight ring
+  __shared__ uint64_t bar_hfull[2], bar_hempty[2];                         // halo group buffers
+  __shared__ uint64_t bar_afull[TC_MAX_SLOTS], bar_aempty[TC_MAX_SLOTS];   // TMEM A slots
   __shared__ uint64_t bar_tfull[2], bar_tempty[2], bar_w;
   __shared__ uint32_t tmem_slot;
-  __shared__ int4 sched[TC_MAX_CHUNKS];       // per K chunk: {flags, ci0, kglob, kc}
-  __shared__ uint32_t sbytes[TC_MAX_CHUNKS];  // per stage: TMA bytes
+  __shared__ int4 sched[TC_MAX_CHUNKS];  // per K entry: {chunk-in-group | tap << 8, chunk, kglob, kc}
+  __shared__ int2 stg[TC_MAX_CHUNKS];    // per stage: {kb0 | kb1 << 16, group | last stage of group << 16}
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = p.ntile;  // output channels of this CTA's work items; p.cout = row stride of out
-  const int stages = lay.stages, G = lay.G, kcmax = KC ? KC : lay.kcmax, nslots = lay.nslots;
-  const bool ncat = NCAT >= 0 ? NCAT != 0 : lay.ncat != 0;
-  const int accw = ncat ? 2 * N : N;          // TMEM columns per accumulator buffer [main | correction]
-  const int slot_cols = G * 2 * kcmax;        // TMEM columns per A slot: G x [hi | lo]
-  const int slot0 = lay.nacc * accw;          // first A-slot column
+  const int G = lay.G, kcmax = KC ? KC : lay.kcmax, nslots = lay.nslots, stages = lay.stages;
+  const int CG = lay.CG, nhbuf = lay.nhbuf, nchunk = lay.nchunk;
+  const int accw = 2 * N;                // TMEM columns per accumulator buffer [main | correction]
+  const int slot_cols = G * 2 * kcmax;   // TMEM columns per A slot: G x [hi | lo]
+  const int slot0 = lay.nacc * accw;     // first A-slot column
   const int tiles_x = p.W / p.bw, tiles_y = p.H / p.bh;
-  const int ntiles = p.B * tiles_x * tiles_y * p.nsplit;
+  const int ntiles = p.B * tiles_x * tiles_y * p.nsplit * p.ksplit;
+  const int hw = p.bw + 2;               // halo tile row pitch (pixels)
   // 1024-align by offset (not by integer cast) so the compiler keeps the shared address space
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  // a stage holds G consecutive K chunks: A[G] then [W_hi ; W_lo][G]
-  const int a_bytes = TC_M * kcmax * 4, w_bytes = 2 * N * kcmax * 4;
+  const int w_bytes = 2 * N * kcmax * 4;  // one K entry of [W_hi ; W_lo]
   const bool wres = lay.wres != 0;
-  const int stage_bytes = G * (a_bytes + (wres ? 0 : w_bytes));
-  unsigned char* wbase = base + stages * stage_bytes;  // resident weights: chunk kb at wbase + kb * w_bytes
-  auto sA = [&](int s, int g) { return base + s * stage_bytes + g * a_bytes; };
-  auto sW = [&](int s, int g) { return base + s * stage_bytes + G * a_bytes + g * w_bytes; };
+  const int hbuf_bytes = CG * lay.box_bytes;
+  unsigned char* wbase = base + nhbuf * hbuf_bytes;  // resident weights (entry kb) or the weight ring
+  const int wstage_bytes = G * w_bytes;
+  const int nca = p.s.ca / p.s.kca;
   const int cin = p.s.ca + p.s.cb;
-  const int nchunk_a = p.s.ca / p.s.kca, nchunk_b = p.s.cb ? p.s.cb / p.s.kcb : 0;
-  const int per_tap = nchunk_a + nchunk_b;
-  const int nk = 9 * per_tap;
-  const int nst = (nk + G - 1) / G;  // stage iterations per tile
-  const bool mixed = KC == 0;
+  const int ngrp = (nchunk + CG - 1) / CG;
+  const int spg = (9 * CG + G - 1) / G;  // stages of a full group
+  const int cg_last = nchunk - (ngrp - 1) * CG;
+  const int nst = (ngrp - 1) * spg + (9 * cg_last + G - 1) / G;
+  const int nk = 9 * nchunk;
   for (int kb = threadIdx.x; kb < nk; kb += blockDim.x) {
-    const int tap = kb / per_tap, r = kb - tap * per_tap;
-    const bool srcb = r >= nchunk_a;
+    const int g = kb / (9 * CG), r = kb - g * 9 * CG;
+    const int cgn = min(CG, nchunk - g * CG);
+    const int tap = r / cgn, j = r - tap * cgn;
+    const int ch = g * CG + j;
+    const bool srcb = ch >= nca;
     const int kc = srcb ? p.s.kcb : p.s.kca;
-    const int ci0 = srcb ? (r - nchunk_a) * kc : r * kc;
-    sched[kb] = make_int4(int(srcb) | ((tap % 3) << 2) | ((tap / 3) << 4), ci0, tap * cin + (srcb ? p.s.ca : 0) + ci0,
-                          kc);
+    const int cglob = srcb ? p.s.ca + (ch - nca) * kc : ch * kc;
+    sched[kb] = make_int4(j | (tap << 8), ch, tap * cin + cglob, kc);
+  }
+  for (int st = threadIdx.x; st < nst; st += blockDim.x) {
+    const int g = min(st / spg, ngrp - 1), ls = st - g * spg;
+    const int cgn = min(CG, nchunk - g * CG);
+    const int gend = 9 * g * CG + 9 * cgn;
+    const int kb0 = 9 * g * CG + ls * G, kb1 = min(kb0 + G, gend);
+    stg[st] = make_int2(kb0 | (kb1 << 16), g | ((kb1 == gend ? 1 : 0) << 16));
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; ++s) {
       mbar_init(&bar_full[s], 1);
-      mbar_init(&bar_empty[s], wres ? 256 : 256 + 1);  // converter threads (A read) [+ MMA commit (W read)]
+      mbar_init(&bar_empty[s], 1);
+    }
+    for (int h = 0; h < 2; ++h) {
+      mbar_init(&bar_hfull[h], 1);
+      mbar_init(&bar_hempty[h], 256);
     }
     for (int j = 0; j < nslots; ++j) {
       mbar_init(&bar_afull[j], 256);
@@ -265,17 +291,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  for (int st = threadIdx.x; st < nst; st += blockDim.x) {
-    uint32_t bytes = 0;
-    for (int kb = st * G; kb < min(nk, st * G + G); ++kb) bytes += uint32_t((TC_M + (wres ? 0 : 2 * N)) * sched[kb].w * 4);
-    sbytes[st] = (dbg & 8) ? 0u : bytes;
-  }
-  __syncthreads();
   const uint32_t tmem_base = tmem_slot;
 
-  // work item -> (image, pixel box, output-channel block n0)
-  int n0 = 0;
+  // work item -> (image, pixel box, output-channel block n0, K split: stages [s0, s1))
+  int n0 = 0, ks = 0, s0 = 0, s1 = 0;
+  const int sps = p.ksplit > 1 ? p.sps : nst;
   auto tile_coords = [&](int item, int& b, int& y0, int& x0) {
+    ks = item % p.ksplit;
+    s0 = ks * sps;
+    s1 = min(nst, s0 + sps);
+    item /= p.ksplit;
     n0 = (item % p.nsplit) * N;
     const int tile = item / p.nsplit;
     b = tile / (tiles_x * tiles_y);
@@ -283,45 +308,59 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     x0 = (tile % tiles_x) * p.bw;
   };
 
-  if ((dbg & 16) && warp != 1) {
-    // debug: everything but the MMA issuer idles
-  } else if (warp == 0) {
-    {  // ---------------- TMA producer (whole warp, elected lane issues)
-      int s = 0;
-      uint32_t ph = 0;
-      int it = 0;
-      if (wres) {  // the whole [W_hi ; W_lo] schedule, once
-        uint32_t wb = 0;
-        for (int kb = 0; kb < nk; ++kb) wb += uint32_t(2 * N * sched[kb].w * 4);
-        mbar_expect_tx_elect(&bar_w, (dbg & 8) ? 0u : wb);
-        for (int kb = 0; kb < nk && !(dbg & 8); ++kb) {
-          const int4 e = sched[kb];
-          const int kc = KC ? KC : e.w;
-          unsigned char* w = wbase + kb * w_bytes;
-          tma_load_2d_elect(w, kc == 32 ? &mapWh32 : &mapWh16, &bar_w, e.z, 0);
-          tma_load_2d_elect(w + N * kc * 4, kc == 32 ? &mapWl32 : &mapWl16, &bar_w, e.z, 0);
-        }
+  if (warp == 0) {
+    // ---------------- producer (whole warp, elected lane issues)
+    int s = 0, it = 0, hb = 0, hit = 0;
+    uint32_t ph = 0, hph = 0;
+    if (wres) {  // the whole [W_hi ; W_lo] schedule, once
+      uint32_t wb = 0;
+      for (int kb = 0; kb < nk; ++kb) wb += uint32_t(2 * N * sched[kb].w * 4);
+      mbar_expect_tx_elect(&bar_w, (dbg & 8) ? 0u : wb);
+      for (int kb = 0; kb < nk && !(dbg & 8); ++kb) {
+        const int4 e = sched[kb];
+        const int kc = KC ? KC : e.w;
+        unsigned char* w = wbase + kb * w_bytes;
+        tma_load_2d_elect(w, kc == 32 ? &mapWh32 : &mapWh16, &bar_w, e.z, 0);
+        tma_load_2d_elect(w + N * kc * 4, kc == 32 ? &mapWl32 : &mapWl16, &bar_w, e.z, 0);
       }
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int b, y0, x0;
-        tile_coords(tile, b, y0, x0);
-        if (p.act && !p.act[b]) continue;
-        const int bb = p.s.b_is_ctx ? 0 : b;
-        for (int st = 0, kb = 0; st < nst; ++st, ++it) {
-          if (it >= stages) mbar_wait(&bar_empty[s], ph ^ 1);
+    }
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int b, y0, x0;
+      tile_coords(tile, b, y0, x0);
+      if (p.act && !p.act[b]) continue;
+      const int bb = p.s.b_is_ctx ? 0 : b;
+      for (int st = s0; st < s1; ++st) {
+        const int2 sg2 = stg[st];
+        const int4 sg = make_int4(sg2.x & 0xffff, sg2.x >> 16, sg2.y & 0xffff, sg2.y >> 16);
+        if (sg.x == 9 * sg.z * CG || st == s0) {  // first stage of a group (in this split): its halo boxes
+          if (hit >= nhbuf) mbar_wait(&bar_hempty[hb], hph ^ 1);
+          const int c0 = sg.z * CG, c1 = min(nchunk, c0 + CG);
+          uint32_t bytes = 0;
+          for (int ch = c0; ch < c1; ++ch) bytes += uint32_t((ch >= nca ? p.s.kcb : p.s.kca) * 4 * hw * (p.bh + 2));
           if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 4 + 0] = clock64();
-          mbar_expect_tx_elect(&bar_full[s], sbytes[st]);
-          for (int g = 0; g < G && kb < nk; ++g, ++kb) {
-            if (dbg & 8) continue;
-            const int4 e = sched[kb];
-            const int kx = (e.x >> 2) & 3, ky = e.x >> 4;
-            const int kc = KC ? KC : e.w;
-            if (!(e.x & 1))
-              tma_load_4d_elect(sA(s, g), &mapA, &bar_full[s], e.y, x0 + kx - 1, y0 + ky - 1, b);
+          mbar_expect_tx_elect(&bar_hfull[hb], (dbg & 8) ? 0u : bytes);
+          for (int ch = c0; ch < c1 && !(dbg & 8); ++ch) {
+            unsigned char* dst = base + hb * hbuf_bytes + (ch - c0) * lay.box_bytes;
+            if (ch < nca)
+              tma_load_4d_elect(dst, &mapA, &bar_hfull[hb], ch * p.s.kca, x0 - 1, y0 - 1, b);
             else
-              tma_load_4d_elect(sA(s, g), &mapB, &bar_full[s], e.y, x0 + kx - 1, y0 + ky - 1, bb);
-            if (wres) continue;
-            unsigned char* w = sW(s, g);
+              tma_load_4d_elect(dst, &mapB, &bar_hfull[hb], (ch - nca) * p.s.kcb, x0 - 1, y0 - 1, bb);
+          }
+          if (++hb == nhbuf) {
+            hb = 0;
+            hph ^= 1;
+          }
+          ++hit;
+        }
+        if (!wres) {  // this stage's weights
+          if (it >= stages) mbar_wait(&bar_empty[s], ph ^ 1);
+          uint32_t wb = 0;
+          for (int kb = sg.x; kb < sg.y; ++kb) wb += uint32_t(2 * N * sched[kb].w * 4);
+          mbar_expect_tx_elect(&bar_full[s], (dbg & 8) ? 0u : wb);
+          for (int kb = sg.x; kb < sg.y && !(dbg & 8); ++kb) {
+            const int4 e = sched[kb];
+            const int kc = KC ? KC : e.w;
+            unsigned char* w = wbase + s * wstage_bytes + (kb - sg.x) * w_bytes;
             tma_load_2d_elect(w, kc == 32 ? &mapWh32 : &mapWh16, &bar_full[s], e.z, n0);
             tma_load_2d_elect(w + N * kc * 4, kc == 32 ? &mapWl32 : &mapWl16, &bar_full[s], e.z, n0);
           }
@@ -329,112 +368,106 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             s = 0;
             ph ^= 1;
           }
+          ++it;
         }
       }
     }
   } else if (warp == 1) {
-    {  // ---------------- MMA issuer (whole warp, elected lane issues)
-      // B descriptors as (lo, hi) words: lo = start >> 4 | LBO, hi = SBO |
-      // version | layout; chunk and K-step offsets are 32-bit adds on lo (the
-      // 14-bit start field never carries for smem < 256 KB)
-      const uint32_t idN = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
-      const uint32_t id2N = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t((2 * N) >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
-      const uint32_t hi32 = (1024u >> 4) | (1u << 14) | (2u << 29);  // 128-B rows, SWIZZLE_128B
-      const uint32_t hi16 = (512u >> 4) | (1u << 14) | (4u << 29);   // 64-B rows, SWIZZLE_64B
-      const uint32_t lo0 = (smem_u32(base) >> 4) | (1u << 16);
-      const uint32_t st16 = uint32_t(stage_bytes) >> 4, w16 = uint32_t(w_bytes) >> 4;
-      // warp-uniform copies (shfl from lane 0 lets the compiler keep them in uniform registers)
-      const uint32_t tbase = __shfl_sync(0xffffffff, tmem_base, 0);
-      const uint32_t lo0u = __shfl_sync(0xffffffff, lo0, 0);
-      const uint32_t wlo0 = __shfl_sync(0xffffffff, (smem_u32(wbase) >> 4) | (1u << 16), 0);
-      if (wres) mbar_wait(&bar_w, 0);
-      int s = 0, j = 0;
-      uint32_t ph = 0, aph = 0;
-      int tl = 0;  // local tile counter
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int b, y0, x0;
-        tile_coords(tile, b, y0, x0);
-        if (p.act && !p.act[b]) continue;
-        const int acc = lay.nacc == 2 ? (tl & 1) : 0;
-        const uint32_t tmem_d = tbase + uint32_t(acc * accw);
-        if (dbg & 16) {
-        } else if (lay.nacc == 2) {
-          if (tl >= 2) mbar_wait(&bar_tempty[acc], ((tl >> 1) - 1) & 1);  // epilogue drained this buffer
-        } else if (tl >= 1) {
-          mbar_wait(&bar_tempty[0], (tl - 1) & 1);
-        }
-        tc_fence_after();
-        uint32_t first = 0;  // accumulate flag: 0 only for the tile's first MMA
-        for (int st = 0, kb = 0; st < nst; ++st) {
-          if (!(dbg & 16)) {
-            if (!wres) mbar_wait(&bar_full[s], ph);  // W in smem
-            mbar_wait(&bar_afull[j], aph);           // A hi/lo in TMEM
-          }
-          tc_fence_after();
-          if (p.trace && blockIdx.x == 0 && lane == 0 && tl * nst + st < 64) p.trace[(tl * nst + st) * 4 + 2] = clock64();
-          uint32_t lW = wres ? wlo0 + uint32_t(kb) * w16 : lo0u + uint32_t(s) * st16 + (uint32_t(G * a_bytes) >> 4);
-          uint32_t ta = tbase + uint32_t(slot0 + j * slot_cols);
-          for (int g = 0; g < G && kb < nk; ++g, ++kb, lW += w16, ta += uint32_t(2 * kcmax)) {
-            const int kc = mixed ? sched[kb].w : kcmax;
-            if (dbg & 1) continue;
-            const uint32_t hi = kc == 32 ? hi32 : hi16;
-            const uint32_t lWl = lW + uint32_t((N * kc * 4) >> 4);
-            const uint32_t tal = ta + uint32_t(kc);
-#pragma unroll
-            for (int k = 0; k < kc / 8; ++k) {
-              if (ncat) {  // small terms accumulate apart from A_hi W_hi: D[:, N:2N] = A_hi W_lo + A_lo W_hi
-                umma_ts(tmem_d, ta + 8 * k, lW + 2 * k, hi, id2N, first);
-                umma_ts(tmem_d + uint32_t(N), tal + 8 * k, lW + 2 * k, hi, idN, 1u);
-              } else {
-                umma_ts(tmem_d, ta + 8 * k, lW + 2 * k, hi, idN, first);
-                umma_ts(tmem_d, ta + 8 * k, lWl + 2 * k, hi, idN, 1u);
-                umma_ts(tmem_d, tal + 8 * k, lW + 2 * k, hi, idN, 1u);
-              }
-              first = 1;
-            }
-          }
-          if (!(dbg & 16)) {
-            if (!wres) umma_commit_elect(&bar_empty[s]);  // W stage free once these MMAs completed
-            umma_commit_elect(&bar_aempty[j]);  // A slot free likewise
-          }
-          if (++s == stages) {
-            s = 0;
-            ph ^= 1;
-          }
-          if (++j == nslots) {
-            j = 0;
-            aph ^= 1;
-          }
-        }
-        if (!(dbg & 16)) umma_commit_elect(&bar_tfull[acc]);
-        ++tl;
-      }
-    }
-  } else if (warp < 10) {
-    // ---------------- warps 2..9: A chunk (smem, fp32) -> TMEM slot [hi | lo];
-    // two warps per TMEM lane quarter, taking alternate chunks of a stage
-    const int q = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int r = 32 * q + lane;  // tile pixel row = TMEM lane
+    // ---------------- MMA issuer (whole warp, elected lane issues)
+    // B descriptors as (lo, hi) words: lo = start >> 4 | LBO, hi = SBO |
+    // version | layout; entry and K-step offsets are 32-bit adds on lo (the
+    // 14-bit start field never carries for smem < 256 KB)
+    const uint32_t idN = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
+    const uint32_t id2N = (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t((2 * N) >> 3) << 17) | (uint32_t(TC_M >> 4) << 24);
+    const uint32_t hi32 = (1024u >> 4) | (1u << 14) | (2u << 29);  // 128-B rows, SWIZZLE_128B
+    const uint32_t hi16 = (512u >> 4) | (1u << 14) | (4u << 29);   // 64-B rows, SWIZZLE_64B
+    // warp-uniform copies (shfl from lane 0 lets the compiler keep them in uniform registers)
+    const uint32_t tbase = __shfl_sync(0xffffffff, tmem_base, 0);
+    const uint32_t wlo0 = __shfl_sync(0xffffffff, (smem_u32(wbase) >> 4) | (1u << 16), 0);
+    const uint32_t w16 = uint32_t(w_bytes) >> 4, ws16 = uint32_t(wstage_bytes) >> 4;
+    if (wres) mbar_wait(&bar_w, 0);
     int s = 0, j = 0;
     uint32_t ph = 0, aph = 0;
-    int itc = 0;
+    int tl = 0;  // local tile counter
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int b, y0, x0;
       tile_coords(tile, b, y0, x0);
       if (p.act && !p.act[b]) continue;
-      for (int st = 0, kb = 0; st < nst; ++st, ++itc) {
-        mbar_wait(&bar_full[s], ph);
+      const int acc = lay.nacc == 2 ? (tl & 1) : 0;
+      const uint32_t tmem_d = tbase + uint32_t(acc * accw);
+      if (lay.nacc == 2) {
+        if (tl >= 2) mbar_wait(&bar_tempty[acc], ((tl >> 1) - 1) & 1);  // epilogue drained this buffer
+      } else if (tl >= 1) {
+        mbar_wait(&bar_tempty[0], (tl - 1) & 1);
+      }
+      tc_fence_after();
+      uint32_t first = 0;  // accumulate flag: 0 only for the tile's first MMA
+      for (int st = s0; st < s1; ++st) {
+        const int2 sg2 = stg[st];
+        const int4 sg = make_int4(sg2.x & 0xffff, sg2.x >> 16, sg2.y & 0xffff, sg2.y >> 16);
+        if (!wres) mbar_wait(&bar_full[s], ph);  // weights in smem
+        mbar_wait(&bar_afull[j], aph);           // A hi/lo in TMEM
+        tc_fence_after();
+        if (p.trace && blockIdx.x == 0 && lane == 0 && tl * nst + st < 64) p.trace[(tl * nst + st) * 4 + 2] = clock64();
+        uint32_t lW = wres ? wlo0 + uint32_t(sg.x) * w16 : wlo0 + uint32_t(s) * ws16;
+        uint32_t ta = tbase + uint32_t(slot0 + j * slot_cols);
+        for (int kb = sg.x; kb < sg.y; ++kb, lW += w16, ta += uint32_t(2 * kcmax)) {
+          const int kc = KC ? KC : sched[kb].w;
+          if (dbg & 1) continue;
+          const uint32_t hi = kc == 32 ? hi32 : hi16;
+          const uint32_t tal = ta + uint32_t(kc);
+#pragma unroll
+          for (int k = 0; k < kc / 8; ++k) {
+            umma_ts(tmem_d, ta + 8 * k, lW + 2 * k, hi, id2N, first);
+            umma_ts(tmem_d + uint32_t(N), tal + 8 * k, lW + 2 * k, hi, idN, 1u);
+            first = 1;
+          }
+        }
+        if (!wres) umma_commit_elect(&bar_empty[s]);  // weight stage free once these MMAs completed
+        umma_commit_elect(&bar_aempty[j]);             // A slot free likewise
+        if (!wres && ++s == stages) {
+          s = 0;
+          ph ^= 1;
+        }
+        if (++j == nslots) {
+          j = 0;
+          aph ^= 1;
+        }
+      }
+      umma_commit_elect(&bar_tfull[acc]);
+      ++tl;
+    }
+  } else if (warp < 10) {
+    // ---------------- warps 2..9: A build, halo smem -> TMEM slot [hi | lo];
+    // two warps per TMEM lane quarter, taking alternate entries of a stage
+    const int q = warp & 3;
+    const int half = (warp - 2) >> 2;
+    const int r = 32 * q + lane;  // tile pixel = TMEM lane
+    const int yy = r / p.bw, xx = r - yy * p.bw;
+    int j = 0, hb = 0, itc = 0;
+    uint32_t aph = 0, hph = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      int b, y0, x0;
+      tile_coords(tile, b, y0, x0);
+      if (p.act && !p.act[b]) continue;
+      for (int st = s0; st < s1; ++st, ++itc) {
+        const int2 sg2 = stg[st];
+        const int4 sg = make_int4(sg2.x & 0xffff, sg2.x >> 16, sg2.y & 0xffff, sg2.y >> 16);
+        if (sg.x == 9 * sg.z * CG || st == s0) mbar_wait(&bar_hfull[hb], hph);
         if (itc >= nslots) mbar_wait(&bar_aempty[j], aph ^ 1);
         tc_fence_after();
         if (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && itc < 64) p.trace[itc * 4 + 1] = clock64();
+        const unsigned char* hbuf = base + hb * hbuf_bytes;
         uint32_t ta = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(slot0 + j * slot_cols);
-        for (int g = 0; g < G && kb < nk; ++g, ++kb, ta += uint32_t(2 * kcmax)) {
-          const int kc = mixed ? sched[kb].w : kcmax;
-          if ((dbg & 2) || (g & 1) != half) continue;
-          const unsigned char* row = sA(s, g) + r * (kc * 4);
-          // swizzled 16-B chunk c of row r sits at chunk c ^ f(r): SW128 f = r & 7, SW64 f = (r >> 1) & 3
-          const int f = kc == 32 ? (r & 7) : ((r >> 1) & 3);
+        for (int kb = sg.x; kb < sg.y; ++kb, ta += uint32_t(2 * kcmax)) {
+          if ((dbg & 2) || ((kb - sg.x) & 1) != half) continue;
+          const int4 e = sched[kb];
+          const int kc = KC ? KC : e.w;
+          const int tap = e.x >> 8, cj = e.x & 255;
+          const int hp = (yy + tap / 3) * hw + xx + tap % 3;  // shifted halo pixel
+          const unsigned char* row = hbuf + cj * lay.box_bytes + hp * (kc * 4);
+          // swizzled 16-B chunk c of smem row hp sits at c ^ f(hp): SW128 f = hp & 7, SW64 f = (hp >> 1) & 3
+          const int f = kc == 32 ? (hp & 7) : ((hp >> 1) & 3);
 #pragma unroll
           for (int h = 0; h < kc / 16; ++h) {
             uint32_t vh[16], vl[16];
@@ -443,25 +476,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const float4 x = *reinterpret_cast<const float4*>(row + (((4 * h + c) ^ f) << 4));
               const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const uint32_t hb = __float_as_uint(xs[e]) & 0xffffe000u;
-                vh[4 * c + e] = hb;
-                vl[4 * c + e] = __float_as_uint(xs[e] - __uint_as_float(hb));
+              for (int u = 0; u < 4; ++u) {
+                const uint32_t hbits = __float_as_uint(xs[u]) & 0xffffe000u;
+                vh[4 * c + u] = hbits;
+                vl[4 * c + u] = __float_as_uint(xs[u] - __uint_as_float(hbits));
               }
             }
             tmem_st16(ta + uint32_t(16 * h), vh);
             tmem_st16(ta + uint32_t(kc + 16 * h), vl);
           }
         }
-        mbar_arrive(&bar_empty[s]);  // this thread's smem reads are done (values are in registers)
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         tc_fence_before();
         mbar_arrive(&bar_afull[j]);
-        if (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && itc < 64) p.trace[itc * 4 + 3] = clock64();
-        if (++s == stages) {
-          s = 0;
-          ph ^= 1;
+        if (sg.w || st == s1 - 1) {  // group (or split) done: its halo buffer may be refilled
+          mbar_arrive(&bar_hempty[hb]);
+          if (++hb == nhbuf) {
+            hb = 0;
+            hph ^= 1;
+          }
         }
+        if (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && itc < 64) p.trace[itc * 4 + 3] = clock64();
         if (++j == nslots) {
           j = 0;
           aph ^= 1;
@@ -482,20 +517,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       tc_fence_after();
       const int row = 32 * q + lane;
       const int yy = row / p.bw, xx = row % p.bw;
-      float* orow = p.out + ((size_t(b) * p.H + (y0 + yy)) * p.W + (x0 + xx)) * p.cout + n0;
+      const size_t pix = (size_t(b) * p.H + (y0 + yy)) * p.W + (x0 + xx);
+      const bool part = p.ksplit > 1;  // raw partial sum; bias + ReLU after the K reduction
+      float* orow = (part ? p.ws + size_t(ks) * p.B * p.H * p.W * p.cout : p.out) + pix * p.cout + n0;
       const float* bias = p.bias + n0;
       const uint32_t trow = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * accw);
       for (int c0 = 0; c0 < ((dbg & 4) ? 0 : N); c0 += 16) {
         uint32_t v[16], u[16];
         tmem_ld16(trow + uint32_t(c0), v);
-        if (ncat) tmem_ld16(trow + uint32_t(N + c0), u);
+        tmem_ld16(trow + uint32_t(N + c0), u);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         float o[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          float x = __uint_as_float(v[i]) + __ldg(bias + c0 + i);
-          if (ncat) x += __uint_as_float(u[i]);
-          o[i] = p.relu ? fmaxf(x, 0.f) : x;
+          const float x = __uint_as_float(v[i]) + __uint_as_float(u[i]);
+          if (part) {
+            o[i] = x;
+          } else {
+            const float y = x + __ldg(bias + c0 + i);
+            o[i] = p.relu ? fmaxf(y, 0.f) : y;
+          }
         }
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
@@ -514,6 +555,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
+// split-K reduction: out = act(bias + sum_s ws[s]) in fixed order (deterministic)
+__global__ void k_conv_ksum(int ksplit, size_t n4, int cout4, size_t img4, const int* act, const float4* __restrict__ ws,
+                            const float4* __restrict__ bias, int relu, float4* __restrict__ out) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x) {
+    if (act && !act[i / img4]) continue;  // frozen column: its partials were not written
+    float4 a = __ldg(bias + (i % cout4));
+    for (int s = 0; s < ksplit; ++s) {
+      const float4 v = __ldg(ws + size_t(s) * n4 + i);
+      a.x += v.x;
+      a.y += v.y;
+      a.z += v.z;
+      a.w += v.w;
+    }
+    if (relu) a = make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
+    out[i] = a;
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -527,6 +586,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 // activation map: NHWC fp32 [B][H][W][C] as 4-D (C, W, H, B); box (kc, bw, bh, 1)
+// (the conv loads halo tiles: bw, bh include the 1-pixel border)
 CUtensorMap act_map(const float* ptr, int B, int H, int W, int C, int kc, int bw, int bh) {
   CUtensorMap m;
   const cuuint64_t dims[4] = {cuuint64_t(C), cuuint64_t(W), cuuint64_t(H), cuuint64_t(B)};
@@ -594,20 +654,73 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   if (cw.cout % 16 || cw.cout > 256 || cw.cout < 16) return false;
   const int bw = W < TC_M ? W : TC_M;
   const int bh = TC_M / bw;
-  if (W % bw || H % bh || bw * bh != TC_M || !cw.dwh.p) return false;
+  if (W % bw || H % bh || bw * bh != TC_M || bw < 8 || !cw.dwh.p) return false;
   const int kca = ca % 32 == 0 ? 32 : 16, kcb = cb ? (cb % 32 == 0 ? 32 : 16) : 32;
-  const CUtensorMap mA = act_map(a, B, H, W, ca, kca, bw, bh);
-  const CUtensorMap mB = cb ? act_map(bsrc, b_ctx ? 1 : B, H, W, cb, kcb, bw, bh) : mA;
-  const int K = 9 * cw.cin;
+  const int kcmax = (kca == 32 || (cb && kcb == 32)) ? 32 : 16;
+  const int nchunk = ca / kca + (cb ? cb / kcb : 0);
+  const int nk = 9 * nchunk;
+  if (nk > TC_MAX_CHUNKS) return false;
   // Cout > 128 is split into 128-channel work items so every layer uses the
   // split-accumulator form (correction terms summed apart, better accuracy)
   const int nsplit = cw.cout > 128 ? cw.cout / 128 : 1;
   const int ntile = cw.cout / nsplit;
   if (ntile * nsplit != cw.cout || ntile > 128) return false;
+
+  TcLayout lay{};
+  lay.kcmax = kcmax;
+  lay.nchunk = nchunk;
+  // TMEM (512 columns): accumulators [nacc x 2N] then A slots of G x [hi | lo] entries
+  const int accw = 2 * ntile;
+  lay.nacc = 2 * accw + 2 * (2 * 2 * kcmax) <= 512 ? 2 : 1;
+  const int free_cols = 512 - lay.nacc * accw;
+  if (free_cols < 2 * 2 * kcmax) return false;
+  lay.G = std::max(1, std::min(9, free_cols / (3 * 2 * kcmax)));  // aim for ~3 slots in flight
+  lay.nslots = std::min(TC_MAX_SLOTS, free_cols / (lay.G * 2 * kcmax));
+  if (lay.nslots < 2) return false;
+  // shared memory: halo group buffers, then resident weights or a weight ring
+  const int budget = TC_DYN_SMEM - 1024;
+  const int w_chunk = 2 * ntile * kcmax * 4;
+  lay.wres = nsplit == 1 && nk * w_chunk <= 96 * 1024 ? 1 : 0;
+  lay.stages = lay.wres ? 1 : 4;
+  lay.box_bytes = ((kcmax * 4 * (bw + 2) * (bh + 2)) + 1023) & ~1023;
+  auto wsmem = [&]() { return lay.wres ? nk * w_chunk : lay.stages * lay.G * w_chunk; };
+  for (;;) {
+    const int room = budget - wsmem();
+    lay.CG = std::min(nchunk, room / (2 * lay.box_bytes));
+    lay.nhbuf = 2;
+    if (lay.CG < 1) {
+      lay.CG = std::min(nchunk, room / lay.box_bytes);
+      lay.nhbuf = 1;
+    }
+    if (lay.CG >= 1 || lay.wres || lay.stages == 2) break;
+    --lay.stages;
+  }
+  if (lay.CG < 1) return false;
+  const int ngrp = (nchunk + lay.CG - 1) / lay.CG;
+  const int spg = (9 * lay.CG + lay.G - 1) / lay.G;
+  if (ngrp * spg > TC_MAX_CHUNKS) return false;
+  const size_t smem = size_t(lay.nhbuf) * lay.CG * lay.box_bytes + size_t(wsmem()) + 1024;
+
+  const CUtensorMap mA = act_map(a, B, H, W, ca, kca, bw + 2, bh + 2);
+  const CUtensorMap mB = cb ? act_map(bsrc, b_ctx ? 1 : B, H, W, cb, kcb, bw + 2, bh + 2) : mA;
+  const int K = 9 * cw.cin;
   const CUtensorMap wh32 = w_map(cw.dwh.p, cw.cout, K, 32, ntile), wl32 = w_map(cw.dwl.p, cw.cout, K, 32, ntile);
   const CUtensorMap wh16 = w_map(cw.dwh.p, cw.cout, K, 16, ntile), wl16 = w_map(cw.dwl.p, cw.cout, K, 16, ntile);
-  TcParams p{B,  H,  W,  cw.cout, relu, ntile, nsplit, bw, bh, TcSources{ca, cb, kca, kcb, b_ctx ? 1 : 0}, cw.db.p,
-             out, act, nullptr};
+  // split K when the pixel tiles alone cannot fill the SMs (low-resolution levels)
+  const int tiles0 = B * (H / bh) * (W / bw) * nsplit;
+  const int nst = (ngrp - 1) * spg + (9 * (nchunk - (ngrp - 1) * lay.CG) + lay.G - 1) / lay.G;
+  int ksplit = 1;
+  if (c.opt_conv_ksplit && tiles0 * 2 <= c.num_sms)
+    ksplit = std::max(1, std::min({nst, c.num_sms / tiles0, 8}));
+  const int sps = (nst + ksplit - 1) / ksplit;
+  ksplit = (nst + sps - 1) / sps;  // no empty split
+  float* ws = nullptr;
+  if (ksplit > 1) {
+    c.conv_ws.ensure(size_t(ksplit) * B * H * W * cw.cout);
+    ws = c.conv_ws.p;
+  }
+  TcParams p{B,  H,  W,     cw.cout, relu, ntile,   nsplit, ksplit, sps, ws, bw, bh,
+             TcSources{ca, cb, kca, kcb, b_ctx ? 1 : 0}, cw.db.p, out, act, nullptr};
   static const bool trace = getenv("HB_CONV_TRACE") != nullptr;
   static long long* dtrace = nullptr;
   if (trace) {
@@ -615,47 +728,18 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
     HB_CUDA(cudaMemsetAsync(dtrace, 0, 256 * sizeof(long long), c.stream));
     p.trace = dtrace;
   }
-  const int kcmax = (kca == 32 || (cb && kcb == 32)) ? 32 : 16;
-  if (9 * (ca / kca + (cb ? cb / kcb : 0)) > TC_MAX_CHUNKS) return false;
-  // TMEM (512 columns): accumulators [nacc x accw] then nslots A slots of G x [hi | lo] chunks
-  TcLayout lay{};
-  lay.kcmax = kcmax;
-  lay.ncat = 1;
-  const int accw = 2 * ntile;
-  lay.nacc = 2 * accw + 2 * (2 * 2 * kcmax) <= 512 ? 2 : 1;
-  const int free_cols = 512 - lay.nacc * accw;
-  if (free_cols < 2 * 2 * kcmax) return false;
-  const int nk = 9 * (ca / kca + (cb ? cb / kcb : 0));
-  const int w_chunk = 2 * ntile * kcmax * 4;
-  // small layers keep all weights resident (one TMA burst per CTA instead of
-  // two weight TMAs per chunk: TMA issue, not bytes, limits 16-channel layers)
-  lay.wres = nsplit == 1 && nk * w_chunk <= 96 * 1024 ? 1 : 0;
-  const int wres_bytes = lay.wres ? nk * w_chunk : 0;
-  const int chunk_bytes = TC_M * kcmax * 4 + (lay.wres ? 0 : w_chunk);
-  // a stage should carry enough tensor work to amortise its handshakes: aim
-  // for ~3 TMEM slots and <= 54 KB of smem per stage
-  lay.G = std::max(1, std::min({9, free_cols / (3 * 2 * kcmax), (54 * 1024) / chunk_bytes,
-                                 (220 * 1024 - 1024 - wres_bytes) / (3 * chunk_bytes)}));
-  lay.nslots = std::min(TC_MAX_SLOTS, free_cols / (lay.G * 2 * kcmax));
-  const int stage_bytes = lay.G * chunk_bytes;
-  lay.stages = TC_MAX_STAGES;
-  while (lay.stages > 2 && lay.stages * stage_bytes + wres_bytes + 1024 > 220 * 1024) --lay.stages;
-  if (lay.stages * stage_bytes + wres_bytes + 1024 > 220 * 1024 || lay.nslots < 2) return false;
-  const size_t smem = size_t(lay.stages) * stage_bytes + wres_bytes + 1024;
-  // instantiation: uniform chunk width and the 3xTF32 form as template arguments
-  // (fully unrolled issue loops); mixed-width sources take the generic one
+  // uniform chunk width as a template argument (fully unrolled issue loops);
+  // mixed-width sources take the generic instantiation
   const bool uni = !cb || kca == kcb;
   void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams, TcLayout, int) =
-      !uni ? k_conv_tc<0, -1>
-           : kcmax == 32 ? (lay.ncat ? k_conv_tc<32, 1> : k_conv_tc<32, 0>)
-                         : (lay.ncat ? k_conv_tc<16, 1> : k_conv_tc<16, 0>);
+      !uni ? k_conv_tc<0> : kcmax == 32 ? k_conv_tc<32> : k_conv_tc<16>;
   static int attr_dev = -1;
   if (attr_dev != c.device) {
-    for (auto k : {k_conv_tc<0, -1>, k_conv_tc<32, 1>, k_conv_tc<32, 0>, k_conv_tc<16, 1>, k_conv_tc<16, 0>})
-      HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    for (auto k : {k_conv_tc<0>, k_conv_tc<32>, k_conv_tc<16>})
+      HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
     attr_dev = c.device;
   }
-  const int tiles = B * (H / bh) * (W / bw) * nsplit;
+  const int tiles = tiles0 * ksplit;
   const int grid = std::min(tiles, c.num_sms);
   const int tok = prof_begin(c, PC_CONV);
   if (c.prof_detail)
@@ -663,6 +747,13 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
   static const int dbg = getenv("HB_CONV_DEBUG") ? atoi(getenv("HB_CONV_DEBUG")) : 0;
   kern<<<grid, TC_THREADS, smem, c.stream>>>(mA, mB, wh32, wl32, wh16, wl16, p, lay, dbg);
+  if (ksplit > 1) {
+    HB_CUDA(cudaGetLastError());
+    const size_t n4 = size_t(B) * H * W * cw.cout / 4;
+    k_conv_ksum<<<int(std::min<size_t>((n4 + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
+        ksplit, n4, cw.cout / 4, size_t(H) * W * cw.cout / 4, act, reinterpret_cast<const float4*>(ws), reinterpret_cast<const float4*>(cw.db.p), relu,
+        reinterpret_cast<float4*>(out));
+  }
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout),
            2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());
@@ -670,8 +761,11 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
     long long h[256];
     HB_CUDA(cudaStreamSynchronize(c.stream));
     HB_CUDA(cudaMemcpy(h, dtrace, sizeof(h), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "conv_tc %dx%dx%d %d+%d->%d G=%d stages=%d slots=%d nacc=%d ncat=%d wres=%d: it prod cvt_in mma cvt_out\n",
-            B, H, W, ca, cb, cw.cout, lay.G, lay.stages, lay.nslots, lay.nacc, lay.ncat, lay.wres);
+    fprintf(stderr,
+            "conv_tc %dx%dx%d %d+%d->%d G=%d slots=%d nacc=%d wres=%d stages=%d CG=%d nhbuf=%d box=%d ksplit=%d: it "
+            "prod cvt_in mma cvt_out\n",
+            B, H, W, ca, cb, cw.cout, lay.G, lay.nslots, lay.nacc, lay.wres, lay.stages, lay.CG, lay.nhbuf,
+            lay.box_bytes, ksplit);
     const long long t0 = h[0] ? h[0] : h[2];
     for (int i = 0; i < 64 && (h[i * 4] || h[i * 4 + 2]); ++i)
       fprintf(stderr, "  %2d %7lld %7lld %7lld %7lld\n", i, h[i * 4] - t0, h[i * 4 + 1] - t0, h[i * 4 + 2] - t0,

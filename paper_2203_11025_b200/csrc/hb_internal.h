@@ -224,7 +224,7 @@ struct Context {
   DBuf<float> pc_io, cn_io;
   DBuf<float2> pc_e0;
   // options
-  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true;
+  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {
@@ -238,6 +238,7 @@ struct Context {
   std::vector<GraphEntry> graphs;
   // net activations
   DBuf<float> net_act;       // arena
+  DBuf<float> conv_ws;       // split-K partial sums of the tensor-core conv
   std::vector<DBuf<float>> ctx_maps;  // encoder context per level (NHWC)
   bool ctx_valid = false;
   // profiling

@@ -10,6 +10,8 @@
 //
 //   down:  v = wD^-1 f ; r = f - M v ; fc(jy, jx) = sum_k W_k r(2j+o+k)
 //   up:    v = wD^-1 f + P_o vc ; z = v + wD^-1 (f - M v)
+#include <cstdlib>
+
 #include "hb_common.cuh"
 #include "hb_internal.h"
 
@@ -232,9 +234,11 @@ void launch_down_stream(Context& c, const LevelView& L, int offset, int B, const
   const int cnx = L.nx / 2, cny = L.ny / 2;
   const int tok = prof_begin(c, PC_DOWN);
   // rows per warp: enough warps to fill the machine, >= 4 coarse rows to amortise the halo
+  static const int env_d = getenv("HB_RPC_DOWN") ? atoi(getenv("HB_RPC_DOWN")) : 0;
   int rpc = 8;
   while (rpc > 4 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((cny + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
     rpc /= 2;
+  if (env_d) rpc = env_d;
   const int chunks = (cny + rpc - 1) / rpc;
   const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
   k_down_stream<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
@@ -245,9 +249,11 @@ void launch_down_stream(Context& c, const LevelView& L, int offset, int B, const
 void launch_up_stream(Context& c, const LevelView& L, int offset, int cnx, int cny, int B, const int* act,
                       const float2* f, const float* fscale, const float2* vc, float2* z) {
   const int tok = prof_begin(c, PC_UP);
+  static const int env_u = getenv("HB_RPC_UP") ? atoi(getenv("HB_RPC_UP")) : 0;
   int rpc = 16;
   while (rpc > 8 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((L.ny + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
     rpc /= 2;
+  if (env_u) rpc = env_u;
   const int chunks = (L.ny + rpc - 1) / rpc;
   const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
   k_up_stream<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, cnx, cny, rpc, act, f, fscale, vc, z);

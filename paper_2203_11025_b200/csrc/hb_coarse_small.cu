@@ -8,10 +8,15 @@
 // the 2j+1 inner products (MGS via the Gram recurrence) are reduced with one
 // warp reduce-scatter butterfly (62 shuffles for 32 complex slots) instead of
 // 5 shuffles per value.
+#include <cstdio>
+#include <cstdlib>
+
 #include "hb_common.cuh"
 #include "hb_internal.h"
 
 namespace hb {
+
+__device__ long long* g_coarse_trace = nullptr;
 
 namespace {
 
@@ -329,6 +334,269 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_small(LevelView L, int m, cons
   }
 }
 
+// Register-resident variant (N <= NT*NPT, m <= MAXK): each thread keeps its
+// NPT nodes of every basis vector in registers, so the inner products, the
+// Gram row and the basis update read no shared memory; only u_j = D^-1 V_j
+// goes through a zero-bordered smem tile for the stencil's neighbours (four
+// independent loads per node, no bounds branches).  Same arithmetic and
+// summation order as k_coarse_small (the MGS correction is fed from per-warp
+// smem broadcasts instead of double-precision shuffles).
+template <int NT, int NPT, int MAXK>
+__global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const int* act,
+                                                       const float2* __restrict__ f, float2* __restrict__ x) {
+  const int b = blockIdx.x;
+  if (act && !act[b]) return;
+  long long* const tr = (b == 0 && threadIdx.x == 0) ? g_coarse_trace : nullptr;  // HB_COARSE_TRACE
+  extern __shared__ float2 sU2[];  // 2 x (nx+2) x (ny+2) zero-bordered u_j = D^-1 V_j (double-buffered by j)
+  __shared__ SmallSmem S;
+  __shared__ double2 sHc[NT / 32][MAXK + 1], sGj[NT / 32][MAXK + 1];
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int nx = L.nx, ny = L.ny, N = nx * ny, px2 = nx + 2;
+  const float ih2 = L.inv_h2;
+  float2 V[MAXK + 1][NPT];
+  float2 d[NPT], di[NPT];
+  int ui[NPT];  // this node's index in the bordered tile
+  bool ok[NPT];
+  const int tile = (nx + 2) * (ny + 2);
+  for (int i = t; i < 2 * tile; i += NT) sU2[i] = make_float2(0.f, 0.f);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    const int p = t + q * NT;
+    ok[q] = p < N;
+    const int xq = ok[q] ? p % nx : 0, yq = ok[q] ? p / nx : 0;
+    ui[q] = (yq + 1) * px2 + xq + 1;
+    d[q] = ok[q] ? ld(L.dM, p) : make_float2(1.f, 0.f);
+    di[q] = crcp(d[q]);
+    V[0][q] = ok[q] ? ld(f + size_t(b) * N, p) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 1; i <= MAXK; ++i) V[i][q] = make_float2(0.f, 0.f);
+    if (ok[q]) sU2[ui[q]] = cmul(V[0][q], di[q]);
+  }
+  __syncthreads();
+  int k = m;
+  double hn_prev = 0.0;
+#pragma unroll 1
+  for (int j = 0; j <= m; ++j) {
+    if (tr && j < 16) tr[j * 8 + 0] = clock64();
+    const float2* sU = sU2 + (j & 1) * tile;
+    float2 w[NPT], vj[NPT];
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      vj[q] = V[0][q];
+#pragma unroll
+      for (int i = 1; i <= MAXK; ++i)
+        if (i == j) vj[q] = V[i][q];
+    }
+    float nrm_part = 0.f;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      nrm_part = fmaf(vj[q].x, vj[q].x, fmaf(vj[q].y, vj[q].y, nrm_part));
+      w[q] = make_float2(0.f, 0.f);
+      if (j == m || !ok[q]) continue;
+      // neighbours (zero border = out of range), same summation order as k_coarse_small
+      const float2 ul = sU[ui[q] - 1], ur = sU[ui[q] + 1], uu = sU[ui[q] - px2], ud = sU[ui[q] + px2];
+      const float2 nb = cadd(cadd(cadd(ul, ur), uu), ud);
+      float2 yv = cmul(d[q], cmul(vj[q], di[q]));
+      yv.x = fmaf(-ih2, nb.x, yv.x);
+      yv.y = fmaf(-ih2, nb.y, yv.y);
+      w[q] = yv;
+    }
+    float v[32];
+#pragma unroll
+    for (int s2 = 0; s2 < 32; ++s2) v[s2] = 0.f;
+    if (j < m) {
+#pragma unroll
+      for (int i = 0; i <= MAXK; ++i) {
+        if (i > j) break;
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) {
+          const float2 a = V[i][q], c = w[q];
+          v[2 * i] = fmaf(a.x, c.x, fmaf(a.y, c.y, v[2 * i]));
+          v[2 * i + 1] = fmaf(a.x, c.y, fmaf(-a.y, c.x, v[2 * i + 1]));
+        }
+      }
+    }
+    if (tr && j < 16) tr[j * 8 + 1] = clock64();
+    warp_reduce_scatter32(v);
+    S.part[warp][lane] = v[0];
+#pragma unroll
+    for (int s2 = 0; s2 < 32; ++s2) v[s2] = 0.f;
+    v[30] = nrm_part;
+    if (j < m) {
+#pragma unroll
+      for (int i = 0; i < MAXK; ++i) {
+        if (i >= j) break;
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) {
+          const float2 a = V[i][q], e = vj[q];
+          v[2 * i] = fmaf(e.x, a.x, fmaf(e.y, a.y, v[2 * i]));
+          v[2 * i + 1] = fmaf(e.x, a.y, fmaf(-e.y, a.x, v[2 * i + 1]));
+        }
+      }
+    }
+    warp_reduce_scatter32(v);
+    if (tr && j < 16) tr[j * 8 + 2] = clock64();
+    S.part[warp][32 + lane] = v[0];
+    __syncthreads();
+    if (tr && j < 16) tr[j * 8 + 3] = clock64();
+    double2 val = make_double2(0.0, 0.0);
+    {
+      const int f0 = lane < 16 ? 2 * lane : 32 + 2 * (lane - 16);
+      float px_[NT / 32], py_[NT / 32];
+#pragma unroll
+      for (int w2 = 0; w2 < NT / 32; ++w2) {
+        px_[w2] = S.part[w2][f0];
+        py_[w2] = S.part[w2][f0 + 1];
+      }
+#pragma unroll
+      for (int w2 = 0; w2 < NT / 32; ++w2) {
+        val.x += px_[w2];
+        val.y += py_[w2];
+      }
+    }
+    const double nrm = sqrt(__shfl_sync(0xffffffffu, val.x, 31));
+    if (j == 0) {
+      if (t == 0) S.beta0 = nrm;
+      if (nrm == 0.0) {
+        k = 0;
+        break;
+      }
+    } else {
+      const double hn = hn_prev * nrm;
+      if (t == 0) S.H[j - 1][j] = make_double2(hn, 0.0);
+      if (hn <= 1e-14 * S.beta0) {
+        k = j;
+        break;
+      }
+    }
+    const double sj = 1.0 / nrm;
+    if (t == 0) S.scale[j] = sj;
+    if (j == m) break;
+    hn_prev = sj;
+    const double si = (lane < j) ? S.scale[lane] : sj;
+    double2 hcgs = make_double2(0.0, 0.0);
+    if (lane <= j) hcgs = zscale(val, si * sj);
+    double2 gjk = make_double2(0.0, 0.0);
+    {
+      const double2 e = make_double2(__shfl_sync(0xffffffffu, val.x, (16 + lane) & 31),
+                                     __shfl_sync(0xffffffffu, val.y, (16 + lane) & 31));
+      if (lane < j) gjk = zscale(e, sj * S.scale[lane]);
+    }
+    // first-order MGS correction h_i -= sum_{k<i} hcgs_k G_ik, operands broadcast from this warp's smem rows
+    if (lane <= MAXK) {
+      sHc[warp][lane] = hcgs;
+      sGj[warp][lane] = gjk;
+    }
+    __syncwarp();
+    double2 h = hcgs;
+    if (lane <= j) {
+#pragma unroll
+      for (int kk = 0; kk < MAXK; ++kk) {
+        if (kk < lane) {
+          const double2 hk = sHc[warp][kk];
+          const double2 Gik = (lane == j) ? sGj[warp][kk] : S.G[lane][kk];
+          h = zsub(h, zmul(hk, Gik));
+        }
+      }
+    }
+    if (warp == 0) {
+      if (lane <= j) S.H[j][lane] = h;
+      if (lane < j) S.G[j][lane] = gjk;
+    }
+    if (tr && j < 16) tr[j * 8 + 4] = clock64();
+    const double2 cc = zscale(h, si / sj);
+    const float2 cf = make_float2(float(cc.x), float(cc.y));
+    float2 ci[MAXK + 1];
+#pragma unroll
+    for (int i = 0; i <= MAXK; ++i) ci[i] = make_float2(__shfl_sync(0xffffffffu, cf.x, i), __shfl_sync(0xffffffffu, cf.y, i));
+    float2 vn[NPT];
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      vn[q] = w[q];
+#pragma unroll
+      for (int i = 0; i <= MAXK; ++i)
+        if (i <= j) vn[q] = csub(vn[q], cmul(ci[i], V[i][q]));
+    }
+    if (tr && j < 16) tr[j * 8 + 5] = clock64();
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      if (!ok[q]) vn[q] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int i = 1; i <= MAXK; ++i)
+        if (i == j + 1) V[i][q] = vn[q];
+    }
+    // u_{j+1} into the other tile (its last readers, step j-1, passed barrier 1 of step j)
+    float2* sUn = sU2 + ((j + 1) & 1) * tile;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
+      if (ok[q]) sUn[ui[q]] = cmul(vn[q], di[q]);
+    __syncthreads();
+    if (tr && j < 16) tr[j * 8 + 6] = clock64();
+  }
+  if (k == 0) {
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
+      if (ok[q]) x[size_t(b) * N + t + q * NT] = make_float2(0.f, 0.f);
+    return;
+  }
+  __syncthreads();
+  if (t == 0) {
+    double* cs = S.cs;
+    double2* sn = S.sn;
+    double2* g = S.g;
+    for (int i = 0; i <= k; ++i) g[i] = make_double2(0.0, 0.0);
+    g[0] = make_double2(S.beta0, 0.0);
+    for (int j = 0; j < k; ++j) {
+      double2* hj = S.H[j];
+      for (int i = 0; i < j; ++i) {
+        const double2 t1 = dadd(zscale(hj[i], cs[i]), zmul(sn[i], hj[i + 1]));
+        hj[i + 1] = dadd(zscale(zmul(zconj(sn[i]), hj[i]), -1.0), zscale(hj[i + 1], cs[i]));
+        hj[i] = t1;
+      }
+      const double2 a = hj[j];
+      const double hn = hj[j + 1].x;
+      const double a2 = a.x * a.x + a.y * a.y;
+      if (a2 + hn * hn == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = make_double2(0.0, 0.0);
+      } else if (a2 == 0.0) {
+        cs[j] = 0.0;
+        sn[j] = make_double2(1.0, 0.0);
+      } else {
+        const double ia = rsqrt(a2), ir = rsqrt(a2 + hn * hn);
+        cs[j] = a2 * ia * ir;
+        sn[j] = zscale(a, hn * ia * ir);
+      }
+      hj[j] = dadd(zscale(hj[j], cs[j]), zmul(sn[j], hj[j + 1]));
+      hj[j + 1] = make_double2(0.0, 0.0);
+      g[j + 1] = zscale(zmul(zconj(sn[j]), g[j]), -1.0);
+      g[j] = zscale(g[j], cs[j]);
+    }
+    for (int i = k - 1; i >= 0; --i) {
+      double2 sum = g[i];
+      for (int l = i + 1; l < k; ++l) sum = zsub(sum, zmul(S.H[l][i], S.y[l]));
+      const double2 dd = S.H[i][i];
+      const double inv = 1.0 / (dd.x * dd.x + dd.y * dd.y);
+      S.y[i] = zscale(zmul(sum, zconj(dd)), inv);
+    }
+    for (int i = 0; i < k; ++i) {
+      const double2 c = zscale(S.y[i], S.scale[i]);
+      S.coef[i] = make_float2(float(c.x), float(c.y));
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    if (!ok[q]) continue;
+    float2 u = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < MAXK; ++i)
+      if (i < k) u = cadd(u, cmul(S.coef[i], V[i][q]));
+    x[size_t(b) * N + t + q * NT] = cmul(u, di[q]);
+  }
+}
+
 }  // namespace
 
 bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
@@ -350,7 +618,15 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
   }
   const int tok = prof_begin(c, PC_COARSE);
   const int nt = c.coarse_threads;
-  if (nt == 1024 && N <= 1024) {
+  static bool reg_attr = false;
+  if (c.opt_coarse_reg && iters <= 10 && N <= 1024 && nt == 256) {
+    if (!reg_attr) {
+      HB_CUDA(cudaFuncSetAttribute(k_coarse_reg<256, 4, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      reg_attr = true;
+    }
+    const size_t su = 2 * sizeof(float2) * size_t(L.nx + 2) * (L.ny + 2);
+    k_coarse_reg<256, 4, 10><<<B, 256, su, c.stream>>>(L, iters, act, f, x);
+  } else if (nt == 1024 && N <= 1024) {
     k_coarse_small<1024, 1, 15><<<B, 1024, smem, c.stream>>>(L, iters, act, f, x);
   } else if (nt >= 512 && N <= 1024) {
     k_coarse_small<512, 2, 15><<<B, 512, smem, c.stream>>>(L, iters, act, f, x);
@@ -365,6 +641,25 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
   }
   prof_end(c, PC_COARSE, tok, double(B) * N * 16.0 + double(N) * 8.0, 0);  // f in, x out; diag
   HB_CUDA(cudaGetLastError());
+  static const bool trace = getenv("HB_COARSE_TRACE") != nullptr;
+  static long long* dtr = nullptr;
+  static int ntr = 0;
+  if (trace && ntr < 3) {
+    if (!dtr) {
+      HB_CUDA(cudaMalloc(&dtr, 16 * 8 * sizeof(long long)));
+      HB_CUDA(cudaMemcpyToSymbol(g_coarse_trace, &dtr, sizeof(dtr)));
+    }
+    long long h[128];
+    HB_CUDA(cudaStreamSynchronize(c.stream));
+    HB_CUDA(cudaMemcpy(h, dtr, sizeof(h), cudaMemcpyDeviceToHost));
+    if (++ntr == 3) {
+      fprintf(stderr, "coarse trace (cycles from step start): start acc bfly bar1 scalar update bar2\n");
+      for (int j = 0; j <= iters && j < 16; ++j)
+        fprintf(stderr, "  j=%2d %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", j, 0ll, h[j * 8 + 1] - h[j * 8],
+                h[j * 8 + 2] - h[j * 8], h[j * 8 + 3] - h[j * 8], h[j * 8 + 4] - h[j * 8], h[j * 8 + 5] - h[j * 8],
+                h[j * 8 + 6] - h[j * 8]);
+    }
+  }
   return true;
 }
 

@@ -224,7 +224,8 @@ struct Context {
   DBuf<float> pc_io, cn_io;
   DBuf<float2> pc_e0;
   // options
-  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true;
+  bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
+       opt_coarse_reg = true;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {

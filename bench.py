@@ -373,7 +373,8 @@ def fixed_budget(name, local, args, ws, rank):
     ctx, arr = problems.gpu_setup(cfg, device=local)
     Bh = np.ascontiguousarray(problems.rhs_block(arr)[cols])
     nb = Bh.shape[0]
-    kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=args.budget, rel_tol=1e-6)
+    budget = {"c3": max(2, args.budget // 5), "c2": max(2, args.budget // 2)}.get(name, args.budget)
+    kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=budget, rel_tol=1e-6)
     dev = torch.device("cuda", local)
     dB = torch.from_numpy(Bh).to(dev)
     dX = torch.zeros_like(dB)
@@ -392,15 +393,32 @@ def fixed_budget(name, local, args, ws, rank):
     dX.zero_()
     ctx.fgmres_device(cfg["precond"], dB.data_ptr(), dX.data_ptr(), nb, kc, want_report=False)
     ctx.prof_enable(False)
+    torch.cuda.synchronize()
     prof = ctx.prof()
     conv = prof.get("conv3x3", {})
-    out = {"grid": cfg["n"], "rhs": nb, "iterations_budget": args.budget, "ms": ms,
-           "ms_per_iteration": ms / max(1, max(rep.iterations)),
+    its = max(1, max(rep.iterations))
+    out = {"grid": cfg["n"], "rhs": nb, "precond": cfg["precond"], "iterations_budget": budget, "ms": ms,
+           "ms_per_iteration": ms / its,
            "rel_residual_end": [round(float(h[-1] / h[0]), 6) for h in rep.residual_history],
            "converged": [bool(c) for c in rep.converged]}
     if conv.get("ms", 0) > 0:
         out["conv_tflops"] = conv["flops"] / (conv["ms"] / 1e3) / 1e12
         out["conv_share"] = conv["ms"] / max(1e-9, sum(v["ms"] for v in prof.values()))
+    # per kernel class: achieved GB/s (algorithmic bytes) and fraction of
+    # the measured HBM peak -- meaningful here, the working sets exceed L2 from c2 on
+    pk, _ = peaks()
+    total = max(1e-9, sum(v["ms"] for v in prof.values()))
+    out["kernels"] = {}
+    for k, v in prof.items():
+        if not v["launches"]:
+            continue
+        row = {"ms_per_iteration": v["ms"] / its, "share": v["ms"] / total}
+        if v["bytes"] > 0:
+            row["gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9
+            row["hbm_frac"] = row["gbs"] / pk.get("hbm_gbs", 6650.0)
+        if v["flops"] > 0:
+            row["tflops"] = v["flops"] / (v["ms"] / 1e3) / 1e12
+        out["kernels"][k] = row
     ctx.close()
     return out
 
@@ -414,7 +432,8 @@ def main():
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = one per SM)")
-    ap.add_argument("--also", default="c1", help="comma list of configs measured on a fixed iteration budget")
+    ap.add_argument("--also", default="c1,c2,c3", help="comma list of configs measured on a fixed iteration budget "
+                                                       "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

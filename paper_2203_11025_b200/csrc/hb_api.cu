@@ -78,8 +78,8 @@ void prof_end(Context& c, int cls, int token, double bytes, double flops) {
   c.prof_label.clear();
   Prof& p = c.prof[size_t(cls)];
   p.launches += 1;
-  p.bytes += bytes;
-  p.flops += flops;
+  p.bytes += bytes * c.prof_scale;
+  p.flops += flops * c.prof_scale;
   if (c.ev_pending.size() > 8192) prof_collect(c);
 }
 
@@ -224,12 +224,12 @@ static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const fl
     // initial guess, shared-memory tiles otherwise)
     const bool stream = c.opt_stream && e0 == nullptr && L.nx >= 16;
     if (stream)
-      launch_down_stream(c, V, offset, B, act, f, fscale, Cf);
+      launch_down_stream(c, V, w, offset, B, act, f, fscale, Cf);
     else
       launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
     vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
     if (stream)
-      launch_up_stream(c, V, offset, C.nx, C.ny, B, act, f, fscale, Cx, out);
+      launch_up_stream(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, Cx, out);
     else
       launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
     return;
@@ -337,16 +337,31 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
   const size_t N = c.levels[0]->N();
   const size_t BN = size_t(B) * N;
   if (!c.h_count) HB_CUDA(cudaMallocHost(&c.h_count, sizeof(int)));
+  // profiling (eager) only: scale each launch's algorithmic bytes/flops by the
+  // fraction of still-active columns -- frozen columns early-exit in every kernel
+  std::vector<int> h_act;
+  auto prof_active = [&]() {
+    if (!c.prof_on) return;
+    h_act.resize(size_t(B));
+    HB_CUDA(cudaMemcpyAsync(h_act.data(), c.kact.p, sizeof(int) * size_t(B), cudaMemcpyDeviceToHost, c.stream));
+    HB_CUDA(cudaStreamSynchronize(c.stream));
+    int a = 0;
+    for (int v : h_act) a += v != 0;
+    c.prof_scale = double(a) / double(B);
+  };
   auto cycle_body = [&]() {
     for (int j = 0; j < m; ++j) {
+      prof_active();
       float2* Vj = c.kV.p + size_t(j) * BN;
       float2* Zj = c.kZ.p + size_t(j) * BN;
       precond_apply_dev(c, kind, B, c.kact.p, Vj, c.kscale.p, Zj);
       launch_fg_adots(c, B, j, Zj, c.kW.p, c.kV.p);
       launch_fg_update(c, B, j, m, c.kW.p, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
     }
+    prof_active();
     launch_fg_finalize(c, B, m, c.kZ.p, dX);
     launch_fg_restart(c, B, dB, dX, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
+    c.prof_scale = 1.0;
   };
   auto read_count = [&]() {
     HB_CUDA(cudaMemcpyAsync(c.h_count, c.kcount.p, sizeof(int), cudaMemcpyDeviceToHost, c.stream));
@@ -828,6 +843,10 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_conv_ksplit = value != 0;
   else if (k == "coarse_reg")
     ctx->opt_coarse_reg = value != 0;
+  else if (k == "wide_legs")
+    ctx->opt_wide_legs = value != 0;
+  else if (k == "legs_wd")
+    ctx->opt_legs_wd = value != 0;
   else if (k == "stream_vcycle")
     ctx->opt_stream = value != 0;
   else

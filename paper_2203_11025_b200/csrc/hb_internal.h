@@ -144,9 +144,9 @@ void conv_tc_prepare(ConvW& cw);
 bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                     const float* bsrc, int cb, bool b_ctx, int relu, float* out);
 // row-streaming legs, zero initial guess (hb_mg_stream.cu)
-void launch_down_stream(Context& c, const LevelView& L, int offset, int B, const int* act, const float2* f,
+void launch_down_stream(Context& c, const LevelView& L, float damping, int offset, int B, const int* act, const float2* f,
                         const float* fscale, float2* fc);
-void launch_up_stream(Context& c, const LevelView& L, int offset, int cnx, int cny, int B, const int* act,
+void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B, const int* act,
                       const float2* f, const float* fscale, const float2* vc, float2* z);
 // network pack / unpack (hb_net.cu)
 void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const int* act, const float2* r,
@@ -224,8 +224,9 @@ struct Context {
   DBuf<float> pc_io, cn_io;
   DBuf<float2> pc_e0;
   // options
+  double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
-       opt_coarse_reg = true;
+       opt_coarse_reg = true, opt_wide_legs = false, opt_legs_wd = false;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {

@@ -22,6 +22,13 @@ namespace {
 constexpr int SW_OUT = 30;  // coarse columns emitted per warp
 constexpr int WARPS = 4;    // warps per CTA (independent row chunks)
 
+// damping / d (0 for the zero padding outside the grid), fast reciprocal
+__device__ __forceinline__ float2 wfrom(float2 d, float damping) {
+  const float m = fmaf(d.x, d.x, d.y * d.y);
+  const float s = m > 0.f ? __frcp_rn(m) * damping : 0.f;
+  return make_float2(d.x * s, -d.y * s);
+}
+
 struct Pair {
   float2 a, b;  // fine columns c0 = 2jx+o, c1 = c0+1
 };
@@ -56,7 +63,8 @@ __device__ __forceinline__ Pair apply_M(const Pair& d, const Pair& vm, const Pai
 }
 
 // down leg: grid (ceil(cnx / 30), ceil(row chunks / WARPS), B), block 32 x WARPS
-__global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, int offset, int rows_per_chunk,
+template <bool WD>  // WD: Jacobi factor w = damping / d formed from d in registers (no wdi stream)
+__global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, float damping, int offset, int rows_per_chunk,
                                                             const int* act, const float2* __restrict__ f,
                                                             const float* fscale, float2* __restrict__ fc) {
   const int b = blockIdx.z;
@@ -84,8 +92,13 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, int off
     }
     const size_t o = size_t(y) * nx;
     r.f = ld_pair(fb + o, c0, nx);
-    r.w = ld_pair(L.wdi + o, c0, nx);
     r.d = ld_pair(L.dM + o, c0, nx);
+    if (WD) {
+      r.w.a = wfrom(r.d.a, damping);
+      r.w.b = wfrom(r.d.b, damping);
+    } else {
+      r.w = ld_pair(L.wdi + o, c0, nx);
+    }
     return r;
   };
   auto vrow = [&](const Raw& r) {
@@ -135,7 +148,8 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, int off
 
 // up leg: grid (ceil(cnx / 30), ceil(row chunks / WARPS), B); each warp produces
 // fine rows [y0, y1) for its 60 fine columns
-__global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, int offset, int cnx, int cny,
+template <bool WD>
+__global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float damping, int offset, int cnx, int cny,
                                                           int rows_per_chunk, const int* act,
                                                           const float2* __restrict__ f, const float* fscale,
                                                           const float2* __restrict__ vc, float2* __restrict__ z) {
@@ -173,8 +187,13 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, int offse
     }
     const size_t o = size_t(y) * nx;
     r.f = ld_pair(fb + o, c0, nx);
-    r.w = ld_pair(L.wdi + o, c0, nx);
     r.d = ld_pair(L.dM + o, c0, nx);
+    if (WD) {
+      r.w.a = wfrom(r.d.a, damping);
+      r.w.b = wfrom(r.d.b, damping);
+    } else {
+      r.w = ld_pair(L.wdi + o, c0, nx);
+    }
     const int t = y - offset;
     if ((t & 1) == 0) {
       r.c0v = cload(t >> 1);
@@ -227,10 +246,136 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, int offse
   }
 }
 
+// ---------------------------------------------------------------------------
+// Wide variants: each lane owns 4 consecutive fine columns F..F+3 (F a multiple
+// of 4, so a lane's columns are all inside or all outside the grid and its
+// row loads are two aligned float4 per array); a warp covers 128 fine columns,
+// lanes 0 and 31 are halo, lanes 1..30 emit 2 coarse columns each (60 per
+// warp).  Half the loads, shuffles and bounds tests per node of the 2-column
+// kernels above, same arithmetic.
+constexpr int SW4_FINE = 120;  // fine columns emitted per warp
+
+struct Quad {
+  float2 c[4];
+};
+__device__ __forceinline__ Quad ld_quad(const float2* row, int F, bool ok) {
+  Quad q;
+  if (ok) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(row + F));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(row + F + 2));
+    q.c[0] = make_float2(a.x, a.y);
+    q.c[1] = make_float2(a.z, a.w);
+    q.c[2] = make_float2(b.x, b.y);
+    q.c[3] = make_float2(b.z, b.w);
+  } else {
+    q.c[0] = q.c[1] = q.c[2] = q.c[3] = make_float2(0.f, 0.f);
+  }
+  return q;
+}
+// M v on one row of a lane's 4 columns: d v - ih2 (up + down + left + right)
+__device__ __forceinline__ Quad apply_M4(const Quad& d, const Quad& vm, const Quad& v, const Quad& vp, float ih2) {
+  const float2 left = shfl_up2(v.c[3]);    // column F - 1
+  const float2 right = shfl_down2(v.c[0]); // column F + 4
+  Quad o;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 l = k == 0 ? left : v.c[k - 1];
+    const float2 r = k == 3 ? right : v.c[k + 1];
+    const float2 nb = cadd(cadd(vm.c[k], vp.c[k]), cadd(l, r));
+    o.c[k] = cmul(d.c[k], v.c[k]);
+    o.c[k].x = fmaf(-ih2, nb.x, o.c[k].x);
+    o.c[k].y = fmaf(-ih2, nb.y, o.c[k].y);
+  }
+  return o;
+}
+
+// down leg, wide: grid (ceil(nx / 120), ceil(row chunks / WARPS), B), block 32 x WARPS
+__global__ void __launch_bounds__(32 * WARPS) k_down_stream4(LevelView L, int offset, int rows_per_chunk,
+                                                             const int* act, const float2* __restrict__ f,
+                                                             const float* fscale, float2* __restrict__ fc) {
+  const int b = blockIdx.z;
+  if (act && !act[b]) return;
+  const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
+  const int F = blockIdx.x * SW4_FINE - 4 + 4 * lane;
+  const bool colok = F >= 0 && F < nx;
+  const int jy0 = (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
+  if (jy0 >= cny) return;
+  const int jy1 = min(cny, jy0 + rows_per_chunk);
+  const size_t N = size_t(nx) * ny;
+  const float2* fb = f + b * N;
+  const float s = fscale ? fscale[b] : 1.0f;
+  const float ih2 = L.inv_h2;
+  struct Raw {
+    Quad f, w, d;
+  };
+  auto load_raw = [&](int y) {
+    Raw r;
+    const bool ok = colok && y >= 0 && y < ny;
+    const size_t o = ok ? size_t(y) * nx : 0;
+    r.f = ld_quad(fb + o, F, ok);
+    r.w = ld_quad(L.wdi + o, F, ok);
+    r.d = ld_quad(L.dM + o, F, ok);
+    return r;
+  };
+  auto vrow = [&](const Raw& r) {
+    Quad v;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v.c[k] = cmul(cscale(r.f.c[k], s), r.w.c[k]);
+    return v;
+  };
+  int y = 2 * jy0 + offset - 1;
+  Raw r_c = load_raw(y), r_p1 = load_raw(y + 1), r_p2 = load_raw(y + 2);
+  Quad v_m = vrow(load_raw(y - 1)), v_c = vrow(r_c);
+  float2 a_m2 = make_float2(0.f, 0.f), a_m1 = a_m2, b_m2 = a_m2, b_m1 = a_m2;  // horizontal sums, 2 coarse cols
+  const int yend = 2 * (jy1 - 1) + offset + 1;
+  const bool emit = lane >= 1 && lane <= 30 && colok && F / 2 + 1 < cnx;
+  for (; y <= yend; ++y) {
+    const Raw r_p3 = load_raw(y + 3);
+    const Quad v_p = vrow(r_p1);
+    const Quad mv = apply_M4(r_c.d, v_m, v_c, v_p, ih2);
+    Quad r;
+    const bool rowok = y >= 0 && y < ny;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      r.c[k] = (rowok && colok) ? csub(cscale(r_c.f.c[k], s), mv.c[k]) : make_float2(0.f, 0.f);
+    // horizontal full weighting around the two coarse centres of this lane
+    float2 ha, hb;
+    if (offset == 0) {  // centres F, F+2
+      const float2 rl = shfl_up2(r.c[3]);
+      ha = caxpy(cscale(r.c[0], 0.5f), 0.25f, cadd(rl, r.c[1]));
+      hb = caxpy(cscale(r.c[2], 0.5f), 0.25f, cadd(r.c[1], r.c[3]));
+    } else {            // centres F+1, F+3
+      const float2 rr = shfl_down2(r.c[0]);
+      ha = caxpy(cscale(r.c[1], 0.5f), 0.25f, cadd(r.c[0], r.c[2]));
+      hb = caxpy(cscale(r.c[3], 0.5f), 0.25f, cadd(r.c[2], rr));
+    }
+    // y = 2 jy + o + 1 closes coarse row jy
+    const int t = y - offset - 1;
+    if (t >= 2 * jy0 && ((t & 1) == 0)) {
+      const int jy = t >> 1;
+      if (emit && jy < jy1) {
+        const float2 ca = caxpy(cscale(a_m1, 0.5f), 0.25f, cadd(a_m2, ha));
+        const float2 cb = caxpy(cscale(b_m1, 0.5f), 0.25f, cadd(b_m2, hb));
+        *reinterpret_cast<float4*>(fc + size_t(b) * cnx * cny + size_t(jy) * cnx + F / 2) =
+            make_float4(ca.x, ca.y, cb.x, cb.y);
+      }
+    }
+    a_m2 = a_m1;
+    a_m1 = ha;
+    b_m2 = b_m1;
+    b_m1 = hb;
+    v_m = v_c;
+    v_c = v_p;
+    r_c = r_p1;
+    r_p1 = r_p2;
+    r_p2 = r_p3;
+  }
+}
+
 }  // namespace
 
-void launch_down_stream(Context& c, const LevelView& L, int offset, int B, const int* act, const float2* f,
-                        const float* fscale, float2* fc) {
+void launch_down_stream(Context& c, const LevelView& L, float damping, int offset, int B, const int* act,
+                        const float2* f, const float* fscale, float2* fc) {
   const int cnx = L.nx / 2, cny = L.ny / 2;
   const int tok = prof_begin(c, PC_DOWN);
   // rows per warp: enough warps to fill the machine, >= 4 coarse rows to amortise the halo
@@ -240,14 +385,22 @@ void launch_down_stream(Context& c, const LevelView& L, int offset, int B, const
     rpc /= 2;
   if (env_d) rpc = env_d;
   const int chunks = (cny + rpc - 1) / rpc;
-  const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
-  k_down_stream<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
+  if (c.opt_wide_legs && L.nx % 4 == 0) {
+    const dim3 grid((L.nx + SW4_FINE - 1) / SW4_FINE, (chunks + WARPS - 1) / WARPS, B);
+    k_down_stream4<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
+  } else {
+    const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
+    if (c.opt_legs_wd)
+      k_down_stream<true><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, rpc, act, f, fscale, fc);
+    else
+      k_down_stream<false><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, rpc, act, f, fscale, fc);
+  }
   prof_end(c, PC_DOWN, tok, double(B) * L.nx * L.ny * 10.0 + double(L.nx) * L.ny * 16.0, 0);
   HB_CUDA(cudaGetLastError());
 }
 
-void launch_up_stream(Context& c, const LevelView& L, int offset, int cnx, int cny, int B, const int* act,
-                      const float2* f, const float* fscale, const float2* vc, float2* z) {
+void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B,
+                      const int* act, const float2* f, const float* fscale, const float2* vc, float2* z) {
   const int tok = prof_begin(c, PC_UP);
   static const int env_u = getenv("HB_RPC_UP") ? atoi(getenv("HB_RPC_UP")) : 0;
   int rpc = 16;
@@ -256,7 +409,10 @@ void launch_up_stream(Context& c, const LevelView& L, int offset, int cnx, int c
   if (env_u) rpc = env_u;
   const int chunks = (L.ny + rpc - 1) / rpc;
   const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
-  k_up_stream<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, cnx, cny, rpc, act, f, fscale, vc, z);
+  if (c.opt_legs_wd)
+    k_up_stream<true><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
+  else
+    k_up_stream<false><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
   prof_end(c, PC_UP, tok, double(B) * L.nx * L.ny * 18.0 + double(L.nx) * L.ny * 16.0, 0);
   HB_CUDA(cudaGetLastError());
 }

@@ -227,23 +227,27 @@ __global__ void __launch_bounds__(CS_NT) k_conv_small(ConvArgs p) {
   }
 }
 
-// 2x2 max-pool / x2 bilinear upsample, NHWC, 4 channels per thread (C % 4 == 0)
-__global__ void k_maxpool2_v4(int H, int W, int C4, const float4* __restrict__ in, float4* __restrict__ out,
-                              const int* act) {
-  const int b = blockIdx.z, oy = blockIdx.y;
+// 2x2 max-pool / x2 bilinear upsample, NHWC, 4 channels per thread (C % 4 == 0);
+// one CTA per output row (grid (rows, B)), threads stride along the row
+__global__ void __launch_bounds__(256) k_maxpool2_v4(int H, int W, int C4, const float4* __restrict__ in,
+                                                     float4* __restrict__ out, const int* act) {
+  const int b = blockIdx.y, oy = blockIdx.x;
   if (act && !act[b]) return;
-  const int Wo = W / 2;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (ox, c4)
-  if (i >= Wo * C4) return;
-  const int ox = i / C4, c = i - ox * C4;
-  const float4* s = in + ((size_t(b) * H + 2 * oy) * W + 2 * ox) * C4 + c;
-  const float4 a0 = s[0], a1 = s[C4], a2 = s[size_t(W) * C4], a3 = s[size_t(W) * C4 + C4];
-  float4 m;
-  m.x = fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x));
-  m.y = fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y));
-  m.z = fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z));
-  m.w = fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w));
-  out[((size_t(b) * (H / 2) + oy) * Wo + ox) * C4 + c] = m;
+  const int Wo = W / 2, n = Wo * C4;
+  const float4* s0 = in + (size_t(b) * H + 2 * oy) * W * C4;
+  const float4* s1 = s0 + size_t(W) * C4;
+  float4* o = out + (size_t(b) * (H / 2) + oy) * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int ox = i / C4, c = i - ox * C4;
+    const int k = 2 * ox * C4 + c;
+    const float4 a0 = __ldg(s0 + k), a1 = __ldg(s0 + k + C4), a2 = __ldg(s1 + k), a3 = __ldg(s1 + k + C4);
+    float4 m;
+    m.x = fmaxf(fmaxf(a0.x, a1.x), fmaxf(a2.x, a3.x));
+    m.y = fmaxf(fmaxf(a0.y, a1.y), fmaxf(a2.y, a3.y));
+    m.z = fmaxf(fmaxf(a0.z, a1.z), fmaxf(a2.z, a3.z));
+    m.w = fmaxf(fmaxf(a0.w, a1.w), fmaxf(a2.w, a3.w));
+    o[i] = m;
+  }
 }
 
 __global__ void k_maxpool2(int B, int H, int W, int C, const float* __restrict__ in, float* __restrict__ out,
@@ -295,27 +299,29 @@ __global__ void k_upsample2(int B, int H, int W, int C, const float* __restrict_
   }
 }
 
-__global__ void k_upsample2_v4(int H, int W, int C4, const float4* __restrict__ in, long long sin4,
-                               float4* __restrict__ out, const int* act) {
-  const int b = blockIdx.z, oy = blockIdx.y;
+__global__ void __launch_bounds__(256) k_upsample2_v4(int H, int W, int C4, const float4* __restrict__ in,
+                                                      long long sin4, float4* __restrict__ out, const int* act) {
+  const int b = blockIdx.y, oy = blockIdx.x;
   if (act && !act[b]) return;
-  const int Wo = 2 * W;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;  // (ox, c4)
-  if (i >= Wo * C4) return;
-  const int ox = i / C4, c = i - ox * C4;
+  const int Wo = 2 * W, n = Wo * C4;
   int y0, y1, x0, x1;
   float fy, fx;
   up_taps(oy, H, &y0, &y1, &fy);
-  up_taps(ox, W, &x0, &x1, &fx);
   const float4* s = in + b * sin4;
-  const float4 v00 = s[(size_t(y0) * W + x0) * C4 + c], v01 = s[(size_t(y0) * W + x1) * C4 + c];
-  const float4 v10 = s[(size_t(y1) * W + x0) * C4 + c], v11 = s[(size_t(y1) * W + x1) * C4 + c];
-  auto lerp2 = [&](float a, float bq, float cq, float d) {
-    return (1.f - fy) * ((1.f - fx) * a + fx * bq) + fy * ((1.f - fx) * cq + fx * d);
-  };
-  out[((size_t(b) * 2 * H + oy) * Wo + ox) * C4 + c] =
-      make_float4(lerp2(v00.x, v01.x, v10.x, v11.x), lerp2(v00.y, v01.y, v10.y, v11.y),
-                  lerp2(v00.z, v01.z, v10.z, v11.z), lerp2(v00.w, v01.w, v10.w, v11.w));
+  const float4* r0 = s + size_t(y0) * W * C4;
+  const float4* r1 = s + size_t(y1) * W * C4;
+  float4* o = out + (size_t(b) * 2 * H + oy) * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int ox = i / C4, c = i - ox * C4;
+    up_taps(ox, W, &x0, &x1, &fx);
+    const float4 v00 = __ldg(r0 + x0 * C4 + c), v01 = __ldg(r0 + x1 * C4 + c);
+    const float4 v10 = __ldg(r1 + x0 * C4 + c), v11 = __ldg(r1 + x1 * C4 + c);
+    auto lerp2 = [&](float a, float bq, float cq, float d) {
+      return (1.f - fy) * ((1.f - fx) * a + fx * bq) + fy * ((1.f - fx) * cq + fx * d);
+    };
+    o[i] = make_float4(lerp2(v00.x, v01.x, v10.x, v11.x), lerp2(v00.y, v01.y, v10.y, v11.y),
+                       lerp2(v00.z, v01.z, v10.z, v11.z), lerp2(v00.w, v01.w, v10.w, v11.w));
+  }
 }
 
 // [h^2 Re r, h^2 Im r, kappa^2] NHWC (inc/precond.hpp:74-83, gamma dropped)
@@ -415,8 +421,8 @@ static void maxpool(Context& c, int B, const int* act, int H, int W, int C, cons
   NScope ns(c, PC_NETIO);
   if (C % 4 == 0) {
     const int n = (W / 2) * (C / 4);
-    k_maxpool2_v4<<<dim3((n + 127) / 128, H / 2, B), 128, 0, c.stream>>>(H, W, C / 4, reinterpret_cast<const float4*>(in),
-                                                                          reinterpret_cast<float4*>(out), act);
+    k_maxpool2_v4<<<dim3(H / 2, B), n >= 256 ? 256 : ((n + 31) / 32) * 32, 0, c.stream>>>(
+        H, W, C / 4, reinterpret_cast<const float4*>(in), reinterpret_cast<float4*>(out), act);
     HB_CUDA(cudaGetLastError());
     return;
   }
@@ -429,7 +435,7 @@ static void upsample(Context& c, int B, const int* act, int H, int W, int C, con
   NScope ns(c, PC_NETIO);
   if (C % 4 == 0 && sin_ % 4 == 0) {
     const int n = 2 * W * (C / 4);
-    k_upsample2_v4<<<dim3((n + 127) / 128, 2 * H, B), 128, 0, c.stream>>>(
+    k_upsample2_v4<<<dim3(2 * H, B), n >= 256 ? 256 : ((n + 31) / 32) * 32, 0, c.stream>>>(
         H, W, C / 4, reinterpret_cast<const float4*>(in), sin_ / 4, reinterpret_cast<float4*>(out), act);
     HB_CUDA(cudaGetLastError());
     return;

@@ -115,6 +115,8 @@ int hb_coarse_solve(hb_ctx* ctx, int batch, const double* f, double* x);
 /* ---- preconditioners ----------------------------------------------------- */
 #define HB_PC_V 0  /* SL V-cycle from zero (M_V; with HB_COARSE_NET = coarse-net cycle) */
 #define HB_PC_VU 1 /* e0 = net(h^2 r, kappa^2) then V-cycle from e0 (M_VU) */
+#define HB_PC_JU 2 /* e1 = J_A(0, r); z = J_A(e1 + net(h^2 (r - A e1), kappa^2), r)  (M_JU,
+                      inc/precond.hpp:104-139, JacobiUnetPreconditioner::apply with the A5 net) */
 int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* z);
 /* name() and requires_flexible() of the reference plugin (inc/precond.hpp:14-27) */
 const char* hb_precond_name(int kind);

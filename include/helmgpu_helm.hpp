@@ -126,6 +126,12 @@ class GpuUnetVCycle : public GpuPreconditioner {
   explicit GpuUnetVCycle(std::shared_ptr<Context> ctx) : GpuPreconditioner(std::move(ctx), HB_PC_VU) {}
 };
 
+// drop-in for JacobiUnetPreconditioner (inc/precond.hpp:104-139), name() == "ju"
+class GpuJacobiUnet : public GpuPreconditioner {
+ public:
+  explicit GpuJacobiUnet(std::shared_ptr<Context> ctx) : GpuPreconditioner(std::move(ctx), HB_PC_JU) {}
+};
+
 // Device-resident block FGMRES with A = A^h of the context's problem and M =
 // the plugin; same contract and SolveReport as inc/krylov.hpp:83-267.
 inline std::pair<std::vector<ComplexField>, SolveReport> block_fgmres(GpuPreconditioner& M,

@@ -997,9 +997,10 @@ HO_EXPORT void ho_coarse_gmres(const ho_mg* mg, int l, int iters, const double* 
 }
 
 /* ------------------------------------------------------- preconditioners --
- * inc/precond.hpp: M_V (:35-53), M_VU (:143-165, A8), coarse-net cycle
- * (A4; it is M_V whose hierarchy has coarse_kind NET). */
-enum { HO_PC_V = 0, HO_PC_VU = 1 };
+ * inc/precond.hpp: M_V (:35-53), M_VU (:143-165, A8), M_JU (:104-139, with
+ * the classic A5 net), coarse-net cycle (A4; it is M_V whose hierarchy has
+ * coarse_kind NET). */
+enum { HO_PC_V = 0, HO_PC_VU = 1, HO_PC_JU = 2 };
 
 typedef struct {
   int kind;
@@ -1059,7 +1060,24 @@ static void pc_net_guess(const ho_pc* p, const cplx* r, cplx* e0) {
 
 static void pc_apply_one(void* c, const cplx* r, cplx* z) {
   const ho_pc* p = (const ho_pc*)c;
-  const size_t n = (size_t)p->mg->lev[0].nx * p->mg->lev[0].ny;
+  const ho_level* L0 = &p->mg->lev[0];
+  const size_t n = (size_t)L0->nx * L0->ny;
+  if (p->kind == HO_PC_JU) {
+    /* inc/precond.hpp:112-130: e1 = J_A(0, r); de = net(r - A e1); z = J_A(e1 + de, r), omega = 0.8 */
+    cplx* e1 = (cplx*)calloc(n, sizeof(cplx));
+    cplx* res = (cplx*)malloc(sizeof(cplx) * n);
+    cplx* de = (cplx*)malloc(sizeof(cplx) * n);
+    jacobi(L0->nx, L0->ny, L0->h, L0->diagA, e1, r, 0.8, 1);
+    stencil_apply(L0->nx, L0->ny, L0->h, L0->diagA, e1, res);
+    for (size_t i = 0; i < n; ++i) res[i] = r[i] - res[i];
+    pc_net_guess(p, res, de);
+    for (size_t i = 0; i < n; ++i) z[i] = e1[i] + de[i];
+    jacobi(L0->nx, L0->ny, L0->h, L0->diagA, z, r, 0.8, 1);
+    free(e1);
+    free(res);
+    free(de);
+    return;
+  }
   if (p->kind == HO_PC_V) {
     memset(z, 0, sizeof(cplx) * n);
   } else {

@@ -246,7 +246,7 @@ class Hierarchy:
         return x
 
 
-PC = {"v": 0, "vu": 1}
+PC = {"v": 0, "vu": 1, "ju": 2}
 
 
 class Precond:

@@ -304,6 +304,29 @@ void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2
     vcycle(c, B, act, r, rscale, nullptr, z);
     return;
   }
+  if (kind == HB_PC_JU) {
+    // M_JU (inc/precond.hpp:112-130), damped Jacobi on A^h with omega = 0.8:
+    // e1 = J_A(0, r); de = net(r - A e1) (fine-h packing, :74-83); z = J_A(e1 + de, r)
+    Net& n = c.nets[0];
+    if (!n.set) throw HbError{HB_ERR_STATE, "M_JU needs net slot 0"};
+    Level& L = *c.levels[0];
+    LevelView VA = L.view();
+    VA.dM = L.dA.p;  // Jacobi / residual on A^h, not the shifted M^h
+    const size_t np = size_t(B) * L.N();
+    DBuf<float>& io = c.pc_io;
+    DBuf<float2>& e1 = c.pc_e0;
+    io.ensure(np * 5 + np * 2);
+    e1.ensure(np);
+    float2* res = reinterpret_cast<float2*>(io.p + np * 5);
+    const float om = 0.8f;
+    launch_jacobi_zero(c, VA, om, B, act, r, rscale, e1.p);
+    launch_residual(c, VA, B, act, e1.p, r, rscale, res);
+    launch_pack_input(c, VA, L.h * L.h, B, act, res, nullptr, io.p);
+    net_forward_dev(c, 0, B, act, L.ny, L.nx, io.p, io.p + np * 3);
+    launch_unpack_add(c, int(L.N()), B, act, io.p + np * 3, e1.p, e1.p);  // e2 = e1 + de (in place)
+    launch_jacobi_sweep(c, VA, om, B, act, e1.p, r, rscale, z);
+    return;
+  }
   if (kind != HB_PC_VU) throw HbError{HB_ERR_ARG, "unknown preconditioner kind"};
   // M_VU (inc/precond.hpp:151-158): e0 = net(h^2 r, kappa^2); z = cycle(e0, r)
   Net& n = c.nets[0];
@@ -707,12 +730,12 @@ int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* 
   HB_API_END
 }
 
-const char* hb_precond_name(int kind) { return kind == HB_PC_VU ? "vu" : "v"; }
+const char* hb_precond_name(int kind) { return kind == HB_PC_VU ? "vu" : kind == HB_PC_JU ? "ju" : "v"; }
 
 int hb_precond_requires_flexible(hb_ctx* ctx, int kind) {
   if (!ctx) return 1;
   // network-based preconditioners are non-stationary (inc/precond.hpp:132,160)
-  return kind == HB_PC_VU || ctx->vc.coarse_solver == HB_COARSE_NET;
+  return kind == HB_PC_VU || kind == HB_PC_JU || ctx->vc.coarse_solver == HB_COARSE_NET;
 }
 
 int hb_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,

@@ -152,6 +152,11 @@ void launch_up_stream(Context& c, const LevelView& L, float damping, int offset,
 void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const int* act, const float2* r,
                        const float* rscale, float* x /*NHWC, 3 ch*/);
 void launch_unpack_output(Context& c, int N, int B, const int* act, const float* y /*NHWC 2ch*/, float2* e);
+// e = base + y (NHWC 2ch -> c64); base may alias e
+void launch_unpack_add(Context& c, int N, int B, const int* act, const float* y, const float2* base, float2* e);
+// out = s f - Op u  (Op = the level operator whose diagonal is L.dM), hb_mg.cu
+void launch_residual(Context& c, const LevelView& L, int B, const int* act, const float2* u, const float2* f,
+                     const float* fscale, float2* out);
 
 // ---- Krylov (hb_krylov.cu)
 struct ColState;

@@ -59,6 +59,19 @@ __global__ void __launch_bounds__(TBX* TBY) k_jacobi_sweep(LevelView L, float da
   out[b * N + i] = caxpy(ld(v, b * N + i), damping, corr);
 }
 
+// out = s f - Op u, Op the 5-point operator with diagonal L.dM
+__global__ void __launch_bounds__(TBX* TBY) k_residual(LevelView L, const int* act, const float2* __restrict__ u,
+                                                      const float2* __restrict__ f, const float* fscale,
+                                                      float2* __restrict__ out) {
+  const int b = blockIdx.z;
+  if (!col_active(act, b)) return;
+  const int ix = blockIdx.x * TBX + threadIdx.x, iy = blockIdx.y * TBY + threadIdx.y;
+  if (ix >= L.nx || iy >= L.ny) return;
+  const size_t N = size_t(L.nx) * L.ny, i = size_t(iy) * L.nx + ix;
+  const float2 au = stencil_at(u + b * N, L.nx, L.ny, ix, iy, ld(L.dM, i), L.inv_h2, 1.0f);
+  out[b * N + i] = csub(cscale(ld(f, b * N + i), col_scale(fscale, b)), au);
+}
+
 // fc(j) = sum_k w_k (f - M v)(2j + o + k), w = [1 2 1]x[1 2 1]/16, out-of-range skipped
 __global__ void __launch_bounds__(TBX* TBY) k_residual_restrict(LevelView L, int offset, const int* act,
                                                                const float2* __restrict__ v,
@@ -392,6 +405,13 @@ void launch_jacobi_zero(Context& c, const LevelView& L, float damping, int B, co
                         const float* fscale, float2* v) {
   ProfScope ps(c, PC_SMOOTH, double(B) * L.nx * L.ny * 24.0);
   k_jacobi_zero<<<grid2(L.nx, L.ny, B), dim3(TBX, TBY), 0, c.stream>>>(L, damping, act, f, fscale, v);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_residual(Context& c, const LevelView& L, int B, const int* act, const float2* u, const float2* f,
+                     const float* fscale, float2* out) {
+  ProfScope ps(c, PC_SMOOTH, double(B) * L.nx * L.ny * 24.0);
+  k_residual<<<grid2(L.nx, L.ny, B), dim3(TBX, TBY), 0, c.stream>>>(L, act, u, f, fscale, out);
   HB_CUDA(cudaGetLastError());
 }
 

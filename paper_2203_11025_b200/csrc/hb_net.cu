@@ -348,6 +348,16 @@ __global__ void k_unpack(int N, const int* act, const float* __restrict__ y, flo
   }
 }
 
+__global__ void k_unpack_add(int N, const int* act, const float* __restrict__ y, const float2* base, float2* e) {
+  const int b = blockIdx.y;
+  if (act && !act[b]) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
+    const float* s = y + (size_t(b) * N + i) * 2;
+    const float2 o = base[size_t(b) * N + i];
+    e[size_t(b) * N + i] = make_float2(o.x + s[0], o.y + s[1]);
+  }
+}
+
 __global__ void k_nhwc_to_nchw(int B, int C, int HW, const float* __restrict__ in, float* __restrict__ out) {
   const size_t total = size_t(B) * C * HW;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < total; i += size_t(gridDim.x) * blockDim.x) {
@@ -449,6 +459,12 @@ void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const i
   NScope ns(c, PC_NETIO);
   const int N = L.nx * L.ny;
   k_pack<<<dim3(grid1(N), B), 256, 0, c.stream>>>(N, float(h2), act, r, rscale, L.k2f, x);
+  HB_CUDA(cudaGetLastError());
+}
+
+void launch_unpack_add(Context& c, int N, int B, const int* act, const float* y, const float2* base, float2* e) {
+  NScope ns(c, PC_NETIO);
+  k_unpack_add<<<dim3(grid1(N), B), 256, 0, c.stream>>>(N, act, y, base, e);
   HB_CUDA(cudaGetLastError());
 }
 

@@ -30,7 +30,7 @@ _u8p = C.POINTER(C.c_uint8)
 _vp = C.c_void_p
 
 HB_COARSE = {"gmres": 0, "jacobi": 1, "net": 2}
-HB_PC = {"v": 0, "vu": 1}
+HB_PC = {"v": 0, "vu": 1, "ju": 2}
 
 
 class _VCycleCfg(C.Structure):
@@ -435,6 +435,10 @@ class SLVCyclePreconditioner(_GpuPrecond):  # M_V (inc/precond.hpp:35-53); coars
 
 class UnetVCyclePreconditioner(_GpuPrecond):  # M_VU (inc/precond.hpp:143-165)
     kind = "vu"
+
+
+class JacobiUnetPreconditioner(_GpuPrecond):  # M_JU (inc/precond.hpp:104-139), A5 net
+    kind = "ju"
 
 
 def check_flexible_contract(cfg: KrylovConfig, m: Preconditioner):  # inc/precond.hpp:29-32

@@ -123,6 +123,17 @@ def main():
     Hv = O.RefHierarchy(k2c, gc, om, 1 / 16, 1 / 2.25, levels=3)
     vnet = O.RefNet(0, 3, 16, 3, 0, seed=8)
     g["vu_z"] = O.RefPrecond("vu", Hv, net=vnet).apply(r)[0]
+    # M_JU (inc/precond.hpp:112-130) assembled from reference primitives with the
+    # classic net: e1 = J_A(0, r); de = net(h^2 (r - A e1), kappa^2); z = J_A(e1 + de, r)
+    jnet = O.RefNet(0, 3, 16, 3, 0, seed=11)
+    h2 = (1.0 / nn) ** 2
+    e1 = Hv.jacobi(np.zeros_like(r), r, 0.8, 1, 0, shifted=False)
+    res = r - Hv.apply(e1, 0, shifted=False)
+    xin = np.stack([h2 * res.real, h2 * res.imag, k2c]).astype(np.float32)[None]
+    de = jnet.forward(xin)[0]
+    g["ju_z"] = Hv.jacobi(e1 + (de[0].astype(np.float64) + 1j * de[1].astype(np.float64)), r, 0.8, 1, 0,
+                          shifted=False)
+    g["ju0_z"] = Hv.jacobi(np.zeros_like(r), r, 0.8, 2, 0, shifted=False)  # zero-net M_JU == J_A o J_A
 
     np.savez_compressed(OUT, **g)
     print("wrote", OUT, os.path.getsize(OUT), "bytes;", len(g), "arrays")

@@ -214,6 +214,19 @@ def run_reference(args, ws, rank):
     print(json.dumps(line), flush=True)
 
 
+def ncu_traffic(kernel_class):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) of the
+    dominant kernel class, from the committed ncu --set full capture of the same
+    bench command (profiles/ncu_traffic.json, written by tools/ncu_traffic.py)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f)
+        e = t["classes"][kernel_class]
+        return {"bytes_per_launch": e["dram_bytes_per_launch"], "source": t["source"]}
+    except Exception:
+        return None
+
+
 def run_ours(args, ws, rank, local):
     import torch
     from paper_2203_11025_b200 import helmgpu as hg
@@ -297,12 +310,16 @@ def run_ours(args, ws, rank, local):
 
     # ---- roofline pass: same workload, per-kernel-class CUDA events on the library
     # stream (eager launches; the timed region above replays CUDA graphs)
+    # the two half-batch V-cycle streams are serialised for this pass so that
+    # per-launch event times are not inflated by the other stream's kernels
+    ctx.set_option("split_vcycle", 0)
     ctx.prof_reset()
     ctx.prof_enable(True)
     for _ in range(args.steps):
         solve()
     torch.cuda.synchronize()
     ctx.prof_enable(False)
+    ctx.set_option("split_vcycle", 1)
     prof = ctx.prof()
     total_ms = sum(p["ms"] for p in prof.values()) or 1.0
     pk, src = peaks()
@@ -333,6 +350,10 @@ def run_ours(args, ws, rank, local):
                                                        "launch as DESIGN.md 'Roofline accounting'"}
     rl["share_of_step"] = p["ms"] / total_ms
     rl["avg_launch_us"] = 1e3 * p["ms"] / max(1, p["launches"])
+    tr = ncu_traffic(name)
+    if tr is not None:
+        rl["traffic"] = tr["bytes_per_launch"]
+        rl["traffic_source"] = tr["source"]
 
     line = {"metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,

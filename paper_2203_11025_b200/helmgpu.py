@@ -294,12 +294,18 @@ class Context:
         self._check(lib().hb_precond_apply(self.h, HB_PC[kind], B, _p(r), _p(z)))
         return z
 
-    def fgmres(self, kind, B, cfg: KrylovConfig, X0=None):
+    def fgmres(self, kind, B, cfg: KrylovConfig, X0=None, out=None):
+        """out: optional preallocated (e.g. pinned) c128 array receiving X."""
         B = _c128(B)
         if B.ndim == 2:
             B = B[None]
         nb = B.shape[0]
-        X = np.zeros_like(B)
+        if out is not None:
+            if out.shape != B.shape or out.dtype != np.complex128 or not out.flags.c_contiguous:
+                raise ValueError("out must be a C-contiguous complex128 array shaped like B")
+            X = out
+        else:
+            X = np.zeros_like(B)
         cap = cfg.max_iters + 2
         hist = np.zeros((nb, cap))
         hl = np.zeros(nb, np.int32)

@@ -237,41 +237,82 @@ def run_ours(args, ws, rank, local):
     cfg = config_for(args.config)
     R = args.replicas or sms
     cols = columns(cfg, ws, rank, R)
-    ctx, arr = problems.gpu_setup(cfg, device=local)
+    # G column groups = G independent solver contexts on their own streams, driven
+    # from G host threads: one group's latency-bound coarsest solves overlap the
+    # other's bandwidth-bound legs / Krylov kernels
+    G = max(1, min(args.groups, len(cols) // 16 or 1))
+    bounds = [len(cols) * g // G for g in range(G + 1)]
+    groups = []
+    for g in range(G):
+        cg, arr = problems.gpu_setup(cfg, device=local)
+        groups.append(cg)
+    ctx = groups[0]
     Bh = np.ascontiguousarray(problems.rhs_block(arr)[cols])
     nb = Bh.shape[0]
     kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=cfg["max_iters"], rel_tol=1e-6)
     kind = cfg["precond"]
     dB = torch.from_numpy(Bh).to(dev)
     dX = torch.zeros_like(dB)
-    stream = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    streams = [torch.cuda.ExternalStream(cg.stream, device=dev) for cg in groups]
+    stream = streams[0]
     flush = torch.empty(128 * 1024 * 1024, dtype=torch.float32, device=dev)
 
-    def solve(report=False):
-        dX.zero_()
-        return ctx.fgmres_device(kind, dB.data_ptr(), dX.data_ptr(), nb, kc, want_report=report)
+    def run_groups(fn):
+        """fn(g) for every group from its own host thread; returns the results"""
+        out = [None] * G
+        def body(g):
+            out[g] = fn(g)
+        th = [threading.Thread(target=body, args=(g,)) for g in range(1, G)]
+        for t in th:
+            t.start()
+        body(0)
+        for t in th:
+            t.join()
+        return out
+
+    def solve_group(g, report=False):
+        lo, hi = bounds[g], bounds[g + 1]
+        return groups[g].fgmres_device(kind, dB[lo:hi].data_ptr(), dX[lo:hi].data_ptr(), hi - lo, kc,
+                                       want_report=report)
+
+    def timed(fn):
+        """device time of fn() over all group streams: start event on stream 0 (the
+        others wait on it), end = the latest stream"""
+        e0 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for st in streams[1:]:
+            st.wait_event(e0)
+        fn()
+        ends = []
+        for st in streams:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(st)
+            ends.append(e)
+        return e0, ends
 
     for _ in range(args.warmup):
-        solve()
-    rep = solve(report=True)
+        dX.zero_()
+        run_groups(lambda g: solve_group(g))
+    dX.zero_()
+    reps = run_groups(lambda g: solve_group(g, report=True))
     torch.cuda.synchronize()
+    rep = hg.SolveReport(sum((r.residual_history for r in reps), []), sum((r.iterations for r in reps), []),
+                         sum((r.converged for r in reps), []), sum((r.breakdown for r in reps), []))
 
-    # ---- timed region: K steps, events on the library stream, L2 flushed between steps
+    # ---- timed region: K steps, CUDA events on the library streams, L2 flushed between steps
     barrier(ws)
     torch.cuda.synchronize()
-    n0 = ctx.launch_count()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    n0 = sum(cg.launch_count() for cg in groups)
+    marks = []
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush.add_(1.0)
             dX.zero_()
             torch.cuda.synchronize()
-            ev[k][0].record(stream)
-            ctx.fgmres_device(kind, dB.data_ptr(), dX.data_ptr(), nb, kc, want_report=False)
-            ev[k][1].record(stream)
+            marks.append(timed(lambda: run_groups(lambda g: solve_group(g))))
         torch.cuda.synchronize()
-    launches = (ctx.launch_count() - n0) // max(1, args.steps)
-    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    launches = (sum(cg.launch_count() for cg in groups) - n0) // max(1, args.steps)
+    t_ms = sum(max(e0.elapsed_time(e) for e in ends) for e0, ends in marks)
     barrier(ws)
     t_ms = max_over_ranks(t_ms, ws)
     solves = nb * args.steps * ws
@@ -281,17 +322,18 @@ def run_ours(args, ws, rank, local):
     # D2H of X inside the timed region every step
     Bpin = torch.from_numpy(Bh).pin_memory()
     Xpin = torch.zeros_like(Bpin).pin_memory()
-    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    Bn, Xn = Bpin.numpy(), Xpin.numpy()
+    emarks = []
     for k in range(args.steps):
         flush.add_(1.0)
         torch.cuda.synchronize()
-        ee[k][0].record(stream)
-        X, _ = ctx.fgmres(kind, Bpin.numpy(), kc, out=Xpin.numpy())
-        ee[k][1].record(stream)
+        emarks.append(timed(lambda: run_groups(
+            lambda g: groups[g].fgmres(kind, Bn[bounds[g]:bounds[g + 1]], kc, out=Xn[bounds[g]:bounds[g + 1]]))))
     torch.cuda.synchronize()
-    e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ee), ws)
+    e_ms = max_over_ranks(sum(max(e0.elapsed_time(e) for e in ends) for e0, ends in emarks), ws)
     e2e = {"value": solves / (e_ms / 1e3), "unit": "solves/s", "h2d_bytes_per_step": int(Bh.nbytes),
-           "d2h_bytes_per_step": int(Bh.nbytes), "path": "hb_fgmres (pinned host c128 buffers)"}
+           "d2h_bytes_per_step": int(Bh.nbytes), "path": f"hb_fgmres (pinned host c128 buffers), {G} column groups"}
+    d_g0 = (dB[bounds[0]:bounds[1]], dX[bounds[0]:bounds[1]], bounds[1] - bounds[0])
 
     # ---- single-solve latency (R = 1)
     lat = None
@@ -311,13 +353,14 @@ def run_ours(args, ws, rank, local):
 
     # ---- roofline pass: same workload, per-kernel-class CUDA events on the library
     # stream (eager launches; the timed region above replays CUDA graphs)
-    # the two half-batch V-cycle streams are serialised for this pass so that
-    # per-launch event times are not inflated by the other stream's kernels
+    # one column group, its two half-batch V-cycle streams serialised, so that
+    # per-launch event times are not inflated by concurrently running kernels
     ctx.set_option("split_vcycle", 0)
     ctx.prof_reset()
     ctx.prof_enable(True)
     for _ in range(args.steps):
-        solve()
+        d_g0[1].zero_()
+        ctx.fgmres_device(kind, d_g0[0].data_ptr(), d_g0[1].data_ptr(), d_g0[2], kc, want_report=False)
     torch.cuda.synchronize()
     ctx.prof_enable(False)
     ctx.set_option("split_vcycle", 1)
@@ -367,12 +410,14 @@ def run_ours(args, ws, rank, local):
                        "restart": cfg["restart"], "precond": kind, "iterations": int(max(rep.iterations)),
                        "all_converged": bool(all(rep.converged)),
                        "l2": "working set > L2; L2 flushed (512 MiB write) between steps",
-                       "single_solve_latency_ms": lat, "parallelism": f"independent solves x{ws} GPUs"},
+                       "single_solve_latency_ms": lat, "column_groups_per_gpu": G,
+                       "parallelism": f"independent solves x{ws} GPUs"},
             "roofline": rl, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(args.config, cfg)
-    ctx.close()
+    for cg in groups:
+        cg.close()
     if rank == 0 and args.also:
         line["also"] = {}
         for nm in [s for s in args.also.split(",") if s]:
@@ -457,6 +502,8 @@ def main():
     ap.add_argument("--also", default="c1,c2,c3", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
+    ap.add_argument("--groups", type=int, default=2, help="independent column groups (solver contexts on their own "
+                                                          "streams and host threads) per GPU")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

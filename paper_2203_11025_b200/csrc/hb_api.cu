@@ -870,6 +870,10 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_wide_legs = value != 0;
   else if (k == "legs_wd")
     ctx->opt_legs_wd = value != 0;
+  else if (k == "conv_rows")
+    ctx->opt_conv_rows = value != 0;
+  else if (k == "conv_rows_ring")
+    ctx->conv_rows_ring = value == 3 ? 3 : 4;
   else if (k == "stream_vcycle")
     ctx->opt_stream = value != 0;
   else

@@ -97,6 +97,7 @@ struct ConvW {
   DBuf<float> dw;           // device packed weights [9*cin][cout] (k-major rows), SIMT path
   DBuf<float> db;
   DBuf<float> dwh, dwl;     // tensor-core path: [cout][9*cin] tf32 hi / lo split
+  DBuf<float> dwrow;        // row-streaming path (Cout = 16): packed (chunk, kx) blocks, hb_conv_rows.cu
 };
 
 struct Net {
@@ -139,8 +140,11 @@ void launch_down_fused(Context& c, const LevelView& L, float damping, int offset
 void launch_up_fused(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B,
                      const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
                      float2* z);
-// tensor-core conv (hb_conv_tc.cu)
+// tensor-core conv (hb_conv_tc.cu, hb_conv_rows.cu)
 void conv_tc_prepare(ConvW& cw);
+void conv_rows_prepare(ConvW& cw);
+bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
+                      const float* bsrc, int cb, bool b_ctx, int relu, float* out);
 bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                     const float* bsrc, int cb, bool b_ctx, int relu, float* out);
 // row-streaming legs, zero initial guess (hb_mg_stream.cu)
@@ -231,7 +235,9 @@ struct Context {
   // options
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
-       opt_coarse_reg = true, opt_wide_legs = false, opt_legs_wd = false;
+       opt_coarse_reg = true, opt_wide_legs = false, opt_legs_wd = false,
+       opt_conv_rows = true;
+  int conv_rows_ring = 4;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {

@@ -394,6 +394,7 @@ struct NScope {
 static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, long long sa,
                  int ca, const float* b, long long sb, int cb, int relu, float* out) {
   if (ca + cb != cw.cin) throw HbError{HB_ERR_ARG, "conv input channels mismatch"};
+  if (launch_conv_rows(c, cw, B, act, H, W, a, ca, b, cb, b != nullptr && sb == 0, relu, out)) return;
   if (launch_conv_tc(c, cw, B, act, H, W, a, ca, b, cb, b != nullptr && sb == 0, relu, out)) return;
   ConvArgs p{B, H, W, a, sa, ca, b, sb, cb, cw.dw.p, cw.db.p, cw.cout, relu, out, act};
   const int cin = ca + cb;
@@ -522,6 +523,7 @@ void net_upload(Context& c, int slot) {
     HB_CUDA(cudaMemcpy(cw.dw.p, pk.data(), pk.size() * sizeof(float), cudaMemcpyHostToDevice));
     HB_CUDA(cudaMemcpy(cw.db.p, cw.b.data(), cw.b.size() * sizeof(float), cudaMemcpyHostToDevice));
     conv_tc_prepare(cw);
+    conv_rows_prepare(cw);
   }
   n.dirty = false;
   if (slot == 1) c.ctx_valid = false;

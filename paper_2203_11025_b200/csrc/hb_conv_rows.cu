@@ -42,10 +42,13 @@ constexpr int CR_MAXRING = 4;
 struct CrParams {
   int B, H, W, relu;
   int ca, cb, b_is_ctx;  // source channels (multiples of 16)
-  int nch;               // (ca + cb) / 16: 1 or 2
+  int nch;               // (ca + cb) / 16 input chunks
+  int nslice;            // cout / 16 output slices (one work item each)
+  int gch;               // chunks per step (input row group), 1 or 2
   int rb;                // output rows per work item
   int ring, na;          // D ring depth, A slots
-  const float* wrow;     // [nch][3 kx][96 rows][16 ci] packed, SW64-swizzled
+  int rbuf;              // input-row smem buffers (<= CR_RBUF)
+  const float* wrow;     // [nslice][nch][3 kx][96 rows][16 ci] packed, SW64-swizzled
   const float* bias;
   float* out;
   const int* act;
@@ -60,13 +63,14 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
   __shared__ uint32_t tmem_slot;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  const int nch = p.nch, ring = p.ring, na = p.na;
+  const int nch = p.nch, ring = p.ring, na = p.na, gch = p.gch, nrb = p.rbuf;
+  const int ngrp = (nch + gch - 1) / gch;  // steps per input row
   const int nca = p.ca / 16;
-  const int rowbuf = nch * CR_BOX;
-  unsigned char* wsm = base + CR_RBUF * rowbuf;
+  const int rowbuf = gch * CR_BOX;
+  unsigned char* wsm = base + nrb * rowbuf;
   const int strips = p.W / 128, rblocks = (p.H + p.rb - 1) / p.rb;
-  const int nitems = p.B * strips * rblocks;
-  const int aw = nch * 3 * 32;   // TMEM columns of one A slot: (chunk, kx) x [hi 16 | lo 16]
+  const int nitems = p.nslice * p.B * strips * rblocks;
+  const int aw = gch * 3 * 32;   // TMEM columns of one A slot: (chunk, kx) x [hi 16 | lo 16]
   const int a0 = ring * 96;      // first A-slot column (D ring first)
   if (threadIdx.x == 0) {
     for (int i = 0; i < CR_RBUF; ++i) {
@@ -94,40 +98,46 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
 
-  // item -> image b, strip x0, output rows [y0, y1); rows are the fastest index
+  // item -> output slice sl, image b, strip x0, output rows [y0, y1); rows fastest
+  int sl = 0;
   auto decode = [&](int item, int& b, int& x0, int& y0, int& y1) {
-    const int rbk = item % rblocks, rest = item / rblocks;
+    const int rbk = item % rblocks;
+    int rest = item / rblocks;
     x0 = (rest % strips) * 128;
-    b = rest / strips;
+    rest /= strips;
+    b = rest % p.B;
+    sl = rest / p.B;
     y0 = rbk * p.rb;
     y1 = min(p.H, y0 + p.rb);
   };
 
   if (warp == 0) {
     // ---------------- producer: weights once, then one row box per chunk and input row
-    mbar_expect_tx_elect(&bar_w, uint32_t(nch * 3 * CR_WBLK));
-    bulk_load_elect(wsm, p.wrow, uint32_t(nch * 3 * CR_WBLK), &bar_w);
+    mbar_expect_tx_elect(&bar_w, uint32_t(p.nslice * nch * 3 * CR_WBLK));
+    bulk_load_elect(wsm, p.wrow, uint32_t(p.nslice * nch * 3 * CR_WBLK), &bar_w);
     int s = 0;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       int b, x0, y0, y1;
       decode(item, b, x0, y0, y1);
       if (p.act && !p.act[b]) continue;
       const int bb = p.b_is_ctx ? 0 : b;
-      for (int r = y0 - 1; r <= y1; ++r, ++s) {
-        const int rb_ = s % CR_RBUF;
-        if (s >= CR_RBUF) mbar_wait(&bar_rempty[rb_], ((s / CR_RBUF) - 1) & 1);
-        const bool valid = r >= 0 && r < p.H;
-        mbar_expect_tx_elect(&bar_rfull[rb_], valid ? uint32_t(nch * 130 * 64) : 0u);
-        if (valid) {
-          for (int ch = 0; ch < nch; ++ch) {
-            unsigned char* dst = base + rb_ * rowbuf + ch * CR_BOX;
-            if (ch < nca)
-              tma_load_4d_elect(dst, &mapA, &bar_rfull[rb_], ch * 16, x0 - 1, r, b);
-            else
-              tma_load_4d_elect(dst, &mapB, &bar_rfull[rb_], (ch - nca) * 16, x0 - 1, r, bb);
+      for (int r = y0 - 1; r <= y1; ++r)
+        for (int g = 0; g < ngrp; ++g, ++s) {
+          const int rb_ = s % nrb;
+          if (s >= nrb) mbar_wait(&bar_rempty[rb_], ((s / nrb) - 1) & 1);
+          const bool valid = r >= 0 && r < p.H;
+          const int c0 = g * gch, c1 = min(nch, c0 + gch);
+          mbar_expect_tx_elect(&bar_rfull[rb_], valid ? uint32_t((c1 - c0) * 130 * 64) : 0u);
+          if (valid) {
+            for (int ch = c0; ch < c1; ++ch) {
+              unsigned char* dst = base + rb_ * rowbuf + (ch - c0) * CR_BOX;
+              if (ch < nca)
+                tma_load_4d_elect(dst, &mapA, &bar_rfull[rb_], ch * 16, x0 - 1, r, b);
+              else
+                tma_load_4d_elect(dst, &mapB, &bar_rfull[rb_], (ch - nca) * 16, x0 - 1, r, bb);
+            }
           }
         }
-      }
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer (whole warp, elected lane issues)
@@ -137,31 +147,36 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     const uint32_t wlo0 = __shfl_sync(0xffffffffu, (smem_u32(wsm) >> 4) | (1u << 16), 0);
     mbar_wait(&bar_w, 0);
-    int s = 0;
+    int s = 0, rs = 0;  // step, input-row step (D slot index)
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       int b, x0, y0, y1;
       decode(item, b, x0, y0, y1);
       if (p.act && !p.act[b]) continue;
-      for (int r = y0 - 1; r <= y1; ++r, ++s) {
-        const int ds = s % ring, as = s % na;
-        if (s >= ring) mbar_wait(&bar_dempty[ds], ((s / ring) - 1) & 1);  // epilogue released this slot
-        mbar_wait(&bar_afull[as], (s / na) & 1);
-        tc_fence_after();
-        if (r >= 0 && r < p.H) {
-          const uint32_t d = tbase + uint32_t(ds * 96);
-          uint32_t first = 0;
-          for (int u = 0; u < nch * 3; ++u) {
-            const uint32_t lw = wlo0 + uint32_t(u * (CR_WBLK >> 4));
-            const uint32_t ta = tbase + uint32_t(a0 + as * aw + u * 32);
+      for (int r = y0 - 1; r <= y1; ++r, ++rs) {
+        const int ds = rs % ring;
+        if (rs >= ring) mbar_wait(&bar_dempty[ds], ((rs / ring) - 1) & 1);  // epilogue released this slot
+        const uint32_t d = tbase + uint32_t(ds * 96);
+        uint32_t first = 0;
+        for (int g = 0; g < ngrp; ++g, ++s) {
+          const int as = s % na;
+          mbar_wait(&bar_afull[as], (s / na) & 1);
+          tc_fence_after();
+          if (r >= 0 && r < p.H) {
+            const int c0 = g * gch, c1 = min(nch, c0 + gch);
+            for (int u = 0; u < (c1 - c0) * 3; ++u) {
+              const int ch = c0 + u / 3, kx = u - 3 * (u / 3);
+              const uint32_t lw = wlo0 + uint32_t(((sl * nch + ch) * 3 + kx) * (CR_WBLK >> 4));
+              const uint32_t ta = tbase + uint32_t(a0 + as * aw + u * 32);
 #pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-              umma_ts(d, ta + 8 * kk, lw + 2 * kk, hi16, id96, first);            // A_hi [W_hi | W_lo]
-              umma_ts(d + 48, ta + 16 + 8 * kk, lw + 2 * kk, hi16, id48, 1u);   // A_lo W_hi -> correction
-              first = 1;
+              for (int kk = 0; kk < 2; ++kk) {
+                umma_ts(d, ta + 8 * kk, lw + 2 * kk, hi16, id96, first);            // A_hi [W_hi | W_lo]
+                umma_ts(d + 48, ta + 16 + 8 * kk, lw + 2 * kk, hi16, id48, 1u);   // A_lo W_hi -> correction
+                first = 1;
+              }
             }
           }
+          umma_commit_elect(&bar_aempty[as]);
         }
-        umma_commit_elect(&bar_aempty[as]);
         umma_commit_elect(&bar_dfull[ds]);
       }
     }
@@ -174,15 +189,17 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
       int b, x0, y0, y1;
       decode(item, b, x0, y0, y1);
       if (p.act && !p.act[b]) continue;
-      for (int r = y0 - 1; r <= y1; ++r, ++s) {
-        const int rb_ = s % CR_RBUF, as = s % na;
-        mbar_wait(&bar_rfull[rb_], (s / CR_RBUF) & 1);
+      for (int r = y0 - 1; r <= y1; ++r)
+       for (int g = 0; g < ngrp; ++g, ++s) {
+        const int rb_ = s % nrb, as = s % na;
+        mbar_wait(&bar_rfull[rb_], (s / nrb) & 1);
         if (s >= na) mbar_wait(&bar_aempty[as], ((s / na) - 1) & 1);
         tc_fence_after();
         if (r >= 0 && r < p.H) {
           const uint32_t ta = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(a0 + as * aw);
-          for (int u = half; u < nch * 3; u += 2) {
-            const int ch = u / 3, kx = u - 3 * ch;
+          const int nu = (min(nch, (g + 1) * gch) - g * gch) * 3;
+          for (int u = half; u < nu; u += 2) {
+            const int ch = u / 3, kx = u - 3 * ch;  // chunk within this step's group
             const int hp = pix + kx;  // halo pixel (the box starts at x0 - 1)
             const unsigned char* row = base + rb_ * rowbuf + ch * CR_BOX + hp * 64;
             const int f = (hp >> 1) & 3;  // SWIZZLE_64B: 16-B chunk c of row hp sits at c ^ f
@@ -212,10 +229,8 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
     // ---------------- epilogue: out[y] = bias + sum_ky D_{y+ky-1}[ky] (main + correction)
     const int q = warp & 3;
     const int pix = 32 * q + lane;
-    float bias[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) bias[i] = __ldg(p.bias + i);
     const uint32_t trow = tmem_base + (uint32_t(32 * q) << 16);
+    const int cout = p.nslice * 16;
     int sb = 0;  // step of the item's first input row
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       int b, x0, y0, y1;
@@ -229,7 +244,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
         tc_fence_after();
         float o[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) o[i] = bias[i];
+        for (int i = 0; i < 16; ++i) o[i] = __ldg(p.bias + sl * 16 + i);
 #pragma unroll
         for (int ky = 0; ky < 3; ++ky) {
           const int rr = y + ky - 1;
@@ -246,7 +261,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
 #pragma unroll
           for (int i = 0; i < 16; ++i) o[i] = fmaxf(o[i], 0.f);
         }
-        float* dst = p.out + ((size_t(b) * p.H + y) * p.W + x0 + pix) * 16;
+        float* dst = p.out + ((size_t(b) * p.H + y) * p.W + x0 + pix) * cout + sl * 16;
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
           *reinterpret_cast<float4*>(dst + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
@@ -273,9 +288,9 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
 // rows (part, ky, co), part 0 = W_hi, 1 = W_lo (tf32 round-to-nearest split),
 // stored pre-swizzled (SWIZZLE_64B) so a linear bulk copy lands in UMMA layout
 void conv_rows_prepare(ConvW& cw) {
-  if (cw.cout != 16 || cw.cin % 16 || cw.cin > 32) return;
-  const int nch = cw.cin / 16;
-  std::vector<float> pk(size_t(nch) * 3 * 96 * 16, 0.f);
+  if (cw.cout % 16 || cw.cout > 32 || cw.cin % 16 || cw.cin > 64) return;
+  const int nch = cw.cin / 16, nsl = cw.cout / 16;
+  std::vector<float> pk(size_t(nsl) * nch * 3 * 96 * 16, 0.f);
   auto tf32 = [](float x) {
     uint32_t u;
     std::memcpy(&u, &x, 4);
@@ -284,6 +299,7 @@ void conv_rows_prepare(ConvW& cw) {
     std::memcpy(&r, &u, 4);
     return r;
   };
+  for (int sl = 0; sl < nsl; ++sl)
   for (int ch = 0; ch < nch; ++ch)
     for (int kx = 0; kx < 3; ++kx)
       for (int part = 0; part < 2; ++part)
@@ -291,11 +307,11 @@ void conv_rows_prepare(ConvW& cw) {
           for (int co = 0; co < 16; ++co)
             for (int k = 0; k < 16; ++k) {
               const int ci = ch * 16 + k;
-              const float w = cw.w[(size_t(co) * cw.cin + ci) * 9 + ky * 3 + kx];
+              const float w = cw.w[(size_t(sl * 16 + co) * cw.cin + ci) * 9 + ky * 3 + kx];
               const float h = tf32(w);
               const float v = part == 0 ? h : tf32(w - h);
               const int row = part * 48 + ky * 16 + co;
-              const size_t blk = size_t(ch * 3 + kx) * 96 * 16;
+              const size_t blk = size_t((sl * nch + ch) * 3 + kx) * 96 * 16;
               const int pos = ((k >> 2) ^ ((row >> 1) & 3)) * 4 + (k & 3);  // SW64 within the 512-B atom
               pk[blk + size_t(row) * 16 + size_t(pos)] = v;
             }
@@ -306,7 +322,9 @@ void conv_rows_prepare(ConvW& cw) {
 bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                       const float* bsrc, int cb, bool b_ctx, int relu, float* out) {
   if (!c.opt_conv_rows || !c.opt_tc_conv) return false;
-  if (cw.cout != 16 || !cw.dwrow.p || W % 128 || ca % 16 || cb % 16 || ca + cb != cw.cin || cw.cin > 32) return false;
+  if (cw.cout % 16 || cw.cout > 32 || !cw.dwrow.p || W % 128 || ca % 16 || cb % 16 || ca + cb != cw.cin ||
+      cw.cin > 64)
+    return false;
   CrParams p{};
   p.B = B;
   p.H = H;
@@ -316,29 +334,35 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
   p.cb = cb;
   p.b_is_ctx = b_ctx ? 1 : 0;
   p.nch = cw.cin / 16;
-  p.ring = p.nch == 1 ? c.conv_rows_ring : 3;
-  p.na = (p.ring * 96 + 2 * p.nch * 96 <= 512) ? 2 : 1;
+  p.nslice = cw.cout / 16;
+  p.gch = p.nch == 1 ? 1 : 2;
+  p.ring = p.gch == 1 ? c.conv_rows_ring : 3;
+  p.na = (p.ring * 96 + 2 * p.gch * 96 <= 512) ? 2 : 1;
   const int strips = W / 128;
   // rows per work item: enough items for ~2 per SM, each >= 4 rows (halo: 2 extra input rows)
-  p.rb = std::max(4, std::min(32, (B * strips * H) / std::max(1, 2 * c.num_sms)));
+  p.rb = std::max(4, std::min(32, (cw.cout / 16 * B * strips * H) / std::max(1, 2 * c.num_sms)));
   p.wrow = cw.dwrow.p;
   p.bias = cw.db.p;
   p.out = out;
   p.act = act;
   const CUtensorMap mA = act_map(a, B, H, W, ca, 16, 130, 1);
   const CUtensorMap mB = cb ? act_map(bsrc, b_ctx ? 1 : B, H, W, cb, 16, 130, 1) : mA;
-  const size_t smem = size_t(CR_RBUF) * p.nch * CR_BOX + size_t(p.nch) * 3 * CR_WBLK + 1024;
+  const size_t wbytes = size_t(p.nslice) * p.nch * 3 * CR_WBLK;
+  p.rbuf = CR_RBUF;
+  while (p.rbuf > 2 && size_t(p.rbuf) * p.gch * CR_BOX + wbytes + 1024 > 200 * 1024) --p.rbuf;
+  const size_t smem = size_t(p.rbuf) * p.gch * CR_BOX + wbytes + 1024;
+  if (smem > 200 * 1024) return false;
   static int attr_dev = -1;
   if (attr_dev != c.device) {
     HB_CUDA(cudaFuncSetAttribute(k_conv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr_dev = c.device;
   }
-  const int items = B * strips * ((H + p.rb - 1) / p.rb);
+  const int items = p.nslice * B * strips * ((H + p.rb - 1) / p.rb);
   const int grid = std::min(items, c.num_sms);
   const int tok = prof_begin(c, PC_CONV);
   if (c.prof_detail)
     c.prof_label = "conv_rows " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
-                   std::to_string(ca) + "+" + std::to_string(cb) + "->16";
+                   std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
   k_conv_rows<<<grid, CR_THREADS, smem, c.stream>>>(mA, mB, p);
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());

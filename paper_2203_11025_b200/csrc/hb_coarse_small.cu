@@ -619,13 +619,17 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
   const int tok = prof_begin(c, PC_COARSE);
   const int nt = c.coarse_threads;
   static bool reg_attr = false;
-  if (c.opt_coarse_reg && iters <= 10 && N <= 1024 && nt == 256) {
+  if (c.opt_coarse_reg && iters <= 10 && N <= 1024 && (nt == 256 || nt == 512)) {
     if (!reg_attr) {
       HB_CUDA(cudaFuncSetAttribute(k_coarse_reg<256, 4, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+      HB_CUDA(cudaFuncSetAttribute(k_coarse_reg<512, 2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       reg_attr = true;
     }
     const size_t su = 2 * sizeof(float2) * size_t(L.nx + 2) * (L.ny + 2);
-    k_coarse_reg<256, 4, 10><<<B, 256, su, c.stream>>>(L, iters, act, f, x);
+    if (nt == 512)
+      k_coarse_reg<512, 2, 10><<<B, 512, su, c.stream>>>(L, iters, act, f, x);
+    else
+      k_coarse_reg<256, 4, 10><<<B, 256, su, c.stream>>>(L, iters, act, f, x);
   } else if (nt == 1024 && N <= 1024) {
     k_coarse_small<1024, 1, 15><<<B, 1024, smem, c.stream>>>(L, iters, act, f, x);
   } else if (nt >= 512 && N <= 1024) {

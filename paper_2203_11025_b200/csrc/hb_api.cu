@@ -57,7 +57,7 @@ void prof_collect(Context& c) {
     float ms = 0.f;
     HB_CUDA(cudaEventElapsedTime(&ms, e.second.first, e.second.second));
     times[i] = ms;
-    c.prof[size_t(e.first)].ms += ms;
+    if (e.first >= 0) c.prof[size_t(e.first)].ms += ms;  // < 0: launch with no active column, not counted
     c.ev_pool.push_back(e.second.first);
     c.ev_pool.push_back(e.second.second);
   }
@@ -77,6 +77,10 @@ void prof_end(Context& c, int cls, int token, double bytes, double flops) {
                                           size_t(token), 0.0, bytes, flops});
   c.prof_label.clear();
   Prof& p = c.prof[size_t(cls)];
+  if (c.prof_scale <= 0.0) {  // every column frozen: the launch is a no-op, keep it out of the rates
+    c.ev_pending[size_t(token)].first = -1;
+    return;
+  }
   p.launches += 1;
   p.bytes += bytes * c.prof_scale;
   p.flops += flops * c.prof_scale;
@@ -870,6 +874,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_wide_legs = value != 0;
   else if (k == "legs_wd")
     ctx->opt_legs_wd = value != 0;
+  else if (k == "lean_legs")
+    ctx->opt_lean_legs = value != 0;
   else if (k == "conv_rows")
     ctx->opt_conv_rows = value != 0;
   else if (k == "conv_rows_ring")

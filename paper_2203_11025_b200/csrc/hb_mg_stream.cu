@@ -246,6 +246,87 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
   }
 }
 
+// Lean down leg: same geometry and arithmetic as k_down_stream, written
+// branch-free for the issue-bound regime -- column and row validity become
+// 0/1 masks folded into the column scale (loads hit clamped, always-valid
+// addresses), shuffles are unconditional, row offsets are 32-bit, and the
+// 3-row window rotates through registers in a 2x-unrolled loop.
+struct RowIn {
+  float2 fa, fb, wa, wb, da, db;  // f (scaled, masked), wD^-1, D at the lane's two fine columns
+};
+
+__global__ void __launch_bounds__(32 * WARPS) k_down_lean(LevelView L, int offset, int rows_per_chunk, const int* act,
+                                                          const float2* __restrict__ f, const float* fscale,
+                                                          float2* __restrict__ fc) {
+  const int b = blockIdx.z;
+  if (act && !act[b]) return;
+  const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
+  const int jx = blockIdx.x * SW_OUT - 1 + lane;  // lane 0 / 31: halo
+  const int c0 = 2 * jx + offset;
+  const int jy0 = (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
+  if (jy0 >= cny) return;
+  const int jy1 = min(cny, jy0 + rows_per_chunk);
+  const float2* fb = f + size_t(b) * nx * ny;
+  const float s = fscale ? fscale[b] : 1.0f;
+  const float ih2 = L.inv_h2;
+  const int ca = min(max(c0, 0), nx - 1), cb = min(max(c0 + 1, 0), nx - 1);
+  const float sa = (c0 >= 0 && c0 < nx) ? s : 0.f, sb = (c0 + 1 >= 0 && c0 + 1 < nx) ? s : 0.f;
+  const float ma = sa != 0.f ? 1.f : 0.f, mb = sb != 0.f ? 1.f : 0.f;
+  auto load = [&](int y) {
+    const bool ok = y >= 0 && y < ny;
+    const int o = (ok ? y : 0) * nx;
+    const float rm = ok ? 1.f : 0.f;
+    RowIn r;
+    r.fa = cscale(__ldg(fb + o + ca), sa * rm);
+    r.fb = cscale(__ldg(fb + o + cb), sb * rm);
+    r.wa = __ldg(L.wdi + o + ca);
+    r.wb = __ldg(L.wdi + o + cb);
+    r.da = __ldg(L.dM + o + ca);
+    r.db = __ldg(L.dM + o + cb);
+    return r;
+  };
+  const int yb = 2 * jy0 + offset - 1;
+  const int yend = 2 * (jy1 - 1) + offset + 1;
+  RowIn r_c = load(yb), r_p1 = load(yb + 1), r_p2 = load(yb + 2);
+  RowIn r_m = load(yb - 1);
+  float2 vma = cmul(r_m.fa, r_m.wa), vmb = cmul(r_m.fb, r_m.wb);
+  float2 vca = cmul(r_c.fa, r_c.wa), vcb = cmul(r_c.fb, r_c.wb);
+  float2 h_m2 = make_float2(0.f, 0.f), h_m1 = h_m2;
+  const bool emit_col = lane >= 1 && lane <= SW_OUT && jx < cnx;
+  float2* fcb = fc + size_t(b) * cnx * cny;
+#pragma unroll 2
+  for (int y = yb; y <= yend; ++y) {
+    const RowIn r_p3 = load(y + 3);  // in flight during this row
+    const float2 vpa = cmul(r_p1.fa, r_p1.wa), vpb = cmul(r_p1.fb, r_p1.wb);
+    const float2 left = shfl_up2(vcb), right = shfl_down2(vca);
+    float2 nb = cadd(cadd(vma, vpa), cadd(left, vcb));
+    float2 mva = cmul(r_c.da, vca);
+    mva.x = fmaf(-ih2, nb.x, mva.x);
+    mva.y = fmaf(-ih2, nb.y, mva.y);
+    nb = cadd(cadd(vmb, vpb), cadd(vca, right));
+    float2 mvb = cmul(r_c.db, vcb);
+    mvb.x = fmaf(-ih2, nb.x, mvb.x);
+    mvb.y = fmaf(-ih2, nb.y, mvb.y);
+    const float rowm = (y >= 0 && y < ny) ? 1.f : 0.f;
+    const float2 ra = cscale(csub(r_c.fa, mva), ma * rowm), rb = cscale(csub(r_c.fb, mvb), mb * rowm);
+    const float2 rl = shfl_up2(rb);  // r at c0 - 1
+    const float2 h = caxpy(cscale(ra, 0.5f), 0.25f, cadd(rl, rb));
+    // y = 2 jy + o + 1 closes coarse row jy
+    const int t = y - offset - 1;
+    if (t >= 2 * jy0 && ((t & 1) == 0) && emit_col)
+      fcb[size_t(t >> 1) * cnx + jx] = caxpy(cscale(h_m1, 0.5f), 0.25f, cadd(h_m2, h));
+    h_m2 = h_m1;
+    h_m1 = h;
+    vma = vca;
+    vmb = vcb;
+    vca = vpa;
+    vcb = vpb;
+    r_c = r_p1;
+    r_p1 = r_p2;
+    r_p2 = r_p3;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Wide variants: each lane owns 4 consecutive fine columns F..F+3 (F a multiple
 // of 4, so a lane's columns are all inside or all outside the grid and its
@@ -390,7 +471,9 @@ void launch_down_stream(Context& c, const LevelView& L, float damping, int offse
     k_down_stream4<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
   } else {
     const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
-    if (c.opt_legs_wd)
+    if (c.opt_lean_legs)
+      k_down_lean<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
+    else if (c.opt_legs_wd)
       k_down_stream<true><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, rpc, act, f, fscale, fc);
     else
       k_down_stream<false><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, rpc, act, f, fscale, fc);

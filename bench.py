@@ -383,6 +383,16 @@ def run_ours(args, ws, rank, local):
             row["gbs"] = v["bytes"] / (v["ms"] / 1e3) / 1e9
             row["hbm_frac"] = row["gbs"] / pk.get("hbm_gbs", 6650.0)
         kernels[k] = row
+    # BASELINE's second metric: precond-apply % of roofline -- the V-cycle classes
+    # (legs + coarsest solve) per apply, algorithmic bytes vs HBM peak
+    pcls = [k for k in ("vcycle_down", "vcycle_up", "coarse_solve", "smooth", "transfer") if prof.get(k, {}).get("launches")]
+    n_apply = max(1, prof.get("coarse_solve", {}).get("launches", 0))
+    pc_ms = sum(prof[k]["ms"] for k in pcls)
+    pc_bytes = sum(prof[k]["bytes"] for k in pcls)
+    precond_apply = {"classes": pcls, "applies": n_apply, "us_per_apply": 1e3 * pc_ms / n_apply,
+                     "bytes_per_apply": pc_bytes / n_apply,
+                     "gbs": pc_bytes / (pc_ms / 1e3) / 1e9 if pc_ms > 0 else 0.0}
+    precond_apply["hbm_frac"] = precond_apply["gbs"] / pk.get("hbm_gbs", 6650.0)
     name, p = max(prof.items(), key=lambda kv: kv[1]["ms"])
     if p["flops"] > 0:
         achieved = p["flops"] / (p["ms"] / 1e3) / 1e12
@@ -416,7 +426,8 @@ def run_ours(args, ws, rank, local):
                        "l2": "working set > L2; L2 flushed (512 MiB write) between steps",
                        "single_solve_latency_ms": lat, "column_groups_per_gpu": G,
                        "parallelism": f"independent solves x{ws} GPUs"},
-            "roofline": rl, "kernels": kernels, "e2e": e2e, "gpu_launches": int(launches),
+            "roofline": rl, "kernels": kernels, "precond_apply": precond_apply, "e2e": e2e,
+            "gpu_launches": int(launches),
             "clocks": clk.summary()}
     if rank == 0 and ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_sample(args.config, cfg)
@@ -481,6 +492,13 @@ def fixed_budget(name, local, args, ws, rank):
     # the measured HBM peak -- meaningful here, the working sets exceed L2 from c2 on
     pk, _ = peaks()
     total = max(1e-9, sum(v["ms"] for v in prof.values()))
+    pcls = [k for k in ("vcycle_down", "vcycle_up", "coarse_solve", "smooth", "transfer") if prof.get(k, {}).get("launches")]
+    pc_ms = sum(prof[k]["ms"] for k in pcls)
+    pc_bytes = sum(prof[k]["bytes"] for k in pcls)
+    if pc_ms > 0:
+        out["vcycle_apply"] = {"classes": pcls, "gbs": pc_bytes / (pc_ms / 1e3) / 1e9,
+                               "hbm_frac": pc_bytes / (pc_ms / 1e3) / 1e9 / pk.get("hbm_gbs", 6650.0),
+                               "ms_per_iteration": pc_ms / its}
     out["kernels"] = {}
     for k, v in prof.items():
         if not v["launches"]:

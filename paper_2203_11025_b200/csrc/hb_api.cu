@@ -104,11 +104,12 @@ static void require_hier(Context& c) {
   if (!c.has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built (hb_build_hierarchy)"};
 }
 
-static void fill_level_device(Level& L, double omega, double alpha, double beta, double damping, bool fp64A) {
+static void fill_level_device(Level& L, double omega, double alpha, double beta, double damping, bool fp64A,
+                              bool fp64M) {
   const size_t n = L.N();
   const double inv_h2 = 1.0 / (L.h * L.h);
   std::vector<float2> dm(n), da(n), wd(n);
-  std::vector<double2> da64(fp64A ? n : 0);
+  std::vector<double2> da64(fp64A ? n : 0), dm64(fp64M ? n : 0);
   std::vector<float> kf(n);
   const std::complex<double> sh(alpha, -beta), sh0(1.0, 0.0);
   for (size_t i = 0; i < n; ++i) {
@@ -123,6 +124,7 @@ static void fill_level_device(Level& L, double omega, double alpha, double beta,
     wd[i] = make_float2(float(w.real()), float(w.imag()));
     da[i] = make_float2(float(dAd.real()), float(dAd.imag()));
     if (fp64A) da64[i] = make_double2(dAd.real(), dAd.imag());
+    if (fp64M) dm64[i] = make_double2(dMd.real(), dMd.imag());
     kf[i] = float(L.k2[i]);
   }
   L.dM.ensure(n);
@@ -136,6 +138,10 @@ static void fill_level_device(Level& L, double omega, double alpha, double beta,
   if (fp64A) {
     L.dA64.ensure(n);
     HB_CUDA(cudaMemcpy(L.dA64.p, da64.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+  if (fp64M) {
+    L.dM64.ensure(n);
+    HB_CUDA(cudaMemcpy(L.dM64.p, dm64.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
   }
 }
 
@@ -166,9 +172,13 @@ static void coarsest_solve(Context& c, int B, int c0, const int* act, const floa
   float2* tbuf = L.t.p + size_t(c0) * L.N();
   switch (c.vc.coarse_solver) {
     case HB_COARSE_GMRES:
-      if (!(c.opt_small_coarse && launch_coarse_small(c, V, c.vc.coarse_iters, B, act, f, out)))
-        launch_coarse_gmres(c, V, c.vc.coarse_iters, B, act, f, out,
-                            c.scratch_c64.p + size_t(c0) * (kMaxCoarseIters + 2) * L.N());
+      if (c.opt_small_coarse && launch_coarse_small(c, V, c.vc.coarse_iters, B, act, f, out)) break;
+      if (c.opt_coarse_krylov && L.N() > 2048 && c.vc.coarse_iters <= kMaxRestart) {  // multi-CTA Krylov kernels: fills the GPU at 128^2+
+        coarse_krylov_solve(c, L, c.vc.coarse_iters, B, c0 != 0 ? 1 : 0, f, out);
+        break;
+      }
+      launch_coarse_gmres(c, V, c.vc.coarse_iters, B, act, f, out,
+                          c.scratch_c64.p + size_t(c0) * (kMaxCoarseIters + 2) * L.N());
       break;
     case HB_COARSE_JACOBI: {  // A3: iters damped sweeps from zero
       const float w = float(c.vc.damping);
@@ -606,7 +616,8 @@ int hb_build_hierarchy(hb_ctx* ctx, const hb_vcycle_cfg* cfg) {
     ctx->levels.push_back(std::move(L));
   }
   for (size_t l = 0; l < ctx->levels.size(); ++l)
-    fill_level_device(*ctx->levels[l], ctx->omega, cfg->alpha, cfg->beta, cfg->damping, l == 0);
+    fill_level_device(*ctx->levels[l], ctx->omega, cfg->alpha, cfg->beta, cfg->damping, l == 0,
+                      l == int(ctx->levels.size()) - 1);
   ctx->has_hier = true;
   HB_API_END
 }
@@ -874,6 +885,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_wide_legs = value != 0;
   else if (k == "legs_wd")
     ctx->opt_legs_wd = value != 0;
+  else if (k == "coarse_krylov")
+    ctx->opt_coarse_krylov = value != 0;
   else if (k == "lean_legs")
     ctx->opt_lean_legs = value != 0;
   else if (k == "conv_rows")

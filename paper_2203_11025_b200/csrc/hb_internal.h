@@ -82,6 +82,7 @@ struct Level {
   std::vector<double> k2, gam;  // host fp64 coefficients (inc/stencil.hpp:169-185 coarsening)
   DBuf<float2> dM, dA, wdi;
   DBuf<double2> dA64;  // level 0: fp64 diagonal of A^h for the restart residual
+  DBuf<double2> dM64;  // coarsest level: fp64 diagonal of M^H (multi-CTA coarse GMRES restart)
   DBuf<float> k2f;
   // V-cycle work buffers [B][N]
   DBuf<float2> f, v, t, x;
@@ -131,6 +132,8 @@ void launch_prolong_add(Context& c, const LevelView& Lf, int cnx, int cny, int o
 void launch_restrict_plain(Context& c, int nx, int ny, int offset, int B, const float2* fine, float2* coarse);
 void launch_coarse_gmres(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
                          float2* x, float2* scratch);
+// coarsest GMRES(iters) with D^-1 on the multi-CTA Krylov kernels (hb_krylov.cu), large coarse grids
+void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot, const float2* f, float2* x);
 // register-resident variant for <= 1024-node coarse grids, iters <= 10 (hb_coarse_small.cu); false if not applicable
 bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
                          float2* x);
@@ -227,6 +230,16 @@ struct Context {
   DBuf<int> kcount;          // number of unfrozen columns (host-visible after restart)
   DBuf<float2> kV, kZ, kW;   // [B][m+1][N], [B][m][N], [B][N]
   DBuf<double2> kX, kB;      // c128 solution / rhs when called with host buffers
+  struct KrylovBufs {        // coarsest-level GMRES on the Krylov kernels, one set per half-batch stream
+    DBuf<char> state;
+    DBuf<double2> part;
+    DBuf<double> hist;
+    DBuf<int> act, count;
+    DBuf<float> scale;
+    DBuf<unsigned> ticket;
+    DBuf<float2> V, Z, W;
+    DBuf<double2> b, x;
+  } kcoarse[2];
   int k_B = 0, k_m = 0, k_hist = 0;
   int* h_count = nullptr;    // pinned
   // preconditioner staging (context-owned so captured graphs see stable pointers)
@@ -236,7 +249,7 @@ struct Context {
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
        opt_coarse_reg = true, opt_wide_legs = false, opt_legs_wd = false,
-       opt_conv_rows = true, opt_lean_legs = true;
+       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true;
   int conv_rows_ring = 4;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs

@@ -624,6 +624,90 @@ void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x) {
   HB_CUDA(cudaGetLastError());
 }
 
+// ---------------------------------------------------------------------------
+// Coarsest-level GMRES(k) with D^-1 (coarse_solve_with_op, inc/multigrid.hpp:
+// 45-61) on the same multi-CTA Krylov kernels as the fine level, for coarse
+// grids too large for one CTA per column (c2: 128^2, c3: 256^2): right
+// preconditioning with Z_j = D^-1 V_j is FGMRES with a fixed diagonal
+// preconditioner, x0 = 0, tol 1e-300 (fixed budget), happy breakdown as
+// krylov.hpp:240.  Operator = the level's shifted M^H (fp64 diagonal for the
+// restart residual).  One state set per half-batch stream (slot).
+namespace {
+__global__ void k_c64_to_c128(size_t n, const float2* __restrict__ a, double2* __restrict__ b) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    b[i] = make_double2(a[i].x, a[i].y);
+}
+__global__ void k_c128_to_c64(size_t n, const double2* __restrict__ a, float2* __restrict__ b) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    b[i] = make_float2(float(a[i].x), float(a[i].y));
+}
+// Z = D^-1 (s_b V)  (the diagonal "preconditioner" of the coarse GMRES)
+__global__ void k_diag_precond(int N, const int* act, const float2* __restrict__ V, const float* scale,
+                               const float2* __restrict__ d, float2* __restrict__ Z) {
+  const int b = blockIdx.y;
+  if (act && !act[b]) return;
+  const float s = scale[b];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+    Z[size_t(b) * N + i] = cmul(cscale(V[size_t(b) * N + i], s), crcp(__ldg(d + i)));
+}
+}  // namespace
+
+void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot, const float2* f, float2* x) {
+  if (iters < 1 || iters > kMaxRestart) throw HbError{HB_ERR_ARG, "coarse GMRES iterations out of range"};
+  if (!L.dM64.p) throw HbError{HB_ERR_STATE, "coarsest level lacks the fp64 M diagonal"};
+  Context::KrylovBufs& K = c.kcoarse[slot & 1];
+  const size_t N = L.N();
+  const int m = iters, cap = iters + 2;
+  K.state.ensure(size_t(B) * sizeof(ColState));
+  K.V.ensure(size_t(m + 1) * B * N);
+  K.Z.ensure(size_t(m) * B * N);
+  K.W.ensure(size_t(B) * N);
+  K.b.ensure(size_t(B) * N);
+  K.x.ensure(size_t(B) * N);
+  const int nbk = std::max(nblk_for(c, N, B), nblk_adots(c, N, B, 256 * KNPT));
+  K.part.ensure(size_t(B) * nbk * KMAXV);
+  K.hist.ensure(size_t(B) * cap);
+  K.act.ensure(B);
+  K.scale.ensure(B);
+  K.count.ensure(1);
+  if (K.ticket.n < size_t(B)) {
+    K.ticket.ensure(B);
+    HB_CUDA(cudaMemsetAsync(K.ticket.p, 0, sizeof(unsigned) * B, c.stream));
+  }
+  const FineView F{L.nx, L.ny, 1.0 / (L.h * L.h), L.dM64.p, L.dM.p};
+  ColState* st = reinterpret_cast<ColState*>(K.state.p);
+  const size_t BN = size_t(B) * N;
+  const int g1 = int(std::min<size_t>((BN + 255) / 256, size_t(c.num_sms) * 8));
+  const int tok = prof_begin(c, PC_COARSE);
+  c.launches += 4 + 3 * m;  // prof_begin counted one of the 5 + 3m kernels below
+  k_init_state<<<(B + 127) / 128, 128, 0, c.stream>>>(st, B);
+  k_c64_to_c128<<<g1, 256, 0, c.stream>>>(BN, f, K.b.p);
+  HB_CUDA(cudaMemsetAsync(K.x.p, 0, sizeof(double2) * BN, c.stream));
+  HB_CUDA(cudaMemsetAsync(K.count.p, 0, sizeof(int), c.stream));
+  const int nb = nblk_for(c, N, B);
+  const double tol = 1e-300;
+  k_restart<<<dim3(nb, B), KT, 0, c.stream>>>(F, B, st, K.b.p, K.x.p, K.V.p, reinterpret_cast<double*>(K.part.p),
+                                               K.ticket.p, K.hist.p, cap, tol, m, K.act.p, K.scale.p, K.count.p);
+  const int na = nblk_adots(c, N, B, 256 * KNPT);
+  const dim3 gz(unsigned(std::max<size_t>(1, std::min<size_t>((N + 255) / 256, size_t(4) * c.num_sms / B))), B);
+  for (int j = 0; j < m; ++j) {
+    float2* Vj = K.V.p + size_t(j) * BN;
+    float2* Zj = K.Z.p + size_t(j) * BN;
+    k_diag_precond<<<gz, 256, 0, c.stream>>>(int(N), K.act.p, Vj, K.scale.p, L.dM.p, Zj);
+    k_adots<256><<<dim3(na, B), 256, 0, c.stream>>>(F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p);
+    k_update<<<dim3(nb, B), KT, 0, c.stream>>>(F, B, j, m, st, K.act.p, K.W.p, K.V.p,
+                                                reinterpret_cast<double*>(K.part.p), K.ticket.p, K.hist.p, cap, tol,
+                                                m, K.scale.p);
+  }
+  const int nf = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
+  k_finalize<<<dim3(nf, B), KT, 0, c.stream>>>(F, B, st, K.Z.p, K.x.p);
+  k_c128_to_c64<<<g1, 256, 0, c.stream>>>(BN, K.x.p, x);
+  // algorithmic bytes: f in, x out (c64) -- the Krylov traffic of the coarse
+  // level is accounted like the fine level's (Arnoldi over m steps)
+  prof_end(c, PC_COARSE, tok, double(B) * N * 16.0 + double(N) * 8.0, 0);
+  HB_CUDA(cudaGetLastError());
+}
+
 // report readback helpers (host side of hb_fgmres)
 void krylov_report(Context& c, int B, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv,
                    uint8_t* brk) {

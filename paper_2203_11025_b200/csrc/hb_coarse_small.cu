@@ -341,6 +341,69 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_small(LevelView L, int m, cons
 // independent loads per node, no bounds branches).  Same arithmetic and
 // summation order as k_coarse_small (the MGS correction is fed from per-warp
 // smem broadcasts instead of double-precision shuffles).
+// Least squares min |beta0 e1 - H y| of the coarse GMRES on one warp
+// (krylov.hpp Givens + back substitution, same per-element operations as the
+// serial loop in k_coarse_small): lane j owns Hessenberg column j; rotation i
+// is generated by lane i once rotations 0..i-1 reached it and is broadcast to
+// lanes > i (depth k rotations instead of k(k+1)/2).  The triangle is then
+// transposed through smem so lane i owns row i for a column-sweep back
+// substitution.  Writes S.coef[i] = y_i * scale_i.
+template <int MAXK>
+__device__ __forceinline__ void coarse_lsq_warp(SmallSmem& S, int k, int lane) {
+  // rolled loops over smem-resident columns: this code runs once per launch,
+  // so its size (cold instruction fetch) matters more than its registers
+  double2 gi = make_double2(lane == 0 ? S.beta0 : 0.0, 0.0);  // lane i holds g[i]
+  double2 gcarry = make_double2(S.beta0, 0.0);                 // g[i] before rotation i (all lanes)
+  double2 dg = make_double2(1.0, 0.0);                         // this lane's final diagonal
+  double2* hc = S.H[lane < k ? lane : 0];
+#pragma unroll 1
+  for (int i = 0; i < k; ++i) {
+    double cs = 0.0;
+    double2 sn = make_double2(0.0, 0.0);
+    if (lane == i) {
+      const double2 a = hc[i];
+      const double hn = hc[i + 1].x;
+      const double a2 = a.x * a.x + a.y * a.y;
+      if (a2 + hn * hn == 0.0) {
+        cs = 1.0;
+      } else if (a2 == 0.0) {
+        sn = make_double2(1.0, 0.0);
+      } else {
+        const double ia = rsqrt(a2), ir = rsqrt(a2 + hn * hn);
+        cs = a2 * ia * ir;
+        sn = zscale(a, hn * ia * ir);
+      }
+      dg = dadd(zscale(a, cs), zmul(sn, hc[i + 1]));
+      hc[i] = dg;
+    }
+    cs = __shfl_sync(0xffffffffu, cs, i);
+    sn = make_double2(__shfl_sync(0xffffffffu, sn.x, i), __shfl_sync(0xffffffffu, sn.y, i));
+    if (lane > i && lane < k) {
+      const double2 h0 = hc[i], h1 = hc[i + 1];
+      hc[i] = dadd(zscale(h0, cs), zmul(sn, h1));
+      hc[i + 1] = dadd(zscale(zmul(zconj(sn), h0), -1.0), zscale(h1, cs));
+    }
+    const double2 gnext = zscale(zmul(zconj(sn), gcarry), -1.0);
+    if (lane == i) gi = zscale(gcarry, cs);
+    if (lane == i + 1) gi = gnext;
+    gcarry = gnext;
+  }
+  __syncwarp();
+  // column-sweep back substitution: lane i accumulates row i of R y
+  const double inv = 1.0 / (dg.x * dg.x + dg.y * dg.y);
+  double2 acc = gi, yl = make_double2(0.0, 0.0);
+#pragma unroll 1
+  for (int l = k - 1; l >= 0; --l) {
+    if (lane == l) yl = zscale(zmul(acc, zconj(dg)), inv);
+    const double2 y = make_double2(__shfl_sync(0xffffffffu, yl.x, l), __shfl_sync(0xffffffffu, yl.y, l));
+    if (lane < l) acc = zsub(acc, zmul(S.H[l][lane], y));
+  }
+  if (lane <= MAXK) {
+    const double2 c = lane < k ? zscale(yl, S.scale[lane]) : make_double2(0.0, 0.0);
+    S.coef[lane] = make_float2(float(c.x), float(c.y));  // zero beyond k: the x sum runs over all MAXK
+  }
+}
+
 template <int NT, int NPT, int MAXK>
 __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const int* act,
                                                        const float2* __restrict__ f, float2* __restrict__ x) {
@@ -376,18 +439,14 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
   __syncthreads();
   int k = m;
   double hn_prev = 0.0;
+  float2 vj[NPT];  // V_j, carried from the previous step (no register-array select)
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) vj[q] = V[0][q];
 #pragma unroll 1
   for (int j = 0; j <= m; ++j) {
     if (tr && j < 16) tr[j * 8 + 0] = clock64();
     const float2* sU = sU2 + (j & 1) * tile;
-    float2 w[NPT], vj[NPT];
-#pragma unroll
-    for (int q = 0; q < NPT; ++q) {
-      vj[q] = V[0][q];
-#pragma unroll
-      for (int i = 1; i <= MAXK; ++i)
-        if (i == j) vj[q] = V[i][q];
-    }
+    float2 w[NPT];
     float nrm_part = 0.f;
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
@@ -443,19 +502,25 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
     double2 val = make_double2(0.0, 0.0);
     {
       const int f0 = lane < 16 ? 2 * lane : 32 + 2 * (lane - 16);
-      float px_[NT / 32], py_[NT / 32];
+      double px_[NT / 32], py_[NT / 32];
 #pragma unroll
       for (int w2 = 0; w2 < NT / 32; ++w2) {
-        px_[w2] = S.part[w2][f0];
-        py_[w2] = S.part[w2][f0 + 1];
+        const float2 pp = *reinterpret_cast<const float2*>(&S.part[w2][f0]);
+        px_[w2] = pp.x;
+        py_[w2] = pp.y;
       }
 #pragma unroll
-      for (int w2 = 0; w2 < NT / 32; ++w2) {
-        val.x += px_[w2];
-        val.y += py_[w2];
-      }
+      for (int st = 1; st < NT / 32; st *= 2)  // pairwise fold (depth log2 of the warp count)
+#pragma unroll
+        for (int w2 = 0; w2 + st < NT / 32; w2 += 2 * st) {
+          px_[w2] += px_[w2 + st];
+          py_[w2] += py_[w2 + st];
+        }
+      val = make_double2(px_[0], py_[0]);
     }
-    const double nrm = sqrt(__shfl_sync(0xffffffffu, val.x, 31));
+    const double nrm2 = __shfl_sync(0xffffffffu, val.x, 31);
+    const double rnrm = nrm2 > 0.0 ? rsqrt(nrm2) : 0.0;
+    const double nrm = nrm2 * rnrm;
     if (j == 0) {
       if (t == 0) S.beta0 = nrm;
       if (nrm == 0.0) {
@@ -470,7 +535,7 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
         break;
       }
     }
-    const double sj = 1.0 / nrm;
+    const double sj = rnrm;
     if (t == 0) S.scale[j] = sj;
     if (j == m) break;
     hn_prev = sj;
@@ -483,6 +548,7 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
                                      __shfl_sync(0xffffffffu, val.y, (16 + lane) & 31));
       if (lane < j) gjk = zscale(e, sj * S.scale[lane]);
     }
+    if (tr && j < 16) tr[j * 8 + 7] = clock64();
     // first-order MGS correction h_i -= sum_{k<i} hcgs_k G_ik, operands broadcast from this warp's smem rows
     if (lane <= MAXK) {
       sHc[warp][lane] = hcgs;
@@ -505,27 +571,29 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
       if (lane < j) S.G[j][lane] = gjk;
     }
     if (tr && j < 16) tr[j * 8 + 4] = clock64();
-    const double2 cc = zscale(h, si / sj);
+    const double2 cc = zscale(h, si * nrm);  // si / sj
     const float2 cf = make_float2(float(cc.x), float(cc.y));
-    float2 ci[MAXK + 1];
-#pragma unroll
-    for (int i = 0; i <= MAXK; ++i) ci[i] = make_float2(__shfl_sync(0xffffffffu, cf.x, i), __shfl_sync(0xffffffffu, cf.y, i));
     float2 vn[NPT];
 #pragma unroll
-    for (int q = 0; q < NPT; ++q) {
-      vn[q] = w[q];
+    for (int q = 0; q < NPT; ++q) vn[q] = w[q];
 #pragma unroll
-      for (int i = 0; i <= MAXK; ++i)
-        if (i <= j) vn[q] = csub(vn[q], cmul(ci[i], V[i][q]));
+    for (int i = 0; i <= MAXK; ++i) {
+      if (i > j) break;
+      const float2 ci = make_float2(__shfl_sync(0xffffffffu, cf.x, i), __shfl_sync(0xffffffffu, cf.y, i));
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) vn[q] = csub(vn[q], cmul(ci, V[i][q]));
     }
     if (tr && j < 16) tr[j * 8 + 5] = clock64();
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
       if (!ok[q]) vn[q] = make_float2(0.f, 0.f);
+      vj[q] = vn[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
 #pragma unroll
       for (int i = 1; i <= MAXK; ++i)
         if (i == j + 1) V[i][q] = vn[q];
-    }
     // u_{j+1} into the other tile (its last readers, step j-1, passed barrier 1 of step j)
     float2* sUn = sU2 + ((j + 1) & 1) * tile;
 #pragma unroll
@@ -541,60 +609,24 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
     return;
   }
   __syncthreads();
+  if (tr) tr[11 * 8 + 0] = clock64();
+  if (warp == 0) coarse_lsq_warp<MAXK>(S, k, lane);
   if (t == 0) {
-    double* cs = S.cs;
-    double2* sn = S.sn;
-    double2* g = S.g;
-    for (int i = 0; i <= k; ++i) g[i] = make_double2(0.0, 0.0);
-    g[0] = make_double2(S.beta0, 0.0);
-    for (int j = 0; j < k; ++j) {
-      double2* hj = S.H[j];
-      for (int i = 0; i < j; ++i) {
-        const double2 t1 = dadd(zscale(hj[i], cs[i]), zmul(sn[i], hj[i + 1]));
-        hj[i + 1] = dadd(zscale(zmul(zconj(sn[i]), hj[i]), -1.0), zscale(hj[i + 1], cs[i]));
-        hj[i] = t1;
-      }
-      const double2 a = hj[j];
-      const double hn = hj[j + 1].x;
-      const double a2 = a.x * a.x + a.y * a.y;
-      if (a2 + hn * hn == 0.0) {
-        cs[j] = 1.0;
-        sn[j] = make_double2(0.0, 0.0);
-      } else if (a2 == 0.0) {
-        cs[j] = 0.0;
-        sn[j] = make_double2(1.0, 0.0);
-      } else {
-        const double ia = rsqrt(a2), ir = rsqrt(a2 + hn * hn);
-        cs[j] = a2 * ia * ir;
-        sn[j] = zscale(a, hn * ia * ir);
-      }
-      hj[j] = dadd(zscale(hj[j], cs[j]), zmul(sn[j], hj[j + 1]));
-      hj[j + 1] = make_double2(0.0, 0.0);
-      g[j + 1] = zscale(zmul(zconj(sn[j]), g[j]), -1.0);
-      g[j] = zscale(g[j], cs[j]);
-    }
-    for (int i = k - 1; i >= 0; --i) {
-      double2 sum = g[i];
-      for (int l = i + 1; l < k; ++l) sum = zsub(sum, zmul(S.H[l][i], S.y[l]));
-      const double2 dd = S.H[i][i];
-      const double inv = 1.0 / (dd.x * dd.x + dd.y * dd.y);
-      S.y[i] = zscale(zmul(sum, zconj(dd)), inv);
-    }
-    for (int i = 0; i < k; ++i) {
-      const double2 c = zscale(S.y[i], S.scale[i]);
-      S.coef[i] = make_float2(float(c.x), float(c.y));
-    }
+    if (tr) tr[11 * 8 + 1] = clock64();
   }
   __syncthreads();
+  if (tr) tr[11 * 8 + 3] = clock64();
+  float2 cf[MAXK];
+#pragma unroll
+  for (int i = 0; i < MAXK; ++i) cf[i] = S.coef[i];
 #pragma unroll
   for (int q = 0; q < NPT; ++q) {
-    if (!ok[q]) continue;
     float2 u = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < MAXK; ++i)
-      if (i < k) u = cadd(u, cmul(S.coef[i], V[i][q]));
-    x[size_t(b) * N + t + q * NT] = cmul(u, di[q]);
+    for (int i = 0; i < MAXK; ++i) u = cadd(u, cmul(cf[i], V[i][q]));
+    if (ok[q]) x[size_t(b) * N + t + q * NT] = cmul(u, di[q]);
   }
+  if (tr) tr[11 * 8 + 2] = clock64();
 }
 
 }  // namespace
@@ -662,6 +694,10 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
         fprintf(stderr, "  j=%2d %6lld %6lld %6lld %6lld %6lld %6lld %6lld\n", j, 0ll, h[j * 8 + 1] - h[j * 8],
                 h[j * 8 + 2] - h[j * 8], h[j * 8 + 3] - h[j * 8], h[j * 8 + 4] - h[j * 8], h[j * 8 + 5] - h[j * 8],
                 h[j * 8 + 6] - h[j * 8]);
+      fprintf(stderr, "  total %lld, least squares %lld, barrier %lld, x %lld (cycles)\n", h[88 + 2] - h[0],
+              h[89] - h[88], h[91] - h[89], h[90] - h[91]);
+      for (int j = 0; j < iters && j < 16; ++j) fprintf(stderr, " %lld", h[j * 8 + 7] - h[j * 8 + 3]);
+      fprintf(stderr, " <- bar1 to pre-MGS\n");
     }
   }
   return true;

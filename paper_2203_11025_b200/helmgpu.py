@@ -173,7 +173,10 @@ class Context:
             self.h = None
 
     def __del__(self):
-        self.close()
+        try:
+            self.close()
+        except TypeError:  # interpreter shutdown: module globals already cleared
+            pass
 
     def _check(self, rc):
         if rc != 0:

@@ -80,14 +80,14 @@ __device__ __forceinline__ void warp_reduce_scatter32(float (&v)[32]) {
 struct SmallSmem {
   float part[CS_MAXW][2 * CS_SLOTS];  // [warp][float]: 0..31 dots (re,im), 32..63 Gram / norm
   double2 H[kMaxCoarseIters + 1][kMaxCoarseIters + 1];  // H[col][row], col < k, row <= col+1
-  double2 G[kMaxCoarseIters][kMaxCoarseIters];          // G[i][k] = <V_i, V_k>, k < i
+  double2 G[kMaxCoarseIters][kMaxCoarseIters + 1];      // G[i][k] = <V_i, V_k>, k < i (padded: lane-per-row reads)
   double2 y[kMaxCoarseIters];
   double2 sn[kMaxCoarseIters], g[kMaxCoarseIters + 1];
   double cs[kMaxCoarseIters];
   double scale[kMaxCoarseIters + 2];                    // V_i = scale[i] * Vraw_i
   float2 coef[kMaxCoarseIters + 1];
   double beta0;
-  int k;
+  int k, stop;
 };
 
 // Per Arnoldi step j (two CTA barriers):
@@ -412,7 +412,7 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
   long long* const tr = (b == 0 && threadIdx.x == 0) ? g_coarse_trace : nullptr;  // HB_COARSE_TRACE
   extern __shared__ float2 sU2[];  // 2 x (nx+2) x (ny+2) zero-bordered u_j = D^-1 V_j (double-buffered by j)
   __shared__ SmallSmem S;
-  __shared__ double2 sHc[NT / 32][MAXK + 1], sGj[NT / 32][MAXK + 1];
+  __shared__ double2 sHc[MAXK + 1], sGj[MAXK + 1];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const int nx = L.nx, ny = L.ny, N = nx * ny, px2 = nx + 2;
   const float ih2 = L.inv_h2;
@@ -447,10 +447,8 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
     if (tr && j < 16) tr[j * 8 + 0] = clock64();
     const float2* sU = sU2 + (j & 1) * tile;
     float2 w[NPT];
-    float nrm_part = 0.f;
 #pragma unroll
     for (int q = 0; q < NPT; ++q) {
-      nrm_part = fmaf(vj[q].x, vj[q].x, fmaf(vj[q].y, vj[q].y, nrm_part));
       w[q] = make_float2(0.f, 0.f);
       if (j == m || !ok[q]) continue;
       // neighbours (zero border = out of range), same summation order as k_coarse_small
@@ -461,6 +459,10 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
       yv.y = fmaf(-ih2, nb.y, yv.y);
       w[q] = yv;
     }
+    // slots: <V_i, w> at (2i, 2i+1); Gram <V_j, V_i> (i <= j, i == j: |V_j|^2)
+    // mirrored at (31-2i re, 30-2i im).  Both fit one 32-slot butterfly while
+    // 4j + 4 <= 32; later steps use a second butterfly for the Gram row.
+    const bool one = j <= 7 || j == m;  // (j == m: no <V_i, w> slots)
     float v[32];
 #pragma unroll
     for (int s2 = 0; s2 < 32; ++s2) v[s2] = 0.f;
@@ -477,109 +479,132 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
       }
     }
     if (tr && j < 16) tr[j * 8 + 1] = clock64();
-    warp_reduce_scatter32(v);
-    S.part[warp][lane] = v[0];
+    if (!one) {
+      warp_reduce_scatter32(v);
+      S.part[warp][lane] = v[0];
 #pragma unroll
-    for (int s2 = 0; s2 < 32; ++s2) v[s2] = 0.f;
-    v[30] = nrm_part;
-    if (j < m) {
+      for (int s2 = 0; s2 < 32; ++s2) v[s2] = 0.f;
+    }
 #pragma unroll
-      for (int i = 0; i < MAXK; ++i) {
-        if (i >= j) break;
+    for (int i = 0; i <= MAXK; ++i) {
+      if (i > j) break;
 #pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-          const float2 a = V[i][q], e = vj[q];
-          v[2 * i] = fmaf(e.x, a.x, fmaf(e.y, a.y, v[2 * i]));
-          v[2 * i + 1] = fmaf(e.x, a.y, fmaf(-e.y, a.x, v[2 * i + 1]));
-        }
+      for (int q = 0; q < NPT; ++q) {
+        const float2 a = V[i][q], e = vj[q];
+        v[31 - 2 * i] = fmaf(e.x, a.x, fmaf(e.y, a.y, v[31 - 2 * i]));
+        v[30 - 2 * i] = fmaf(e.x, a.y, fmaf(-e.y, a.x, v[30 - 2 * i]));
       }
     }
     warp_reduce_scatter32(v);
     if (tr && j < 16) tr[j * 8 + 2] = clock64();
-    S.part[warp][32 + lane] = v[0];
+    S.part[warp][(one ? 0 : 32) + lane] = v[0];
     __syncthreads();
     if (tr && j < 16) tr[j * 8 + 3] = clock64();
-    double2 val = make_double2(0.0, 0.0);
-    {
-      const int f0 = lane < 16 ? 2 * lane : 32 + 2 * (lane - 16);
-      double px_[NT / 32], py_[NT / 32];
-#pragma unroll
-      for (int w2 = 0; w2 < NT / 32; ++w2) {
-        const float2 pp = *reinterpret_cast<const float2*>(&S.part[w2][f0]);
-        px_[w2] = pp.x;
-        py_[w2] = pp.y;
-      }
-#pragma unroll
-      for (int st = 1; st < NT / 32; st *= 2)  // pairwise fold (depth log2 of the warp count)
-#pragma unroll
-        for (int w2 = 0; w2 + st < NT / 32; w2 += 2 * st) {
-          px_[w2] += px_[w2 + st];
-          py_[w2] += py_[w2 + st];
-        }
-      val = make_double2(px_[0], py_[0]);
-    }
-    const double nrm2 = __shfl_sync(0xffffffffu, val.x, 31);
-    const double rnrm = nrm2 > 0.0 ? rsqrt(nrm2) : 0.0;
-    const double nrm = nrm2 * rnrm;
-    if (j == 0) {
-      if (t == 0) S.beta0 = nrm;
-      if (nrm == 0.0) {
-        k = 0;
-        break;
-      }
-    } else {
-      const double hn = hn_prev * nrm;
-      if (t == 0) S.H[j - 1][j] = make_double2(hn, 0.0);
-      if (hn <= 1e-14 * S.beta0) {
-        k = j;
-        break;
-      }
-    }
-    const double sj = rnrm;
-    if (t == 0) S.scale[j] = sj;
-    if (j == m) break;
-    hn_prev = sj;
-    const double si = (lane < j) ? S.scale[lane] : sj;
-    double2 hcgs = make_double2(0.0, 0.0);
-    if (lane <= j) hcgs = zscale(val, si * sj);
-    double2 gjk = make_double2(0.0, 0.0);
-    {
-      const double2 e = make_double2(__shfl_sync(0xffffffffu, val.x, (16 + lane) & 31),
-                                     __shfl_sync(0xffffffffu, val.y, (16 + lane) & 31));
-      if (lane < j) gjk = zscale(e, sj * S.scale[lane]);
-    }
-    if (tr && j < 16) tr[j * 8 + 7] = clock64();
-    // first-order MGS correction h_i -= sum_{k<i} hcgs_k G_ik, operands broadcast from this warp's smem rows
-    if (lane <= MAXK) {
-      sHc[warp][lane] = hcgs;
-      sGj[warp][lane] = gjk;
-    }
-    __syncwarp();
-    double2 h = hcgs;
-    if (lane <= j) {
-#pragma unroll
-      for (int kk = 0; kk < MAXK; ++kk) {
-        if (kk < lane) {
-          const double2 hk = sHc[warp][kk];
-          const double2 Gik = (lane == j) ? sGj[warp][kk] : S.G[lane][kk];
-          h = zsub(h, zmul(hk, Gik));
-        }
-      }
-    }
+    // scalar phase on warp 0 only (the fp64 work and its smem reads are not
+    // repeated by every warp); results go through smem behind one barrier
     if (warp == 0) {
-      if (lane <= j) S.H[j][lane] = h;
-      if (lane < j) S.G[j][lane] = gjk;
+      double2 val = make_double2(0.0, 0.0);
+      {
+        // lane i < 16: <V_i, w>; lane 16 + i: Gram i (re at the odd slot)
+        const int f0 = lane < 16 ? 2 * lane : (one ? 0 : 32) + 30 - 2 * (lane - 16);
+        double px_[NT / 32], py_[NT / 32];
+#pragma unroll
+        for (int w2 = 0; w2 < NT / 32; ++w2) {
+          const float2 pp = *reinterpret_cast<const float2*>(&S.part[w2][f0]);
+          px_[w2] = lane < 16 ? pp.x : pp.y;
+          py_[w2] = lane < 16 ? pp.y : pp.x;
+        }
+#pragma unroll
+        for (int st = 1; st < NT / 32; st *= 2)  // pairwise fold (depth log2 of the warp count)
+#pragma unroll
+          for (int w2 = 0; w2 + st < NT / 32; w2 += 2 * st) {
+            px_[w2] += px_[w2 + st];
+            py_[w2] += py_[w2 + st];
+          }
+        val = make_double2(px_[0], py_[0]);
+      }
+      const double nrm2 = __shfl_sync(0xffffffffu, val.x, 16 + j);
+      const double rnrm = nrm2 > 0.0 ? rsqrt(nrm2) : 0.0;
+      const double nrm = nrm2 * rnrm;
+      int stop = 0, kf = 0;
+      if (j == 0) {
+        if (lane == 0) S.beta0 = nrm;
+        if (nrm == 0.0) stop = 1;  // k = 0
+      } else {
+        const double hn = hn_prev * nrm;
+        if (lane == 0) S.H[j - 1][j] = make_double2(hn, 0.0);
+        if (hn <= 1e-14 * S.beta0) {
+          stop = 1;
+          kf = j;
+        }
+      }
+      const double sj = rnrm;
+      if (!stop) {
+        if (lane == 0) S.scale[j] = sj;
+        if (j == m) {
+          stop = 1;
+          kf = m;
+        }
+      }
+      if (!stop) {
+        hn_prev = sj;
+        const double si = (lane < j) ? S.scale[lane] : sj;
+        double2 hcgs = make_double2(0.0, 0.0);
+        if (lane <= j) hcgs = zscale(val, si * sj);
+        double2 gjk = make_double2(0.0, 0.0);
+        {
+          const double2 e = make_double2(__shfl_sync(0xffffffffu, val.x, (16 + lane) & 31),
+                                         __shfl_sync(0xffffffffu, val.y, (16 + lane) & 31));
+          if (lane < j) gjk = zscale(e, sj * S.scale[lane]);
+        }
+        if (tr && j < 16) tr[j * 8 + 7] = clock64();
+        // first-order MGS correction h_i -= sum_{k<i} hcgs_k G_ik (operands broadcast through smem)
+        if (lane <= MAXK) {
+          sHc[lane] = hcgs;
+          sGj[lane] = gjk;
+        }
+        __syncwarp();
+        double2 h = hcgs;
+        {
+          // branch-free: all products issued at once (masked), then a pairwise sum
+          const int row = lane < MAXK ? lane : MAXK - 1;
+          double2 pr[MAXK];
+#pragma unroll
+          for (int kk = 0; kk < MAXK; ++kk) {
+            const double2 hk = sHc[kk];
+            const double2 g1 = sGj[kk], g2 = S.G[row][kk];
+            const double2 p = zmul(hk, lane == j ? g1 : g2);
+            pr[kk] = (kk < lane && lane <= j) ? p : make_double2(0.0, 0.0);
+          }
+#pragma unroll
+          for (int st = 1; st < MAXK; st *= 2)
+#pragma unroll
+            for (int kk = 0; kk + st < MAXK; kk += 2 * st) pr[kk] = dadd(pr[kk], pr[kk + st]);
+          h = zsub(h, pr[0]);
+        }
+        if (lane <= j) S.H[j][lane] = h;
+        if (lane < j) S.G[j][lane] = gjk;
+        const double2 cc = zscale(h, si * nrm);  // si / sj
+        if (lane <= MAXK) S.coef[lane] = lane <= j ? make_float2(float(cc.x), float(cc.y)) : make_float2(0.f, 0.f);
+      }
+      if (lane == 0) {
+        S.stop = stop;
+        S.k = kf;
+      }
+      if (tr && j < 16) tr[j * 8 + 4] = clock64();
     }
-    if (tr && j < 16) tr[j * 8 + 4] = clock64();
-    const double2 cc = zscale(h, si * nrm);  // si / sj
-    const float2 cf = make_float2(float(cc.x), float(cc.y));
+    __syncthreads();
+    if (S.stop) {
+      k = S.k;
+      break;
+    }
     float2 vn[NPT];
 #pragma unroll
     for (int q = 0; q < NPT; ++q) vn[q] = w[q];
 #pragma unroll
     for (int i = 0; i <= MAXK; ++i) {
       if (i > j) break;
-      const float2 ci = make_float2(__shfl_sync(0xffffffffu, cf.x, i), __shfl_sync(0xffffffffu, cf.y, i));
+      const float2 ci = S.coef[i];
 #pragma unroll
       for (int q = 0; q < NPT; ++q) vn[q] = csub(vn[q], cmul(ci, V[i][q]));
     }

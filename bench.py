@@ -250,6 +250,9 @@ def run_ours(args, ws, rank, local):
     groups = []
     for g in range(G):
         cg, arr = problems.gpu_setup(cfg, device=local)
+        for kv in args.opt:  # library options (experiments), e.g. --opt pdl=0
+            k, v = kv.split("=")
+            cg.set_option(k, int(v))
         groups.append(cg)
     ctx = groups[0]
     Bh = np.ascontiguousarray(problems.rhs_block(arr)[cols])
@@ -531,6 +534,7 @@ def main():
     ap.add_argument("--also", default="c1,c2,c3", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")
     ap.add_argument("--groups", type=int, default=3, help="independent column groups (solver contexts on their own "
                                                           "streams and host threads) per GPU")
     ap.add_argument("--no-cpu", action="store_true")

@@ -885,6 +885,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_wide_legs = value != 0;
   else if (k == "legs_wd")
     ctx->opt_legs_wd = value != 0;
+  else if (k == "pdl")
+    ctx->opt_pdl = value != 0;
   else if (k == "coarse_krylov")
     ctx->opt_coarse_krylov = value != 0;
   else if (k == "lean_legs")

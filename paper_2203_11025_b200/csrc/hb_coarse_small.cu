@@ -106,6 +106,7 @@ struct SmallSmem {
 template <int NT, int NPT, int MAXK>
 __global__ void __launch_bounds__(NT, 1) k_coarse_small(LevelView L, int m, const int* act,
                                                          const float2* __restrict__ f, float2* __restrict__ x) {
+  pdl_enter();
   const int b = blockIdx.x;
   if (act && !act[b]) return;
   extern __shared__ float2 dyn[];  // Vraw_0..Vraw_m [m+1][N], then D^-1 [N]
@@ -407,6 +408,7 @@ __device__ __forceinline__ void coarse_lsq_warp(SmallSmem& S, int k, int lane) {
 template <int NT, int NPT, int MAXK>
 __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const int* act,
                                                        const float2* __restrict__ f, float2* __restrict__ x) {
+  pdl_enter();
   const int b = blockIdx.x;
   if (act && !act[b]) return;
   long long* const tr = (b == 0 && threadIdx.x == 0) ? g_coarse_trace : nullptr;  // HB_COARSE_TRACE
@@ -507,7 +509,7 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
       {
         // lane i < 16: <V_i, w>; lane 16 + i: Gram i (re at the odd slot)
         const int f0 = lane < 16 ? 2 * lane : (one ? 0 : 32) + 30 - 2 * (lane - 16);
-        double px_[NT / 32], py_[NT / 32];
+        float px_[NT / 32], py_[NT / 32];  // fp32 pairwise fold of the per-warp sums, one conversion
 #pragma unroll
         for (int w2 = 0; w2 < NT / 32; ++w2) {
           const float2 pp = *reinterpret_cast<const float2*>(&S.part[w2][f0]);
@@ -523,9 +525,11 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
           }
         val = make_double2(px_[0], py_[0]);
       }
+      if (tr && j < 16) tr[96 + j] = clock64();
       const double nrm2 = __shfl_sync(0xffffffffu, val.x, 16 + j);
       const double rnrm = nrm2 > 0.0 ? rsqrt(nrm2) : 0.0;
       const double nrm = nrm2 * rnrm;
+      if (tr && j < 16) tr[112 + j] = clock64();
       int stop = 0, kf = 0;
       if (j == 0) {
         if (lane == 0) S.beta0 = nrm;
@@ -684,21 +688,21 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
     }
     const size_t su = 2 * sizeof(float2) * size_t(L.nx + 2) * (L.ny + 2);
     if (nt == 512)
-      k_coarse_reg<512, 2, 10><<<B, 512, su, c.stream>>>(L, iters, act, f, x);
+      launch_pdl(c, k_coarse_reg<512, 2, 10>, dim3(B), dim3(512), su, L, iters, act, f, x);
     else
-      k_coarse_reg<256, 4, 10><<<B, 256, su, c.stream>>>(L, iters, act, f, x);
+      launch_pdl(c, k_coarse_reg<256, 4, 10>, dim3(B), dim3(256), su, L, iters, act, f, x);
   } else if (nt == 1024 && N <= 1024) {
-    k_coarse_small<1024, 1, 15><<<B, 1024, smem, c.stream>>>(L, iters, act, f, x);
+    launch_pdl(c, k_coarse_small<1024, 1, 15>, dim3(B), dim3(1024), smem, L, iters, act, f, x);
   } else if (nt >= 512 && N <= 1024) {
-    k_coarse_small<512, 2, 15><<<B, 512, smem, c.stream>>>(L, iters, act, f, x);
+    launch_pdl(c, k_coarse_small<512, 2, 15>, dim3(B), dim3(512), smem, L, iters, act, f, x);
   } else if (N <= 256) {
-    k_coarse_small<256, 1, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+    launch_pdl(c, k_coarse_small<256, 1, 15>, dim3(B), dim3(256), smem, L, iters, act, f, x);
   } else if (N <= 512) {
-    k_coarse_small<256, 2, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+    launch_pdl(c, k_coarse_small<256, 2, 15>, dim3(B), dim3(256), smem, L, iters, act, f, x);
   } else if (N <= 1024) {
-    k_coarse_small<256, 4, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+    launch_pdl(c, k_coarse_small<256, 4, 15>, dim3(B), dim3(256), smem, L, iters, act, f, x);
   } else {
-    k_coarse_small<256, 8, 15><<<B, 256, smem, c.stream>>>(L, iters, act, f, x);
+    launch_pdl(c, k_coarse_small<256, 8, 15>, dim3(B), dim3(256), smem, L, iters, act, f, x);
   }
   prof_end(c, PC_COARSE, tok, double(B) * N * 16.0 + double(N) * 8.0, 0);  // f in, x out; diag
   HB_CUDA(cudaGetLastError());
@@ -723,6 +727,8 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
               h[89] - h[88], h[91] - h[89], h[90] - h[91]);
       for (int j = 0; j < iters && j < 16; ++j) fprintf(stderr, " %lld", h[j * 8 + 7] - h[j * 8 + 3]);
       fprintf(stderr, " <- bar1 to pre-MGS\n");
+      for (int j = 0; j <= iters && j < 16; ++j) fprintf(stderr, " %lld/%lld", h[96 + j] - h[j * 8 + 3], h[112 + j] - h[j * 8 + 3]);
+      fprintf(stderr, " <- bar1 to fold done / rsqrt done\n");
     }
   }
   return true;

@@ -30,6 +30,13 @@ __device__ __forceinline__ double dnorm2(float2 a) {
 }
 __device__ __forceinline__ float2 ld(const float2* p, size_t i) { return __ldg(p + i); }
 
+// programmatic dependent launch (launch_pdl): block until the previous kernel's
+// writes are visible.  No early launch_dependents: resident-but-waiting CTAs of
+// the next kernel (the coarse solve takes a whole SM) would starve the other
+// column groups' work (measured: early trigger 7.6k, wait-only 9.2k, off 9.0k
+// c0 solves/s with 3 groups).
+__device__ __forceinline__ void pdl_enter() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

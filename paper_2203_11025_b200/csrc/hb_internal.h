@@ -249,7 +249,7 @@ struct Context {
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
        opt_coarse_reg = true, opt_wide_legs = false, opt_legs_wd = false,
-       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true;
+       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_pdl = true;
   int conv_rows_ring = 4;
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
@@ -283,6 +283,25 @@ struct Context {
   std::vector<DetailRec> detail, detail_done;
   int64_t launches = 0;
 };
+
+// Launch with programmatic dependent launch (PDL, sm_90+): the kernel may be
+// scheduled while its stream predecessor drains, hiding the launch gap of the
+// latency-bound FGMRES chain.  Every kernel launched this way calls
+// pdl_wait() (hb_common.cuh) before it touches memory its predecessor writes.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(Context& c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = c.opt_pdl ? 1 : 0;
+  HB_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+}
 
 void ensure_batch(Context& c, int B);
 // V-cycle driver (hb_api.cu)

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(KT) k_restart(FineView F, int B, ColState* st,
                                                 double* part, unsigned* ticket, double* hist, int hist_cap,
                                                 double rel_tol, int max_iters, int* act, float* scale_out,
                                                 int* count) {
+  pdl_enter();
   const int b = blockIdx.y;
   ColState& S = st[b];
   if (S.frozen) {
@@ -198,6 +199,7 @@ template <int NT>
 __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
                                               const float2* __restrict__ Z, float2* __restrict__ W,
                                               const float2* __restrict__ V, double2* part, unsigned* ticket) {
+  pdl_enter();
   const int b = blockIdx.y;
   if (!act[b]) return;
   const size_t N = size_t(F.nx) * F.ny;
@@ -344,6 +346,7 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
                                                const float2* __restrict__ W, float2* __restrict__ V, double* part,
                                                unsigned* ticket, double* hist, int hist_cap, double rel_tol,
                                                int max_iters, float* scale_out) {
+  pdl_enter();
   const int b = blockIdx.y;
   if (!act[b]) return;
   ColState& S = st[b];
@@ -480,6 +483,7 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
 // y = R^-1 g (back-substitution, inc/krylov.hpp:119-126); x += sum_i y_i Z_i
 __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st, const float2* __restrict__ Z,
                                                  double2* __restrict__ x) {
+  pdl_enter();
   const int b = blockIdx.y;
   const ColState& S = st[b];
   const int k = S.k;
@@ -589,7 +593,7 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
   const int nb = nblk_for(c, N, B);
   KScope ks(c, PC_KRYLOV_RESTART, double(B) * N * 40.0 + double(N) * 16.0);  // b, x (c128) in; V0 (c64) out; dA64
   HB_CUDA(cudaMemsetAsync(c.kcount.p, 0, sizeof(int), c.stream));
-  k_restart<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), b, x, V0,
+  launch_pdl(c, k_restart, dim3(nb, B), dim3(KT), 0, fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), b, x, V0,
                                                reinterpret_cast<double*>(c.kpart.p), c.kticket.p, c.khist.p,
                                                hist_cap, rel_tol, max_iters, c.kact.p, c.kscale.p, c.kcount.p);
   HB_CUDA(cudaGetLastError());
@@ -599,7 +603,7 @@ void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, cons
   const size_t N = c.levels[0]->N();
   KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0) + double(N) * 8.0);  // Z_j, V_0..V_j in; w out; dA
   const int nb = nblk_adots(c, N, B, 256 * KNPT);
-  k_adots<256><<<dim3(nb, B), 256, 0, c.stream>>>(fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p),
+  launch_pdl(c, k_adots<256>, dim3(nb, B), dim3(256), 0, fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p),
                                                    c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p);
   HB_CUDA(cudaGetLastError());
 }
@@ -609,7 +613,7 @@ void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* 
   const size_t N = c.levels[0]->N();
   const int nb = nblk_for(c, N, B);
   KScope ks(c, PC_KRYLOV_UPDATE, double(B) * N * (8.0 * (j + 1) + 16.0));  // w, V_0..V_j in; V_{j+1} out
-  k_update<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p),
+  launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p),
                                               c.kact.p, w, V, reinterpret_cast<double*>(c.kpart.p), c.kticket.p,
                                               c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p);
   HB_CUDA(cudaGetLastError());
@@ -620,7 +624,7 @@ void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x) {
   const size_t N = c.levels[0]->N();
   const int nb = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
   KScope ks(c, PC_KRYLOV_FINAL, double(B) * N * (32.0 + 8.0 * m));  // x (c128) in+out, Z_0..Z_{k-1} in (upper bound k = m)
-  k_finalize<<<dim3(nb, B), KT, 0, c.stream>>>(fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), Z, x);
+  launch_pdl(c, k_finalize, dim3(nb, B), dim3(KT), 0, fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), Z, x);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -686,7 +690,7 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
   HB_CUDA(cudaMemsetAsync(K.count.p, 0, sizeof(int), c.stream));
   const int nb = nblk_for(c, N, B);
   const double tol = 1e-300;
-  k_restart<<<dim3(nb, B), KT, 0, c.stream>>>(F, B, st, K.b.p, K.x.p, K.V.p, reinterpret_cast<double*>(K.part.p),
+  launch_pdl(c, k_restart, dim3(nb, B), dim3(KT), 0, F, B, st, K.b.p, K.x.p, K.V.p, reinterpret_cast<double*>(K.part.p),
                                                K.ticket.p, K.hist.p, cap, tol, m, K.act.p, K.scale.p, K.count.p);
   const int na = nblk_adots(c, N, B, 256 * KNPT);
   const dim3 gz(unsigned(std::max<size_t>(1, std::min<size_t>((N + 255) / 256, size_t(4) * c.num_sms / B))), B);
@@ -694,13 +698,13 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
     float2* Vj = K.V.p + size_t(j) * BN;
     float2* Zj = K.Z.p + size_t(j) * BN;
     k_diag_precond<<<gz, 256, 0, c.stream>>>(int(N), K.act.p, Vj, K.scale.p, L.dM.p, Zj);
-    k_adots<256><<<dim3(na, B), 256, 0, c.stream>>>(F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p);
-    k_update<<<dim3(nb, B), KT, 0, c.stream>>>(F, B, j, m, st, K.act.p, K.W.p, K.V.p,
+    launch_pdl(c, k_adots<256>, dim3(na, B), dim3(256), 0, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p);
+    launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, F, B, j, m, st, K.act.p, K.W.p, K.V.p,
                                                 reinterpret_cast<double*>(K.part.p), K.ticket.p, K.hist.p, cap, tol,
                                                 m, K.scale.p);
   }
   const int nf = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
-  k_finalize<<<dim3(nf, B), KT, 0, c.stream>>>(F, B, st, K.Z.p, K.x.p);
+  launch_pdl(c, k_finalize, dim3(nf, B), dim3(KT), 0, F, B, st, K.Z.p, K.x.p);
   k_c128_to_c64<<<g1, 256, 0, c.stream>>>(BN, K.x.p, x);
   // algorithmic bytes: f in, x out (c64) -- the Krylov traffic of the coarse
   // level is accounted like the fine level's (Arnoldi over m steps)

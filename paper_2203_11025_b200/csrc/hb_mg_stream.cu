@@ -67,6 +67,7 @@ template <bool WD>  // WD: Jacobi factor w = damping / d formed from d in regist
 __global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, float damping, int offset, int rows_per_chunk,
                                                             const int* act, const float2* __restrict__ f,
                                                             const float* fscale, float2* __restrict__ fc) {
+  pdl_enter();
   const int b = blockIdx.z;
   if (act && !act[b]) return;
   const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
                                                           int rows_per_chunk, const int* act,
                                                           const float2* __restrict__ f, const float* fscale,
                                                           const float2* __restrict__ vc, float2* __restrict__ z) {
+  pdl_enter();
   const int b = blockIdx.z;
   if (act && !act[b]) return;
   const int lane = threadIdx.x, nx = L.nx, ny = L.ny;
@@ -258,6 +260,7 @@ struct RowIn {
 __global__ void __launch_bounds__(32 * WARPS) k_down_lean(LevelView L, int offset, int rows_per_chunk, const int* act,
                                                           const float2* __restrict__ f, const float* fscale,
                                                           float2* __restrict__ fc) {
+  pdl_enter();
   const int b = blockIdx.z;
   if (act && !act[b]) return;
   const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
@@ -374,6 +377,7 @@ __device__ __forceinline__ Quad apply_M4(const Quad& d, const Quad& vm, const Qu
 __global__ void __launch_bounds__(32 * WARPS) k_down_stream4(LevelView L, int offset, int rows_per_chunk,
                                                              const int* act, const float2* __restrict__ f,
                                                              const float* fscale, float2* __restrict__ fc) {
+  pdl_enter();
   const int b = blockIdx.z;
   if (act && !act[b]) return;
   const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
@@ -468,15 +472,15 @@ void launch_down_stream(Context& c, const LevelView& L, float damping, int offse
   const int chunks = (cny + rpc - 1) / rpc;
   if (c.opt_wide_legs && L.nx % 4 == 0) {
     const dim3 grid((L.nx + SW4_FINE - 1) / SW4_FINE, (chunks + WARPS - 1) / WARPS, B);
-    k_down_stream4<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
+    launch_pdl(c, k_down_stream4, dim3(grid), dim3(32, WARPS), 0, L, offset, rpc, act, f, fscale, fc);
   } else {
     const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
     if (c.opt_lean_legs)
-      k_down_lean<<<grid, dim3(32, WARPS), 0, c.stream>>>(L, offset, rpc, act, f, fscale, fc);
+      launch_pdl(c, k_down_lean, dim3(grid), dim3(32, WARPS), 0, L, offset, rpc, act, f, fscale, fc);
     else if (c.opt_legs_wd)
-      k_down_stream<true><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, rpc, act, f, fscale, fc);
+      launch_pdl(c, k_down_stream<true>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, rpc, act, f, fscale, fc);
     else
-      k_down_stream<false><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, rpc, act, f, fscale, fc);
+      launch_pdl(c, k_down_stream<false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, rpc, act, f, fscale, fc);
   }
   prof_end(c, PC_DOWN, tok, double(B) * L.nx * L.ny * 10.0 + double(L.nx) * L.ny * 16.0, 0);
   HB_CUDA(cudaGetLastError());
@@ -493,9 +497,9 @@ void launch_up_stream(Context& c, const LevelView& L, float damping, int offset,
   const int chunks = (L.ny + rpc - 1) / rpc;
   const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
   if (c.opt_legs_wd)
-    k_up_stream<true><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
+    launch_pdl(c, k_up_stream<true>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
   else
-    k_up_stream<false><<<grid, dim3(32, WARPS), 0, c.stream>>>(L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
+    launch_pdl(c, k_up_stream<false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
   prof_end(c, PC_UP, tok, double(B) * L.nx * L.ny * 18.0 + double(L.nx) * L.ny * 16.0, 0);
   HB_CUDA(cudaGetLastError());
 }

@@ -143,6 +143,37 @@ int hb_fgmres_device(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch,
                      double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
                      uint8_t* breakdown);
 
+/* ---- row slabs: one large grid over several GPUs --
+ * The reference solves one grid in one process (block_fgmres,
+ * inc/krylov.hpp:83-267; cycle_at, inc/multigrid.hpp:108-119); these entry
+ * points run the same FGMRES + M_V on a grid split into row slabs, slab r owning
+ * level-0 rows [a_r, a_{r+1}) (multiples of 2^(levels-1)).  Every level but the
+ * coarsest keeps 2 ghost rows per side (halo exchange), the coarsest is
+ * all-gathered and solved replicated, the Arnoldi sums are allreduced in fp64.
+ * Call after hb_set_problem + hb_build_hierarchy (nu1 = nu2 = 1) with the WHOLE
+ * problem on every slab; afterwards the context only serves the *_slab calls.
+ * Host buffers hold the rows the calling process supplies (hb_slab_rows):
+ * [batch][row_end - row_begin][nx] c128. */
+#define HB_NCCL_ID_BYTES 128
+/* slab `slab` of `nslabs` for an ny-row grid with `levels` levels (host only) */
+int hb_slab_partition(int ny, int levels, int nslabs, int slab, int* row_begin, int* row_end);
+/* ncclGetUniqueId of the process's NCCL (libnccl.so.2, loaded on first use) */
+int hb_nccl_unique_id(unsigned char* id);
+/* one slab per process (one GPU per rank): NCCL halos / allreduce / gathers */
+int hb_slab_init_nccl(hb_ctx* ctx, int rank, int nranks, const unsigned char* id);
+/* nslabs contexts of one process on one device as slabs 0..nslabs-1 (they
+ * share one stream; halos are device copies); drive the group through ctxs[0] */
+int hb_slab_init_local(hb_ctx** ctxs, int nslabs);
+/* rows [row_begin, row_end) whose data this process supplies / receives */
+int hb_slab_rows(hb_ctx* ctx, int* row_begin, int* row_end);
+/* Preconditioner::apply (M_V only) on slabs; r, z: host c128 rows of this process */
+int hb_precond_apply_slab(hb_ctx* ctx, int kind, int batch, const double* r, double* z);
+/* block_fgmres on slabs (M_V); B, X0 (may be NULL), X: host c128 rows of this process;
+ * the report arrays as hb_fgmres (identical on every slab) */
+int hb_fgmres_slab(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,
+                   double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
+                   uint8_t* breakdown);
+
 /* ---- setup helpers (host restatements of the reference RNG / generators) -- */
 /* Rng (inc/rng.hpp:9-67): n normals from Rng(seed) */
 void hb_rng_normals(uint64_t seed, int64_t n, double* out);

@@ -9,9 +9,9 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhelmgpu.so")
 SOURCES = ["hb_api.cu", "hb_mg.cu", "hb_mg_fused.cu", "hb_mg_stream.cu", "hb_coarse_small.cu", "hb_krylov.cu", "hb_net.cu",
-           "hb_conv_tc.cu", "hb_conv_rows.cu", "hb_host.cpp"]
+           "hb_conv_tc.cu", "hb_conv_rows.cu", "hb_slab.cu", "hb_host.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared"]
+              "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared", "-ldl"]
 
 
 def _deps():
@@ -28,11 +28,41 @@ def needs_build() -> bool:
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
+OBJDIR = os.path.join(os.path.dirname(HERE), "build", "obj")
+
+
+def _headers():
+    out = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".h", ".cuh"))]
+    out.append(os.path.join(os.path.dirname(HERE), "include", "helmgpu.h"))
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
+    """Compile each translation unit to an object (in parallel, only the stale
+    ones), then link the shared library."""
     if not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc] + NVCC_FLAGS + ["-o", LIB + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]
+    os.makedirs(OBJDIR, exist_ok=True)
+    hdr_t = max(os.path.getmtime(h) for h in _headers())
+    flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-ldl")]
+
+    def compile_one(src):
+        obj = os.path.join(OBJDIR, src + ".o")
+        path = os.path.join(CSRC, src)
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(hdr_t, os.path.getmtime(path)):
+            return obj
+        cmd = [nvcc] + flags + ["-c", path, "-o", obj + ".tmp"]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+        os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = [nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB + ".tmp"] + objs + ["-ldl"]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     subprocess.check_call(cmd)

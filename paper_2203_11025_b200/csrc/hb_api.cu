@@ -104,19 +104,28 @@ static void require_hier(Context& c) {
   if (!c.has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built (hb_build_hierarchy)"};
 }
 
-static void fill_level_device(Level& L, double omega, double alpha, double beta, double damping, bool fp64A,
+void require_whole(const Context& c) {
+  if (c.slab) throw HbError{HB_ERR_STATE, "context holds a row slab: use the hb_*_slab entry points"};
+}
+
+void fill_level_device(Level& L, double omega, double alpha, double beta, double damping, bool fp64A,
                               bool fp64M) {
+  // storage window [row0, row0 + rows) of the (global) level; rows outside the
+  // domain are zero padding
   const size_t n = L.N();
   const double inv_h2 = 1.0 / (L.h * L.h);
-  std::vector<float2> dm(n), da(n), wd(n);
-  std::vector<double2> da64(fp64A ? n : 0), dm64(fp64M ? n : 0);
-  std::vector<float> kf(n);
+  std::vector<float2> dm(n, make_float2(0.f, 0.f)), da(n, make_float2(0.f, 0.f)), wd(n, make_float2(0.f, 0.f));
+  std::vector<double2> da64(fp64A ? n : 0, make_double2(0.0, 0.0)), dm64(fp64M ? n : 0, make_double2(0.0, 0.0));
+  std::vector<float> kf(n, 0.f);
   const std::complex<double> sh(alpha, -beta), sh0(1.0, 0.0);
   for (size_t i = 0; i < n; ++i) {
+    const int gy = L.row0 + int(i / size_t(L.nx));
+    if (gy < 0 || gy >= L.ny) continue;
+    const size_t gi = size_t(gy) * L.nx + i % size_t(L.nx);
     // inc/stencil.hpp:27-34: d = 4/h^2 - omega^2 kappa^2 (alpha - beta i)(1 - gamma i)
-    const std::complex<double> damp(1.0, -L.gam[i]);
-    const std::complex<double> mM = -omega * omega * L.k2[i] * sh * damp;
-    const std::complex<double> mA = -omega * omega * L.k2[i] * sh0 * damp;
+    const std::complex<double> damp(1.0, -L.gam[gi]);
+    const std::complex<double> mM = -omega * omega * L.k2[gi] * sh * damp;
+    const std::complex<double> mA = -omega * omega * L.k2[gi] * sh0 * damp;
     const std::complex<double> dMd = 4.0 * inv_h2 + mM, dAd = 4.0 * inv_h2 + mA;
     if (dMd == 0.0 || dAd == 0.0) throw HbError{HB_ERR_NUMERIC, "zero stencil diagonal"};
     dm[i] = make_float2(float(dMd.real()), float(dMd.imag()));
@@ -125,7 +134,7 @@ static void fill_level_device(Level& L, double omega, double alpha, double beta,
     da[i] = make_float2(float(dAd.real()), float(dAd.imag()));
     if (fp64A) da64[i] = make_double2(dAd.real(), dAd.imag());
     if (fp64M) dm64[i] = make_double2(dMd.real(), dMd.imag());
-    kf[i] = float(L.k2[i]);
+    kf[i] = float(L.k2[gi]);
   }
   L.dM.ensure(n);
   L.dA.ensure(n);
@@ -166,7 +175,7 @@ void ensure_batch(Context& c, int B) {
 // ------------------------------------------------------------- V-cycle --
 // cycle_at (inc/multigrid.hpp:108-119) on device buffers; level-0 input f may
 // carry a per-column scale (FGMRES basis vectors are stored unnormalised).
-static void coarsest_solve(Context& c, int B, int c0, const int* act, const float2* f, float2* out) {
+void coarsest_solve(Context& c, int B, int c0, const int* act, const float2* f, float2* out) {
   Level& L = *c.levels.back();
   const LevelView V = L.view();
   float2* tbuf = L.t.p + size_t(c0) * L.N();
@@ -238,12 +247,12 @@ static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const fl
     // initial guess, shared-memory tiles otherwise)
     const bool stream = c.opt_stream && e0 == nullptr && L.nx >= 16;
     if (stream)
-      launch_down_stream(c, V, w, offset, B, act, f, fscale, Cf);
+      launch_down_stream(c, V, C.win(), w, offset, B, act, f, fscale, Cf);
     else
       launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
     vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
     if (stream)
-      launch_up_stream(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, Cx, out);
+      launch_up_stream(c, V, w, offset, C.nx, C.ny, C.win(), B, act, f, fscale, Cx, out);
     else
       launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
     return;
@@ -530,8 +539,9 @@ void hb_destroy(hb_ctx* ctx) {
   }
   if (ctx->h_count) cudaFreeHost(ctx->h_count);
   for (auto& g : ctx->graphs) cudaGraphExecDestroy(g.exec);
-  cudaStreamDestroy(ctx->stream);
+  cudaStreamDestroy(ctx->stream_own ? ctx->stream_own : ctx->stream);
   cudaStreamDestroy(ctx->stream2);
+  ctx->slab.reset();  // the last member of an in-process slab group releases the group stream
   cudaEventDestroy(ctx->ev_fork);
   cudaEventDestroy(ctx->ev_join);
   delete ctx;
@@ -574,6 +584,7 @@ int hb_set_problem(hb_ctx* ctx, int nx, int ny, double h, double omega, const do
   ctx->levels.clear();
   ctx->batch_cap = 0;
   ctx->ctx_valid = false;
+  ctx->slab.reset();
   HB_API_END
 }
 
@@ -606,6 +617,7 @@ int hb_build_hierarchy(hb_ctx* ctx, const hb_vcycle_cfg* cfg) {
     L->nx = P.nx / 2;
     L->ny = P.ny / 2;
     L->h = P.h * 2.0;
+    L->rows = L->hi = L->ny;  // whole grid (row slabs re-lay this in hb_slab.cu)
     L->k2.resize(L->N());
     L->gam.resize(L->N());
     const int off = (l - 1) % 2;
@@ -615,6 +627,11 @@ int hb_build_hierarchy(hb_ctx* ctx, const hb_vcycle_cfg* cfg) {
     for (double& x : L->gam) x = std::max(x, 0.0);
     ctx->levels.push_back(std::move(L));
   }
+  for (auto& L : ctx->levels) {
+    L->row0 = L->lo = 0;
+    L->rows = L->hi = L->ny;
+  }
+  ctx->slab.reset();
   for (size_t l = 0; l < ctx->levels.size(); ++l)
     fill_level_device(*ctx->levels[l], ctx->omega, cfg->alpha, cfg->beta, cfg->damping, l == 0,
                       l == int(ctx->levels.size()) - 1);
@@ -642,6 +659,7 @@ static Level& level_at(hb_ctx* ctx, int level) {
 
 int hb_operator_apply(hb_ctx* ctx, int level, int shifted, int batch, const double* u, double* y) {
   HB_API_BEGIN
+  require_whole(*ctx);
   Level& L = level_at(ctx, level);
   const size_t n = L.N() * size_t(batch);
   ctx->io_f.ensure(n);
@@ -657,6 +675,7 @@ int hb_operator_apply(hb_ctx* ctx, int level, int shifted, int batch, const doub
 
 int hb_jacobi(hb_ctx* ctx, int level, int batch, double* v, const double* f, int iters) {
   HB_API_BEGIN
+  require_whole(*ctx);
   Level& L = level_at(ctx, level);
   if (iters < 0) throw HbError{HB_ERR_ARG, "iters must be >= 0"};
   const size_t n = L.N() * size_t(batch);
@@ -680,6 +699,7 @@ int hb_jacobi(hb_ctx* ctx, int level, int batch, double* v, const double* f, int
 
 int hb_restrict(hb_ctx* ctx, int level, int batch, const double* fine, double* coarse) {
   HB_API_BEGIN
+  require_whole(*ctx);
   Level& L = level_at(ctx, level);
   const size_t n = L.N() * size_t(batch), nc = n / 4;
   ctx->io_f.ensure(n);
@@ -696,6 +716,7 @@ int hb_restrict(hb_ctx* ctx, int level, int batch, const double* fine, double* c
 
 int hb_prolong(hb_ctx* ctx, int level, int batch, const double* coarse, double* fine) {
   HB_API_BEGIN
+  require_whole(*ctx);
   Level& L = level_at(ctx, level);
   const size_t n = L.N() * size_t(batch), nc = n / 4;
   ctx->io_f.ensure(n);
@@ -713,6 +734,7 @@ int hb_prolong(hb_ctx* ctx, int level, int batch, const double* coarse, double* 
 
 int hb_coarse_solve(hb_ctx* ctx, int batch, const double* f, double* x) {
   HB_API_BEGIN
+  require_whole(*ctx);
   require_hier(*ctx);
   ensure_batch(*ctx, batch);
   Level& C = *ctx->levels.back();
@@ -730,6 +752,7 @@ int hb_coarse_solve(hb_ctx* ctx, int batch, const double* f, double* x) {
 
 int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* z) {
   HB_API_BEGIN
+  require_whole(*ctx);
   require_hier(*ctx);
   if (batch < 1) throw HbError{HB_ERR_ARG, "batch must be >= 1"};
   ensure_batch(*ctx, batch);
@@ -757,6 +780,7 @@ int hb_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const 
               double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
               uint8_t* breakdown) {
   HB_API_BEGIN
+  require_whole(*ctx);
   require_hier(*ctx);
   if (!B || !X) throw HbError{HB_ERR_ARG, "null B or X"};
   const size_t n = ctx->levels[0]->N() * size_t(batch);
@@ -777,6 +801,7 @@ int hb_fgmres_device(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch,
                      double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
                      uint8_t* breakdown) {
   HB_API_BEGIN
+  require_whole(*ctx);
   if (!dB || !dX) throw HbError{HB_ERR_ARG, "null device buffer"};
   fgmres_dev(*ctx, cfg, kind, batch, static_cast<const double2*>(dB), static_cast<double2*>(dX), hist, hist_stride,
              hist_len, iters, converged, breakdown);

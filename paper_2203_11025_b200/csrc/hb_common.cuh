@@ -64,4 +64,20 @@ __device__ __forceinline__ float2 stencil_at(const float2* __restrict__ u, int n
   return cscale(y, s);
 }
 
+// same at storage index p of a row-slab field (u indexed by storage position;
+// the rows above / below the slab are its ghost rows), bounds on global (ix, iy)
+__device__ __forceinline__ float2 stencil_at_p(const float2* __restrict__ u, size_t p, int nx, int ny, int ix, int iy,
+                                               float2 d, float inv_h2) {
+  float2 nb = make_float2(0.f, 0.f);
+  if (ix > 0) nb = cadd(nb, ld(u, p - 1));
+  if (ix + 1 < nx) nb = cadd(nb, ld(u, p + 1));
+  if (iy > 0) nb = cadd(nb, ld(u, p - nx));
+  if (iy + 1 < ny) nb = cadd(nb, ld(u, p + nx));
+  const float2 c = ld(u, p);
+  float2 y = cmul(d, c);
+  y.x = fmaf(-inv_h2, nb.x, y.x);
+  y.y = fmaf(-inv_h2, nb.y, y.y);
+  return y;
+}
+
 }  // namespace hb

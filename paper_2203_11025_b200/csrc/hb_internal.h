@@ -66,18 +66,29 @@ struct DBuf {
   }
 };
 
+// Row window of one level's storage (all rows are GLOBAL row indices).  A
+// whole-grid level is {0, ny, 0, ny}; a row slab of a distributed grid stores
+// rows [row0, row0 + rows) = its owned rows [lo, hi) plus ghost rows, and rows
+// outside [0, ny) of the storage are zero-padding (outside the domain).
+struct RowWin {
+  int row0, rows;  // storage origin and row count (batch stride = nx * rows)
+  int lo, hi;      // rows this slab owns (computed / emitted)
+};
+
 // device view of one multigrid level (passed by value to kernels)
 struct LevelView {
-  int nx, ny;
+  int nx, ny;        // GLOBAL grid size
   float inv_h2;
   const float2* dM;  // diagonal of the shifted operator M^h (c64)
   const float2* dA;  // diagonal of A^h (c64)
   const float* k2f;  // kappa^2 (fp32)
   const float2* wdi; // damping / diag(M^h) (c64), the Jacobi update factor
+  RowWin w;          // storage window; only the row-streaming legs and the Krylov kernels honour a slab window
 };
 
 struct Level {
-  int nx = 0, ny = 0;
+  int nx = 0, ny = 0;  // global size
+  int row0 = 0, rows = 0, lo = 0, hi = 0;  // storage window (RowWin); whole grid: 0, ny, 0, ny
   double h = 0;
   std::vector<double> k2, gam;  // host fp64 coefficients (inc/stencil.hpp:169-185 coarsening)
   DBuf<float2> dM, dA, wdi;
@@ -87,9 +98,10 @@ struct Level {
   // V-cycle work buffers [B][N]
   DBuf<float2> f, v, t, x;
   LevelView view() const {
-    return LevelView{nx, ny, float(1.0 / (h * h)), dM.p, dA.p, k2f.p, wdi.p};
+    return LevelView{nx, ny, float(1.0 / (h * h)), dM.p, dA.p, k2f.p, wdi.p, win()};
   }
-  size_t N() const { return size_t(nx) * ny; }
+  RowWin win() const { return RowWin{row0, rows, lo, hi}; }
+  size_t N() const { return size_t(nx) * rows; }  // storage nodes per column
 };
 
 struct ConvW {
@@ -117,6 +129,7 @@ struct Prof {
 };
 
 struct Context;
+struct SlabState;  // row-slab decomposition of one grid (hb_slab.cu)
 
 // ---- multigrid / operator launchers (hb_mg.cu)
 void launch_apply(Context& c, const LevelView& L, int which, int B, const int* act, const float2* u, float2* y,
@@ -151,10 +164,11 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
 bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                     const float* bsrc, int cb, bool b_ctx, int relu, float* out);
 // row-streaming legs, zero initial guess (hb_mg_stream.cu)
-void launch_down_stream(Context& c, const LevelView& L, float damping, int offset, int B, const int* act, const float2* f,
-                        const float* fscale, float2* fc);
-void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B, const int* act,
-                      const float2* f, const float* fscale, const float2* vc, float2* z);
+// cw: storage window of the coarse field (down: emitted rows [cw.lo, cw.hi); up: vc)
+void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float damping, int offset, int B,
+                        const int* act, const float2* f, const float* fscale, float2* fc);
+void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, const RowWin& cw,
+                      int B, const int* act, const float2* f, const float* fscale, const float2* vc, float2* z);
 // network pack / unpack (hb_net.cu)
 void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const int* act, const float2* r,
                        const float* rscale, float* x /*NHWC, 3 ch*/);
@@ -168,12 +182,22 @@ void launch_residual(Context& c, const LevelView& L, int B, const int* act, cons
 // ---- Krylov (hb_krylov.cu)
 struct ColState;
 void krylov_alloc(Context& c, int B, int m, int hist_cap);
+// gsum != nullptr: row-slab split mode (fold the slab's partial sums into
+// gsum[B][kMaxDots] and stop; the *_finish launchers run the scalar part on the
+// slab-summed gsum)
+constexpr int kMaxDots = 2 * kMaxRestart + 1;
 void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, float2* V0, int hist_cap,
-                       double rel_tol, int max_iters);
-void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V);
+                       double rel_tol, int max_iters, double2* gsum = nullptr);
+void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V, double2* gsum = nullptr);
 void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* V, int hist_cap, double rel_tol,
-                      int max_iters);
+                      int max_iters, double2* gsum = nullptr);
+void launch_fg_restart_finish(Context& c, int B, const double2* gsum, int hist_cap, double rel_tol, int max_iters);
+void launch_fg_adots_finish(Context& c, int B, int j, const double2* gsum);
+void launch_fg_update_finish(Context& c, int B, int j, int m, const double2* gsum, int hist_cap, double rel_tol,
+                             int max_iters);
 void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x);
+void krylov_report(Context& c, int B, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv,
+                   uint8_t* brk);
 
 // ---- profiling / launch accounting
 int prof_begin(Context& c, int cls);
@@ -198,6 +222,7 @@ enum ProfClass {
 struct Context {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t stream_own = nullptr;  // the context's own stream while an in-process slab group lends it one
   cudaStream_t stream2 = nullptr;  // second branch for split V-cycles
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_at_coarse = nullptr;  // recorded when a V-cycle reaches its coarsest level
@@ -282,6 +307,8 @@ struct Context {
   };
   std::vector<DetailRec> detail, detail_done;
   int64_t launches = 0;
+  // row-slab decomposition (null: whole grid)
+  std::shared_ptr<SlabState> slab;
 };
 
 // Launch with programmatic dependent launch (PDL, sm_90+): the kernel may be
@@ -304,6 +331,10 @@ inline void launch_pdl(Context& c, void (*k)(KArgs...), dim3 grid, dim3 block, s
 }
 
 void ensure_batch(Context& c, int B);
+// coarsest-level solve on a whole-grid coarsest level (hb_api.cu)
+void coarsest_solve(Context& c, int B, int c0, const int* act, const float2* f, float2* out);
+void fill_level_device(Level& L, double omega, double alpha, double beta, double damping, bool fp64A, bool fp64M);
+void require_whole(const Context& c);  // throws for a row-slab context on whole-grid entry points
 // V-cycle driver (hb_api.cu)
 void vcycle(Context& c, int B, const int* act, const float2* f0, const float* fscale, const float2* e0, float2* z);
 void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2* r, const float* rscale,

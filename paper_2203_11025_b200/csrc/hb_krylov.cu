@@ -58,11 +58,22 @@ __device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
 }
 
 struct FineView {
-  int nx, ny;
+  int nx, ny;           // global grid
   double inv_h2;
   const double2* dA64;  // fp64 diagonal of A^h (restart residual)
   const float2* dA;     // fp32 diagonal (A z per inner step)
+  RowWin w;             // storage window: vectors are [B][w.rows][nx]; nodes of rows [w.lo, w.hi) are owned
+  __device__ __forceinline__ size_t ns() const { return size_t(nx) * w.rows; }         // batch stride
+  __device__ __forceinline__ size_t nown() const { return size_t(nx) * (w.hi - w.lo); }  // owned nodes
+  __device__ __forceinline__ size_t off() const { return size_t(nx) * (w.lo - w.row0); } // first owned node
 };
+
+// Row-slab mode (gsum != nullptr): the per-column fold of the CTA partials is
+// written to gsum[b][KMAXV] and the kernel stops there; the caller sums gsum
+// over all slabs (NCCL allreduce or the in-process group sum) and launches the
+// *_finish kernel, which runs the scalar recurrence on the global sums.  Every
+// slab receives the same bits, so the replicated Hessenberg / Givens / flags
+// stay identical across slabs.
 
 // last CTA of column b? (classic threadfence + ticket pattern; resets the ticket)
 __device__ bool last_cta(unsigned* ticket, int b, int nblk) {
@@ -89,11 +100,14 @@ __device__ void cta_fold(double2 (*part)[KMAXV], int nv, double2* out) {
 }
 
 // r = b - A x (fp64), V0raw = r, ||r||^2 -> restart logic (inc/krylov.hpp:143-188)
+__device__ void restart_scalar(ColState& S, int b, double t, double* hist, int hist_cap, double rel_tol,
+                               int max_iters, int* act, float* scale_out, int* count);
+
 __global__ void __launch_bounds__(KT) k_restart(FineView F, int B, ColState* st, const double2* __restrict__ bvec,
                                                 const double2* __restrict__ x, float2* __restrict__ V0,
                                                 double* part, unsigned* ticket, double* hist, int hist_cap,
                                                 double rel_tol, int max_iters, int* act, float* scale_out,
-                                                int* count) {
+                                                int* count, double2* gsum) {
   pdl_enter();
   const int b = blockIdx.y;
   ColState& S = st[b];
@@ -104,24 +118,26 @@ __global__ void __launch_bounds__(KT) k_restart(FineView F, int B, ColState* st,
     }
     return;
   }
-  const size_t N = size_t(F.nx) * F.ny;
-  const double2* xb = x + b * N;
-  const double2* bb = bvec + b * N;
+  const size_t N = F.ns(), NO = F.nown(), OFF = F.off();
+  const double2* xb = x + b * N + OFF;
+  const double2* bb = bvec + b * N + OFF;
+  const double2* dA64 = F.dA64 + OFF;
+  float2* v0 = V0 + b * N + OFF;
   double acc = 0.0;
-  for (size_t base = size_t(blockIdx.x) * KTILE; base < N; base += size_t(gridDim.x) * KTILE) {
+  for (size_t base = size_t(blockIdx.x) * KTILE; base < NO; base += size_t(gridDim.x) * KTILE) {
 #pragma unroll
     for (int q = 0; q < KNPT; ++q) {
       const size_t p = base + q * KT + threadIdx.x;
-      if (p >= N) break;
-      const int ix = int(p % F.nx), iy = int(p / F.nx);
+      if (p >= NO) break;
+      const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row
       double2 nb = make_double2(0.0, 0.0);
       if (ix > 0) nb = dadd(nb, xb[p - 1]);
       if (ix + 1 < F.nx) nb = dadd(nb, xb[p + 1]);
       if (iy > 0) nb = dadd(nb, xb[p - F.nx]);
       if (iy + 1 < F.ny) nb = dadd(nb, xb[p + F.nx]);
-      const double2 ax = zsub(zmul(F.dA64[p], xb[p]), zscale(nb, F.inv_h2));
+      const double2 ax = zsub(zmul(dA64[p], xb[p]), zscale(nb, F.inv_h2));
       const double2 r = zsub(bb[p], ax);
-      V0[b * N + p] = make_float2(float(r.x), float(r.y));
+      v0[p] = make_float2(float(r.x), float(r.y));
       acc += r.x * r.x + r.y * r.y;
     }
   }
@@ -138,6 +154,23 @@ __global__ void __launch_bounds__(KT) k_restart(FineView F, int B, ColState* st,
   if (threadIdx.x != 0) return;
   double t = 0.0;
   for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
+  if (gsum) {
+    gsum[size_t(b) * KMAXV] = make_double2(t, 0.0);
+    return;
+  }
+  restart_scalar(S, b, t, hist, hist_cap, rel_tol, max_iters, act, scale_out, count);
+}
+
+__global__ void k_restart_finish(int B, ColState* st, const double2* gsum, double* hist, int hist_cap,
+                                 double rel_tol, int max_iters, int* act, float* scale_out, int* count) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || st[b].frozen) return;
+  restart_scalar(st[b], b, gsum[size_t(b) * KMAXV].x, hist, hist_cap, rel_tol, max_iters, act, scale_out, count);
+}
+
+// restart logic on the squared global residual norm t (inc/krylov.hpp:143-188)
+__device__ void restart_scalar(ColState& S, int b, double t, double* hist, int hist_cap, double rel_tol,
+                               int max_iters, int* act, float* scale_out, int* count) {
   const double beta = sqrt(t);
   S.k = 0;
   S.active = 0;
@@ -195,18 +228,23 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[NF]) {
 // the thread's nodes and reduced across the warp by one 16-float butterfly,
 // the warp partial accumulates in shared memory; warps and CTAs fold in fp64;
 // the last CTA of the column forms the MGS coefficients.
+__device__ void adots_scalar(ColState& S, int j, const double2* red);
+
 template <int NT>
 __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
                                               const float2* __restrict__ Z, float2* __restrict__ W,
-                                              const float2* __restrict__ V, double2* part, unsigned* ticket) {
+                                              const float2* __restrict__ V, double2* part, unsigned* ticket,
+                                              double2* gsum) {
   pdl_enter();
   const int b = blockIdx.y;
   if (!act[b]) return;
-  const size_t N = size_t(F.nx) * F.ny;
-  const size_t BN = size_t(B) * N;
-  const float2* zb = Z + b * N;
-  float2* wb = W + b * N;
-  const float2* Vj = V + size_t(j) * BN + b * N;
+  const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
+  const size_t BN = size_t(B) * NS;
+  const float2* zb = Z + b * NS + OFF;
+  float2* wb = W + b * NS + OFF;
+  const float2* dA = F.dA + OFF;
+  V += OFF;
+  const float2* Vj = V + size_t(j) * BN + b * NS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nv = 2 * j + 1;
   const float inv_h2 = float(F.inv_h2);
@@ -223,8 +261,8 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
       const size_t p = base + q * NT + threadIdx.x;
       ok[q] = p < N;
       if (ok[q]) {
-        const int ix = int(p % F.nx), iy = int(p / F.nx);
-        w[q] = stencil_at(zb, F.nx, F.ny, ix, iy, ld(F.dA, p), inv_h2, 1.0f);
+        const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
+        w[q] = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
         wb[p] = w[q];
         vj[q] = ld(Vj, p);
       } else {
@@ -235,7 +273,7 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
       float2 a[4][KNPT];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float2* Vi = V + size_t(i0 + u) * BN + b * N;
+        const float2* Vi = V + size_t(i0 + u) * BN + b * NS;
 #pragma unroll
         for (int q = 0; q < KNPT; ++q)
           a[u][q] = (ok[q] && i0 + u <= j) ? ld(Vi, base + q * NT + threadIdx.x) : make_float2(0.f, 0.f);
@@ -309,15 +347,31 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
       s.y += pp->y;
     }
     red[t] = s;
+    if (gsum) gsum[size_t(b) * KMAXV + t] = s;
   }
+  if (gsum) return;
+  adots_scalar(st[b], j, red);
+}
+
+__global__ void k_adots_finish(int j, ColState* st, const int* act, const double2* gsum) {
+  const int b = blockIdx.x;
+  if (!act[b]) return;
+  __shared__ double2 red[KMAXV];
+  for (int t = threadIdx.x; t < 2 * j + 1; t += blockDim.x) red[t] = gsum[size_t(b) * KMAXV + t];
+  adots_scalar(st[b], j, red);
+}
+
+// MGS coefficients from the global sums red[0..j] = <Vraw_i, w>, red[j+1..2j] =
+// <Vraw_j, Vraw_k> (called by a whole CTA; red in shared memory)
+__device__ void adots_scalar(ColState& S, int j, const double2* red) {
+  const int lane = threadIdx.x & 31;
   // stage the Gram rows this step needs, then warp 0 forms the MGS coefficients
   // with lanes in parallel: h_i = s_i <Vraw_i, w> - sum_{k<i} h_k^(cgs) G_ik
   // (first-order Gram correction; G = O(eps32) off the diagonal)
-  ColState& S = st[b];
   __shared__ double2 sG[kMaxRestart][kMaxRestart];
   __shared__ double ssc[kMaxRestart + 1];
-  for (int t = threadIdx.x; t <= j; t += NT) ssc[t] = S.scale[t];
-  for (int t = threadIdx.x; t < j * j; t += NT) {
+  for (int t = threadIdx.x; t <= j; t += blockDim.x) ssc[t] = S.scale[t];
+  for (int t = threadIdx.x; t < j * j; t += blockDim.x) {
     const int i = t / j, kk = t % j;
     if (kk < i) sG[i][kk] = S.G[i][kk];
   }
@@ -342,21 +396,26 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
 }
 
 // V_{j+1}raw = w - sum_i coef_i Vraw_i ; hnorm ; Givens + convergence (inc/krylov.hpp:219-254)
+__device__ void update_scalar(ColState& S, int b, int j, int m, double t, int* act, double* hist, int hist_cap,
+                              double rel_tol, int max_iters, float* scale_out);
+
 __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, ColState* st, int* act,
                                                const float2* __restrict__ W, float2* __restrict__ V, double* part,
                                                unsigned* ticket, double* hist, int hist_cap, double rel_tol,
-                                               int max_iters, float* scale_out) {
+                                               int max_iters, float* scale_out, double2* gsum) {
   pdl_enter();
   const int b = blockIdx.y;
   if (!act[b]) return;
   ColState& S = st[b];
-  const size_t N = size_t(F.nx) * F.ny;
-  const size_t BN = size_t(B) * N;
+  const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
+  const size_t BN = size_t(B) * NS;
+  W += OFF;
+  V += OFF;
   __shared__ float2 cf[kMaxRestart + 4];
   for (int i = threadIdx.x; i <= j; i += KT) cf[i] = make_float2(float(S.coef[i].x), float(S.coef[i].y));
   __syncthreads();
-  const float2* wb = W + b * N;
-  float2* Vn = V + size_t(j + 1) * BN + b * N;
+  const float2* wb = W + b * NS;
+  float2* Vn = V + size_t(j + 1) * BN + b * NS;
   double acc = 0.0;
   for (size_t base = size_t(blockIdx.x) * KTILE; base < N; base += size_t(gridDim.x) * KTILE) {
     float2 t[KNPT];
@@ -371,7 +430,7 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
       float2 a[4][KNPT];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const float2* Vi = V + size_t(i0 + u) * BN + b * N;
+        const float2* Vi = V + size_t(i0 + u) * BN + b * NS;
 #pragma unroll
         for (int q = 0; q < KNPT; ++q)
           a[u][q] = (ok[q] && i0 + u <= j) ? ld(Vi, base + q * KT + threadIdx.x) : make_float2(0.f, 0.f);
@@ -406,6 +465,24 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
   double t = 0.0;
   for (unsigned q = lane; q < gridDim.x; q += 32) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
   t = warp_sum(t);
+  if (gsum) {
+    if (lane == 0) gsum[size_t(b) * KMAXV] = make_double2(t, 0.0);
+    return;
+  }
+  update_scalar(S, b, j, m, t, act, hist, hist_cap, rel_tol, max_iters, scale_out);
+}
+
+__global__ void k_update_finish(int j, int m, ColState* st, int* act, const double2* gsum, double* hist,
+                                int hist_cap, double rel_tol, int max_iters, float* scale_out) {
+  const int b = blockIdx.x;
+  if (!act[b]) return;
+  update_scalar(st[b], b, j, m, gsum[size_t(b) * KMAXV].x, act, hist, hist_cap, rel_tol, max_iters, scale_out);
+}
+
+// Givens + convergence on the global squared norm t of V_{j+1}raw (one warp)
+__device__ void update_scalar(ColState& S, int b, int j, int m, double t, int* act, double* hist, int hist_cap,
+                              double rel_tol, int max_iters, float* scale_out) {
+  const int lane = threadIdx.x & 31;
   const double hnorm = sqrt(t);
   __shared__ double2 hcol[kMaxRestart + 1], ssn[kMaxRestart];
   __shared__ double scs[kMaxRestart];
@@ -511,16 +588,16 @@ __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st
     }
   }
   __syncthreads();
-  const size_t N = size_t(F.nx) * F.ny;
-  const size_t BN = size_t(B) * N;
+  const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
+  const size_t BN = size_t(B) * NS;
   for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
-    double2 acc = x[b * N + p];
+    double2 acc = x[b * NS + OFF + p];
     for (int i = 0; i < k; ++i) {
-      const float2 z = ld(Z + size_t(i) * BN + b * N, p);
+      const float2 z = ld(Z + size_t(i) * BN + b * NS + OFF, p);
       acc.x += y[i].x * double(z.x) - y[i].y * double(z.y);
       acc.y += y[i].x * double(z.y) + y[i].y * double(z.x);
     }
-    x[b * N + p] = acc;
+    x[b * NS + OFF + p] = acc;
   }
 }
 
@@ -535,7 +612,7 @@ __global__ void k_init_state(ColState* st, int B) {
 
 FineView fine_view(Context& c) {
   Level& L = *c.levels[0];
-  return FineView{L.nx, L.ny, 1.0 / (L.h * L.h), L.dA64.p, L.dA.p};
+  return FineView{L.nx, L.ny, 1.0 / (L.h * L.h), L.dA64.p, L.dA.p, L.win()};
 }
 
 // one tile per CTA for small columns (latency), capped for huge columns so the
@@ -587,41 +664,67 @@ void krylov_alloc(Context& c, int B, int m, int hist_cap) {
   c.k_hist = hist_cap;
 }
 
+// owned nodes of the fine level (whole grid, or this slab's rows)
+static size_t owned_nodes(Context& c) {
+  const Level& L = *c.levels[0];
+  return size_t(L.nx) * (L.hi - L.lo);
+}
+
 void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, float2* V0, int hist_cap,
-                       double rel_tol, int max_iters) {
-  const size_t N = c.levels[0]->N();
+                       double rel_tol, int max_iters, double2* gsum) {
+  const size_t N = owned_nodes(c);
   const int nb = nblk_for(c, N, B);
   KScope ks(c, PC_KRYLOV_RESTART, double(B) * N * 40.0 + double(N) * 16.0);  // b, x (c128) in; V0 (c64) out; dA64
   HB_CUDA(cudaMemsetAsync(c.kcount.p, 0, sizeof(int), c.stream));
   launch_pdl(c, k_restart, dim3(nb, B), dim3(KT), 0, fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), b, x, V0,
                                                reinterpret_cast<double*>(c.kpart.p), c.kticket.p, c.khist.p,
-                                               hist_cap, rel_tol, max_iters, c.kact.p, c.kscale.p, c.kcount.p);
+                                               hist_cap, rel_tol, max_iters, c.kact.p, c.kscale.p, c.kcount.p, gsum);
   HB_CUDA(cudaGetLastError());
 }
 
-void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V) {
-  const size_t N = c.levels[0]->N();
+void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V, double2* gsum) {
+  const size_t N = owned_nodes(c);
   KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0) + double(N) * 8.0);  // Z_j, V_0..V_j in; w out; dA
   const int nb = nblk_adots(c, N, B, 256 * KNPT);
   launch_pdl(c, k_adots<256>, dim3(nb, B), dim3(256), 0, fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p),
-                                                   c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p);
+                                                   c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p, gsum);
   HB_CUDA(cudaGetLastError());
 }
 
 void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* V, int hist_cap, double rel_tol,
-                      int max_iters) {
-  const size_t N = c.levels[0]->N();
+                      int max_iters, double2* gsum) {
+  const size_t N = owned_nodes(c);
   const int nb = nblk_for(c, N, B);
   KScope ks(c, PC_KRYLOV_UPDATE, double(B) * N * (8.0 * (j + 1) + 16.0));  // w, V_0..V_j in; V_{j+1} out
   launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p),
                                               c.kact.p, w, V, reinterpret_cast<double*>(c.kpart.p), c.kticket.p,
-                                              c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p);
+                                              c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p, gsum);
+  HB_CUDA(cudaGetLastError());
+}
+
+// scalar halves of the split (row-slab) reductions, on the slab-summed gsum
+void launch_fg_restart_finish(Context& c, int B, const double2* gsum, int hist_cap, double rel_tol, int max_iters) {
+  c.launches++;
+  k_restart_finish<<<(B + 31) / 32, 32, 0, c.stream>>>(B, reinterpret_cast<ColState*>(c.kstate.p), gsum, c.khist.p,
+                                                      hist_cap, rel_tol, max_iters, c.kact.p, c.kscale.p, c.kcount.p);
+  HB_CUDA(cudaGetLastError());
+}
+void launch_fg_adots_finish(Context& c, int B, int j, const double2* gsum) {
+  c.launches++;
+  k_adots_finish<<<B, 64, 0, c.stream>>>(j, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, gsum);
+  HB_CUDA(cudaGetLastError());
+}
+void launch_fg_update_finish(Context& c, int B, int j, int m, const double2* gsum, int hist_cap, double rel_tol,
+                             int max_iters) {
+  c.launches++;
+  k_update_finish<<<B, 32, 0, c.stream>>>(j, m, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, gsum, c.khist.p,
+                                          hist_cap, rel_tol, max_iters, c.kscale.p);
   HB_CUDA(cudaGetLastError());
 }
 
 void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x) {
   (void)m;
-  const size_t N = c.levels[0]->N();
+  const size_t N = owned_nodes(c);
   const int nb = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
   KScope ks(c, PC_KRYLOV_FINAL, double(B) * N * (32.0 + 8.0 * m));  // x (c128) in+out, Z_0..Z_{k-1} in (upper bound k = m)
   launch_pdl(c, k_finalize, dim3(nb, B), dim3(KT), 0, fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), Z, x);
@@ -678,7 +781,7 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
     K.ticket.ensure(B);
     HB_CUDA(cudaMemsetAsync(K.ticket.p, 0, sizeof(unsigned) * B, c.stream));
   }
-  const FineView F{L.nx, L.ny, 1.0 / (L.h * L.h), L.dM64.p, L.dM.p};
+  const FineView F{L.nx, L.ny, 1.0 / (L.h * L.h), L.dM64.p, L.dM.p, L.win()};
   ColState* st = reinterpret_cast<ColState*>(K.state.p);
   const size_t BN = size_t(B) * N;
   const int g1 = int(std::min<size_t>((BN + 255) / 256, size_t(c.num_sms) * 8));
@@ -691,17 +794,19 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
   const int nb = nblk_for(c, N, B);
   const double tol = 1e-300;
   launch_pdl(c, k_restart, dim3(nb, B), dim3(KT), 0, F, B, st, K.b.p, K.x.p, K.V.p, reinterpret_cast<double*>(K.part.p),
-                                               K.ticket.p, K.hist.p, cap, tol, m, K.act.p, K.scale.p, K.count.p);
+                                               K.ticket.p, K.hist.p, cap, tol, m, K.act.p, K.scale.p, K.count.p,
+                                               (double2*)nullptr);
   const int na = nblk_adots(c, N, B, 256 * KNPT);
   const dim3 gz(unsigned(std::max<size_t>(1, std::min<size_t>((N + 255) / 256, size_t(4) * c.num_sms / B))), B);
   for (int j = 0; j < m; ++j) {
     float2* Vj = K.V.p + size_t(j) * BN;
     float2* Zj = K.Z.p + size_t(j) * BN;
     k_diag_precond<<<gz, 256, 0, c.stream>>>(int(N), K.act.p, Vj, K.scale.p, L.dM.p, Zj);
-    launch_pdl(c, k_adots<256>, dim3(na, B), dim3(256), 0, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p);
+    launch_pdl(c, k_adots<256>, dim3(na, B), dim3(256), 0, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p,
+               (double2*)nullptr);
     launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, F, B, j, m, st, K.act.p, K.W.p, K.V.p,
                                                 reinterpret_cast<double*>(K.part.p), K.ticket.p, K.hist.p, cap, tol,
-                                                m, K.scale.p);
+                                                m, K.scale.p, (double2*)nullptr);
   }
   const int nf = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
   launch_pdl(c, k_finalize, dim3(nf, B), dim3(KT), 0, F, B, st, K.Z.p, K.x.p);

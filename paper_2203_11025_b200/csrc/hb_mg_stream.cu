@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, float d
 // fine rows [y0, y1) for its 60 fine columns
 template <bool WD>
 __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float damping, int offset, int cnx, int cny,
-                                                          int rows_per_chunk, const int* act,
+                                                          RowWin cw, int rows_per_chunk, const int* act,
                                                           const float2* __restrict__ f, const float* fscale,
                                                           const float2* __restrict__ vc, float2* __restrict__ z) {
   pdl_enter();
@@ -160,12 +160,16 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
   const int lane = threadIdx.x, nx = L.nx, ny = L.ny;
   const int jx = blockIdx.x * SW_OUT - 1 + lane;
   const int c0 = 2 * jx + offset;
-  const int y0 = (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
-  if (y0 >= ny) return;
-  const int y1 = min(ny, y0 + rows_per_chunk);
-  const size_t N = size_t(nx) * ny;
-  const float2* fb = f + b * N;
-  const float2* cb = vc + size_t(b) * cnx * cny;
+  // fine rows [L.w.lo, L.w.hi) are emitted; storage rows are global - L.w.row0;
+  // loads outside the storage window (and the domain) read zero
+  const int y0 = L.w.lo + (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
+  if (y0 >= L.w.hi) return;
+  const int y1 = min(L.w.hi, y0 + rows_per_chunk);
+  const int ylo = max(0, L.w.row0), yhi = min(ny, L.w.row0 + L.w.rows);
+  const int clo = max(0, cw.row0), chi = min(cny, cw.row0 + cw.rows);
+  const size_t N = size_t(nx) * L.w.rows;
+  const float2* fb = f + b * N - size_t(L.w.row0) * nx;  // indexed by global row
+  const float2* cb = vc + size_t(b) * cnx * cw.rows - ptrdiff_t(cw.row0) * cnx;
   const float s = fscale ? fscale[b] : 1.0f;
   const float ih2 = L.inv_h2;
   const bool colok_a = c0 >= 0 && c0 < nx, colok_b = c0 + 1 >= 0 && c0 + 1 < nx;
@@ -177,24 +181,24 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
     int even;         // (y - o) even: one coarse row
   };
   auto cload = [&](int jy) {
-    return (jy >= 0 && jy < cny && jx >= 0 && jx < cnx) ? __ldg(cb + size_t(jy) * cnx + jx) : make_float2(0.f, 0.f);
+    return (jy >= clo && jy < chi && jx >= 0 && jx < cnx) ? __ldg(cb + ptrdiff_t(jy) * cnx + jx) : make_float2(0.f, 0.f);
   };
   auto load_raw = [&](int y) {
     Raw r;
     r.even = 1;
-    if (y < 0 || y >= ny) {
+    if (y < ylo || y >= yhi) {
       r.f.a = r.f.b = r.w.a = r.w.b = r.d.a = r.d.b = make_float2(0.f, 0.f);
       r.c0v = r.c1v = make_float2(0.f, 0.f);
       return r;
     }
-    const size_t o = size_t(y) * nx;
+    const ptrdiff_t o = ptrdiff_t(y) * nx, oc = ptrdiff_t(y - L.w.row0) * nx;
     r.f = ld_pair(fb + o, c0, nx);
-    r.d = ld_pair(L.dM + o, c0, nx);
+    r.d = ld_pair(L.dM + oc, c0, nx);
     if (WD) {
       r.w.a = wfrom(r.d.a, damping);
       r.w.b = wfrom(r.d.b, damping);
     } else {
-      r.w = ld_pair(L.wdi + o, c0, nx);
+      r.w = ld_pair(L.wdi + oc, c0, nx);
     }
     const int t = y - offset;
     if ((t & 1) == 0) {
@@ -219,11 +223,11 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
   };
   Raw r_c = load_raw(y0), r_p1 = load_raw(y0 + 1), r_p2 = load_raw(y0 + 2);
   Pair v_m = vrow(load_raw(y0 - 1)), v_c = vrow(r_c);
-  float2* zb = z + b * N;
+  float2* zb = z + b * N - size_t(L.w.row0) * nx;
   for (int y = y0; y < y1; ++y) {
     const Raw r_p3 = load_raw(y + 3);
     const Pair v_p = vrow(r_p1);
-    const size_t o = size_t(y) * nx;
+    const ptrdiff_t o = ptrdiff_t(y) * nx;
     const Pair mv = apply_M(r_c.d, v_m, v_c, v_p, ih2);
     const float2 fa = cscale(r_c.f.a, s), fb2 = cscale(r_c.f.b, s);
     if (lane >= 1 && lane <= SW_OUT) {
@@ -257,27 +261,30 @@ struct RowIn {
   float2 fa, fb, wa, wb, da, db;  // f (scaled, masked), wD^-1, D at the lane's two fine columns
 };
 
-__global__ void __launch_bounds__(32 * WARPS) k_down_lean(LevelView L, int offset, int rows_per_chunk, const int* act,
-                                                          const float2* __restrict__ f, const float* fscale,
-                                                          float2* __restrict__ fc) {
+__global__ void __launch_bounds__(32 * WARPS) k_down_lean(LevelView L, RowWin cw, int offset, int rows_per_chunk,
+                                                          const int* act, const float2* __restrict__ f,
+                                                          const float* fscale, float2* __restrict__ fc) {
   pdl_enter();
   const int b = blockIdx.z;
   if (act && !act[b]) return;
-  const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
+  const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2;
   const int jx = blockIdx.x * SW_OUT - 1 + lane;  // lane 0 / 31: halo
   const int c0 = 2 * jx + offset;
-  const int jy0 = (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
-  if (jy0 >= cny) return;
-  const int jy1 = min(cny, jy0 + rows_per_chunk);
-  const float2* fb = f + size_t(b) * nx * ny;
+  // coarse rows [cw.lo, cw.hi) are emitted into the coarse storage window cw;
+  // fine rows are loaded from the storage window L.w (zero outside it)
+  const int jy0 = cw.lo + (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
+  if (jy0 >= cw.hi) return;
+  const int jy1 = min(cw.hi, jy0 + rows_per_chunk);
+  const int ylo = max(0, L.w.row0), yhi = min(ny, L.w.row0 + L.w.rows);
+  const float2* fb = f + size_t(b) * nx * L.w.rows;
   const float s = fscale ? fscale[b] : 1.0f;
   const float ih2 = L.inv_h2;
   const int ca = min(max(c0, 0), nx - 1), cb = min(max(c0 + 1, 0), nx - 1);
   const float sa = (c0 >= 0 && c0 < nx) ? s : 0.f, sb = (c0 + 1 >= 0 && c0 + 1 < nx) ? s : 0.f;
   const float ma = sa != 0.f ? 1.f : 0.f, mb = sb != 0.f ? 1.f : 0.f;
   auto load = [&](int y) {
-    const bool ok = y >= 0 && y < ny;
-    const int o = (ok ? y : 0) * nx;
+    const bool ok = y >= ylo && y < yhi;
+    const int o = ((ok ? y : ylo) - L.w.row0) * nx;
     const float rm = ok ? 1.f : 0.f;
     RowIn r;
     r.fa = cscale(__ldg(fb + o + ca), sa * rm);
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_lean(LevelView L, int offse
   float2 vca = cmul(r_c.fa, r_c.wa), vcb = cmul(r_c.fb, r_c.wb);
   float2 h_m2 = make_float2(0.f, 0.f), h_m1 = h_m2;
   const bool emit_col = lane >= 1 && lane <= SW_OUT && jx < cnx;
-  float2* fcb = fc + size_t(b) * cnx * cny;
+  float2* fcb = fc + size_t(b) * cnx * cw.rows - ptrdiff_t(cw.row0) * cnx;
 #pragma unroll 2
   for (int y = yb; y <= yend; ++y) {
     const RowIn r_p3 = load(y + 3);  // in flight during this row
@@ -317,7 +324,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_lean(LevelView L, int offse
     // y = 2 jy + o + 1 closes coarse row jy
     const int t = y - offset - 1;
     if (t >= 2 * jy0 && ((t & 1) == 0) && emit_col)
-      fcb[size_t(t >> 1) * cnx + jx] = caxpy(cscale(h_m1, 0.5f), 0.25f, cadd(h_m2, h));
+      fcb[ptrdiff_t(t >> 1) * cnx + jx] = caxpy(cscale(h_m1, 0.5f), 0.25f, cadd(h_m2, h));
     h_m2 = h_m1;
     h_m1 = h;
     vma = vca;
@@ -459,9 +466,11 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_stream4(LevelView L, int of
 
 }  // namespace
 
-void launch_down_stream(Context& c, const LevelView& L, float damping, int offset, int B, const int* act,
-                        const float2* f, const float* fscale, float2* fc) {
-  const int cnx = L.nx / 2, cny = L.ny / 2;
+void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float damping, int offset, int B,
+                        const int* act, const float2* f, const float* fscale, float2* fc) {
+  const int cnx = L.nx / 2, cny = cw.hi - cw.lo;  // coarse rows emitted
+  // only the lean kernel honours row windows (row slabs)
+  const bool slab = L.w.rows != L.ny || cw.rows != L.ny / 2 || cw.lo != 0;
   const int tok = prof_begin(c, PC_DOWN);
   // rows per warp: enough warps to fill the machine, >= 4 coarse rows to amortise the halo
   static const int env_d = getenv("HB_RPC_DOWN") ? atoi(getenv("HB_RPC_DOWN")) : 0;
@@ -470,37 +479,39 @@ void launch_down_stream(Context& c, const LevelView& L, float damping, int offse
     rpc /= 2;
   if (env_d) rpc = env_d;
   const int chunks = (cny + rpc - 1) / rpc;
-  if (c.opt_wide_legs && L.nx % 4 == 0) {
+  if (c.opt_wide_legs && L.nx % 4 == 0 && !slab) {
     const dim3 grid((L.nx + SW4_FINE - 1) / SW4_FINE, (chunks + WARPS - 1) / WARPS, B);
     launch_pdl(c, k_down_stream4, dim3(grid), dim3(32, WARPS), 0, L, offset, rpc, act, f, fscale, fc);
   } else {
     const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
-    if (c.opt_lean_legs)
-      launch_pdl(c, k_down_lean, dim3(grid), dim3(32, WARPS), 0, L, offset, rpc, act, f, fscale, fc);
+    if (c.opt_lean_legs || slab)
+      launch_pdl(c, k_down_lean, dim3(grid), dim3(32, WARPS), 0, L, cw, offset, rpc, act, f, fscale, fc);
     else if (c.opt_legs_wd)
       launch_pdl(c, k_down_stream<true>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, rpc, act, f, fscale, fc);
     else
       launch_pdl(c, k_down_stream<false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, rpc, act, f, fscale, fc);
   }
-  prof_end(c, PC_DOWN, tok, double(B) * L.nx * L.ny * 10.0 + double(L.nx) * L.ny * 16.0, 0);
+  const double rows = 2.0 * cny;  // fine rows behind the emitted coarse rows
+  prof_end(c, PC_DOWN, tok, double(B) * L.nx * rows * 10.0 + double(L.nx) * rows * 16.0, 0);
   HB_CUDA(cudaGetLastError());
 }
 
-void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, int B,
-                      const int* act, const float2* f, const float* fscale, const float2* vc, float2* z) {
+void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, const RowWin& cw,
+                      int B, const int* act, const float2* f, const float* fscale, const float2* vc, float2* z) {
   const int tok = prof_begin(c, PC_UP);
   static const int env_u = getenv("HB_RPC_UP") ? atoi(getenv("HB_RPC_UP")) : 0;
+  const int nrows = L.w.hi - L.w.lo;
   int rpc = 16;
-  while (rpc > 8 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((L.ny + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
+  while (rpc > 8 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((nrows + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
     rpc /= 2;
   if (env_u) rpc = env_u;
-  const int chunks = (L.ny + rpc - 1) / rpc;
+  const int chunks = (nrows + rpc - 1) / rpc;
   const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
   if (c.opt_legs_wd)
-    launch_pdl(c, k_up_stream<true>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
+    launch_pdl(c, k_up_stream<true>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, vc, z);
   else
-    launch_pdl(c, k_up_stream<false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, rpc, act, f, fscale, vc, z);
-  prof_end(c, PC_UP, tok, double(B) * L.nx * L.ny * 18.0 + double(L.nx) * L.ny * 16.0, 0);
+    launch_pdl(c, k_up_stream<false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, vc, z);
+  prof_end(c, PC_UP, tok, double(B) * L.nx * nrows * 18.0 + double(L.nx) * nrows * 16.0, 0);
   HB_CUDA(cudaGetLastError());
 }
 

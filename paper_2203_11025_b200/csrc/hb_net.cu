@@ -753,6 +753,7 @@ int hb_net_forward(hb_ctx* ctx, int batch, int H, int W, const float* in, float*
 int hb_encode(hb_ctx* ctx) {
   HB_API_BEGIN
   if (!ctx->has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built"};
+  require_whole(*ctx);
   const Level& L = *ctx->levels[0];
   encoder_forward_dev(*ctx, L.ny, L.nx, L.k2f.p);
   HB_CUDA(cudaStreamSynchronize(ctx->stream));

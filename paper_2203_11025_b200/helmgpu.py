@@ -91,6 +91,14 @@ def lib():
                                 _u8p, _u8p]
         L.hb_fgmres_device.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _vp, _vp, _dp, C.c_int, _ip,
                                        _ip, _u8p, _u8p]
+        L.hb_slab_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]
+        L.hb_nccl_unique_id.argtypes = [C.c_char_p]
+        L.hb_slab_init_nccl.argtypes = [_vp, C.c_int, C.c_int, C.c_char_p]
+        L.hb_slab_init_local.argtypes = [C.POINTER(_vp), C.c_int]
+        L.hb_slab_rows.argtypes = [_vp, _ip, _ip]
+        L.hb_precond_apply_slab.argtypes = [_vp, C.c_int, C.c_int, _dp, _dp]
+        L.hb_fgmres_slab.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.c_int, _ip,
+                                     _ip, _u8p, _u8p]
         L.hb_rng_normals.argtypes = [C.c_uint64, C.c_int64, _dp]
         L.hb_absorbing_layer.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, _dp]
         L.hb_make_medium.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_double, C.c_double, C.c_double, C.c_int,
@@ -323,6 +331,47 @@ class Context:
                           [bool(v) for v in cv], [bool(v) for v in bk])
         return X, rep
 
+    # ---- row slabs (one large grid over several GPUs)
+    def slab_init_nccl(self, rank: int, nranks: int, nccl_id: bytes):
+        """This context becomes slab `rank` of `nranks` (one GPU per process, NCCL transport)."""
+        if len(nccl_id) != NCCL_ID_BYTES:
+            raise ValueError("nccl_id must be 128 bytes (nccl_unique_id())")
+        self._check(lib().hb_slab_init_nccl(self.h, rank, nranks, nccl_id))
+
+    def slab_rows(self):
+        lo, hi = C.c_int(), C.c_int()
+        self._check(lib().hb_slab_rows(self.h, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
+    def precond_apply_slab(self, kind, r):
+        """M_V on this process's slab rows r [B][rows][nx] (hb_slab_rows)."""
+        r = _c128(r)
+        B = 1 if r.ndim == 2 else r.shape[0]
+        z = np.zeros_like(r)
+        self._check(lib().hb_precond_apply_slab(self.h, HB_PC[kind], B, _p(r), _p(z)))
+        return z
+
+    def fgmres_slab(self, kind, B, cfg: KrylovConfig, X0=None):
+        """block_fgmres over row slabs; B, X0, X hold this process's slab rows."""
+        B = _c128(B)
+        if B.ndim == 2:
+            B = B[None]
+        nb = B.shape[0]
+        X = np.zeros_like(B)
+        cap = cfg.max_iters + 2
+        hist = np.zeros((nb, cap))
+        hl = np.zeros(nb, np.int32)
+        it = np.zeros(nb, np.int32)
+        cv = np.zeros(nb, np.uint8)
+        bk = np.zeros(nb, np.uint8)
+        kc = _KrylovCfg(cfg.restart, cfg.max_iters, cfg.rel_tol, int(cfg.flexible))
+        x0p = _p(_c128(X0)) if X0 is not None else None
+        self._check(lib().hb_fgmres_slab(self.h, C.byref(kc), HB_PC[kind], nb, _p(B), x0p, _p(X), _p(hist), cap,
+                                         _p(hl, _ip), _p(it, _ip), _p(cv, _u8p), _p(bk, _u8p)))
+        rep = SolveReport([hist[c, :hl[c]].copy() for c in range(nb)], [int(v) for v in it],
+                          [bool(v) for v in cv], [bool(v) for v in bk])
+        return X, rep
+
     def fgmres_device(self, kind, dB: int, dX: int, nb: int, cfg: KrylovConfig, want_report=True):
         """B, X are device pointers (c128 [nb][ny][nx]); e.g. torch tensors' data_ptr()."""
         kc = _KrylovCfg(cfg.restart, cfg.max_iters, cfg.rel_tol, int(cfg.flexible))
@@ -372,6 +421,45 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().hb_launch_count(self.h))
+
+
+# ------------------------------------------------------------- row slabs
+NCCL_ID_BYTES = 128
+
+
+def slab_partition(ny: int, levels: int, nslabs: int, slab: int):
+    """Level-0 rows [begin, end) of slab `slab` (host-only; multiples of 2^(levels-1))."""
+    lo, hi = C.c_int(), C.c_int()
+    rc = lib().hb_slab_partition(ny, levels, nslabs, slab, C.byref(lo), C.byref(hi))
+    if rc != 0:
+        raise ValueError(f"no {nslabs}-slab partition of {ny} rows with {levels} levels")
+    return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(NCCL_ID_BYTES)
+    if lib().hb_nccl_unique_id(buf) != 0:
+        raise RuntimeError("ncclGetUniqueId failed (libnccl.so.2 not loadable?)")
+    return buf.raw
+
+
+def slab_init_distributed(ctx: Context):
+    """Slab rank = torch.distributed rank (one GPU per process): rank 0's NCCL
+    unique id travels over the existing process group (plumbing only)."""
+    import torch.distributed as dist
+    rank, ws = dist.get_rank(), dist.get_world_size()
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    ctx.slab_init_nccl(rank, ws, obj[0])
+
+
+def slab_init_local(ctxs: Sequence[Context]):
+    """Bind contexts of this process (one device) as slabs 0..n-1; drive them through ctxs[0]."""
+    arr = (_vp * len(ctxs))(*[c.h for c in ctxs])
+    rc = lib().hb_slab_init_local(arr, len(ctxs))
+    if rc != 0:
+        msg = lib().hb_last_error(ctxs[0].h).decode()
+        raise (ValueError if rc == -1 else RuntimeError)(msg)
 
 
 # --------------------------------------------------------- setup helpers

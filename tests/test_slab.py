@@ -1,0 +1,285 @@
+"""Row-slab decomposition of one grid.
+
+CPU (gloo, world size 2): the decomposition itself -- the product's partition
+(hb_slab_partition), 2 ghost rows per side on every slab-stored level, the
+all-gathered coarsest level -- is checked by NaN poisoning: each rank holds a
+full-size array whose rows outside its slab + ghosts are NaN, runs the oracle's
+V-cycle stages on it (inc/multigrid.hpp:108-119: jacobi, residual, restrict,
+coarse solve, prolong, jacobi), keeps only its owned rows and exchanges ghost
+rows with gloo exactly where the CUDA path exchanges them (hb_slab.cu halo /
+gather_coarse).  Insufficient halos would leak NaN into owned rows; the
+gathered result must equal the whole-grid oracle cycle.
+
+GPU: the CUDA slab path (in-process groups of 2 and 4 slabs on one B200, device
+copies for halos, the group-sum kernel for the allreduce) against the
+whole-grid CUDA path and the oracle: M_V bit-for-bit, FGMRES iterations +-1
+and solutions within 1e-4, at c0 (3 levels, GMRES(10) coarse) and a c4-shaped
+4-level hierarchy with the U-Net coarse solver.
+"""
+import math
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GHOST = 2  # hb_slab.cu kGhost
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _problem(n):
+    from oracle import oracle as O
+    om = 2 * math.pi * 1.5 * n / 10
+    k2 = O.make_medium(n, n, 4321)
+    g = O.absorbing_layer(n, n, 8, 2 * om)
+    return k2, g, om
+
+
+# ------------------------------------------------------------------ CPU ---
+def test_partition_host():
+    from paper_2203_11025_b200 import helmgpu as hg
+    assert [hg.slab_partition(4096, 4, 8, r) for r in range(8)] == [(512 * r, 512 * (r + 1)) for r in range(8)]
+    b = [hg.slab_partition(128, 3, 3, r) for r in range(3)]
+    assert b[0][0] == 0 and b[-1][1] == 128 and all(x[1] == y[0] for x, y in zip(b, b[1:]))
+    assert all(lo % 4 == 0 and hi % 4 == 0 for lo, hi in b)
+    with pytest.raises(ValueError):
+        hg.slab_partition(64, 4, 16, 0)  # more slabs than 8-row units
+    with pytest.raises(ValueError):
+        hg.slab_partition(100, 4, 2, 0)  # rows not divisible by 2^(levels-1)
+
+
+def _rank_main(rank, ws, port, out_dir, n, levels):
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(ws), RANK=str(rank))
+    import torch
+    import torch.distributed as dist
+
+    from oracle import oracle as O
+    from paper_2203_11025_b200 import helmgpu as hg
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    k2, g, om = _problem(n)
+    H = O.Hierarchy(k2, g, om, 1 / 16, 1 / 2.25, levels=levels)
+    f = O.random_complex_normal(99, (n, n))
+    bounds = [hg.slab_partition(n, levels, ws, r) for r in range(ws)]
+    lo0, hi0 = bounds[rank]
+
+    def owned(l):
+        return lo0 >> l, hi0 >> l
+
+    def poison(full, l, ghosts):
+        lo, hi = owned(l)
+        out = np.full_like(full, np.nan)
+        a, b = max(0, lo - ghosts), min(full.shape[0], hi + ghosts)
+        out[a:b] = full[a:b]
+        return out
+
+    def t(a):
+        return torch.from_numpy(np.ascontiguousarray(a).view(np.float64).copy())
+
+    def halo(x, l):
+        """Owned rows of x valid -> also the GHOST rows above / below (hb_slab.cu halo)."""
+        lo, hi = owned(l)
+        reqs, bufs = [], []
+        if rank > 0:
+            reqs.append(dist.isend(t(x[lo:lo + GHOST]), rank - 1))
+            buf = torch.empty((GHOST, x.shape[1] * 2), dtype=torch.float64)
+            reqs.append(dist.irecv(buf, rank - 1))
+            bufs.append((lo - GHOST, buf))
+        if rank + 1 < ws:
+            reqs.append(dist.isend(t(x[hi - GHOST:hi]), rank + 1))
+            buf = torch.empty((GHOST, x.shape[1] * 2), dtype=torch.float64)
+            reqs.append(dist.irecv(buf, rank + 1))
+            bufs.append((hi, buf))
+        for r in reqs:
+            r.wait()
+        x = x.copy()
+        for row, buf in bufs:
+            x[row:row + GHOST] = buf.numpy().view(np.complex128)
+        return x
+
+    def gather(x, l):
+        """Owned rows of every rank -> whole level (hb_slab.cu gather_coarse)."""
+        lo, hi = owned(l)
+        parts = [None] * ws
+        dist.all_gather_object(parts, (lo, hi, x[lo:hi].copy()))
+        out = np.full_like(x, np.nan)
+        for a, b, rows in parts:
+            out[a:b] = rows
+        return out
+
+    # down legs: v = J(0, f); r = f - M v; fc = R_o r (owned coarse rows), then
+    # halo (slab levels) or gather (coarsest)
+    fl = [None] * levels
+    fl[0] = halo(poison(f, 0, 0), 0)
+    for l in range(levels - 1):
+        v = H.jacobi(np.zeros_like(fl[l]), fl[l], 0.8, 1, level=l)
+        r = fl[l] - H.apply(v, level=l, shifted=True)
+        nx, ny, _ = H.level_info(l)
+        fc = np.zeros((ny // 2, nx // 2), np.complex128)
+        O.lib().ho_restrict(nx, ny, l % 2, 2, O.cptr(np.ascontiguousarray(r)), O.cptr(fc))
+        fc = poison(fc, l + 1, 0)
+        fl[l + 1] = halo(fc, l + 1) if l + 1 < levels - 1 else gather(fc, l + 1)
+    # coarsest: replicated solve on the gathered rhs
+    xc = H.coarse_gmres(fl[-1], levels - 1)
+    # up legs: v = J(0, f) + P_o vc; z = J(v, f); owned rows, then halo for the next finer level
+    for l in range(levels - 2, -1, -1):
+        nx, ny, _ = H.level_info(l)
+        corr = np.zeros((ny, nx), np.complex128)
+        O.lib().ho_prolong(nx // 2, ny // 2, l % 2, 2, O.cptr(np.ascontiguousarray(xc)), O.cptr(corr))
+        v = H.jacobi(np.zeros_like(fl[l]), fl[l], 0.8, 1, level=l) + corr
+        z = poison(H.jacobi(v, fl[l], 0.8, 1, level=l), l, 0)
+        xc = halo(z, l) if l > 0 else z
+    z = gather(xc, 0)
+    np.save(os.path.join(out_dir, f"z{rank}.npy"), z)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "zref.npy"), H.cycle(f))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n,levels", [(64, 3), (128, 4)])
+def test_slab_vcycle_halos_gloo(tmp_path, n, levels):
+    import torch.multiprocessing as mp
+    ws = 2
+    mp.start_processes(_rank_main, args=(ws, _free_port(), str(tmp_path), n, levels), nprocs=ws, join=True,
+                       start_method="spawn")
+    zref = np.load(tmp_path / "zref.npy")
+    for r in range(ws):
+        z = np.load(tmp_path / f"z{r}.npy")
+        assert np.isfinite(z).all(), "NaN leaked into owned rows: halo too narrow"
+        np.testing.assert_allclose(z, zref, rtol=0, atol=1e-12 * np.abs(zref).max())
+
+
+# ------------------------------------------------------------------ GPU ---
+def _ctx(hg, k2, g, om, levels, coarse, net_seed=None):
+    c = hg.Context(0)
+    c.set_problem(k2, g, om, 1 / 16, 1 / 2.25)
+    c.build_hierarchy(hg.VCycleConfig(levels=levels, coarse_solver=coarse))
+    if net_seed is not None:
+        c.set_net(0, "solver", 3, 16, 3, 0)
+        c.init_net_he(0, net_seed)
+    return c
+
+
+def _group(hg, k2, g, om, levels, coarse, k, net_seed=None):
+    cs = [_ctx(hg, k2, g, om, levels, coarse, net_seed) for _ in range(k)]
+    hg.slab_init_local(cs)
+    return cs
+
+
+@pytest.fixture(scope="module")
+def hgm():
+    from paper_2203_11025_b200 import build, helmgpu
+    build.build()
+    return helmgpu
+
+
+def rel(a, b):
+    return float(np.linalg.norm(a - b) / (np.linalg.norm(b) + 1e-300))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [2, 4])
+def test_slab_precond_equals_whole_c0(hgm, k):
+    from oracle import oracle as O
+    n = 128
+    k2, g, om = _problem(n)
+    whole = _ctx(hgm, k2, g, om, 3, "gmres")
+    cs = _group(hgm, k2, g, om, 3, "gmres", k)
+    assert cs[0].slab_rows() == (0, n)
+    r = O.random_complex_normal(7, (2, n, n))
+    zw = whole.precond_apply("v", r)
+    zs = cs[0].precond_apply_slab("v", r)
+    # same per-node arithmetic on the same inputs: the legs and the replicated
+    # coarse solve reproduce the whole-grid result bit for bit
+    assert rel(zs, zw) == 0.0, rel(zs, zw)
+    H = O.Hierarchy(k2, g, om, 1 / 16, 1 / 2.25, levels=3)
+    zo = np.stack([H.cycle(r[b]) for b in range(2)])
+    assert rel(zs, zo) < 1e-4
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [2, 4])
+def test_slab_fgmres_matches_whole_c0(hgm, k):
+    n = 128
+    k2, g, om = _problem(n)
+    b = np.zeros((1, n, n), np.complex128)
+    b[0, n // 2, n // 2] = 1.0
+    cfg = hgm.KrylovConfig(restart=10, max_iters=400)
+    Xw, rw = _ctx(hgm, k2, g, om, 3, "gmres").fgmres("v", b, cfg)
+    cs = _group(hgm, k2, g, om, 3, "gmres", k)
+    Xs, rs = cs[0].fgmres_slab("v", b, cfg)
+    assert rw.converged[0] and rs.converged[0]
+    assert abs(rs.iterations[0] - rw.iterations[0]) <= 1, (rs.iterations, rw.iterations)
+    assert rel(Xs, Xw) < 1e-4
+    h0s, h0w = rs.residual_history[0], rw.residual_history[0]
+    m = min(len(h0s), len(h0w))
+    np.testing.assert_allclose(h0s[:m] / h0s[0], h0w[:m] / h0w[0], rtol=1e-3, atol=1e-9)
+    # a second solve replays the captured slab cycle graph
+    Xs2, rs2 = cs[0].fgmres_slab("v", b, cfg)
+    assert rs2.iterations == rs.iterations and rel(Xs2, Xs) < 1e-6
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("coarse", ["net", "gmres"])
+def test_slab_c4_shape(hgm, coarse):
+    """c4 structure at 256^2: 4 levels (three slab-stored, halos at levels 1
+    and 2), 2 slabs, coarsest 32^2 replicated: the classic U-Net (L=3, He init)
+    or GMRES(10).  M_V is bit-identical to the whole grid.  FGMRES(20): with
+    the random net (a stagnating, non-stationary preconditioner) one cycle is
+    compared -- after a restart its histories amplify the rounding of the
+    slab-split dot products -- with GMRES(10) two cycles."""
+    from oracle import oracle as O
+    n = 256
+    k2, g, om = _problem(n)
+    seed = 11 if coarse == "net" else None
+    whole = _ctx(hgm, k2, g, om, 4, coarse, net_seed=seed)
+    cs = _group(hgm, k2, g, om, 4, coarse, 2, net_seed=seed)
+    r = O.random_complex_normal(8, (1, n, n))
+    zw = whole.precond_apply("v", r)
+    zs = cs[0].precond_apply_slab("v", r)
+    assert rel(zs, zw) == 0.0, rel(zs, zw)
+    budget = 20 if coarse == "net" else 40
+    cfg = hgm.KrylovConfig(restart=20, max_iters=budget)
+    Xw, rw = whole.fgmres("v", r, cfg)
+    Xs, rs = cs[0].fgmres_slab("v", r, cfg)
+    assert rs.iterations == rw.iterations == [budget]
+    hw, hs = rw.residual_history[0], rs.residual_history[0]
+    np.testing.assert_allclose(hs / hs[0], hw / hw[0], rtol=1e-4)
+    assert rel(Xs, Xw) < 1e-4
+
+
+@pytest.mark.gpu
+def test_slab_nccl_single_rank(hgm):
+    """The NCCL transport with one rank (this box has one GPU): the slab
+    solve's grouped send/recv, broadcast gathers and fp64 allreduces are issued
+    and captured in the cycle graph; results equal the whole-grid solve."""
+    n = 128
+    k2, g, om = _problem(n)
+    b = np.zeros((1, n, n), np.complex128)
+    b[0, n // 3, n // 2] = 1.0
+    cfg = hgm.KrylovConfig(restart=10, max_iters=400)
+    Xw, rw = _ctx(hgm, k2, g, om, 3, "gmres").fgmres("v", b, cfg)
+    c = _ctx(hgm, k2, g, om, 3, "gmres")
+    c.slab_init_nccl(0, 1, hgm.nccl_unique_id())
+    assert c.slab_rows() == (0, n)
+    Xs, rs = c.fgmres_slab("v", b, cfg)
+    assert rs.converged[0] and abs(rs.iterations[0] - rw.iterations[0]) <= 1
+    assert rel(Xs, Xw) < 1e-4
+
+
+@pytest.mark.gpu
+def test_slab_context_rejects_whole_grid_calls(hgm):
+    n = 64
+    k2, g, om = _problem(n)
+    cs = _group(hgm, k2, g, om, 3, "gmres", 2)
+    with pytest.raises(RuntimeError, match="row slab"):
+        cs[0].precond_apply("v", np.zeros((1, n, n), np.complex128))
+    with pytest.raises(ValueError):
+        cs[1].fgmres_slab("v", np.zeros((1, n, n), np.complex128), hgm.KrylovConfig())  # not the group's slab 0

@@ -441,9 +441,19 @@ def run_ours(args, ws, rank, local):
         line["cpu_baseline"] = cpu_baseline_sample(args.config, cfg)
     for cg in groups:
         cg.close()
-    if rank == 0 and args.also:
+    also = [s for s in args.also.split(",") if s]
+    slab = None
+    if "c4slab" in also:  # every rank takes part (one slab per rank)
+        try:
+            slab = slab_budget(local, args, ws, rank)
+        except Exception as e:  # reported, not hidden
+            slab = {"error": repr(e)}
+    if rank == 0 and also:
         line["also"] = {}
-        for nm in [s for s in args.also.split(",") if s]:
+        for nm in also:
+            if nm == "c4slab":
+                line["also"][nm] = slab
+                continue
             try:
                 line["also"][nm] = fixed_budget(nm, local, args, ws, rank)
             except Exception as e:  # reported, not hidden
@@ -522,6 +532,56 @@ def fixed_budget(name, local, args, ws, rank):
     return out
 
 
+def slab_budget(local, args, ws, rank):
+    """c4 (one 4096^2 RHS, 4-level V-cycle, U-Net coarsest at 512^2) on row slabs
+    (SURVEY 8(e)): one slab per rank over NCCL when ws > 1, else an in-process
+    group of 2 slabs on this GPU (device-copy halos: the decomposition's
+    overhead against the whole-grid c4 entry).  Marginal device time per FGMRES
+    iteration = difference of two fixed budgets (same I/O and setup), max over
+    ranks."""
+    import torch
+    from paper_2203_11025_b200 import helmgpu as hg
+    from paper_2203_11025_b200 import problems
+    cfg = config_for("c4")
+    arr = problems.problem_arrays(cfg)
+    if ws == 1:
+        ctxs = [problems.gpu_setup(cfg, device=local, arr=arr)[0] for _ in range(2)]
+        hg.slab_init_local(ctxs)
+        lead, nslabs, transport = ctxs[0], 2, "in-process (device copies), 1 GPU"
+    else:
+        lead = problems.gpu_setup(cfg, device=local, arr=arr)[0]
+        hg.slab_init_distributed(lead)
+        ctxs, nslabs, transport = [lead], ws, "nccl"
+    lo, hi = lead.slab_rows()
+    B = np.ascontiguousarray(problems.rhs_block(arr)[:, lo:hi])
+    dev = torch.device("cuda", local)
+    st = torch.cuda.ExternalStream(lead.stream, device=dev)
+
+    def run(budget):
+        kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=budget, rel_tol=1e-6)
+        barrier(ws)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        X, rep = lead.fgmres_slab(cfg["precond"], B, kc)
+        e1.record(st)
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1), ws), rep
+
+    b1, b2 = 10, 10 + args.budget
+    run(b1)  # warm-up: allocations, graph capture
+    t1, _ = run(b1)
+    t2, rep = run(b2)
+    out = {"grid": cfg["n"], "levels": cfg["levels"], "slabs": nslabs, "transport": transport,
+           "rows_per_slab": hi - lo if ws > 1 else cfg["n"] // 2,
+           "ms_per_iteration": (t2 - t1) / (b2 - b1), "iterations": [b1, b2],
+           "rel_residual_end": round(float(rep.residual_history[0][-1] / rep.residual_history[0][0]), 6),
+           "note": "coarsest level all-gathered and solved replicated; 2 ghost rows per slab level"}
+    for c in ctxs:
+        c.close()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -531,7 +591,7 @@ def main():
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = one per SM)")
-    ap.add_argument("--also", default="c1,c2,c3", help="comma list of configs measured on a fixed iteration budget "
+    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")

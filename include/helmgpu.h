@@ -143,6 +143,40 @@ int hb_fgmres_device(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch,
                      double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
                      uint8_t* breakdown);
 
+/* ---- the paper's U-Net ------------------------------
+ * UNetConfig (inc/unet.hpp:113-120) and the network built by build_unet /
+ * build_encoder (inc/unet.hpp:139-257): 5x5 stride-2 down convs + batch norm +
+ * ELU, ResNet blocks, transposed 5x5 stride-2 up convs, 4 input channels
+ * (h^2 Re r, h^2 Im r, kappa^2, gamma; inc/precond.hpp:74-90), eval mode.
+ * Once set, it is the network of M_JU and M_VU (JacobiUnetPreconditioner /
+ * UnetVCyclePreconditioner with NetworkApplier, inc/precond.hpp:57-165);
+ * hb_set_net(slot 0) switches back to the classic net. */
+typedef struct hb_unet_cfg {
+  int levels;             /* downsamplings */
+  int base_channels;      /* even */
+  int resnet_per_level;
+  int bottleneck_resnets;
+  int updown_kernel;      /* odd (5) */
+  int res_kernel;         /* odd (3) */
+} hb_unet_cfg;
+/* variant 0: standalone ("unet." names), 1: encoder_solver ("enc." + "sol.");
+ * parameters are created in the reference's registry order and initialised as
+ * NetworkWeights() (seed 0x5eed) */
+int hb_set_paper_net(hb_ctx* ctx, const hb_unet_cfg* cfg, int variant);
+/* NetworkWeights(seed) initialisation (inc/unet.hpp:13-33) */
+int hb_paper_init(hb_ctx* ctx, uint64_t seed);
+int hb_paper_param_count(hb_ctx* ctx);
+/* name (NUL-terminated, cap bytes) and dims (n, c, h, w) of parameter i */
+int hb_paper_param_info(hb_ctx* ctx, int i, char* name, int cap, int* dims);
+/* in != NULL: set the parameter's values; out != NULL: read them */
+int hb_paper_param(hb_ctx* ctx, const char* name, const float* in, float* out);
+/* UNW1 checkpoints (load_checkpoint / save_checkpoint, inc/checkpoint.hpp:51-104) */
+int hb_load_checkpoint(hb_ctx* ctx, const char* path);
+int hb_save_checkpoint(hb_ctx* ctx, const char* path, const char* digest);
+/* unet_forward / solver_forward (inc/unet.hpp:261-295), eval mode:
+ * in NCHW [batch][4][H][W] -> out NCHW [batch][2][H][W] (host fp32) */
+int hb_paper_forward(hb_ctx* ctx, int batch, int H, int W, const float* in, float* out);
+
 /* ---- row slabs: one large grid over several GPUs --
  * The reference solves one grid in one process (block_fgmres,
  * inc/krylov.hpp:83-267; cycle_at, inc/multigrid.hpp:108-119); these entry

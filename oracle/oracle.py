@@ -354,6 +354,20 @@ def ref():
         R.hr_pc_apply.argtypes = [_vp, C.c_int, _dp, _dp]
         R.hr_fgmres.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, _dp, _dp, _dp, C.c_int,
                                 _ip, _ip, _ip, _ip, C.c_int, _dp]
+        R.hr_paper_create.restype = _vp
+        R.hr_paper_create.argtypes = [C.c_int] * 7 + [C.c_uint64]
+        R.hr_paper_destroy.argtypes = [_vp]
+        R.hr_paper_zero_shifts.argtypes = [_vp]
+        R.hr_paper_save.argtypes = [_vp, C.c_char_p, C.c_char_p]
+        R.hr_paper_load.argtypes = [_vp, C.c_char_p]
+        R.hr_paper_encode.argtypes = [_vp, C.c_int, C.c_int, _dp]
+        R.hr_paper_forward.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp]
+        R.hr_paper_feature.argtypes = [_vp, C.c_int, _fp]
+        R.hr_paper_pc_create.restype = _vp
+        R.hr_paper_pc_create.argtypes = [C.c_int, _vp, _vp]
+        R.hr_paper_pc_destroy.argtypes = [_vp]
+        R.hr_paper_pc_apply.argtypes = [_vp, C.c_int, _dp, _dp]
+        R.hr_paper_fgmres.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, C.c_int, _ip, _ip]
         R.hr_init()
         _ref = R
     return _ref
@@ -500,3 +514,70 @@ def ref_conv2d(x, w, b, stride=1):
     y = np.zeros((N, cout, Ho, Wo), np.float32)
     _rcheck(ref().hr_conv2d(N, cin, cout, H, W, k, stride, _p(x, _fp), _p(w, _fp), _p(b, _fp), _p(y, _fp)))
     return y
+
+
+class RefPaperNet:
+    """The reference's paper U-Net (inc/unet.hpp:113-295) with seeded weights
+    and seeded batch-norm buffers (ref_capi.cpp hr_paper_create)."""
+
+    def __init__(self, levels=3, base=8, rpl=1, bot=1, kud=5, kres=3, variant=0, seed=77):
+        self.variant = variant
+        self.h = ref().hr_paper_create(levels, base, rpl, bot, kud, kres, variant, seed)
+        if not self.h:
+            raise ValueError(ref().hr_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().hr_paper_destroy(self.h)
+            self.h = None
+
+    def zero_shifts(self):
+        ref().hr_paper_zero_shifts(self.h)
+
+    def save(self, path, digest="helmbench"):
+        _rcheck(ref().hr_paper_save(self.h, path.encode(), digest.encode()))
+
+    def encode(self, kappa2):
+        k = np.ascontiguousarray(kappa2, np.float64)
+        _rcheck(ref().hr_paper_encode(self.h, k.shape[1], k.shape[0], _p(k)))
+
+    def forward(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        B, _, H, W = x.shape
+        y = np.zeros((B, 2, H, W), np.float32)
+        _rcheck(ref().hr_paper_forward(self.h, B, H, W, _p(x, _fp), _p(y, _fp)))
+        return y
+
+
+class RefPaperPrecond:
+    """kind "ju": JacobiUnetPreconditioner, "vu": UnetVCyclePreconditioner (inc/precond.hpp:104-165)."""
+
+    def __init__(self, kind, hier, net):
+        self.hier, self.net = hier, net
+        self.nx, self.ny = hier.nx, hier.ny
+        self.h = ref().hr_paper_pc_create({"ju": 0, "vu": 1}[kind], hier.ptr, net.h)
+        if not self.h:
+            raise ValueError(ref().hr_last_error().decode())
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            ref().hr_paper_pc_destroy(self.h)
+            self.h = None
+
+    def apply(self, r):
+        r = np.ascontiguousarray(r, np.complex128)
+        z = np.zeros_like(r)
+        _rcheck(ref().hr_paper_pc_apply(self.h, r.shape[0], cptr(r), cptr(z)))
+        return z
+
+    def fgmres(self, B, restart=10, max_iters=20, rel_tol=1e-6):
+        B = np.ascontiguousarray(B, np.complex128)
+        nb = B.shape[0]
+        X = np.zeros_like(B)
+        cap = max_iters + 2
+        hist = np.zeros((nb, cap))
+        it = np.zeros(nb, np.int32)
+        hl = np.zeros(nb, np.int32)
+        _rcheck(ref().hr_paper_fgmres(self.h, restart, max_iters, rel_tol, nb, cptr(B), cptr(X), _p(hist), cap,
+                                      _p(it, _ip), _p(hl, _ip)))
+        return X, [hist[c, :hl[c]].copy() for c in range(nb)], it

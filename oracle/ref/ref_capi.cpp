@@ -14,8 +14,10 @@
 #include <chrono>
 #include <cstring>
 #include <memory>
+#include <optional>
 #include <thread>
 
+#include "helmbench/checkpoint.hpp"
 #include "helmbench/datagen.hpp"
 #include "helmbench/grid.hpp"
 #include "helmbench/krylov.hpp"
@@ -504,5 +506,188 @@ HR_EXPORT int hr_fgmres(void* p, int restart, int max_iters, double rel_tol, int
     if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
     for (auto& e : errs)
       if (!e.empty()) throw std::runtime_error(e);
+  })
+}
+
+// ---------------- paper U-Net on the reference's own builders ----
+// NetworkWeights + build_unet / build_encoder (inc/unet.hpp:10-111,139-257), eval-mode
+// forward through unet_forward / solver_forward (:261-295), UNW1 checkpoints
+// (inc/checkpoint.hpp:51-104), JacobiUnetPreconditioner / UnetVCyclePreconditioner
+// (inc/precond.hpp:104-165).  Parameters are materialised by one train-mode forward
+// (creation order = the reference's), then the batch-norm buffers are set to seeded
+// values (count = 1) so eval mode is meaningful on untrained weights.
+namespace {
+struct PaperNet {
+  std::shared_ptr<NetworkWeights> w;
+  UNetConfig cfg;
+  NetVariant variant = NetVariant::standalone;
+  std::optional<FeatureStack> feats;
+};
+}  // namespace
+
+HR_EXPORT void* hr_paper_create(int levels, int base, int rpl, int bot, int kud, int kres, int variant,
+                                uint64_t seed) {
+  try {
+    auto* p = new PaperNet();
+    p->w = std::make_shared<NetworkWeights>(seed);
+    p->cfg.levels = levels;
+    p->cfg.base_channels = base;
+    p->cfg.resnet_per_level = rpl;
+    p->cfg.bottleneck_resnets = bot;
+    p->cfg.updown_kernel = kud;
+    p->cfg.res_kernel = kres;
+    p->variant = variant ? NetVariant::encoder_solver : NetVariant::standalone;
+    const int n = 2 << levels;
+    Tensor4 in(1, 4, n, n, 0.1f);
+    if (p->variant == NetVariant::encoder_solver) {
+      RealField k(n, n);
+      for (auto& x : k.v) x = 0.3;
+      const FeatureStack fs = encoder_forward(*p->w, p->cfg, k, true);  // NetworkApplier order: encoder first
+      solver_forward(*p->w, p->cfg, in, fs, true);
+    } else {
+      unet_forward(*p->w, p->cfg, in, true);
+    }
+    Rng r(seed ^ 0x9e3779b97f4a7c15ULL);
+    for (std::size_t i = 0; i < p->w->size(); ++i) {
+      Param& q = p->w->at(i);
+      auto ends = [&](const char* s) {
+        const std::string t(s);
+        return q.name.size() >= t.size() && q.name.compare(q.name.size() - t.size(), t.size(), t) == 0;
+      };
+      if (ends(".count")) q.value.v[0] = 1.0f;
+      else if (ends(".rmean") || ends(".offset") || ends(".b") || ends(".b1") || ends(".b2"))
+        for (auto& x : q.value.v) x = float(r.uniform(-0.2, 0.2));
+      else if (ends(".rvar")) for (auto& x : q.value.v) x = float(r.uniform(0.5, 2.0));
+      else if (ends(".scale")) for (auto& x : q.value.v) x = float(r.uniform(0.5, 1.5));
+    }
+    return p;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+HR_EXPORT void hr_paper_destroy(void* p) { delete static_cast<PaperNet*>(p); }
+// zero every bias, batch-norm offset and running mean: the net becomes
+// positively homogeneous up to ELU's curvature (well-conditioned FGMRES fixtures)
+HR_EXPORT void hr_paper_zero_shifts(void* p) {
+  auto* q = static_cast<PaperNet*>(p);
+  for (std::size_t i = 0; i < q->w->size(); ++i) {
+    Param& x = q->w->at(i);
+    auto ends = [&](const char* s) {
+      const std::string t(s);
+      return x.name.size() >= t.size() && x.name.compare(x.name.size() - t.size(), t.size(), t) == 0;
+    };
+    if (ends(".b") || ends(".b1") || ends(".b2") || ends(".offset") || ends(".rmean"))
+      std::fill(x.value.v.begin(), x.value.v.end(), 0.0f);
+    if (ends("out.k"))  // damp the head: the untrained net becomes a small correction
+      for (auto& v : x.value.v) v *= 0.01f;
+    if (x.name == "unet.down0.k")  // drop the kappa^2 / gamma input channels: net(a r) = a net(r) up to ELU curvature
+      for (int o = 0; o < x.value.n; ++o)
+        for (int c = 2; c < 4; ++c)
+          for (int t = 0; t < x.value.h * x.value.w; ++t)
+            x.value.v[(std::size_t(o) * x.value.c + c) * x.value.h * x.value.w + t] = 0.0f;
+  }
+  q->feats.reset();
+}
+HR_EXPORT int hr_paper_save(void* p, const char* path, const char* digest) {
+  HR_TRY(save_checkpoint(*static_cast<PaperNet*>(p)->w, path, digest))
+}
+HR_EXPORT int hr_paper_load(void* p, const char* path) {
+  HR_TRY({
+    auto* q = static_cast<PaperNet*>(p);
+    q->w = std::make_shared<NetworkWeights>();
+    load_checkpoint(path, *q->w);
+    q->feats.reset();
+  })
+}
+HR_EXPORT int hr_paper_encode(void* p, int nx, int ny, const double* kappa2) {
+  HR_TRY({
+    auto* q = static_cast<PaperNet*>(p);
+    RealField k(nx, ny);
+    std::memcpy(k.v.data(), kappa2, sizeof(double) * k.v.size());
+    q->feats = encoder_forward(*q->w, q->cfg, k, false);
+  })
+}
+// in: NCHW [B][4][H][W] -> out NCHW [B][2][H][W]
+HR_EXPORT int hr_paper_forward(void* p, int B, int H, int W, const float* in, float* out) {
+  HR_TRY({
+    auto* q = static_cast<PaperNet*>(p);
+    Tensor4 x(B, 4, H, W);
+    std::memcpy(x.v.data(), in, sizeof(float) * x.v.size());
+    Tensor4 y = q->variant == NetVariant::standalone ? unet_forward(*q->w, q->cfg, x, false)
+                                                     : solver_forward(*q->w, q->cfg, x, q->feats.value(), false);
+    std::memcpy(out, y.v.data(), sizeof(float) * y.v.size());
+  })
+}
+// encoder feature level l -> NCHW [1][C][H>>l][W>>l]
+HR_EXPORT int hr_paper_feature(void* p, int l, float* out) {
+  HR_TRY({
+    const auto& f = static_cast<PaperNet*>(p)->feats.value().f.at(std::size_t(l));
+    std::memcpy(out, f.v.data(), sizeof(float) * f.v.size());
+  })
+}
+
+namespace {
+struct PaperPC {
+  std::unique_ptr<Preconditioner> pc;
+  HelmholtzProblem prob;
+};
+}  // namespace
+
+// kind 0: M_JU (JacobiUnetPreconditioner), 1: M_VU (UnetVCyclePreconditioner over mg's hierarchy)
+HR_EXPORT void* hr_paper_pc_create(int kind, void* mg, void* net) {
+  try {
+    auto* m = static_cast<RefMG*>(mg);
+    auto* q = static_cast<PaperNet*>(net);
+    auto* p = new PaperPC();
+    p->prob = m->prob;
+    if (kind == 0)
+      p->pc = std::make_unique<JacobiUnetPreconditioner>(p->prob, q->w, q->cfg, q->variant);
+    else
+      p->pc = std::make_unique<UnetVCyclePreconditioner>(m->hier, q->w, q->cfg, q->variant);
+    return p;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return nullptr;
+  }
+}
+HR_EXPORT void hr_paper_pc_destroy(void* p) { delete static_cast<PaperPC*>(p); }
+HR_EXPORT int hr_paper_pc_apply(void* p, int B, const double* r, double* z) {
+  HR_TRY({
+    auto* q = static_cast<PaperPC*>(p);
+    const int nx = q->prob.grid.nx, ny = q->prob.grid.ny;
+    std::vector<ComplexField> R;
+    for (int b = 0; b < B; ++b) R.push_back(to_field(r + std::size_t(b) * nx * ny * 2, nx, ny));
+    auto Z = q->pc->apply(R);
+    for (int b = 0; b < B; ++b) from_field(Z[std::size_t(b)], z + std::size_t(b) * nx * ny * 2);
+  })
+}
+// block_fgmres (inc/krylov.hpp:83) with the paper preconditioner, as run_preconditioner_test
+HR_EXPORT int hr_paper_fgmres(void* p, int restart, int max_iters, double rel_tol, int B, const double* b, double* x,
+                              double* hist, int hist_cap, int* iters, int* hlen) {
+  HR_TRY({
+    auto* q = static_cast<PaperPC*>(p);
+    const int nx = q->prob.grid.nx, ny = q->prob.grid.ny;
+    KrylovConfig cfg;
+    cfg.restart = restart;
+    cfg.max_iters = max_iters;
+    cfg.rel_tol = rel_tol;
+    cfg.flexible = true;
+    StencilOperator A(q->prob, kHelmholtzShift);
+    BatchedOp apply_A = [&A](const std::vector<ComplexField>& in) {
+      std::vector<ComplexField> out;
+      for (const auto& f : in) out.push_back(A.apply(f));
+      return out;
+    };
+    std::vector<ComplexField> Bc;
+    for (int c = 0; c < B; ++c) Bc.push_back(to_field(b + std::size_t(c) * nx * ny * 2, nx, ny));
+    auto [X, rep] = block_fgmres(apply_A, q->pc->as_batched_op(), Bc, cfg);
+    for (int c = 0; c < B; ++c) {
+      from_field(X[std::size_t(c)], x + std::size_t(c) * nx * ny * 2);
+      const auto& h = rep.residual_history[std::size_t(c)];
+      hlen[c] = int(h.size());
+      for (int i = 0; i < std::min<int>(hist_cap, int(h.size())); ++i) hist[std::size_t(c) * hist_cap + i] = h[std::size_t(i)];
+      iters[c] = rep.iterations[std::size_t(c)];
+    }
   })
 }

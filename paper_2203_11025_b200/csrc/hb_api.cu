@@ -330,12 +330,24 @@ void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2
   if (kind == HB_PC_JU) {
     // M_JU (inc/precond.hpp:112-130), damped Jacobi on A^h with omega = 0.8:
     // e1 = J_A(0, r); de = net(r - A e1) (fine-h packing, :74-83); z = J_A(e1 + de, r)
+    const bool paper = paper_active(c);
     Net& n = c.nets[0];
-    if (!n.set) throw HbError{HB_ERR_STATE, "M_JU needs net slot 0"};
+    if (!n.set && !paper) throw HbError{HB_ERR_STATE, "M_JU needs net slot 0 or the paper net"};
     Level& L = *c.levels[0];
     LevelView VA = L.view();
     VA.dM = L.dA.p;  // Jacobi / residual on A^h, not the shifted M^h
     const size_t np = size_t(B) * L.N();
+    if (paper) {  // the paper's network (inc/precond.hpp:112-130 with NetworkApplier, :57-98)
+      DBuf<float2>& e1 = c.pc_e0;
+      e1.ensure(np);
+      c.pc_res.ensure(np);
+      const float om = 0.8f;
+      launch_jacobi_zero(c, VA, om, B, act, r, rscale, e1.p);
+      launch_residual(c, VA, B, act, e1.p, r, rscale, c.pc_res.p);
+      paper_infer(c, B, act, c.pc_res.p, nullptr, e1.p, e1.p);  // e2 = e1 + net(h^2 res)
+      launch_jacobi_sweep(c, VA, om, B, act, e1.p, r, rscale, z);
+      return;
+    }
     DBuf<float>& io = c.pc_io;
     DBuf<float2>& e1 = c.pc_e0;
     io.ensure(np * 5 + np * 2);
@@ -352,6 +364,13 @@ void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2
   }
   if (kind != HB_PC_VU) throw HbError{HB_ERR_ARG, "unknown preconditioner kind"};
   // M_VU (inc/precond.hpp:151-158): e0 = net(h^2 r, kappa^2); z = cycle(e0, r)
+  if (paper_active(c)) {  // UnetVCyclePreconditioner with the paper net (inc/precond.hpp:151-158)
+    DBuf<float2>& e0 = c.pc_e0;
+    e0.ensure(size_t(B) * c.levels[0]->N());
+    paper_infer(c, B, act, r, rscale, nullptr, e0.p);
+    vcycle(c, B, act, r, rscale, e0.p, z);
+    return;
+  }
   Net& n = c.nets[0];
   if (!n.set) throw HbError{HB_ERR_STATE, "M_VU needs net slot 0"};
   Level& L = *c.levels[0];
@@ -585,6 +604,7 @@ int hb_set_problem(hb_ctx* ctx, int nx, int ny, double h, double omega, const do
   ctx->batch_cap = 0;
   ctx->ctx_valid = false;
   ctx->slab.reset();
+  ++ctx->prob_gen;
   HB_API_END
 }
 

@@ -130,6 +130,7 @@ struct Prof {
 
 struct Context;
 struct SlabState;  // row-slab decomposition of one grid (hb_slab.cu)
+struct PaperState;  // the paper's U-Net (hb_paper.cu)
 
 // ---- multigrid / operator launchers (hb_mg.cu)
 void launch_apply(Context& c, const LevelView& L, int which, int B, const int* act, const float2* u, float2* y,
@@ -269,7 +270,7 @@ struct Context {
   int* h_count = nullptr;    // pinned
   // preconditioner staging (context-owned so captured graphs see stable pointers)
   DBuf<float> pc_io, cn_io;
-  DBuf<float2> pc_e0;
+  DBuf<float2> pc_e0, pc_res;
   // options
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
@@ -309,6 +310,9 @@ struct Context {
   int64_t launches = 0;
   // row-slab decomposition (null: whole grid)
   std::shared_ptr<SlabState> slab;
+  // the paper's U-Net (inc/unet.hpp:139-257); when active it is the network of M_JU / M_VU
+  std::shared_ptr<PaperState> paper;
+  unsigned long long prob_gen = 0;  // bumped by hb_set_problem
 };
 
 // Launch with programmatic dependent launch (PDL, sm_90+): the kernel may be
@@ -343,5 +347,10 @@ void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2
 void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, const float* x, float* y);
 void encoder_forward_dev(Context& c, int H, int W, const float* k2f);
 void net_upload(Context& c, int slot);
+// paper U-Net (hb_paper.cu): e = net(h^2 s r, kappa^2, gamma) [+ base]
+bool paper_active(const Context& c);
+void paper_deactivate(Context& c);
+void paper_infer(Context& c, int B, const int* act, const float2* r, const float* rscale, const float2* base,
+                 float2* e);
 
 }  // namespace hb

@@ -675,6 +675,7 @@ int hb_set_net(hb_ctx* ctx, int slot, const hb_net_cfg* cfg) {
   n.cfg = *cfg;
   build_topology(n);
   n.set = true;
+  if (slot == 0) paper_deactivate(*ctx);  // the classic net becomes slot 0's network
   if (slot == 1) ctx->ctx_valid = false;
   HB_API_END
 }

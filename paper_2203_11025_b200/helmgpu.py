@@ -44,6 +44,11 @@ class _NetCfg(C.Structure):
                 ("ctx_ch", C.c_int)]
 
 
+class _UNetCfg(C.Structure):
+    _fields_ = [("levels", C.c_int), ("base_channels", C.c_int), ("resnet_per_level", C.c_int),
+                ("bottleneck_resnets", C.c_int), ("updown_kernel", C.c_int), ("res_kernel", C.c_int)]
+
+
 class _KrylovCfg(C.Structure):
     _fields_ = [("restart", C.c_int), ("max_iters", C.c_int), ("rel_tol", C.c_double), ("flexible", C.c_int)]
 
@@ -91,6 +96,14 @@ def lib():
                                 _u8p, _u8p]
         L.hb_fgmres_device.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _vp, _vp, _dp, C.c_int, _ip,
                                        _ip, _u8p, _u8p]
+        L.hb_set_paper_net.argtypes = [_vp, C.POINTER(_UNetCfg), C.c_int]
+        L.hb_paper_init.argtypes = [_vp, C.c_uint64]
+        L.hb_paper_param_count.argtypes = [_vp]
+        L.hb_paper_param_info.argtypes = [_vp, C.c_int, C.c_char_p, C.c_int, _ip]
+        L.hb_paper_param.argtypes = [_vp, C.c_char_p, _fp, _fp]
+        L.hb_load_checkpoint.argtypes = [_vp, C.c_char_p]
+        L.hb_save_checkpoint.argtypes = [_vp, C.c_char_p, C.c_char_p]
+        L.hb_paper_forward.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp]
         L.hb_slab_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]
         L.hb_nccl_unique_id.argtypes = [C.c_char_p]
         L.hb_slab_init_nccl.argtypes = [_vp, C.c_int, C.c_int, C.c_char_p]
@@ -145,6 +158,19 @@ class VCycleConfig:  # inc/multigrid.hpp:13-21
     beta: float = 0.5
     coarse_iters: int = 10
     coarse_solver: str = "gmres"  # gmres | jacobi | net
+
+
+@dataclasses.dataclass
+class UNetConfig:  # inc/unet.hpp:113-120 (the paper's network)
+    levels: int = 3
+    base_channels: int = 16
+    resnet_per_level: int = 1
+    bottleneck_resnets: int = 3
+    updown_kernel: int = 5
+    res_kernel: int = 3
+
+
+NET_VARIANT = {"standalone": 0, "encoder_solver": 1}  # NetVariant, inc/precond.hpp:55
 
 
 @dataclasses.dataclass
@@ -250,6 +276,46 @@ class Context:
         B, _, H, W = x.shape
         y = np.zeros((B, 2, H, W), np.float32)
         self._check(lib().hb_net_forward(self.h, B, H, W, _p(x, _fp), _p(y, _fp)))
+        return y
+
+    # the paper's U-Net (inc/unet.hpp:113-295) -- the network of M_JU / M_VU once set
+    def set_paper_net(self, cfg: UNetConfig, variant: str = "standalone"):
+        c = _UNetCfg(cfg.levels, cfg.base_channels, cfg.resnet_per_level, cfg.bottleneck_resnets,
+                     cfg.updown_kernel, cfg.res_kernel)
+        self._check(lib().hb_set_paper_net(self.h, C.byref(c), NET_VARIANT[variant]))
+
+    def paper_init(self, seed: int):
+        self._check(lib().hb_paper_init(self.h, seed))
+
+    def paper_params(self):
+        """[(name, (n, c, h, w))] in the reference's registry order."""
+        out = []
+        buf = C.create_string_buffer(256)
+        d = (C.c_int * 4)()
+        for i in range(lib().hb_paper_param_count(self.h)):
+            self._check(lib().hb_paper_param_info(self.h, i, buf, 256, d))
+            out.append((buf.value.decode(), tuple(d)))
+        return out
+
+    def paper_param(self, name: str, value=None):
+        dims = dict(self.paper_params())[name]
+        out = np.zeros(dims, np.float32)
+        inp = None if value is None else np.ascontiguousarray(value, np.float32).reshape(dims)
+        self._check(lib().hb_paper_param(self.h, name.encode(), _p(inp, _fp) if inp is not None else None,
+                                         _p(out, _fp)))
+        return out
+
+    def load_checkpoint(self, path: str):  # inc/checkpoint.hpp:83-104
+        self._check(lib().hb_load_checkpoint(self.h, os.fspath(path).encode()))
+
+    def save_checkpoint(self, path: str, digest: str = ""):  # inc/checkpoint.hpp:57-78
+        self._check(lib().hb_save_checkpoint(self.h, os.fspath(path).encode(), digest.encode()))
+
+    def paper_forward(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        B, _, H, W = x.shape
+        y = np.zeros((B, 2, H, W), np.float32)
+        self._check(lib().hb_paper_forward(self.h, B, H, W, _p(x, _fp), _p(y, _fp)))
         return y
 
     def encode(self):

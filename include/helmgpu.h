@@ -177,6 +177,15 @@ int hb_save_checkpoint(hb_ctx* ctx, const char* path, const char* digest);
  * in NCHW [batch][4][H][W] -> out NCHW [batch][2][H][W] (host fp32) */
 int hb_paper_forward(hb_ctx* ctx, int batch, int H, int W, const float* in, float* out);
 
+/* ---- training pairs ----------------------------------
+ * gen_sample_pair (inc/datagen.hpp:191-219) for `count` seeds: x ~ CN(0, I)
+ * from Rng(seed), b = A x, k = k_forced (>= 0) or uniform_int(1, k_max),
+ * x~ = FGMRES(A, M_V, b, 0; restart 10, k iterations, tol 1e-6), r = b - A x~,
+ * e = x - x~.  r_out, e_out: host c128 [count][ny][nx]; k_used may be NULL.
+ * Samples are grouped by k into batched device solves. */
+int hb_gen_sample_pairs(hb_ctx* ctx, int count, const uint64_t* seeds, int k_forced, int k_max, double* r_out,
+                        double* e_out, int* k_used);
+
 /* ---- row slabs: one large grid over several GPUs --
  * The reference solves one grid in one process (block_fgmres,
  * inc/krylov.hpp:83-267; cycle_at, inc/multigrid.hpp:108-119); these entry

@@ -368,6 +368,7 @@ def ref():
         R.hr_paper_pc_destroy.argtypes = [_vp]
         R.hr_paper_pc_apply.argtypes = [_vp, C.c_int, _dp, _dp]
         R.hr_paper_fgmres.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, C.c_int, _ip, _ip]
+        R.hr_gen_sample_pair.argtypes = [_vp, C.c_uint64, C.c_int, C.c_int, _dp, _dp]
         R.hr_init()
         _ref = R
     return _ref
@@ -581,3 +582,11 @@ class RefPaperPrecond:
         _rcheck(ref().hr_paper_fgmres(self.h, restart, max_iters, rel_tol, nb, cptr(B), cptr(X), _p(hist), cap,
                                       _p(it, _ip), _p(hl, _ip)))
         return X, [hist[c, :hl[c]].copy() for c in range(nb)], it
+
+
+def ref_gen_sample_pair(hier, seed, k_forced=-1, k_max=10):
+    """gen_sample_pair (inc/datagen.hpp:191-219) of the reference: (r, e)."""
+    r = np.zeros((hier.ny, hier.nx), np.complex128)
+    e = np.zeros_like(r)
+    _rcheck(ref().hr_gen_sample_pair(hier.ptr, seed, k_forced, k_max, cptr(r), cptr(e)))
+    return r, e

@@ -691,3 +691,13 @@ HR_EXPORT int hr_paper_fgmres(void* p, int restart, int max_iters, double rel_to
     }
   })
 }
+
+// ---------------- training pairs: gen_sample_pair (inc/datagen.hpp:191-219)
+HR_EXPORT int hr_gen_sample_pair(void* mg, uint64_t seed, int k_forced, int k_max, double* r, double* e) {
+  HR_TRY({
+    auto* m = static_cast<RefMG*>(mg);
+    const SamplePair s = gen_sample_pair(m->prob, *m->hier, seed, k_forced, k_max);
+    from_field(s.r, r);
+    from_field(s.e, e);
+  })
+}

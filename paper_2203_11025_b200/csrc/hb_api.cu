@@ -483,6 +483,10 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
   if (hist || hist_len || iters || conv || brk) krylov_report(c, B, hist, hist_stride, hist_len, iters, conv, brk);
 }
 
+void fgmres_dev_entry(Context& c, const hb_krylov_cfg* cfg, int kind, int B, const double2* dB, double2* dX) {
+  fgmres_dev(c, cfg, kind, B, dB, dX, nullptr, 0, nullptr, nullptr, nullptr, nullptr);
+}
+
 }  // namespace hb
 
 // ===================================================================== C ABI

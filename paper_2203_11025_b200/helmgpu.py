@@ -104,6 +104,7 @@ def lib():
         L.hb_load_checkpoint.argtypes = [_vp, C.c_char_p]
         L.hb_save_checkpoint.argtypes = [_vp, C.c_char_p, C.c_char_p]
         L.hb_paper_forward.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp]
+        L.hb_gen_sample_pairs.argtypes = [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.c_int, _dp, _dp, _ip]
         L.hb_slab_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]
         L.hb_nccl_unique_id.argtypes = [C.c_char_p]
         L.hb_slab_init_nccl.argtypes = [_vp, C.c_int, C.c_int, C.c_char_p]
@@ -396,6 +397,18 @@ class Context:
         rep = SolveReport([hist[c, :hl[c]].copy() for c in range(nb)], [int(v) for v in it],
                           [bool(v) for v in cv], [bool(v) for v in bk])
         return X, rep
+
+    def gen_sample_pairs(self, seeds, k_forced=-1, k_max=10):
+        """gen_sample_pair (inc/datagen.hpp:191-219) for each seed: (r, e, k) with
+        r, e complex128 [count][ny][nx] and k the FGMRES iterations drawn."""
+        seeds = np.ascontiguousarray(seeds, np.uint64)
+        cnt = seeds.shape[0]
+        r = np.zeros((cnt, self.ny, self.nx), np.complex128)
+        e = np.zeros_like(r)
+        k = np.zeros(cnt, np.int32)
+        self._check(lib().hb_gen_sample_pairs(self.h, cnt, seeds.ctypes.data_as(C.POINTER(C.c_uint64)), k_forced,
+                                              k_max, _p(r), _p(e), _p(k, _ip)))
+        return r, e, k
 
     # ---- row slabs (SURVEY 8(e): one large grid over several GPUs)
     def slab_init_nccl(self, rank: int, nranks: int, nccl_id: bytes):

@@ -169,3 +169,33 @@ def test_classic_net_switches_back(hg, gold):
     c.init_net_he(0, 3)
     z_classic = c.precond_apply("ju", gold["r"])
     assert rel(z_classic, z_paper) > 1e-3
+
+
+@pytest.mark.gpu
+def test_training_pairs_match_reference(hg, gold):
+    """gen_sample_pair (inc/datagen.hpp:191-219) batched on the device: k = 0
+    pins the draws bit for bit (imaginary part first, as the compiled reference
+    evaluates Complex(normal(), normal())), k = 3 and the seeded random k the
+    FGMRES(M_V) part; every pair satisfies A e = r (rel_residual_defect,
+    :221-230, checked < 1e-10 by the reference's generator)."""
+    c = hg.Context(0)
+    c.set_problem(gold["k2"], gold["gamma"], float(gold["omega"]), 1 / 16, 1 / 2.25)
+    c.build_hierarchy(hg.VCycleConfig(levels=3))
+    r0, e0, k0 = c.gen_sample_pairs([101], k_forced=0)
+    assert k0.tolist() == [0]
+    assert np.array_equal(e0[0], gold["pair_101_e"])
+    assert rel(r0[0], gold["pair_101_r"]) < 1e-14
+    seeds = [102, 103, 104]
+    r, e, k = c.gen_sample_pairs(seeds[:1], k_forced=3)
+    assert rel(r[0], gold["pair_102_r"]) < 1e-4 and rel(e[0], gold["pair_102_e"]) < 1e-4
+    r, e, k = c.gen_sample_pairs(seeds[1:])
+    assert all(1 <= x <= 10 for x in k)
+    for i, s in enumerate(seeds[1:]):
+        # r is the residual of a complex64-basis iterate (D0) after k steps, so
+        # its relative error grows as it shrinks: 1e-3; e = x - x~ to 1e-4
+        assert rel(r[i], gold[f"pair_{s}_r"]) < 1e-3, (s, rel(r[i], gold[f"pair_{s}_r"]))
+        assert rel(e[i], gold[f"pair_{s}_e"]) < 1e-4
+    from oracle import oracle as O
+    H = O.Hierarchy(gold["k2"], gold["gamma"], float(gold["omega"]), 1 / 16, 1 / 2.25, levels=3)
+    for i in range(2):
+        assert rel(H.apply(e[i]), r[i]) < 1e-10  # A e = r in fp64 (the generator's invariant)

@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_stream(LevelView L, float d
 
 // up leg: grid (ceil(cnx / 30), ceil(row chunks / WARPS), B); each warp produces
 // fine rows [y0, y1) for its 60 fine columns
-template <bool WD>
+template <bool WD, bool SLAB>  // SLAB: honour row windows (whole grid: compile-time identity)
 __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float damping, int offset, int cnx, int cny,
                                                           RowWin cw, int rows_per_chunk, const int* act,
                                                           const float2* __restrict__ f, const float* fscale,
@@ -162,14 +162,17 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
   const int c0 = 2 * jx + offset;
   // fine rows [L.w.lo, L.w.hi) are emitted; storage rows are global - L.w.row0;
   // loads outside the storage window (and the domain) read zero
-  const int y0 = L.w.lo + (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
-  if (y0 >= L.w.hi) return;
-  const int y1 = min(L.w.hi, y0 + rows_per_chunk);
-  const int ylo = max(0, L.w.row0), yhi = min(ny, L.w.row0 + L.w.rows);
-  const int clo = max(0, cw.row0), chi = min(cny, cw.row0 + cw.rows);
-  const size_t N = size_t(nx) * L.w.rows;
-  const float2* fb = f + b * N - size_t(L.w.row0) * nx;  // indexed by global row
-  const float2* cb = vc + size_t(b) * cnx * cw.rows - ptrdiff_t(cw.row0) * cnx;
+  const int row0 = SLAB ? L.w.row0 : 0, rows = SLAB ? L.w.rows : ny;
+  const int wlo = SLAB ? L.w.lo : 0, whi = SLAB ? L.w.hi : ny;
+  const int y0 = wlo + (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
+  if (y0 >= whi) return;
+  const int y1 = min(whi, y0 + rows_per_chunk);
+  const int ylo = SLAB ? max(0, row0) : 0, yhi = SLAB ? min(ny, row0 + rows) : ny;
+  const int crow0 = SLAB ? cw.row0 : 0, crows = SLAB ? cw.rows : cny;
+  const int clo = SLAB ? max(0, crow0) : 0, chi = SLAB ? min(cny, crow0 + crows) : cny;
+  const size_t N = size_t(nx) * rows;
+  const float2* fb = f + b * N - size_t(row0) * nx;  // indexed by global row
+  const float2* cb = vc + size_t(b) * cnx * crows - ptrdiff_t(crow0) * cnx;
   const float s = fscale ? fscale[b] : 1.0f;
   const float ih2 = L.inv_h2;
   const bool colok_a = c0 >= 0 && c0 < nx, colok_b = c0 + 1 >= 0 && c0 + 1 < nx;
@@ -191,7 +194,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
       r.c0v = r.c1v = make_float2(0.f, 0.f);
       return r;
     }
-    const ptrdiff_t o = ptrdiff_t(y) * nx, oc = ptrdiff_t(y - L.w.row0) * nx;
+    const ptrdiff_t o = ptrdiff_t(y) * nx, oc = ptrdiff_t(y - row0) * nx;
     r.f = ld_pair(fb + o, c0, nx);
     r.d = ld_pair(L.dM + oc, c0, nx);
     if (WD) {
@@ -223,7 +226,7 @@ __global__ void __launch_bounds__(32 * WARPS) k_up_stream(LevelView L, float dam
   };
   Raw r_c = load_raw(y0), r_p1 = load_raw(y0 + 1), r_p2 = load_raw(y0 + 2);
   Pair v_m = vrow(load_raw(y0 - 1)), v_c = vrow(r_c);
-  float2* zb = z + b * N - size_t(L.w.row0) * nx;
+  float2* zb = z + b * N - size_t(row0) * nx;
   for (int y = y0; y < y1; ++y) {
     const Raw r_p3 = load_raw(y + 3);
     const Pair v_p = vrow(r_p1);
@@ -507,10 +510,16 @@ void launch_up_stream(Context& c, const LevelView& L, float damping, int offset,
   if (env_u) rpc = env_u;
   const int chunks = (nrows + rpc - 1) / rpc;
   const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
-  if (c.opt_legs_wd)
-    launch_pdl(c, k_up_stream<true>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, vc, z);
+  const bool slab = L.w.rows != L.ny || L.w.lo != 0 || L.w.hi != L.ny || cw.rows != cny || cw.row0 != 0;
+  if (slab)
+    launch_pdl(c, k_up_stream<false, true>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act, f,
+               fscale, vc, z);
+  else if (c.opt_legs_wd)
+    launch_pdl(c, k_up_stream<true, false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act,
+               f, fscale, vc, z);
   else
-    launch_pdl(c, k_up_stream<false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, vc, z);
+    launch_pdl(c, k_up_stream<false, false>, dim3(grid), dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act,
+               f, fscale, vc, z);
   prof_end(c, PC_UP, tok, double(B) * L.nx * nrows * 18.0 + double(L.nx) * nrows * 16.0, 0);
   HB_CUDA(cudaGetLastError());
 }

@@ -177,6 +177,13 @@ int hb_save_checkpoint(hb_ctx* ctx, const char* path, const char* digest);
  * in NCHW [batch][4][H][W] -> out NCHW [batch][2][H][W] (host fp32) */
 int hb_paper_forward(hb_ctx* ctx, int batch, int H, int W, const float* in, float* out);
 
+/* ---- SLW1 raw fields (write_slw1 / read_slw1, inc/field_io.hpp:46-76) ------
+ * "SLW1", u32 nx, u32 ny (LE), nx*ny f32 LE row-major; host only.  read with
+ * values == NULL reports the dims.  Errors: HB_ERR_ARG (cannot open),
+ * HB_ERR_NUMERIC (bad magic / dims / truncated). */
+int hb_write_slw1(const char* path, int nx, int ny, const double* values);
+int hb_read_slw1(const char* path, int* nx, int* ny, double* values);
+
 /* ---- training pairs ----------------------------------
  * gen_sample_pair (inc/datagen.hpp:191-219) for `count` seeds: x ~ CN(0, I)
  * from Rng(seed), b = A x, k = k_forced (>= 0) or uniform_int(1, k_max),

@@ -369,6 +369,8 @@ def ref():
         R.hr_paper_pc_apply.argtypes = [_vp, C.c_int, _dp, _dp]
         R.hr_paper_fgmres.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, C.c_int, _ip, _ip]
         R.hr_gen_sample_pair.argtypes = [_vp, C.c_uint64, C.c_int, C.c_int, _dp, _dp]
+        R.hr_write_slw1.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
+        R.hr_read_slw1.argtypes = [C.c_char_p, _ip, _ip, _dp]
         R.hr_init()
         _ref = R
     return _ref

@@ -701,3 +701,20 @@ HR_EXPORT int hr_gen_sample_pair(void* mg, uint64_t seed, int k_forced, int k_ma
     from_field(s.e, e);
   })
 }
+
+// ---------------- SLW1 fields (inc/field_io.hpp:46-76)
+HR_EXPORT int hr_write_slw1(const char* path, int nx, int ny, const double* v) {
+  HR_TRY({
+    RealField f(nx, ny);
+    std::memcpy(f.v.data(), v, sizeof(double) * f.v.size());
+    write_slw1(std::string(path), f);
+  })
+}
+HR_EXPORT int hr_read_slw1(const char* path, int* nx, int* ny, double* v) {
+  HR_TRY({
+    const RealField f = read_slw1(std::string(path));
+    *nx = f.nx;
+    *ny = f.ny;
+    if (v) std::memcpy(v, f.v.data(), sizeof(double) * f.v.size());
+  })
+}

@@ -116,3 +116,69 @@ void gaussian_blur(const double* src, int nx, int ny, double sigma, double* out)
 }
 
 }  // namespace hb
+
+// ---- SLW1 raw fields (inc/field_io.hpp:12-76): "SLW1", u32 nx, u32 ny (LE),
+// nx*ny f32 LE row-major.  Host-only; the slowness-model exchange format of
+// the reference's dataset tooling.
+#include <cstring>
+#include <fstream>
+
+#include "../../include/helmgpu.h"
+
+namespace {
+void put_u32(std::ostream& os, uint32_t v) {
+  const unsigned char b[4] = {uint8_t(v), uint8_t(v >> 8), uint8_t(v >> 16), uint8_t(v >> 24)};
+  os.write(reinterpret_cast<const char*>(b), 4);
+}
+bool get_u32(std::istream& is, uint32_t& v) {
+  unsigned char b[4];
+  is.read(reinterpret_cast<char*>(b), 4);
+  v = uint32_t(b[0]) | uint32_t(b[1]) << 8 | uint32_t(b[2]) << 16 | uint32_t(b[3]) << 24;
+  return bool(is);
+}
+}  // namespace
+
+extern "C" {
+
+int hb_write_slw1(const char* path, int nx, int ny, const double* values) {
+  if (!path || nx <= 0 || ny <= 0 || !values) return HB_ERR_ARG;
+  std::ofstream os(path, std::ios::binary);
+  if (!os) return HB_ERR_ARG;
+  os.write("SLW1", 4);
+  put_u32(os, uint32_t(nx));
+  put_u32(os, uint32_t(ny));
+  for (size_t i = 0; i < size_t(nx) * ny; ++i) {
+    const float f = float(values[i]);
+    uint32_t bits;
+    std::memcpy(&bits, &f, 4);
+    put_u32(os, bits);
+  }
+  return os ? HB_OK : HB_ERR_ARG;
+}
+
+// values == NULL: only report the dims
+int hb_read_slw1(const char* path, int* nx, int* ny, double* values) {
+  if (!path) return HB_ERR_ARG;
+  std::ifstream is(path, std::ios::binary);
+  if (!is) return HB_ERR_ARG;
+  char magic[4];
+  is.read(magic, 4);
+  if (!is || std::memcmp(magic, "SLW1", 4) != 0) return HB_ERR_NUMERIC;  // "bad SLW1 magic"
+  uint32_t w = 0, h = 0;
+  if (!get_u32(is, w) || !get_u32(is, h)) return HB_ERR_NUMERIC;
+  if (w == 0 || h == 0 || size_t(w) * h > (size_t(1) << 28) || w > (1u << 30) || h > (1u << 30))
+    return HB_ERR_NUMERIC;  // "bad SLW1 dims"
+  if (nx) *nx = int(w);
+  if (ny) *ny = int(h);
+  if (!values) return HB_OK;
+  for (size_t i = 0; i < size_t(w) * h; ++i) {
+    uint32_t bits;
+    if (!get_u32(is, bits)) return HB_ERR_NUMERIC;  // "unexpected end of file"
+    float f;
+    std::memcpy(&f, &bits, 4);
+    values[i] = double(f);
+  }
+  return HB_OK;
+}
+
+}  // extern "C"

@@ -105,6 +105,8 @@ def lib():
         L.hb_save_checkpoint.argtypes = [_vp, C.c_char_p, C.c_char_p]
         L.hb_paper_forward.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp]
         L.hb_gen_sample_pairs.argtypes = [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.c_int, _dp, _dp, _ip]
+        L.hb_write_slw1.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
+        L.hb_read_slw1.argtypes = [C.c_char_p, _ip, _ip, _dp]
         L.hb_slab_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]
         L.hb_nccl_unique_id.argtypes = [C.c_char_p]
         L.hb_slab_init_nccl.argtypes = [_vp, C.c_int, C.c_int, C.c_char_p]
@@ -186,7 +188,7 @@ class SolveReport:  # inc/krylov.hpp:20-35
         for c, h in enumerate(self.residual_history):
             r0 = h[0] if len(h) and h[0] > 0 else 1.0
             for i, v in enumerate(h):
-                os_.write(f"{i},{c},{v / r0:.17g}\n")
+                os_.write(f"{i},{c},{v / r0:g}\n")  # operator<< default: 6 significant digits
 
 
 # ------------------------------------------------------------------ context
@@ -500,6 +502,27 @@ class Context:
 
     def launch_count(self) -> int:
         return int(lib().hb_launch_count(self.h))
+
+
+# ------------------------------------------------------------ SLW1 fields
+def write_slw1(path, field):
+    """write_slw1 (inc/field_io.hpp:46-57): real field [ny][nx] -> f32 file."""
+    f = np.ascontiguousarray(field, np.float64)
+    if lib().hb_write_slw1(os.fspath(path).encode(), f.shape[1], f.shape[0], _p(f)) != 0:
+        raise RuntimeError(f"cannot write {path}")
+
+
+def read_slw1(path):
+    """read_slw1 (inc/field_io.hpp:59-76) -> float64 [ny][nx]."""
+    nx, ny = C.c_int(), C.c_int()
+    p = os.fspath(path).encode()
+    rc = lib().hb_read_slw1(p, C.byref(nx), C.byref(ny), None)
+    if rc != 0:
+        raise RuntimeError("bad SLW1 file" if rc == -4 else f"cannot open {path}")
+    out = np.zeros((ny.value, nx.value))
+    if lib().hb_read_slw1(p, None, None, _p(out)) != 0:
+        raise RuntimeError("truncated SLW1 file")
+    return out
 
 
 # ------------------------------------------------------------- row slabs

@@ -454,6 +454,12 @@ def run_ours(args, ws, rank, local):
             if nm == "c4slab":
                 line["also"][nm] = slab
                 continue
+            if nm in ("datagen", "paper_ju"):
+                try:
+                    line["also"][nm] = (datagen_budget if nm == "datagen" else paper_ju_budget)(local, args)
+                except Exception as e:  # reported, not hidden
+                    line["also"][nm] = {"error": repr(e)}
+                continue
             try:
                 line["also"][nm] = fixed_budget(nm, local, args, ws, rank)
             except Exception as e:  # reported, not hidden
@@ -532,6 +538,83 @@ def fixed_budget(name, local, args, ws, rank):
     return out
 
 
+def datagen_budget(local, args):
+    """Training pairs (gen_sample_pair, inc/datagen.hpp:191-219)
+    on the c0 problem through the public C ABI (host draws, per-k batched
+    FGMRES(M_V) on the device, r / e back in host memory): pairs/s, against
+    the reference's own gen_sample_pair on one host thread."""
+    import time
+    import torch
+    from paper_2203_11025_b200 import problems
+    cfg = config_for("c0")
+    ctx, arr = problems.gpu_setup(cfg, device=local)
+    count = 2 * torch.cuda.get_device_properties(local).multi_processor_count
+    seeds = np.arange(1000, 1000 + count, dtype=np.uint64)
+    ctx.gen_sample_pairs(seeds[:16])  # warm-up: graphs / buffers
+    dev = torch.device("cuda", local)
+    st = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    r, e, k = ctx.gen_sample_pairs(seeds)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out = {"grid": cfg["n"], "pairs": int(count), "k_mean": float(k.mean()), "ms": ms,
+           "pairs_per_s": count / (ms / 1e3), "path": "hb_gen_sample_pairs (host draws + device FGMRES, host r/e)"}
+    ctx.close()
+    try:  # the reference's gen_sample_pair, one host thread, bounded sample
+        from oracle import oracle as O
+        if O.have_ref():
+            H = O.RefHierarchy(arr["kappa2"], arr["gamma"], arr["omega"], arr["lo"], arr["hi"], levels=cfg["levels"])
+            t0, n = time.perf_counter(), 0
+            while time.perf_counter() - t0 < 3.0:
+                O.ref_gen_sample_pair(H, 1000 + n, -1, 10)
+                n += 1
+            dt = time.perf_counter() - t0
+            out["cpu_reference"] = {"pairs_per_s": n / dt, "pairs": n, "cores": 1, "kind": "reference"}
+    except Exception as ex:  # reported, not hidden
+        out["cpu_reference"] = {"error": repr(ex)}
+    return out
+
+
+def paper_ju_budget(local, args):
+    """M_JU with the paper's U-Net (inc/precond.hpp:104-139, UNetConfig defaults
+    inc/unet.hpp:113-120: 3 levels, base 16, 1 ResNet per level, 3 bottleneck
+    ResNets, 5x5 up/down) on the c0 problem, NetworkWeights default init with
+    the batch-norm buffers marked initialised (mark_bn_initialized): applies/s
+    for a batch of 16 and the conv rate."""
+    import torch
+    from paper_2203_11025_b200 import helmgpu as hg
+    from paper_2203_11025_b200 import problems
+    cfg = config_for("c0")
+    ctx, arr = problems.gpu_setup(cfg, device=local)
+    ctx.set_paper_net(hg.UNetConfig(), "standalone")
+    for name, dims in ctx.paper_params():
+        if name.endswith(".count"):
+            ctx.paper_param(name, np.ones(dims, np.float32))
+    B = 16
+    n = cfg["n"]
+    r = np.random.default_rng(0).standard_normal((B, n, n)) + 1j * np.random.default_rng(1).standard_normal((B, n, n))
+    ctx.precond_apply("ju", r)
+    ctx.prof_reset()
+    ctx.prof_enable(True)
+    reps = 5
+    for _ in range(reps):
+        ctx.precond_apply("ju", r)
+    ctx.prof_enable(False)
+    prof = ctx.prof()
+    dev_ms = sum(v["ms"] for v in prof.values()) / reps
+    conv = prof.get("conv3x3", {})
+    out = {"grid": n, "batch": B, "net": "UNetConfig() standalone (3 levels, base 16)", "us_per_apply_batch": 1e3 * dev_ms,
+           "applies_per_s": B / (dev_ms / 1e3) if dev_ms > 0 else None,
+           "conv_share": conv.get("ms", 0) / max(1e-9, dev_ms * reps),
+           "conv_tflops": conv["flops"] / (conv["ms"] / 1e3) / 1e12 if conv.get("ms") else None,
+           "note": "device time of the M_JU apply (CUDA events per kernel class); host c128 staging excluded"}
+    ctx.close()
+    return out
+
+
 def slab_budget(local, args, ws, rank):
     """c4 (one 4096^2 RHS, 4-level V-cycle, U-Net coarsest at 512^2) on row slabs
     (SURVEY 8(e)): one slab per rank over NCCL when ws > 1, else an in-process
@@ -591,7 +674,7 @@ def main():
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = one per SM)")
-    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab", help="comma list of configs measured on a fixed iteration budget "
+    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,datagen,paper_ju", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")

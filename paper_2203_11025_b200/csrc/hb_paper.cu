@@ -341,6 +341,162 @@ __global__ void __launch_bounds__(128) k_pconv(PConv a) {
   }
 }
 
+// Register-tiled variant: a CTA owns 128*P output pixels x 16 output channels;
+// each thread P pixels (128 apart: coalesced stores) x 16 channels = 16P
+// accumulators.  Weights of a 16-input-channel chunk (all taps, 16 outputs,
+// zero-padded) are staged in shared memory and read as warp-uniform float4
+// broadcasts; inputs come from global (L1) as float4 over 4 channels.  Per
+// input channel and tap: 4 LDS.128 + P/4 LDG.128 for 16P FMAs.
+constexpr int PC_T = 128, PC_CO = 16, PC_CI = 16;
+// Stride-2 transposed convolutions run per output parity class (blockIdx.z):
+// class (py, px) only meets taps ky = py + pad (mod 2), kx = px + pad (mod 2),
+// so no work is spent on the 3/4 of the taps that miss.
+template <int P, bool VEC>  // VEC: cin % 4 == 0 and ldx % 4 == 0 (float4 input loads)
+__global__ void __launch_bounds__(PC_T) k_pconv_tiled(PConv a) {
+  extern __shared__ float4 sw4[];  // [tap][ci_local][PC_CO] as float4 x 4
+  float* sw = reinterpret_cast<float*>(sw4);
+  const int t = threadIdx.x;
+  const int co0 = blockIdx.y * PC_CO;
+  const int nco = min(PC_CO, a.cout - co0);
+  const bool par = a.transpose && a.stride == 2;
+  const int cls = blockIdx.z, py = cls >> 1, px = cls & 1;
+  const int Hc = par ? (a.Ho - py + 1) / 2 : a.Ho, Wc = par ? (a.Wo - px + 1) / 2 : a.Wo;  // class grid
+  const long long npix = (long long)a.B * Hc * Wc;
+  const int pad = (a.k - 1) / 2, kk = a.k * a.k;
+  const int ky0 = par ? ((py + pad) & 1) : 0, kx0 = par ? ((px + pad) & 1) : 0, kst = par ? 2 : 1;
+  int pb[P], poy[P], pox[P];
+  long long pout[P];
+  bool pv[P];
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    const long long p = (long long)blockIdx.x * (PC_T * P) + q * PC_T + t;
+    pv[q] = p < npix;
+    const long long pp = pv[q] ? p : 0;
+    pb[q] = int(pp / ((long long)Hc * Wc));
+    const int rem = int(pp - (long long)pb[q] * Hc * Wc);
+    poy[q] = rem / Wc;
+    pox[q] = rem - poy[q] * Wc;
+    if (par) {
+      poy[q] = 2 * poy[q] + py;
+      pox[q] = 2 * pox[q] + px;
+    }
+    pout[q] = ((long long)pb[q] * a.Ho + poy[q]) * a.Wo + pox[q];
+    if (!a.xbatch) pb[q] = 0;
+  }
+  float acc[P][PC_CO];
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+#pragma unroll
+    for (int j = 0; j < PC_CO; ++j) acc[q][j] = 0.f;
+  for (int ci0 = 0; ci0 < a.cin; ci0 += PC_CI) {
+    const int nci = min(PC_CI, a.cin - ci0);
+    __syncthreads();
+    for (int i = t; i < kk * PC_CI * PC_CO; i += PC_T) {
+      const int j = i % PC_CO, cl = (i / PC_CO) % PC_CI, tap = i / (PC_CO * PC_CI);
+      sw[i] = (j < nco && cl < nci) ? __ldg(a.w + (size_t(tap) * a.cin + ci0 + cl) * a.cout + co0 + j) : 0.f;
+    }
+    __syncthreads();
+    for (int ky = ky0; ky < a.k; ky += kst)
+      for (int kx = kx0; kx < a.k; kx += kst) {
+        const float* xp[P];
+        bool ok[P];
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          int iy, ix;
+          if (!a.transpose) {
+            iy = poy[q] * a.stride + ky - pad;
+            ix = pox[q] * a.stride + kx - pad;
+            ok[q] = pv[q];
+          } else {
+            iy = poy[q] + pad - ky;
+            ix = pox[q] + pad - kx;
+            ok[q] = pv[q];
+            if (a.stride == 2) {
+              ok[q] = ok[q] && !((iy | ix) & 1);
+              iy >>= 1;
+              ix >>= 1;
+            }
+          }
+          ok[q] = ok[q] && iy >= 0 && iy < a.Hin && ix >= 0 && ix < a.Win;
+          xp[q] = a.x + ((size_t(pb[q]) * a.Hin + (ok[q] ? iy : 0)) * a.Win + (ok[q] ? ix : 0)) * a.ldx + ci0;
+        }
+        const float4* wt = sw4 + (size_t(ky * a.k + kx) * PC_CI) * (PC_CO / 4);
+        if (VEC) {
+          for (int c4 = 0; c4 < nci; c4 += 4) {
+            float4 xv[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+              xv[q] = ok[q] ? __ldg(reinterpret_cast<const float4*>(xp[q] + c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
+              if (a.in_elu) {
+                xv[q].x = elu(xv[q].x);
+                xv[q].y = elu(xv[q].y);
+                xv[q].z = elu(xv[q].z);
+                xv[q].w = elu(xv[q].w);
+              }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float4* wr = wt + (c4 + u) * (PC_CO / 4);
+              float w[PC_CO];
+#pragma unroll
+              for (int j4 = 0; j4 < PC_CO / 4; ++j4) {
+                const float4 v = wr[j4];
+                w[4 * j4] = v.x;
+                w[4 * j4 + 1] = v.y;
+                w[4 * j4 + 2] = v.z;
+                w[4 * j4 + 3] = v.w;
+              }
+#pragma unroll
+              for (int q = 0; q < P; ++q) {
+                const float xs = u == 0 ? xv[q].x : u == 1 ? xv[q].y : u == 2 ? xv[q].z : xv[q].w;
+#pragma unroll
+                for (int j = 0; j < PC_CO; ++j) acc[q][j] = fmaf(xs, w[j], acc[q][j]);
+              }
+            }
+          }
+        } else {
+          for (int cl = 0; cl < nci; ++cl) {
+            const float4* wr = wt + cl * (PC_CO / 4);
+            float w[PC_CO];
+#pragma unroll
+            for (int j4 = 0; j4 < PC_CO / 4; ++j4) {
+              const float4 v = wr[j4];
+              w[4 * j4] = v.x;
+              w[4 * j4 + 1] = v.y;
+              w[4 * j4 + 2] = v.z;
+              w[4 * j4 + 3] = v.w;
+            }
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+              float xs = ok[q] ? __ldg(xp[q] + cl) : 0.f;
+              if (a.in_elu) xs = elu(xs);
+#pragma unroll
+              for (int j = 0; j < PC_CO; ++j) acc[q][j] = fmaf(xs, w[j], acc[q][j]);
+            }
+          }
+        }
+      }
+  }
+  // epilogue: bias, residual, batch norm (eval), ELU
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    if (!pv[q]) continue;
+    const long long p = pout[q];
+    float* yp = a.y + size_t(p) * a.ldy + co0;
+    const float* rp = a.res ? a.res + size_t(p) * a.ldres + co0 : nullptr;
+#pragma unroll
+    for (int j = 0; j < PC_CO; ++j) {
+      if (j >= nco) break;
+      const int co = co0 + j;
+      float v = acc[q][j] + a.bias[co];
+      if (rp) v = rp[j] + v;
+      if (a.mu) v = ((v - a.mu[co]) * a.is[co]) * a.g[co] + a.be[co];
+      if (a.act) v = elu(v);
+      yp[j] = v;
+    }
+  }
+}
+
 // dst[pix][off + c] = src[pix (mod plane if bcast)][c]
 __global__ void k_copy_ch(long long npix, int plane, int bcast, int C, const float* __restrict__ src, int lds,
                           float* __restrict__ dst, int ldd) {
@@ -421,9 +577,35 @@ struct Exec {
     a.xbatch = xbatch;
     const long long npix = (long long)a.B * a.Ho * a.Wo;
     const int tok = prof_begin(c, PC_CONV);
-    k_pconv<16><<<unsigned((npix + 127) / 128), 128, 0, c.stream>>>(a);
+    {
+      const bool par = a.transpose && a.stride == 2;
+      const long long cpix = par ? (npix + 3) / 4 : npix;  // pixels per parity class
+      const int coblk = (a.cout + PC_CO - 1) / PC_CO;
+      // 4 pixels per thread when that still gives >= 2 CTAs per SM, else 1
+      const bool big = (cpix + PC_T * 4 - 1) / (PC_T * 4) * coblk * (par ? 4 : 1) >= 2 * c.num_sms;
+      const int P = big ? 4 : 1;
+      const dim3 grid(unsigned((cpix + PC_T * P - 1) / (PC_T * P)), unsigned(coblk), par ? 4u : 1u);
+      const size_t smem = size_t(D.k) * D.k * PC_CI * PC_CO * sizeof(float);
+      const bool vec = a.cin % 4 == 0 && a.ldx % 4 == 0;
+      static bool attr = false;
+      if (!attr) {
+        const int mx = 100 * 1024;
+        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        attr = true;
+      }
+      if (smem > 100 * 1024)
+        k_pconv<16><<<unsigned((npix + 127) / 128), 128, 0, c.stream>>>(a);
+      else if (P == 4)
+        (vec ? k_pconv_tiled<4, true> : k_pconv_tiled<4, false>)<<<grid, PC_T, smem, c.stream>>>(a);
+      else
+        (vec ? k_pconv_tiled<1, true> : k_pconv_tiled<1, false>)<<<grid, PC_T, smem, c.stream>>>(a);
+    }
     HB_CUDA(cudaGetLastError());
     const double taps = D.transpose && stride == 2 ? double(D.k) * D.k / 4.0 : double(D.k) * D.k;
+    if (c.prof_detail) c.prof_label = kname;
     prof_end(c, PC_CONV, tok, 0, 2.0 * npix * taps * D.cin * D.cout);
   }
   void copy(const TView& src, const TView& dst, bool bcast) {

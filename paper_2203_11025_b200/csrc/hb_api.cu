@@ -388,7 +388,8 @@ void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2
 
 // ------------------------------------------------------------- FGMRES --
 static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, const double2* dB, double2* dX,
-                       double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv, uint8_t* brk) {
+                       double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv, uint8_t* brk,
+                       const int* d_limits = nullptr) {
   require_hier(c);
   if (!cfg) throw HbError{HB_ERR_ARG, "null krylov config"};
   if (cfg->restart < 1) throw HbError{HB_ERR_ARG, "restart must be >= 1"};
@@ -398,7 +399,7 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
   ensure_batch(c, B);
   const int m = cfg->restart;
   const int cap = std::max(1, cfg->max_iters + 2);
-  krylov_alloc(c, B, m, cap);
+  krylov_alloc(c, B, m, cap, d_limits);
   const size_t N = c.levels[0]->N();
   const size_t BN = size_t(B) * N;
   if (!c.h_count) HB_CUDA(cudaMallocHost(&c.h_count, sizeof(int)));
@@ -483,8 +484,9 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
   if (hist || hist_len || iters || conv || brk) krylov_report(c, B, hist, hist_stride, hist_len, iters, conv, brk);
 }
 
-void fgmres_dev_entry(Context& c, const hb_krylov_cfg* cfg, int kind, int B, const double2* dB, double2* dX) {
-  fgmres_dev(c, cfg, kind, B, dB, dX, nullptr, 0, nullptr, nullptr, nullptr, nullptr);
+void fgmres_dev_entry(Context& c, const hb_krylov_cfg* cfg, int kind, int B, const double2* dB, double2* dX,
+                      const int* d_limits) {
+  fgmres_dev(c, cfg, kind, B, dB, dX, nullptr, 0, nullptr, nullptr, nullptr, nullptr, d_limits);
 }
 
 }  // namespace hb

@@ -182,7 +182,8 @@ void launch_residual(Context& c, const LevelView& L, int B, const int* act, cons
 
 // ---- Krylov (hb_krylov.cu)
 struct ColState;
-void krylov_alloc(Context& c, int B, int m, int hist_cap);
+// limits: optional DEVICE array of per-column iteration limits (0 = max_iters)
+void krylov_alloc(Context& c, int B, int m, int hist_cap, const int* limits = nullptr);
 // gsum != nullptr: row-slab split mode (fold the slab's partial sums into
 // gsum[B][kMaxDots] and stop; the *_finish launchers run the scalar part on the
 // slab-summed gsum)
@@ -251,6 +252,7 @@ struct Context {
   DBuf<double2> kpart;       // per-CTA partials
   DBuf<double> khist;        // [B][hist_cap]
   DBuf<int> kact;            // per-column: active in the current inner step
+  DBuf<int> klimit;          // per-column iteration limits (training-pair generation)
   DBuf<float> kscale;        // per-column: scale of the current V_j
   DBuf<unsigned> kticket;    // per-column last-CTA counters
   DBuf<int> kcount;          // number of unfrozen columns (host-visible after restart)

@@ -25,6 +25,7 @@ struct ColState {
   double beta0;
   int iters, k, hist_len;
   int frozen, converged, breakdown, active;
+  int max_it;  // per-column iteration limit (0: the solve's max_iters)
   double cs[kMaxRestart];
   double2 sn[kMaxRestart];
   double2 g[kMaxRestart + 1];
@@ -187,7 +188,7 @@ __device__ void restart_scalar(ColState& S, int b, double t, double* hist, int h
     if (beta / S.beta0 <= rel_tol) {
       S.frozen = 1;
       S.converged = 1;
-    } else if (S.iters >= max_iters) {
+    } else if (S.iters >= (S.max_it > 0 ? S.max_it : max_iters)) {
       S.frozen = 1;
     } else {
       for (int i = 0; i <= kMaxRestart; ++i) S.g[i] = make_double2(0.0, 0.0);
@@ -540,7 +541,7 @@ __device__ void update_scalar(ColState& S, int b, int j, int m, double t, int* a
       S.converged = 1;
       S.frozen = 1;
       active = 0;
-    } else if (iters >= max_iters) {
+    } else if (iters >= (S.max_it > 0 ? S.max_it : max_iters)) {
       S.frozen = 1;
       active = 0;
     } else if (j + 1 < m) {
@@ -601,13 +602,14 @@ __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st
   }
 }
 
-__global__ void k_init_state(ColState* st, int B) {
+__global__ void k_init_state(ColState* st, int B, const int* limits) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
   ColState& S = st[b];
   S.beta0 = 0.0;
   S.iters = S.k = S.hist_len = 0;
   S.frozen = S.converged = S.breakdown = S.active = 0;
+  S.max_it = limits ? limits[b] : 0;
 }
 
 FineView fine_view(Context& c) {
@@ -639,7 +641,7 @@ struct KScope {
   ~KScope() { prof_end(c, cls, tok, bytes, 0); }
 };
 
-void krylov_alloc(Context& c, int B, int m, int hist_cap) {
+void krylov_alloc(Context& c, int B, int m, int hist_cap, const int* limits) {
   if (m < 1 || m > kMaxRestart) throw HbError{HB_ERR_ARG, "restart must be in [1, 32]"};
   const size_t N = c.levels[0]->N();
   c.kstate.ensure(size_t(B) * sizeof(ColState));
@@ -657,7 +659,7 @@ void krylov_alloc(Context& c, int B, int m, int hist_cap) {
     HB_CUDA(cudaMemsetAsync(c.kticket.p, 0, sizeof(unsigned) * B, c.stream));
   }
   HB_CUDA(cudaMemsetAsync(c.kticket.p, 0, sizeof(unsigned) * B, c.stream));
-  k_init_state<<<(B + 127) / 128, 128, 0, c.stream>>>(reinterpret_cast<ColState*>(c.kstate.p), B);
+  k_init_state<<<(B + 127) / 128, 128, 0, c.stream>>>(reinterpret_cast<ColState*>(c.kstate.p), B, limits);
   HB_CUDA(cudaGetLastError());
   c.k_B = B;
   c.k_m = m;
@@ -787,7 +789,7 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
   const int g1 = int(std::min<size_t>((BN + 255) / 256, size_t(c.num_sms) * 8));
   const int tok = prof_begin(c, PC_COARSE);
   c.launches += 4 + 3 * m;  // prof_begin counted one of the 5 + 3m kernels below
-  k_init_state<<<(B + 127) / 128, 128, 0, c.stream>>>(st, B);
+  k_init_state<<<(B + 127) / 128, 128, 0, c.stream>>>(st, B, nullptr);
   k_c64_to_c128<<<g1, 256, 0, c.stream>>>(BN, f, K.b.p);
   HB_CUDA(cudaMemsetAsync(K.x.p, 0, sizeof(double2) * BN, c.stream));
   HB_CUDA(cudaMemsetAsync(K.count.p, 0, sizeof(int), c.stream));

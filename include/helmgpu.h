@@ -168,8 +168,9 @@ int hb_paper_init(hb_ctx* ctx, uint64_t seed);
 int hb_paper_param_count(hb_ctx* ctx);
 /* name (NUL-terminated, cap bytes) and dims (n, c, h, w) of parameter i */
 int hb_paper_param_info(hb_ctx* ctx, int i, char* name, int cap, int* dims);
-/* in != NULL: set the parameter's values; out != NULL: read them */
-int hb_paper_param(hb_ctx* ctx, const char* name, const float* in, float* out);
+/* in != NULL: set the parameter's values; out != NULL: read them; count =
+ * the caller's element count, which must equal the parameter's (n*c*h*w) */
+int hb_paper_param(hb_ctx* ctx, const char* name, int64_t count, const float* in, float* out);
 /* UNW1 checkpoints (load_checkpoint / save_checkpoint, inc/checkpoint.hpp:51-104) */
 int hb_load_checkpoint(hb_ctx* ctx, const char* path);
 int hb_save_checkpoint(hb_ctx* ctx, const char* path, const char* digest);

@@ -6,6 +6,11 @@
 //   helm::gpu::GpuSLVCycle             : helm::Preconditioner   (M_V, inc/precond.hpp:35-53;
 //                                        with a net coarse solver: the SURVEY A4 coarse-net cycle)
 //   helm::gpu::GpuUnetVCycle           : helm::Preconditioner   (M_VU, inc/precond.hpp:143-165)
+//   helm::gpu::GpuJacobiUnet           : helm::Preconditioner   (M_JU, inc/precond.hpp:104-139)
+//   helm::gpu::make_jacobi_unet / make_unet_vcycle
+//                                      the reference constructors (problem / hierarchy, shared
+//                                      NetworkWeights, UNetConfig, NetVariant) on the device with the
+//                                      paper U-Net (inc/unet.hpp:113-257)
 //   helm::gpu::block_fgmres(M, B, cfg) device-resident block_fgmres (inc/krylov.hpp:83-86)
 //
 // Error convention of the reference: contract violations throw
@@ -58,6 +63,25 @@ class Context {
   void set_net(int slot, const hb_net_cfg& cfg, uint64_t he_seed) {
     check(c_, hb_set_net(c_, slot, &cfg));
     check(c_, hb_init_net_he(c_, slot, he_seed));
+  }
+  // the paper's U-Net (inc/unet.hpp:113-257) with the reference's own weights
+  // registry: every parameter copied by name (dims checked); M_JU / M_VU then use it
+  void set_paper_net(const UNetConfig& cfg, NetVariant variant, const NetworkWeights& w) {
+    const hb_unet_cfg c{cfg.levels, cfg.base_channels, cfg.resnet_per_level, cfg.bottleneck_resnets,
+                        cfg.updown_kernel, cfg.res_kernel};
+    check(c_, hb_set_paper_net(c_, &c, variant == NetVariant::encoder_solver ? 1 : 0));
+    for (std::size_t i = 0; i < w.size(); ++i) {
+      const Param& p = w.at(i);
+      if (p.name.rfind("adam.", 0) == 0) continue;
+      check(c_, hb_paper_param(c_, p.name.c_str(), int64_t(p.value.v.size()), p.value.v.data(), nullptr));
+    }
+  }
+  // UNW1 checkpoint written by save_checkpoint (inc/checkpoint.hpp:57-104)
+  void load_checkpoint(const UNetConfig& cfg, NetVariant variant, const std::string& path) {
+    const hb_unet_cfg c{cfg.levels, cfg.base_channels, cfg.resnet_per_level, cfg.bottleneck_resnets,
+                        cfg.updown_kernel, cfg.res_kernel};
+    check(c_, hb_set_paper_net(c_, &c, variant == NetVariant::encoder_solver ? 1 : 0));
+    check(c_, hb_load_checkpoint(c_, path.c_str()));
   }
   int nx() const { return nx_; }
   int ny() const { return ny_; }
@@ -131,6 +155,27 @@ class GpuJacobiUnet : public GpuPreconditioner {
  public:
   explicit GpuJacobiUnet(std::shared_ptr<Context> ctx) : GpuPreconditioner(std::move(ctx), HB_PC_JU) {}
 };
+
+// JacobiUnetPreconditioner(problem, weights, cfg, variant) (inc/precond.hpp:106-110)
+// and UnetVCyclePreconditioner(hier, weights, cfg, variant) (:145-149) on one
+// device: same arguments, the network is the paper U-Net with those weights.
+inline GpuJacobiUnet make_jacobi_unet(const HelmholtzProblem& problem, std::shared_ptr<NetworkWeights> weights,
+                                      UNetConfig cfg, NetVariant variant, int device = 0) {
+  auto ctx = std::make_shared<Context>(device);
+  VCycleConfig vc;
+  vc.levels = 2;  // M_JU runs on the fine grid only; the hierarchy is the minimal one
+  ctx->set_problem(problem, vc);
+  ctx->set_paper_net(cfg, variant, *weights);
+  return GpuJacobiUnet(std::move(ctx));
+}
+inline GpuUnetVCycle make_unet_vcycle(const HelmholtzProblem& problem, const VCycleConfig& vc,
+                                      std::shared_ptr<NetworkWeights> weights, UNetConfig cfg, NetVariant variant,
+                                      int device = 0) {
+  auto ctx = std::make_shared<Context>(device);
+  ctx->set_problem(problem, vc);
+  ctx->set_paper_net(cfg, variant, *weights);
+  return GpuUnetVCycle(std::move(ctx));
+}
 
 // Device-resident block FGMRES with A = A^h of the context's problem and M =
 // the plugin; same contract and SolveReport as inc/krylov.hpp:83-267.

@@ -853,11 +853,13 @@ int hb_paper_param_info(hb_ctx* ctx, int i, char* name, int cap, int* dims) {
   HB_API_END
 }
 
-int hb_paper_param(hb_ctx* ctx, const char* name, const float* in, float* out) {
+int hb_paper_param(hb_ctx* ctx, const char* name, int64_t count, const float* in, float* out) {
   HB_API_BEGIN
   if (!name) throw HbError{HB_ERR_ARG, "null name"};
   PaperState& P = state(*ctx);
   PParam& q = param(P, name);
+  if (count != int64_t(q.v.size()))
+    throw HbError{HB_ERR_ARG, "parameter " + std::string(name) + " dims changed"};
   if (out) std::memcpy(out, q.v.data(), q.v.size() * sizeof(float));
   if (in) {
     std::memcpy(q.v.data(), in, q.v.size() * sizeof(float));

@@ -100,7 +100,7 @@ def lib():
         L.hb_paper_init.argtypes = [_vp, C.c_uint64]
         L.hb_paper_param_count.argtypes = [_vp]
         L.hb_paper_param_info.argtypes = [_vp, C.c_int, C.c_char_p, C.c_int, _ip]
-        L.hb_paper_param.argtypes = [_vp, C.c_char_p, _fp, _fp]
+        L.hb_paper_param.argtypes = [_vp, C.c_char_p, C.c_int64, _fp, _fp]
         L.hb_load_checkpoint.argtypes = [_vp, C.c_char_p]
         L.hb_save_checkpoint.argtypes = [_vp, C.c_char_p, C.c_char_p]
         L.hb_paper_forward.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp]
@@ -304,7 +304,7 @@ class Context:
         dims = dict(self.paper_params())[name]
         out = np.zeros(dims, np.float32)
         inp = None if value is None else np.ascontiguousarray(value, np.float32).reshape(dims)
-        self._check(lib().hb_paper_param(self.h, name.encode(), _p(inp, _fp) if inp is not None else None,
+        self._check(lib().hb_paper_param(self.h, name.encode(), out.size, _p(inp, _fp) if inp is not None else None,
                                          _p(out, _fp)))
         return out
 

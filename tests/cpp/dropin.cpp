@@ -12,6 +12,7 @@
 #include "helmbench/multigrid.hpp"
 #include "helmbench/precond.hpp"
 #include "helmbench/rng.hpp"
+#include "helmbench/unet.hpp"
 #include "helmgpu_helm.hpp"
 
 using namespace helm;
@@ -84,7 +85,26 @@ int main() {
   }
   const double xe = rel(X_gpu, X_ref), xm = rel(X_mix, X_ref);
   ok = ok && xe < 1e-4 && xm < 1e-4 && M_gpu.name() == M_cpu.name();
-  std::printf("], \"x_rel_device\": %.3e, \"x_rel_plugin\": %.3e, \"name\": \"%s\", \"ok\": %s}\n", xe, xm,
-              M_gpu.name().c_str(), ok ? "true" : "false");
+
+  // (4) the paper U-Net preconditioners from the reference's own weights
+  // registry: the reference constructors vs the device drop-ins
+  UNetConfig ucfg;  // 3 levels, base 16, 1 ResNet per level, 3 bottleneck ResNets, 5x5 / 3x3
+  ucfg.bottleneck_resnets = 1;
+  auto w = std::make_shared<NetworkWeights>(1234);
+  {
+    Tensor4 x(1, 4, n, n, 0.1f);
+    unet_forward(*w, ucfg, x, true);  // creates the parameters (registry order), one running-stat update
+  }
+  mark_bn_initialized(*w);
+  JacobiUnetPreconditioner ju_cpu(prob, w, ucfg, NetVariant::standalone);
+  auto ju_gpu = gpu::make_jacobi_unet(prob, w, ucfg, NetVariant::standalone);
+  UnetVCyclePreconditioner vu_cpu(hier, w, ucfg, NetVariant::standalone);
+  auto vu_gpu = gpu::make_unet_vcycle(prob, vc, w, ucfg, NetVariant::standalone);
+  const double ju_err = rel(ju_gpu.apply(B), ju_cpu.apply(B)), vu_err = rel(vu_gpu.apply(B), vu_cpu.apply(B));
+  ok = ok && ju_err < 1e-4 && vu_err < 1e-4 && ju_gpu.name() == "ju" && vu_gpu.name() == "vu" &&
+       ju_gpu.requires_flexible() && vu_gpu.requires_flexible();
+  std::printf("], \"x_rel_device\": %.3e, \"x_rel_plugin\": %.3e, \"name\": \"%s\", \"ju_rel\": %.3e, "
+              "\"vu_rel\": %.3e, \"ok\": %s}\n",
+              xe, xm, M_gpu.name().c_str(), ju_err, vu_err, ok ? "true" : "false");
   return ok ? 0 : 1;
 }

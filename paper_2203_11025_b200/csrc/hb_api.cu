@@ -245,14 +245,14 @@ static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const fl
   if (c.opt_fused && nu1 == 1 && nu2 == 1) {
     // fused legs: v and r stay on chip (row-streaming kernels for a zero
     // initial guess, shared-memory tiles otherwise)
-    const bool stream = c.opt_stream && e0 == nullptr && L.nx >= 16;
+    const bool stream = c.opt_stream && (e0 == nullptr || c.opt_stream_e0) && L.nx >= 16;
     if (stream)
-      launch_down_stream(c, V, C.win(), w, offset, B, act, f, fscale, Cf);
+      launch_down_stream(c, V, C.win(), w, offset, B, act, f, fscale, e0, Cf);
     else
       launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
     vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
     if (stream)
-      launch_up_stream(c, V, w, offset, C.nx, C.ny, C.win(), B, act, f, fscale, Cx, out);
+      launch_up_stream(c, V, w, offset, C.nx, C.ny, C.win(), B, act, f, fscale, e0, Cx, out);
     else
       launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
     return;
@@ -539,6 +539,7 @@ int hb_create(int device, hb_ctx** out) {
   auto* c = new hb_ctx();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  c->l2_bytes = size_t(prop.l2CacheSize);
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
@@ -935,7 +936,7 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
   else if (k == "wide_legs")
     ctx->opt_wide_legs = value != 0;
   else if (k == "legs_wd")
-    ctx->opt_legs_wd = value != 0;
+    ctx->opt_legs_wd = int(value);
   else if (k == "pdl")
     ctx->opt_pdl = value != 0;
   else if (k == "coarse_krylov")
@@ -948,6 +949,10 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->conv_rows_ring = value == 3 ? 3 : 4;
   else if (k == "stream_vcycle")
     ctx->opt_stream = value != 0;
+  else if (k == "staged_legs")
+    ctx->opt_staged_legs = int(value);
+  else if (k == "stream_e0")
+    ctx->opt_stream_e0 = value != 0;
   else
     throw HbError{HB_ERR_ARG, "unknown option " + k};
   HB_API_END

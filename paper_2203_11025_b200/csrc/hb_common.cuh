@@ -18,6 +18,43 @@ __device__ __forceinline__ float2 crcp(float2 d) {
   const float s = 1.0f / fmaf(d.x, d.x, d.y * d.y);
   return make_float2(d.x * s, -d.y * s);
 }
+
+// Packed complex64 arithmetic on the sm_100 paired-fp32 pipe (FADD2 / FMUL2 /
+// FFMA2: one instruction per complex add, two per complex multiply; ptxas folds
+// the broadcasts, swizzles and per-lane negation into operand modifiers).
+// Rounding is identical to the scalar helpers above (same fma association).
+__device__ __forceinline__ unsigned long long pk2(float2 a) { return *reinterpret_cast<unsigned long long*>(&a); }
+__device__ __forceinline__ float2 upk2(unsigned long long a) { return *reinterpret_cast<float2*>(&a); }
+__device__ __forceinline__ float2 padd(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 psub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 pmulv(float2 a, float2 b) {  // element-wise
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 pfmav(float2 a, float2 b, float2 c) {  // element-wise a*b + c
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(pk2(a)), "l"(pk2(b)), "l"(pk2(c)));
+  return upk2(r);
+}
+__device__ __forceinline__ float2 pscale(float2 a, float s) { return pmulv(a, make_float2(s, s)); }
+// a + s*b
+__device__ __forceinline__ float2 paxpy(float2 a, float s, float2 b) { return pfmav(make_float2(s, s), b, a); }
+// complex a*b (same roundings as cmul)
+__device__ __forceinline__ float2 pmul(float2 a, float2 b) {
+  float2 t = pmulv(make_float2(a.y, a.y), make_float2(b.y, b.x));
+  t.x = -t.x;
+  return pfmav(make_float2(a.x, a.x), b, t);
+}
+
 __device__ __forceinline__ double2 dadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 // conj(a) * b in fp64
 __device__ __forceinline__ double2 dconjmul(float2 a, float2 b) {

@@ -319,7 +319,7 @@ static void slab_vcycle(std::vector<Context*>& S, int B, const std::vector<const
       Level& L = *c.levels[size_t(l)];
       Level& C = *c.levels[size_t(l) + 1];
       launch_down_stream(c, L.view(), C.win(), w, l % 2, B, act[s], l == 0 ? f0[s] : L.f.p, l == 0 ? fs[s] : nullptr,
-                         C.f.p);
+                         nullptr, C.f.p);
     }
     if (l + 1 < nl - 1)
       halo(S, l + 1, B, sizeof(float2), f_level, 0);
@@ -338,7 +338,7 @@ static void slab_vcycle(std::vector<Context*>& S, int B, const std::vector<const
       Level& L = *c.levels[size_t(l)];
       Level& C = *c.levels[size_t(l) + 1];
       launch_up_stream(c, L.view(), w, l % 2, C.nx, C.ny, C.win(), B, act[s], l == 0 ? f0[s] : L.f.p,
-                       l == 0 ? fs[s] : nullptr, C.x.p, l == 0 ? z[s] : L.x.p);
+                       l == 0 ? fs[s] : nullptr, nullptr, C.x.p, l == 0 ? z[s] : L.x.p);
     }
   }
 }

@@ -157,8 +157,10 @@ def test_slab_vcycle_halos_gloo(tmp_path, n, levels):
 
 
 # ------------------------------------------------------------------ GPU ---
-def _ctx(hg, k2, g, om, levels, coarse, net_seed=None):
+def _ctx(hg, k2, g, om, levels, coarse, net_seed=None, opts=()):
     c = hg.Context(0)
+    for key, val in opts:
+        c.set_option(key, val)
     c.set_problem(k2, g, om, 1 / 16, 1 / 2.25)
     c.build_hierarchy(hg.VCycleConfig(levels=levels, coarse_solver=coarse))
     if net_seed is not None:
@@ -167,8 +169,8 @@ def _ctx(hg, k2, g, om, levels, coarse, net_seed=None):
     return c
 
 
-def _group(hg, k2, g, om, levels, coarse, k, net_seed=None):
-    cs = [_ctx(hg, k2, g, om, levels, coarse, net_seed) for _ in range(k)]
+def _group(hg, k2, g, om, levels, coarse, k, net_seed=None, opts=()):
+    cs = [_ctx(hg, k2, g, om, levels, coarse, net_seed, opts) for _ in range(k)]
     hg.slab_init_local(cs)
     return cs
 
@@ -185,13 +187,15 @@ def rel(a, b):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("k", [2, 4])
-def test_slab_precond_equals_whole_c0(hgm, k):
+@pytest.mark.parametrize("k,staged", [(2, 2), (4, 2), (2, 1), (4, 1)])
+def test_slab_precond_equals_whole_c0(hgm, k, staged):
+    """staged 1: the cp.async-staged legs (HBM-bound sizes) on slab windows"""
     from oracle import oracle as O
     n = 128
     k2, g, om = _problem(n)
-    whole = _ctx(hgm, k2, g, om, 3, "gmres")
-    cs = _group(hgm, k2, g, om, 3, "gmres", k)
+    opts = (("staged_legs", staged), ("legs_wd", staged % 2))
+    whole = _ctx(hgm, k2, g, om, 3, "gmres", opts=opts)
+    cs = _group(hgm, k2, g, om, 3, "gmres", k, opts=opts)
     assert cs[0].slab_rows() == (0, n)
     r = O.random_complex_normal(7, (2, n, n))
     zw = whole.precond_apply("v", r)

@@ -194,6 +194,51 @@ int hb_read_slw1(const char* path, int* nx, int* ny, double* values);
 int hb_gen_sample_pairs(hb_ctx* ctx, int count, const uint64_t* seeds, int k_forced, int k_max, double* r_out,
                         double* e_out, int* k_used);
 
+/* ---- training -----------------------------------------
+ * The paper net's training on the device: traindet::run_batch (train-mode
+ * forward of build_unet / build_encoder, MSE loss, reverse sweep of the Tape
+ * rules; inc/training.hpp:121-147, inc/autodiff.hpp:121-480) and adam_step
+ * (inc/adam.hpp:25-58).  Trainable parameters are the reference's (kernels,
+ * biases, batch-norm scale / offset); running buffers update in train mode.
+ * TrainConfig (inc/training.hpp:12-20): */
+typedef struct hb_train_cfg {
+  int epochs;           /* 40 */
+  double lr0;           /* 1e-4 */
+  int batch0;           /* 20 */
+  int t0;               /* 48 */
+  double val_fraction;  /* 0.1 */
+  int encoder_solver;   /* must match the net's variant */
+  uint64_t seed;        /* 1 */
+} hb_train_cfg;
+/* One run_batch on host NCHW fp32 input [batch][4][H][W], kappa [batch][1][H][W]
+ * (encoder_solver only; else NULL), target [batch][2][H][W]: train_mode (batch
+ * statistics) or eval, gradients (zeroed first, as zero_grads) when with_grad,
+ * then one ADAM step at lr when step (Adam moments persist across calls until
+ * hb_paper_adam_reset).  loss: the MSE; out (may be NULL): the net output. */
+int hb_paper_train_batch(hb_ctx* ctx, int batch, int H, int W, const float* input, const float* kappa,
+                         const float* target, int train_mode, int with_grad, int step, double lr, double* loss,
+                         float* out);
+/* trainable element count, and the last batch's trainable gradients concatenated in registry order */
+int64_t hb_paper_trainable_count(hb_ctx* ctx);
+int hb_paper_grads(hb_ctx* ctx, int64_t count, float* grads);
+/* NetworkWeights::set_trainable_prefix (inc/unet.hpp:78-86) */
+int hb_paper_set_trainable_prefix(hb_ctx* ctx, const char* prefix, int trainable);
+int hb_paper_adam_reset(hb_ctx* ctx);
+/* train() (inc/training.hpp:152-227) over an in-memory Dataset: count samples
+ * r_hat / e_true [count][2][H][W] fp32 (quantize_sample form), model_id[count]
+ * into models problems' kappa2 / gamma [models][H][W] fp64 (row-major y, x).
+ * hist [hist_cap][4] per epoch: mean train rel error, mean val rel error, lr,
+ * batch.  aborted: a non-finite loss stopped training (weights restored to the
+ * last finite epoch). */
+int hb_paper_train(hb_ctx* ctx, const hb_train_cfg* cfg, int count, int H, int W, const float* r_hat,
+                   const float* e_true, const int* model_id, int models, const double* kappa2, const double* gamma,
+                   double* hist, int hist_cap, int* epochs_run, int* aborted);
+/* retrain() (inc/training.hpp:229-298) on the context's problem: n_pairs
+ * gen_sample_pair samples (seeds seed*6151+i, on the context's hierarchy),
+ * lr0/10, batch min(20, n_pairs); encoder_solver freezes the encoder. */
+int hb_paper_retrain(hb_ctx* ctx, int n_pairs, int epochs, const hb_train_cfg* base, uint64_t seed, double* hist,
+                     int hist_cap, int* epochs_run, int* aborted);
+
 /* ---- row slabs: one large grid over several GPUs --
  * The reference solves one grid in one process (block_fgmres,
  * inc/krylov.hpp:83-267; cycle_at, inc/multigrid.hpp:108-119); these entry

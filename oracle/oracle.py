@@ -369,6 +369,15 @@ def ref():
         R.hr_paper_pc_apply.argtypes = [_vp, C.c_int, _dp, _dp]
         R.hr_paper_fgmres.argtypes = [_vp, C.c_int, C.c_int, C.c_double, C.c_int, _dp, _dp, _dp, C.c_int, _ip, _ip]
         R.hr_gen_sample_pair.argtypes = [_vp, C.c_uint64, C.c_int, C.c_int, _dp, _dp]
+        R.hr_paper_trainable_count.argtypes = [_vp]
+        R.hr_paper_trainable_count.restype = C.c_int64
+        R.hr_paper_train_batch.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp, _fp, C.c_int, C.c_int, C.c_int,
+                                           C.c_double, _dp, _fp, _fp]
+        R.hr_paper_train.argtypes = [_vp, C.c_int, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64,
+                                     C.c_int, C.c_int, C.c_int, _fp, _fp, _ip, C.c_int, _dp, _dp, _dp, C.c_int, _ip,
+                                     _ip]
+        R.hr_paper_retrain.argtypes = [_vp, _vp, C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64, _dp, C.c_int, _ip,
+                                       _ip]
         R.hr_write_slw1.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
         R.hr_read_slw1.argtypes = [C.c_char_p, _ip, _ip, _dp]
         R.hr_init()
@@ -550,6 +559,50 @@ class RefPaperNet:
         y = np.zeros((B, 2, H, W), np.float32)
         _rcheck(ref().hr_paper_forward(self.h, B, H, W, _p(x, _fp), _p(y, _fp)))
         return y
+
+
+def _paper_train_methods():
+    def train_batch(self, x, target, kappa=None, train_mode=True, with_grad=True, step=False, lr=1e-4):
+        """traindet::run_batch (+ adam_step) -> (loss, out, trainable grads concatenated)"""
+        x = np.ascontiguousarray(x, np.float32)
+        t = np.ascontiguousarray(target, np.float32)
+        k = None if kappa is None else np.ascontiguousarray(kappa, np.float32)
+        B, _, H, W = x.shape
+        out = np.zeros((B, 2, H, W), np.float32)
+        g = np.zeros(ref().hr_paper_trainable_count(self.h), np.float32)
+        loss = C.c_double()
+        _rcheck(ref().hr_paper_train_batch(self.h, B, H, W, _p(x, _fp), _p(k, _fp) if k is not None else None,
+                                           _p(t, _fp), int(train_mode), int(with_grad), int(step), lr, C.byref(loss),
+                                           _p(out, _fp), _p(g, _fp)))
+        return loss.value, out, g
+
+    def train(self, epochs, lr0, batch0, t0, val_fraction, es, seed, r_hat, e_true, model_id, kappa2, gamma):
+        r = np.ascontiguousarray(r_hat, np.float32)
+        e = np.ascontiguousarray(e_true, np.float32)
+        m = np.ascontiguousarray(model_id, np.int32)
+        k2 = np.ascontiguousarray(kappa2, np.float64)
+        gm = np.ascontiguousarray(gamma, np.float64)
+        N, _, H, W = r.shape
+        h = np.zeros((max(epochs, 1), 4))
+        n, ab = C.c_int(), C.c_int()
+        _rcheck(ref().hr_paper_train(self.h, epochs, lr0, batch0, t0, val_fraction, int(es), seed, N, H, W, _p(r, _fp),
+                                     _p(e, _fp), _p(m, _ip), k2.shape[0], _p(k2), _p(gm), _p(h), h.shape[0],
+                                     C.byref(n), C.byref(ab)))
+        return h[:n.value], bool(ab.value)
+
+    def retrain(self, hier, n_pairs, epochs, lr0, es, seed):
+        h = np.zeros((max(epochs, 1), 4))
+        n, ab = C.c_int(), C.c_int()
+        _rcheck(ref().hr_paper_retrain(self.h, hier.ptr, n_pairs, epochs, lr0, int(es), seed, _p(h), h.shape[0],
+                                       C.byref(n), C.byref(ab)))
+        return h[:n.value], bool(ab.value)
+
+    RefPaperNet.train_batch = train_batch
+    RefPaperNet.train = train
+    RefPaperNet.retrain = retrain
+
+
+_paper_train_methods()
 
 
 class RefPaperPrecond:

@@ -26,6 +26,7 @@
 #include "helmbench/rng.hpp"
 #include "helmbench/stencil.hpp"
 #include "helmbench/tensor.hpp"
+#include "helmbench/training.hpp"
 #include "helmbench/unet.hpp"
 
 extern "C" void openblas_set_num_threads(int);
@@ -522,6 +523,8 @@ struct PaperNet {
   UNetConfig cfg;
   NetVariant variant = NetVariant::standalone;
   std::optional<FeatureStack> feats;
+  AdamState adam;                 // hr_paper_train_batch's ADAM state
+  std::vector<Param*> trainable;
 };
 }  // namespace
 
@@ -624,6 +627,111 @@ HR_EXPORT int hr_paper_feature(void* p, int l, float* out) {
   HR_TRY({
     const auto& f = static_cast<PaperNet*>(p)->feats.value().f.at(std::size_t(l));
     std::memcpy(out, f.v.data(), sizeof(float) * f.v.size());
+  })
+}
+
+
+// ---------------- training: traindet::run_batch + adam_step,
+// train() and retrain() (inc/training.hpp:121-298) on the reference's own code
+HR_EXPORT int64_t hr_paper_trainable_count(void* p) {
+  auto* q = static_cast<PaperNet*>(p);
+  int64_t n = 0;
+  for (Param* x : q->w->trainable()) n += int64_t(x->value.size());
+  return n;
+}
+// one run_batch (+ optional adam_step); grads: trainable gradients concatenated in registry order
+HR_EXPORT int hr_paper_train_batch(void* p, int B, int H, int W, const float* input, const float* kappa,
+                                   const float* target, int train_mode, int with_grad, int step, double lr,
+                                   double* loss, float* out, float* grads) {
+  HR_TRY({
+    auto* q = static_cast<PaperNet*>(p);
+    Tensor4 in(B, 4, H, W), tg(B, 2, H, W), kp(B, 1, H, W);
+    std::memcpy(in.v.data(), input, sizeof(float) * in.v.size());
+    std::memcpy(tg.v.data(), target, sizeof(float) * tg.v.size());
+    if (kappa) std::memcpy(kp.v.data(), kappa, sizeof(float) * kp.v.size());
+    q->w->zero_grads();
+    auto res = traindet::run_batch(*q->w, q->cfg, q->variant == NetVariant::encoder_solver, in, kp, tg,
+                                   train_mode != 0, with_grad != 0);
+    if (loss) *loss = res.loss;
+    if (out) std::memcpy(out, res.out.v.data(), sizeof(float) * res.out.v.size());
+    if (grads) {
+      std::size_t o = 0;
+      for (Param* x : q->w->trainable()) {
+        if (x->grad.size() == x->value.size())
+          std::memcpy(grads + o, x->grad.v.data(), sizeof(float) * x->grad.v.size());
+        else
+          std::fill(grads + o, grads + o + x->value.size(), 0.0f);
+        o += x->value.size();
+      }
+    }
+    if (step) {
+      if (q->trainable.empty()) q->trainable = q->w->trainable();
+      adam_step(q->trainable, q->adam, lr);
+    }
+  })
+}
+static TrainConfig train_cfg(int epochs, double lr0, int batch0, int t0, double val_fraction, int es, uint64_t seed) {
+  TrainConfig c;
+  c.epochs = epochs;
+  c.lr0 = lr0;
+  c.batch0 = batch0;
+  c.t0 = t0;
+  c.val_fraction = val_fraction;
+  c.encoder_solver = es != 0;
+  c.seed = seed;
+  return c;
+}
+static void put_hist(const TrainHistory& h, double* hist, int cap, int* n, int* aborted) {
+  for (std::size_t i = 0; i < h.epochs.size() && int(i) < cap; ++i) {
+    hist[i * 4 + 0] = h.epochs[i].mean_rel_error_train;
+    hist[i * 4 + 1] = h.epochs[i].mean_rel_error_val;
+    hist[i * 4 + 2] = h.epochs[i].lr;
+    hist[i * 4 + 3] = h.epochs[i].batch;
+  }
+  *n = int(h.epochs.size());
+  *aborted = h.aborted_non_finite ? 1 : 0;
+}
+// train() over an in-memory dataset: r_hat / e_true [count][2][H][W], kappa2 / gamma [models][H][W]
+HR_EXPORT int hr_paper_train(void* p, int epochs, double lr0, int batch0, int t0, double val_fraction, int es,
+                             uint64_t seed, int count, int H, int W, const float* r_hat, const float* e_true,
+                             const int* model_id, int models, const double* kappa2, const double* gamma, double* hist,
+                             int cap, int* n, int* aborted) {
+  HR_TRY({
+    auto* q = static_cast<PaperNet*>(p);
+    Dataset ds;
+    ds.spec.nx = W;
+    ds.spec.ny = H;
+    const std::size_t pl = std::size_t(H) * W;
+    for (int m = 0; m < models; ++m) {
+      HelmholtzProblem pr;
+      pr.kappa2.values = RealField(W, H);
+      pr.gamma.values = RealField(W, H);
+      std::memcpy(pr.kappa2.values.v.data(), kappa2 + m * pl, sizeof(double) * pl);
+      std::memcpy(pr.gamma.values.v.data(), gamma + m * pl, sizeof(double) * pl);
+      ds.problems.push_back(pr);
+      ds.model_refs.push_back("(in-memory)");
+    }
+    for (int s = 0; s < count; ++s) {
+      TrainingSample t;
+      t.model_id = model_id[s];
+      t.r_hat = Tensor4(1, 2, H, W);
+      t.e_true = Tensor4(1, 2, H, W);
+      std::memcpy(t.r_hat.v.data(), r_hat + std::size_t(s) * 2 * pl, sizeof(float) * 2 * pl);
+      std::memcpy(t.e_true.v.data(), e_true + std::size_t(s) * 2 * pl, sizeof(float) * 2 * pl);
+      ds.samples.push_back(std::move(t));
+    }
+    const TrainHistory h = train(ds, *q->w, q->cfg, train_cfg(epochs, lr0, batch0, t0, val_fraction, es, seed));
+    put_hist(h, hist, cap, n, aborted);
+  })
+}
+// retrain() on the problem of a RefMG (its own default-VCycleConfig hierarchy, as the reference)
+HR_EXPORT int hr_paper_retrain(void* p, void* mg, int n_pairs, int epochs, double lr0, int es, uint64_t seed,
+                               double* hist, int cap, int* n, int* aborted) {
+  HR_TRY({
+    auto* q = static_cast<PaperNet*>(p);
+    const auto* m = static_cast<RefMG*>(mg);
+    const TrainHistory h = retrain(*q->w, q->cfg, m->prob, n_pairs, epochs, train_cfg(1, lr0, 20, 48, 0.1, es, 1), seed);
+    put_hist(h, hist, cap, n, aborted);
   })
 }
 

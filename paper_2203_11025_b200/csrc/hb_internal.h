@@ -131,6 +131,7 @@ struct Prof {
 struct Context;
 struct SlabState;  // row-slab decomposition of one grid (hb_slab.cu)
 struct PaperState;  // the paper's U-Net (hb_paper.cu)
+struct TrainState;  // its training state (hb_train.cu)
 
 // ---- multigrid / operator launchers (hb_mg.cu)
 void launch_apply(Context& c, const LevelView& L, int which, int B, const int* act, const float2* u, float2* y,
@@ -324,6 +325,7 @@ struct Context {
   std::shared_ptr<SlabState> slab;
   // the paper's U-Net (inc/unet.hpp:139-257); when active it is the network of M_JU / M_VU
   std::shared_ptr<PaperState> paper;
+  std::shared_ptr<TrainState> train;  // device parameters, tape and ADAM moments while training
   unsigned long long prob_gen = 0;  // bumped by hb_set_problem
 };
 

@@ -27,41 +27,9 @@
 
 #include "hb_host.h"
 #include "hb_internal.h"
+#include "hb_paper.h"
 
 namespace hb {
-
-namespace {
-
-struct PParam {
-  std::string name;
-  int d[4];
-  std::vector<float> v;
-  size_t size() const { return size_t(d[0]) * d[1] * d[2] * d[3]; }
-};
-
-struct DevConv {  // one convolution with its fused epilogue
-  int cout = 0, cin = 0, k = 0;
-  bool transpose = false, bn = false;
-  DBuf<float> w, bias, mu, is, g, be;
-};
-
-}  // namespace
-
-struct PaperState {
-  hb_unet_cfg cfg{};
-  int variant = 0;  // 0 standalone ("unet."), 1 encoder_solver ("enc." + "sol.")
-  bool active = false;
-  std::vector<PParam> params;  // registry order
-  std::map<std::string, size_t> index;
-  std::map<std::string, DevConv> dev;  // by kernel name
-  bool dirty = true;
-  // encoder features (batch 1), per level
-  std::vector<DBuf<float>> feat;
-  unsigned long long feat_gen = ~0ull;
-  DBuf<float> k2f, gamf;  // fine-level kappa^2 and gamma (fp32) for the input stack
-  unsigned long long coef_gen = ~0ull;
-  DBuf<float> arena, io;
-};
 
 namespace {
 
@@ -176,6 +144,7 @@ void set_layout(PaperState& P, const hb_unet_cfg& c, int variant) {
   }
   P.dev.clear();
   P.dirty = true;
+  ++P.host_gen;
   P.feat_gen = ~0ull;
 }
 
@@ -749,6 +718,7 @@ void paper_forward_dev(Context& c, int B, int H, int W, const float* in, float* 
 
 }  // namespace
 
+PaperState& paper_state(Context& c) { return state(c); }
 bool paper_active(const Context& c) { return c.paper && c.paper->active; }
 void paper_deactivate(Context& c) {
   if (c.paper) c.paper->active = false;
@@ -832,6 +802,7 @@ int hb_paper_init(hb_ctx* ctx, uint64_t seed) {
   if (!P.active) throw HbError{HB_ERR_STATE, "paper net not set"};
   init_params(P, seed);
   P.dirty = true;
+  ++P.host_gen;
   P.feat_gen = ~0ull;
   HB_API_END
 }
@@ -864,6 +835,7 @@ int hb_paper_param(hb_ctx* ctx, const char* name, int64_t count, const float* in
   if (in) {
     std::memcpy(q.v.data(), in, q.v.size() * sizeof(float));
     P.dirty = true;
+  ++P.host_gen;
     P.feat_gen = ~0ull;
   }
   HB_API_END
@@ -909,6 +881,7 @@ int hb_load_checkpoint(hb_ctx* ctx, const char* path) {
     seen[it->second] = true;
   }
   P.dirty = true;
+  ++P.host_gen;
   P.feat_gen = ~0ull;
   HB_API_END
 }

@@ -1,0 +1,1220 @@
+// Training of the paper's U-Net on the device:
+// traindet::run_batch (inc/training.hpp:121-147) -- the train-mode forward of
+// build_unet / build_encoder (inc/unet.hpp:139-257), the MSE loss, the reverse
+// sweep of the Tape rules (inc/autodiff.hpp:121-480) -- and bias-corrected
+// ADAM (inc/adam.hpp:25-58), driven by the reference's epoch loops train() and
+// retrain() (inc/training.hpp:152-298).
+//
+// The tape is a static op list built once per (batch, H, W, mode) from the same
+// registry the inference path uses (hb_paper.h), so parameter names, creation
+// order and trainable flags are the reference's.  Layout NCHW fp32 like the
+// reference's Tensor4, all activations and gradients in one device arena each,
+// all parameters / gradients / ADAM moments in flat device buffers in registry
+// order.  Kernels:
+//   conv forward          direct, thread = 1 output pixel x 8 output channels
+//   transposed conv       gather form of the exact adjoint (same kernel layout)
+//   conv input gradient   = transposed conv of dy with the conv's kernel; the
+//                           transposed conv's input gradient = conv of dz
+//   kernel gradient       one CTA per (channel pair), thread-strided pixels,
+//                           per-tap fp32 partials, fp64 block reduction
+//   batch norm            fp64 channel statistics (two passes, as the
+//                           reference), normalise; backward fp64 channel sums
+//   ELU / add / concat / MSE / ADAM   elementwise (ADAM in fp64 arithmetic)
+// The reductions the reference carries in double (batch-norm statistics, bias
+// and loss sums, ADAM) are double here; convolution sums are fp32 in both
+// (the reference's Eigen / sgemm products), in a different order.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "hb_common.cuh"
+#include "hb_host.h"
+#include "hb_internal.h"
+#include "hb_paper.h"
+
+namespace hb {
+
+namespace {
+
+constexpr int TB = 256;  // threads per CTA of the elementwise / pixel kernels
+constexpr int CO = 8;    // output channels per thread (conv forward kernels)
+
+inline int nblk(size_t n) { return int(std::min<size_t>((n + TB - 1) / TB, size_t(1) << 20)); }
+
+// ------------------------------------------------------------------ kernels
+// y[b,co,oy,ox] = bias[co] + sum_{ci,ky,kx} x[b,ci,oy*s+ky-p,ox*s+kx-p] K[co,ci,ky,kx]
+// (conv2d, inc/autodiff.hpp:121-150: zero padding p = (k-1)/2, cross-correlation)
+__global__ void __launch_bounds__(TB) k_conv_fwd(const float* __restrict__ x, int cin, int H, int W,
+                                                 const float* __restrict__ K, const float* __restrict__ bias, int cout,
+                                                 int k, int s, int Ho, int Wo, float* __restrict__ y) {
+  const int pix = blockIdx.x * TB + threadIdx.x;
+  const int co0 = blockIdx.y * CO, b = blockIdx.z;
+  if (pix >= Ho * Wo) return;
+  const int oy = pix / Wo, ox = pix % Wo, p = (k - 1) / 2;
+  float acc[CO];
+#pragma unroll
+  for (int j = 0; j < CO; ++j) acc[j] = 0.f;
+  const int kk = k * k;
+  for (int ci = 0; ci < cin; ++ci) {
+    const float* xp = x + (size_t(b) * cin + ci) * H * W;
+    for (int ky = 0; ky < k; ++ky) {
+      const int iy = oy * s + ky - p;
+      if (iy < 0 || iy >= H) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int ix = ox * s + kx - p;
+        if (ix < 0 || ix >= W) continue;
+        const float xv = __ldg(xp + size_t(iy) * W + ix);
+        const int t = ky * k + kx;
+#pragma unroll
+        for (int j = 0; j < CO; ++j) {
+          const int co = min(co0 + j, cout - 1);
+          acc[j] = fmaf(xv, __ldg(K + (size_t(co) * cin + ci) * kk + t), acc[j]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CO; ++j) {
+    const int co = co0 + j;
+    if (co < cout) y[(size_t(b) * cout + co) * Ho * Wo + pix] = acc[j] + (bias ? __ldg(bias + co) : 0.f);
+  }
+}
+
+// z[b,cb,Y,X] = bias[cb] + sum_{ca, ky, kx: Y = y*s+ky-p, X = x*s+kx-p} u[b,ca,y,x] K[ca,cb,ky,kx]
+// (conv2d_transpose, inc/autodiff.hpp:155-211: the exact adjoint of conv2d)
+__global__ void __launch_bounds__(TB) k_convT_fwd(const float* __restrict__ u, int ca, int h, int w,
+                                                  const float* __restrict__ K, const float* __restrict__ bias, int cb,
+                                                  int k, int s, int H, int W, float* __restrict__ z) {
+  const int pix = blockIdx.x * TB + threadIdx.x;
+  const int c0 = blockIdx.y * CO, b = blockIdx.z;
+  if (pix >= H * W) return;
+  const int Y = pix / W, X = pix % W, p = (k - 1) / 2;
+  float acc[CO];
+#pragma unroll
+  for (int j = 0; j < CO; ++j) acc[j] = 0.f;
+  const int kk = k * k;
+  for (int a = 0; a < ca; ++a) {
+    const float* up = u + (size_t(b) * ca + a) * h * w;
+    for (int ky = 0; ky < k; ++ky) {
+      const int ty = Y + p - ky;
+      if (ty < 0 || ty % s) continue;
+      const int y = ty / s;
+      if (y >= h) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int tx = X + p - kx;
+        if (tx < 0 || tx % s) continue;
+        const int xx = tx / s;
+        if (xx >= w) continue;
+        const float uv = __ldg(up + size_t(y) * w + xx);
+        const int t = ky * k + kx;
+#pragma unroll
+        for (int j = 0; j < CO; ++j) {
+          const int c = min(c0 + j, cb - 1);
+          acc[j] = fmaf(uv, __ldg(K + (size_t(a) * cb + c) * kk + t), acc[j]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < CO; ++j) {
+    const int c = c0 + j;
+    if (c < cb) z[(size_t(b) * cb + c) * H * W + pix] += acc[j] + (bias ? __ldg(bias + c) : 0.f);
+  }
+}
+
+// dK[a,c,ky,kx] += sum_{b,y,x} A[b,a,y,x] X[b,c,y*s+ky-p,x*s+kx-p]
+// conv2d: A = dy (cout), X = x (cin); conv2d_transpose: A = u (x channels), X = dz
+template <int KMAX>
+__global__ void __launch_bounds__(TB) k_wgrad(int nb, const float* __restrict__ A, int na, int h, int w,
+                                              const float* __restrict__ X, int nc, int H, int W, int k, int s,
+                                              float* __restrict__ dK) {
+  const int a = blockIdx.x / nc, c = blockIdx.x % nc;
+  const int p = (k - 1) / 2, kk = k * k;
+  float acc[KMAX * KMAX];
+#pragma unroll
+  for (int t = 0; t < KMAX * KMAX; ++t) acc[t] = 0.f;
+  const int hw = h * w;
+  const size_t total = size_t(nb) * hw;
+  for (size_t i = threadIdx.x; i < total; i += TB) {
+    const int b = int(i / hw), q = int(i % hw);
+    const int y = q / w, x = q % w;
+    const float av = __ldg(A + (size_t(b) * na + a) * hw + q);
+    const float* xp = X + (size_t(b) * nc + c) * H * W;
+#pragma unroll
+    for (int ky = 0; ky < KMAX; ++ky) {
+      const int iy = y * s + ky - p;
+      const bool oky = ky < k && iy >= 0 && iy < H;
+#pragma unroll
+      for (int kx = 0; kx < KMAX; ++kx) {
+        const int ix = x * s + kx - p;
+        if (oky && kx < k && ix >= 0 && ix < W) acc[ky * KMAX + kx] = fmaf(av, __ldg(xp + size_t(iy) * W + ix), acc[ky * KMAX + kx]);
+      }
+    }
+  }
+  __shared__ double red[TB / 32];
+  for (int ky = 0; ky < k; ++ky)
+    for (int kx = 0; kx < k; ++kx) {
+      double v = acc[ky * KMAX + kx];
+      v = warp_sum(v);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0;
+        for (int i = 0; i < TB / 32; ++i) t += red[i];
+        dK[(size_t(a) * nc + c) * kk + ky * k + kx] += float(t);
+      }
+      __syncthreads();
+    }
+}
+
+// per-channel fp64 sum over (batch, plane): out[c] += float(sum)  (bias gradients)
+__global__ void __launch_bounds__(TB) k_chsum(int nb, int C, int plane, const float* __restrict__ g, float* out) {
+  const int c = blockIdx.x;
+  double s = 0;
+  for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
+    const size_t b = i / plane, q = i % plane;
+    s += g[(b * C + c) * plane + q];
+  }
+  __shared__ double red[TB / 32];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int i = 0; i < TB / 32; ++i) t += red[i];
+    out[c] += float(t);
+  }
+}
+
+__device__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double t = 0;
+  for (int i = 0; i < TB / 32; ++i) t += red[i];
+  __syncthreads();
+  return t;
+}
+
+// batch norm statistics (inc/autodiff.hpp:228-262).  train: biased batch mean /
+// variance in fp64 (two passes), running buffers folded with momentum 0.9 and
+// the update count bumped; eval: the running buffers.  st[c] = (mean_f, inv_std_f)
+__global__ void __launch_bounds__(TB) k_bn_stats(int nb, int C, int plane, const float* __restrict__ x, int train,
+                                                 float eps, float momentum, float* rmean, float* rvar, float* count,
+                                                 float2* st) {
+  const int c = blockIdx.x;
+  __shared__ double red[TB / 32];
+  double mean, var;
+  if (train) {
+    const double cnt = double(nb) * plane;
+    double s = 0;
+    for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) s += x[((i / plane) * C + c) * plane + i % plane];
+    mean = block_sum(s, red) / cnt;
+    s = 0;
+    for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
+      const double d = x[((i / plane) * C + c) * plane + i % plane] - mean;
+      s += d * d;
+    }
+    var = block_sum(s, red) / cnt;
+    if (threadIdx.x == 0) {
+      rmean[c] = momentum * rmean[c] + (1.0f - momentum) * float(mean);
+      rvar[c] = momentum * rvar[c] + (1.0f - momentum) * float(var);
+      if (c == 0) count[0] += 1.0f;
+    }
+  } else {
+    mean = rmean[c];
+    var = rvar[c];
+  }
+  if (threadIdx.x == 0) st[c] = make_float2(float(mean), float(1.0 / sqrt(var + double(eps))));
+}
+
+// y = (x - mu) * is * g + be
+__global__ void k_bn_apply(size_t n, int C, int plane, const float* __restrict__ x, const float2* __restrict__ st,
+                           const float* __restrict__ g, const float* __restrict__ be, float* __restrict__ y) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) {
+    const int c = int((i / plane) % C);
+    const float2 m = st[c];
+    y[i] = (x[i] - m.x) * m.y * g[c] + be[c];
+  }
+}
+
+// batch norm backward (inc/autodiff.hpp:281-318): fp64 channel sums of dy and
+// dy * xhat -> scale / offset gradients, then dx (train: through the batch
+// statistics; eval: g * is * dy)
+__global__ void __launch_bounds__(TB) k_bn_bwd(int nb, int C, int plane, const float* __restrict__ x,
+                                               const float* __restrict__ go, const float2* __restrict__ st,
+                                               const float* __restrict__ g, int train, float* dscale, float* doffset,
+                                               float* dx) {
+  const int c = blockIdx.x;
+  __shared__ double red[TB / 32];
+  const float mu = st[c].x, is = st[c].y, gc = g[c];
+  double sdy = 0, sdyx = 0;
+  for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
+    const size_t o = ((i / plane) * C + c) * plane + i % plane;
+    const double gp = go[o];
+    sdy += gp;
+    sdyx += gp * (x[o] - mu) * is;
+  }
+  sdy = block_sum(sdy, red);
+  sdyx = block_sum(sdyx, red);
+  if (threadIdx.x == 0) {
+    if (dscale) dscale[c] += float(sdyx);
+    if (doffset) doffset[c] += float(sdy);
+  }
+  if (!dx) return;
+  const double cnt = double(nb) * plane, a = sdy / cnt, c2 = sdyx / cnt;
+  for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
+    const size_t o = ((i / plane) * C + c) * plane + i % plane;
+    if (train) {
+      const double xhat = double(x[o] - mu) * is;
+      dx[o] += float(double(gc) * is * (go[o] - a - xhat * c2));
+    } else {
+      dx[o] += gc * is * go[o];
+    }
+  }
+}
+
+__global__ void k_elu(size_t n, const float* __restrict__ x, float* __restrict__ y) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) {
+    const float t = x[i];
+    y[i] = t >= 0.0f ? t : expm1f(t);
+  }
+}
+__global__ void k_elu_bwd(size_t n, const float* __restrict__ x, const float* __restrict__ y,
+                          const float* __restrict__ go, float* gx) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB)
+    gx[i] += go[i] * (x[i] >= 0.0f ? 1.0f : y[i] + 1.0f);
+}
+__global__ void k_add(size_t n, const float* __restrict__ a, const float* __restrict__ b, float* __restrict__ y) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) y[i] = a[i] + b[i];
+}
+__global__ void k_acc(size_t n, const float* __restrict__ g, float* d) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) d[i] += g[i];
+}
+// channel concatenation [a | b] per batch slab; bsl = 0 broadcasts b over the batch
+__global__ void k_concat(int nb, size_t sa, size_t sb, const float* __restrict__ a, const float* __restrict__ b,
+                         size_t bsl, float* __restrict__ y) {
+  const size_t so = sa + sb, n = size_t(nb) * so;
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) {
+    const size_t bi = i / so, q = i % so;
+    y[i] = q < sa ? a[bi * sa + q] : b[bi * bsl + q - sa];
+  }
+}
+__global__ void k_concat_bwd(int nb, size_t sa, size_t sb, const float* __restrict__ go, float* ga, float* gb) {
+  const size_t so = sa + sb, n = size_t(nb) * so;
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) {
+    const size_t bi = i / so, q = i % so;
+    if (q < sa) {
+      if (ga) ga[bi * sa + q] += go[i];
+    } else if (gb) {
+      gb[bi * sb + q - sa] += go[i];
+    }
+  }
+}
+// mse (inc/autodiff.hpp:448-470): loss = sum (p - t)^2 / n in fp64; gp += 2 / n (p - t)
+__global__ void __launch_bounds__(TB) k_mse(size_t n, int nb, const float* __restrict__ p, const float* __restrict__ t,
+                                            double* loss, float* gp) {
+  __shared__ double red[TB / 32];
+  double s = 0;
+  for (size_t i = threadIdx.x; i < n; i += TB) {
+    const double d = double(p[i]) - t[i];
+    s += d * d;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *loss = double(float(s / nb));
+  if (!gp) return;
+  const float scale = 2.0f * 1.0f / float(nb);
+  for (size_t i = threadIdx.x; i < n; i += TB) gp[i] += scale * (p[i] - t[i]);
+}
+// non-finite count over a buffer
+__global__ void k_nonfinite(size_t n, const float* __restrict__ g, int* bad) {
+  int any = 0;
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) any |= !isfinite(g[i]);
+  if (__syncthreads_or(any) && threadIdx.x == 0) atomicAdd(bad, 1);
+}
+// ADAM (inc/adam.hpp:38-55), fp64 arithmetic, fp32 state
+__global__ void k_adam(size_t n, const float* __restrict__ g, float* m, float* v, float* w, double lr, double b1,
+                       double b2, double bc1, double bc2, double eps) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) {
+    const double gi = g[i];
+    m[i] = float(b1 * m[i] + (1.0 - b1) * gi);
+    v[i] = float(b2 * v[i] + (1.0 - b2) * gi * gi);
+    const double mh = m[i] / bc1, vh = v[i] / bc2;
+    w[i] -= float(lr * mh / (sqrt(vh) + eps));
+  }
+}
+
+// ------------------------------------------------------------------ the tape
+struct Ten {
+  int n, c, h, w;
+  size_t off;    // value offset in the arena
+  bool grad;     // carries a gradient (not a leaf)
+  size_t size() const { return size_t(n) * c * h * w; }
+};
+
+enum OpK { OP_CONV, OP_CONVT, OP_BN, OP_ELU, OP_ADD, OP_CONCAT };
+
+struct Op {
+  OpK kind;
+  int a = -1, b = -1, y = -1;  // tensor ids
+  int pk = -1, pb = -1;        // kernel / bias parameter (registry index)
+  int k = 0, s = 1;
+  int pbn = -1;                // batch norm: registry index of ".scale" (offset, rmean, rvar, count follow)
+  bool train = true;
+  size_t st = 0;               // batch norm: offset of its (mean, inv_std) pairs in the stats buffer
+  bool bcast_b = false;        // concat: b is batch-1, broadcast
+};
+
+}  // namespace
+
+struct TrainState {
+  // flat parameter store (registry order) and per-parameter offsets
+  std::vector<size_t> poff;
+  size_t ptotal = 0;
+  std::vector<char> trainable;
+  DBuf<float> dparam, dgrad, adam_m, adam_v, snapshot;
+  bool params_on_device = false;
+  unsigned long long gen = ~0ull;  // PaperState::host_gen of the uploaded parameters
+  long long adam_step = 0, adam_skipped = 0;
+  bool adam_init = false;
+  // tape
+  int key_B = -1, key_H = -1, key_W = -1, key_mode = -1;
+  std::vector<Ten> tens;
+  std::vector<Op> ops;
+  int t_input = -1, t_kappa = -1, t_target = -1, t_out = -1;
+  std::vector<int> t_feats;  // frozen feature leaves (encoder_solver retrain)
+  size_t arena = 0, nstats = 0;
+  DBuf<float> vals, grads, tmp;
+  DBuf<float2> stats;
+  DBuf<double> dloss;
+  DBuf<int> dbad;
+  // frozen encoder features (batch 1) for retrain
+  std::vector<std::vector<float>> frozen;  // per level, NCHW [1][C][H>>l][W>>l]
+  std::vector<std::array<int, 3>> frozen_dims;
+};
+
+namespace {
+
+
+bool ends_with(const std::string& s, const char* t) {
+  const size_t n = std::strlen(t);
+  return s.size() >= n && s.compare(s.size() - n, n, t) == 0;
+}
+bool is_buffer(const std::string& n) { return ends_with(n, ".rmean") || ends_with(n, ".rvar") || ends_with(n, ".count"); }
+
+TrainState& tstate(Context& c) {
+  if (!c.train) c.train = std::make_shared<TrainState>();
+  return *c.train;
+}
+
+// parameters to the device (flat, registry order); trainable flags default to
+// the reference's (every kernel / bias / scale / offset; buffers are not)
+void ensure_params(Context& c) {
+  PaperState& P = paper_state(c);
+  TrainState& T = tstate(c);
+  if (!P.active) throw HbError{HB_ERR_STATE, "paper net not set (hb_set_paper_net)"};
+  if (T.params_on_device && T.gen == P.host_gen && T.poff.size() == P.params.size()) return;
+  T.poff.assign(P.params.size(), 0);
+  T.trainable.assign(P.params.size(), 0);
+  size_t o = 0;
+  for (size_t i = 0; i < P.params.size(); ++i) {
+    T.poff[i] = o;
+    o += (P.params[i].size() + 3) & ~size_t(3);
+    T.trainable[i] = !is_buffer(P.params[i].name);
+  }
+  T.ptotal = o;
+  T.dparam.ensure(o);
+  T.dgrad.ensure(o);
+  std::vector<float> h(o, 0.f);
+  for (size_t i = 0; i < P.params.size(); ++i)
+    std::copy(P.params[i].v.begin(), P.params[i].v.end(), h.begin() + long(T.poff[i]));
+  HB_CUDA(cudaMemcpy(T.dparam.p, h.data(), o * sizeof(float), cudaMemcpyHostToDevice));
+  T.params_on_device = true;
+  T.gen = P.host_gen;
+  T.adam_init = false;
+  T.adam_step = 0;
+  T.key_B = -1;
+}
+
+// device parameters back to the host registry (inference path re-uploads)
+void params_to_host(Context& c) {
+  PaperState& P = paper_state(c);
+  TrainState& T = tstate(c);
+  if (!T.params_on_device) return;
+  std::vector<float> h(T.ptotal);
+  HB_CUDA(cudaMemcpy(h.data(), T.dparam.p, T.ptotal * sizeof(float), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < P.params.size(); ++i)
+    std::copy(h.begin() + long(T.poff[i]), h.begin() + long(T.poff[i] + P.params[i].size()), P.params[i].v.begin());
+  P.dirty = true;
+  P.feat_gen = ~0ull;
+}
+
+struct Builder {
+  const PaperState& P;
+  TrainState& T;
+  bool train;
+  int pidx(const std::string& n) const {
+    auto it = P.index.find(n);
+    if (it == P.index.end()) throw HbError{HB_ERR_STATE, "paper net has no parameter " + n};
+    return int(it->second);
+  }
+  int ten(int n, int c, int h, int w, bool grad) {
+    T.tens.push_back(Ten{n, c, h, w, 0, grad});
+    return int(T.tens.size()) - 1;
+  }
+  int conv(int x, const std::string& kn, const std::string& bn, int stride) {
+    const Ten& X = T.tens[size_t(x)];
+    const PParam& K = P.params[size_t(pidx(kn))];
+    const int k = K.d[2];
+    if (k > 5) throw HbError{HB_ERR_ARG, "training supports kernels up to 5x5"};
+    if (K.d[1] != X.c) throw HbError{HB_ERR_STATE, "conv kernel in-channels mismatch at " + kn};
+    const int p = (k - 1) / 2;
+    const int ho = (X.h + 2 * p - k) / stride + 1, wo = (X.w + 2 * p - k) / stride + 1;
+    Op o{OP_CONV};
+    o.a = x;
+    o.pk = pidx(kn);
+    o.pb = pidx(bn);
+    o.k = k;
+    o.s = stride;
+    o.y = ten(X.n, K.d[0], ho, wo, true);
+    T.ops.push_back(o);
+    return o.y;
+  }
+  int convT(int x, const std::string& kn, const std::string& bn, int stride) {
+    const Ten& X = T.tens[size_t(x)];
+    const PParam& K = P.params[size_t(pidx(kn))];
+    if (K.d[0] != X.c) throw HbError{HB_ERR_STATE, "deconv kernel in-channels mismatch at " + kn};
+    if (K.d[2] > 5) throw HbError{HB_ERR_ARG, "training supports kernels up to 5x5"};
+    Op o{OP_CONVT};
+    o.a = x;
+    o.pk = pidx(kn);
+    o.pb = pidx(bn);
+    o.k = K.d[2];
+    o.s = stride;
+    o.y = ten(X.n, K.d[1], X.h * stride, X.w * stride, true);
+    T.ops.push_back(o);
+    return o.y;
+  }
+  int bn(int x, const std::string& name) {
+    const Ten& X = T.tens[size_t(x)];
+    Op o{OP_BN};
+    o.a = x;
+    o.pbn = pidx(name + ".scale");
+    o.train = train;
+    o.st = T.nstats;
+    T.nstats += size_t(X.c);
+    o.y = ten(X.n, X.c, X.h, X.w, true);
+    T.ops.push_back(o);
+    return o.y;
+  }
+  int elu(int x) {
+    const Ten& X = T.tens[size_t(x)];
+    Op o{OP_ELU};
+    o.a = x;
+    o.y = ten(X.n, X.c, X.h, X.w, true);
+    T.ops.push_back(o);
+    return o.y;
+  }
+  int add(int a, int b) {
+    const Ten& A = T.tens[size_t(a)];
+    Op o{OP_ADD};
+    o.a = a;
+    o.b = b;
+    o.y = ten(A.n, A.c, A.h, A.w, true);
+    T.ops.push_back(o);
+    return o.y;
+  }
+  int concat(int a, int b) {
+    const Ten A = T.tens[size_t(a)], Bt = T.tens[size_t(b)];
+    Op o{OP_CONCAT};
+    o.a = a;
+    o.b = b;
+    o.bcast_b = Bt.n == 1 && A.n > 1;
+    o.y = ten(A.n, A.c + Bt.c, A.h, A.w, true);
+    T.ops.push_back(o);
+    return o.y;
+  }
+  // x <- elu(BN2(x + K2 elu(BN1(K1 x))))  (netdet::resnet_block, inc/unet.hpp:147-160)
+  int resnet(const std::string& n, int x) {
+    int t = conv(x, n + ".k1", n + ".b1", 1);
+    t = elu(bn(t, n + ".bn1"));
+    t = conv(t, n + ".k2", n + ".b2", 1);
+    return elu(bn(add(x, t), n + ".bn2"));
+  }
+  // build_encoder (inc/unet.hpp:231-257)
+  std::vector<int> encoder(int kap) {
+    const hb_unet_cfg& c = P.cfg;
+    std::vector<int> f;
+    int x = elu(bn(conv(kap, "enc.entry.k", "enc.entry.b", 1), "enc.entry.bn"));
+    f.push_back(x);
+    for (int l = 0; l < c.levels; ++l) {
+      const std::string d = "enc.down" + std::to_string(l);
+      x = elu(bn(conv(x, d + ".k", d + ".b", 2), d + ".bn"));
+      for (int r = 0; r < c.resnet_per_level; ++r) x = resnet("enc.res" + std::to_string(l + 1) + "_" + std::to_string(r), x);
+      f.push_back(x);
+    }
+    return f;
+  }
+  // build_unet (inc/unet.hpp:165-226)
+  int unet(int input, const std::string& pre, const std::vector<int>& feats) {
+    const hb_unet_cfg& c = P.cfg;
+    const bool es = !feats.empty();
+    std::vector<int> skips(size_t(c.levels));
+    skips[0] = input;
+    int x = input;
+    for (int l = 0; l < c.levels; ++l) {
+      if (es) x = concat(x, feats[size_t(l)]);
+      const std::string d = pre + "down" + std::to_string(l);
+      x = elu(bn(conv(x, d + ".k", d + ".b", 2), d + ".bn"));
+      if (l < c.levels - 1) {
+        for (int r = 0; r < c.resnet_per_level; ++r) x = resnet(pre + "res" + std::to_string(l + 1) + "_" + std::to_string(r), x);
+        skips[size_t(l) + 1] = x;
+      }
+    }
+    for (int r = 0; r < c.bottleneck_resnets; ++r) x = resnet(pre + "bot" + std::to_string(r), x);
+    for (int s = c.levels; s >= 1; --s) {
+      const int t = s - 1;
+      if (es) x = concat(x, feats[size_t(s)]);
+      x = elu(x);
+      const std::string u = pre + "up" + std::to_string(t);
+      x = bn(convT(x, u + ".k", u + ".b", 2), u + ".bn");
+      x = concat(x, skips[size_t(t)]);
+    }
+    return conv(x, pre + "out.k", pre + "out.b", 1);
+  }
+};
+
+// mode: 0 standalone, 1 encoder_solver joint, 2 encoder_solver with frozen
+// features, 3 the encoder alone in eval mode (frozen features)
+void build_tape(Context& c, int B, int H, int W, int mode, bool train) {
+  PaperState& P = paper_state(c);
+  TrainState& T = tstate(c);
+  const int key_mode = mode * 2 + (train ? 1 : 0);
+  if (T.key_B == B && T.key_H == H && T.key_W == W && T.key_mode == key_mode) return;
+  if (H % (1 << P.cfg.levels) || W % (1 << P.cfg.levels))
+    throw HbError{HB_ERR_ARG, "input dims must be divisible by 2^levels"};
+  T.tens.clear();
+  T.ops.clear();
+  T.t_feats.clear();
+  T.nstats = 0;
+  Builder bd{P, T, train};
+  if (mode == 3) {
+    T.t_kappa = bd.ten(1, 1, H, W, false);
+    T.t_feats = bd.encoder(T.t_kappa);
+    T.t_input = T.t_target = T.t_out = -1;
+  } else {
+    T.t_input = bd.ten(B, 4, H, W, false);
+    T.t_target = bd.ten(B, 2, H, W, false);
+    T.t_kappa = -1;
+    std::vector<int> feats;
+    if (mode == 1) {
+      T.t_kappa = bd.ten(B, 1, H, W, false);
+      feats = bd.encoder(T.t_kappa);
+    } else if (mode == 2) {
+      if (T.frozen.size() != size_t(P.cfg.levels) + 1) throw HbError{HB_ERR_STATE, "no frozen encoder features"};
+      for (size_t l = 0; l < T.frozen.size(); ++l)
+        feats.push_back(bd.ten(1, T.frozen_dims[l][0u], T.frozen_dims[l][1u], T.frozen_dims[l][2u], false));
+      T.t_feats = feats;
+    }
+    T.t_out = bd.unet(T.t_input, mode == 0 ? "unet." : "sol.", feats);
+  }
+  size_t o = 0;
+  for (auto& t : T.tens) {
+    t.off = o;
+    o += (t.size() + 3) & ~size_t(3);
+  }
+  T.arena = o;
+  T.vals.ensure(o);
+  T.grads.ensure(o);
+  T.stats.ensure(std::max<size_t>(1, T.nstats));
+  T.dloss.ensure(1);
+  T.dbad.ensure(1);
+  T.key_B = B;
+  T.key_H = H;
+  T.key_W = W;
+  T.key_mode = key_mode;
+}
+
+float* V(TrainState& T, int t) { return T.vals.p + T.tens[size_t(t)].off; }
+float* G(TrainState& T, int t) { return T.tens[size_t(t)].grad ? T.grads.p + T.tens[size_t(t)].off : nullptr; }
+float* PV(TrainState& T, int i) { return T.dparam.p + T.poff[size_t(i)]; }
+float* PG(TrainState& T, int i) { return T.trainable[size_t(i)] ? T.dgrad.p + T.poff[size_t(i)] : nullptr; }
+int egrid(size_t n) { return nblk(n); }
+
+void run_forward(Context& c) {
+  TrainState& T = tstate(c);
+  cudaStream_t st = c.stream;
+  for (const Op& o : T.ops) {
+    const Ten& A = T.tens[size_t(o.a)];
+    const Ten& Y = T.tens[size_t(o.y)];
+    switch (o.kind) {
+      case OP_CONV: {
+        const dim3 g((Y.h * Y.w + TB - 1) / TB, (Y.c + CO - 1) / CO, Y.n);
+        k_conv_fwd<<<g, TB, 0, st>>>(V(T, o.a), A.c, A.h, A.w, PV(T, o.pk), PV(T, o.pb), Y.c, o.k, o.s, Y.h, Y.w,
+                                     V(T, o.y));
+        break;
+      }
+      case OP_CONVT: {
+        HB_CUDA(cudaMemsetAsync(V(T, o.y), 0, Y.size() * sizeof(float), st));
+        const dim3 g((Y.h * Y.w + TB - 1) / TB, (Y.c + CO - 1) / CO, Y.n);
+        k_convT_fwd<<<g, TB, 0, st>>>(V(T, o.a), A.c, A.h, A.w, PV(T, o.pk), PV(T, o.pb), Y.c, o.k, o.s, Y.h, Y.w,
+                                      V(T, o.y));
+        break;
+      }
+      case OP_BN: {
+        const int plane = A.h * A.w;
+        k_bn_stats<<<A.c, TB, 0, st>>>(A.n, A.c, plane, V(T, o.a), o.train ? 1 : 0, 1e-5f, 0.9f, PV(T, o.pbn + 2),
+                                       PV(T, o.pbn + 3), PV(T, o.pbn + 4), T.stats.p + o.st);
+        k_bn_apply<<<egrid(A.size()), TB, 0, st>>>(A.size(), A.c, plane, V(T, o.a), T.stats.p + o.st, PV(T, o.pbn),
+                                                   PV(T, o.pbn + 1), V(T, o.y));
+        break;
+      }
+      case OP_ELU:
+        k_elu<<<egrid(A.size()), TB, 0, st>>>(A.size(), V(T, o.a), V(T, o.y));
+        break;
+      case OP_ADD:
+        k_add<<<egrid(A.size()), TB, 0, st>>>(A.size(), V(T, o.a), V(T, o.b), V(T, o.y));
+        break;
+      case OP_CONCAT: {
+        const Ten& Bt = T.tens[size_t(o.b)];
+        const size_t sa = size_t(A.c) * A.h * A.w, sb = size_t(Bt.c) * Bt.h * Bt.w;
+        k_concat<<<egrid(Y.size()), TB, 0, st>>>(A.n, sa, sb, V(T, o.a), V(T, o.b), o.bcast_b ? 0 : sb, V(T, o.y));
+        break;
+      }
+    }
+    HB_CUDA(cudaGetLastError());
+  }
+}
+
+void run_backward(Context& c) {
+  TrainState& T = tstate(c);
+  cudaStream_t st = c.stream;
+  for (auto it = T.ops.rbegin(); it != T.ops.rend(); ++it) {
+    const Op& o = *it;
+    const Ten& A = T.tens[size_t(o.a)];
+    const Ten& Y = T.tens[size_t(o.y)];
+    const float* gy = G(T, o.y);
+    switch (o.kind) {
+      case OP_CONV: {
+        if (float* dk = PG(T, o.pk)) {
+          const int grid = Y.c * A.c;
+          if (o.k <= 3)
+            k_wgrad<3><<<grid, TB, 0, st>>>(Y.n, gy, Y.c, Y.h, Y.w, V(T, o.a), A.c, A.h, A.w, o.k, o.s, dk);
+          else
+            k_wgrad<5><<<grid, TB, 0, st>>>(Y.n, gy, Y.c, Y.h, Y.w, V(T, o.a), A.c, A.h, A.w, o.k, o.s, dk);
+        }
+        if (float* db = PG(T, o.pb)) k_chsum<<<Y.c, TB, 0, st>>>(Y.n, Y.c, Y.h * Y.w, gy, db);
+        if (float* dx = G(T, o.a)) {  // dx += conv^T(dy; K)
+          const dim3 g((A.h * A.w + TB - 1) / TB, (A.c + CO - 1) / CO, A.n);
+          k_convT_fwd<<<g, TB, 0, st>>>(gy, Y.c, Y.h, Y.w, PV(T, o.pk), nullptr, A.c, o.k, o.s, A.h, A.w, dx);
+        }
+        break;
+      }
+      case OP_CONVT: {
+        // dK[a, c] += sum u[a] dz[c] (shifted); du += conv(dz; K viewed as (a, c))
+        if (float* dk = PG(T, o.pk)) {
+          const int grid = A.c * Y.c;
+          if (o.k <= 3)
+            k_wgrad<3><<<grid, TB, 0, st>>>(A.n, V(T, o.a), A.c, A.h, A.w, gy, Y.c, Y.h, Y.w, o.k, o.s, dk);
+          else
+            k_wgrad<5><<<grid, TB, 0, st>>>(A.n, V(T, o.a), A.c, A.h, A.w, gy, Y.c, Y.h, Y.w, o.k, o.s, dk);
+        }
+        if (float* db = PG(T, o.pb)) k_chsum<<<Y.c, TB, 0, st>>>(Y.n, Y.c, Y.h * Y.w, gy, db);
+        if (float* dx = G(T, o.a)) {
+          // the conv kernel writes its output: run it into scratch, then accumulate
+          T.tmp.ensure(A.size());
+          float* tmp = T.tmp.p;
+          const dim3 g((A.h * A.w + TB - 1) / TB, (A.c + CO - 1) / CO, A.n);
+          k_conv_fwd<<<g, TB, 0, st>>>(gy, Y.c, Y.h, Y.w, PV(T, o.pk), nullptr, A.c, o.k, o.s, A.h, A.w, tmp);
+          k_acc<<<egrid(A.size()), TB, 0, st>>>(A.size(), tmp, dx);
+        }
+        break;
+      }
+      case OP_BN:
+        k_bn_bwd<<<A.c, TB, 0, st>>>(A.n, A.c, A.h * A.w, V(T, o.a), gy, T.stats.p + o.st, PV(T, o.pbn), o.train ? 1 : 0,
+                                     PG(T, o.pbn), PG(T, o.pbn + 1), G(T, o.a));
+        break;
+      case OP_ELU:
+        if (float* gx = G(T, o.a)) k_elu_bwd<<<egrid(A.size()), TB, 0, st>>>(A.size(), V(T, o.a), V(T, o.y), gy, gx);
+        break;
+      case OP_ADD:
+        if (float* ga = G(T, o.a)) k_acc<<<egrid(A.size()), TB, 0, st>>>(A.size(), gy, ga);
+        if (float* gb = G(T, o.b)) k_acc<<<egrid(A.size()), TB, 0, st>>>(A.size(), gy, gb);
+        break;
+      case OP_CONCAT: {
+        const Ten& Bt = T.tens[size_t(o.b)];
+        float* ga = G(T, o.a);
+        float* gb = o.bcast_b ? nullptr : G(T, o.b);
+        if (ga || gb)
+          k_concat_bwd<<<egrid(Y.size()), TB, 0, st>>>(A.n, size_t(A.c) * A.h * A.w, size_t(Bt.c) * Bt.h * Bt.w, gy, ga,
+                                                       gb);
+        break;
+      }
+    }
+    HB_CUDA(cudaGetLastError());
+  }
+}
+
+// run_batch (inc/training.hpp:121-147) on host NCHW inputs; returns the loss
+double run_batch(Context& c, int B, int H, int W, const float* input, const float* kappa, const float* target,
+                 bool train, bool with_grad, float* out_host) {
+  PaperState& P = paper_state(c);
+  TrainState& T = tstate(c);
+  ensure_params(c);
+  const int mode = P.variant == 0 ? 0 : (T.frozen.empty() ? 1 : 2);
+  build_tape(c, B, H, W, mode, train);
+  cudaStream_t st = c.stream;
+  HB_CUDA(cudaMemcpyAsync(V(T, T.t_input), input, sizeof(float) * size_t(B) * 4 * H * W, cudaMemcpyHostToDevice, st));
+  HB_CUDA(cudaMemcpyAsync(V(T, T.t_target), target, sizeof(float) * size_t(B) * 2 * H * W, cudaMemcpyHostToDevice, st));
+  if (mode == 1) {
+    if (!kappa) throw HbError{HB_ERR_ARG, "encoder_solver training needs the kappa^2 batch"};
+    HB_CUDA(cudaMemcpyAsync(V(T, T.t_kappa), kappa, sizeof(float) * size_t(B) * H * W, cudaMemcpyHostToDevice, st));
+  }
+  if (mode == 2)
+    for (size_t l = 0; l < T.frozen.size(); ++l)
+      HB_CUDA(cudaMemcpyAsync(V(T, T.t_feats[l]), T.frozen[l].data(), sizeof(float) * T.frozen[l].size(),
+                              cudaMemcpyHostToDevice, st));
+  run_forward(c);
+  const Ten& O = T.tens[size_t(T.t_out)];
+  if (with_grad) {
+    HB_CUDA(cudaMemsetAsync(T.grads.p, 0, sizeof(float) * T.arena, st));
+    HB_CUDA(cudaMemsetAsync(T.dgrad.p, 0, sizeof(float) * T.ptotal, st));
+  }
+  k_mse<<<1, TB, 0, st>>>(O.size(), O.n, V(T, T.t_out), V(T, T.t_target), T.dloss.p, with_grad ? G(T, T.t_out) : nullptr);
+  HB_CUDA(cudaGetLastError());
+  if (with_grad) run_backward(c);
+  double loss = 0;
+  HB_CUDA(cudaMemcpyAsync(&loss, T.dloss.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out_host) HB_CUDA(cudaMemcpyAsync(out_host, V(T, T.t_out), sizeof(float) * O.size(), cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaStreamSynchronize(st));
+  return loss;
+}
+
+// adam_step (inc/adam.hpp:25-58) over the trainable parameters; false = skipped
+bool adam_step(Context& c, double lr) {
+  PaperState& P = paper_state(c);
+  TrainState& T = tstate(c);
+  cudaStream_t st = c.stream;
+  if (!T.adam_init) {
+    T.adam_m.ensure(T.ptotal);
+    T.adam_v.ensure(T.ptotal);
+    HB_CUDA(cudaMemsetAsync(T.adam_m.p, 0, sizeof(float) * T.ptotal, st));
+    HB_CUDA(cudaMemsetAsync(T.adam_v.p, 0, sizeof(float) * T.ptotal, st));
+    T.adam_init = true;
+    T.adam_step = 0;
+  }
+  HB_CUDA(cudaMemsetAsync(T.dbad.p, 0, sizeof(int), st));
+  for (size_t i = 0; i < P.params.size(); ++i)
+    if (T.trainable[i])
+      k_nonfinite<<<egrid(P.params[i].size()), TB, 0, st>>>(P.params[i].size(), PG(T, int(i)), T.dbad.p);
+  int bad = 0;
+  HB_CUDA(cudaMemcpyAsync(&bad, T.dbad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  HB_CUDA(cudaStreamSynchronize(st));
+  if (bad) {
+    ++T.adam_skipped;
+    return false;
+  }
+  T.adam_step += 1;
+  const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  const double bc1 = 1.0 - std::pow(b1, double(T.adam_step)), bc2 = 1.0 - std::pow(b2, double(T.adam_step));
+  for (size_t i = 0; i < P.params.size(); ++i) {
+    if (!T.trainable[i]) continue;
+    const size_t n = P.params[i].size(), o = T.poff[i];
+    k_adam<<<egrid(n), TB, 0, st>>>(n, T.dgrad.p + o, T.adam_m.p + o, T.adam_v.p + o, T.dparam.p + o, lr, b1, b2, bc1,
+                                    bc2, eps);
+  }
+  HB_CUDA(cudaGetLastError());
+  return true;
+}
+
+void snapshot(Context& c) {
+  TrainState& T = tstate(c);
+  T.snapshot.ensure(T.ptotal);
+  HB_CUDA(cudaMemcpyAsync(T.snapshot.p, T.dparam.p, sizeof(float) * T.ptotal, cudaMemcpyDeviceToDevice, c.stream));
+}
+void restore(Context& c) {
+  TrainState& T = tstate(c);
+  HB_CUDA(cudaMemcpyAsync(T.dparam.p, T.snapshot.p, sizeof(float) * T.ptotal, cudaMemcpyDeviceToDevice, c.stream));
+}
+
+// per-sample relative error (traindet::accumulate_rel_errors)
+void acc_rel(const std::vector<float>& out, const float* target, int B, size_t slab, double& sum, size_t& count) {
+  for (int b = 0; b < B; ++b) {
+    double num = 0, den = 0;
+    for (size_t i = 0; i < slab; ++i) {
+      const double d = double(out[size_t(b) * slab + i]) - target[size_t(b) * slab + i];
+      num += d * d;
+      den += double(target[size_t(b) * slab + i]) * target[size_t(b) * slab + i];
+    }
+    sum += std::sqrt(num) / (std::sqrt(den) + 1e-30);
+    ++count;
+  }
+}
+
+// in-memory dataset (Dataset of TrainingSamples, inc/datagen.hpp:179-183,330-339)
+struct DS {
+  int H, W;
+  const float* r_hat;   // [N][2][H][W]
+  const float* e_true;  // [N][2][H][W]
+  const int* model;     // [N]
+  const double* kappa2; // [M][H][W] (row-major y, x)
+  const double* gamma;
+};
+
+// traindet::assemble_batch (inc/training.hpp:61-87)
+void assemble(const DS& ds, const std::vector<int>& idx, size_t lo, size_t hi, std::vector<float>& in,
+              std::vector<float>& tg, std::vector<float>& kp) {
+  const int B = int(hi - lo), H = ds.H, W = ds.W;
+  const size_t pl = size_t(H) * W;
+  in.assign(size_t(B) * 4 * pl, 0.f);
+  tg.assign(size_t(B) * 2 * pl, 0.f);
+  kp.assign(size_t(B) * pl, 0.f);
+  for (int b = 0; b < B; ++b) {
+    const int s = idx[lo + size_t(b)];
+    const int m = ds.model[s];
+    const float* r = ds.r_hat + size_t(s) * 2 * pl;
+    const float* e = ds.e_true + size_t(s) * 2 * pl;
+    for (size_t q = 0; q < pl; ++q) {
+      in[(size_t(b) * 4 + 0) * pl + q] = r[q];
+      in[(size_t(b) * 4 + 1) * pl + q] = r[pl + q];
+      in[(size_t(b) * 4 + 2) * pl + q] = float(ds.kappa2[size_t(m) * pl + q]);
+      in[(size_t(b) * 4 + 3) * pl + q] = float(ds.gamma[size_t(m) * pl + q]);
+      tg[(size_t(b) * 2 + 0) * pl + q] = e[q];
+      tg[(size_t(b) * 2 + 1) * pl + q] = e[pl + q];
+      kp[size_t(b) * pl + q] = float(ds.kappa2[size_t(m) * pl + q]);
+    }
+  }
+}
+
+// schedule_at (inc/training.hpp:22-39)
+std::pair<double, int> schedule_at(int epoch, const hb_train_cfg& cfg) {
+  int drops = 0;
+  double anchor = cfg.t0, gap = cfg.t0 / 2.0;
+  while (epoch > anchor) {
+    ++drops;
+    anchor += std::max(1.0, std::round(gap));
+    gap /= 2.0;
+  }
+  double lr = cfg.lr0;
+  long long batch = cfg.batch0;
+  for (int i = 0; i < drops; ++i) {
+    lr /= 10.0;
+    if (batch < (1 << 20)) batch *= 2;
+  }
+  return {lr, int(batch)};
+}
+
+struct Hist {
+  double* out;  // [cap][4]: train rel error, val rel error, lr, batch
+  int cap, n = 0;
+  void push(double tr, double va, double lr, int batch) {
+    if (n < cap && out) {
+      out[n * 4 + 0] = tr;
+      out[n * 4 + 1] = va;
+      out[n * 4 + 2] = lr;
+      out[n * 4 + 3] = batch;
+    }
+    ++n;
+  }
+};
+
+void set_trainable_prefix(Context& c, const std::string& prefix, bool on) {
+  PaperState& P = paper_state(c);
+  TrainState& T = tstate(c);
+  ensure_params(c);
+  for (size_t i = 0; i < P.params.size(); ++i)
+    if (P.params[i].name.compare(0, prefix.size(), prefix) == 0 && !is_buffer(P.params[i].name))
+      T.trainable[i] = on ? 1 : 0;
+}
+
+// encoder_forward in eval mode (inc/unet.hpp:276-283) -> frozen features
+void freeze_features(Context& c, const std::vector<float>& kappa, int H, int W) {
+  TrainState& T = tstate(c);
+  PaperState& P = paper_state(c);
+  ensure_params(c);
+  T.frozen.clear();
+  build_tape(c, 1, H, W, 3, false);
+  HB_CUDA(cudaMemcpyAsync(V(T, T.t_kappa), kappa.data(), sizeof(float) * kappa.size(), cudaMemcpyHostToDevice,
+                          c.stream));
+  run_forward(c);
+  std::vector<std::vector<float>> f;
+  std::vector<std::array<int, 3>> dims;
+  for (int t : T.t_feats) {
+    const Ten& F = T.tens[size_t(t)];
+    std::vector<float> h(F.size());
+    HB_CUDA(cudaMemcpyAsync(h.data(), V(T, t), sizeof(float) * F.size(), cudaMemcpyDeviceToHost, c.stream));
+    f.push_back(std::move(h));
+    dims.push_back({F.c, F.h, F.w});
+  }
+  HB_CUDA(cudaStreamSynchronize(c.stream));
+  T.frozen = std::move(f);
+  T.frozen_dims = std::move(dims);
+  T.key_B = -1;
+  (void)P;
+}
+
+// train() (inc/training.hpp:152-227)
+int train_loop(Context& c, const hb_train_cfg& cfg, const DS& ds, int N, Hist& hist, int* aborted) {
+  TrainState& T = tstate(c);
+  ensure_params(c);
+  Rng rng(cfg.seed);
+  std::vector<int> order(static_cast<size_t>(N));
+  std::iota(order.begin(), order.end(), 0);
+  for (size_t i = order.size(); i > 1; --i) std::swap(order[i - 1], order[size_t(rng.uniform_int(0, int64_t(i) - 1))]);
+  const size_t val_count = size_t(double(order.size()) * cfg.val_fraction);
+  std::vector<int> val_idx(order.begin(), order.begin() + long(val_count));
+  std::vector<int> train_idx(order.begin() + long(val_count), order.end());
+  if (train_idx.empty()) throw HbError{HB_ERR_ARG, "no training samples after split"};
+  T.adam_init = false;
+  bool have_good = false;
+  std::vector<float> in, tg, kp, out;
+  const size_t slab = size_t(2) * ds.H * ds.W;
+  *aborted = 0;
+  for (int epoch = 1; epoch <= cfg.epochs; ++epoch) {
+    auto [lr, batch] = schedule_at(epoch, cfg);
+    batch = std::min<int>(batch, int(train_idx.size()));
+    for (size_t i = train_idx.size(); i > 1; --i)
+      std::swap(train_idx[i - 1], train_idx[size_t(rng.uniform_int(0, int64_t(i) - 1))]);
+    double rel_sum = 0;
+    size_t rel_count = 0;
+    bool finite = true;
+    for (size_t lo = 0; lo < train_idx.size(); lo += size_t(batch)) {
+      const size_t hi = std::min(lo + size_t(batch), train_idx.size());
+      assemble(ds, train_idx, lo, hi, in, tg, kp);
+      out.resize(size_t(hi - lo) * slab);
+      const double loss = run_batch(c, int(hi - lo), ds.H, ds.W, in.data(), kp.data(), tg.data(), true, true, out.data());
+      if (!std::isfinite(loss)) {
+        finite = false;
+        break;
+      }
+      adam_step(c, lr);
+      acc_rel(out, tg.data(), int(hi - lo), slab, rel_sum, rel_count);
+    }
+    if (!finite) {
+      *aborted = 1;
+      if (have_good) restore(c);
+      break;
+    }
+    double val_sum = 0;
+    size_t val_n = 0;
+    for (size_t lo = 0; lo < val_idx.size(); lo += size_t(batch)) {
+      const size_t hi = std::min(lo + size_t(batch), val_idx.size());
+      assemble(ds, val_idx, lo, hi, in, tg, kp);
+      out.resize(size_t(hi - lo) * slab);
+      run_batch(c, int(hi - lo), ds.H, ds.W, in.data(), kp.data(), tg.data(), false, false, out.data());
+      acc_rel(out, tg.data(), int(hi - lo), slab, val_sum, val_n);
+    }
+    hist.push(rel_count ? rel_sum / double(rel_count) : 0.0, val_n ? val_sum / double(val_n) : 0.0, lr, batch);
+    snapshot(c);
+    have_good = true;
+  }
+  params_to_host(c);
+  return hist.n;
+}
+
+// retrain() (inc/training.hpp:229-298): n_pairs fresh samples of the context's
+// problem (gen_sample_pair seeds seed * 6151 + i, on the device hierarchy),
+// lr0 / 10, batch min(20, n), no schedule, no validation; encoder_solver: the
+// encoder frozen and evaluated once
+int retrain_loop(Context& c, int n_pairs, int epochs, const hb_train_cfg& base, uint64_t seed, Hist& hist,
+                 int* aborted) {
+  TrainState& T = tstate(c);
+  PaperState& P = paper_state(c);
+  *aborted = 0;
+  if (epochs == 0 || n_pairs == 0) return 0;
+  ensure_params(c);
+  const int H = c.ny, W = c.nx;
+  const size_t pl = size_t(H) * W;
+  std::vector<uint64_t> seeds(static_cast<size_t>(n_pairs));
+  for (int i = 0; i < n_pairs; ++i) seeds[size_t(i)] = seed * 6151ULL + uint64_t(i);
+  std::vector<double> r(size_t(n_pairs) * pl * 2), e(size_t(n_pairs) * pl * 2);
+  const int rc = hb_gen_sample_pairs(reinterpret_cast<hb_ctx*>(&c), n_pairs, seeds.data(), -1, 10, r.data(), e.data(), nullptr);
+  if (rc != HB_OK) throw HbError{rc, c.err};
+  // quantize_sample (inc/datagen.hpp:290-305): r_hat = float(h^2 r), e_true = float(e)
+  const double h2 = c.h * c.h;
+  std::vector<float> rh(size_t(n_pairs) * 2 * pl), et(size_t(n_pairs) * 2 * pl);
+  for (int s = 0; s < n_pairs; ++s)
+    for (size_t q = 0; q < pl; ++q) {
+      const double* rq = r.data() + (size_t(s) * pl + q) * 2;
+      const double* eq = e.data() + (size_t(s) * pl + q) * 2;
+      rh[(size_t(s) * 2 + 0) * pl + q] = float(h2 * rq[0]);
+      rh[(size_t(s) * 2 + 1) * pl + q] = float(h2 * rq[1]);
+      et[(size_t(s) * 2 + 0) * pl + q] = float(eq[0]);
+      et[(size_t(s) * 2 + 1) * pl + q] = float(eq[1]);
+    }
+  std::vector<int> model(static_cast<size_t>(n_pairs), 0);
+  DS ds{H, W, rh.data(), et.data(), model.data(), c.k2.data(), c.gam.data()};
+  const bool es = base.encoder_solver != 0;
+  if (es) {
+    std::vector<float> kap(pl);
+    for (size_t q = 0; q < pl; ++q) kap[q] = float(c.k2[q]);
+    freeze_features(c, kap, H, W);
+    set_trainable_prefix(c, "enc.", false);
+  }
+  Rng rng(seed);
+  std::vector<int> idx(static_cast<size_t>(n_pairs));
+  std::iota(idx.begin(), idx.end(), 0);
+  const double lr = base.lr0 / 10.0;
+  const int batch = std::min<int>(20, n_pairs);
+  T.adam_init = false;
+  snapshot(c);
+  std::vector<float> in, tg, kp, out;
+  const size_t slab = 2 * pl;
+  for (int epoch = 1; epoch <= epochs; ++epoch) {
+    for (size_t i = idx.size(); i > 1; --i) std::swap(idx[i - 1], idx[size_t(rng.uniform_int(0, int64_t(i) - 1))]);
+    double rel_sum = 0;
+    size_t rel_count = 0;
+    bool finite = true;
+    for (size_t lo = 0; lo < idx.size(); lo += size_t(batch)) {
+      const size_t hi = std::min(lo + size_t(batch), idx.size());
+      assemble(ds, idx, lo, hi, in, tg, kp);
+      out.resize(size_t(hi - lo) * slab);
+      const double loss = run_batch(c, int(hi - lo), H, W, in.data(), kp.data(), tg.data(), true, true, out.data());
+      if (!std::isfinite(loss)) {
+        finite = false;
+        break;
+      }
+      adam_step(c, lr);
+      acc_rel(out, tg.data(), int(hi - lo), slab, rel_sum, rel_count);
+    }
+    if (!finite) {
+      *aborted = 1;
+      restore(c);
+      break;
+    }
+    hist.push(rel_count ? rel_sum / double(rel_count) : 0.0, 0.0, lr, batch);
+    snapshot(c);
+  }
+  if (es) {
+    set_trainable_prefix(c, "enc.", true);
+    T.frozen.clear();
+    T.key_B = -1;
+  }
+  params_to_host(c);
+  (void)P;
+  return hist.n;
+}
+
+}  // namespace
+
+}  // namespace hb
+
+// ===================================================================== C ABI
+using namespace hb;
+struct hb_ctx : hb::Context {};
+
+#define HB_API_BEGIN \
+  if (!ctx) return HB_ERR_ARG; \
+  try {
+#define HB_API_END                  \
+  return HB_OK;                     \
+  }                                 \
+  catch (const HbError& e) {        \
+    ctx->err = e.msg;               \
+    return e.code;                  \
+  }                                 \
+  catch (const std::exception& e) { \
+    ctx->err = e.what();            \
+    return HB_ERR_ARG;              \
+  }
+
+extern "C" {
+
+int hb_paper_train_batch(hb_ctx* ctx, int batch, int H, int W, const float* input, const float* kappa,
+                         const float* target, int train_mode, int with_grad, int step, double lr, double* loss,
+                         float* out) {
+  HB_API_BEGIN
+  if (batch < 1 || H < 1 || W < 1 || !input || !target) throw HbError{HB_ERR_ARG, "bad batch"};
+  if (step && !with_grad) throw HbError{HB_ERR_ARG, "an ADAM step needs gradients"};
+  const double l = run_batch(*ctx, batch, H, W, input, kappa, target, train_mode != 0, with_grad != 0, out);
+  if (loss) *loss = l;
+  if (step) adam_step(*ctx, lr);
+  params_to_host(*ctx);
+  HB_API_END
+}
+
+int64_t hb_paper_trainable_count(hb_ctx* ctx) {
+  if (!ctx || !ctx->paper) return 0;
+  try {
+    ensure_params(*ctx);
+  } catch (...) {
+    return 0;
+  }
+  int64_t n = 0;
+  for (size_t i = 0; i < ctx->paper->params.size(); ++i)
+    if (ctx->train->trainable[i]) n += int64_t(ctx->paper->params[i].size());
+  return n;
+}
+
+int hb_paper_grads(hb_ctx* ctx, int64_t count, float* grads) {
+  HB_API_BEGIN
+  ensure_params(*ctx);
+  PaperState& P = paper_state(*ctx);
+  TrainState& T = tstate(*ctx);
+  if (count != hb_paper_trainable_count(ctx) || !grads) throw HbError{HB_ERR_ARG, "gradient count mismatch"};
+  std::vector<float> h(T.ptotal);
+  HB_CUDA(cudaMemcpy(h.data(), T.dgrad.p, sizeof(float) * T.ptotal, cudaMemcpyDeviceToHost));
+  size_t o = 0;
+  for (size_t i = 0; i < P.params.size(); ++i)
+    if (T.trainable[i]) {
+      std::copy(h.begin() + long(T.poff[i]), h.begin() + long(T.poff[i] + P.params[i].size()), grads + o);
+      o += P.params[i].size();
+    }
+  HB_API_END
+}
+
+int hb_paper_set_trainable_prefix(hb_ctx* ctx, const char* prefix, int trainable) {
+  HB_API_BEGIN
+  if (!prefix) throw HbError{HB_ERR_ARG, "null prefix"};
+  set_trainable_prefix(*ctx, prefix, trainable != 0);
+  HB_API_END
+}
+
+int hb_paper_adam_reset(hb_ctx* ctx) {
+  HB_API_BEGIN
+  tstate(*ctx).adam_init = false;
+  HB_API_END
+}
+
+int hb_paper_train(hb_ctx* ctx, const hb_train_cfg* cfg, int count, int H, int W, const float* r_hat,
+                   const float* e_true, const int* model_id, int models, const double* kappa2, const double* gamma,
+                   double* hist, int hist_cap, int* epochs_run, int* aborted) {
+  HB_API_BEGIN
+  if (!cfg || count < 1 || !r_hat || !e_true || !model_id || models < 1 || !kappa2 || !gamma)
+    throw HbError{HB_ERR_ARG, "bad dataset"};
+  for (int s = 0; s < count; ++s)
+    if (model_id[s] < 0 || model_id[s] >= models) throw HbError{HB_ERR_ARG, "model id out of range"};
+  PaperState& P = paper_state(*ctx);
+  if ((cfg->encoder_solver != 0) != (P.variant == 1)) throw HbError{HB_ERR_ARG, "encoder_solver does not match the net"};
+  tstate(*ctx).frozen.clear();
+  DS ds{H, W, r_hat, e_true, model_id, kappa2, gamma};
+  Hist h{hist, hist_cap};
+  int ab = 0;
+  train_loop(*ctx, *cfg, ds, count, h, &ab);
+  if (epochs_run) *epochs_run = h.n;
+  if (aborted) *aborted = ab;
+  HB_API_END
+}
+
+int hb_paper_retrain(hb_ctx* ctx, int n_pairs, int epochs, const hb_train_cfg* base, uint64_t seed, double* hist,
+                     int hist_cap, int* epochs_run, int* aborted) {
+  HB_API_BEGIN
+  if (!base || n_pairs < 0 || epochs < 0) throw HbError{HB_ERR_ARG, "bad retrain arguments"};
+  if (!ctx->has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built (hb_build_hierarchy)"};
+  PaperState& P = paper_state(*ctx);
+  if ((base->encoder_solver != 0) != (P.variant == 1)) throw HbError{HB_ERR_ARG, "encoder_solver does not match the net"};
+  Hist h{hist, hist_cap};
+  int ab = 0;
+  retrain_loop(*ctx, n_pairs, epochs, *base, seed, h, &ab);
+  if (epochs_run) *epochs_run = h.n;
+  if (aborted) *aborted = ab;
+  HB_API_END
+}
+
+}  // extern "C"

@@ -49,6 +49,11 @@ class _UNetCfg(C.Structure):
                 ("bottleneck_resnets", C.c_int), ("updown_kernel", C.c_int), ("res_kernel", C.c_int)]
 
 
+class _TrainCfg(C.Structure):  # hb_train_cfg (TrainConfig, inc/training.hpp:12-20)
+    _fields_ = [("epochs", C.c_int), ("lr0", C.c_double), ("batch0", C.c_int), ("t0", C.c_int),
+                ("val_fraction", C.c_double), ("encoder_solver", C.c_int), ("seed", C.c_uint64)]
+
+
 class _KrylovCfg(C.Structure):
     _fields_ = [("restart", C.c_int), ("max_iters", C.c_int), ("rel_tol", C.c_double), ("flexible", C.c_int)]
 
@@ -105,6 +110,17 @@ def lib():
         L.hb_save_checkpoint.argtypes = [_vp, C.c_char_p, C.c_char_p]
         L.hb_paper_forward.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp]
         L.hb_gen_sample_pairs.argtypes = [_vp, C.c_int, C.POINTER(C.c_uint64), C.c_int, C.c_int, _dp, _dp, _ip]
+        L.hb_paper_train_batch.argtypes = [_vp, C.c_int, C.c_int, C.c_int, _fp, _fp, _fp, C.c_int, C.c_int, C.c_int,
+                                           C.c_double, _dp, _fp]
+        L.hb_paper_trainable_count.argtypes = [_vp]
+        L.hb_paper_trainable_count.restype = C.c_int64
+        L.hb_paper_grads.argtypes = [_vp, C.c_int64, _fp]
+        L.hb_paper_set_trainable_prefix.argtypes = [_vp, C.c_char_p, C.c_int]
+        L.hb_paper_adam_reset.argtypes = [_vp]
+        L.hb_paper_train.argtypes = [_vp, C.POINTER(_TrainCfg), C.c_int, C.c_int, C.c_int, _fp, _fp, _ip, C.c_int,
+                                     _dp, _dp, _dp, C.c_int, _ip, _ip]
+        L.hb_paper_retrain.argtypes = [_vp, C.c_int, C.c_int, C.POINTER(_TrainCfg), C.c_uint64, _dp, C.c_int, _ip,
+                                       _ip]
         L.hb_write_slw1.argtypes = [C.c_char_p, C.c_int, C.c_int, _dp]
         L.hb_read_slw1.argtypes = [C.c_char_p, _ip, _ip, _dp]
         L.hb_slab_partition.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _ip, _ip]
@@ -174,6 +190,36 @@ class UNetConfig:  # inc/unet.hpp:113-120 (the paper's network)
 
 
 NET_VARIANT = {"standalone": 0, "encoder_solver": 1}  # NetVariant, inc/precond.hpp:55
+
+
+@dataclasses.dataclass
+class TrainConfig:  # inc/training.hpp:12-20
+    epochs: int = 40
+    lr0: float = 1e-4
+    batch0: int = 20
+    t0: int = 48
+    val_fraction: float = 0.1
+    encoder_solver: bool = False
+    seed: int = 1
+
+    def _c(self):
+        return _TrainCfg(self.epochs, self.lr0, self.batch0, self.t0, self.val_fraction, int(self.encoder_solver),
+                         self.seed)
+
+
+@dataclasses.dataclass
+class TrainHistory:  # inc/training.hpp:48-59
+    epochs: list  # [(epoch, mean_rel_error_train, mean_rel_error_val, lr, batch)]
+    aborted_non_finite: bool = False
+
+    def write_csv(self, f):
+        f.write("epoch,mean_rel_error_train,mean_rel_error_val,lr,batch\n")
+        for e in self.epochs:
+            f.write(f"{e[0]},{_g6(e[1])},{_g6(e[2])},{_g6(e[3])},{e[4]}\n")
+
+
+def _g6(x):  # std::ostream default (6 significant digits)
+    return f"{x:.6g}"
 
 
 @dataclasses.dataclass
@@ -320,6 +366,61 @@ class Context:
         y = np.zeros((B, 2, H, W), np.float32)
         self._check(lib().hb_paper_forward(self.h, B, H, W, _p(x, _fp), _p(y, _fp)))
         return y
+
+    # training (inc/training.hpp:121-298, inc/adam.hpp:25-58) on the device
+    def paper_train_batch(self, x, target, kappa=None, train_mode=True, with_grad=True, step=False, lr=1e-4):
+        """run_batch (+ adam_step): x [B][4][H][W], target [B][2][H][W] -> (loss, out)"""
+        x = np.ascontiguousarray(x, np.float32)
+        t = np.ascontiguousarray(target, np.float32)
+        k = None if kappa is None else np.ascontiguousarray(kappa, np.float32)
+        B, _, H, W = x.shape
+        out = np.zeros((B, 2, H, W), np.float32)
+        loss = C.c_double()
+        self._check(lib().hb_paper_train_batch(self.h, B, H, W, _p(x, _fp), _p(k, _fp) if k is not None else None,
+                                               _p(t, _fp), int(train_mode), int(with_grad), int(step), lr,
+                                               C.byref(loss), _p(out, _fp)))
+        return loss.value, out
+
+    def paper_grads(self):
+        """the last batch's trainable gradients {name: array} (registry order)"""
+        n = lib().hb_paper_trainable_count(self.h)
+        g = np.zeros(n, np.float32)
+        self._check(lib().hb_paper_grads(self.h, n, _p(g, _fp)))
+        return g
+
+    def paper_set_trainable_prefix(self, prefix: str, trainable: bool):
+        self._check(lib().hb_paper_set_trainable_prefix(self.h, prefix.encode(), int(trainable)))
+
+    def paper_adam_reset(self):
+        self._check(lib().hb_paper_adam_reset(self.h))
+
+    @staticmethod
+    def _hist(h, n, ab):
+        return TrainHistory([(i + 1, h[i, 0], h[i, 1], h[i, 2], int(h[i, 3])) for i in range(n)], bool(ab))
+
+    def paper_train(self, cfg: TrainConfig, r_hat, e_true, model_id, kappa2, gamma) -> TrainHistory:
+        """train() over an in-memory dataset (quantized samples, per-model kappa2 / gamma)"""
+        r = np.ascontiguousarray(r_hat, np.float32)
+        e = np.ascontiguousarray(e_true, np.float32)
+        m = np.ascontiguousarray(model_id, np.int32)
+        k2 = np.ascontiguousarray(kappa2, np.float64)
+        g = np.ascontiguousarray(gamma, np.float64)
+        N, _, H, W = r.shape
+        h = np.zeros((max(cfg.epochs, 1), 4))
+        n, ab = C.c_int(), C.c_int()
+        c = cfg._c()
+        self._check(lib().hb_paper_train(self.h, C.byref(c), N, H, W, _p(r, _fp), _p(e, _fp), _p(m, _ip), k2.shape[0],
+                                         _p(k2), _p(g), _p(h), h.shape[0], C.byref(n), C.byref(ab)))
+        return self._hist(h, n.value, ab.value)
+
+    def paper_retrain(self, n_pairs: int, epochs: int, base: TrainConfig, seed: int) -> TrainHistory:
+        """retrain() on this context's problem (inc/training.hpp:229-298)"""
+        h = np.zeros((max(epochs, 1), 4))
+        n, ab = C.c_int(), C.c_int()
+        c = base._c()
+        self._check(lib().hb_paper_retrain(self.h, n_pairs, epochs, C.byref(c), seed, _p(h), h.shape[0], C.byref(n),
+                                           C.byref(ab)))
+        return self._hist(h, n.value, ab.value)
 
     def encode(self):
         self._check(lib().hb_encode(self.h))

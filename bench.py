@@ -454,9 +454,10 @@ def run_ours(args, ws, rank, local):
             if nm == "c4slab":
                 line["also"][nm] = slab
                 continue
-            if nm in ("datagen", "paper_ju"):
+            if nm in ("datagen", "paper_ju", "train"):
                 try:
-                    line["also"][nm] = (datagen_budget if nm == "datagen" else paper_ju_budget)(local, args)
+                    fn = {"datagen": datagen_budget, "paper_ju": paper_ju_budget, "train": train_budget}[nm]
+                    line["also"][nm] = fn(local, args)
                 except Exception as e:  # reported, not hidden
                     line["also"][nm] = {"error": repr(e)}
                 continue
@@ -615,6 +616,47 @@ def paper_ju_budget(local, args):
     return out
 
 
+def train_budget(local, args):
+    """Training of the paper U-Net: one run_batch (train-
+    mode forward, MSE, reverse sweep) + adam_step per step, UNetConfig()
+    defaults at 128^2 with the paper's retraining batch of 20, through the C
+    ABI (host batch in, host loss / output / weights back every step); against
+    the reference's own run_batch + adam_step on one host thread (one batch)."""
+    import time
+    import torch
+    from paper_2203_11025_b200 import helmgpu as hg
+    n, B, steps = 128, 20, 10
+    rs = np.random.default_rng(0)
+    x = rs.standard_normal((B, 4, n, n)).astype(np.float32)
+    x[:, :2] *= 1e-3
+    t = rs.standard_normal((B, 2, n, n)).astype(np.float32)
+    ctx = hg.Context(local)
+    ctx.set_paper_net(hg.UNetConfig(), "standalone")
+    ctx.paper_init(3)
+    for _ in range(2):
+        ctx.paper_train_batch(x, t, step=True, lr=1e-5)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        loss, _ = ctx.paper_train_batch(x, t, step=True, lr=1e-5)
+    dt = (time.perf_counter() - t0) / steps
+    out = {"grid": n, "batch": B, "net": "UNetConfig() standalone (3 levels, base 16)", "ms_per_batch": dt * 1e3,
+           "samples_per_s": B / dt, "loss": loss,
+           "path": "hb_paper_train_batch (host batch in; loss, output and weights back each step)"}
+    ctx.close()
+    try:
+        from oracle import oracle as O
+        if O.have_ref():
+            net = O.RefPaperNet(levels=3, base=16, rpl=1, bot=3, kud=5, kres=3, variant=0, seed=3)
+            t0 = time.perf_counter()
+            net.train_batch(x, t, step=True, lr=1e-5)
+            dr = time.perf_counter() - t0
+            out["cpu_reference"] = {"ms_per_batch": dr * 1e3, "samples_per_s": B / dr, "cores": 1, "kind": "reference"}
+    except Exception as ex:  # reported, not hidden
+        out["cpu_reference"] = {"error": repr(ex)}
+    return out
+
+
 def slab_budget(local, args, ws, rank):
     """c4 (one 4096^2 RHS, 4-level V-cycle, U-Net coarsest at 512^2) on row slabs
     (SURVEY 8(e)): one slab per rank over NCCL when ws > 1, else an in-process
@@ -674,7 +716,7 @@ def main():
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = one per SM)")
-    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,datagen,paper_ju", help="comma list of configs measured on a fixed iteration budget "
+    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,datagen,paper_ju,train", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")

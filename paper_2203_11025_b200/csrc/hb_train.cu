@@ -18,7 +18,9 @@
 //   kernel gradient       one CTA per (channel pair), thread-strided pixels,
 //                           per-tap fp32 partials, fp64 block reduction
 //   batch norm            fp64 channel statistics (two passes, as the
-//                           reference), normalise; backward fp64 channel sums
+//                           reference), normalise; backward fp64 channel sums;
+//                           every channel reduction is split over (channel,
+//                           slice) CTAs and folded in a fixed order
 //   ELU / add / concat / MSE / ADAM   elementwise (ADAM in fp64 arithmetic)
 // The reductions the reference carries in double (batch-norm statistics, bias
 // and loss sums, ADAM) are double here; convolution sums are fp32 in both
@@ -173,25 +175,6 @@ __global__ void __launch_bounds__(TB) k_wgrad(int nb, const float* __restrict__ 
     }
 }
 
-// per-channel fp64 sum over (batch, plane): out[c] += float(sum)  (bias gradients)
-__global__ void __launch_bounds__(TB) k_chsum(int nb, int C, int plane, const float* __restrict__ g, float* out) {
-  const int c = blockIdx.x;
-  double s = 0;
-  for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
-    const size_t b = i / plane, q = i % plane;
-    s += g[(b * C + c) * plane + q];
-  }
-  __shared__ double red[TB / 32];
-  s = warp_sum(s);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0;
-    for (int i = 0; i < TB / 32; ++i) t += red[i];
-    out[c] += float(t);
-  }
-}
-
 __device__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
@@ -200,38 +183,6 @@ __device__ double block_sum(double v, double* red) {
   for (int i = 0; i < TB / 32; ++i) t += red[i];
   __syncthreads();
   return t;
-}
-
-// batch norm statistics (inc/autodiff.hpp:228-262).  train: biased batch mean /
-// variance in fp64 (two passes), running buffers folded with momentum 0.9 and
-// the update count bumped; eval: the running buffers.  st[c] = (mean_f, inv_std_f)
-__global__ void __launch_bounds__(TB) k_bn_stats(int nb, int C, int plane, const float* __restrict__ x, int train,
-                                                 float eps, float momentum, float* rmean, float* rvar, float* count,
-                                                 float2* st) {
-  const int c = blockIdx.x;
-  __shared__ double red[TB / 32];
-  double mean, var;
-  if (train) {
-    const double cnt = double(nb) * plane;
-    double s = 0;
-    for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) s += x[((i / plane) * C + c) * plane + i % plane];
-    mean = block_sum(s, red) / cnt;
-    s = 0;
-    for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
-      const double d = x[((i / plane) * C + c) * plane + i % plane] - mean;
-      s += d * d;
-    }
-    var = block_sum(s, red) / cnt;
-    if (threadIdx.x == 0) {
-      rmean[c] = momentum * rmean[c] + (1.0f - momentum) * float(mean);
-      rvar[c] = momentum * rvar[c] + (1.0f - momentum) * float(var);
-      if (c == 0) count[0] += 1.0f;
-    }
-  } else {
-    mean = rmean[c];
-    var = rvar[c];
-  }
-  if (threadIdx.x == 0) st[c] = make_float2(float(mean), float(1.0 / sqrt(var + double(eps))));
 }
 
 // y = (x - mu) * is * g + be
@@ -244,40 +195,116 @@ __global__ void k_bn_apply(size_t n, int C, int plane, const float* __restrict__
   }
 }
 
-// batch norm backward (inc/autodiff.hpp:281-318): fp64 channel sums of dy and
-// dy * xhat -> scale / offset gradients, then dx (train: through the batch
-// statistics; eval: g * is * dy)
-__global__ void __launch_bounds__(TB) k_bn_bwd(int nb, int C, int plane, const float* __restrict__ x,
-                                               const float* __restrict__ go, const float2* __restrict__ st,
-                                               const float* __restrict__ g, int train, float* dscale, float* doffset,
-                                               float* dx) {
-  const int c = blockIdx.x;
+
+// ---- split channel reductions: grid (C, S), CTA (c, j) sums slice j of the
+// channel's nb * plane elements into part[c * S + j] (fp64, fixed order), a
+// finishing kernel adds the S partials in order (deterministic)
+enum { RED_SUM = 0, RED_SQDEV = 1, RED_BNBWD = 2 };
+template <int MODE>
+__global__ void __launch_bounds__(TB) k_chpart(int nb, int C, int plane, const float* __restrict__ x,
+                                               const float* __restrict__ go, const double* __restrict__ mean,
+                                               const float2* __restrict__ st, double2* part) {
+  const int c = blockIdx.x, S = gridDim.y, j = blockIdx.y;
+  const size_t n = size_t(nb) * plane, per = (n + S - 1) / S, lo = j * per, hi = min(n, lo + per);
   __shared__ double red[TB / 32];
-  const float mu = st[c].x, is = st[c].y, gc = g[c];
-  double sdy = 0, sdyx = 0;
-  for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
+  double a = 0, b = 0;
+  const double mu64 = MODE == RED_SQDEV ? mean[c] : 0.0;
+  const float mu = MODE == RED_BNBWD ? st[c].x : 0.f, is = MODE == RED_BNBWD ? st[c].y : 0.f;
+  for (size_t i = lo + threadIdx.x; i < hi; i += TB) {
     const size_t o = ((i / plane) * C + c) * plane + i % plane;
-    const double gp = go[o];
-    sdy += gp;
-    sdyx += gp * (x[o] - mu) * is;
-  }
-  sdy = block_sum(sdy, red);
-  sdyx = block_sum(sdyx, red);
-  if (threadIdx.x == 0) {
-    if (dscale) dscale[c] += float(sdyx);
-    if (doffset) doffset[c] += float(sdy);
-  }
-  if (!dx) return;
-  const double cnt = double(nb) * plane, a = sdy / cnt, c2 = sdyx / cnt;
-  for (size_t i = threadIdx.x; i < size_t(nb) * plane; i += TB) {
-    const size_t o = ((i / plane) * C + c) * plane + i % plane;
-    if (train) {
-      const double xhat = double(x[o] - mu) * is;
-      dx[o] += float(double(gc) * is * (go[o] - a - xhat * c2));
+    if (MODE == RED_SUM) {
+      a += x[o];
+    } else if (MODE == RED_SQDEV) {
+      const double d = x[o] - mu64;
+      a += d * d;
     } else {
-      dx[o] += gc * is * go[o];
+      const double gp = go[o];
+      a += gp;
+      b += gp * (x[o] - mu) * is;
     }
   }
+  a = block_sum(a, red);
+  if (MODE == RED_BNBWD) b = block_sum(b, red);
+  if (threadIdx.x == 0) part[size_t(c) * S + j] = make_double2(a, b);
+}
+__device__ __forceinline__ double2 fold(const double2* part, int c, int S) {
+  double2 t = make_double2(0, 0);
+  for (int j = 0; j < S; ++j) {
+    t.x += part[size_t(c) * S + j].x;
+    t.y += part[size_t(c) * S + j].y;
+  }
+  return t;
+}
+// mean[c] = sum / cnt
+__global__ void k_fin_mean(int C, int S, double cnt, const double2* part, double* mean) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) mean[c] = fold(part, c, S).x / cnt;
+}
+// var, running buffers, (mean_f, inv_std_f)
+__global__ void k_fin_var(int C, int S, double cnt, const double2* part, const double* mean, float eps, float momentum,
+                          float* rmean, float* rvar, float* count, float2* st) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double var = fold(part, c, S).x / cnt;
+  rmean[c] = momentum * rmean[c] + (1.0f - momentum) * float(mean[c]);
+  rvar[c] = momentum * rvar[c] + (1.0f - momentum) * float(var);
+  if (c == 0) count[0] += 1.0f;
+  st[c] = make_float2(float(mean[c]), float(1.0 / sqrt(var + double(eps))));
+}
+__global__ void k_bn_eval_stats(int C, float eps, const float* rmean, const float* rvar, float2* st) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) st[c] = make_float2(float(double(rmean[c])), float(1.0 / sqrt(double(rvar[c]) + double(eps))));
+}
+// bias gradients: out[c] += float(sum)
+__global__ void k_fin_sum(int C, int S, const double2* part, float* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < C) out[c] += float(fold(part, c, S).x);
+}
+// batch norm backward: scale / offset gradients and the (sum dy, sum dy xhat) / cnt pairs
+__global__ void k_fin_bnbwd(int C, int S, double cnt, const double2* part, float* dscale, float* doffset,
+                            double2* coef) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double2 t = fold(part, c, S);
+  if (dscale) dscale[c] += float(t.y);
+  if (doffset) doffset[c] += float(t.x);
+  coef[c] = make_double2(t.x / cnt, t.y / cnt);
+}
+__global__ void k_bn_dx(size_t n, int C, int plane, const float* __restrict__ x, const float* __restrict__ go,
+                        const float2* __restrict__ st, const float* __restrict__ g, const double2* __restrict__ coef,
+                        int train, float* dx) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) {
+    const int c = int((i / plane) % C);
+    const float mu = st[c].x, is = st[c].y, gc = g[c];
+    if (train) {
+      const double xhat = double(x[i] - mu) * is;
+      dx[i] += float(double(gc) * is * (go[i] - coef[c].x - xhat * coef[c].y));
+    } else {
+      dx[i] += gc * is * go[i];
+    }
+  }
+}
+// mse: partial sums of (p - t)^2 over slices, then loss = float(sum / nb); gp += 2/nb (p - t)
+__global__ void __launch_bounds__(TB) k_sqdiff_part(size_t n, const float* __restrict__ p, const float* __restrict__ t,
+                                                    double* part) {
+  const size_t per = (n + gridDim.x - 1) / gridDim.x, lo = blockIdx.x * per, hi = min(n, lo + per);
+  __shared__ double red[TB / 32];
+  double s = 0;
+  for (size_t i = lo + threadIdx.x; i < hi; i += TB) {
+    const double d = double(p[i]) - t[i];
+    s += d * d;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+__global__ void k_fin_mse(int S, int nb, const double* part, double* loss) {
+  double s = 0;
+  for (int j = 0; j < S; ++j) s += part[j];
+  *loss = double(float(s / nb));
+}
+__global__ void k_mse_grad(size_t n, int nb, const float* __restrict__ p, const float* __restrict__ t, float* gp) {
+  const float scale = 2.0f * 1.0f / float(nb);
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) gp[i] += scale * (p[i] - t[i]);
 }
 
 __global__ void k_elu(size_t n, const float* __restrict__ x, float* __restrict__ y) {
@@ -316,21 +343,6 @@ __global__ void k_concat_bwd(int nb, size_t sa, size_t sb, const float* __restri
       gb[bi * sb + q - sa] += go[i];
     }
   }
-}
-// mse (inc/autodiff.hpp:448-470): loss = sum (p - t)^2 / n in fp64; gp += 2 / n (p - t)
-__global__ void __launch_bounds__(TB) k_mse(size_t n, int nb, const float* __restrict__ p, const float* __restrict__ t,
-                                            double* loss, float* gp) {
-  __shared__ double red[TB / 32];
-  double s = 0;
-  for (size_t i = threadIdx.x; i < n; i += TB) {
-    const double d = double(p[i]) - t[i];
-    s += d * d;
-  }
-  s = block_sum(s, red);
-  if (threadIdx.x == 0) *loss = double(float(s / nb));
-  if (!gp) return;
-  const float scale = 2.0f * 1.0f / float(nb);
-  for (size_t i = threadIdx.x; i < n; i += TB) gp[i] += scale * (p[i] - t[i]);
 }
 // non-finite count over a buffer
 __global__ void k_nonfinite(size_t n, const float* __restrict__ g, int* bad) {
@@ -392,7 +404,8 @@ struct TrainState {
   size_t arena = 0, nstats = 0;
   DBuf<float> vals, grads, tmp;
   DBuf<float2> stats;
-  DBuf<double> dloss;
+  DBuf<double> dloss, dmean;
+  DBuf<double2> dpart, dcoef;
   DBuf<int> dbad;
   // frozen encoder features (batch 1) for retrain
   std::vector<std::vector<float>> frozen;  // per level, NCHW [1][C][H>>l][W>>l]
@@ -647,6 +660,59 @@ float* PV(TrainState& T, int i) { return T.dparam.p + T.poff[size_t(i)]; }
 float* PG(TrainState& T, int i) { return T.trainable[size_t(i)] ? T.dgrad.p + T.poff[size_t(i)] : nullptr; }
 int egrid(size_t n) { return nblk(n); }
 
+// slices per channel so that C * S CTAs fill the GPU (>= 2048 elements per slice)
+int split_s(const Context& c, int C, size_t per_channel) {
+  const size_t want = (size_t(4) * c.num_sms + size_t(C) - 1) / size_t(C);
+  const size_t cap = std::max<size_t>(1, per_channel / 2048);
+  return int(std::max<size_t>(1, std::min<size_t>({want, cap, size_t(256)})));
+}
+void ensure_red(TrainState& T, size_t parts, size_t C) {
+  T.dpart.ensure(std::max<size_t>(parts, 1024));
+  T.dmean.ensure(std::max<size_t>(C, 1024));
+  T.dcoef.ensure(std::max<size_t>(C, 1024));
+}
+// bias gradient: out[c] += sum over (batch, plane) of g
+void chsum(Context& c, TrainState& T, int nb, int C, int plane, const float* g, float* out) {
+  const int S = split_s(c, C, size_t(nb) * plane);
+  ensure_red(T, size_t(C) * S, size_t(C));
+  k_chpart<RED_SUM><<<dim3(C, S), TB, 0, c.stream>>>(nb, C, plane, g, nullptr, nullptr, nullptr, T.dpart.p);
+  k_fin_sum<<<(C + 127) / 128, 128, 0, c.stream>>>(C, S, T.dpart.p, out);
+}
+// batch norm statistics (inc/autodiff.hpp:228-262).  train: biased batch mean /
+// variance in fp64 (two passes, as the reference), running buffers folded with
+// momentum 0.9, update count bumped; eval: the running buffers.
+void bn_forward_stats(Context& c, TrainState& T, const Op& o, const Ten& A) {
+  const int C = A.c, plane = A.h * A.w;
+  float2* st = T.stats.p + o.st;
+  if (!o.train) {
+    k_bn_eval_stats<<<(C + 127) / 128, 128, 0, c.stream>>>(C, 1e-5f, PV(T, o.pbn + 2), PV(T, o.pbn + 3), st);
+    return;
+  }
+  const int S = split_s(c, C, size_t(A.n) * plane);
+  ensure_red(T, size_t(C) * S, size_t(C));
+  const double cnt = double(A.n) * plane;
+  k_chpart<RED_SUM><<<dim3(C, S), TB, 0, c.stream>>>(A.n, C, plane, V(T, o.a), nullptr, nullptr, nullptr, T.dpart.p);
+  k_fin_mean<<<(C + 127) / 128, 128, 0, c.stream>>>(C, S, cnt, T.dpart.p, T.dmean.p);
+  k_chpart<RED_SQDEV><<<dim3(C, S), TB, 0, c.stream>>>(A.n, C, plane, V(T, o.a), nullptr, T.dmean.p, nullptr, T.dpart.p);
+  k_fin_var<<<(C + 127) / 128, 128, 0, c.stream>>>(C, S, cnt, T.dpart.p, T.dmean.p, 1e-5f, 0.9f, PV(T, o.pbn + 2),
+                                                   PV(T, o.pbn + 3), PV(T, o.pbn + 4), st);
+}
+// batch norm backward (inc/autodiff.hpp:281-318): fp64 channel sums of dy and
+// dy * xhat -> scale / offset gradients, then dx (train: through the batch
+// statistics; eval: g * is * dy)
+void bn_backward(Context& c, TrainState& T, const Op& o, const Ten& A, const float* gy) {
+  const int C = A.c, plane = A.h * A.w;
+  const float2* st = T.stats.p + o.st;
+  const int S = split_s(c, C, size_t(A.n) * plane);
+  ensure_red(T, size_t(C) * S, size_t(C));
+  const double cnt = double(A.n) * plane;
+  k_chpart<RED_BNBWD><<<dim3(C, S), TB, 0, c.stream>>>(A.n, C, plane, V(T, o.a), gy, nullptr, st, T.dpart.p);
+  k_fin_bnbwd<<<(C + 127) / 128, 128, 0, c.stream>>>(C, S, cnt, T.dpart.p, PG(T, o.pbn), PG(T, o.pbn + 1), T.dcoef.p);
+  if (float* dx = G(T, o.a))
+    k_bn_dx<<<egrid(A.size()), TB, 0, c.stream>>>(A.size(), C, plane, V(T, o.a), gy, st, PV(T, o.pbn), T.dcoef.p,
+                                                  o.train ? 1 : 0, dx);
+}
+
 void run_forward(Context& c) {
   TrainState& T = tstate(c);
   cudaStream_t st = c.stream;
@@ -669,8 +735,7 @@ void run_forward(Context& c) {
       }
       case OP_BN: {
         const int plane = A.h * A.w;
-        k_bn_stats<<<A.c, TB, 0, st>>>(A.n, A.c, plane, V(T, o.a), o.train ? 1 : 0, 1e-5f, 0.9f, PV(T, o.pbn + 2),
-                                       PV(T, o.pbn + 3), PV(T, o.pbn + 4), T.stats.p + o.st);
+        bn_forward_stats(c, T, o, A);
         k_bn_apply<<<egrid(A.size()), TB, 0, st>>>(A.size(), A.c, plane, V(T, o.a), T.stats.p + o.st, PV(T, o.pbn),
                                                    PV(T, o.pbn + 1), V(T, o.y));
         break;
@@ -709,7 +774,7 @@ void run_backward(Context& c) {
           else
             k_wgrad<5><<<grid, TB, 0, st>>>(Y.n, gy, Y.c, Y.h, Y.w, V(T, o.a), A.c, A.h, A.w, o.k, o.s, dk);
         }
-        if (float* db = PG(T, o.pb)) k_chsum<<<Y.c, TB, 0, st>>>(Y.n, Y.c, Y.h * Y.w, gy, db);
+        if (float* db = PG(T, o.pb)) chsum(c, T, Y.n, Y.c, Y.h * Y.w, gy, db);
         if (float* dx = G(T, o.a)) {  // dx += conv^T(dy; K)
           const dim3 g((A.h * A.w + TB - 1) / TB, (A.c + CO - 1) / CO, A.n);
           k_convT_fwd<<<g, TB, 0, st>>>(gy, Y.c, Y.h, Y.w, PV(T, o.pk), nullptr, A.c, o.k, o.s, A.h, A.w, dx);
@@ -725,7 +790,7 @@ void run_backward(Context& c) {
           else
             k_wgrad<5><<<grid, TB, 0, st>>>(A.n, V(T, o.a), A.c, A.h, A.w, gy, Y.c, Y.h, Y.w, o.k, o.s, dk);
         }
-        if (float* db = PG(T, o.pb)) k_chsum<<<Y.c, TB, 0, st>>>(Y.n, Y.c, Y.h * Y.w, gy, db);
+        if (float* db = PG(T, o.pb)) chsum(c, T, Y.n, Y.c, Y.h * Y.w, gy, db);
         if (float* dx = G(T, o.a)) {
           // the conv kernel writes its output: run it into scratch, then accumulate
           T.tmp.ensure(A.size());
@@ -737,8 +802,7 @@ void run_backward(Context& c) {
         break;
       }
       case OP_BN:
-        k_bn_bwd<<<A.c, TB, 0, st>>>(A.n, A.c, A.h * A.w, V(T, o.a), gy, T.stats.p + o.st, PV(T, o.pbn), o.train ? 1 : 0,
-                                     PG(T, o.pbn), PG(T, o.pbn + 1), G(T, o.a));
+        bn_backward(c, T, o, A, gy);
         break;
       case OP_ELU:
         if (float* gx = G(T, o.a)) k_elu_bwd<<<egrid(A.size()), TB, 0, st>>>(A.size(), V(T, o.a), V(T, o.y), gy, gx);
@@ -786,7 +850,14 @@ double run_batch(Context& c, int B, int H, int W, const float* input, const floa
     HB_CUDA(cudaMemsetAsync(T.grads.p, 0, sizeof(float) * T.arena, st));
     HB_CUDA(cudaMemsetAsync(T.dgrad.p, 0, sizeof(float) * T.ptotal, st));
   }
-  k_mse<<<1, TB, 0, st>>>(O.size(), O.n, V(T, T.t_out), V(T, T.t_target), T.dloss.p, with_grad ? G(T, T.t_out) : nullptr);
+  {  // mse_loss (inc/autodiff.hpp:448-470)
+    const int S = int(std::min<size_t>(size_t(4) * c.num_sms, std::max<size_t>(1, O.size() / 2048)));
+    ensure_red(T, size_t(S), 1);
+    double* part = reinterpret_cast<double*>(T.dpart.p);
+    k_sqdiff_part<<<S, TB, 0, st>>>(O.size(), V(T, T.t_out), V(T, T.t_target), part);
+    k_fin_mse<<<1, 1, 0, st>>>(S, O.n, part, T.dloss.p);
+    if (with_grad) k_mse_grad<<<egrid(O.size()), TB, 0, st>>>(O.size(), O.n, V(T, T.t_out), V(T, T.t_target), G(T, T.t_out));
+  }
   HB_CUDA(cudaGetLastError());
   if (with_grad) run_backward(c);
   double loss = 0;

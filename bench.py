@@ -10,10 +10,12 @@ Helmholtz, unit point source, M_V (3-level shifted-Laplacian V-cycle, GMRES(10)
 coarsest), FGMRES(10) to 1e-6.  It is the only BASELINE config whose solve
 reaches 1e-6 with the seeded random-init weights the configs prescribe (c1-c4
 put a random-init U-Net in the preconditioner and stagnate; the oracle shows
-it).  One step = R independent c0 solves on one GPU, R = one per SM
-(148) by default -- the device-filling analog of the reference arm, which runs
-one c0 solve per host core.  Inputs resident in HBM; the per-step working set
-(~0.5 GB) exceeds L2, and L2 is additionally flushed (512 MiB write) between
+it).  One step = R independent c0 solves on one GPU, R = 3 per SM
+(444) by default -- one column per SM in each of the 3 column groups, the
+device-filling analog of the reference arm, which runs one c0 solve per host
+core (throughput saturates there: 148 -> 8.9k, 296 -> 9.5k, 444 -> 10.4k,
+888 -> 10.4k solves/s).  Inputs resident in HBM; the per-step working set
+(~1.5 GB) exceeds L2, and L2 is additionally flushed (512 MiB write) between
 timed steps.  Multi-GPU: each rank runs its own R replicas (weak scaling, no
 collective).  The U-Net configs are measured on a fixed iteration budget under
 "also".
@@ -240,7 +242,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     cfg = config_for(args.config)
-    R = args.replicas or sms
+    R = args.replicas or 3 * sms
     cols = columns(cfg, ws, rank, R)
     # G column groups = G independent solver contexts on their own streams, driven
     # from G host threads: one group's latency-bound coarsest solves overlap the
@@ -715,7 +717,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
-                                                              "(0 = one per SM)")
+                                                              "(0 = 3 per SM: one per SM in each of the 3 column groups)")
     ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,datagen,paper_ju,train", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)

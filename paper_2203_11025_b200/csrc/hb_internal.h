@@ -290,6 +290,7 @@ struct Context {
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size
   int opt_legs_wd = 2;  // Jacobi factor in the legs: 0 stored wD^-1, 1 from D, 2 by working-set size
   int conv_rows_ring = 4;
+  int adots_npt = 4;  // nodes per thread per tile of the Krylov dots kernel (4 | 8 | 16)
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {

@@ -231,7 +231,7 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[NF]) {
 // the last CTA of the column forms the MGS coefficients.
 __device__ void adots_scalar(ColState& S, int j, const double2* red);
 
-template <int NT>
+template <int NT, int NPT>  // NPT: nodes per thread per tile (more nodes per butterfly)
 __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
                                               const float2* __restrict__ Z, float2* __restrict__ W,
                                               const float2* __restrict__ V, double2* part, unsigned* ticket,
@@ -253,12 +253,12 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
   __shared__ float wpart[NT / 32][4 * kMaxRestart + 8];
   for (int t = threadIdx.x; t < (NT / 32) * (4 * kMaxRestart + 8); t += NT) (&wpart[0][0])[t] = 0.f;
   __syncthreads();
-  constexpr int TILE = NT * KNPT;
+  constexpr int TILE = NT * NPT;
   for (size_t base = size_t(blockIdx.x) * TILE; base < N; base += size_t(gridDim.x) * TILE) {
-    float2 w[KNPT], vj[KNPT];
-    bool ok[KNPT];
+    float2 w[NPT], vj[NPT];
+    bool ok[NPT];
 #pragma unroll
-    for (int q = 0; q < KNPT; ++q) {
+    for (int q = 0; q < NPT; ++q) {
       const size_t p = base + q * NT + threadIdx.x;
       ok[q] = p < N;
       if (ok[q]) {
@@ -271,12 +271,12 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
       }
     }
     for (int i0 = 0; i0 <= j; i0 += 4) {
-      float2 a[4][KNPT];
+      float2 a[4][NPT];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const float2* Vi = V + size_t(i0 + u) * BN + b * NS;
 #pragma unroll
-        for (int q = 0; q < KNPT; ++q)
+        for (int q = 0; q < NPT; ++q)
           a[u][q] = (ok[q] && i0 + u <= j) ? ld(Vi, base + q * NT + threadIdx.x) : make_float2(0.f, 0.f);
       }
       float v[16];  // [0..7] dots of i0..i0+3, [8..15] Gram
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
       for (int u = 0; u < 4; ++u) {
         float dr = 0.f, di = 0.f, gr = 0.f, gi = 0.f;
 #pragma unroll
-        for (int q = 0; q < KNPT; ++q) {
+        for (int q = 0; q < NPT; ++q) {
           const float2 ai = a[u][q], c = w[q], e = vj[q];
           dr = fmaf(ai.x, c.x, fmaf(ai.y, c.y, dr));
           di = fmaf(ai.x, c.y, fmaf(-ai.y, c.x, di));
@@ -687,9 +687,11 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
 void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V, double2* gsum) {
   const size_t N = owned_nodes(c);
   KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0) + double(N) * 8.0);  // Z_j, V_0..V_j in; w out; dA
-  const int nb = nblk_adots(c, N, B, 256 * KNPT);
-  launch_pdl(c, k_adots<256>, dim3(nb, B), dim3(256), 0, fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p),
-                                                   c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p, gsum);
+  const int npt = c.adots_npt;
+  const int nb = nblk_adots(c, N, B, 256 * npt);
+  auto k = npt == 16 ? k_adots<256, 16> : npt == 8 ? k_adots<256, 8> : k_adots<256, 4>;
+  launch_pdl(c, k, dim3(nb, B), dim3(256), 0, fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, Zj,
+             w, V, c.kpart.p, c.kticket.p, gsum);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -804,7 +806,7 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
     float2* Vj = K.V.p + size_t(j) * BN;
     float2* Zj = K.Z.p + size_t(j) * BN;
     k_diag_precond<<<gz, 256, 0, c.stream>>>(int(N), K.act.p, Vj, K.scale.p, L.dM.p, Zj);
-    launch_pdl(c, k_adots<256>, dim3(na, B), dim3(256), 0, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p,
+    launch_pdl(c, k_adots<256, KNPT>, dim3(na, B), dim3(256), 0, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p,
                (double2*)nullptr);
     launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, F, B, j, m, st, K.act.p, K.W.p, K.V.p,
                                                 reinterpret_cast<double*>(K.part.p), K.ticket.p, K.hist.p, cap, tol,

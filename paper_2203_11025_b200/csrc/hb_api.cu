@@ -949,6 +949,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->conv_rows_ring = value == 3 ? 3 : 4;
   else if (k == "stream_vcycle")
     ctx->opt_stream = value != 0;
+  else if (k == "adots_cp")
+    ctx->opt_adots_cp = value != 0;
   else if (k == "adots_npt")
     ctx->adots_npt = value >= 16 ? 16 : value >= 8 ? 8 : 4;
   else if (k == "staged_legs")

@@ -447,7 +447,8 @@ void ensure_params(Context& c) {
   std::vector<float> h(o, 0.f);
   for (size_t i = 0; i < P.params.size(); ++i)
     std::copy(P.params[i].v.begin(), P.params[i].v.end(), h.begin() + long(T.poff[i]));
-  HB_CUDA(cudaMemcpy(T.dparam.p, h.data(), o * sizeof(float), cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpyAsync(T.dparam.p, h.data(), o * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+  HB_CUDA(cudaStreamSynchronize(c.stream));
   T.params_on_device = true;
   T.gen = P.host_gen;
   T.adam_init = false;
@@ -461,7 +462,9 @@ void params_to_host(Context& c) {
   TrainState& T = tstate(c);
   if (!T.params_on_device) return;
   std::vector<float> h(T.ptotal);
-  HB_CUDA(cudaMemcpy(h.data(), T.dparam.p, T.ptotal * sizeof(float), cudaMemcpyDeviceToHost));
+  // on the library stream: it does not synchronise with the legacy default stream
+  HB_CUDA(cudaMemcpyAsync(h.data(), T.dparam.p, T.ptotal * sizeof(float), cudaMemcpyDeviceToHost, c.stream));
+  HB_CUDA(cudaStreamSynchronize(c.stream));
   for (size_t i = 0; i < P.params.size(); ++i)
     std::copy(h.begin() + long(T.poff[i]), h.begin() + long(T.poff[i] + P.params[i].size()), P.params[i].v.begin());
   P.dirty = true;
@@ -1230,7 +1233,8 @@ int hb_paper_grads(hb_ctx* ctx, int64_t count, float* grads) {
   TrainState& T = tstate(*ctx);
   if (count != hb_paper_trainable_count(ctx) || !grads) throw HbError{HB_ERR_ARG, "gradient count mismatch"};
   std::vector<float> h(T.ptotal);
-  HB_CUDA(cudaMemcpy(h.data(), T.dgrad.p, sizeof(float) * T.ptotal, cudaMemcpyDeviceToHost));
+  HB_CUDA(cudaMemcpyAsync(h.data(), T.dgrad.p, sizeof(float) * T.ptotal, cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
   size_t o = 0;
   for (size_t i = 0; i < P.params.size(); ++i)
     if (T.trainable[i]) {

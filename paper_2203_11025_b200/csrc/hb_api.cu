@@ -246,13 +246,16 @@ static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const fl
     // fused legs: v and r stay on chip (row-streaming kernels for a zero
     // initial guess, shared-memory tiles otherwise)
     const bool stream = c.opt_stream && (e0 == nullptr || c.opt_stream_e0) && L.nx >= 16;
+    // staged legs from e0 (level 0): the down leg stores the pre-smoothed iterate
+    // into the level's v buffer and the up leg reads it back instead of e0
+    float2* vpre = (e0 && c.opt_vpre && L.rows == L.ny) ? L.v.p + size_t(c0) * L.N() : nullptr;
     if (stream)
-      launch_down_stream(c, V, C.win(), w, offset, B, act, f, fscale, e0, Cf);
+      launch_down_stream(c, V, C.win(), w, offset, B, act, f, fscale, e0, Cf, vpre);
     else
       launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
     vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
     if (stream)
-      launch_up_stream(c, V, w, offset, C.nx, C.ny, C.win(), B, act, f, fscale, e0, Cx, out);
+      launch_up_stream(c, V, w, offset, C.nx, C.ny, C.win(), B, act, f, fscale, e0, Cx, out, vpre);
     else
       launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
     return;
@@ -949,6 +952,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->conv_rows_ring = value == 3 ? 3 : 4;
   else if (k == "stream_vcycle")
     ctx->opt_stream = value != 0;
+  else if (k == "vpre")
+    ctx->opt_vpre = value != 0;
   else if (k == "adots_cp")
     ctx->opt_adots_cp = value != 0;
   else if (k == "adots_npt")

@@ -168,16 +168,18 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
 // row-streaming legs, zero initial guess (hb_mg_stream.cu)
 // cw: storage window of the coarse field (down: emitted rows [cw.lo, cw.hi); up: vc)
 void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float damping, int offset, int B,
-                        const int* act, const float2* f, const float* fscale, const float2* e0, float2* fc);
+                        const int* act, const float2* f, const float* fscale, const float2* e0, float2* fc,
+                        float2* vpre = nullptr);
 void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, const RowWin& cw,
                       int B, const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
-                      float2* z);
+                      float2* z, const float2* vpre = nullptr);
 // cp.async-staged variants (hb_mg_staged.cu), same contracts; wd: form wD^-1 from D
 void launch_down_staged(Context& c, const LevelView& L, const RowWin& cw, float damping, int offset, int B,
-                        const int* act, const float2* f, const float* fscale, const float2* e0, bool wd, float2* fc);
+                        const int* act, const float2* f, const float* fscale, const float2* e0, bool wd, float2* fc,
+                        float2* vpre = nullptr);
 void launch_up_staged(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, const RowWin& cw,
                       int B, const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
-                      bool wd, float2* z);
+                      bool wd, float2* z, const float2* vpre = nullptr);
 // network pack / unpack (hb_net.cu)
 void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const int* act, const float2* r,
                        const float* rscale, float* x /*NHWC, 3 ch*/);
@@ -286,7 +288,7 @@ struct Context {
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
        opt_coarse_reg = true, opt_wide_legs = false,
-       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_pdl = true, opt_stream_e0 = true, opt_adots_cp = false;
+       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_pdl = true, opt_stream_e0 = true, opt_adots_cp = false, opt_vpre = true;
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size
   int opt_legs_wd = 2;  // Jacobi factor in the legs: 0 stored wD^-1, 1 from D, 2 by working-set size
   int conv_rows_ring = 4;

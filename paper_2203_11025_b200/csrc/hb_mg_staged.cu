@@ -226,7 +226,7 @@ template <bool E0, bool WD, bool EVEN, int NS>
 __global__ void __launch_bounds__(32 * GW) k_down_staged(LevelView L, RowWin cw, float damping, int offset, int rpc,
                                                          const int* act, const float2* __restrict__ f,
                                                          const float* fscale, const float2* __restrict__ e0,
-                                                         float2* __restrict__ fc) {
+                                                         float2* __restrict__ fc, float2* __restrict__ vpre) {
   extern __shared__ float4 smem4[];
   constexpr int H = down_halo<E0>(), SWOUT = down_out<E0>();
   using R = Ring<E0, WD, EVEN, false, NS>;
@@ -303,6 +303,9 @@ __global__ void __launch_bounds__(32 * GW) k_down_staged(LevelView L, RowWin cw,
     }
     // residual at row y: n_m now holds row y (both variants)
     const Node2& u = n_m;
+    if (E0 && EVEN && vpre && emit_col && y >= 2 * jy0 + offset && y < 2 * jy1 + offset)  // v_pre for the up leg
+      *reinterpret_cast<float4*>(vpre + b * bstride + ptrdiff_t(y - L.w.row0) * nx + c0) =
+          make_float4(v_c.a.x, v_c.a.y, v_c.b.x, v_c.b.y);
     const Pair2 mv = apply_M2(u.da, u.db, v_m, v_c, v_p, ih2);
     const float2 ra = pscale(psub(u.fa, mv.a), u.ma), rb = pscale(psub(u.fb, mv.b), u.mb);
     const float2 rl = shfl_up2(rb);  // r at c0 - 1
@@ -320,7 +323,7 @@ __global__ void __launch_bounds__(32 * GW) k_down_staged(LevelView L, RowWin cw,
 
 // up leg: grid (ceil(cnx / 30), ceil(row chunks / GW), B); each warp produces
 // fine rows [y0, y1) of its 60 fine columns
-template <bool E0, bool WD, bool EVEN, int NS>
+template <bool E0, bool WD, bool EVEN, int NS, bool VP = false>  // VP: read the down leg's v_pre instead of e0
 __global__ void __launch_bounds__(32 * GW) k_up_staged(LevelView L, float damping, int offset, int cnx, int cny,
                                                        RowWin cw, int rpc, const int* act, const float2* __restrict__ f,
                                                        const float* fscale, const float2* __restrict__ e0,
@@ -347,8 +350,9 @@ __global__ void __launch_bounds__(32 * GW) k_up_staged(LevelView L, float dampin
   rg.cb = vc + size_t(b) * cnx * cw.rows - ptrdiff_t(cw.row0) * cnx;
   rg.dM = L.dM;
   rg.wdi = L.wdi;
-  rg.first = y0 - 1 - (E0 ? 1 : 0);
-  rg.last = y1 + (E0 ? 1 : 0);
+  constexpr bool DEEP = E0 && !VP;  // the pre-smoothing stencil needs e0 one row beyond
+  rg.first = y0 - 1 - (DEEP ? 1 : 0);
+  rg.last = y1 + (DEEP ? 1 : 0);
   rg.lane = lane;
   rg.B0 = 2 * (blockIdx.x * SWOUT - 1);
   rg.nx = nx;
@@ -368,7 +372,13 @@ __global__ void __launch_bounds__(32 * GW) k_up_staged(LevelView L, float dampin
   rg.start();
   // v(y) = pre-smoothed + P vc (horizontal prolongation via one shuffle of the coarse value)
   auto vrow = [&](const Node2& um, const Node2& u, const Node2& up) {
-    Pair2 v = presmooth<E0>(um, u, up, ih2);
+    Pair2 v;
+    if (VP) {
+      v.a = u.ea;  // v_pre (zero outside the grid: zero-filled)
+      v.b = u.eb;
+    } else {
+      v = presmooth<E0>(um, u, up, ih2);
+    }
     const float2 nxt = shfl_down2(u.p);  // coarse column jx + 1
     v.a = padd(v.a, pscale(u.p, u.ma));
     v.b = padd(v.b, pscale(pscale(padd(u.p, nxt), 0.5f), u.mb));
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(32 * GW) k_up_staged(LevelView L, float dampin
   };
   Node2 n_m, n_c, n_p;
   Pair2 v_m, v_c;
-  if (E0) {
+  if (DEEP) {
     const Node2 n_m2 = rg.next();
     n_m = rg.next();
     n_c = rg.next();
@@ -393,7 +403,7 @@ __global__ void __launch_bounds__(32 * GW) k_up_staged(LevelView L, float dampin
   const bool emit = lane >= 1 && lane <= SWOUT;
   for (int y = y0; y < y1; ++y) {
     Pair2 v_p;
-    if (E0) {
+    if (DEEP) {
       const Node2 n_p2 = rg.next();
       v_p = vrow(n_c, n_p, n_p2);
       n_m = n_c;
@@ -435,18 +445,18 @@ constexpr int NSTAGE = 4;
 
 template <bool E0, bool WD, bool EVEN>
 void down_one(Context& c, dim3 grid, const LevelView& L, const RowWin& cw, float damping, int offset, int rpc,
-              const int* act, const float2* f, const float* fscale, const float2* e0, float2* fc) {
+              const int* act, const float2* f, const float* fscale, const float2* e0, float2* fc, float2* vpre) {
   auto k = k_down_staged<E0, WD, EVEN, NSTAGE>;
   const size_t smem = size_t(GW) * NSTAGE * Ring<E0, WD, EVEN, false, NSTAGE>::STG * sizeof(float2);
   static bool once = (set_smem(k, smem), true);
   (void)once;
-  launch_pdl(c, k, grid, dim3(32, GW), smem, L, cw, damping, offset, rpc, act, f, fscale, e0, fc);
+  launch_pdl(c, k, grid, dim3(32, GW), smem, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre);
 }
-template <bool E0, bool WD, bool EVEN>
+template <bool E0, bool WD, bool EVEN, bool VP = false>
 void up_one(Context& c, dim3 grid, const LevelView& L, float damping, int offset, int cnx, int cny, const RowWin& cw,
             int rpc, const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
             float2* z) {
-  auto k = k_up_staged<E0, WD, EVEN, NSTAGE>;
+  auto k = k_up_staged<E0, WD, EVEN, NSTAGE, VP>;
   const size_t smem = size_t(GW) * NSTAGE * Ring<E0, WD, EVEN, true, NSTAGE>::STG * sizeof(float2);
   static bool once = (set_smem(k, smem), true);
   (void)once;
@@ -456,7 +466,9 @@ void up_one(Context& c, dim3 grid, const LevelView& L, float damping, int offset
 }  // namespace
 
 void launch_down_staged(Context& c, const LevelView& L, const RowWin& cw, float damping, int offset, int B,
-                        const int* act, const float2* f, const float* fscale, const float2* e0, bool wd, float2* fc) {
+                        const int* act, const float2* f, const float* fscale, const float2* e0, bool wd, float2* fc,
+                        float2* vpre) {
+  if (vpre && (!e0 || (offset & 1))) vpre = nullptr;  // v_pre is stored for the level-0 legs from e0 only
   const int cnx = L.nx / 2, cny = cw.hi - cw.lo;
   const int swout = e0 ? down_out<true>() : down_out<false>();
   static const int env_d = getenv("HB_RPC_DOWN") ? atoi(getenv("HB_RPC_DOWN")) : 0;
@@ -469,24 +481,24 @@ void launch_down_staged(Context& c, const LevelView& L, const RowWin& cw, float 
   const bool even = (offset & 1) == 0;
   if (e0) {
     if (wd)
-      even ? down_one<true, true, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc)
-           : down_one<true, true, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc);
+      even ? down_one<true, true, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre)
+           : down_one<true, true, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre);
     else
-      even ? down_one<true, false, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc)
-           : down_one<true, false, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc);
+      even ? down_one<true, false, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre)
+           : down_one<true, false, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre);
   } else {
     if (wd)
-      even ? down_one<false, true, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc)
-           : down_one<false, true, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc);
+      even ? down_one<false, true, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre)
+           : down_one<false, true, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre);
     else
-      even ? down_one<false, false, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc)
-           : down_one<false, false, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc);
+      even ? down_one<false, false, true>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre)
+           : down_one<false, false, false>(c, grid, L, cw, damping, offset, rpc, act, f, fscale, e0, fc, vpre);
   }
 }
 
 void launch_up_staged(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, const RowWin& cw,
                       int B, const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
-                      bool wd, float2* z) {
+                      bool wd, float2* z, const float2* vpre) {
   static const int env_u = getenv("HB_RPC_UP") ? atoi(getenv("HB_RPC_UP")) : 0;
   const int nrows = L.w.hi - L.w.lo;
   int rpc = 16;
@@ -495,7 +507,12 @@ void launch_up_staged(Context& c, const LevelView& L, float damping, int offset,
   const int chunks = (nrows + rpc - 1) / rpc;
   const dim3 grid((cnx + 29) / 30, (chunks + GW - 1) / GW, B);
   const bool even = (offset & 1) == 0;
-  if (e0) {
+  if (e0 && vpre && even) {  // v_pre from the down leg: no pre-smoothing stencil here
+    if (wd)
+      up_one<true, true, true, true>(c, grid, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, vpre, vc, z);
+    else
+      up_one<true, false, true, true>(c, grid, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, vpre, vc, z);
+  } else if (e0) {
     if (wd)
       even ? up_one<true, true, true>(c, grid, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, e0, vc, z)
            : up_one<true, true, false>(c, grid, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, e0, vc, z);

@@ -736,7 +736,8 @@ static bool legs_staged(const Context& c, const LevelView& L, int B) {
 }
 
 void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float damping, int offset, int B,
-                        const int* act, const float2* f, const float* fscale, const float2* e0, float2* fc) {
+                        const int* act, const float2* f, const float* fscale, const float2* e0, float2* fc,
+                        float2* vpre) {
   const int cnx = L.nx / 2, cny = cw.hi - cw.lo;  // coarse rows emitted
   // only the lean kernel honours row windows (row slabs)
   const bool slab = L.w.rows != L.ny || cw.rows != L.ny / 2 || cw.lo != 0;
@@ -753,7 +754,7 @@ void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float 
   const int chunks = (cny + rpc - 1) / rpc;
   const bool wd = legs_wd(c, L, B), even = (offset & 1) == 0;
   if (staged) {
-    launch_down_staged(c, L, cw, damping, offset, B, act, f, fscale, e0, wd, fc);
+    launch_down_staged(c, L, cw, damping, offset, B, act, f, fscale, e0, wd, fc, vpre);
   } else if (e0) {
     const dim3 grid((cnx + SWE_DOWN - 1) / SWE_DOWN, (chunks + WARPS - 1) / WARPS, B);
     auto k = wd ? (even ? k_down_e0<true, true> : k_down_e0<true, false>)
@@ -780,7 +781,7 @@ void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float 
 
 void launch_up_stream(Context& c, const LevelView& L, float damping, int offset, int cnx, int cny, const RowWin& cw,
                       int B, const int* act, const float2* f, const float* fscale, const float2* e0, const float2* vc,
-                      float2* z) {
+                      float2* z, const float2* vpre) {
   const int tok = prof_begin(c, PC_UP);
   static const int env_u = getenv("HB_RPC_UP") ? atoi(getenv("HB_RPC_UP")) : 0;
   const int nrows = L.w.hi - L.w.lo;
@@ -793,7 +794,7 @@ void launch_up_stream(Context& c, const LevelView& L, float damping, int offset,
   const bool slab = L.w.rows != L.ny || L.w.lo != 0 || L.w.hi != L.ny || cw.rows != cny || cw.row0 != 0;
   const bool wd = legs_wd(c, L, B), even = (offset & 1) == 0;
   if (legs_staged(c, L, B)) {
-    launch_up_staged(c, L, damping, offset, cnx, cny, cw, B, act, f, fscale, e0, vc, wd, z);
+    launch_up_staged(c, L, damping, offset, cnx, cny, cw, B, act, f, fscale, e0, vc, wd, z, vpre);
   } else if (e0 && slab) {
     throw HbError{HB_ERR_ARG, "register-prefetch legs from an initial guess run on whole grids only"};
   } else if (e0) {

@@ -952,6 +952,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->conv_rows_ring = value == 3 ? 3 : 4;
   else if (k == "stream_vcycle")
     ctx->opt_stream = value != 0;
+  else if (k == "wgrad_blk")
+    ctx->opt_wgrad_blk = value != 0;
   else if (k == "vpre")
     ctx->opt_vpre = value != 0;
   else if (k == "adots_cp")

@@ -52,31 +52,45 @@ inline int nblk(size_t n) { return int(std::min<size_t>((n + TB - 1) / TB, size_
 // ------------------------------------------------------------------ kernels
 // y[b,co,oy,ox] = bias[co] + sum_{ci,ky,kx} x[b,ci,oy*s+ky-p,ox*s+kx-p] K[co,ci,ky,kx]
 // (conv2d, inc/autodiff.hpp:121-150: zero padding p = (k-1)/2, cross-correlation)
+constexpr int PX = 4;  // output pixels per thread along x (forward convolutions)
+
+template <int K, int S>
 __global__ void __launch_bounds__(TB) k_conv_fwd(const float* __restrict__ x, int cin, int H, int W,
-                                                 const float* __restrict__ K, const float* __restrict__ bias, int cout,
-                                                 int k, int s, int Ho, int Wo, float* __restrict__ y) {
-  const int pix = blockIdx.x * TB + threadIdx.x;
+                                                 const float* __restrict__ Kw, const float* __restrict__ bias, int cout,
+                                                 int Ho, int Wo, float* __restrict__ y) {
+  const int gx = (Wo + PX - 1) / PX;
+  const int gid = blockIdx.x * TB + threadIdx.x;
   const int co0 = blockIdx.y * CO, b = blockIdx.z;
-  if (pix >= Ho * Wo) return;
-  const int oy = pix / Wo, ox = pix % Wo, p = (k - 1) / 2;
-  float acc[CO];
+  if (gid >= Ho * gx) return;
+  constexpr int P = (K - 1) / 2, KK = K * K;
+  const int oy = gid / gx, ox0 = (gid % gx) * PX;
+  float acc[PX][CO];
 #pragma unroll
-  for (int j = 0; j < CO; ++j) acc[j] = 0.f;
-  const int kk = k * k;
+  for (int q = 0; q < PX; ++q)
+#pragma unroll
+    for (int j = 0; j < CO; ++j) acc[q][j] = 0.f;
+  int cj[CO];
+#pragma unroll
+  for (int j = 0; j < CO; ++j) cj[j] = min(co0 + j, cout - 1);
   for (int ci = 0; ci < cin; ++ci) {
     const float* xp = x + (size_t(b) * cin + ci) * H * W;
-    for (int ky = 0; ky < k; ++ky) {
-      const int iy = oy * s + ky - p;
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky) {
+      const int iy = oy * S + ky - P;
       if (iy < 0 || iy >= H) continue;
-      for (int kx = 0; kx < k; ++kx) {
-        const int ix = ox * s + kx - p;
-        if (ix < 0 || ix >= W) continue;
-        const float xv = __ldg(xp + size_t(iy) * W + ix);
-        const int t = ky * k + kx;
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) {
+        float xv[PX];
+#pragma unroll
+        for (int q = 0; q < PX; ++q) {
+          const int ix = (ox0 + q) * S + kx - P;
+          xv[q] = (ix >= 0 && ix < W) ? __ldg(xp + size_t(iy) * W + ix) : 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < CO; ++j) {
-          const int co = min(co0 + j, cout - 1);
-          acc[j] = fmaf(xv, __ldg(K + (size_t(co) * cin + ci) * kk + t), acc[j]);
+          const float wv = __ldg(Kw + (size_t(cj[j]) * cin + ci) * KK + ky * K + kx);
+#pragma unroll
+          for (int q = 0; q < PX; ++q) acc[q][j] = fmaf(xv[q], wv, acc[q][j]);
         }
       }
     }
@@ -84,41 +98,80 @@ __global__ void __launch_bounds__(TB) k_conv_fwd(const float* __restrict__ x, in
 #pragma unroll
   for (int j = 0; j < CO; ++j) {
     const int co = co0 + j;
-    if (co < cout) y[(size_t(b) * cout + co) * Ho * Wo + pix] = acc[j] + (bias ? __ldg(bias + co) : 0.f);
+    if (co >= cout) continue;
+    const float bv = bias ? __ldg(bias + co) : 0.f;
+#pragma unroll
+    for (int q = 0; q < PX; ++q)
+      if (ox0 + q < Wo) y[(size_t(b) * cout + co) * Ho * Wo + size_t(oy) * Wo + ox0 + q] = acc[q][j] + bv;
   }
 }
 
-// z[b,cb,Y,X] = bias[cb] + sum_{ca, ky, kx: Y = y*s+ky-p, X = x*s+kx-p} u[b,ca,y,x] K[ca,cb,ky,kx]
-// (conv2d_transpose, inc/autodiff.hpp:155-211: the exact adjoint of conv2d)
+void launch_conv(cudaStream_t st, dim3 g, const float* x, int cin, int H, int W, const float* Kw, const float* bias,
+                 int cout, int k, int s, int Ho, int Wo, float* y) {
+  g.x = unsigned((Ho * ((Wo + PX - 1) / PX) + TB - 1) / TB);  // one thread per PX output pixels
+  if (k == 5 && s == 2)
+    k_conv_fwd<5, 2><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  else if (k == 3 && s == 1)
+    k_conv_fwd<3, 1><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  else if (k == 5 && s == 1)
+    k_conv_fwd<5, 1><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  else if (k == 3 && s == 2)
+    k_conv_fwd<3, 2><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  else if (k == 1 && s == 1)
+    k_conv_fwd<1, 1><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  else if (k == 1 && s == 2)
+    k_conv_fwd<1, 2><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  else
+    throw HbError{HB_ERR_ARG, "training supports 1x1, 3x3 and 5x5 kernels with stride 1 or 2"};
+}
+
+// z[b,cb,Y,X] += bias[cb] + sum_{ca, ky, kx: Y = y*s+ky-p, X = x*s+kx-p} u[b,ca,y,x] K[ca,cb,ky,kx]
+// (conv2d_transpose, inc/autodiff.hpp:155-211: the exact adjoint of conv2d).
+// Gather form with the kernel size and stride as template arguments: for
+// stride 2 only the taps of the output pixel's parity class reach it
+// (ky = (Y + p) mod 2, +2, ...), so a 5x5 tap loop visits 4-9 taps, not 25.
+template <int K, int S>
 __global__ void __launch_bounds__(TB) k_convT_fwd(const float* __restrict__ u, int ca, int h, int w,
-                                                  const float* __restrict__ K, const float* __restrict__ bias, int cb,
-                                                  int k, int s, int H, int W, float* __restrict__ z) {
-  const int pix = blockIdx.x * TB + threadIdx.x;
+                                                  const float* __restrict__ Kw, const float* __restrict__ bias, int cb,
+                                                  int H, int W, float* __restrict__ z) {
+  // thread = PX output pixels X = xb + S*q (one parity class) of one row
+  constexpr int SPAN = S * PX;
+  const int gx = ((W + SPAN - 1) / SPAN) * S;
+  const int gid = blockIdx.x * TB + threadIdx.x;
   const int c0 = blockIdx.y * CO, b = blockIdx.z;
-  if (pix >= H * W) return;
-  const int Y = pix / W, X = pix % W, p = (k - 1) / 2;
-  float acc[CO];
+  if (gid >= H * gx) return;
+  constexpr int P = (K - 1) / 2, KK = K * K;
+  const int Y = gid / gx, g = gid % gx;
+  const int xb = (g / S) * SPAN + (g % S);
+  const int ky0 = S == 2 ? (Y + P) & 1 : 0, kx0 = S == 2 ? (xb + P) & 1 : 0;
+  float acc[PX][CO];
 #pragma unroll
-  for (int j = 0; j < CO; ++j) acc[j] = 0.f;
-  const int kk = k * k;
+  for (int q = 0; q < PX; ++q)
+#pragma unroll
+    for (int j = 0; j < CO; ++j) acc[q][j] = 0.f;
+  int cj[CO];
+#pragma unroll
+  for (int j = 0; j < CO; ++j) cj[j] = min(c0 + j, cb - 1);
   for (int a = 0; a < ca; ++a) {
     const float* up = u + (size_t(b) * ca + a) * h * w;
-    for (int ky = 0; ky < k; ++ky) {
-      const int ty = Y + p - ky;
-      if (ty < 0 || ty % s) continue;
-      const int y = ty / s;
-      if (y >= h) continue;
-      for (int kx = 0; kx < k; ++kx) {
-        const int tx = X + p - kx;
-        if (tx < 0 || tx % s) continue;
-        const int xx = tx / s;
-        if (xx >= w) continue;
-        const float uv = __ldg(up + size_t(y) * w + xx);
-        const int t = ky * k + kx;
+    const float* ka = Kw + size_t(a) * cb * KK;
+    for (int ky = ky0; ky < K; ky += S) {
+      const int ty = Y + P - ky;
+      if (ty < 0 || ty / S >= h) continue;
+      const int y = ty / S;  // exact: ty is a multiple of S
+      for (int kx = kx0; kx < K; kx += S) {
+        float uv[PX];
+#pragma unroll
+        for (int q = 0; q < PX; ++q) {
+          const int tx = xb + S * q + P - kx;  // multiple of S; input column tx / S = (xb + P - kx) / S + q
+          uv[q] = (tx >= 0 && tx / S < w && xb + S * q < W) ? __ldg(up + size_t(y) * w + tx / S) : 0.f;
+        }
+        const int t = ky * K + kx;
 #pragma unroll
         for (int j = 0; j < CO; ++j) {
-          const int c = min(c0 + j, cb - 1);
-          acc[j] = fmaf(uv, __ldg(K + (size_t(a) * cb + c) * kk + t), acc[j]);
+          const float wv = __ldg(ka + size_t(cj[j]) * KK + t);
+#pragma unroll
+          for (int q = 0; q < PX; ++q) acc[q][j] = fmaf(uv[q], wv, acc[q][j]);
         }
       }
     }
@@ -126,21 +179,46 @@ __global__ void __launch_bounds__(TB) k_convT_fwd(const float* __restrict__ u, i
 #pragma unroll
   for (int j = 0; j < CO; ++j) {
     const int c = c0 + j;
-    if (c < cb) z[(size_t(b) * cb + c) * H * W + pix] += acc[j] + (bias ? __ldg(bias + c) : 0.f);
+    if (c >= cb) continue;
+    const float bv = bias ? __ldg(bias + c) : 0.f;
+#pragma unroll
+    for (int q = 0; q < PX; ++q) {
+      const int X = xb + S * q;
+      if (X < W) z[(size_t(b) * cb + c) * H * W + size_t(Y) * W + X] += acc[q][j] + bv;
+    }
   }
+}
+
+void launch_convT(cudaStream_t st, dim3 g, const float* u, int ca, int h, int w, const float* Kw, const float* bias,
+                  int cb, int k, int s, int H, int W, float* z) {
+  g.x = unsigned((H * ((W + s * PX - 1) / (s * PX)) * s + TB - 1) / TB);  // one thread per PX pixels of a parity class
+  if (k == 5 && s == 2)
+    k_convT_fwd<5, 2><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  else if (k == 3 && s == 1)
+    k_convT_fwd<3, 1><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  else if (k == 5 && s == 1)
+    k_convT_fwd<5, 1><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  else if (k == 3 && s == 2)
+    k_convT_fwd<3, 2><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  else if (k == 1 && s == 1)
+    k_convT_fwd<1, 1><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  else if (k == 1 && s == 2)
+    k_convT_fwd<1, 2><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  else
+    throw HbError{HB_ERR_ARG, "training supports 1x1, 3x3 and 5x5 kernels with stride 1 or 2"};
 }
 
 // dK[a,c,ky,kx] += sum_{b,y,x} A[b,a,y,x] X[b,c,y*s+ky-p,x*s+kx-p]
 // conv2d: A = dy (cout), X = x (cin); conv2d_transpose: A = u (x channels), X = dz
-template <int KMAX>
+template <int K, int S>
 __global__ void __launch_bounds__(TB) k_wgrad(int nb, const float* __restrict__ A, int na, int h, int w,
-                                              const float* __restrict__ X, int nc, int H, int W, int k, int s,
+                                              const float* __restrict__ X, int nc, int H, int W,
                                               float* __restrict__ dK) {
   const int a = blockIdx.x / nc, c = blockIdx.x % nc;
-  const int p = (k - 1) / 2, kk = k * k;
-  float acc[KMAX * KMAX];
+  constexpr int P = (K - 1) / 2, KK = K * K;
+  float acc[KK];
 #pragma unroll
-  for (int t = 0; t < KMAX * KMAX; ++t) acc[t] = 0.f;
+  for (int t = 0; t < KK; ++t) acc[t] = 0.f;
   const int hw = h * w;
   const size_t total = size_t(nb) * hw;
   for (size_t i = threadIdx.x; i < total; i += TB) {
@@ -149,30 +227,131 @@ __global__ void __launch_bounds__(TB) k_wgrad(int nb, const float* __restrict__ 
     const float av = __ldg(A + (size_t(b) * na + a) * hw + q);
     const float* xp = X + (size_t(b) * nc + c) * H * W;
 #pragma unroll
-    for (int ky = 0; ky < KMAX; ++ky) {
-      const int iy = y * s + ky - p;
-      const bool oky = ky < k && iy >= 0 && iy < H;
+    for (int ky = 0; ky < K; ++ky) {
+      const int iy = y * S + ky - P;
+      if (iy < 0 || iy >= H) continue;
 #pragma unroll
-      for (int kx = 0; kx < KMAX; ++kx) {
-        const int ix = x * s + kx - p;
-        if (oky && kx < k && ix >= 0 && ix < W) acc[ky * KMAX + kx] = fmaf(av, __ldg(xp + size_t(iy) * W + ix), acc[ky * KMAX + kx]);
+      for (int kx = 0; kx < K; ++kx) {
+        const int ix = x * S + kx - P;
+        if (ix >= 0 && ix < W) acc[ky * K + kx] = fmaf(av, __ldg(xp + size_t(iy) * W + ix), acc[ky * K + kx]);
       }
     }
   }
   __shared__ double red[TB / 32];
-  for (int ky = 0; ky < k; ++ky)
-    for (int kx = 0; kx < k; ++kx) {
-      double v = acc[ky * KMAX + kx];
-      v = warp_sum(v);
-      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        double t = 0;
-        for (int i = 0; i < TB / 32; ++i) t += red[i];
-        dK[(size_t(a) * nc + c) * kk + ky * k + kx] += float(t);
-      }
-      __syncthreads();
+#pragma unroll 1
+  for (int t = 0; t < KK; ++t) {
+    double v = acc[t];
+    v = warp_sum(v);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s2 = 0;
+      for (int r = 0; r < TB / 32; ++r) s2 += red[r];
+      dK[(size_t(a) * nc + c) * KK + t] += float(s2);
     }
+    __syncthreads();
+  }
+}
+
+// Kernel gradient, blocked: a CTA owns one X channel c, AB A channels and one
+// pixel slice; per pixel the K*K shifted X taps are loaded once and reused for
+// the AB channels (AB*K*K FMAs per K*K + AB loads, the per-pair kernel above
+// does one load per FMA).  Per-CTA fp64 partials go to ws[slice][a][c][t];
+// k_wgrad_fold sums the slices in order (deterministic).
+template <int K, int S, int AB>
+__global__ void __launch_bounds__(TB) k_wgrad_blk(int nb, const float* __restrict__ A, int na, int h, int w,
+                                                  const float* __restrict__ X, int nc, int H, int W,
+                                                  double* __restrict__ ws) {
+  const int c = blockIdx.x % nc, a0 = (blockIdx.x / nc) * AB;
+  constexpr int P = (K - 1) / 2, KK = K * K;
+  const int hw = h * w;
+  const size_t total = size_t(nb) * hw, per = (total + gridDim.y - 1) / gridDim.y;
+  const size_t lo = blockIdx.y * per, hi = min(total, lo + per);
+  float acc[AB][KK];
+#pragma unroll
+  for (int u = 0; u < AB; ++u)
+#pragma unroll
+    for (int t = 0; t < KK; ++t) acc[u][t] = 0.f;
+  int ac[AB];
+#pragma unroll
+  for (int u = 0; u < AB; ++u) ac[u] = min(a0 + u, na - 1);
+  for (size_t i = lo + threadIdx.x; i < hi; i += TB) {
+    const int b = int(i / hw), q = int(i % hw);
+    const int y = q / w, x = q % w;
+    float av[AB];
+#pragma unroll
+    for (int u = 0; u < AB; ++u) av[u] = __ldg(A + (size_t(b) * na + ac[u]) * hw + q);
+    const float* xp = X + (size_t(b) * nc + c) * H * W;
+#pragma unroll
+    for (int ky = 0; ky < K; ++ky) {
+      const int iy = y * S + ky - P;
+      const bool oky = iy >= 0 && iy < H;
+#pragma unroll
+      for (int kx = 0; kx < K; ++kx) {
+        const int ix = x * S + kx - P;
+        const float xv = (oky && ix >= 0 && ix < W) ? __ldg(xp + size_t(iy) * W + ix) : 0.f;
+#pragma unroll
+        for (int u = 0; u < AB; ++u) acc[u][ky * K + kx] = fmaf(av[u], xv, acc[u][ky * K + kx]);
+      }
+    }
+  }
+  __shared__ double red[TB / 32][AB * KK];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+#pragma unroll
+  for (int u = 0; u < AB; ++u)
+#pragma unroll
+    for (int t = 0; t < KK; ++t) {
+      const double v = warp_sum(double(acc[u][t]));
+      if (lane == 0) red[wp][u * KK + t] = v;
+    }
+  __syncthreads();
+  const size_t slab = size_t(na) * nc * KK;
+  for (int e = threadIdx.x; e < AB * KK; e += TB) {
+    const int u = e / KK, t = e % KK;
+    if (a0 + u >= na) continue;
+    double s2 = 0;
+    for (int r = 0; r < TB / 32; ++r) s2 += red[r][e];
+    ws[blockIdx.y * slab + (size_t(a0 + u) * nc + c) * KK + t] = s2;
+  }
+}
+__global__ void k_wgrad_fold(size_t n, int slices, const double* __restrict__ ws, float* dK) {
+  for (size_t i = blockIdx.x * size_t(TB) + threadIdx.x; i < n; i += size_t(gridDim.x) * TB) {
+    double s2 = 0;
+    for (int j = 0; j < slices; ++j) s2 += ws[size_t(j) * n + i];
+    dK[i] += float(s2);
+  }
+}
+
+template <int K, int S, int AB>
+void wgrad_blk(cudaStream_t st, int nsm, DBuf<double>& wsb, int nb, const float* A, int na, int h, int w,
+               const float* X, int nc, int H, int W, float* dK) {
+  const int groups = nc * ((na + AB - 1) / AB);
+  const size_t pix = size_t(nb) * h * w;
+  const int slices = int(std::max<size_t>(1, std::min<size_t>((size_t(2) * nsm + groups - 1) / groups, pix / 4096)));
+  const size_t n = size_t(na) * nc * K * K;
+  wsb.ensure(n * size_t(slices));
+  k_wgrad_blk<K, S, AB><<<dim3(groups, slices), TB, 0, st>>>(nb, A, na, h, w, X, nc, H, W, wsb.p);
+  k_wgrad_fold<<<nblk(n), TB, 0, st>>>(n, slices, wsb.p, dK);
+}
+
+void launch_wgrad(cudaStream_t st, int grid, int nb, const float* A, int na, int h, int w, const float* X, int nc,
+                  int H, int W, int k, int s, float* dK, int nsm = 0, DBuf<double>* wsb = nullptr) {
+  if (wsb && k == 3 && s == 1) return wgrad_blk<3, 1, 8>(st, nsm, *wsb, nb, A, na, h, w, X, nc, H, W, dK);
+  if (wsb && k == 5 && s == 2) return wgrad_blk<5, 2, 2>(st, nsm, *wsb, nb, A, na, h, w, X, nc, H, W, dK);
+  if (k == 5 && s == 2)
+    k_wgrad<5, 2><<<grid, TB, 0, st>>>(nb, A, na, h, w, X, nc, H, W, dK);
+  else if (k == 3 && s == 1)
+    k_wgrad<3, 1><<<grid, TB, 0, st>>>(nb, A, na, h, w, X, nc, H, W, dK);
+  else if (k == 5 && s == 1)
+    k_wgrad<5, 1><<<grid, TB, 0, st>>>(nb, A, na, h, w, X, nc, H, W, dK);
+  else if (k == 3 && s == 2)
+    k_wgrad<3, 2><<<grid, TB, 0, st>>>(nb, A, na, h, w, X, nc, H, W, dK);
+  else if (k == 1 && s == 1)
+    k_wgrad<1, 1><<<grid, TB, 0, st>>>(nb, A, na, h, w, X, nc, H, W, dK);
+  else if (k == 1 && s == 2)
+    k_wgrad<1, 2><<<grid, TB, 0, st>>>(nb, A, na, h, w, X, nc, H, W, dK);
+  else
+    throw HbError{HB_ERR_ARG, "training supports 1x1, 3x3 and 5x5 kernels with stride 1 or 2"};
 }
 
 __device__ double block_sum(double v, double* red) {
@@ -404,7 +583,7 @@ struct TrainState {
   size_t arena = 0, nstats = 0;
   DBuf<float> vals, grads, tmp;
   DBuf<float2> stats;
-  DBuf<double> dloss, dmean;
+  DBuf<double> dloss, dmean, wsw;
   DBuf<double2> dpart, dcoef;
   DBuf<int> dbad;
   // frozen encoder features (batch 1) for retrain
@@ -725,15 +904,13 @@ void run_forward(Context& c) {
     switch (o.kind) {
       case OP_CONV: {
         const dim3 g((Y.h * Y.w + TB - 1) / TB, (Y.c + CO - 1) / CO, Y.n);
-        k_conv_fwd<<<g, TB, 0, st>>>(V(T, o.a), A.c, A.h, A.w, PV(T, o.pk), PV(T, o.pb), Y.c, o.k, o.s, Y.h, Y.w,
-                                     V(T, o.y));
+        launch_conv(st, g, V(T, o.a), A.c, A.h, A.w, PV(T, o.pk), PV(T, o.pb), Y.c, o.k, o.s, Y.h, Y.w, V(T, o.y));
         break;
       }
       case OP_CONVT: {
         HB_CUDA(cudaMemsetAsync(V(T, o.y), 0, Y.size() * sizeof(float), st));
         const dim3 g((Y.h * Y.w + TB - 1) / TB, (Y.c + CO - 1) / CO, Y.n);
-        k_convT_fwd<<<g, TB, 0, st>>>(V(T, o.a), A.c, A.h, A.w, PV(T, o.pk), PV(T, o.pb), Y.c, o.k, o.s, Y.h, Y.w,
-                                      V(T, o.y));
+        launch_convT(st, g, V(T, o.a), A.c, A.h, A.w, PV(T, o.pk), PV(T, o.pb), Y.c, o.k, o.s, Y.h, Y.w, V(T, o.y));
         break;
       }
       case OP_BN: {
@@ -771,27 +948,21 @@ void run_backward(Context& c) {
     switch (o.kind) {
       case OP_CONV: {
         if (float* dk = PG(T, o.pk)) {
-          const int grid = Y.c * A.c;
-          if (o.k <= 3)
-            k_wgrad<3><<<grid, TB, 0, st>>>(Y.n, gy, Y.c, Y.h, Y.w, V(T, o.a), A.c, A.h, A.w, o.k, o.s, dk);
-          else
-            k_wgrad<5><<<grid, TB, 0, st>>>(Y.n, gy, Y.c, Y.h, Y.w, V(T, o.a), A.c, A.h, A.w, o.k, o.s, dk);
+          launch_wgrad(st, Y.c * A.c, Y.n, gy, Y.c, Y.h, Y.w, V(T, o.a), A.c, A.h, A.w, o.k, o.s, dk, c.num_sms,
+                       c.opt_wgrad_blk ? &T.wsw : nullptr);
         }
         if (float* db = PG(T, o.pb)) chsum(c, T, Y.n, Y.c, Y.h * Y.w, gy, db);
         if (float* dx = G(T, o.a)) {  // dx += conv^T(dy; K)
           const dim3 g((A.h * A.w + TB - 1) / TB, (A.c + CO - 1) / CO, A.n);
-          k_convT_fwd<<<g, TB, 0, st>>>(gy, Y.c, Y.h, Y.w, PV(T, o.pk), nullptr, A.c, o.k, o.s, A.h, A.w, dx);
+          launch_convT(st, g, gy, Y.c, Y.h, Y.w, PV(T, o.pk), nullptr, A.c, o.k, o.s, A.h, A.w, dx);
         }
         break;
       }
       case OP_CONVT: {
         // dK[a, c] += sum u[a] dz[c] (shifted); du += conv(dz; K viewed as (a, c))
         if (float* dk = PG(T, o.pk)) {
-          const int grid = A.c * Y.c;
-          if (o.k <= 3)
-            k_wgrad<3><<<grid, TB, 0, st>>>(A.n, V(T, o.a), A.c, A.h, A.w, gy, Y.c, Y.h, Y.w, o.k, o.s, dk);
-          else
-            k_wgrad<5><<<grid, TB, 0, st>>>(A.n, V(T, o.a), A.c, A.h, A.w, gy, Y.c, Y.h, Y.w, o.k, o.s, dk);
+          launch_wgrad(st, A.c * Y.c, A.n, V(T, o.a), A.c, A.h, A.w, gy, Y.c, Y.h, Y.w, o.k, o.s, dk, c.num_sms,
+                       c.opt_wgrad_blk ? &T.wsw : nullptr);
         }
         if (float* db = PG(T, o.pb)) chsum(c, T, Y.n, Y.c, Y.h * Y.w, gy, db);
         if (float* dx = G(T, o.a)) {
@@ -799,7 +970,7 @@ void run_backward(Context& c) {
           T.tmp.ensure(A.size());
           float* tmp = T.tmp.p;
           const dim3 g((A.h * A.w + TB - 1) / TB, (A.c + CO - 1) / CO, A.n);
-          k_conv_fwd<<<g, TB, 0, st>>>(gy, Y.c, Y.h, Y.w, PV(T, o.pk), nullptr, A.c, o.k, o.s, A.h, A.w, tmp);
+          launch_conv(st, g, gy, Y.c, Y.h, Y.w, PV(T, o.pk), nullptr, A.c, o.k, o.s, A.h, A.w, tmp);
           k_acc<<<egrid(A.size()), TB, 0, st>>>(A.size(), tmp, dx);
         }
         break;

@@ -954,6 +954,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_stream = value != 0;
   else if (k == "wgrad_blk")
     ctx->opt_wgrad_blk = value != 0;
+  else if (k == "small_pw")
+    ctx->opt_small_pw = value != 0;
   else if (k == "vpre")
     ctx->opt_vpre = value != 0;
   else if (k == "adots_cp")

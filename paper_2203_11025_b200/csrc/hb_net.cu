@@ -227,6 +227,106 @@ __global__ void __launch_bounds__(CS_NT) k_conv_small(ConvArgs p) {
   }
 }
 
+// The same narrow convolution with the weights and bias passed by value in
+// the kernel parameter space (up to 32 KB on sm_70+): fully unrolled over
+// (ky, ci, kx, co), every weight is a compile-time constant-bank operand of its
+// FFMA, so the inner loop issues no weight loads (the smem-weight kernel above
+// spends ~2 LDS per FFMA and ran at 11-19 TFLOP/s).  Weight changes bump
+// g_alloc_gen (net_upload), which drops captured graphs holding old values.
+template <int CIN, int COUT>
+struct SmallW {
+  float w[9 * CIN * COUT];  // [(ky*3 + kx)][ci][co]
+  float b[COUT];
+};
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(CS_NT) k_conv_small_pw(ConvArgs p, const __grid_constant__ SmallW<CIN, COUT> wt) {
+  extern __shared__ __align__(16) float cs_sm[];
+  const int bz = blockIdx.z;
+  if (p.act && !p.act[bz]) return;
+  constexpr int cp = CIN | 1;
+  float* tile = cs_sm;  // [(TH+2)(TW+2)][cp]
+  const int tilesW = (p.W + CS_TW - 1) / CS_TW;
+  const int y0 = (blockIdx.x / tilesW) * CS_TH, x0 = (blockIdx.x % tilesW) * CS_TW;
+  const int t = threadIdx.x;
+  const float* A = p.a + bz * p.sa;
+  const float* Bsrc = p.b ? p.b + bz * p.sb : nullptr;
+  constexpr int npix = (CS_TH + 2) * (CS_TW + 2);
+  for (int pix = t; pix < npix; pix += CS_NT) {
+    const int gy = y0 + pix / (CS_TW + 2) - 1, gx = x0 + pix % (CS_TW + 2) - 1;
+    float* dst = tile + pix * cp;
+    if (gy >= 0 && gy < p.H && gx >= 0 && gx < p.W) {
+      const size_t px = size_t(gy) * p.W + gx;
+      const float* sa = A + px * p.ca;
+      if ((p.ca & 3) == 0) {
+        for (int c = 0; c < p.ca; c += 4) {
+          const float4 v = __ldg(reinterpret_cast<const float4*>(sa + c));
+          dst[c] = v.x;
+          dst[c + 1] = v.y;
+          dst[c + 2] = v.z;
+          dst[c + 3] = v.w;
+        }
+      } else {
+        for (int c = 0; c < p.ca; ++c) dst[c] = __ldg(sa + c);
+      }
+      if (p.cb) {
+        const float* sb = Bsrc + px * p.cb;
+        for (int c = 0; c < p.cb; ++c) dst[p.ca + c] = __ldg(sb + c);
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < CIN; ++c) dst[c] = 0.f;
+    }
+  }
+  __syncthreads();
+  const int ty = t / CS_TW, tx = t % CS_TW;
+  float acc[COUT];
+#pragma unroll
+  for (int co = 0; co < COUT; ++co) acc[co] = wt.b[co];
+#pragma unroll
+  for (int ky = 0; ky < 3; ++ky) {
+    const float* rp = tile + ((ty + ky) * (CS_TW + 2) + tx) * cp;
+#pragma unroll
+    for (int ci = 0; ci < CIN; ++ci) {
+      const float v0 = rp[ci], v1 = rp[cp + ci], v2 = rp[2 * cp + ci];
+#pragma unroll
+      for (int co = 0; co < COUT; ++co) {
+        acc[co] = fmaf(v0, wt.w[((ky * 3 + 0) * CIN + ci) * COUT + co], acc[co]);
+        acc[co] = fmaf(v1, wt.w[((ky * 3 + 1) * CIN + ci) * COUT + co], acc[co]);
+        acc[co] = fmaf(v2, wt.w[((ky * 3 + 2) * CIN + ci) * COUT + co], acc[co]);
+      }
+    }
+  }
+  const int y = y0 + ty, x = x0 + tx;
+  if (y >= p.H || x >= p.W) return;
+  float* O = p.out + ((size_t(bz) * p.H + y) * p.W + x) * COUT;
+  float r[COUT];
+#pragma unroll
+  for (int co = 0; co < COUT; ++co) r[co] = p.relu ? fmaxf(acc[co], 0.f) : acc[co];
+  if constexpr (COUT % 4 == 0) {
+#pragma unroll
+    for (int co = 0; co < COUT; co += 4)
+      *reinterpret_cast<float4*>(O + co) = make_float4(r[co], r[co + 1], r[co + 2], r[co + 3]);
+  } else {
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) O[co] = r[co];
+  }
+}
+
+template <int CIN, int COUT>
+bool conv_small_pw(Context& c, const ConvW& cw, const ConvArgs& p, dim3 g) {
+  if (cw.cin != CIN || cw.cout != COUT) return false;
+  SmallW<CIN, COUT> wt;
+  for (int co = 0; co < COUT; ++co) {
+    wt.b[co] = cw.b[size_t(co)];
+    for (int ci = 0; ci < CIN; ++ci)
+      for (int tap = 0; tap < 9; ++tap) wt.w[(tap * CIN + ci) * COUT + co] = cw.w[(size_t(co) * CIN + ci) * 9 + tap];
+  }
+  const size_t smem = size_t(CS_TH + 2) * (CS_TW + 2) * size_t(CIN | 1) * sizeof(float);
+  k_conv_small_pw<CIN, COUT><<<g, CS_NT, smem, c.stream>>>(p, wt);
+  return true;
+}
+
 // 2x2 max-pool / x2 bilinear upsample, NHWC, 4 channels per thread (C % 4 == 0);
 // one CTA per output row (grid (rows, B)), threads stride along the row
 __global__ void __launch_bounds__(256) k_maxpool2_v4(int H, int W, int C4, const float4* __restrict__ in,
@@ -412,10 +512,15 @@ static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int 
       HB_CUDA(cudaFuncSetAttribute(k_conv_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    if (cw.cout == 16)
+    const bool pw = c.opt_small_pw && (conv_small_pw<3, 16>(c, cw, p, g) || conv_small_pw<19, 16>(c, cw, p, g) ||
+                                       conv_small_pw<1, 16>(c, cw, p, g) || conv_small_pw<16, 2>(c, cw, p, g) ||
+                                       conv_small_pw<8, 2>(c, cw, p, g));
+    if (pw) {
+    } else if (cw.cout == 16) {
       k_conv_small<16><<<g, CS_NT, smem, c.stream>>>(p);
-    else
+    } else {
       k_conv_small<2><<<g, CS_NT, smem, c.stream>>>(p);
+    }
     HB_CUDA(cudaGetLastError());
     return;
   }
@@ -525,6 +630,7 @@ void net_upload(Context& c, int slot) {
     conv_tc_prepare(cw);
     conv_rows_prepare(cw);
   }
+  ++g_alloc_gen;  // the narrow convolutions carry their weights as kernel parameters: drop captured graphs
   n.dirty = false;
   if (slot == 1) c.ctx_valid = false;
 }

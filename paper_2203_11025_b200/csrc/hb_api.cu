@@ -961,7 +961,7 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
   else if (k == "adots_cp")
     ctx->opt_adots_cp = value != 0;
   else if (k == "adots_npt")
-    ctx->adots_npt = value >= 16 ? 16 : value >= 8 ? 8 : 4;
+    ctx->adots_npt = value >= 16 ? 16 : value >= 8 ? 8 : value <= 2 ? 2 : 4;
   else if (k == "staged_legs")
     ctx->opt_staged_legs = int(value);
   else if (k == "stream_e0")

@@ -857,7 +857,7 @@ void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, cons
     HB_CUDA(cudaGetLastError());
     return;
   }
-  auto k = npt == 16 ? k_adots<256, 16> : npt == 8 ? k_adots<256, 8> : k_adots<256, 4>;
+  auto k = npt == 16 ? k_adots<256, 16> : npt == 8 ? k_adots<256, 8> : npt == 2 ? k_adots<256, 2> : k_adots<256, 4>;
   launch_pdl(c, k, dim3(nb, B), dim3(256), 0, fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, Zj,
              w, V, c.kpart.p, c.kticket.p, gsum);
   HB_CUDA(cudaGetLastError());

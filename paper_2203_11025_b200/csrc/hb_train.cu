@@ -54,7 +54,7 @@ inline int nblk(size_t n) { return int(std::min<size_t>((n + TB - 1) / TB, size_
 // (conv2d, inc/autodiff.hpp:121-150: zero padding p = (k-1)/2, cross-correlation)
 constexpr int PX = 4;  // output pixels per thread along x (forward convolutions)
 
-template <int K, int S>
+template <int K, int S, int CO>
 __global__ void __launch_bounds__(TB) k_conv_fwd(const float* __restrict__ x, int cin, int H, int W,
                                                  const float* __restrict__ Kw, const float* __restrict__ bias, int cout,
                                                  int Ho, int Wo, float* __restrict__ y) {
@@ -106,21 +106,36 @@ __global__ void __launch_bounds__(TB) k_conv_fwd(const float* __restrict__ x, in
   }
 }
 
+// output channels per thread: the layer's count rounded up to 2 / 4, else 8
+template <int K, int S>
+void conv_co(cudaStream_t st, dim3 g, const float* x, int cin, int H, int W, const float* Kw, const float* bias,
+             int cout, int Ho, int Wo, float* y) {
+  if (cout <= 2) {
+    g.y = unsigned((cout + 1) / 2);
+    k_conv_fwd<K, S, 2><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  } else if (cout <= 4) {
+    g.y = 1;
+    k_conv_fwd<K, S, 4><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  } else {  // 16 channels per thread measured slower (registers)
+    g.y = unsigned((cout + 7) / 8);
+    k_conv_fwd<K, S, 8><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+  }
+}
 void launch_conv(cudaStream_t st, dim3 g, const float* x, int cin, int H, int W, const float* Kw, const float* bias,
                  int cout, int k, int s, int Ho, int Wo, float* y) {
   g.x = unsigned((Ho * ((Wo + PX - 1) / PX) + TB - 1) / TB);  // one thread per PX output pixels
   if (k == 5 && s == 2)
-    k_conv_fwd<5, 2><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+    conv_co<5, 2>(st, g, x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
   else if (k == 3 && s == 1)
-    k_conv_fwd<3, 1><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+    conv_co<3, 1>(st, g, x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
   else if (k == 5 && s == 1)
-    k_conv_fwd<5, 1><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+    conv_co<5, 1>(st, g, x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
   else if (k == 3 && s == 2)
-    k_conv_fwd<3, 2><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+    conv_co<3, 2>(st, g, x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
   else if (k == 1 && s == 1)
-    k_conv_fwd<1, 1><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+    conv_co<1, 1>(st, g, x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
   else if (k == 1 && s == 2)
-    k_conv_fwd<1, 2><<<g, TB, 0, st>>>(x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
+    conv_co<1, 2>(st, g, x, cin, H, W, Kw, bias, cout, Ho, Wo, y);
   else
     throw HbError{HB_ERR_ARG, "training supports 1x1, 3x3 and 5x5 kernels with stride 1 or 2"};
 }
@@ -130,7 +145,7 @@ void launch_conv(cudaStream_t st, dim3 g, const float* x, int cin, int H, int W,
 // Gather form with the kernel size and stride as template arguments: for
 // stride 2 only the taps of the output pixel's parity class reach it
 // (ky = (Y + p) mod 2, +2, ...), so a 5x5 tap loop visits 4-9 taps, not 25.
-template <int K, int S>
+template <int K, int S, int CO>
 __global__ void __launch_bounds__(TB) k_convT_fwd(const float* __restrict__ u, int ca, int h, int w,
                                                   const float* __restrict__ Kw, const float* __restrict__ bias, int cb,
                                                   int H, int W, float* __restrict__ z) {
@@ -189,21 +204,35 @@ __global__ void __launch_bounds__(TB) k_convT_fwd(const float* __restrict__ u, i
   }
 }
 
+template <int K, int S>
+void convT_co(cudaStream_t st, dim3 g, const float* u, int ca, int h, int w, const float* Kw, const float* bias, int cb,
+              int H, int W, float* z) {
+  if (cb <= 2) {
+    g.y = 1;
+    k_convT_fwd<K, S, 2><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  } else if (cb <= 4) {
+    g.y = 1;
+    k_convT_fwd<K, S, 4><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  } else {
+    g.y = unsigned((cb + 7) / 8);
+    k_convT_fwd<K, S, 8><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+  }
+}
 void launch_convT(cudaStream_t st, dim3 g, const float* u, int ca, int h, int w, const float* Kw, const float* bias,
                   int cb, int k, int s, int H, int W, float* z) {
   g.x = unsigned((H * ((W + s * PX - 1) / (s * PX)) * s + TB - 1) / TB);  // one thread per PX pixels of a parity class
   if (k == 5 && s == 2)
-    k_convT_fwd<5, 2><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+    convT_co<5, 2>(st, g, u, ca, h, w, Kw, bias, cb, H, W, z);
   else if (k == 3 && s == 1)
-    k_convT_fwd<3, 1><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+    convT_co<3, 1>(st, g, u, ca, h, w, Kw, bias, cb, H, W, z);
   else if (k == 5 && s == 1)
-    k_convT_fwd<5, 1><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+    convT_co<5, 1>(st, g, u, ca, h, w, Kw, bias, cb, H, W, z);
   else if (k == 3 && s == 2)
-    k_convT_fwd<3, 2><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+    convT_co<3, 2>(st, g, u, ca, h, w, Kw, bias, cb, H, W, z);
   else if (k == 1 && s == 1)
-    k_convT_fwd<1, 1><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+    convT_co<1, 1>(st, g, u, ca, h, w, Kw, bias, cb, H, W, z);
   else if (k == 1 && s == 2)
-    k_convT_fwd<1, 2><<<g, TB, 0, st>>>(u, ca, h, w, Kw, bias, cb, H, W, z);
+    convT_co<1, 2>(st, g, u, ca, h, w, Kw, bias, cb, H, W, z);
   else
     throw HbError{HB_ERR_ARG, "training supports 1x1, 3x3 and 5x5 kernels with stride 1 or 2"};
 }

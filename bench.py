@@ -141,14 +141,23 @@ def config_for(name):
 
 
 def columns(cfg, ws, rank, replicas):
-    """RHS of this rank: the config's own RHS block sharded by rank,
-    or R replicas of a single-RHS config."""
+    """RHS of this rank: the config's own RHS block sharded by rank (SURVEY 8(e);
+    uneven world sizes get contiguous np.array_split shards, a rank beyond B gets
+    none), or R replicas of a single-RHS config."""
     B = cfg["B"]
     if B > 1:
-        if B % ws == 0 and B >= ws:
-            return list(range(rank * B // ws, (rank + 1) * B // ws))
-        return list(range(B))
+        return [int(c) for c in np.array_split(np.arange(B), ws)[rank]]
     return [0] * replicas
+
+
+def sum_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], dtype=torch.float64, device="cuda" if torch.cuda.is_available() else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
 
 
 def make_solver(O, kind, cfg, arr):
@@ -160,14 +169,21 @@ def make_solver(O, kind, cfg, arr):
     return H, P, solve
 
 
+def ref_config(name):
+    """Config table for the CPU legs, loaded without importing the product."""
+    from oracle import problems as OP
+    return dict(OP.configs().CONFIGS[name])
+
+
 def cpu_baseline_sample(cfg_name, cfg):
     """The reference CPU path (oracle/_ref: the reference headers compiled in place)
     on a bounded sample: one full solve, one thread.  Falls back to the C
-    restatement ('port') if the reference build is absent."""
+    restatement ('port') if the reference build is absent.  Inputs come from the
+    oracle's generators (oracle/problems.py), bit-identical to the product's."""
     from oracle import oracle as O
-    from paper_2203_11025_b200 import problems
-    arr = problems.problem_arrays(cfg)
-    B = problems.rhs_block(arr)[:1]
+    from oracle import problems as OP
+    arr = OP.problem_arrays(cfg)
+    B = OP.rhs_block(arr)[:1]
     kind = "reference" if O.have_ref() else "port"
     H, P, solve = make_solver(O, kind, cfg, arr)
     # repeated full solves until ~10 s of CPU work (bounded sample)
@@ -178,21 +194,89 @@ def cpu_baseline_sample(cfg_name, cfg):
         dt = time.perf_counter() - t0
         if dt >= 10.0 or n >= 500:
             break
-    return {"value": n / dt, "unit": "solves/s", "cores": 1, "kind": kind,
+    return {"value": n / dt, "unit": "solves/s", "cores": 1, "kind": kind, "cpu": cpu_model(),
             "sample": f"{n} full {cfg_name} solves ({int(rep['iterations'][0])} FGMRES iterations each, "
                       f"converged={bool(rep['converged'][0])}) on 1 host thread, {dt:.2f} s"}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip() + f" ({os.cpu_count()} logical cpus)"
+    except OSError:
+        pass
+    return None
+
+
+# full-solve iteration counts used to extrapolate fixed-budget CPU times (BASELINE.md
+# 4.4): the reference's converged M_V counts on the BASELINE medium;
+# c4 is the survey's extrapolation (~1e4).  Labelled "extrapolated" in the output.
+MV_ITERS_FULL = {"c1": 346, "c2": 795, "c3": 1885, "c4": 10000}
+
+
+def cpu_reference_budget(name, iters):
+    """The reference CPU path on a fixed FGMRES budget of one column of config
+    `name` (1 host thread): seconds per iteration, plus a full-solve time
+    extrapolated with MV_ITERS_FULL (labelled as such)."""
+    from oracle import oracle as O
+    from oracle import problems as OP
+    cfg = ref_config(name)
+    arr = OP.problem_arrays(cfg)
+    kind = "reference" if O.have_ref() else "port"
+    t0 = time.perf_counter()
+    H, P = ref_preconditioner(O, kind, cfg, arr)
+    setup = time.perf_counter() - t0
+    B = OP.rhs_block(arr)[:1]
+    solve = O.ref_fgmres if kind == "reference" else O.fgmres
+    t0 = time.perf_counter()
+    X, rep = solve(P, B, restart=cfg["restart"], max_iters=iters, nthreads=1)
+    dt = time.perf_counter() - t0
+    its = max(1, int(rep["iterations"][0]))
+    out = {"kind": kind, "cores": 1, "cpu": cpu_model(), "iterations": its, "s": dt,
+           "ms_per_iteration": 1e3 * dt / its, "setup_s": setup,
+           "sample": f"{its} FGMRES iterations of 1 {name} column on 1 host thread"}
+    if name in MV_ITERS_FULL:
+        out["extrapolated_solve_s"] = dt / its * MV_ITERS_FULL[name]
+        out["extrapolation"] = (f"ms_per_iteration x {MV_ITERS_FULL[name]} iterations (the reference M_V count "
+                                "at this grid, SURVEY App. B) -- extrapolated, not measured")
+    del H, P
+    return out
+
+
+def ref_preconditioner(O, kind, cfg, arr):
+    """Hierarchy + preconditioner of config cfg on the CPU side (reference build or
+    the C restatement), including the config's nets with the same He seeds."""
+    pre = "Ref" if kind == "reference" else ""
+    Net = O.RefNet if kind == "reference" else O.UNet
+    net = enc = None
+    if cfg["net"] is not None:
+        L, base, seed, ctx_ch = cfg["net"]
+        net = Net(0, L, base, 3, ctx_ch, seed=seed)
+    if cfg["enc"] is not None:
+        L, base, seed = cfg["enc"]
+        enc = Net(1, L, base, 1, 0, seed=seed)
+    Hc = getattr(O, pre + "Hierarchy")
+    coarse_net = net if cfg["coarse"] == "net" else None
+    H = Hc(arr["kappa2"], arr["gamma"], arr["omega"], arr["lo"], arr["hi"], levels=cfg["levels"],
+           coarse=cfg["coarse"], coarse_iters=max(1, cfg["coarse_iters"]), coarse_net=coarse_net)
+    P = getattr(O, pre + "Precond")(cfg["precond"], H, net=net if cfg["precond"] != "v" else None, enc=enc)
+    P._keep = (net, enc, H)
+    return H, P
+
+
 def run_reference(args, ws, rank):
     """--impl reference: the reference's own CPU implementation (oracle/_ref) on all
-    host threads, one c0 solve per thread per step (replicas, as our arm)."""
+    host threads, one c0 solve per thread per step (replicas, as our arm).  Inputs
+    from the oracle's generators: this process never loads libhelmgpu.so."""
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2203_11025_b200 import problems
-    cfg = config_for(args.config)
-    arr = problems.problem_arrays(cfg)
-    Bfull = problems.rhs_block(arr)
+    from oracle import problems as OP
+    cfg = ref_config(args.config)
+    arr = OP.problem_arrays(cfg)
+    Bfull = OP.rhs_block(arr)
     threads = os.cpu_count() or 1
     kind = "reference" if O.have_ref() else "port"
     H, P, solve = make_solver(O, kind, cfg, arr)
@@ -214,8 +298,8 @@ def run_reference(args, ws, rank):
             "data": "synthetic (seeded media / point sources, SURVEY 8(d))", "impl": "reference",
             "config": {"workload": args.config, "grid": cfg["n"], "rhs_per_step": threads,
                        "iterations": iters[-1] if iters else None, "converged": all(conv),
-                       "note": "one independent solve per host thread per step"},
-            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": kind,
+                       "note": "one independent solve per host thread per step; inputs from oracle/problems.py"},
+            "cpu_baseline": {"value": value, "unit": "solves/s", "cores": threads, "kind": kind, "cpu": cpu_model(),
                              "sample": f"{threads} concurrent {args.config} solves per step x {args.steps} steps"},
             "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -325,7 +409,7 @@ def run_ours(args, ws, rank, local):
     t_ms = sum(max(e0.elapsed_time(e) for e in ends) for e0, ends in marks)
     barrier(ws)
     t_ms = max_over_ranks(t_ms, ws)
-    solves = nb * args.steps * ws
+    solves = sum_over_ranks(nb, ws) * args.steps  # distinct RHS over all ranks (uneven shards allowed)
     value = solves / (t_ms / 1e3)
 
     # ---- e2e: the public C ABI (hb_fgmres) on pinned host buffers; H2D of B and
@@ -538,7 +622,18 @@ def fixed_budget(name, local, args, ws, rank):
             row["tflops"] = v["flops"] / (v["ms"] / 1e3) / 1e12
         out["kernels"][k] = row
     ctx.close()
+    if rank == 0 and not args.no_cpu:
+        try:
+            cr = cpu_reference_budget(name, CPU_BUDGET.get(name, 1))
+            cr["speedup_per_iteration_per_rhs"] = (cr["ms_per_iteration"] / (out["ms_per_iteration"] / nb))
+            out["cpu_reference"] = cr
+        except Exception as e:  # reported, not hidden
+            out["cpu_reference"] = {"error": repr(e)}
     return out
+
+
+# FGMRES iterations of the CPU reference per `also` config (bounded: ~1-15 s each)
+CPU_BUDGET = {"c1": 3, "c2": 1, "c3": 1, "c4": 1}
 
 
 def datagen_budget(local, args):
@@ -709,6 +804,42 @@ def slab_budget(local, args, ws, rank):
     return out
 
 
+def spawn_ranks(n):
+    """`bench.py --gpus N` without a launcher: start N ranks of this script (one per
+    GPU, LOCAL_RANK = i) with torchrun's environment, rank 0's stdout is the JSON
+    line.  NCCL's init log stays on (NCCL_DEBUG=INFO on stderr) so the ranks are
+    visible."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    procs = []
+    for i in range(n):
+        env = dict(os.environ, WORLD_SIZE=str(n), RANK=str(i), LOCAL_RANK=str(i), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env,
+                                      stdout=None if i == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
+def dry_run(args, ws, rank):
+    """Host plumbing only (CPU, gloo): rank -> column partition, barriers,
+    max-over-ranks timing and the solve count -- used by the CPU test of the
+    self-launch path.  Prints a line marked dry_run (not a measurement)."""
+    cfg = ref_config(args.config)
+    cols = columns(cfg, ws, rank, args.replicas or 3)
+    barrier(ws)
+    t = max_over_ranks(1.0 + rank, ws)
+    solves = sum_over_ranks(len(cols), ws)
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": ws, "config": {"workload": args.config}, "rhs_total": solves,
+                          "rank0_columns": cols, "max_over_ranks": t}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -725,12 +856,19 @@ def main():
     ap.add_argument("--groups", type=int, default=3, help="independent column groups (solver contexts on their own "
                                                           "streams and host threads) per GPU")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--dry-run", action="store_true", help="host plumbing only (no GPU work; CPU test of --gpus N)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(spawn_ranks(args.gpus))
     ws, rank, local = dist_init()
-    if args.impl == "reference":
+    if args.dry_run:
+        dry_run(args, ws, rank)
+    elif args.impl == "reference":
         run_reference(args, ws, rank)
     else:
+        if ws != args.gpus and rank == 0:
+            print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE {ws}; measuring {ws} GPU(s)", file=sys.stderr)
         run_ours(args, ws, rank, local)
     if ws > 1:
         import torch.distributed as dist

@@ -64,6 +64,7 @@ int hb_set_problem(hb_ctx* ctx, int nx, int ny, double h, double omega, const do
 #define HB_COARSE_GMRES 0  /* GMRES(coarse_iters) with D^-1, inc/multigrid.hpp:45-61 */
 #define HB_COARSE_JACOBI 1 /* coarse_iters damped-Jacobi sweeps */
 #define HB_COARSE_NET 2    /* U-Net in net slot 0 as coarsest solver */
+#define HB_COARSE_DENSE 3  /* exact solve, CoarseSolver::dense (inc/multigrid.hpp:84,95-104); coarsest <= 1024 nodes */
 
 typedef struct hb_vcycle_cfg {
   int levels;          /* >= 2 (inc/multigrid.hpp:73) */
@@ -127,7 +128,9 @@ typedef struct hb_krylov_cfg {
   int restart;    /* m */
   int max_iters;  /* preconditioner applications per column */
   double rel_tol; /* in (0, 1) */
-  int flexible;   /* must be 1 (device path stores Z) */
+  int flexible;   /* 1: flexible GMRES (x += Z y); 0: standard right-preconditioned GMRES
+                     (x += M (V y), inc/krylov.hpp:127-136), stationary preconditioners only
+                     (HB_ERR_ARG otherwise, check_flexible_contract, inc/precond.hpp:29-32) */
 } hb_krylov_cfg;
 
 /* Solve A X = B for `batch` independent columns (block_fgmres semantics).

@@ -51,10 +51,10 @@ class Context {
   void set_problem(const HelmholtzProblem& p, const VCycleConfig& vc, int coarse_solver_override = -1) {
     check(c_, hb_set_problem(c_, p.grid.nx, p.grid.ny, p.grid.h, p.omega, p.kappa2.values.v.data(),
                              p.gamma.values.v.data(), p.kappa2.lo, p.kappa2.hi));
-    hb_vcycle_cfg cfg{vc.levels, vc.nu1, vc.nu2, vc.damping, vc.shift.alpha, vc.shift.beta,
-                      coarse_solver_override >= 0 ? coarse_solver_override : HB_COARSE_GMRES, vc.coarse_iters};
-    if (vc.coarse_solver == CoarseSolver::dense && coarse_solver_override < 0)
-      throw std::invalid_argument("CoarseSolver::dense is a test-only path; not offered on the device");
+    const int coarse = coarse_solver_override >= 0                   ? coarse_solver_override
+                       : vc.coarse_solver == CoarseSolver::dense ? HB_COARSE_DENSE
+                                                                   : HB_COARSE_GMRES;
+    hb_vcycle_cfg cfg{vc.levels, vc.nu1, vc.nu2, vc.damping, vc.shift.alpha, vc.shift.beta, coarse, vc.coarse_iters};
     check(c_, hb_build_hierarchy(c_, &cfg));
     nx_ = p.grid.nx;
     ny_ = p.grid.ny;
@@ -179,6 +179,9 @@ inline GpuUnetVCycle make_unet_vcycle(const HelmholtzProblem& problem, const VCy
 
 // Device-resident block FGMRES with A = A^h of the context's problem and M =
 // the plugin; same contract and SolveReport as inc/krylov.hpp:83-267.
+// cfg.flexible = false runs standard right-preconditioned GMRES (x += M V y,
+// inc/krylov.hpp:127-136) on the device; network preconditioners throw
+// std::invalid_argument there, as check_flexible_contract does.
 inline std::pair<std::vector<ComplexField>, SolveReport> block_fgmres(GpuPreconditioner& M,
                                                                       const std::vector<ComplexField>& B,
                                                                       const KrylovConfig& cfg,
@@ -197,7 +200,7 @@ inline std::pair<std::vector<ComplexField>, SolveReport> block_fgmres(GpuPrecond
   std::vector<double> hist(size_t(nb) * cap);
   std::vector<int> hl(nb), it(nb);
   std::vector<uint8_t> cv(nb), bk(nb);
-  hb_krylov_cfg kc{cfg.restart, cfg.max_iters, cfg.rel_tol, 1};
+  hb_krylov_cfg kc{cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.flexible ? 1 : 0};
   check(c.get(), hb_fgmres(c.get(), &kc, M.kind(), nb, b.data(), X0 ? x0.data() : nullptr, x.data(), hist.data(),
                            cap, hl.data(), it.data(), cv.data(), bk.data()));
   SolveReport rep;
@@ -208,6 +211,40 @@ inline std::pair<std::vector<ComplexField>, SolveReport> block_fgmres(GpuPrecond
   rep.converged.assign(cv.begin(), cv.end());
   rep.breakdown.assign(bk.begin(), bk.end());
   return {detail::unpack(x, nb, c.nx(), c.ny()), std::move(rep)};
+}
+
+// The reference signature block_fgmres(apply_A, apply_M, B, cfg, X0)
+// (inc/krylov.hpp:83-86) with M a device plugin.  The device solve applies
+// A^h of M's context itself, so apply_A must BE that operator: it is probed
+// once on a seeded random field against hb_operator_apply (relative L2
+// difference <= 1e-5: the device applies it in complex64) and a different operator is rejected with std::invalid_argument
+// (no host-callback Krylov path exists on the device).
+inline std::pair<std::vector<ComplexField>, SolveReport> block_fgmres(const BatchedOp& apply_A,
+                                                                      GpuPreconditioner& M,
+                                                                      const std::vector<ComplexField>& B,
+                                                                      const KrylovConfig& cfg,
+                                                                      const std::vector<ComplexField>* X0 = nullptr) {
+  Context& c = M.context();
+  if (!B.empty()) {
+    Rng rng(0x5eedULL);
+    ComplexField u(c.nx(), c.ny());
+    for (auto& z : u.v) z = Complex(rng.normal(), rng.normal());
+    const auto host = apply_A(std::vector<ComplexField>{u});
+    if (host.size() != 1 || host[0].nx != c.nx() || host[0].ny != c.ny())
+      throw std::invalid_argument("apply_A returned a batch of the wrong shape");
+    const auto in = detail::pack({u});
+    std::vector<double> dev(in.size());
+    check(c.get(), hb_operator_apply(c.get(), 0, 0, 1, in.data(), dev.data()));
+    double num = 0.0, den = 0.0;
+    for (std::size_t i = 0; i < host[0].v.size(); ++i) {
+      const Complex d(dev[2 * i], dev[2 * i + 1]);
+      num += std::norm(host[0].v[i] - d);
+      den += std::norm(host[0].v[i]);
+    }
+    if (!(num <= 1e-10 * den))
+      throw std::invalid_argument("apply_A is not the Helmholtz operator A^h of the preconditioner's problem");
+  }
+  return block_fgmres(M, B, cfg, X0);
 }
 
 }  // namespace gpu

@@ -326,6 +326,8 @@ def ref():
         R.hr_rng_u64.argtypes = [C.c_uint64, C.c_int64, C.POINTER(C.c_uint64)]
         R.hr_absorbing_layer.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, _dp]
         R.hr_restrict.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp]
+        R.hr_synthetic_slowness.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_double, C.c_double, _dp]
+        R.hr_random_rhs_block.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, _dp]
         R.hr_prolong.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, _dp, _dp]
         R.hr_mg_create.restype = _vp
         R.hr_mg_create.argtypes = [C.c_int, C.c_int, C.c_double, _dp, _dp, C.c_double, C.c_double, C.c_int,
@@ -383,6 +385,20 @@ def ref():
         R.hr_init()
         _ref = R
     return _ref
+
+
+def ref_synthetic_slowness(seed, nx, ny, lo=0.25, hi=1.0):
+    """inc/datagen.hpp:94-119 (the reference build)."""
+    out = np.zeros((ny, nx))
+    _rcheck(ref().hr_synthetic_slowness(seed, nx, ny, lo, hi, _p(out)))
+    return out
+
+
+def ref_random_rhs_block(nx, ny, count, seed):
+    """inc/bench.hpp:83-90 (the reference build)."""
+    out = np.zeros((count, ny, nx), np.complex128)
+    _rcheck(ref().hr_random_rhs_block(nx, ny, count, seed, cptr(out)))
+    return out
 
 
 def _rcheck(rc):

@@ -17,6 +17,7 @@
 #include <optional>
 #include <thread>
 
+#include "helmbench/bench.hpp"
 #include "helmbench/checkpoint.hpp"
 #include "helmbench/datagen.hpp"
 #include "helmbench/grid.hpp"
@@ -238,6 +239,22 @@ HR_EXPORT int hr_absorbing_layer(int nx, int ny, int width, double gmax, double*
   HR_TRY({
     auto att = make_absorbing_layer(make_grid(nx, ny, 1), width, gmax);
     std::memcpy(out, att.values.v.data(), sizeof(double) * att.values.v.size());
+  })
+}
+
+// synthetic_slowness (inc/datagen.hpp:94-119): the media of the reference's
+// acceptance gates (tests/acceptance.cpp:62-67,184-186)
+HR_EXPORT int hr_synthetic_slowness(uint64_t seed, int nx, int ny, double lo, double hi, double* out) {
+  HR_TRY({
+    auto s = synthetic_slowness(seed, make_grid(nx, ny, 1), SlownessRange{lo, hi});
+    std::memcpy(out, s.values.v.data(), sizeof(double) * s.values.v.size());
+  })
+}
+// random_rhs_block (inc/bench.hpp:83-90): count c128 fields [count][ny][nx]
+HR_EXPORT int hr_random_rhs_block(int nx, int ny, int count, uint64_t seed, double* out) {
+  HR_TRY({
+    auto B = random_rhs_block(make_grid(nx, ny, 1), count, seed);
+    for (int c = 0; c < count; ++c) from_field(B[size_t(c)], out + size_t(c) * 2 * nx * ny);
   })
 }
 

@@ -100,6 +100,59 @@ static void from_c64(const std::vector<float2>& v, double* p) {
   }
 }
 
+// CoarseSolver::dense setup: assemble M^H as assemble_dense does
+// (inc/multigrid.hpp:24-42), invert it by Gauss-Jordan elimination with partial
+// pivoting in fp64 (the reference factors it once with PartialPivLU, :84, and
+// solves per call, :95-104), upload the inverse
+static void build_dense_inverse(Level& L, double omega, double alpha, double beta) {
+  const int nx = L.nx, ny = L.ny, n = nx * ny;
+  if (n > 1024) throw HbError{HB_ERR_ARG, "dense coarse solver: coarsest grid larger than 32x32 nodes"};
+  using cd = std::complex<double>;
+  const double inv_h2 = 1.0 / (L.h * L.h);
+  const cd sh(alpha, -beta);
+  std::vector<cd> A(size_t(n) * n, cd(0.0)), I(size_t(n) * n, cd(0.0));
+  for (int iy = 0; iy < ny; ++iy)
+    for (int ix = 0; ix < nx; ++ix) {
+      const size_t i = size_t(iy) * nx + ix;
+      const cd damp(1.0, -L.gam[i]);
+      A[i * n + i] = 4.0 * inv_h2 - omega * omega * L.k2[i] * sh * damp;
+      if (ix > 0) A[i * n + i - 1] = -inv_h2;
+      if (ix + 1 < nx) A[i * n + i + 1] = -inv_h2;
+      if (iy > 0) A[i * n + i - nx] = -inv_h2;
+      if (iy + 1 < ny) A[i * n + i + nx] = -inv_h2;
+      I[i * n + i] = 1.0;
+    }
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    for (int r = k + 1; r < n; ++r)
+      if (std::abs(A[size_t(r) * n + k]) > std::abs(A[size_t(piv) * n + k])) piv = r;
+    if (std::abs(A[size_t(piv) * n + k]) == 0.0) throw HbError{HB_ERR_NUMERIC, "dense coarse operator is singular"};
+    if (piv != k)
+      for (int j = 0; j < n; ++j) {
+        std::swap(A[size_t(k) * n + j], A[size_t(piv) * n + j]);
+        std::swap(I[size_t(k) * n + j], I[size_t(piv) * n + j]);
+      }
+    const cd d = 1.0 / A[size_t(k) * n + k];
+    for (int j = 0; j < n; ++j) {
+      A[size_t(k) * n + j] *= d;
+      I[size_t(k) * n + j] *= d;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == k) continue;
+      const cd f = A[size_t(r) * n + k];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        A[size_t(r) * n + j] -= f * A[size_t(k) * n + j];
+        I[size_t(r) * n + j] -= f * I[size_t(k) * n + j];
+      }
+    }
+  }
+  std::vector<double2> h(size_t(n) * n);
+  for (size_t i = 0; i < h.size(); ++i) h[i] = make_double2(I[i].real(), I[i].imag());
+  L.dinv.ensure(h.size());
+  HB_CUDA(cudaMemcpy(L.dinv.p, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
+}
+
 static void require_hier(Context& c) {
   if (!c.has_hier) throw HbError{HB_ERR_STATE, "hierarchy not built (hb_build_hierarchy)"};
 }
@@ -204,6 +257,9 @@ void coarsest_solve(Context& c, int B, int c0, const int* act, const float2* f, 
       }
       break;
     }
+    case HB_COARSE_DENSE:  // exact coarsest solve (inc/multigrid.hpp:84,95-104)
+      launch_coarse_dense(c, L, B, act, f, out);
+      break;
     case HB_COARSE_NET: {  // A4: U-Net on [H^2 Re f, H^2 Im f, kappa^2]
       if (c0 != 0) throw HbError{HB_ERR_STATE, "split V-cycle with a net coarse solver"};
       Net& n = c.nets[0];
@@ -390,6 +446,13 @@ void precond_apply_dev(Context& c, int kind, int B, const int* act, const float2
 }
 
 // ------------------------------------------------------------- FGMRES --
+// name() / requires_flexible() of the reference plugins (inc/precond.hpp:14-27):
+// network-based preconditioners are non-stationary (inc/precond.hpp:132,160)
+static const char* precond_name(int kind) { return kind == HB_PC_VU ? "vu" : kind == HB_PC_JU ? "ju" : "v"; }
+static bool requires_flexible(const Context& c, int kind) {
+  return kind == HB_PC_VU || kind == HB_PC_JU || c.vc.coarse_solver == HB_COARSE_NET;
+}
+
 static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, const double2* dB, double2* dX,
                        double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv, uint8_t* brk,
                        const int* d_limits = nullptr) {
@@ -397,7 +460,12 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
   if (!cfg) throw HbError{HB_ERR_ARG, "null krylov config"};
   if (cfg->restart < 1) throw HbError{HB_ERR_ARG, "restart must be >= 1"};
   if (!(cfg->rel_tol > 0.0 && cfg->rel_tol < 1.0)) throw HbError{HB_ERR_ARG, "rel_tol in (0,1)"};
-  if (!cfg->flexible) throw HbError{HB_ERR_ARG, "the device FGMRES stores Z: flexible must be 1"};
+  // flexible = 0: standard right-preconditioned GMRES (inc/krylov.hpp:127-136) --
+  // same Arnoldi, x += M (V y) at the end of each cycle; the preconditioner must be
+  // stationary (check_flexible_contract, inc/precond.hpp:29-32)
+  const bool flexible = cfg->flexible != 0;
+  if (!flexible && requires_flexible(c, kind))
+    throw HbError{HB_ERR_ARG, std::string("preconditioner ") + precond_name(kind) + " requires flexible = true"};
   if (B < 1) throw HbError{HB_ERR_ARG, "batch must be >= 1"};
   ensure_batch(c, B);
   const int m = cfg->restart;
@@ -428,7 +496,14 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
       launch_fg_update(c, B, j, m, c.kW.p, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
     }
     prof_active();
-    launch_fg_finalize(c, B, m, c.kZ.p, dX);
+    if (flexible) {
+      launch_fg_finalize(c, B, m, c.kZ.p, dX);
+    } else {
+      c.kfin.ensure(B);
+      launch_fg_finalize_v(c, B, c.kV.p, c.kW.p, c.kfin.p);
+      precond_apply_dev(c, kind, B, c.kfin.p, c.kW.p, nullptr, c.kZ.p);
+      launch_fg_add_to_x(c, B, c.kfin.p, c.kZ.p, dX);
+    }
     launch_fg_restart(c, B, dB, dX, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
     c.prof_scale = 1.0;
   };
@@ -444,7 +519,7 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
     // one CUDA graph per restart cycle: m inner steps + finalize + next restart
     Context::GraphEntry* ge = nullptr;
     for (auto& g : c.graphs)
-      if (g.gen == g_alloc_gen && g.kind == kind && g.B == B && g.m == m && g.cap == cap &&
+      if (g.gen == g_alloc_gen && g.kind == kind && g.B == B && g.m == m && g.cap == cap && g.flexible == flexible &&
           g.max_iters == cfg->max_iters && g.tol == cfg->rel_tol && g.dB == dB && g.dX == dX)
         ge = &g;
     bool more = true;
@@ -471,7 +546,7 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
       HB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
       HB_CUDA(cudaGraphDestroy(graph));
       c.graphs.push_back(Context::GraphEntry{g_alloc_gen, kind, B, m, cap, cfg->max_iters, cfg->rel_tol, dB, dX,
-                                             exec, per_cycle});
+                                             exec, per_cycle, flexible});
       ge = &c.graphs.back();
     }
     while (more) {
@@ -665,6 +740,7 @@ int hb_build_hierarchy(hb_ctx* ctx, const hb_vcycle_cfg* cfg) {
   for (size_t l = 0; l < ctx->levels.size(); ++l)
     fill_level_device(*ctx->levels[l], ctx->omega, cfg->alpha, cfg->beta, cfg->damping, l == 0,
                       l == int(ctx->levels.size()) - 1);
+  if (cfg->coarse_solver == HB_COARSE_DENSE) build_dense_inverse(*ctx->levels.back(), ctx->omega, cfg->alpha, cfg->beta);
   ctx->has_hier = true;
   HB_API_END
 }
@@ -798,13 +874,9 @@ int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* 
   HB_API_END
 }
 
-const char* hb_precond_name(int kind) { return kind == HB_PC_VU ? "vu" : kind == HB_PC_JU ? "ju" : "v"; }
+const char* hb_precond_name(int kind) { return precond_name(kind); }
 
-int hb_precond_requires_flexible(hb_ctx* ctx, int kind) {
-  if (!ctx) return 1;
-  // network-based preconditioners are non-stationary (inc/precond.hpp:132,160)
-  return kind == HB_PC_VU || kind == HB_PC_JU || ctx->vc.coarse_solver == HB_COARSE_NET;
-}
+int hb_precond_requires_flexible(hb_ctx* ctx, int kind) { return !ctx || requires_flexible(*ctx, kind) ? 1 : 0; }
 
 int hb_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,
               double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
@@ -958,10 +1030,6 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_small_pw = value != 0;
   else if (k == "vpre")
     ctx->opt_vpre = value != 0;
-  else if (k == "adots_cp")
-    ctx->opt_adots_cp = value != 0;
-  else if (k == "adots_npt")
-    ctx->adots_npt = value >= 16 ? 16 : value >= 8 ? 8 : value <= 2 ? 2 : 4;
   else if (k == "staged_legs")
     ctx->opt_staged_legs = int(value);
   else if (k == "stream_e0")

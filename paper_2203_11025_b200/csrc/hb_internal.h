@@ -94,6 +94,7 @@ struct Level {
   DBuf<float2> dM, dA, wdi;
   DBuf<double2> dA64;  // level 0: fp64 diagonal of A^h for the restart residual
   DBuf<double2> dM64;  // coarsest level: fp64 diagonal of M^H (multi-CTA coarse GMRES restart)
+  DBuf<double2> dinv;  // coarsest level, CoarseSolver::dense: (M^H)^-1 row-major fp64
   DBuf<float> k2f;
   // V-cycle work buffers [B][N]
   DBuf<float2> f, v, t, x;
@@ -145,6 +146,7 @@ void launch_residual_restrict(Context& c, const LevelView& L, int offset, int B,
 void launch_prolong_add(Context& c, const LevelView& Lf, int cnx, int cny, int offset, int B, const int* act,
                         const float2* vc, float2* v);
 void launch_restrict_plain(Context& c, int nx, int ny, int offset, int B, const float2* fine, float2* coarse);
+void launch_coarse_dense(Context& c, const Level& L, int B, const int* act, const float2* f, float2* x);
 void launch_coarse_gmres(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
                          float2* x, float2* scratch);
 // coarsest GMRES(iters) with D^-1 on the multi-CTA Krylov kernels (hb_krylov.cu), large coarse grids
@@ -208,6 +210,9 @@ void launch_fg_adots_finish(Context& c, int B, int j, const double2* gsum);
 void launch_fg_update_finish(Context& c, int B, int j, int m, const double2* gsum, int hist_cap, double rel_tol,
                              int max_iters);
 void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x);
+// non-flexible (standard right-preconditioned) GMRES: u = V y, fin[b] = k > 0; then x += z
+void launch_fg_finalize_v(Context& c, int B, const float2* V, float2* u, int* fin);
+void launch_fg_add_to_x(Context& c, int B, const int* fin, const float2* z, double2* x);
 void krylov_report(Context& c, int B, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv,
                    uint8_t* brk);
 
@@ -261,6 +266,7 @@ struct Context {
   // Krylov
   DBuf<char> kstate;         // ColState[B]
   DBuf<double2> kpart;       // per-CTA partials
+  DBuf<int> kfin;            // non-flexible finalize: columns with k > 0
   DBuf<double> khist;        // [B][hist_cap]
   DBuf<int> kact;            // per-column: active in the current inner step
   DBuf<int> klimit;          // per-column iteration limits (training-pair generation)
@@ -288,11 +294,10 @@ struct Context {
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
        opt_coarse_reg = true, opt_wide_legs = false,
-       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_pdl = true, opt_stream_e0 = true, opt_adots_cp = false, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
+       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size
   int opt_legs_wd = 2;  // Jacobi factor in the legs: 0 stored wD^-1, 1 from D, 2 by working-set size
   int conv_rows_ring = 4;
-  int adots_npt = 4;  // nodes per thread per tile of the Krylov dots kernel (4 | 8 | 16)
   int coarse_threads = 256;  // CTA size of the CTA-resident coarse GMRES (256 | 512 | 1024)
   // captured FGMRES cycle graphs
   struct GraphEntry {
@@ -302,6 +307,7 @@ struct Context {
     const void *dB, *dX;
     cudaGraphExec_t exec;
     int64_t launches;
+    bool flexible;
   };
   std::vector<GraphEntry> graphs;
   // net activations

@@ -354,162 +354,6 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
   adots_scalar(st[b], j, red);
 }
 
-__device__ __forceinline__ void cpa8(float2* dst, const float2* src, bool ok) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(s), "l"(src), "r"(ok ? 8 : 0) : "memory");
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// k_adots with the basis groups double-buffered in shared memory: each thread
-// cp.asyncs ITS OWN nodes of group g+1 (so no CTA barrier is needed) while it
-// reduces group g, keeping loads in flight through the butterflies.
-// dynamic smem: 2 stages x 4 vectors x NPT x NT float2
-template <int NT, int NPT>
-__global__ void __launch_bounds__(NT) k_adots_cp(FineView F, int B, int j, ColState* st, const int* act,
-                                              const float2* __restrict__ Z, float2* __restrict__ W,
-                                              const float2* __restrict__ V, double2* part, unsigned* ticket,
-                                              double2* gsum) {
-  pdl_enter();
-  const int b = blockIdx.y;
-  if (!act[b]) return;
-  const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
-  const size_t BN = size_t(B) * NS;
-  const float2* zb = Z + b * NS + OFF;
-  float2* wb = W + b * NS + OFF;
-  const float2* dA = F.dA + OFF;
-  V += OFF;
-  const float2* Vj = V + size_t(j) * BN + b * NS;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = 2 * j + 1;
-  const float inv_h2 = float(F.inv_h2);
-  // wpart[warp][float]: dots of basis i at floats 2i, 2i+1; Gram k at 2*kMaxRestart + 2k
-  __shared__ float wpart[NT / 32][4 * kMaxRestart + 8];
-  for (int t = threadIdx.x; t < (NT / 32) * (4 * kMaxRestart + 8); t += NT) (&wpart[0][0])[t] = 0.f;
-  __syncthreads();
-  constexpr int TILE = NT * NPT;
-  for (size_t base = size_t(blockIdx.x) * TILE; base < N; base += size_t(gridDim.x) * TILE) {
-    float2 w[NPT], vj[NPT];
-    bool ok[NPT];
-#pragma unroll
-    for (int q = 0; q < NPT; ++q) {
-      const size_t p = base + q * NT + threadIdx.x;
-      ok[q] = p < N;
-      if (ok[q]) {
-        const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
-        w[q] = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
-        wb[p] = w[q];
-        vj[q] = ld(Vj, p);
-      } else {
-        w[q] = vj[q] = make_float2(0.f, 0.f);
-      }
-    }
-    extern __shared__ float2 ring[];  // [2][4][NPT][NT]
-    auto issue = [&](int i0, int stg) {
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2* Vi = V + size_t(min(i0 + u, j)) * BN + b * NS;
-#pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-          const bool okq = ok[q] && i0 + u <= j;
-          const size_t p = okq ? base + q * NT + threadIdx.x : 0;
-          cpa8(&ring[((stg * 4 + u) * NPT + q) * NT + threadIdx.x], Vi + p, okq);
-        }
-      }
-      cpa_commit();
-    };
-    issue(0, 0);
-    for (int i0 = 0, g = 0; i0 <= j; i0 += 4, ++g) {
-      const bool more = i0 + 4 <= j;
-      if (more) {
-        issue(i0 + 4, (g + 1) & 1);
-        cpa_wait<1>();
-      } else {
-        cpa_wait<0>();
-      }
-      float2 a[4][NPT];
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int q = 0; q < NPT; ++q) a[u][q] = ring[(((g & 1) * 4 + u) * NPT + q) * NT + threadIdx.x];
-      float v[16];  // [0..7] dots of i0..i0+3, [8..15] Gram
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float dr = 0.f, di = 0.f, gr = 0.f, gi = 0.f;
-#pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-          const float2 ai = a[u][q], c = w[q], e = vj[q];
-          dr = fmaf(ai.x, c.x, fmaf(ai.y, c.y, dr));
-          di = fmaf(ai.x, c.y, fmaf(-ai.y, c.x, di));
-          gr = fmaf(e.x, ai.x, fmaf(e.y, ai.y, gr));
-          gi = fmaf(e.x, ai.y, fmaf(-e.y, ai.x, gi));
-        }
-        v[2 * u] = dr;
-        v[2 * u + 1] = di;
-        v[8 + 2 * u] = gr;
-        v[8 + 2 * u + 1] = gi;
-      }
-      // 16-float reduce-scatter: 4 halving stages, then a pairwise allreduce
-#pragma unroll
-      for (int stage = 0; stage < 4; ++stage) {
-        const int half = 8 >> stage, mask = 16 >> stage;
-        const bool upper = (lane & mask) != 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (k < half) {
-            const float send = upper ? v[k] : v[k + half];
-            const float keep = upper ? v[k + half] : v[k];
-            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-          }
-        }
-      }
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-      if ((lane & 1) == 0) {
-        const int fidx = lane >> 1;  // float index in the group's 16
-        const int u = (fidx & 7) >> 1, comp = fidx & 1;
-        const int i = i0 + u;
-        if (fidx < 8) {
-          if (i <= j) wpart[warp][2 * i + comp] += v[0];
-        } else {
-          if (i < j) wpart[warp][2 * kMaxRestart + 2 * i + comp] += v[0];
-        }
-      }
-    }
-  }
-  __syncthreads();
-  constexpr int HS = kMaxRestart;
-  // fold warps in fp64: slot s <- floats 2s, 2s+1 (dots s <= j at s, Gram k < j at HS + k)
-  __shared__ double2 red[KMAXV];
-  for (int t = threadIdx.x; t < nv; t += NT) {
-    const int slot = t <= j ? t : HS + (t - j - 1);
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (int w2 = 0; w2 < NT / 32; ++w2) {
-      acc.x += wpart[w2][2 * slot];
-      acc.y += wpart[w2][2 * slot + 1];
-    }
-    red[t] = acc;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < nv; t += NT) part[(size_t(b) * gridDim.x + blockIdx.x) * KMAXV + t] = red[t];
-  if (!last_cta(ticket, b, gridDim.x)) return;
-  for (int t = threadIdx.x; t < nv; t += NT) {
-    double2 s = make_double2(0.0, 0.0);
-    for (unsigned q = 0; q < gridDim.x; ++q) {
-      const volatile double2* pp = part + (size_t(b) * gridDim.x + q) * KMAXV + t;
-      s.x += pp->x;
-      s.y += pp->y;
-    }
-    red[t] = s;
-    if (gsum) gsum[size_t(b) * KMAXV + t] = s;
-  }
-  if (gsum) return;
-  adots_scalar(st[b], j, red);
-}
-
 __global__ void k_adots_finish(int j, ColState* st, const int* act, const double2* gsum) {
   const int b = blockIdx.x;
   if (!act[b]) return;
@@ -714,19 +558,11 @@ __device__ void update_scalar(ColState& S, int b, int j, int m, double t, int* a
   if (lane <= j + 1) S.H[j][lane] = hcol[lane];
 }
 
-// y = R^-1 g (back-substitution, inc/krylov.hpp:119-126); x += sum_i y_i Z_i
-__global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st, const float2* __restrict__ Z,
-                                                 double2* __restrict__ x) {
-  pdl_enter();
-  const int b = blockIdx.y;
-  const ColState& S = st[b];
-  const int k = S.k;
-  if (k == 0) return;
-  // stage R (upper k x k of the rotated Hessenberg) and g, then warp 0 runs a
-  // column-sweep back-substitution (krylov.hpp:119-126) with lanes in parallel
-  __shared__ double2 sH[kMaxRestart][kMaxRestart];  // sH[col][row]
-  __shared__ double2 y[kMaxRestart];
-  for (int t = threadIdx.x; t < k * k; t += KT) {
+// y = R^-1 g (back-substitution, inc/krylov.hpp:119-126) into shared y[0..k):
+// stage R (upper k x k of the rotated Hessenberg) and g, then warp 0 runs a
+// column-sweep back-substitution with lanes in parallel (whole CTA calls)
+__device__ void solve_small(const ColState& S, int k, double2 (*sH)[kMaxRestart], double2* y) {
+  for (int t = threadIdx.x; t < k * k; t += blockDim.x) {
     const int col = t / k, row = t % k;
     if (row <= col) sH[col][row] = S.H[col][row];
   }
@@ -745,6 +581,66 @@ __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st
     }
   }
   __syncthreads();
+}
+
+// standard (non-flexible) right-preconditioned GMRES finalize, first half
+// (inc/krylov.hpp:127-136): u = sum_i y_i V_i (V_i = s_i Vraw_i) into u (c64);
+// fin[b] = 1 for columns with k > 0 -- the caller applies M to u on those and
+// adds the result to x (k_add_to_x)
+__global__ void __launch_bounds__(KT) k_finalize_v(FineView F, int B, ColState* st, const float2* __restrict__ V,
+                                                   float2* __restrict__ u, int* fin) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  const ColState& S = st[b];
+  const int k = S.k;
+  if (blockIdx.x == 0 && threadIdx.x == 0) fin[b] = k > 0;
+  if (k == 0) return;
+  __shared__ double2 sH[kMaxRestart][kMaxRestart];  // sH[col][row]
+  __shared__ double2 y[kMaxRestart];
+  solve_small(S, k, sH, y);
+  if (threadIdx.x < k) y[threadIdx.x] = make_double2(y[threadIdx.x].x * S.scale[threadIdx.x],
+                                                     y[threadIdx.x].y * S.scale[threadIdx.x]);
+  __syncthreads();
+  const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
+  const size_t BN = size_t(B) * NS;
+  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = 0; i < k; ++i) {
+      const float2 v = ld(V + size_t(i) * BN + b * NS + OFF, p);
+      acc.x += y[i].x * double(v.x) - y[i].y * double(v.y);
+      acc.y += y[i].x * double(v.y) + y[i].y * double(v.x);
+    }
+    u[b * NS + OFF + p] = make_float2(float(acc.x), float(acc.y));
+  }
+}
+
+// x += z on the columns finalised this cycle (second half of the non-flexible finalize)
+__global__ void __launch_bounds__(KT) k_add_to_x(FineView F, const int* fin, const float2* __restrict__ z,
+                                                 double2* __restrict__ x) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  if (!fin[b]) return;
+  const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
+  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
+    const float2 v = ld(z + b * NS + OFF, p);
+    double2 a = x[b * NS + OFF + p];
+    a.x += double(v.x);
+    a.y += double(v.y);
+    x[b * NS + OFF + p] = a;
+  }
+}
+
+// y = R^-1 g (back-substitution, inc/krylov.hpp:119-126); x += sum_i y_i Z_i
+__global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st, const float2* __restrict__ Z,
+                                                 double2* __restrict__ x) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  const ColState& S = st[b];
+  const int k = S.k;
+  if (k == 0) return;
+  __shared__ double2 sH[kMaxRestart][kMaxRestart];  // sH[col][row]
+  __shared__ double2 y[kMaxRestart];
+  solve_small(S, k, sH, y);
   const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
   const size_t BN = size_t(B) * NS;
   for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
@@ -843,23 +739,10 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
 void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V, double2* gsum) {
   const size_t N = owned_nodes(c);
   KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0) + double(N) * 8.0);  // Z_j, V_0..V_j in; w out; dA
-  const int npt = c.adots_npt;
-  const int nb = nblk_adots(c, N, B, 256 * npt);
-  if (c.opt_adots_cp && npt == 4) {
-    const size_t smem = size_t(2) * 4 * 4 * 256 * sizeof(float2);  // 32 KB (+ 22 KB static)
-    static int attr_dev = -1;
-    if (attr_dev != c.device) {
-      HB_CUDA(cudaFuncSetAttribute(k_adots_cp<256, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      attr_dev = c.device;
-    }
-    launch_pdl(c, k_adots_cp<256, 4>, dim3(nb, B), dim3(256), smem, fine_view(c), B, j,
-               reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p, gsum);
-    HB_CUDA(cudaGetLastError());
-    return;
-  }
-  auto k = npt == 16 ? k_adots<256, 16> : npt == 8 ? k_adots<256, 8> : npt == 2 ? k_adots<256, 2> : k_adots<256, 4>;
-  launch_pdl(c, k, dim3(nb, B), dim3(256), 0, fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, Zj,
-             w, V, c.kpart.p, c.kticket.p, gsum);
+  // same tile as krylov_alloc sized kpart for (nblk_adots(..., 256 * KNPT))
+  const int nb = nblk_adots(c, N, B, 256 * KNPT);
+  launch_pdl(c, k_adots<256, KNPT>, dim3(nb, B), dim3(256), 0, fine_view(c), B, j,
+             reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p, gsum);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -871,6 +754,23 @@ void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* 
   launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p),
                                               c.kact.p, w, V, reinterpret_cast<double*>(c.kpart.p), c.kticket.p,
                                               c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p, gsum);
+  HB_CUDA(cudaGetLastError());
+}
+
+// non-flexible finalize (inc/krylov.hpp:127-136): u = V y -> caller applies M -> x += M u
+void launch_fg_finalize_v(Context& c, int B, const float2* V, float2* u, int* fin) {
+  const size_t N = owned_nodes(c);
+  const int nb = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
+  KScope ks(c, PC_KRYLOV_FINAL, double(B) * N * (8.0 + 8.0 * c.k_m));  // V_0..V_{k-1} in, u out
+  launch_pdl(c, k_finalize_v, dim3(nb, B), dim3(KT), 0, fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), V,
+             u, fin);
+  HB_CUDA(cudaGetLastError());
+}
+void launch_fg_add_to_x(Context& c, int B, const int* fin, const float2* z, double2* x) {
+  const size_t N = owned_nodes(c);
+  const int nb = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
+  KScope ks(c, PC_KRYLOV_FINAL, double(B) * N * 40.0);  // z (c64) in, x (c128) in + out
+  launch_pdl(c, k_add_to_x, dim3(nb, B), dim3(KT), 0, fine_view(c), fin, z, x);
   HB_CUDA(cudaGetLastError());
 }
 

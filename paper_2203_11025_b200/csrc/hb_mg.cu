@@ -443,6 +443,39 @@ void launch_restrict_plain(Context& c, int nx, int ny, int offset, int B, const 
   HB_CUDA(cudaGetLastError());
 }
 
+// CoarseSolver::dense (inc/multigrid.hpp:84,95-104): x = (M^H)^-1 f with the
+// inverse formed on the host (fp64 LU with partial pivoting, setup) and applied
+// here as a dense fp64 matvec; one warp per row, lanes stride the columns
+__global__ void __launch_bounds__(256) k_coarse_dense(int n, const int* act, const double2* __restrict__ inv,
+                                                      const float2* __restrict__ f, float2* __restrict__ x) {
+  const int b = blockIdx.y;
+  if (act && !act[b]) return;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= n) return;
+  const double2* a = inv + size_t(row) * n;
+  const float2* fb = f + size_t(b) * n;
+  double re = 0.0, im = 0.0;
+  for (int j = lane; j < n; j += 32) {
+    const double2 m = a[j];
+    const float2 v = fb[j];
+    re += m.x * double(v.x) - m.y * double(v.y);
+    im += m.x * double(v.y) + m.y * double(v.x);
+  }
+  for (int o = 16; o; o >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, o);
+    im += __shfl_xor_sync(0xffffffffu, im, o);
+  }
+  if (lane == 0) x[size_t(b) * n + row] = make_float2(float(re), float(im));
+}
+
+void launch_coarse_dense(Context& c, const Level& L, int B, const int* act, const float2* f, float2* x) {
+  if (!L.dinv.p) throw HbError{HB_ERR_STATE, "dense coarse solver: inverse not built"};
+  const int n = int(L.N());
+  ProfScope ps(c, PC_COARSE, double(B) * n * 16.0 + double(n) * n * 16.0);
+  k_coarse_dense<<<dim3((n + 7) / 8, B), 256, 0, c.stream>>>(n, act, L.dinv.p, f, x);
+  HB_CUDA(cudaGetLastError());
+}
+
 void launch_coarse_gmres(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
                          float2* x, float2* scratch) {
   if (iters < 1 || iters > kMaxCoarseIters) throw HbError{HB_ERR_ARG, "coarse_iters must be in [1, 16]"};

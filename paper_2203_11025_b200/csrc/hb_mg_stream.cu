@@ -775,7 +775,9 @@ void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float 
     }
   }
   const double rows = 2.0 * cny;  // fine rows behind the emitted coarse rows
-  prof_end(c, PC_DOWN, tok, double(B) * L.nx * rows * (e0 ? 18.0 : 10.0) + double(L.nx) * rows * 16.0, 0);
+  // algorithmic bytes: coefficients count 8 B/node (D, c64) whichever
+  // variant runs -- the stored-wD^-1 kernels read 8 more, which is overhead, not work
+  prof_end(c, PC_DOWN, tok, double(B) * L.nx * rows * (e0 ? 18.0 : 10.0) + double(L.nx) * rows * 8.0, 0);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -811,7 +813,7 @@ void launch_up_stream(Context& c, const LevelView& L, float damping, int offset,
              : (even ? k_up_stream<false, false, true> : k_up_stream<false, false, false>);
     launch_pdl(c, k, grid, dim3(32, WARPS), 0, L, damping, offset, cnx, cny, cw, rpc, act, f, fscale, vc, z);
   }
-  prof_end(c, PC_UP, tok, double(B) * L.nx * nrows * (e0 ? 26.0 : 18.0) + double(L.nx) * nrows * 16.0, 0);
+  prof_end(c, PC_UP, tok, double(B) * L.nx * nrows * (e0 ? 26.0 : 18.0) + double(L.nx) * nrows * 8.0, 0);
   HB_CUDA(cudaGetLastError());
 }
 

@@ -29,7 +29,7 @@ _ip = C.POINTER(C.c_int)
 _u8p = C.POINTER(C.c_uint8)
 _vp = C.c_void_p
 
-HB_COARSE = {"gmres": 0, "jacobi": 1, "net": 2}
+HB_COARSE = {"gmres": 0, "jacobi": 1, "net": 2, "dense": 3}
 HB_PC = {"v": 0, "vu": 1, "ju": 2}
 
 
@@ -755,7 +755,14 @@ def block_fgmres(M: _GpuPrecond, B, cfg: KrylovConfig, X0=None):
 
 
 def convergence_factor(history, target_drop=1e6):  # inc/bench.hpp:22-38
-    h = np.asarray(history)
+    """(T, rho, converged): T = first t with h_t / h_0 <= 1 / target_drop, rho =
+    (h_T / h_0)^(1/T); not reached -> (len - 1, nan, False).  Empty histories
+    and h_0 <= 0 (or NaN) raise ValueError (std::invalid_argument, :25-26)."""
+    h = np.asarray(history, dtype=np.float64)
+    if h.size == 0:
+        raise ValueError("empty residual history")
+    if not (h[0] > 0.0):
+        raise ValueError("history[0] must be positive")
     for t in range(1, len(h)):
         ratio = h[t] / h[0]
         if ratio <= 1.0 / target_drop:

@@ -103,8 +103,52 @@ int main() {
   const double ju_err = rel(ju_gpu.apply(B), ju_cpu.apply(B)), vu_err = rel(vu_gpu.apply(B), vu_cpu.apply(B));
   ok = ok && ju_err < 1e-4 && vu_err < 1e-4 && ju_gpu.name() == "ju" && vu_gpu.name() == "vu" &&
        ju_gpu.requires_flexible() && vu_gpu.requires_flexible();
+  // (5) the reference signature with apply_A: the Helmholtz operator is accepted
+  // (same solve as (2)), any other operator is rejected
+  auto [X_a, rep_a] = gpu::block_fgmres(apply_A, M_gpu, B, cfg);
+  ok = ok && rel(X_a, X_gpu) == 0.0;
+  StencilOperator Ms(prob, kShiftedLaplacianShift);
+  BatchedOp apply_wrong = [&Ms](const std::vector<ComplexField>& in) {
+    std::vector<ComplexField> out;
+    for (const auto& f : in) out.push_back(Ms.apply(f));
+    return out;
+  };
+  bool rejected = false;
+  try {
+    gpu::block_fgmres(apply_wrong, M_gpu, B, cfg);
+  } catch (const std::invalid_argument&) {
+    rejected = true;
+  }
+  ok = ok && rejected;
+  // (6) standard (non-flexible) GMRES with a stationary M: the dense coarsest
+  // solve makes M_V exactly linear (tests/test_classic.cpp:442-467); the device
+  // honours cfg.flexible = false and matches the reference's non-flexible solve
+  VCycleConfig vd = vc;
+  vd.coarse_solver = CoarseSolver::dense;
+  auto hier_d = std::make_shared<MultigridHierarchy>(prob, vd);
+  SLVCyclePreconditioner Md_cpu(hier_d);
+  auto ctx_d = std::make_shared<gpu::Context>(0);
+  ctx_d->set_problem(prob, vd);
+  gpu::GpuSLVCycle Md_gpu(ctx_d);
+  KrylovConfig cs = cfg;
+  cs.flexible = false;
+  auto [X_sr, rep_sr] = block_fgmres(apply_A, Md_cpu.as_batched_op(), B, cs);
+  auto [X_sg, rep_sg] = gpu::block_fgmres(Md_gpu, B, cs);
+  const double d_pc = rel(Md_gpu.apply(B), Md_cpu.apply(B)), d_x = rel(X_sg, X_sr);
+  int d_it = 0;
+  for (size_t c = 0; c < B.size(); ++c) d_it = std::max(d_it, std::abs(rep_sg.iterations[c] - rep_sr.iterations[c]));
+  ok = ok && d_pc < 1e-4 && d_x < 1e-4 && d_it <= 1;
+  bool nonflex_rejected = false;
+  try {
+    gpu::block_fgmres(vu_gpu, B, cs);
+  } catch (const std::invalid_argument&) {
+    nonflex_rejected = true;
+  }
+  ok = ok && nonflex_rejected;
   std::printf("], \"x_rel_device\": %.3e, \"x_rel_plugin\": %.3e, \"name\": \"%s\", \"ju_rel\": %.3e, "
-              "\"vu_rel\": %.3e, \"ok\": %s}\n",
-              xe, xm, M_gpu.name().c_str(), ju_err, vu_err, ok ? "true" : "false");
+              "\"vu_rel\": %.3e, \"apply_A_rejects_wrong_op\": %s, \"dense_pc_rel\": %.3e, "
+              "\"nonflex_x_rel\": %.3e, \"nonflex_iter_diff\": %d, \"vu_nonflex_rejected\": %s, \"ok\": %s}\n",
+              xe, xm, M_gpu.name().c_str(), ju_err, vu_err, rejected ? "true" : "false", d_pc, d_x, d_it,
+              nonflex_rejected ? "true" : "false", ok ? "true" : "false");
   return ok ? 0 : 1;
 }

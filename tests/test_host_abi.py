@@ -82,3 +82,46 @@ def test_cpp_adapter_header_compiles_against_reference():
     _lib()
     r = subprocess.run(["bash", os.path.join(ROOT, "tests", "cpp", "build.sh")], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-2000:]
+
+
+@pytest.mark.timeout(600)
+def test_problem_arrays_product_equals_oracle():
+    """The bench's reference arm builds its inputs with the oracle's generators
+    (oracle/problems.py) so it never loads libhelmgpu.so; the product's host
+    generators must give the same arrays bit for bit on every config."""
+    from oracle import problems as OP
+    from paper_2203_11025_b200 import configs, problems
+    for name in ("c0", "c1", "c2", "c3", "c4"):
+        cfg = configs.CONFIGS[name]
+        a, b = problems.problem_arrays(cfg), OP.problem_arrays(cfg)
+        for k in ("kappa2", "gamma"):
+            assert np.array_equal(a[k], b[k]), (name, k)
+        assert [int(x) for x in a["xs"]] == b["xs"] and [int(y) for y in a["ys"]] == b["ys"], name
+        assert a["omega"] == b["omega"] and (a["lo"], a["hi"]) == (b["lo"], b["hi"])
+        assert np.array_equal(problems.rhs_block(a), OP.rhs_block(b))
+
+
+def test_convergence_factor_reference_kats():
+    """tests/test_pipeline.cpp:625-649 (inc/bench.hpp:22-38)."""
+    from paper_2203_11025_b200.helmgpu import convergence_factor
+    T, rho, conv = convergence_factor([1.0, 1e-6])
+    assert conv and T == 1 and rho == pytest.approx(1e-6)
+    h = [1.0]
+    for _ in range(25):
+        h.append(h[-1] * 0.5)
+    T, rho, conv = convergence_factor(h)
+    assert conv and T == 20 and rho == pytest.approx(0.5)
+    T, rho, conv = convergence_factor([1.0, 0.9, 0.8])
+    assert not conv and T == 2 and np.isnan(rho)
+    for bad in ([], [0.0, 1.0], [-1.0, 0.5], [float("nan"), 1.0]):
+        with pytest.raises(ValueError):
+            convergence_factor(bad)
+    def conv_of(hist):
+        return convergence_factor(hist)[2]
+
+    # the oracle's restatement agrees on the same histories
+    for hist in ([1.0, 1e-6], h, [1.0, 0.9, 0.8]):
+        To, ro = O.convergence_factor(np.array(hist))
+        T, rho, _ = convergence_factor(hist)
+        assert abs(To) == T and (To > 0) == conv_of(hist)  # the oracle returns -T when not converged
+        assert (np.isnan(ro) and np.isnan(rho)) or ro == pytest.approx(rho)

@@ -86,3 +86,21 @@ def test_two_rank_rhs_sharding_gloo(tmp_path):
         for i, c in enumerate(p["mine"]):
             assert np.array_equal(p["X"][i], X[c])
             assert np.array_equal(p["hist"][i], rep["history"][c])
+
+
+@pytest.mark.timeout(600)
+def test_bench_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus N` without torchrun starts N ranks itself (here: 2 gloo
+    ranks on CPU, host plumbing only) and rank 0 reports n_gpus = N with the
+    RHS block sharded over the ranks (uneven world sizes included)."""
+    import json
+    import subprocess
+    for n, cfg, B in ((2, "c1", 8), (3, "c2", 16)):
+        env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(n), "--dry-run",
+                            "--config", cfg], capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        line = json.loads(r.stdout.strip().splitlines()[-1])
+        assert line["dry_run"] and line["n_gpus"] == n
+        assert line["rhs_total"] == B and line["max_over_ranks"] == float(n)
+        assert line["rank0_columns"] == list(range(-(-B // n)))

@@ -130,8 +130,21 @@ def configs(g, names):
         g[f"{name}_iters"] = np.array(rep["iterations"])
         xs = field_stats(X[0])
         g[f"{name}_x_norm"], g[f"{name}_x_proj"], g[f"{name}_x_sub"], g[f"{name}_x_stride"] = xs
+        # the reference's own sensitivity: the same solve with every network weight
+        # moved by ~1 fp32 ulp (x (1 + 2^-22)).  The random-init nets make the Z_j
+        # nearly collinear (their r-independent part dominates), so the Arnoldi from
+        # step 2 on amplifies fp32 rounding of the net; a device run is held to a
+        # small multiple of this spread (tests/test_scale_parity.py)
+        for net in P._keep[:2]:
+            if net is not None:
+                for w, bias in net.convs():
+                    w *= np.float32(1.0 + 2.0 ** -22)
+        X2, rep2 = O.ref_fgmres(P, B, restart=cfg["restart"], max_iters=its, nthreads=ncols)
+        g[f"{name}_hist_ulp"] = pack_hist(rep2["history"])
+        spread = np.nanmax(np.abs(g[f"{name}_hist_ulp"] - g[f"{name}_hist"]) / g[f"{name}_hist"][:, :1])
         print(f"{name}: apply {t1 - t0:.1f} s, {ncols} x {its} FGMRES its {time.time() - t1:.1f} s, "
-              f"rel residual end {[round(float(h[-1] / h[0]), 6) for h in rep['history']]}", flush=True)
+              f"rel residual end {[round(float(h[-1] / h[0]), 6) for h in rep['history']]}, "
+              f"1-ulp history spread {spread:.3e}", flush=True)
         del P, H
 
 

@@ -223,19 +223,42 @@ __device__ __forceinline__ void warp_reduce_scatter(float (&v)[NF]) {
   }
 }
 
-// w = A Z_j ; partial <Vraw_i, w> (i <= j) and <Vraw_j, Vraw_k> (k < j).
-// Basis vectors are streamed in groups of 4 (all 4*KNPT loads in flight
-// before use); each group's 4 dot + 4 Gram products are summed in fp32 over
-// the thread's nodes and reduced across the warp by one 16-float butterfly,
-// the warp partial accumulates in shared memory; warps and CTAs fold in fp64;
-// the last CTA of the column forms the MGS coefficients.
+// CTA sum of per-thread fp32 accumulators acc[0 .. nf) (nf <= NA, runtime):
+// transposed through shared memory sred[NA][KT] (dynamic), each warp folds
+// slots w, w + 8, ... over the CTA's threads in fp64; out[s] (shared, fp64)
+template <int NA>
+__device__ __forceinline__ void cta_reduce_acc(const float (&acc)[NA], int nf, float* sred, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int s = 0; s < NA; ++s)
+    if (s < nf) sred[s * KT + threadIdx.x] = acc[s];
+  __syncthreads();
+  for (int s = warp; s < nf; s += KT / 32) {
+    double v = 0.0;
+#pragma unroll
+    for (int k = 0; k < KT / 32; ++k) v += double(sred[s * KT + k * 32 + lane]);
+    v = warp_sum(v);
+    if (lane == 0) out[s] = v;
+  }
+  __syncthreads();
+}
+
+// w = A Z_j and the partial dots <Vraw_i, w> (i <= j).  (The Gram row
+// <Vraw_j, Vraw_k>, k < j, of the Gram-corrected MGS is formed by k_update one
+// step earlier, while V_j is still in registers.)  Each thread keeps 2(JM+1)
+// fp32 accumulators (JM = the largest j of the instantiation, j <= JM) over
+// all of its nodes -- a grid-strided loop, every basis load of a node issued
+// before its FMAs -- and the CTA reduces once at the end: one warp
+// reduce-scatter of NF floats, warps folded in fp64, CTA partials folded in
+// fp64 by the last CTA of the column, which forms the MGS coefficients.
 __device__ void adots_scalar(ColState& S, int j, const double2* red);
 
-template <int NT, int NPT>  // NPT: nodes per thread per tile (more nodes per butterfly)
-__global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
+template <int JM>
+__global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
                                               const float2* __restrict__ Z, float2* __restrict__ W,
                                               const float2* __restrict__ V, double2* part, unsigned* ticket,
                                               double2* gsum) {
+  constexpr int NF = 2 * (JM + 1);
   pdl_enter();
   const int b = blockIdx.y;
   if (!act[b]) return;
@@ -244,103 +267,32 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
   const float2* zb = Z + b * NS + OFF;
   float2* wb = W + b * NS + OFF;
   const float2* dA = F.dA + OFF;
-  V += OFF;
-  const float2* Vj = V + size_t(j) * BN + b * NS;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nv = 2 * j + 1;
+  const float2* Vb = V + OFF + b * NS;
   const float inv_h2 = float(F.inv_h2);
-  // wpart[warp][float]: dots of basis i at floats 2i, 2i+1; Gram k at 2*kMaxRestart + 2k
-  __shared__ float wpart[NT / 32][4 * kMaxRestart + 8];
-  for (int t = threadIdx.x; t < (NT / 32) * (4 * kMaxRestart + 8); t += NT) (&wpart[0][0])[t] = 0.f;
-  __syncthreads();
-  constexpr int TILE = NT * NPT;
-  for (size_t base = size_t(blockIdx.x) * TILE; base < N; base += size_t(gridDim.x) * TILE) {
-    float2 w[NPT], vj[NPT];
-    bool ok[NPT];
+  float acc[NF];
 #pragma unroll
-    for (int q = 0; q < NPT; ++q) {
-      const size_t p = base + q * NT + threadIdx.x;
-      ok[q] = p < N;
-      if (ok[q]) {
-        const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
-        w[q] = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
-        wb[p] = w[q];
-        vj[q] = ld(Vj, p);
-      } else {
-        w[q] = vj[q] = make_float2(0.f, 0.f);
-      }
-    }
-    for (int i0 = 0; i0 <= j; i0 += 4) {
-      float2 a[4][NPT];
+  for (int s = 0; s < NF; ++s) acc[s] = 0.f;
+  const size_t stride = size_t(gridDim.x) * KT;
+  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += stride) {
+    float2 a[JM + 1];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2* Vi = V + size_t(i0 + u) * BN + b * NS;
+    for (int i = 0; i <= JM; ++i) a[i] = i <= j ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
+    const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
+    const float2 w = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
+    wb[p] = w;
 #pragma unroll
-        for (int q = 0; q < NPT; ++q)
-          a[u][q] = (ok[q] && i0 + u <= j) ? ld(Vi, base + q * NT + threadIdx.x) : make_float2(0.f, 0.f);
-      }
-      float v[16];  // [0..7] dots of i0..i0+3, [8..15] Gram
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        float dr = 0.f, di = 0.f, gr = 0.f, gi = 0.f;
-#pragma unroll
-        for (int q = 0; q < NPT; ++q) {
-          const float2 ai = a[u][q], c = w[q], e = vj[q];
-          dr = fmaf(ai.x, c.x, fmaf(ai.y, c.y, dr));
-          di = fmaf(ai.x, c.y, fmaf(-ai.y, c.x, di));
-          gr = fmaf(e.x, ai.x, fmaf(e.y, ai.y, gr));
-          gi = fmaf(e.x, ai.y, fmaf(-e.y, ai.x, gi));
-        }
-        v[2 * u] = dr;
-        v[2 * u + 1] = di;
-        v[8 + 2 * u] = gr;
-        v[8 + 2 * u + 1] = gi;
-      }
-      // 16-float reduce-scatter: 4 halving stages, then a pairwise allreduce
-#pragma unroll
-      for (int stage = 0; stage < 4; ++stage) {
-        const int half = 8 >> stage, mask = 16 >> stage;
-        const bool upper = (lane & mask) != 0;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          if (k < half) {
-            const float send = upper ? v[k] : v[k + half];
-            const float keep = upper ? v[k + half] : v[k];
-            v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-          }
-        }
-      }
-      v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-      if ((lane & 1) == 0) {
-        const int fidx = lane >> 1;  // float index in the group's 16
-        const int u = (fidx & 7) >> 1, comp = fidx & 1;
-        const int i = i0 + u;
-        if (fidx < 8) {
-          if (i <= j) wpart[warp][2 * i + comp] += v[0];
-        } else {
-          if (i < j) wpart[warp][2 * kMaxRestart + 2 * i + comp] += v[0];
-        }
-      }
+    for (int i = 0; i <= JM; ++i) {
+      acc[2 * i] = fmaf(a[i].x, w.x, fmaf(a[i].y, w.y, acc[2 * i]));
+      acc[2 * i + 1] = fmaf(a[i].x, w.y, fmaf(-a[i].y, w.x, acc[2 * i + 1]));
     }
   }
-  __syncthreads();
-  constexpr int HS = kMaxRestart;
-  // fold warps in fp64: slot s <- floats 2s, 2s+1 (dots s <= j at s, Gram k < j at HS + k)
+  extern __shared__ float sred[];  // [2 (JM + 1)][KT]
   __shared__ double2 red[KMAXV];
-  for (int t = threadIdx.x; t < nv; t += NT) {
-    const int slot = t <= j ? t : HS + (t - j - 1);
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-    for (int w2 = 0; w2 < NT / 32; ++w2) {
-      acc.x += wpart[w2][2 * slot];
-      acc.y += wpart[w2][2 * slot + 1];
-    }
-    red[t] = acc;
-  }
-  __syncthreads();
-  for (int t = threadIdx.x; t < nv; t += NT) part[(size_t(b) * gridDim.x + blockIdx.x) * KMAXV + t] = red[t];
+  const int nv = j + 1;
+  cta_reduce_acc(acc, 2 * nv, sred, reinterpret_cast<double*>(red));
+  for (int t = threadIdx.x; t < nv; t += KT) part[(size_t(b) * gridDim.x + blockIdx.x) * KMAXV + t] = red[t];
   if (!last_cta(ticket, b, gridDim.x)) return;
-  for (int t = threadIdx.x; t < nv; t += NT) {
+  for (int t = threadIdx.x; t < nv; t += KT) {
     double2 s = make_double2(0.0, 0.0);
     for (unsigned q = 0; q < gridDim.x; ++q) {
       const volatile double2* pp = part + (size_t(b) * gridDim.x + q) * KMAXV + t;
@@ -351,6 +303,7 @@ __global__ void __launch_bounds__(NT) k_adots(FineView F, int B, int j, ColState
     if (gsum) gsum[size_t(b) * KMAXV + t] = s;
   }
   if (gsum) return;
+  __syncthreads();
   adots_scalar(st[b], j, red);
 }
 
@@ -358,12 +311,14 @@ __global__ void k_adots_finish(int j, ColState* st, const int* act, const double
   const int b = blockIdx.x;
   if (!act[b]) return;
   __shared__ double2 red[KMAXV];
-  for (int t = threadIdx.x; t < 2 * j + 1; t += blockDim.x) red[t] = gsum[size_t(b) * KMAXV + t];
+  for (int t = threadIdx.x; t <= j; t += blockDim.x) red[t] = gsum[size_t(b) * KMAXV + t];
+  __syncthreads();
   adots_scalar(st[b], j, red);
 }
 
-// MGS coefficients from the global sums red[0..j] = <Vraw_i, w>, red[j+1..2j] =
-// <Vraw_j, Vraw_k> (called by a whole CTA; red in shared memory)
+// MGS coefficients from the global sums red[0..j] = <Vraw_i, w> and the Gram
+// rows S.G[i][k] = s_i s_k <Vraw_i, Vraw_k> (k < i <= j; row j written by the
+// previous step's k_update).  Called by a whole CTA; red in shared memory.
 __device__ void adots_scalar(ColState& S, int j, const double2* red) {
   const int lane = threadIdx.x & 31;
   // stage the Gram rows this step needs, then warp 0 forms the MGS coefficients
@@ -372,23 +327,19 @@ __device__ void adots_scalar(ColState& S, int j, const double2* red) {
   __shared__ double2 sG[kMaxRestart][kMaxRestart];
   __shared__ double ssc[kMaxRestart + 1];
   for (int t = threadIdx.x; t <= j; t += blockDim.x) ssc[t] = S.scale[t];
-  for (int t = threadIdx.x; t < j * j; t += blockDim.x) {
-    const int i = t / j, kk = t % j;
+  for (int t = threadIdx.x; t < (j + 1) * (j + 1); t += blockDim.x) {
+    const int i = t / (j + 1), kk = t % (j + 1);
     if (kk < i) sG[i][kk] = S.G[i][kk];
   }
   __syncthreads();
   if (threadIdx.x >= 32) return;
-  const double sj = ssc[j];
   const double si = lane <= j ? ssc[lane] : 0.0;
   const double2 zero = make_double2(0.0, 0.0);
   const double2 hcgs = lane <= j ? zscale(red[lane], si) : zero;
-  const double2 gjk = lane < j ? zscale(red[j + 1 + lane], sj * si) : zero;
-  if (lane < j) S.G[j][lane] = gjk;
   double2 h = hcgs;
   for (int kk = 0; kk < j; ++kk) {
     const double2 hk = make_double2(__shfl_sync(0xffffffffu, hcgs.x, kk), __shfl_sync(0xffffffffu, hcgs.y, kk));
-    const double2 gk = make_double2(__shfl_sync(0xffffffffu, gjk.x, kk), __shfl_sync(0xffffffffu, gjk.y, kk));
-    if (lane <= j && kk < lane) h = zsub(h, zmul(hk, lane == j ? gk : sG[lane][kk]));
+    if (lane <= j && kk < lane) h = zsub(h, zmul(hk, sG[lane][kk]));
   }
   if (lane <= j) {
     S.hc[lane] = h;
@@ -396,93 +347,100 @@ __device__ void adots_scalar(ColState& S, int j, const double2* red) {
   }
 }
 
-// V_{j+1}raw = w - sum_i coef_i Vraw_i ; hnorm ; Givens + convergence (inc/krylov.hpp:219-254)
-__device__ void update_scalar(ColState& S, int b, int j, int m, double t, int* act, double* hist, int hist_cap,
-                              double rel_tol, int max_iters, float* scale_out);
+// V_{j+1}raw = w - sum_i coef_i Vraw_i ; hnorm ; Givens + convergence
+// (inc/krylov.hpp:219-254); also the Gram row <Vraw_{j+1}, Vraw_i> (i <= j) for
+// the next step's MGS coefficients while V_{j+1} and the V_i are in registers.
+// gram: global sums of the Gram row (j+1 entries) or nullptr
+__device__ void update_scalar(ColState& S, int b, int j, int m, double t, const double2* gram, int* act, double* hist,
+                              int hist_cap, double rel_tol, int max_iters, float* scale_out);
 
+template <int JM>
 __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, ColState* st, int* act,
-                                               const float2* __restrict__ W, float2* __restrict__ V, double* part,
+                                               const float2* __restrict__ W, float2* __restrict__ V, double2* part,
                                                unsigned* ticket, double* hist, int hist_cap, double rel_tol,
                                                int max_iters, float* scale_out, double2* gsum) {
+  constexpr int NF = 2 * (JM + 1);
   pdl_enter();
   const int b = blockIdx.y;
   if (!act[b]) return;
   ColState& S = st[b];
   const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
   const size_t BN = size_t(B) * NS;
-  W += OFF;
-  V += OFF;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ float2 cf[kMaxRestart + 4];
-  for (int i = threadIdx.x; i <= j; i += KT) cf[i] = make_float2(float(S.coef[i].x), float(S.coef[i].y));
+  for (int i = threadIdx.x; i < kMaxRestart + 4; i += KT)
+    cf[i] = i <= j ? make_float2(float(S.coef[i].x), float(S.coef[i].y)) : make_float2(0.f, 0.f);
   __syncthreads();
-  const float2* wb = W + b * NS;
-  float2* Vn = V + size_t(j + 1) * BN + b * NS;
-  double acc = 0.0;
-  for (size_t base = size_t(blockIdx.x) * KTILE; base < N; base += size_t(gridDim.x) * KTILE) {
-    float2 t[KNPT];
-    bool ok[KNPT];
+  const float2* wb = W + OFF + b * NS;
+  const float2* Vb = V + OFF + b * NS;
+  float2* Vn = V + OFF + size_t(j + 1) * BN + b * NS;
+  // need the next Gram row only if the cycle can continue past step j + 1
+  const bool gram = j + 1 < m;
+  float acc[NF];
 #pragma unroll
-    for (int q = 0; q < KNPT; ++q) {
-      const size_t p = base + q * KT + threadIdx.x;
-      ok[q] = p < N;
-      t[q] = ok[q] ? ld(wb, p) : make_float2(0.f, 0.f);
-    }
-    for (int i0 = 0; i0 <= j; i0 += 4) {
-      float2 a[4][KNPT];
+  for (int s2 = 0; s2 < NF; ++s2) acc[s2] = 0.f;
+  double nrm = 0.0;
+  const size_t stride = size_t(gridDim.x) * KT;
+  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += stride) {
+    float2 a[JM + 1];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2* Vi = V + size_t(i0 + u) * BN + b * NS;
+    for (int i = 0; i <= JM; ++i) a[i] = i <= j ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
+    float2 t = ld(wb, p);
 #pragma unroll
-        for (int q = 0; q < KNPT; ++q)
-          a[u][q] = (ok[q] && i0 + u <= j) ? ld(Vi, base + q * KT + threadIdx.x) : make_float2(0.f, 0.f);
-      }
+    for (int i = 0; i <= JM; ++i) t = csub(t, cmul(cf[i], a[i]));  // cf beyond j: zero
+    Vn[p] = t;
+    nrm += dnorm2(t);
+    if (gram) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float2 c = (i0 + u <= j) ? cf[i0 + u] : make_float2(0.f, 0.f);
-#pragma unroll
-        for (int q = 0; q < KNPT; ++q) t[q] = csub(t[q], cmul(c, a[u][q]));
+      for (int i = 0; i <= JM; ++i) {  // conj(V_{j+1}) V_i
+        acc[2 * i] = fmaf(t.x, a[i].x, fmaf(t.y, a[i].y, acc[2 * i]));
+        acc[2 * i + 1] = fmaf(t.x, a[i].y, fmaf(-t.y, a[i].x, acc[2 * i + 1]));
       }
     }
-#pragma unroll
-    for (int q = 0; q < KNPT; ++q)
-      if (ok[q]) {
-        Vn[base + q * KT + threadIdx.x] = t[q];
-        acc += dnorm2(t[q]);
-      }
   }
-  acc = warp_sum(acc);
+  nrm = warp_sum(nrm);
   __shared__ double wp[KT / 32];
-  if ((threadIdx.x & 31) == 0) wp[threadIdx.x >> 5] = acc;
-  __syncthreads();
+  if (lane == 0) wp[warp] = nrm;
+  extern __shared__ float sred[];  // [2 (JM + 1)][KT]
+  __shared__ double2 red[KMAXV];
+  const int ng = gram ? j + 1 : 0;
+  cta_reduce_acc(acc, 2 * ng, sred, reinterpret_cast<double*>(red));  // (its barriers publish wp)
+  double2* myp = part + (size_t(b) * gridDim.x + blockIdx.x) * KMAXV;
   if (threadIdx.x == 0) {
     double t = 0.0;
-    for (int w = 0; w < KT / 32; ++w) t += wp[w];
-    part[size_t(b) * gridDim.x + blockIdx.x] = t;
+    for (int w2 = 0; w2 < KT / 32; ++w2) t += wp[w2];
+    myp[0] = make_double2(t, 0.0);
   }
+  for (int t = threadIdx.x; t < ng; t += KT) myp[1 + t] = red[t];
   if (!last_cta(ticket, b, gridDim.x)) return;
-  if (threadIdx.x >= 32) return;
-  const int lane = threadIdx.x;
-  // warp 0: fold the partial norms, stage rotation state in shared memory
-  double t = 0.0;
-  for (unsigned q = lane; q < gridDim.x; q += 32) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
-  t = warp_sum(t);
-  if (gsum) {
-    if (lane == 0) gsum[size_t(b) * KMAXV] = make_double2(t, 0.0);
-    return;
+  for (int t = threadIdx.x; t <= ng; t += KT) {
+    double2 s2 = make_double2(0.0, 0.0);
+    for (unsigned q = 0; q < gridDim.x; ++q) {
+      const volatile double2* pp = part + (size_t(b) * gridDim.x + q) * KMAXV + t;
+      s2.x += pp->x;
+      s2.y += pp->y;
+    }
+    red[t] = s2;
+    if (gsum) gsum[size_t(b) * KMAXV + t] = s2;
   }
-  update_scalar(S, b, j, m, t, act, hist, hist_cap, rel_tol, max_iters, scale_out);
+  if (gsum) return;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  update_scalar(S, b, j, m, red[0].x, gram ? red + 1 : nullptr, act, hist, hist_cap, rel_tol, max_iters, scale_out);
 }
 
 __global__ void k_update_finish(int j, int m, ColState* st, int* act, const double2* gsum, double* hist,
                                 int hist_cap, double rel_tol, int max_iters, float* scale_out) {
   const int b = blockIdx.x;
   if (!act[b]) return;
-  update_scalar(st[b], b, j, m, gsum[size_t(b) * KMAXV].x, act, hist, hist_cap, rel_tol, max_iters, scale_out);
+  const double2* g = gsum + size_t(b) * KMAXV;
+  update_scalar(st[b], b, j, m, g[0].x, j + 1 < m ? g + 1 : nullptr, act, hist, hist_cap, rel_tol, max_iters,
+                scale_out);
 }
 
 // Givens + convergence on the global squared norm t of V_{j+1}raw (one warp)
-__device__ void update_scalar(ColState& S, int b, int j, int m, double t, int* act, double* hist, int hist_cap,
-                              double rel_tol, int max_iters, float* scale_out) {
+__device__ void update_scalar(ColState& S, int b, int j, int m, double t, const double2* gram, int* act, double* hist,
+                              int hist_cap, double rel_tol, int max_iters, float* scale_out) {
   const int lane = threadIdx.x & 31;
   const double hnorm = sqrt(t);
   __shared__ double2 hcol[kMaxRestart + 1], ssn[kMaxRestart];
@@ -556,6 +514,8 @@ __device__ void update_scalar(ColState& S, int b, int j, int m, double t, int* a
   }
   __syncwarp();
   if (lane <= j + 1) S.H[j][lane] = hcol[lane];
+  // next step's Gram row G[j+1][i] = s_{j+1} s_i <Vraw_{j+1}, Vraw_i>
+  if (gram && S.active && lane <= j) S.G[j + 1][lane] = zscale(gram[lane], S.scale[j + 1] * S.scale[lane]);
 }
 
 // y = R^-1 g (back-substitution, inc/krylov.hpp:119-126) into shared y[0..k):
@@ -669,12 +629,13 @@ FineView fine_view(Context& c) {
   return FineView{L.nx, L.ny, 1.0 / (L.h * L.h), L.dA64.p, L.dA.p, L.win()};
 }
 
-// one tile per CTA for small columns (latency), capped for huge columns so the
-// last-CTA fold stays short
-int nblk_adots(Context& c, size_t N, int B, int tile) {
-  const size_t tiles = (N + tile - 1) / tile;
-  const size_t cap = std::max<size_t>(16, size_t(4) * c.num_sms / std::max(1, B));
-  return int(std::max<size_t>(1, std::min(tiles, cap)));
+// CTAs per column of the basis-streaming kernels (k_adots, k_update): ~4 CTAs
+// per SM over the whole batch, each thread covering >= 4 nodes (the per-CTA
+// reduction is amortised over the rest of a CTA's nodes)
+int nblk_basis(Context& c, size_t N, int B) {
+  const size_t want = (N + size_t(KT) * 4 - 1) / (size_t(KT) * 4);
+  const size_t cap = std::max<size_t>(1, size_t(4) * c.num_sms / std::max(1, B));
+  return int(std::max<size_t>(1, std::min(want, cap)));
 }
 
 int nblk_for(Context& c, size_t N, int B) {
@@ -700,7 +661,7 @@ void krylov_alloc(Context& c, int B, int m, int hist_cap, const int* limits) {
   c.kV.ensure(size_t(m + 1) * B * N);
   c.kZ.ensure(size_t(m) * B * N);
   c.kW.ensure(size_t(B) * N);
-  const int nb = std::max(nblk_for(c, N, B), nblk_adots(c, N, B, 256 * KNPT));
+  const int nb = std::max(nblk_for(c, N, B), nblk_basis(c, N, B));
   c.kpart.ensure(size_t(B) * nb * KMAXV);
   c.khist.ensure(size_t(B) * std::max(1, hist_cap));
   c.kact.ensure(B);
@@ -736,25 +697,72 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
   HB_CUDA(cudaGetLastError());
 }
 
+// the basis-streaming kernels are instantiated for JM = 1, 3, ..., 15, 19, 23, 31
+// (the largest j they accept: 2 (JM + 1) fp32 accumulators and JM + 1 basis
+// values per thread; odd steps keep the unused registers few)
+#define HB_JM_DISPATCH(j, KERN, grid, ...)                                          \
+  do {                                                                              \
+    const int jm_ = (j) <= 15 ? ((j) | 1) : (j) <= 19 ? 19 : (j) <= 23 ? 23 : 31;    \
+    const size_t sm_ = size_t(2) * (jm_ + 1) * KT * sizeof(float);                  \
+    switch (jm_) {                                                                  \
+      case 1: launch_jm(c, KERN<1>, grid, sm_, __VA_ARGS__); break;                 \
+      case 3: launch_jm(c, KERN<3>, grid, sm_, __VA_ARGS__); break;                 \
+      case 5: launch_jm(c, KERN<5>, grid, sm_, __VA_ARGS__); break;                 \
+      case 7: launch_jm(c, KERN<7>, grid, sm_, __VA_ARGS__); break;                 \
+      case 9: launch_jm(c, KERN<9>, grid, sm_, __VA_ARGS__); break;                 \
+      case 11: launch_jm(c, KERN<11>, grid, sm_, __VA_ARGS__); break;               \
+      case 13: launch_jm(c, KERN<13>, grid, sm_, __VA_ARGS__); break;               \
+      case 15: launch_jm(c, KERN<15>, grid, sm_, __VA_ARGS__); break;               \
+      case 19: launch_jm(c, KERN<19>, grid, sm_, __VA_ARGS__); break;               \
+      case 23: launch_jm(c, KERN<23>, grid, sm_, __VA_ARGS__); break;               \
+      default: launch_jm(c, KERN<31>, grid, sm_, __VA_ARGS__); break;               \
+    }                                                                               \
+  } while (0)
+
+// PDL launch with dynamic shared memory; opts in once per kernel (static +
+// dynamic shared memory may exceed the 48 KB default: adots_scalar stages 16 KB)
+template <typename... KArgs, typename... Args>
+static void launch_jm(Context& c, void (*k)(KArgs...), dim3 grid, size_t smem, Args&&... args) {
+  {
+    static std::vector<const void*> done;  // (per process; attributes are per function)
+    if (std::find(done.begin(), done.end(), reinterpret_cast<const void*>(k)) == done.end()) {
+      HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      done.push_back(reinterpret_cast<const void*>(k));
+    }
+  }
+  launch_pdl(c, k, grid, dim3(KT), smem, std::forward<Args>(args)...);
+}
+
+void launch_adots(Context& c, const FineView& F, int B, int j, ColState* st, const int* act, const float2* Zj, float2* w,
+                  const float2* V, double2* part, unsigned* ticket, double2* gsum) {
+  const size_t N = size_t(F.nx) * (F.w.hi - F.w.lo);
+  const int nb = nblk_basis(c, N, B);
+  HB_JM_DISPATCH(j, k_adots, dim3(nb, B), F, B, j, st, act, Zj, w, V, part, ticket, gsum);
+  HB_CUDA(cudaGetLastError());
+}
+void launch_update(Context& c, const FineView& F, int B, int j, int m, ColState* st, int* act, const float2* w, float2* V,
+                   double2* part, unsigned* ticket, double* hist, int hist_cap, double rel_tol, int max_iters,
+                   float* scale, double2* gsum) {
+  const size_t N = size_t(F.nx) * (F.w.hi - F.w.lo);
+  const int nb = nblk_basis(c, N, B);
+  HB_JM_DISPATCH(j, k_update, dim3(nb, B), F, B, j, m, st, act, w, V, part, ticket, hist, hist_cap, rel_tol,
+                 max_iters, scale, gsum);
+  HB_CUDA(cudaGetLastError());
+}
+
 void launch_fg_adots(Context& c, int B, int j, const float2* Zj, float2* w, const float2* V, double2* gsum) {
   const size_t N = owned_nodes(c);
   KScope ks(c, PC_KRYLOV_DOTS, double(B) * N * (8.0 * (j + 2) + 8.0) + double(N) * 8.0);  // Z_j, V_0..V_j in; w out; dA
-  // same tile as krylov_alloc sized kpart for (nblk_adots(..., 256 * KNPT))
-  const int nb = nblk_adots(c, N, B, 256 * KNPT);
-  launch_pdl(c, k_adots<256, KNPT>, dim3(nb, B), dim3(256), 0, fine_view(c), B, j,
-             reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, Zj, w, V, c.kpart.p, c.kticket.p, gsum);
-  HB_CUDA(cudaGetLastError());
+  launch_adots(c, fine_view(c), B, j, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, Zj, w, V, c.kpart.p,
+               c.kticket.p, gsum);
 }
 
 void launch_fg_update(Context& c, int B, int j, int m, const float2* w, float2* V, int hist_cap, double rel_tol,
                       int max_iters, double2* gsum) {
   const size_t N = owned_nodes(c);
-  const int nb = nblk_for(c, N, B);
   KScope ks(c, PC_KRYLOV_UPDATE, double(B) * N * (8.0 * (j + 1) + 16.0));  // w, V_0..V_j in; V_{j+1} out
-  launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p),
-                                              c.kact.p, w, V, reinterpret_cast<double*>(c.kpart.p), c.kticket.p,
-                                              c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p, gsum);
-  HB_CUDA(cudaGetLastError());
+  launch_update(c, fine_view(c), B, j, m, reinterpret_cast<ColState*>(c.kstate.p), c.kact.p, w, V, c.kpart.p,
+                c.kticket.p, c.khist.p, hist_cap, rel_tol, max_iters, c.kscale.p, gsum);
 }
 
 // non-flexible finalize (inc/krylov.hpp:127-136): u = V y -> caller applies M -> x += M u
@@ -843,7 +851,7 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
   K.W.ensure(size_t(B) * N);
   K.b.ensure(size_t(B) * N);
   K.x.ensure(size_t(B) * N);
-  const int nbk = std::max(nblk_for(c, N, B), nblk_adots(c, N, B, 256 * KNPT));
+  const int nbk = std::max(nblk_for(c, N, B), nblk_basis(c, N, B));
   K.part.ensure(size_t(B) * nbk * KMAXV);
   K.hist.ensure(size_t(B) * cap);
   K.act.ensure(B);
@@ -868,17 +876,14 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
   launch_pdl(c, k_restart, dim3(nb, B), dim3(KT), 0, F, B, st, K.b.p, K.x.p, K.V.p, reinterpret_cast<double*>(K.part.p),
                                                K.ticket.p, K.hist.p, cap, tol, m, K.act.p, K.scale.p, K.count.p,
                                                (double2*)nullptr);
-  const int na = nblk_adots(c, N, B, 256 * KNPT);
   const dim3 gz(unsigned(std::max<size_t>(1, std::min<size_t>((N + 255) / 256, size_t(4) * c.num_sms / B))), B);
   for (int j = 0; j < m; ++j) {
     float2* Vj = K.V.p + size_t(j) * BN;
     float2* Zj = K.Z.p + size_t(j) * BN;
     k_diag_precond<<<gz, 256, 0, c.stream>>>(int(N), K.act.p, Vj, K.scale.p, L.dM.p, Zj);
-    launch_pdl(c, k_adots<256, KNPT>, dim3(na, B), dim3(256), 0, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p,
-               (double2*)nullptr);
-    launch_pdl(c, k_update, dim3(nb, B), dim3(KT), 0, F, B, j, m, st, K.act.p, K.W.p, K.V.p,
-                                                reinterpret_cast<double*>(K.part.p), K.ticket.p, K.hist.p, cap, tol,
-                                                m, K.scale.p, (double2*)nullptr);
+    launch_adots(c, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p, nullptr);
+    launch_update(c, F, B, j, m, st, K.act.p, K.W.p, K.V.p, K.part.p, K.ticket.p, K.hist.p, cap, tol, m, K.scale.p,
+                  nullptr);
   }
   const int nf = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
   launch_pdl(c, k_finalize, dim3(nf, B), dim3(KT), 0, F, B, st, K.Z.p, K.x.p);

@@ -235,6 +235,9 @@ void coarsest_solve(Context& c, int B, int c0, const int* act, const float2* f, 
   switch (c.vc.coarse_solver) {
     case HB_COARSE_GMRES:
       if (c.opt_small_coarse && launch_coarse_small(c, V, c.vc.coarse_iters, B, act, f, out)) break;
+      // one thread-block cluster per column, basis on chip (c2: 128^2)
+      if (c.opt_coarse_cluster && launch_coarse_cluster(c, V, c.vc.coarse_iters, B, c0 != 0 ? 1 : 0, act, f, out))
+        break;
       if (c.opt_coarse_krylov && L.N() > 2048 && c.vc.coarse_iters <= kMaxRestart) {  // multi-CTA Krylov kernels: fills the GPU at 128^2+
         coarse_krylov_solve(c, L, c.vc.coarse_iters, B, c0 != 0 ? 1 : 0, f, out);
         break;
@@ -1016,6 +1019,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_pdl = value != 0;
   else if (k == "coarse_krylov")
     ctx->opt_coarse_krylov = value != 0;
+  else if (k == "coarse_cluster")
+    ctx->opt_coarse_cluster = value != 0;
   else if (k == "lean_legs")
     ctx->opt_lean_legs = value != 0;
   else if (k == "conv_rows")

@@ -147,6 +147,9 @@ void launch_prolong_add(Context& c, const LevelView& Lf, int cnx, int cny, int o
                         const float2* vc, float2* v);
 void launch_restrict_plain(Context& c, int nx, int ny, int offset, int B, const float2* fine, float2* coarse);
 void launch_coarse_dense(Context& c, const Level& L, int B, const int* act, const float2* f, float2* x);
+// coarsest GMRES with one thread-block cluster per column (hb_coarse_cluster.cu); false if not applicable
+bool launch_coarse_cluster(Context& c, const LevelView& L, int iters, int B, int slot, const int* act, const float2* f,
+                           float2* x);
 void launch_coarse_gmres(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
                          float2* x, float2* scratch);
 // coarsest GMRES(iters) with D^-1 on the multi-CTA Krylov kernels (hb_krylov.cu), large coarse grids
@@ -294,7 +297,7 @@ struct Context {
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
        opt_coarse_reg = true, opt_wide_legs = false,
-       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
+       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_coarse_cluster = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size
   int opt_legs_wd = 2;  // Jacobi factor in the legs: 0 stored wD^-1, 1 from D, 2 by working-set size
   int conv_rows_ring = 4;

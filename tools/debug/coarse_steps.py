@@ -1,0 +1,30 @@
+"""Coarse-solve device time vs GMRES iterations (fixed cost vs per-step cost)."""
+import math
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+from paper_2203_11025_b200 import helmgpu as hg  # noqa: E402
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+om = 2 * math.pi * 1.5 * n / 10
+nc = n // 4
+f = np.random.default_rng(0).standard_normal((B, nc, nc)) + 0j
+for it in (1, 2, 5, 10):
+    ctx = hg.Context(0)
+    ctx.set_problem(hg.make_medium(n, n, 1234), hg.absorbing_layer(n, n, 16, 2 * om), om, 1 / 16, 1 / 2.25)
+    ctx.build_hierarchy(hg.VCycleConfig(levels=3, coarse_iters=it))
+    for opt in (1, 0):
+        ctx.set_option("coarse_cluster", opt)
+        ctx.coarse_solve(f)
+        ctx.prof_reset()
+        ctx.prof_enable(True)
+        for _ in range(5):
+            ctx.coarse_solve(f)
+        ctx.prof_enable(False)
+        p = ctx.prof()["coarse_solve"]
+        print(f"n={n} B={B} iters={it} cluster={opt}: {1e3 * p['ms'] / 5:.1f} us", flush=True)
+    ctx.close()

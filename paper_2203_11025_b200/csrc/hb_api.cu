@@ -204,6 +204,14 @@ void fill_level_device(Level& L, double omega, double alpha, double beta, double
   if (fp64M) {
     L.dM64.ensure(n);
     HB_CUDA(cudaMemcpy(L.dM64.p, dm64.data(), n * sizeof(double2), cudaMemcpyHostToDevice));
+    // D^-1 (c64) for the multi-CTA coarse GMRES: the fp32 reciprocal of the c64 diagonal (as crcp)
+    std::vector<float2> dmi(n, make_float2(0.f, 0.f));
+    for (size_t i = 0; i < n; ++i) {
+      const float s = 1.0f / std::fma(dm[i].x, dm[i].x, dm[i].y * dm[i].y);
+      dmi[i] = make_float2(dm[i].x * s, -dm[i].y * s);
+    }
+    L.dMi.ensure(n);
+    HB_CUDA(cudaMemcpy(L.dMi.p, dmi.data(), n * sizeof(float2), cudaMemcpyHostToDevice));
   }
 }
 

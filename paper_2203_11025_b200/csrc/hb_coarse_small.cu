@@ -29,34 +29,6 @@ __device__ __forceinline__ double2 zmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 zconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double2 zsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ double2 zscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-__device__ __forceinline__ double2 zdiv(double2 a, double2 b) {
-  if (fabs(b.x) >= fabs(b.y)) {
-    const double r = b.y / b.x, den = b.x + b.y * r;
-    return make_double2((a.x + a.y * r) / den, (a.y - a.x * r) / den);
-  }
-  const double r = b.x / b.y, den = b.x * r + b.y;
-  return make_double2((a.x * r + a.y) / den, (a.y * r - a.x) / den);
-}
-
-// warp reduce-scatter of 64 floats: on return lane l holds (sum over lanes of
-// v[2l], v[2l+1]) in v[0], v[1]
-__device__ __forceinline__ void warp_reduce_scatter64(float (&v)[64]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int stage = 0; stage < 5; ++stage) {
-    const int half = 32 >> stage;  // number of floats kept after this stage
-    const int mask = 16 >> stage;
-    const bool upper = (lane & mask) != 0;
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      if (k < half) {
-        const float send = upper ? v[k] : v[k + half];
-        const float keep = upper ? v[k + half] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-      }
-    }
-  }
-}
 
 // warp reduce-scatter of 32 floats: on return lane l holds the warp sum of v[l] in v[0]
 __device__ __forceinline__ void warp_reduce_scatter32(float (&v)[32]) {

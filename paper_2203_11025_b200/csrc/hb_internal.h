@@ -95,6 +95,7 @@ struct Level {
   DBuf<double2> dA64;  // level 0: fp64 diagonal of A^h for the restart residual
   DBuf<double2> dM64;  // coarsest level: fp64 diagonal of M^H (multi-CTA coarse GMRES restart)
   DBuf<double2> dinv;  // coarsest level, CoarseSolver::dense: (M^H)^-1 row-major fp64
+  DBuf<float2> dMi;    // coarsest level: D^-1 of M^H (c64), the coarse GMRES right preconditioner
   DBuf<float> k2f;
   // V-cycle work buffers [B][N]
   DBuf<float2> f, v, t, x;

@@ -64,6 +64,7 @@ struct FineView {
   const double2* dA64;  // fp64 diagonal of A^h (restart residual)
   const float2* dA;     // fp32 diagonal (A z per inner step)
   RowWin w;             // storage window: vectors are [B][w.rows][nx]; nodes of rows [w.lo, w.hi) are owned
+  const float2* dI = nullptr;  // coarse GMRES: D^-1 (the dots kernel applies A D^-1 s_j to Vraw_j itself)
   __device__ __forceinline__ size_t ns() const { return size_t(nx) * w.rows; }         // batch stride
   __device__ __forceinline__ size_t nown() const { return size_t(nx) * (w.hi - w.lo); }  // owned nodes
   __device__ __forceinline__ size_t off() const { return size_t(nx) * (w.lo - w.row0); } // first owned node
@@ -88,16 +89,6 @@ __device__ bool last_cta(unsigned* ticket, int b, int nblk) {
   }
   __syncthreads();
   return is_last;
-}
-
-// sum a per-warp smem partial table [8][nv] into out[nv] (threads < nv)
-__device__ void cta_fold(double2 (*part)[KMAXV], int nv, double2* out) {
-  __syncthreads();
-  for (int t = threadIdx.x; t < nv; t += KT) {
-    double2 s = make_double2(0.0, 0.0);
-    for (int w = 0; w < KT / 32; ++w) s = dadd(s, part[w][t]);
-    out[t] = s;
-  }
 }
 
 // r = b - A x (fp64), V0raw = r, ||r||^2 -> restart logic (inc/krylov.hpp:143-188)
@@ -269,6 +260,8 @@ __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState
   const float2* dA = F.dA + OFF;
   const float2* Vb = V + OFF + b * NS;
   const float inv_h2 = float(F.inv_h2);
+  const float2* dI = F.dI ? F.dI + OFF : nullptr;
+  const float sj = dI ? float(st[b].scale[j]) : 1.f;
   float acc[NF];
 #pragma unroll
   for (int s = 0; s < NF; ++s) acc[s] = 0.f;
@@ -278,7 +271,20 @@ __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState
 #pragma unroll
     for (int i = 0; i <= JM; ++i) a[i] = i <= j ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
     const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
-    const float2 w = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
+    float2 w;
+    if (dI) {  // w = A D^-1 (s_j Vraw_j), zb = Vraw_j (coarse GMRES, inc/multigrid.hpp:52-55)
+      float2 nb = make_float2(0.f, 0.f);
+      if (ix > 0) nb = cadd(nb, cmul(ld(zb, p - 1), ld(dI, p - 1)));
+      if (ix + 1 < F.nx) nb = cadd(nb, cmul(ld(zb, p + 1), ld(dI, p + 1)));
+      if (iy > 0) nb = cadd(nb, cmul(ld(zb, p - F.nx), ld(dI, p - F.nx)));
+      if (iy + 1 < F.ny) nb = cadd(nb, cmul(ld(zb, p + F.nx), ld(dI, p + F.nx)));
+      float2 y = cmul(ld(dA, p), cmul(ld(zb, p), ld(dI, p)));
+      y.x = fmaf(-inv_h2, nb.x, y.x);
+      y.y = fmaf(-inv_h2, nb.y, y.y);
+      w = cscale(y, sj);
+    } else {
+      w = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
+    }
     wb[p] = w;
 #pragma unroll
     for (int i = 0; i <= JM; ++i) {
@@ -614,6 +620,67 @@ __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st
   }
 }
 
+// coarse GMRES restart from x0 = 0: V_0raw = f (c64), ||f||^2 -> restart logic
+__global__ void __launch_bounds__(KT) k_coarse_restart(FineView F, int B, ColState* st, const float2* __restrict__ f,
+                                                       float2* __restrict__ V0, double* part, unsigned* ticket,
+                                                       double* hist, int hist_cap, int max_iters, int* act,
+                                                       float* scale_out, int* count) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  ColState& S = st[b];
+  const size_t N = F.nown();
+  double acc = 0.0;
+  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
+    const float2 v = ld(f + b * N, p);
+    V0[b * N + p] = v;
+    acc += dnorm2(v);
+  }
+  acc = warp_sum(acc);
+  __shared__ double wp[KT / 32];
+  if ((threadIdx.x & 31) == 0) wp[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < KT / 32; ++w) t += wp[w];
+    part[size_t(b) * gridDim.x + blockIdx.x] = t;
+  }
+  if (!last_cta(ticket, b, gridDim.x)) return;
+  if (threadIdx.x != 0) return;
+  double t = 0.0;
+  for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
+  restart_scalar(S, b, t, hist, hist_cap, 1e-300, max_iters, act, scale_out, count);
+}
+
+// coarse GMRES finalize: y = R^-1 g; x = D^-1 (sum_i y_i s_i Vraw_i) into the
+// c64 output (x0 = 0; inc/krylov.hpp:119-136, M = D^-1)
+__global__ void __launch_bounds__(KT) k_coarse_finalize(FineView F, int B, ColState* st, const float2* __restrict__ V,
+                                                        float2* __restrict__ x) {
+  pdl_enter();
+  const int b = blockIdx.y;
+  const ColState& S = st[b];
+  const int k = S.k;
+  const size_t N = F.nown();
+  if (k == 0) {
+    for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT)
+      x[b * N + p] = make_float2(0.f, 0.f);
+    return;
+  }
+  __shared__ double2 sH[kMaxRestart][kMaxRestart];
+  __shared__ double2 y[kMaxRestart];
+  __shared__ float2 c[kMaxRestart];
+  solve_small(S, k, sH, y);
+  if (threadIdx.x < k)
+    c[threadIdx.x] = make_float2(float(y[threadIdx.x].x * S.scale[threadIdx.x]),
+                                 float(y[threadIdx.x].y * S.scale[threadIdx.x]));
+  __syncthreads();
+  const size_t BN = size_t(B) * N;
+  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
+    float2 u = make_float2(0.f, 0.f);
+    for (int i = 0; i < k; ++i) u = cadd(u, cmul(c[i], ld(V + size_t(i) * BN + b * N, p)));
+    x[b * N + p] = cmul(u, ld(F.dI, p));
+  }
+}
+
 __global__ void k_init_state(ColState* st, int B, const int* limits) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= B) return;
@@ -819,38 +886,16 @@ void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x) {
 // preconditioner, x0 = 0, tol 1e-300 (fixed budget), happy breakdown as
 // krylov.hpp:240.  Operator = the level's shifted M^H (fp64 diagonal for the
 // restart residual).  One state set per half-batch stream (slot).
-namespace {
-__global__ void k_c64_to_c128(size_t n, const float2* __restrict__ a, double2* __restrict__ b) {
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-    b[i] = make_double2(a[i].x, a[i].y);
-}
-__global__ void k_c128_to_c64(size_t n, const double2* __restrict__ a, float2* __restrict__ b) {
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-    b[i] = make_float2(float(a[i].x), float(a[i].y));
-}
-// Z = D^-1 (s_b V)  (the diagonal "preconditioner" of the coarse GMRES)
-__global__ void k_diag_precond(int N, const int* act, const float2* __restrict__ V, const float* scale,
-                               const float2* __restrict__ d, float2* __restrict__ Z) {
-  const int b = blockIdx.y;
-  if (act && !act[b]) return;
-  const float s = scale[b];
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
-    Z[size_t(b) * N + i] = cmul(cscale(V[size_t(b) * N + i], s), crcp(__ldg(d + i)));
-}
-}  // namespace
 
 void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot, const float2* f, float2* x) {
   if (iters < 1 || iters > kMaxRestart) throw HbError{HB_ERR_ARG, "coarse GMRES iterations out of range"};
-  if (!L.dM64.p) throw HbError{HB_ERR_STATE, "coarsest level lacks the fp64 M diagonal"};
+  if (!L.dMi.p) throw HbError{HB_ERR_STATE, "coarsest level lacks D^-1"};
   Context::KrylovBufs& K = c.kcoarse[slot & 1];
   const size_t N = L.N();
   const int m = iters, cap = iters + 2;
   K.state.ensure(size_t(B) * sizeof(ColState));
   K.V.ensure(size_t(m + 1) * B * N);
-  K.Z.ensure(size_t(m) * B * N);
   K.W.ensure(size_t(B) * N);
-  K.b.ensure(size_t(B) * N);
-  K.x.ensure(size_t(B) * N);
   const int nbk = std::max(nblk_for(c, N, B), nblk_basis(c, N, B));
   K.part.ensure(size_t(B) * nbk * KMAXV);
   K.hist.ensure(size_t(B) * cap);
@@ -861,33 +906,25 @@ void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot,
     K.ticket.ensure(B);
     HB_CUDA(cudaMemsetAsync(K.ticket.p, 0, sizeof(unsigned) * B, c.stream));
   }
-  const FineView F{L.nx, L.ny, 1.0 / (L.h * L.h), L.dM64.p, L.dM.p, L.win()};
+  FineView F{L.nx, L.ny, 1.0 / (L.h * L.h), L.dM64.p, L.dM.p, L.win()};
+  F.dI = L.dMi.p;
   ColState* st = reinterpret_cast<ColState*>(K.state.p);
-  const size_t BN = size_t(B) * N;
-  const int g1 = int(std::min<size_t>((BN + 255) / 256, size_t(c.num_sms) * 8));
   const int tok = prof_begin(c, PC_COARSE);
-  c.launches += 4 + 3 * m;  // prof_begin counted one of the 5 + 3m kernels below
+  c.launches += 2 + 2 * m;  // prof_begin counted one of the 3 + 2m kernels below
   k_init_state<<<(B + 127) / 128, 128, 0, c.stream>>>(st, B, nullptr);
-  k_c64_to_c128<<<g1, 256, 0, c.stream>>>(BN, f, K.b.p);
-  HB_CUDA(cudaMemsetAsync(K.x.p, 0, sizeof(double2) * BN, c.stream));
-  HB_CUDA(cudaMemsetAsync(K.count.p, 0, sizeof(int), c.stream));
   const int nb = nblk_for(c, N, B);
-  const double tol = 1e-300;
-  launch_pdl(c, k_restart, dim3(nb, B), dim3(KT), 0, F, B, st, K.b.p, K.x.p, K.V.p, reinterpret_cast<double*>(K.part.p),
-                                               K.ticket.p, K.hist.p, cap, tol, m, K.act.p, K.scale.p, K.count.p,
-                                               (double2*)nullptr);
-  const dim3 gz(unsigned(std::max<size_t>(1, std::min<size_t>((N + 255) / 256, size_t(4) * c.num_sms / B))), B);
+  launch_pdl(c, k_coarse_restart, dim3(nb, B), dim3(KT), 0, F, B, st, f, K.V.p, reinterpret_cast<double*>(K.part.p),
+             K.ticket.p, K.hist.p, cap, m, K.act.p, K.scale.p, K.count.p);
+  const size_t BN = size_t(B) * N;
   for (int j = 0; j < m; ++j) {
-    float2* Vj = K.V.p + size_t(j) * BN;
-    float2* Zj = K.Z.p + size_t(j) * BN;
-    k_diag_precond<<<gz, 256, 0, c.stream>>>(int(N), K.act.p, Vj, K.scale.p, L.dM.p, Zj);
-    launch_adots(c, F, B, j, st, K.act.p, Zj, K.W.p, K.V.p, K.part.p, K.ticket.p, nullptr);
-    launch_update(c, F, B, j, m, st, K.act.p, K.W.p, K.V.p, K.part.p, K.ticket.p, K.hist.p, cap, tol, m, K.scale.p,
+    // w = A D^-1 (s_j Vraw_j) inside the dots kernel (no Z vectors: right
+    // preconditioning by a fixed diagonal, non-flexible as inc/multigrid.hpp:50)
+    launch_adots(c, F, B, j, st, K.act.p, K.V.p + size_t(j) * BN, K.W.p, K.V.p, K.part.p, K.ticket.p, nullptr);
+    launch_update(c, F, B, j, m, st, K.act.p, K.W.p, K.V.p, K.part.p, K.ticket.p, K.hist.p, cap, 1e-300, m, K.scale.p,
                   nullptr);
   }
   const int nf = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
-  launch_pdl(c, k_finalize, dim3(nf, B), dim3(KT), 0, F, B, st, K.Z.p, K.x.p);
-  k_c128_to_c64<<<g1, 256, 0, c.stream>>>(BN, K.x.p, x);
+  launch_pdl(c, k_coarse_finalize, dim3(nf, B), dim3(KT), 0, F, B, st, K.V.p, x);
   // algorithmic bytes: f in, x out (c64) -- the Krylov traffic of the coarse
   // level is accounted like the fine level's (Arnoldi over m steps)
   prof_end(c, PC_COARSE, tok, double(B) * N * 16.0 + double(N) * 8.0, 0);

@@ -56,6 +56,8 @@ struct TcParams {
   float* out;
   const int* act;
   long long* trace;  // debug: per-stage role timestamps of CTA 0 (HB_CONV_TRACE), else null
+  TcGeo geo;
+  TcEpi epi;
 };
 
 // pipeline geometry chosen on the host (see launch_conv_tc)
@@ -97,7 +99,15 @@ struct TcLayout {
 // All schedules are tabulated in shared memory once per CTA: the producer and
 // MMA loops are serial, and integer division there costs more than a
 // 16-channel chunk's data movement.
-constexpr int TC_MAX_CHUNKS = 320;  // K entries per tile (9 x channel chunks)
+__device__ __forceinline__ float elu_f(float t) { return t >= 0.0f ? t : expm1f(t); }
+// y = act(BN(t [+ res])) for output channel co (t includes the bias)
+__device__ __forceinline__ float tc_epilogue(const TcEpi& e, int co, float t, const float* res) {
+  if (res) t = *res + t;  // tape.add(x, t) (inc/unet.hpp:158)
+  if (e.mu) t = ((t - __ldg(e.mu + co)) * __ldg(e.is + co)) * __ldg(e.g + co) + __ldg(e.be + co);
+  return e.act == 1 ? fmaxf(t, 0.f) : e.act == 2 ? elu_f(t) : t;
+}
+
+constexpr int TC_MAX_CHUNKS = 320;  // K entries per tile (taps x channel chunks)
 constexpr int TC_MAX_SLOTS = 8;
 constexpr int TC_DYN_SMEM = 216 * 1024;  // + ~8 KB of static tables/barriers <= 227 KB
 
@@ -113,7 +123,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __shared__ uint64_t bar_afull[TC_MAX_SLOTS], bar_aempty[TC_MAX_SLOTS];   // TMEM A slots
   __shared__ uint64_t bar_tfull[2], bar_tempty[2], bar_w;
   __shared__ uint32_t tmem_slot;
-  __shared__ int4 sched[TC_MAX_CHUNKS];  // per K entry: {chunk-in-group | tap << 8, chunk, kglob, kc}
+  __shared__ int4 sched[TC_MAX_CHUNKS];  // per K entry: {chunk-in-group | ty << 8 | tx << 16, chunk, kglob, kc}
   __shared__ int2 stg[TC_MAX_CHUNKS];    // per stage: {kb0 | kb1 << 16, group | last stage of group << 16}
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = p.ntile;  // output channels of this CTA's work items; p.cout = row stride of out
@@ -124,7 +134,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int slot0 = lay.nacc * accw;     // first A-slot column
   const int tiles_x = p.W / p.bw, tiles_y = p.H / p.bh;
   const int ntiles = p.B * tiles_x * tiles_y * p.nsplit * p.ksplit;
-  const int hw = p.bw + 2;               // halo tile row pitch (pixels)
+  const int hw = p.geo.boxw;             // halo tile row pitch (pixels)
+  const int NT = p.geo.ntaps, cs = p.geo.s;
   // 1024-align by offset (not by integer cast) so the compiler keeps the shared address space
   unsigned char* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int w_bytes = 2 * N * kcmax * 4;  // one K entry of [W_hi ; W_lo]
@@ -135,25 +146,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int nca = p.s.ca / p.s.kca;
   const int cin = p.s.ca + p.s.cb;
   const int ngrp = (nchunk + CG - 1) / CG;
-  const int spg = (9 * CG + G - 1) / G;  // stages of a full group
+  const int spg = (NT * CG + G - 1) / G;  // stages of a full group
   const int cg_last = nchunk - (ngrp - 1) * CG;
-  const int nst = (ngrp - 1) * spg + (9 * cg_last + G - 1) / G;
-  const int nk = 9 * nchunk;
+  const int nst = (ngrp - 1) * spg + (NT * cg_last + G - 1) / G;
+  const int nk = NT * nchunk;
   for (int kb = threadIdx.x; kb < nk; kb += blockDim.x) {
-    const int g = kb / (9 * CG), r = kb - g * 9 * CG;
+    const int g = kb / (NT * CG), r = kb - g * NT * CG;
     const int cgn = min(CG, nchunk - g * CG);
     const int tap = r / cgn, j = r - tap * cgn;
     const int ch = g * CG + j;
     const bool srcb = ch >= nca;
     const int kc = srcb ? p.s.kcb : p.s.kca;
     const int cglob = srcb ? p.s.ca + (ch - nca) * kc : ch * kc;
-    sched[kb] = make_int4(j | (tap << 8), ch, tap * cin + cglob, kc);
+    // x: chunk-in-group | tap's halo-box offsets (ty << 8, tx << 16)
+    sched[kb] = make_int4(j | (p.geo.ty[tap] << 8) | (p.geo.tx[tap] << 16), ch, tap * cin + cglob, kc);
   }
   for (int st = threadIdx.x; st < nst; st += blockDim.x) {
     const int g = min(st / spg, ngrp - 1), ls = st - g * spg;
     const int cgn = min(CG, nchunk - g * CG);
-    const int gend = 9 * g * CG + 9 * cgn;
-    const int kb0 = 9 * g * CG + ls * G, kb1 = min(kb0 + G, gend);
+    const int gend = NT * g * CG + NT * cgn;
+    const int kb0 = NT * g * CG + ls * G, kb1 = min(kb0 + G, gend);
     stg[st] = make_int2(kb0 | (kb1 << 16), g | ((kb1 == gend ? 1 : 0) << 16));
   }
   if (threadIdx.x == 0) {
@@ -225,19 +237,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int st = s0; st < s1; ++st) {
         const int2 sg2 = stg[st];
         const int4 sg = make_int4(sg2.x & 0xffff, sg2.x >> 16, sg2.y & 0xffff, sg2.y >> 16);
-        if (sg.x == 9 * sg.z * CG || st == s0) {  // first stage of a group (in this split): its halo boxes
+        if (sg.x == NT * sg.z * CG || st == s0) {  // first stage of a group (in this split): its halo boxes
           if (hit >= nhbuf) mbar_wait(&bar_hempty[hb], hph ^ 1);
           const int c0 = sg.z * CG, c1 = min(nchunk, c0 + CG);
           uint32_t bytes = 0;
-          for (int ch = c0; ch < c1; ++ch) bytes += uint32_t((ch >= nca ? p.s.kcb : p.s.kca) * 4 * hw * (p.bh + 2));
+          for (int ch = c0; ch < c1; ++ch) bytes += uint32_t((ch >= nca ? p.s.kcb : p.s.kca) * 4 * hw * p.geo.boxh);
           if (p.trace && blockIdx.x == 0 && lane == 0 && it < 64) p.trace[it * 4 + 0] = clock64();
           mbar_expect_tx_elect(&bar_hfull[hb], (dbg & 8) ? 0u : bytes);
           for (int ch = c0; ch < c1 && !(dbg & 8); ++ch) {
             unsigned char* dst = base + hb * hbuf_bytes + (ch - c0) * lay.box_bytes;
             if (ch < nca)
-              tma_load_4d_elect(dst, &mapA, &bar_hfull[hb], ch * p.s.kca, x0 - 1, y0 - 1, b);
+              tma_load_4d_elect(dst, &mapA, &bar_hfull[hb], ch * p.s.kca, x0 * cs + p.geo.ox, y0 * cs + p.geo.oy, b);
             else
-              tma_load_4d_elect(dst, &mapB, &bar_hfull[hb], (ch - nca) * p.s.kcb, x0 - 1, y0 - 1, bb);
+              tma_load_4d_elect(dst, &mapB, &bar_hfull[hb], (ch - nca) * p.s.kcb, x0 * cs + p.geo.ox, y0 * cs + p.geo.oy,
+                                bb);
           }
           if (++hb == nhbuf) {
             hb = 0;
@@ -346,7 +359,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int st = s0; st < s1; ++st, ++itc) {
         const int2 sg2 = stg[st];
         const int4 sg = make_int4(sg2.x & 0xffff, sg2.x >> 16, sg2.y & 0xffff, sg2.y >> 16);
-        if (sg.x == 9 * sg.z * CG || st == s0) mbar_wait(&bar_hfull[hb], hph);
+        if (sg.x == NT * sg.z * CG || st == s0) mbar_wait(&bar_hfull[hb], hph);
         if (itc >= nslots) mbar_wait(&bar_aempty[j], aph ^ 1);
         tc_fence_after();
         if (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && itc < 64) p.trace[itc * 4 + 1] = clock64();
@@ -356,8 +369,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if ((dbg & 2) || ((kb - sg.x) & 1) != half) continue;
           const int4 e = sched[kb];
           const int kc = KC ? KC : e.w;
-          const int tap = e.x >> 8, cj = e.x & 255;
-          const int hp = (yy + tap / 3) * hw + xx + tap % 3;  // shifted halo pixel
+          const int cj = e.x & 255, ty = (e.x >> 8) & 255, tx = (e.x >> 16) & 255;
+          const int hp = (yy * cs + ty) * hw + xx * cs + tx;  // shifted halo pixel
           const unsigned char* row = hbuf + cj * lay.box_bytes + hp * (kc * 4);
           // swizzled 16-B chunk c of smem row hp sits at c ^ f(hp): SW128 f = hp & 7, SW64 f = (hp >> 1) & 3
           const int f = kc == 32 ? (hp & 7) : ((hp >> 1) & 3);
@@ -366,7 +379,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             uint32_t vh[16], vl[16];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              const float4 x = *reinterpret_cast<const float4*>(row + (((4 * h + c) ^ f) << 4));
+              float4 x = *reinterpret_cast<const float4*>(row + (((4 * h + c) ^ f) << 4));
+              if (p.epi.in_elu) x = make_float4(elu_f(x.x), elu_f(x.y), elu_f(x.z), elu_f(x.w));
               const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
@@ -411,8 +425,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int row = 32 * q + lane;
       const int yy = row / p.bw, xx = row % p.bw;
       const size_t pix = (size_t(b) * p.H + (y0 + yy)) * p.W + (x0 + xx);
-      const bool part = p.ksplit > 1;  // raw partial sum; bias + ReLU after the K reduction
-      float* orow = (part ? p.ws + size_t(ks) * p.B * p.H * p.W * p.cout : p.out) + pix * p.cout + n0;
+      const size_t opix = (size_t(b) * p.geo.Ho + (y0 + yy) * p.geo.os + p.geo.py) * p.geo.Wo +
+                          (x0 + xx) * p.geo.os + p.geo.px;
+      const bool part = p.ksplit > 1;  // raw partial sum; the epilogue runs after the K reduction
+      float* orow = part ? p.ws + size_t(ks) * p.B * p.H * p.W * p.cout + pix * p.cout + n0
+                         : p.out + opix * p.geo.ldo + n0;
+      const float* rrow = p.epi.res ? p.epi.res + opix * p.epi.ldres + n0 : nullptr;
       const float* bias = p.bias + n0;
       const uint32_t trow = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * accw);
       for (int c0 = 0; c0 < ((dbg & 4) ? 0 : N); c0 += 16) {
@@ -424,16 +442,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float x = __uint_as_float(v[i]) + __uint_as_float(u[i]);
-          if (part) {
-            o[i] = x;
-          } else {
-            const float y = x + __ldg(bias + c0 + i);
-            o[i] = p.relu ? fmaxf(y, 0.f) : y;
-          }
+          o[i] = part ? x : tc_epilogue(p.epi, n0 + c0 + i, x + __ldg(bias + c0 + i), rrow ? rrow + c0 + i : nullptr);
         }
+        const int nvalid = p.epi.nco && !part ? p.epi.nco - (n0 + c0) : 16;  // padded output channels: not stored
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
-          *reinterpret_cast<float4*>(orow + c0 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
+          if (i < nvalid) *reinterpret_cast<float4*>(orow + c0 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
       }
       tc_fence_before();
       mbar_arrive(&bar_tempty[acc]);
@@ -448,21 +462,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   }
 }
 
-// split-K reduction: out = act(bias + sum_s ws[s]) in fixed order (deterministic)
-__global__ void k_conv_ksum(int ksplit, size_t n4, int cout4, size_t img4, const int* act, const float4* __restrict__ ws,
-                            const float4* __restrict__ bias, int relu, float4* __restrict__ out) {
-  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x) {
-    if (act && !act[i / img4]) continue;  // frozen column: its partials were not written
-    float4 a = __ldg(bias + (i % cout4));
-    for (int s = 0; s < ksplit; ++s) {
-      const float4 v = __ldg(ws + size_t(s) * n4 + i);
-      a.x += v.x;
-      a.y += v.y;
-      a.z += v.z;
-      a.w += v.w;
-    }
-    if (relu) a = make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
-    out[i] = a;
+// split-K reduction: out = epilogue(bias + sum_s ws[s]) in fixed order
+// (deterministic); ws is dense over the tile grid, out follows the geometry
+__global__ void k_conv_ksum(int ksplit, int B, int H, int W, int cout, const int* act, const float* __restrict__ ws,
+                            const float* __restrict__ bias, TcGeo geo, TcEpi epi, float* __restrict__ out) {
+  const size_t n = size_t(B) * H * W * cout;
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
+    const size_t pix = i / cout;
+    const int co = int(i - pix * cout);
+    const int b = int(pix / (size_t(H) * W));
+    if (act && !act[b]) continue;  // frozen column: its partials were not written
+    const int rem = int(pix - size_t(b) * H * W), y = rem / W, x = rem - y * W;
+    float a = __ldg(bias + co);
+    for (int s = 0; s < ksplit; ++s) a += __ldg(ws + size_t(s) * n + i);
+    if (epi.nco && co >= epi.nco) continue;  // padded output channel
+    const size_t opix = (size_t(b) * geo.Ho + y * geo.os + geo.py) * geo.Wo + x * geo.os + geo.px;
+    out[opix * geo.ldo + co] = tc_epilogue(epi, co, a, epi.res ? epi.res + opix * epi.ldres + co : nullptr);
   }
 }
 
@@ -515,44 +530,41 @@ CUtensorMap w_map(const float* ptr, int cout, int K, int kc, int rows) {
 // hi/lo split of the packed [Cout][9*Cin] weights (host, once per upload)
 void conv_tc_prepare(ConvW& cw) {
   const int K = 9 * cw.cin;
-  std::vector<float> hi(size_t(cw.cout) * K), lo(size_t(cw.cout) * K);
-  auto tf32 = [](float x) {  // round to nearest, ties away (cvt.rna.tf32.f32)
-    uint32_t u;
-    std::memcpy(&u, &x, 4);
-    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
-    float r;
-    std::memcpy(&r, &u, 4);
-    return r;
-  };
+  std::vector<float> packed(size_t(cw.cout) * K);
   for (int co = 0; co < cw.cout; ++co)
     for (int tap = 0; tap < 9; ++tap)
-      for (int ci = 0; ci < cw.cin; ++ci) {
-        const float w = cw.w[(size_t(co) * cw.cin + ci) * 9 + tap];
-        const float h = tf32(w);
-        hi[size_t(co) * K + size_t(tap) * cw.cin + ci] = h;
-        lo[size_t(co) * K + size_t(tap) * cw.cin + ci] = tf32(w - h);
-      }
-  cw.dwh.ensure(hi.size());
-  cw.dwl.ensure(lo.size());
-  HB_CUDA(cudaMemcpy(cw.dwh.p, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
-  HB_CUDA(cudaMemcpy(cw.dwl.p, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice));
+      for (int ci = 0; ci < cw.cin; ++ci)
+        packed[size_t(co) * K + size_t(tap) * cw.cin + ci] = cw.w[(size_t(co) * cw.cin + ci) * 9 + tap];
+  conv_tc_upload_packed(cw, packed);
 }
 
 static bool tc_ok_channels(int c) { return c > 0 && c % 16 == 0; }
 
 // returns false when the shape is not supported by the tensor-core path
-bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
-                    const float* bsrc, int cb, bool b_ctx, int relu, float* out) {
+bool launch_conv_tc_gen(Context& c, const TcConv& t) {
+  const ConvW& cw = *t.cw;
+  const int B = t.B, H = t.H, W = t.W, ca = t.ca, cb = t.cb;
+  const int NT = t.geo.ntaps;
   if (!c.opt_tc_conv) return false;
+  if (NT < 1 || NT > TC_MAX_TAPS) return false;
   if (!tc_ok_channels(ca) || (cb && !tc_ok_channels(cb))) return false;
-  if (cw.cout % 16 || cw.cout > 256 || cw.cout < 16) return false;
+  if (cw.cout % 16 || cw.cout > 256 || cw.cout < 16 || !cw.dwh.p) return false;
   const int bw = W < TC_M ? W : TC_M;
   const int bh = TC_M / bw;
-  if (W % bw || H % bh || bw * bh != TC_M || bw < 8 || !cw.dwh.p) return false;
+  if (W % bw || H % bh || bw * bh != TC_M || bw < 8) return false;
+  int mty = 0, mtx = 0;
+  for (int i = 0; i < NT; ++i) {
+    mty = std::max(mty, t.geo.ty[i]);
+    mtx = std::max(mtx, t.geo.tx[i]);
+  }
+  TcGeo geo = t.geo;
+  geo.boxh = (bh - 1) * geo.s + mty + 1;
+  geo.boxw = (bw - 1) * geo.s + mtx + 1;
+  if (geo.boxh > 256 || geo.boxw > 256) return false;
   const int kca = ca % 32 == 0 ? 32 : 16, kcb = cb ? (cb % 32 == 0 ? 32 : 16) : 32;
   const int kcmax = (kca == 32 || (cb && kcb == 32)) ? 32 : 16;
   const int nchunk = ca / kca + (cb ? cb / kcb : 0);
-  const int nk = 9 * nchunk;
+  const int nk = NT * nchunk;
   if (nk > TC_MAX_CHUNKS) return false;
   // Cout > 128 is split into 128-channel work items so every layer uses the
   // split-accumulator form (correction terms summed apart, better accuracy)
@@ -576,7 +588,7 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   const int w_chunk = 2 * ntile * kcmax * 4;
   lay.wres = nsplit == 1 && nk * w_chunk <= 96 * 1024 ? 1 : 0;
   lay.stages = lay.wres ? 1 : 4;
-  lay.box_bytes = ((kcmax * 4 * (bw + 2) * (bh + 2)) + 1023) & ~1023;
+  lay.box_bytes = ((kcmax * 4 * geo.boxw * geo.boxh) + 1023) & ~1023;
   auto wsmem = [&]() { return lay.wres ? nk * w_chunk : lay.stages * lay.G * w_chunk; };
   for (;;) {
     const int room = budget - wsmem();
@@ -591,18 +603,18 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   }
   if (lay.CG < 1) return false;
   const int ngrp = (nchunk + lay.CG - 1) / lay.CG;
-  const int spg = (9 * lay.CG + lay.G - 1) / lay.G;
+  const int spg = (NT * lay.CG + lay.G - 1) / lay.G;
   if (ngrp * spg > TC_MAX_CHUNKS) return false;
   const size_t smem = size_t(lay.nhbuf) * lay.CG * lay.box_bytes + size_t(wsmem()) + 1024;
 
-  const CUtensorMap mA = act_map(a, B, H, W, ca, kca, bw + 2, bh + 2);
-  const CUtensorMap mB = cb ? act_map(bsrc, b_ctx ? 1 : B, H, W, cb, kcb, bw + 2, bh + 2) : mA;
-  const int K = 9 * cw.cin;
+  const CUtensorMap mA = act_map(t.a, B, t.Hin, t.Win, ca, kca, geo.boxw, geo.boxh);
+  const CUtensorMap mB = cb ? act_map(t.bsrc, t.b_ctx ? 1 : B, t.Hin, t.Win, cb, kcb, geo.boxw, geo.boxh) : mA;
+  const int K = NT * cw.cin;
   const CUtensorMap wh32 = w_map(cw.dwh.p, cw.cout, K, 32, ntile), wl32 = w_map(cw.dwl.p, cw.cout, K, 32, ntile);
   const CUtensorMap wh16 = w_map(cw.dwh.p, cw.cout, K, 16, ntile), wl16 = w_map(cw.dwl.p, cw.cout, K, 16, ntile);
   // split K when the pixel tiles alone cannot fill the SMs (low-resolution levels)
   const int tiles0 = B * (H / bh) * (W / bw) * nsplit;
-  const int nst = (ngrp - 1) * spg + (9 * (nchunk - (ngrp - 1) * lay.CG) + lay.G - 1) / lay.G;
+  const int nst = (ngrp - 1) * spg + (NT * (nchunk - (ngrp - 1) * lay.CG) + lay.G - 1) / lay.G;
   int ksplit = 1;
   if (c.opt_conv_ksplit && tiles0 * 2 <= c.num_sms)
     ksplit = std::max(1, std::min({nst, c.num_sms / tiles0, 8}));
@@ -613,8 +625,8 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
     c.conv_ws.ensure(size_t(ksplit) * B * H * W * cw.cout);
     ws = c.conv_ws.p;
   }
-  TcParams p{B,  H,  W,     cw.cout, relu, ntile,   nsplit, ksplit, sps, ws, bw, bh,
-             TcSources{ca, cb, kca, kcb, b_ctx ? 1 : 0}, cw.db.p, out, act, nullptr};
+  TcParams p{B,  H,  W,     cw.cout, t.epi.act == 1 ? 1 : 0, ntile,   nsplit, ksplit, sps, ws, bw, bh,
+             TcSources{ca, cb, kca, kcb, t.b_ctx ? 1 : 0}, cw.db.p, t.out, t.act, nullptr, geo, t.epi};
   static const bool trace = getenv("HB_CONV_TRACE") != nullptr;
   static long long* dtrace = nullptr;
   if (trace) {
@@ -638,18 +650,18 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   const int tok = prof_begin(c, PC_CONV);
   if (c.prof_detail)
     c.prof_label = "conv_tc " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
-                   std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
+                   std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout) + " taps " +
+                   std::to_string(NT) + " s" + std::to_string(geo.s);
   static const int dbg = getenv("HB_CONV_DEBUG") ? atoi(getenv("HB_CONV_DEBUG")) : 0;
   kern<<<grid, TC_THREADS, smem, c.stream>>>(mA, mB, wh32, wl32, wh16, wl16, p, lay, dbg);
   if (ksplit > 1) {
     HB_CUDA(cudaGetLastError());
-    const size_t n4 = size_t(B) * H * W * cw.cout / 4;
-    k_conv_ksum<<<int(std::min<size_t>((n4 + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
-        ksplit, n4, cw.cout / 4, size_t(H) * W * cw.cout / 4, act, reinterpret_cast<const float4*>(ws), reinterpret_cast<const float4*>(cw.db.p), relu,
-        reinterpret_cast<float4*>(out));
+    const size_t n = size_t(B) * H * W * cw.cout;
+    k_conv_ksum<<<int(std::min<size_t>((n + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
+        ksplit, B, H, W, cw.cout, t.act, ws, cw.db.p, geo, t.epi, t.out);
   }
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout),
-           2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
+           2.0 * B * H * W * double(NT) * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());
   if (trace) {
     long long h[256];
@@ -666,6 +678,65 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
               h[i * 4 + 3] - t0);
   }
   return true;
+}
+
+// the classic U-Net's 3x3 / stride 1 / pad 1 conv with bias + ReLU
+bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
+                    const float* bsrc, int cb, bool b_ctx, int relu, float* out) {
+  TcConv t{};
+  t.cw = &cw;
+  t.B = B;
+  t.Hin = t.H = H;
+  t.Win = t.W = W;
+  t.a = a;
+  t.ca = ca;
+  t.bsrc = bsrc;
+  t.cb = cb;
+  t.b_ctx = b_ctx;
+  t.out = out;
+  t.act = act;
+  t.geo = conv_geo_3x3(H, W, cw.cout);
+  t.epi = TcEpi{nullptr, 0, nullptr, nullptr, nullptr, nullptr, relu ? 1 : 0, 0, 0};
+  return launch_conv_tc_gen(c, t);
+}
+
+// stride-1, pad-1 3x3 geometry on an H x W grid, dense output (ldo = cout)
+TcGeo conv_geo_3x3(int H, int W, int cout) {
+  TcGeo g{};
+  g.ntaps = 9;
+  g.s = 1;
+  g.oy = g.ox = -1;
+  g.os = 1;
+  g.Ho = H;
+  g.Wo = W;
+  g.ldo = cout;
+  for (int tap = 0; tap < 9; ++tap) {
+    g.ty[tap] = tap / 3;
+    g.tx[tap] = tap % 3;
+  }
+  return g;
+}
+
+// hi/lo split (3xTF32) of packed [Cout][K] weights, K = ntaps * Cin ordered
+// (tap, ci), uploaded to cw.dwh / cw.dwl (host, once per upload)
+void conv_tc_upload_packed(ConvW& cw, const std::vector<float>& packed) {
+  auto tf32 = [](float x) {  // round to nearest, ties away (cvt.rna.tf32.f32)
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+    float r;
+    std::memcpy(&r, &u, 4);
+    return r;
+  };
+  std::vector<float> hi(packed.size()), lo(packed.size());
+  for (size_t i = 0; i < packed.size(); ++i) {
+    hi[i] = tf32(packed[i]);
+    lo[i] = tf32(packed[i] - hi[i]);
+  }
+  cw.dwh.ensure(hi.size());
+  cw.dwl.ensure(lo.size());
+  HB_CUDA(cudaMemcpy(cw.dwh.p, hi.data(), hi.size() * 4, cudaMemcpyHostToDevice));
+  HB_CUDA(cudaMemcpy(cw.dwl.p, lo.data(), lo.size() * 4, cudaMemcpyHostToDevice));
 }
 
 }  // namespace hb

@@ -166,6 +166,51 @@ void launch_up_fused(Context& c, const LevelView& L, float damping, int offset, 
                      float2* z);
 // tensor-core conv (hb_conv_tc.cu, hb_conv_rows.cu)
 void conv_tc_prepare(ConvW& cw);
+// generalised tensor-core convolution (hb_conv_tc.cu): any tap set (<= 25),
+// input stride 1 | 2, output scatter / channel slice, fused bias [+ residual]
+// [+ BN eval] [+ ReLU | ELU] epilogue, optional ELU on the inputs
+constexpr int TC_MAX_TAPS = 25;  // up to a 5x5 kernel
+
+// Geometry of one implicit-GEMM launch.  Output tile grid [H][W] (tiles of bh
+// x bw pixels); tap t of output pixel (y, x) reads the input pixel at
+// (y * s + oy + ty[t], x * s + ox + tx[t]) -- inside the tile's halo box of
+// boxh x boxw pixels whose origin is (y0 * s + oy, x0 * s + ox).  Tile-grid
+// pixel (y, x) is stored at output pixel (y * os + py, x * os + px) of [Ho][Wo]
+// with a row stride of ldo floats (a parity class of a stride-2 transposed
+// convolution: os = 2; a channel slice of a concatenation: ldo > cout).
+struct TcGeo {
+  int ntaps, s, oy, ox, boxh, boxw;
+  int os, py, px, Ho, Wo, ldo;
+  int ty[TC_MAX_TAPS], tx[TC_MAX_TAPS];
+};
+// epilogue: y = act(BN(x + bias [+ res])), BN in eval form ((t - mu) is) g + be
+// (inc/autodiff.hpp:289-296); act 0 none, 1 ReLU, 2 ELU; in_elu: ELU applied to
+// the input values as they are loaded (the paper net's up path)
+struct TcEpi {
+  const float* res;
+  int ldres;
+  const float *mu, *is, *g, *be;
+  int act, in_elu;
+  int nco;  // output channels actually stored (< cout when cout was padded to a multiple of 16); 0: all
+};
+
+// one launch: weights cw (dwh / dwl [cout][ntaps * cin], db bias), input a
+// [B][Hin][Win][ca] (+ b [.][Hin][Win][cb], batch-broadcast when b_ctx), output
+// tile grid H x W
+struct TcConv {
+  const ConvW* cw;
+  int B, Hin, Win, H, W;
+  const float *a, *bsrc;
+  int ca, cb;
+  bool b_ctx;
+  TcGeo geo;
+  TcEpi epi;
+  float* out;
+  const int* act;
+};
+bool launch_conv_tc_gen(Context& c, const TcConv& t);
+TcGeo conv_geo_3x3(int H, int W, int cout);
+void conv_tc_upload_packed(ConvW& cw, const std::vector<float>& packed);
 void conv_rows_prepare(ConvW& cw);
 bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                       const float* bsrc, int cb, bool b_ctx, int relu, float* out);

@@ -179,6 +179,71 @@ void upload_conv(PaperState& P, const std::string& kname, const std::string& bna
   };
   up(D.w, w);
   up(D.bias, Bq.v);
+  // tensor-core form (hb_conv_tc.cu): taps as input offsets (dy, dx) of the
+  // output pixel's stride-s origin, weights packed [cout][tap][cin]
+  D.tc.clear();
+  // output channels padded to a multiple of 16 with zero weights (the up path's
+  // base/2 = 8-channel layer); the epilogue stores only the real ones
+  const int coutp = (D.cout + 15) / 16 * 16;
+  if (D.cin % 16 == 0 && coutp <= 256 && k <= 5) {
+    const int pad = (k - 1) / 2;
+    auto padv = [&](const std::vector<float>& v, float fill) {
+      std::vector<float> o(v);
+      o.resize(size_t(coutp), fill);
+      return o;
+    };
+    auto make = [&](const std::vector<std::pair<int, int>>& tk, const std::vector<std::pair<int, int>>& off, int py,
+                    int px) {
+      PaperTc T;
+      T.cw.cout = coutp;
+      T.cw.cin = D.cin;
+      const int nt = int(tk.size());
+      std::vector<float> packed(size_t(coutp) * nt * D.cin, 0.f);
+      for (int co = 0; co < D.cout; ++co)
+        for (int t = 0; t < nt; ++t)
+          for (int ci = 0; ci < D.cin; ++ci)
+            packed[(size_t(co) * nt + t) * D.cin + ci] = w[(size_t(tk[t].first * k + tk[t].second) * D.cin + ci) * D.cout + co];
+      conv_tc_upload_packed(T.cw, packed);
+      up(T.cw.db, padv(Bq.v, 0.f));
+      int oy = 0, ox = 0;
+      for (auto& o : off) {
+        oy = std::min(oy, o.first);
+        ox = std::min(ox, o.second);
+      }
+      T.geo = TcGeo{};
+      T.geo.ntaps = nt;
+      T.geo.oy = oy;
+      T.geo.ox = ox;
+      T.geo.py = py;
+      T.geo.px = px;
+      for (int t = 0; t < nt; ++t) {
+        T.geo.ty[t] = off[t].first - oy;
+        T.geo.tx[t] = off[t].second - ox;
+      }
+      D.tc.push_back(std::move(T));
+    };
+    if (!transpose) {  // conv2d (inc/autodiff.hpp:31-39): input (o s + ky - pad, o s + kx - pad)
+      std::vector<std::pair<int, int>> tk, off;
+      for (int ky = 0; ky < k; ++ky)
+        for (int kx = 0; kx < k; ++kx) {
+          tk.push_back({ky, kx});
+          off.push_back({ky - pad, kx - pad});
+        }
+      make(tk, off, 0, 0);
+    } else {  // conv2d_transpose, stride 2 (:190-215): output class (py, px) of pixel 2 o + p meets taps
+      // k = p + pad (mod 2), input o + (p + pad - k) / 2
+      for (int py = 0; py < 2; ++py)
+        for (int px = 0; px < 2; ++px) {
+          std::vector<std::pair<int, int>> tk, off;
+          for (int ky = (py + pad) & 1; ky < k; ky += 2)
+            for (int kx = (px + pad) & 1; kx < k; kx += 2) {
+              tk.push_back({ky, kx});
+              off.push_back({(py + pad - ky) / 2, (px + pad - kx) / 2});
+            }
+          make(tk, off, py, px);
+        }
+    }
+  }
   D.bn = !bn.empty();
   if (D.bn) {
     if (param(P, bn + ".count").v[0] <= 0.0f)
@@ -190,6 +255,17 @@ void upload_conv(PaperState& P, const std::string& kname, const std::string& bna
     up(D.is, is);
     up(D.g, param(P, bn + ".scale").v);
     up(D.be, param(P, bn + ".offset").v);
+    auto padv = [&](const std::vector<float>& v, float fill) {
+      std::vector<float> o(v);
+      o.resize(size_t(coutp), fill);
+      return o;
+    };
+    for (PaperTc& T : D.tc) {
+      up(T.mu, padv(param(P, bn + ".rmean").v, 0.f));
+      up(T.is, padv(is, 1.f));
+      up(T.g, padv(param(P, bn + ".scale").v, 1.f));
+      up(T.be, padv(param(P, bn + ".offset").v, 0.f));
+    }
   }
 }
 
@@ -545,6 +621,38 @@ struct Exec {
     a.B = nb < 0 ? B : nb;
     a.xbatch = xbatch;
     const long long npix = (long long)a.B * a.Ho * a.Wo;
+    // tensor cores (3xTF32 implicit GEMM, hb_conv_tc.cu) where the layer's
+    // channels and dense input allow; the register-tiled SIMT kernel otherwise
+    if (!D.tc.empty() && xbatch && x.ld == x.C && (!res || res->ld == y.C) && y.ld % 4 == 0 && c.opt_tc_conv &&
+        (!D.transpose || stride == 2)) {
+      bool ok = true;
+      for (const PaperTc& T : D.tc) {
+        TcConv t{};
+        t.cw = &T.cw;
+        t.B = a.B;
+        t.Hin = x.H;
+        t.Win = x.W;
+        t.H = D.transpose ? x.H : y.H;  // tile grid: the output (class) grid
+        t.W = D.transpose ? x.W : y.W;
+        t.a = x.p;
+        t.ca = x.C;
+        t.geo = T.geo;
+        t.geo.s = D.transpose ? 1 : stride;
+        t.geo.os = D.transpose ? 2 : 1;
+        t.geo.Ho = y.H;
+        t.geo.Wo = y.W;
+        t.geo.ldo = y.ld;
+        t.epi = TcEpi{res ? res->p : nullptr, res ? res->ld : 0, D.bn ? T.mu.p : nullptr, T.is.p, T.g.p, T.be.p,
+                      act ? 2 : 0, in_elu ? 1 : 0, D.cout};
+        t.out = y.p;
+        if (c.prof_detail) c.prof_label = kname;
+        if (!launch_conv_tc_gen(c, t)) {
+          ok = false;
+          break;
+        }
+      }
+      if (ok) return;  // (a refused class falls through: the SIMT kernel below rewrites every class)
+    }
     const int tok = prof_begin(c, PC_CONV);
     {
       const bool par = a.transpose && a.stride == 2;

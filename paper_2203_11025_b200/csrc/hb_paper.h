@@ -17,10 +17,19 @@ struct PParam {
   size_t size() const { return size_t(d[0]) * d[1] * d[2] * d[3]; }
 };
 
+// one tensor-core implicit GEMM of a paper-net convolution: the whole conv, or
+// one output parity class of a stride-2 transposed conv (hb_conv_tc.cu)
+struct PaperTc {
+  ConvW cw;  // dwh / dwl [cout][ntaps * cin] (3xTF32 split), db bias; cout padded to a multiple of 16
+  TcGeo geo; // taps, input origin offsets; output class (py, px)
+  DBuf<float> mu, is, g, be;  // batch-norm buffers padded like cout (when the conv has one)
+};
+
 struct DevConv {  // one convolution with its fused epilogue
   int cout = 0, cin = 0, k = 0;
   bool transpose = false, bn = false;
   DBuf<float> w, bias, mu, is, g, be;
+  std::vector<PaperTc> tc;  // tensor-core form (empty: channels not multiples of 16)
 };
 
 struct PaperState {

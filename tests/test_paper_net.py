@@ -199,3 +199,32 @@ def test_training_pairs_match_reference(hg, gold):
     H = O.Hierarchy(gold["k2"], gold["gamma"], float(gold["omega"]), 1 / 16, 1 / 2.25, levels=3)
     for i in range(2):
         assert rel(H.apply(e[i]), r[i]) < 1e-10  # A e = r in fp64 (the generator's invariant)
+
+
+@pytest.mark.gpu
+def test_paper_forward_tensor_core_sizes(hg):
+    """UNetConfig() defaults at 128^2 (tests/golden/make_paper_tc_golden.py): the
+    5x5 stride-2 down convolutions, the 3x3 ResNet convolutions (bias, batch
+    norm, ELU, residual add fused in the epilogue) and the stride-2 transposed
+    up convolutions (four output parity classes, ELU on the inputs) run as
+    3xTF32 tcgen05 implicit GEMMs (hb_conv_tc.cu); the output matches the
+    reference's forward to 1e-4 and the register-tiled SIMT path to 1e-5."""
+    g = np.load(os.path.join(GOLD, "paper_tc.npz"))
+    x = np.random.default_rng(9).standard_normal((2, 4, 128, 128)).astype(np.float32)
+    c = hg.Context(0)
+    c.set_paper_net(hg.UNetConfig(levels=3, base_channels=16, resnet_per_level=1, bottleneck_resnets=3,
+                                  updown_kernel=5, res_kernel=3), VARIANT["s"])
+    c.load_checkpoint(os.path.join(GOLD, "paper_tc_s.unw1"))
+    c.prof_enable(True)
+    c.prof_detail(True)
+    y = c.paper_forward(x)
+    labels = [rec[0] for rec in c.prof_detail(False)]
+    c.prof_enable(False)
+    tc = [ln for ln in labels if ln.startswith("conv_tc")]
+    assert len(tc) >= 10, labels  # down1/2, 2 x 5 ResNets, 4 x up2/up1 classes ...
+    assert any("taps 25 s2" in ln for ln in tc) and any("taps 4 s1" in ln for ln in tc), tc
+    assert rel(y, g["y"]) < 1e-4, rel(y, g["y"])
+    c.set_option("tc_conv", 0)
+    y2 = c.paper_forward(x)
+    assert rel(y, y2) < 1e-5, rel(y, y2)
+    c.close()

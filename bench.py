@@ -540,9 +540,10 @@ def run_ours(args, ws, rank, local):
             if nm == "c4slab":
                 line["also"][nm] = slab
                 continue
-            if nm in ("datagen", "paper_ju", "train"):
+            if nm in ("datagen", "paper_ju", "train", "block"):
                 try:
-                    fn = {"datagen": datagen_budget, "paper_ju": paper_ju_budget, "train": train_budget}[nm]
+                    fn = {"datagen": datagen_budget, "paper_ju": paper_ju_budget, "train": train_budget,
+                          "block": block_budget}[nm]
                     line["also"][nm] = fn(local, args)
                 except Exception as e:  # reported, not hidden
                     line["also"][nm] = {"error": repr(e)}
@@ -673,6 +674,37 @@ def datagen_budget(local, args):
             out["cpu_reference"] = {"pairs_per_s": n / dt, "pairs": n, "cores": 1, "kind": "reference"}
     except Exception as ex:  # reported, not hidden
         out["cpu_reference"] = {"error": repr(ex)}
+    return out
+
+
+def block_budget(local, args):
+    """True block FGMRES (hb_block_fgmres, PAPER.md:580
+    block-size study) on the c0 problem: 8 seeded complex-normal right-hand
+    sides solved as ONE block Krylov space vs the same 8 as independent
+    columns (block_fgmres semantics), M_V, restart 10, to 1e-6.  Device time
+    of the whole solve (host c128 I/O included in both)."""
+    import time
+    import torch
+    from paper_2203_11025_b200 import helmgpu as hg
+    from paper_2203_11025_b200 import problems
+    cfg = config_for("c0")
+    ctx, arr = problems.gpu_setup(cfg, device=local)
+    p = 8
+    rng = np.random.default_rng(11)
+    B = rng.standard_normal((p, cfg["n"], cfg["n"])) + 1j * rng.standard_normal((p, cfg["n"], cfg["n"]))
+    kc = hg.KrylovConfig(restart=10, max_iters=400, rel_tol=1e-6)
+    out = {"grid": cfg["n"], "rhs": p, "restart": 10}
+    for name, fn in (("block", ctx.block_fgmres), ("columns", ctx.fgmres)):
+        fn("v", B, kc)  # warm-up
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        X, rep = fn("v", B, kc)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out[name] = {"iterations": int(max(rep.iterations)), "converged": bool(all(rep.converged)),
+                     "ms": 1e3 * dt, "solves_per_s": p / dt,
+                     "preconditioner_applies": int(max(rep.iterations)) * p}
+    ctx.close()
     return out
 
 
@@ -849,7 +881,7 @@ def main():
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = 3 per SM: one per SM in each of the 3 column groups)")
-    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,datagen,paper_ju,train", help="comma list of configs measured on a fixed iteration budget "
+    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,datagen,paper_ju,train,block", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")

@@ -140,6 +140,17 @@ typedef struct hb_krylov_cfg {
 int hb_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,
               double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
               uint8_t* breakdown);
+/* True block FGMRES (a non-goal of the reference,
+ * SPEC.md:280, its block-size study PAPER.md:580): the batch (<= 16 columns)
+ * shares ONE block Krylov space -- block CGS2 orthogonalisation, CholQR2 of
+ * each new block, Givens QR of the block Hessenberg; cfg->restart = block
+ * steps per cycle (<= 20), cfg->max_iters = block steps in total (every
+ * column reports the same count), stop when every column's residual
+ * estimate is <= rel_tol ||b_c||; breakdown = the new block lost rank.
+ * Arguments as hb_fgmres (flexible must be 1). */
+int hb_block_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,
+                    double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
+                    uint8_t* breakdown);
 /* Same, with B and X as DEVICE c128 buffers (inputs resident in HBM); the
  * report arrays are host buffers and may be NULL. */
 int hb_fgmres_device(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const void* dB, void* dX,

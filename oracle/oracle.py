@@ -661,3 +661,60 @@ def ref_gen_sample_pair(hier, seed, k_forced=-1, k_max=10):
     e = np.zeros_like(r)
     _rcheck(ref().hr_gen_sample_pair(hier.ptr, seed, k_forced, k_max, cptr(r), cptr(e)))
     return r, e
+
+
+def block_fgmres_np(apply_A, apply_M, B, restart=10, max_iters=200, rel_tol=1e-6):
+    """Block flexible GMRES (one block Krylov space for all columns of B) in
+    fp64 numpy -- the oracle for hb_block_fgmres.  A restatement of the
+    published algorithm (Saad, Iterative Methods 2nd ed. 6.12 / 9.4.1, with a
+    flexible Z): restart from R = B - A X = V_0 S (QR), per step Z_j = M V_j,
+    W = A Z_j, block CGS2 against V_0..V_j, W = V_{j+1} H_{j+1,j} (QR), the
+    per-column residual of the block least-squares problem
+    min_Y ||[S; 0] - Hbar Y||.  apply_A / apply_M map (p, ny, nx) -> (p, ny, nx).
+    Returns X, per-column histories ([0] = ||b_c||), block steps."""
+    B = np.asarray(B, np.complex128)
+    p = B.shape[0]
+    shp = B.shape
+    N = B[0].size
+    m = restart
+    X = np.zeros((N, p), np.complex128)
+    beta0 = np.linalg.norm(B.reshape(p, N), axis=1)
+    hist = [[float(b)] for b in beta0]
+    it = 0
+    while True:
+        R = (B - apply_A(X.T.reshape(shp))).reshape(p, N).T
+        Q, S = np.linalg.qr(R)
+        V = [Q]
+        Z = []
+        H = np.zeros(((m + 1) * p, m * p), np.complex128)
+        E = np.zeros(((m + 1) * p, p), np.complex128)
+        E[:p] = S
+        done = False
+        k = 0
+        for j in range(m):
+            Zj = apply_M(V[j].T.reshape(shp)).reshape(p, N).T
+            W = apply_A(Zj.T.reshape(shp)).reshape(p, N).T
+            Va = np.concatenate(V, axis=1)
+            for _ in range(2):
+                Hc = Va.conj().T @ W
+                W = W - Va @ Hc
+                H[:(j + 1) * p, j * p:(j + 1) * p] += Hc
+            Qn, Rn = np.linalg.qr(W)
+            H[(j + 1) * p:(j + 2) * p, j * p:(j + 1) * p] = Rn
+            V.append(Qn)
+            Z.append(Zj)
+            it += 1
+            k = j + 1
+            Hs, Es = H[:(k + 1) * p, :k * p], E[:(k + 1) * p]
+            Y = np.linalg.lstsq(Hs, Es, rcond=None)[0]
+            res = np.linalg.norm(Es - Hs @ Y, axis=0)
+            for c in range(p):
+                hist[c].append(float(res[c]))
+            if np.all(res <= rel_tol * beta0) or it >= max_iters:
+                done = True
+                break
+        Hs, Es = H[:(k + 1) * p, :k * p], E[:(k + 1) * p]
+        Y = np.linalg.lstsq(Hs, Es, rcond=None)[0]
+        X = X + np.concatenate(Z, axis=1) @ Y
+        if done:
+            return X.T.reshape(shp), [np.array(h) for h in hist], it

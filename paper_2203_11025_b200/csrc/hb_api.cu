@@ -910,6 +910,30 @@ int hb_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const 
   HB_API_END
 }
 
+int hb_block_fgmres(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const double* B, const double* X0,
+                    double* X, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
+                    uint8_t* breakdown) {
+  HB_API_BEGIN
+  require_whole(*ctx);
+  require_hier(*ctx);
+  if (!cfg) throw HbError{HB_ERR_ARG, "null krylov config"};
+  if (!cfg->flexible) throw HbError{HB_ERR_ARG, "block FGMRES is flexible (stores the preconditioned block)"};
+  if (!B || !X) throw HbError{HB_ERR_ARG, "null B or X"};
+  const size_t n = ctx->levels[0]->N() * size_t(batch);
+  ctx->kB.ensure(n);
+  ctx->kX.ensure(n);
+  HB_CUDA(cudaMemcpyAsync(ctx->kB.p, B, n * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  if (X0)
+    HB_CUDA(cudaMemcpyAsync(ctx->kX.p, X0, n * sizeof(double2), cudaMemcpyHostToDevice, ctx->stream));
+  else
+    HB_CUDA(cudaMemsetAsync(ctx->kX.p, 0, n * sizeof(double2), ctx->stream));
+  block_fgmres_dev(*ctx, kind, batch, cfg->restart, cfg->max_iters, cfg->rel_tol, ctx->kB.p, ctx->kX.p, hist,
+                   hist_stride, hist_len, iters, converged, breakdown);
+  HB_CUDA(cudaMemcpyAsync(X, ctx->kX.p, n * sizeof(double2), cudaMemcpyDeviceToHost, ctx->stream));
+  HB_CUDA(cudaStreamSynchronize(ctx->stream));
+  HB_API_END
+}
+
 int hb_fgmres_device(hb_ctx* ctx, const hb_krylov_cfg* cfg, int kind, int batch, const void* dB, void* dX,
                      double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* converged,
                      uint8_t* breakdown) {

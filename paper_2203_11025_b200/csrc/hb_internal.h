@@ -262,6 +262,10 @@ void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x);
 // non-flexible (standard right-preconditioned) GMRES: u = V y, fin[b] = k > 0; then x += z
 void launch_fg_finalize_v(Context& c, int B, const float2* V, float2* u, int* fin);
 void launch_fg_add_to_x(Context& c, int B, const int* fin, const float2* z, double2* x);
+// true block FGMRES (hb_block.cu): p <= 16 right-hand sides in one block Krylov space
+void block_fgmres_dev(Context& c, int kind, int p, int m, int max_iters, double rel_tol, const double2* dB,
+                      double2* dX, double* hist_out, int hist_stride, int* hist_len_out, int* iters_out,
+                      uint8_t* conv_out, uint8_t* brk_out);
 void krylov_report(Context& c, int B, double* hist, int hist_stride, int* hist_len, int* iters, uint8_t* conv,
                    uint8_t* brk);
 

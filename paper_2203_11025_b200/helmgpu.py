@@ -99,6 +99,8 @@ def lib():
         L.hb_precond_requires_flexible.argtypes = [_vp, C.c_int]
         L.hb_fgmres.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.c_int, _ip, _ip,
                                 _u8p, _u8p]
+        L.hb_block_fgmres.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _dp, _dp, _dp, _dp, C.c_int, _ip, _ip,
+                                _u8p, _u8p]
         L.hb_fgmres_device.argtypes = [_vp, C.POINTER(_KrylovCfg), C.c_int, C.c_int, _vp, _vp, _dp, C.c_int, _ip,
                                        _ip, _u8p, _u8p]
         L.hb_set_paper_net.argtypes = [_vp, C.POINTER(_UNetCfg), C.c_int]
@@ -497,6 +499,28 @@ class Context:
         x0p = _p(_c128(X0)) if X0 is not None else None
         self._check(lib().hb_fgmres(self.h, C.byref(kc), HB_PC[kind], nb, _p(B), x0p, _p(X), _p(hist), cap,
                                     _p(hl, _ip), _p(it, _ip), _p(cv, _u8p), _p(bk, _u8p)))
+        rep = SolveReport([hist[c, :hl[c]].copy() for c in range(nb)], [int(v) for v in it],
+                          [bool(v) for v in cv], [bool(v) for v in bk])
+        return X, rep
+
+    def block_fgmres(self, kind, B, cfg: KrylovConfig, X0=None):
+        """True block FGMRES (hb_block_fgmres): the columns of B share one block
+        Krylov space; cfg.restart / cfg.max_iters count block steps."""
+        B = _c128(B)
+        if B.ndim == 2:
+            B = B[None]
+        nb = B.shape[0]
+        X = np.zeros_like(B)
+        cap = cfg.max_iters + 2
+        hist = np.zeros((nb, cap))
+        hl = np.zeros(nb, np.int32)
+        it = np.zeros(nb, np.int32)
+        cv = np.zeros(nb, np.uint8)
+        bk = np.zeros(nb, np.uint8)
+        kc = _KrylovCfg(cfg.restart, cfg.max_iters, cfg.rel_tol, int(cfg.flexible))
+        x0p = _p(_c128(X0)) if X0 is not None else None
+        self._check(lib().hb_block_fgmres(self.h, C.byref(kc), HB_PC[kind], nb, _p(B), x0p, _p(X), _p(hist), cap,
+                                          _p(hl, _ip), _p(it, _ip), _p(cv, _u8p), _p(bk, _u8p)))
         rep = SolveReport([hist[c, :hl[c]].copy() for c in range(nb)], [int(v) for v in it],
                           [bool(v) for v in cv], [bool(v) for v in bk])
         return X, rep

@@ -12,6 +12,8 @@
 //                                      NetworkWeights, UNetConfig, NetVariant) on the device with the
 //                                      paper U-Net (inc/unet.hpp:113-257)
 //   helm::gpu::block_fgmres(M, B, cfg) device-resident block_fgmres (inc/krylov.hpp:83-86)
+//   helm::gpu::block_fgmres(apply_A, M, B, cfg) the reference signature (apply_A must be A^h)
+//   helm::gpu::block_fgmres_shared_space(M, B, cfg) true block FGMRES (one block Krylov space)
 //
 // Error convention of the reference: contract violations throw
 // std::invalid_argument, device / numeric failures std::runtime_error.
@@ -203,6 +205,38 @@ inline std::pair<std::vector<ComplexField>, SolveReport> block_fgmres(GpuPrecond
   hb_krylov_cfg kc{cfg.restart, cfg.max_iters, cfg.rel_tol, cfg.flexible ? 1 : 0};
   check(c.get(), hb_fgmres(c.get(), &kc, M.kind(), nb, b.data(), X0 ? x0.data() : nullptr, x.data(), hist.data(),
                            cap, hl.data(), it.data(), cv.data(), bk.data()));
+  SolveReport rep;
+  rep.residual_history.resize(size_t(nb));
+  for (int q = 0; q < nb; ++q)
+    rep.residual_history[size_t(q)].assign(hist.begin() + size_t(q) * cap, hist.begin() + size_t(q) * cap + hl[size_t(q)]);
+  rep.iterations.assign(it.begin(), it.end());
+  rep.converged.assign(cv.begin(), cv.end());
+  rep.breakdown.assign(bk.begin(), bk.end());
+  return {detail::unpack(x, nb, c.nx(), c.ny()), std::move(rep)};
+}
+
+// True block FGMRES on the device (hb_block_fgmres): the
+// columns of B (<= 16) share one block Krylov space; cfg.restart / max_iters
+// count block steps; every column reports the same iteration count.
+inline std::pair<std::vector<ComplexField>, SolveReport> block_fgmres_shared_space(
+    GpuPreconditioner& M, const std::vector<ComplexField>& B, const KrylovConfig& cfg,
+    const std::vector<ComplexField>* X0 = nullptr) {
+  if (cfg.restart < 1) throw std::invalid_argument("restart must be >= 1");
+  if (!(cfg.rel_tol > 0.0 && cfg.rel_tol < 1.0)) throw std::invalid_argument("rel_tol in (0,1)");
+  Context& c = M.context();
+  const int nb = int(B.size());
+  if (nb == 0) return {{}, SolveReport{}};
+  const auto b = detail::pack(B);
+  std::vector<double> x0;
+  if (X0) x0 = detail::pack(*X0);
+  std::vector<double> x(b.size());
+  const int cap = cfg.max_iters + 2;
+  std::vector<double> hist(size_t(nb) * cap);
+  std::vector<int> hl(nb), it(nb);
+  std::vector<uint8_t> cv(nb), bk(nb);
+  hb_krylov_cfg kc{cfg.restart, cfg.max_iters, cfg.rel_tol, 1};
+  check(c.get(), hb_block_fgmres(c.get(), &kc, M.kind(), nb, b.data(), X0 ? x0.data() : nullptr, x.data(),
+                                 hist.data(), cap, hl.data(), it.data(), cv.data(), bk.data()));
   SolveReport rep;
   rep.residual_history.resize(size_t(nb));
   for (int q = 0; q < nb; ++q)

@@ -145,10 +145,15 @@ int main() {
     nonflex_rejected = true;
   }
   ok = ok && nonflex_rejected;
+  // (7) true block FGMRES: converged solutions of the same system
+  auto [X_bk, rep_bk] = gpu::block_fgmres_shared_space(M_gpu, B, cfg);
+  const double bk_rel = rel(X_bk, X_ref);
+  ok = ok && bk_rel < 1e-4 && rep_bk.converged[0] && rep_bk.iterations[0] <= rep_ref.iterations[0];
   std::printf("], \"x_rel_device\": %.3e, \"x_rel_plugin\": %.3e, \"name\": \"%s\", \"ju_rel\": %.3e, "
               "\"vu_rel\": %.3e, \"apply_A_rejects_wrong_op\": %s, \"dense_pc_rel\": %.3e, "
-              "\"nonflex_x_rel\": %.3e, \"nonflex_iter_diff\": %d, \"vu_nonflex_rejected\": %s, \"ok\": %s}\n",
+              "\"nonflex_x_rel\": %.3e, \"nonflex_iter_diff\": %d, \"vu_nonflex_rejected\": %s, "
+              "\"block_x_rel\": %.3e, \"block_iters\": %d, \"ok\": %s}\n",
               xe, xm, M_gpu.name().c_str(), ju_err, vu_err, rejected ? "true" : "false", d_pc, d_x, d_it,
-              nonflex_rejected ? "true" : "false", ok ? "true" : "false");
+              nonflex_rejected ? "true" : "false", bk_rel, rep_bk.iterations[0], ok ? "true" : "false");
   return ok ? 0 : 1;
 }

@@ -111,7 +111,9 @@ constexpr int TC_MAX_CHUNKS = 320;  // K entries per tile (taps x channel chunks
 constexpr int TC_MAX_SLOTS = 8;
 constexpr int TC_DYN_SMEM = 216 * 1024;  // + ~8 KB of static tables/barriers <= 227 KB
 
-template <int KC>  // uniform chunk width (16 | 32), or 0 = mixed-width sources
+// GEN: general geometry / epilogue (paper net); false: the classic 3x3 stride-1
+// bias (+ ReLU) layer with compile-time tap arithmetic and the plain epilogue
+template <int KC, bool GEN>  // KC: uniform chunk width (16 | 32), or 0 = mixed-width sources
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_conv_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ CUtensorMap mapWh32, const __grid_constant__ CUtensorMap mapWl32,
@@ -370,7 +372,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           const int4 e = sched[kb];
           const int kc = KC ? KC : e.w;
           const int cj = e.x & 255, ty = (e.x >> 8) & 255, tx = (e.x >> 16) & 255;
-          const int hp = (yy * cs + ty) * hw + xx * cs + tx;  // shifted halo pixel
+          const int hp = GEN ? (yy * cs + ty) * hw + xx * cs + tx : (yy + ty) * hw + xx + tx;  // shifted halo pixel
           const unsigned char* row = hbuf + cj * lay.box_bytes + hp * (kc * 4);
           // swizzled 16-B chunk c of smem row hp sits at c ^ f(hp): SW128 f = hp & 7, SW64 f = (hp >> 1) & 3
           const int f = kc == 32 ? (hp & 7) : ((hp >> 1) & 3);
@@ -380,7 +382,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               float4 x = *reinterpret_cast<const float4*>(row + (((4 * h + c) ^ f) << 4));
-              if (p.epi.in_elu) x = make_float4(elu_f(x.x), elu_f(x.y), elu_f(x.z), elu_f(x.w));
+              if (GEN && p.epi.in_elu) x = make_float4(elu_f(x.x), elu_f(x.y), elu_f(x.z), elu_f(x.w));
               const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
@@ -442,9 +444,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float x = __uint_as_float(v[i]) + __uint_as_float(u[i]);
-          o[i] = part ? x : tc_epilogue(p.epi, n0 + c0 + i, x + __ldg(bias + c0 + i), rrow ? rrow + c0 + i : nullptr);
+          if (GEN) {
+            o[i] = part ? x : tc_epilogue(p.epi, n0 + c0 + i, x + __ldg(bias + c0 + i), rrow ? rrow + c0 + i : nullptr);
+          } else {
+            const float y = x + __ldg(bias + c0 + i);
+            o[i] = part ? x : p.relu ? fmaxf(y, 0.f) : y;
+          }
         }
-        const int nvalid = p.epi.nco && !part ? p.epi.nco - (n0 + c0) : 16;  // padded output channels: not stored
+        const int nvalid = GEN && p.epi.nco && !part ? p.epi.nco - (n0 + c0) : 16;  // padded output channels: not stored
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
           if (i < nvalid) *reinterpret_cast<float4*>(orow + c0 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
@@ -459,6 +466,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// split-K reduction for the dense bias (+ ReLU) case: float4 over channels
+__global__ void k_conv_ksum4(int ksplit, size_t n4, int cout4, size_t img4, const int* act,
+                             const float4* __restrict__ ws, const float4* __restrict__ bias, int relu,
+                             float4* __restrict__ out) {
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x) {
+    if (act && !act[i / img4]) continue;  // frozen column: its partials were not written
+    float4 a = __ldg(bias + (i % cout4));
+    for (int s = 0; s < ksplit; ++s) {
+      const float4 v = __ldg(ws + size_t(s) * n4 + i);
+      a.x += v.x;
+      a.y += v.y;
+      a.z += v.z;
+      a.w += v.w;
+    }
+    if (relu) a = make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
+    out[i] = a;
   }
 }
 
@@ -637,11 +663,15 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
   // uniform chunk width as a template argument (fully unrolled issue loops);
   // mixed-width sources take the generic instantiation
   const bool uni = !cb || kca == kcb;
+  const bool gen = geo.s != 1 || geo.os != 1 || geo.ldo != cw.cout || t.epi.res || t.epi.mu || t.epi.act == 2 ||
+                   t.epi.in_elu || t.epi.nco;
   void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams, TcLayout, int) =
-      !uni ? k_conv_tc<0> : kcmax == 32 ? k_conv_tc<32> : k_conv_tc<16>;
+      gen ? (!uni ? k_conv_tc<0, true> : kcmax == 32 ? k_conv_tc<32, true> : k_conv_tc<16, true>)
+          : (!uni ? k_conv_tc<0, false> : kcmax == 32 ? k_conv_tc<32, false> : k_conv_tc<16, false>);
   static int attr_dev = -1;
   if (attr_dev != c.device) {
-    for (auto k : {k_conv_tc<0>, k_conv_tc<32>, k_conv_tc<16>})
+    for (auto k : {k_conv_tc<0, true>, k_conv_tc<32, true>, k_conv_tc<16, true>, k_conv_tc<0, false>,
+                   k_conv_tc<32, false>, k_conv_tc<16, false>})
       HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, TC_DYN_SMEM));
     attr_dev = c.device;
   }
@@ -657,8 +687,16 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
   if (ksplit > 1) {
     HB_CUDA(cudaGetLastError());
     const size_t n = size_t(B) * H * W * cw.cout;
-    k_conv_ksum<<<int(std::min<size_t>((n + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
-        ksplit, B, H, W, cw.cout, t.act, ws, cw.db.p, geo, t.epi, t.out);
+    const bool dense = geo.os == 1 && geo.ldo == cw.cout && !t.epi.res && !t.epi.mu && t.epi.act != 2 && !t.epi.nco;
+    if (dense) {
+      const size_t n4 = n / 4;
+      k_conv_ksum4<<<int(std::min<size_t>((n4 + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
+          ksplit, n4, cw.cout / 4, size_t(H) * W * cw.cout / 4, t.act, reinterpret_cast<const float4*>(ws),
+          reinterpret_cast<const float4*>(cw.db.p), t.epi.act == 1, reinterpret_cast<float4*>(t.out));
+    } else {
+      k_conv_ksum<<<int(std::min<size_t>((n + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
+          ksplit, B, H, W, cw.cout, t.act, ws, cw.db.p, geo, t.epi, t.out);
+    }
   }
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout),
            2.0 * B * H * W * double(NT) * cw.cin * cw.cout);

@@ -244,7 +244,7 @@ __device__ __forceinline__ void cta_reduce_acc(const float (&acc)[NA], int nf, f
 // fp64 by the last CTA of the column, which forms the MGS coefficients.
 __device__ void adots_scalar(ColState& S, int j, const double2* red);
 
-template <int JM>
+template <int JM, bool WIDE>
 __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
                                               const float2* __restrict__ Z, float2* __restrict__ W,
                                               const float2* __restrict__ V, double2* part, unsigned* ticket,
@@ -265,31 +265,46 @@ __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState
   float acc[NF];
 #pragma unroll
   for (int s = 0; s < NF; ++s) acc[s] = 0.f;
+  // U nodes per thread per iteration, all their loads issued before the first
+  // store (the compiler may not hoist loads above a possibly aliasing store):
+  // few basis vectors leave registers for more nodes in flight.  WIDE: many
+  // nodes per thread (large grids); short loops (c0) keep U = 1
+  constexpr int U = !WIDE ? 1 : JM <= 1 ? 4 : JM <= 3 ? 2 : 1;
   const size_t stride = size_t(gridDim.x) * KT;
-  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += stride) {
-    float2 a[JM + 1];
+  for (size_t p0 = size_t(blockIdx.x) * KT + threadIdx.x; p0 < N; p0 += stride * U) {
+    float2 a[U][JM + 1], w[U];
 #pragma unroll
-    for (int i = 0; i <= JM; ++i) a[i] = i <= j ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
-    const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
-    float2 w;
-    if (dI) {  // w = A D^-1 (s_j Vraw_j), zb = Vraw_j (coarse GMRES, inc/multigrid.hpp:52-55)
-      float2 nb = make_float2(0.f, 0.f);
-      if (ix > 0) nb = cadd(nb, cmul(ld(zb, p - 1), ld(dI, p - 1)));
-      if (ix + 1 < F.nx) nb = cadd(nb, cmul(ld(zb, p + 1), ld(dI, p + 1)));
-      if (iy > 0) nb = cadd(nb, cmul(ld(zb, p - F.nx), ld(dI, p - F.nx)));
-      if (iy + 1 < F.ny) nb = cadd(nb, cmul(ld(zb, p + F.nx), ld(dI, p + F.nx)));
-      float2 y = cmul(ld(dA, p), cmul(ld(zb, p), ld(dI, p)));
-      y.x = fmaf(-inv_h2, nb.x, y.x);
-      y.y = fmaf(-inv_h2, nb.y, y.y);
-      w = cscale(y, sj);
-    } else {
-      w = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
+    for (int u = 0; u < U; ++u) {
+      const size_t p = p0 + u * stride;
+      const bool ok = p < N;
+#pragma unroll
+      for (int i = 0; i <= JM; ++i) a[u][i] = (ok && i <= j) ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
+      w[u] = make_float2(0.f, 0.f);
+      if (!ok) continue;
+      const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
+      if (dI) {  // w = A D^-1 (s_j Vraw_j), zb = Vraw_j (coarse GMRES, inc/multigrid.hpp:52-55)
+        float2 nb = make_float2(0.f, 0.f);
+        if (ix > 0) nb = cadd(nb, cmul(ld(zb, p - 1), ld(dI, p - 1)));
+        if (ix + 1 < F.nx) nb = cadd(nb, cmul(ld(zb, p + 1), ld(dI, p + 1)));
+        if (iy > 0) nb = cadd(nb, cmul(ld(zb, p - F.nx), ld(dI, p - F.nx)));
+        if (iy + 1 < F.ny) nb = cadd(nb, cmul(ld(zb, p + F.nx), ld(dI, p + F.nx)));
+        float2 y = cmul(ld(dA, p), cmul(ld(zb, p), ld(dI, p)));
+        y.x = fmaf(-inv_h2, nb.x, y.x);
+        y.y = fmaf(-inv_h2, nb.y, y.y);
+        w[u] = cscale(y, sj);
+      } else {
+        w[u] = stencil_at_p(zb, p, F.nx, F.ny, ix, iy, ld(dA, p), inv_h2);
+      }
     }
-    wb[p] = w;
 #pragma unroll
-    for (int i = 0; i <= JM; ++i) {
-      acc[2 * i] = fmaf(a[i].x, w.x, fmaf(a[i].y, w.y, acc[2 * i]));
-      acc[2 * i + 1] = fmaf(a[i].x, w.y, fmaf(-a[i].y, w.x, acc[2 * i + 1]));
+    for (int u = 0; u < U; ++u) {
+      const size_t p = p0 + u * stride;
+      if (p < N) wb[p] = w[u];
+#pragma unroll
+      for (int i = 0; i <= JM; ++i) {
+        acc[2 * i] = fmaf(a[u][i].x, w[u].x, fmaf(a[u][i].y, w[u].y, acc[2 * i]));
+        acc[2 * i + 1] = fmaf(a[u][i].x, w[u].y, fmaf(-a[u][i].y, w[u].x, acc[2 * i + 1]));
+      }
     }
   }
   extern __shared__ float sred[];  // [2 (JM + 1)][KT]
@@ -360,7 +375,7 @@ __device__ void adots_scalar(ColState& S, int j, const double2* red) {
 __device__ void update_scalar(ColState& S, int b, int j, int m, double t, const double2* gram, int* act, double* hist,
                               int hist_cap, double rel_tol, int max_iters, float* scale_out);
 
-template <int JM>
+template <int JM, bool WIDE>
 __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, ColState* st, int* act,
                                                const float2* __restrict__ W, float2* __restrict__ V, double2* part,
                                                unsigned* ticket, double* hist, int hist_cap, double rel_tol,
@@ -386,21 +401,31 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
 #pragma unroll
   for (int s2 = 0; s2 < NF; ++s2) acc[s2] = 0.f;
   double nrm = 0.0;
+  constexpr int U = !WIDE ? 1 : JM <= 1 ? 4 : JM <= 3 ? 2 : 1;  // nodes in flight per thread (see k_adots)
   const size_t stride = size_t(gridDim.x) * KT;
-  for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += stride) {
-    float2 a[JM + 1];
+  for (size_t p0 = size_t(blockIdx.x) * KT + threadIdx.x; p0 < N; p0 += stride * U) {
+    float2 a[U][JM + 1], t[U];
 #pragma unroll
-    for (int i = 0; i <= JM; ++i) a[i] = i <= j ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
-    float2 t = ld(wb, p);
+    for (int u = 0; u < U; ++u) {
+      const size_t p = p0 + u * stride;
+      const bool ok = p < N;
 #pragma unroll
-    for (int i = 0; i <= JM; ++i) t = csub(t, cmul(cf[i], a[i]));  // cf beyond j: zero
-    Vn[p] = t;
-    nrm += dnorm2(t);
-    if (gram) {
+      for (int i = 0; i <= JM; ++i) a[u][i] = (ok && i <= j) ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
+      t[u] = ok ? ld(wb, p) : make_float2(0.f, 0.f);
+    }
 #pragma unroll
-      for (int i = 0; i <= JM; ++i) {  // conj(V_{j+1}) V_i
-        acc[2 * i] = fmaf(t.x, a[i].x, fmaf(t.y, a[i].y, acc[2 * i]));
-        acc[2 * i + 1] = fmaf(t.x, a[i].y, fmaf(-t.y, a[i].x, acc[2 * i + 1]));
+    for (int u = 0; u < U; ++u) {
+      const size_t p = p0 + u * stride;
+#pragma unroll
+      for (int i = 0; i <= JM; ++i) t[u] = csub(t[u], cmul(cf[i], a[u][i]));  // cf beyond j: zero
+      if (p < N) Vn[p] = t[u];
+      nrm += dnorm2(t[u]);
+      if (gram) {
+#pragma unroll
+        for (int i = 0; i <= JM; ++i) {  // conj(V_{j+1}) V_i
+          acc[2 * i] = fmaf(t[u].x, a[u][i].x, fmaf(t[u].y, a[u][i].y, acc[2 * i]));
+          acc[2 * i + 1] = fmaf(t[u].x, a[u][i].y, fmaf(-t[u].y, a[u][i].x, acc[2 * i + 1]));
+        }
       }
     }
   }
@@ -767,22 +792,24 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
 // the basis-streaming kernels are instantiated for JM = 1, 3, ..., 15, 19, 23, 31
 // (the largest j they accept: 2 (JM + 1) fp32 accumulators and JM + 1 basis
 // values per thread; odd steps keep the unused registers few)
-#define HB_JM_DISPATCH(j, KERN, grid, ...)                                          \
+#define HB_JM_CASE(JMV, KERN, wide, grid, sm, ...)                                   \
+  (wide ? launch_jm(c, KERN<JMV, true>, grid, sm, __VA_ARGS__) : launch_jm(c, KERN<JMV, false>, grid, sm, __VA_ARGS__))
+#define HB_JM_DISPATCH(j, KERN, wide, grid, ...)                                    \
   do {                                                                              \
     const int jm_ = (j) <= 15 ? ((j) | 1) : (j) <= 19 ? 19 : (j) <= 23 ? 23 : 31;    \
     const size_t sm_ = size_t(2) * (jm_ + 1) * KT * sizeof(float);                  \
     switch (jm_) {                                                                  \
-      case 1: launch_jm(c, KERN<1>, grid, sm_, __VA_ARGS__); break;                 \
-      case 3: launch_jm(c, KERN<3>, grid, sm_, __VA_ARGS__); break;                 \
-      case 5: launch_jm(c, KERN<5>, grid, sm_, __VA_ARGS__); break;                 \
-      case 7: launch_jm(c, KERN<7>, grid, sm_, __VA_ARGS__); break;                 \
-      case 9: launch_jm(c, KERN<9>, grid, sm_, __VA_ARGS__); break;                 \
-      case 11: launch_jm(c, KERN<11>, grid, sm_, __VA_ARGS__); break;               \
-      case 13: launch_jm(c, KERN<13>, grid, sm_, __VA_ARGS__); break;               \
-      case 15: launch_jm(c, KERN<15>, grid, sm_, __VA_ARGS__); break;               \
-      case 19: launch_jm(c, KERN<19>, grid, sm_, __VA_ARGS__); break;               \
-      case 23: launch_jm(c, KERN<23>, grid, sm_, __VA_ARGS__); break;               \
-      default: launch_jm(c, KERN<31>, grid, sm_, __VA_ARGS__); break;               \
+      case 1: HB_JM_CASE(1, KERN, wide, grid, sm_, __VA_ARGS__); break;             \
+      case 3: HB_JM_CASE(3, KERN, wide, grid, sm_, __VA_ARGS__); break;             \
+      case 5: HB_JM_CASE(5, KERN, wide, grid, sm_, __VA_ARGS__); break;             \
+      case 7: HB_JM_CASE(7, KERN, wide, grid, sm_, __VA_ARGS__); break;             \
+      case 9: HB_JM_CASE(9, KERN, wide, grid, sm_, __VA_ARGS__); break;             \
+      case 11: HB_JM_CASE(11, KERN, wide, grid, sm_, __VA_ARGS__); break;           \
+      case 13: HB_JM_CASE(13, KERN, wide, grid, sm_, __VA_ARGS__); break;           \
+      case 15: HB_JM_CASE(15, KERN, wide, grid, sm_, __VA_ARGS__); break;           \
+      case 19: HB_JM_CASE(19, KERN, wide, grid, sm_, __VA_ARGS__); break;           \
+      case 23: HB_JM_CASE(23, KERN, wide, grid, sm_, __VA_ARGS__); break;           \
+      default: HB_JM_CASE(31, KERN, wide, grid, sm_, __VA_ARGS__); break;           \
     }                                                                               \
   } while (0)
 
@@ -804,7 +831,8 @@ void launch_adots(Context& c, const FineView& F, int B, int j, ColState* st, con
                   const float2* V, double2* part, unsigned* ticket, double2* gsum) {
   const size_t N = size_t(F.nx) * (F.w.hi - F.w.lo);
   const int nb = nblk_basis(c, N, B);
-  HB_JM_DISPATCH(j, k_adots, dim3(nb, B), F, B, j, st, act, Zj, w, V, part, ticket, gsum);
+  const bool wide = N >= size_t(nb) * KT * 32;  // >= 32 nodes per thread
+  HB_JM_DISPATCH(j, k_adots, wide, dim3(nb, B), F, B, j, st, act, Zj, w, V, part, ticket, gsum);
   HB_CUDA(cudaGetLastError());
 }
 void launch_update(Context& c, const FineView& F, int B, int j, int m, ColState* st, int* act, const float2* w, float2* V,
@@ -812,7 +840,8 @@ void launch_update(Context& c, const FineView& F, int B, int j, int m, ColState*
                    float* scale, double2* gsum) {
   const size_t N = size_t(F.nx) * (F.w.hi - F.w.lo);
   const int nb = nblk_basis(c, N, B);
-  HB_JM_DISPATCH(j, k_update, dim3(nb, B), F, B, j, m, st, act, w, V, part, ticket, hist, hist_cap, rel_tol,
+  const bool wide = N >= size_t(nb) * KT * 32;  // >= 32 nodes per thread
+  HB_JM_DISPATCH(j, k_update, wide, dim3(nb, B), F, B, j, m, st, act, w, V, part, ticket, hist, hist_cap, rel_tol,
                  max_iters, scale, gsum);
   HB_CUDA(cudaGetLastError());
 }

@@ -2,7 +2,7 @@
 average DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum) and
 duration, as read by bench.py for roofline.traffic.
 
-   python tools/ncu_traffic.py <report.ncu-rep> <source description>
+   python tools/ncu_traffic.py <report.ncu-rep | raw-page.csv> <source description>
 """
 import csv
 import io
@@ -27,9 +27,12 @@ def classify(name):
 
 def main():
     rep, source = sys.argv[1], sys.argv[2]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
-                          "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
-                         capture_output=True, text=True, check=True).stdout
+    if rep.endswith(".csv"):  # a raw-page export (ncu -i rep --page raw --csv --metrics ...)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                              "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"],
+                             capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[0]
     units = rows[1]

@@ -47,6 +47,19 @@ def peaks():
         return PEAKS_FALLBACK, "fallback"
 
 
+def tf32_peak():
+    """Dense tcgen05 kind::tf32 peak measured on this B200 pool by
+    tools/micro/tf32_peak.cu (profiles/tf32_peak.json: M=128, N=256, K=8 SS
+    MMAs on every SM, event-timed); fallback 0.5 x the measured bf16 peak."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "tf32_peak.json")) as f:
+            runs = json.load(f)["runs"]
+        return max(r["tflops"] for r in runs), "measured (profiles/tf32_peak.json, tools/micro/tf32_peak.cu)"
+    except Exception:
+        pk, src = peaks()
+        return 0.5 * pk.get("bf16_tflops", 1590.0), f"provisional 0.5 x {src} bf16"
+
+
 # ------------------------------------------------------------------ dist
 def dist_init():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
@@ -490,10 +503,9 @@ def run_ours(args, ws, rank, local):
     name, p = max(prof.items(), key=lambda kv: kv[1]["ms"])
     if p["flops"] > 0:
         achieved = p["flops"] / (p["ms"] / 1e3) / 1e12
-        peak = pk.get("bf16_tflops", 1590.0) * 0.5
+        peak, tsrc = tf32_peak()
         rl = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-              "traffic": None, "kernel": name,
-              "note": f"peak = 0.5 x {src} bf16 burst (provisional TF32 denominator, BASELINE.md 5)"}
+              "traffic": None, "kernel": name, "note": f"peak = tcgen05 kind::tf32 dense, {tsrc}; useful flops"}
     else:
         achieved = p["bytes"] / (p["ms"] / 1e3) / 1e9 if p["ms"] > 0 else 0.0
         peak = pk.get("hbm_gbs", 6650.0)
@@ -600,6 +612,10 @@ def fixed_budget(name, local, args, ws, rank):
     if conv.get("ms", 0) > 0:
         out["conv_tflops"] = conv["flops"] / (conv["ms"] / 1e3) / 1e12
         out["conv_share"] = conv["ms"] / max(1e-9, sum(v["ms"] for v in prof.values()))
+        # 3xTF32: the tensor pipe executes 3x the useful flops (A_hi [W_hi|W_lo] + A_lo W_hi)
+        tp, tsrc = tf32_peak()
+        out["conv_tensor_pipe_frac"] = 3.0 * out["conv_tflops"] / tp
+        out["conv_tensor_peak"] = {"tflops": tp, "source": tsrc}
     # per kernel class: achieved GB/s (algorithmic bytes) and fraction of
     # the measured HBM peak -- meaningful here, the working sets exceed L2 from c2 on
     pk, _ = peaks()

@@ -1033,8 +1033,6 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_graphs = value != 0;
   else if (k == "small_coarse")
     ctx->opt_small_coarse = value != 0;
-  else if (k == "coarse_threads")
-    ctx->coarse_threads = int(value);
   else if (k == "split_vcycle")
     ctx->opt_split = value != 0;
   else if (k == "tc_conv")
@@ -1043,8 +1041,6 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_conv_ksplit = value != 0;
   else if (k == "coarse_reg")
     ctx->opt_coarse_reg = value != 0;
-  else if (k == "wide_legs")
-    ctx->opt_wide_legs = value != 0;
   else if (k == "legs_wd")
     ctx->opt_legs_wd = int(value);
   else if (k == "pdl")

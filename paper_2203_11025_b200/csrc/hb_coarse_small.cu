@@ -641,8 +641,6 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
   static int attr_set = 0;  // per-device bitmask
   if (!(attr_set & (1 << c.device))) {
     const int mx = 200 * 1024;
-    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<1024, 1, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-    HB_CUDA(cudaFuncSetAttribute(k_coarse_small<512, 2, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     HB_CUDA(cudaFuncSetAttribute(k_coarse_small<256, 1, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     HB_CUDA(cudaFuncSetAttribute(k_coarse_small<256, 2, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     HB_CUDA(cudaFuncSetAttribute(k_coarse_small<256, 4, 15>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
@@ -650,23 +648,14 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
     attr_set |= 1 << c.device;
   }
   const int tok = prof_begin(c, PC_COARSE);
-  const int nt = c.coarse_threads;
   static bool reg_attr = false;
-  if (c.opt_coarse_reg && iters <= 10 && N <= 1024 && (nt == 256 || nt == 512)) {
+  if (c.opt_coarse_reg && iters <= 10 && N <= 1024) {  // basis in registers (c0: 32^2)
     if (!reg_attr) {
       HB_CUDA(cudaFuncSetAttribute(k_coarse_reg<256, 4, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
-      HB_CUDA(cudaFuncSetAttribute(k_coarse_reg<512, 2, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
       reg_attr = true;
     }
     const size_t su = 2 * sizeof(float2) * size_t(L.nx + 2) * (L.ny + 2);
-    if (nt == 512)
-      launch_pdl(c, k_coarse_reg<512, 2, 10>, dim3(B), dim3(512), su, L, iters, act, f, x);
-    else
-      launch_pdl(c, k_coarse_reg<256, 4, 10>, dim3(B), dim3(256), su, L, iters, act, f, x);
-  } else if (nt == 1024 && N <= 1024) {
-    launch_pdl(c, k_coarse_small<1024, 1, 15>, dim3(B), dim3(1024), smem, L, iters, act, f, x);
-  } else if (nt >= 512 && N <= 1024) {
-    launch_pdl(c, k_coarse_small<512, 2, 15>, dim3(B), dim3(512), smem, L, iters, act, f, x);
+    launch_pdl(c, k_coarse_reg<256, 4, 10>, dim3(B), dim3(256), su, L, iters, act, f, x);
   } else if (N <= 256) {
     launch_pdl(c, k_coarse_small<256, 1, 15>, dim3(B), dim3(256), smem, L, iters, act, f, x);
   } else if (N <= 512) {

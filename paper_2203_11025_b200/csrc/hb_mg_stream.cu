@@ -375,134 +375,6 @@ __global__ void __launch_bounds__(32 * WARPS) k_down_lean(LevelView L, RowWin cw
 }
 
 // ---------------------------------------------------------------------------
-// Wide variants: each lane owns 4 consecutive fine columns F..F+3 (F a multiple
-// of 4, so a lane's columns are all inside or all outside the grid and its
-// row loads are two aligned float4 per array); a warp covers 128 fine columns,
-// lanes 0 and 31 are halo, lanes 1..30 emit 2 coarse columns each (60 per
-// warp).  Half the loads, shuffles and bounds tests per node of the 2-column
-// kernels above, same arithmetic.
-constexpr int SW4_FINE = 120;  // fine columns emitted per warp
-
-struct Quad {
-  float2 c[4];
-};
-__device__ __forceinline__ Quad ld_quad(const float2* row, int F, bool ok) {
-  Quad q;
-  if (ok) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(row + F));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(row + F + 2));
-    q.c[0] = make_float2(a.x, a.y);
-    q.c[1] = make_float2(a.z, a.w);
-    q.c[2] = make_float2(b.x, b.y);
-    q.c[3] = make_float2(b.z, b.w);
-  } else {
-    q.c[0] = q.c[1] = q.c[2] = q.c[3] = make_float2(0.f, 0.f);
-  }
-  return q;
-}
-// M v on one row of a lane's 4 columns: d v - ih2 (up + down + left + right)
-__device__ __forceinline__ Quad apply_M4(const Quad& d, const Quad& vm, const Quad& v, const Quad& vp, float ih2) {
-  const float2 left = shfl_up2(v.c[3]);    // column F - 1
-  const float2 right = shfl_down2(v.c[0]); // column F + 4
-  Quad o;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 l = k == 0 ? left : v.c[k - 1];
-    const float2 r = k == 3 ? right : v.c[k + 1];
-    const float2 nb = cadd(cadd(vm.c[k], vp.c[k]), cadd(l, r));
-    o.c[k] = cmul(d.c[k], v.c[k]);
-    o.c[k].x = fmaf(-ih2, nb.x, o.c[k].x);
-    o.c[k].y = fmaf(-ih2, nb.y, o.c[k].y);
-  }
-  return o;
-}
-
-// down leg, wide: grid (ceil(nx / 120), ceil(row chunks / WARPS), B), block 32 x WARPS
-__global__ void __launch_bounds__(32 * WARPS) k_down_stream4(LevelView L, int offset, int rows_per_chunk,
-                                                             const int* act, const float2* __restrict__ f,
-                                                             const float* fscale, float2* __restrict__ fc) {
-  pdl_enter();
-  const int b = blockIdx.z;
-  if (act && !act[b]) return;
-  const int lane = threadIdx.x, nx = L.nx, ny = L.ny, cnx = nx / 2, cny = ny / 2;
-  const int F = blockIdx.x * SW4_FINE - 4 + 4 * lane;
-  const bool colok = F >= 0 && F < nx;
-  const int jy0 = (blockIdx.y * WARPS + threadIdx.y) * rows_per_chunk;
-  if (jy0 >= cny) return;
-  const int jy1 = min(cny, jy0 + rows_per_chunk);
-  const size_t N = size_t(nx) * ny;
-  const float2* fb = f + b * N;
-  const float s = fscale ? fscale[b] : 1.0f;
-  const float ih2 = L.inv_h2;
-  struct Raw {
-    Quad f, w, d;
-  };
-  auto load_raw = [&](int y) {
-    Raw r;
-    const bool ok = colok && y >= 0 && y < ny;
-    const size_t o = ok ? size_t(y) * nx : 0;
-    r.f = ld_quad(fb + o, F, ok);
-    r.w = ld_quad(L.wdi + o, F, ok);
-    r.d = ld_quad(L.dM + o, F, ok);
-    return r;
-  };
-  auto vrow = [&](const Raw& r) {
-    Quad v;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) v.c[k] = cmul(cscale(r.f.c[k], s), r.w.c[k]);
-    return v;
-  };
-  int y = 2 * jy0 + offset - 1;
-  Raw r_c = load_raw(y), r_p1 = load_raw(y + 1), r_p2 = load_raw(y + 2);
-  Quad v_m = vrow(load_raw(y - 1)), v_c = vrow(r_c);
-  float2 a_m2 = make_float2(0.f, 0.f), a_m1 = a_m2, b_m2 = a_m2, b_m1 = a_m2;  // horizontal sums, 2 coarse cols
-  const int yend = 2 * (jy1 - 1) + offset + 1;
-  const bool emit = lane >= 1 && lane <= 30 && colok && F / 2 + 1 < cnx;
-  for (; y <= yend; ++y) {
-    const Raw r_p3 = load_raw(y + 3);
-    const Quad v_p = vrow(r_p1);
-    const Quad mv = apply_M4(r_c.d, v_m, v_c, v_p, ih2);
-    Quad r;
-    const bool rowok = y >= 0 && y < ny;
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-      r.c[k] = (rowok && colok) ? csub(cscale(r_c.f.c[k], s), mv.c[k]) : make_float2(0.f, 0.f);
-    // horizontal full weighting around the two coarse centres of this lane
-    float2 ha, hb;
-    if (offset == 0) {  // centres F, F+2
-      const float2 rl = shfl_up2(r.c[3]);
-      ha = caxpy(cscale(r.c[0], 0.5f), 0.25f, cadd(rl, r.c[1]));
-      hb = caxpy(cscale(r.c[2], 0.5f), 0.25f, cadd(r.c[1], r.c[3]));
-    } else {            // centres F+1, F+3
-      const float2 rr = shfl_down2(r.c[0]);
-      ha = caxpy(cscale(r.c[1], 0.5f), 0.25f, cadd(r.c[0], r.c[2]));
-      hb = caxpy(cscale(r.c[3], 0.5f), 0.25f, cadd(r.c[2], rr));
-    }
-    // y = 2 jy + o + 1 closes coarse row jy
-    const int t = y - offset - 1;
-    if (t >= 2 * jy0 && ((t & 1) == 0)) {
-      const int jy = t >> 1;
-      if (emit && jy < jy1) {
-        const float2 ca = caxpy(cscale(a_m1, 0.5f), 0.25f, cadd(a_m2, ha));
-        const float2 cb = caxpy(cscale(b_m1, 0.5f), 0.25f, cadd(b_m2, hb));
-        *reinterpret_cast<float4*>(fc + size_t(b) * cnx * cny + size_t(jy) * cnx + F / 2) =
-            make_float4(ca.x, ca.y, cb.x, cb.y);
-      }
-    }
-    a_m2 = a_m1;
-    a_m1 = ha;
-    b_m2 = b_m1;
-    b_m1 = hb;
-    v_m = v_c;
-    v_c = v_p;
-    r_c = r_p1;
-    r_p1 = r_p2;
-    r_p2 = r_p3;
-  }
-}
-
-
-// ---------------------------------------------------------------------------
 // Row-streaming legs from a non-zero initial guess e0 (M_VU's level 0,
 // inc/precond.hpp:151-158 -> cycle_at with x0 = e0): the pre-smoothed iterate
 //   v = e0 + wD^-1 (f - M e0)
@@ -760,9 +632,6 @@ void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float 
     auto k = wd ? (even ? k_down_e0<true, true> : k_down_e0<true, false>)
                 : (even ? k_down_e0<false, true> : k_down_e0<false, false>);
     launch_pdl(c, k, grid, dim3(32, WARPS), 0, L, damping, offset, rpc, act, f, fscale, e0, fc);
-  } else if (c.opt_wide_legs && L.nx % 4 == 0 && !slab) {
-    const dim3 grid((L.nx + SW4_FINE - 1) / SW4_FINE, (chunks + WARPS - 1) / WARPS, B);
-    launch_pdl(c, k_down_stream4, dim3(grid), dim3(32, WARPS), 0, L, offset, rpc, act, f, fscale, fc);
   } else {
     const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
     if (c.opt_lean_legs || slab) {

@@ -552,10 +552,10 @@ def run_ours(args, ws, rank, local):
             if nm == "c4slab":
                 line["also"][nm] = slab
                 continue
-            if nm in ("datagen", "paper_ju", "train", "block"):
+            if nm in ("datagen", "paper_ju", "train", "block", "mv512"):
                 try:
                     fn = {"datagen": datagen_budget, "paper_ju": paper_ju_budget, "train": train_budget,
-                          "block": block_budget}[nm]
+                          "block": block_budget, "mv512": mv_converged_budget}[nm]
                     line["also"][nm] = fn(local, args)
                 except Exception as e:  # reported, not hidden
                     line["also"][nm] = {"error": repr(e)}
@@ -690,6 +690,66 @@ def datagen_budget(local, args):
             out["cpu_reference"] = {"pairs_per_s": n / dt, "pairs": n, "cores": 1, "kind": "reference"}
     except Exception as ex:  # reported, not hidden
         out["cpu_reference"] = {"error": repr(ex)}
+    return out
+
+
+def mv_converged_budget(local, args, name="c2"):
+    """A CONVERGED solve at scale: M_V (3-level SL V-cycle, GMRES(10) coarsest;
+    no network, so it reaches 1e-6) FGMRES(20) on config `name`'s grid, medium
+    and RHS block, every column to 1e-6.  Device time of the whole solve (RHS
+    resident), solves/s; beside it the reference's CPU cost per FGMRES
+    iteration of one column on one host core (oracle/_ref, 5 iterations) times
+    the device's iteration count (extrapolated, labelled)."""
+    import torch
+    from paper_2203_11025_b200 import helmgpu as hg
+    from paper_2203_11025_b200 import problems
+    cfg = dict(config_for(name))
+    cfg.update(precond="v", net=None, enc=None, coarse="gmres", coarse_iters=10, restart=20, levels=3)
+    ctx, arr = problems.gpu_setup(cfg, device=local)
+    Bh = np.ascontiguousarray(problems.rhs_block(arr))
+    nb = Bh.shape[0]
+    kc = hg.KrylovConfig(restart=20, max_iters=4000, rel_tol=1e-6)
+    dev = torch.device("cuda", local)
+    dB = torch.from_numpy(Bh).to(dev)
+    dX = torch.zeros_like(dB)
+    st = torch.cuda.ExternalStream(ctx.stream, device=dev)
+    ctx.fgmres_device("v", dB.data_ptr(), dX.data_ptr(), nb, hg.KrylovConfig(restart=20, max_iters=40), want_report=False)
+    torch.cuda.synchronize()
+    dX.zero_()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    rep = ctx.fgmres_device("v", dB.data_ptr(), dX.data_ptr(), nb, kc)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    its = int(max(rep.iterations))
+    out = {"grid": cfg["n"], "rhs": nb, "precond": "M_V (3 levels, GMRES(10) coarsest)", "restart": 20,
+           "iterations_max": its, "iterations_min": int(min(rep.iterations)), "all_converged": bool(all(rep.converged)),
+           "ms": ms, "solves_per_s": nb / (ms / 1e3)}
+    ctx.close()
+    if not args.no_cpu:
+        try:
+            from oracle import oracle as O
+            from oracle import problems as OP
+            acfg = ref_config(name)
+            acfg.update(precond="v", net=None, enc=None, coarse="gmres", coarse_iters=10, restart=20, levels=3)
+            a2 = OP.problem_arrays(acfg)
+            kind = "reference" if O.have_ref() else "port"
+            H, P = ref_preconditioner(O, kind, acfg, a2)
+            solve = O.ref_fgmres if kind == "reference" else O.fgmres
+            t0 = time.perf_counter()
+            solve(P, OP.rhs_block(a2)[:1], restart=20, max_iters=5, nthreads=1)
+            per_it = (time.perf_counter() - t0) / 5
+            out["cpu_reference"] = {"kind": kind, "cores": 1, "cpu": cpu_model(), "ms_per_iteration": 1e3 * per_it,
+                                    "extrapolated_solve_s_per_rhs": per_it * its,
+                                    "extrapolation": f"EXTRAPOLATED: 5 measured iterations x the device's {its} "
+                                                     "iterations, assuming the reference needs the same count "
+                                                     "(shown +-1 for M_V at 256^2 / 512^2 on the c0 medium, "
+                                                     "tests/test_scale_parity.py)",
+                                    "speedup_solves_per_s": (nb / (ms / 1e3)) / (1.0 / (per_it * its))}
+            del H, P
+        except Exception as ex:  # reported, not hidden
+            out["cpu_reference"] = {"error": repr(ex)}
     return out
 
 
@@ -897,7 +957,7 @@ def main():
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = 3 per SM: one per SM in each of the 3 column groups)")
-    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,datagen,paper_ju,train,block", help="comma list of configs measured on a fixed iteration budget "
+    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,mv512,datagen,paper_ju,train,block", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")

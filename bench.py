@@ -34,6 +34,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the C oracle's OpenMP threads (CPU reference legs) must not spin on the host
+# cores the device path's host work (e.g. training-pair draws) needs afterwards
+os.environ.setdefault("OMP_WAIT_POLICY", "PASSIVE")
 
 METRIC = "Helmholtz solves/s to 1e-6 rel residual"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}

@@ -1,6 +1,6 @@
 """A/B timing of library options on one config (device-resident FGMRES, CUDA events).
 
-  python tools/ab.py c0 "coarse_threads=256" "coarse_threads=1024" ...
+  python tools/ab.py c0 "staged_legs=0" "staged_legs=1" ...
 """
 import os
 import sys

@@ -960,7 +960,7 @@ def main():
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = 3 per SM: one per SM in each of the 3 column groups)")
-    ap.add_argument("--also", default="c1,c2,c3,c4,c4slab,mv512,datagen,paper_ju,train,block", help="comma list of configs measured on a fixed iteration budget "
+    ap.add_argument("--also", default="datagen,c1,c2,c3,c4,c4slab,mv512,paper_ju,train,block", help="comma list of configs measured on a fixed iteration budget "
                                                        "(c2: budget/2, c3: budget/5 iterations)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")

@@ -1045,6 +1045,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_legs_wd = int(value);
   else if (k == "pdl")
     ctx->opt_pdl = value != 0;
+  else if (k == "basis_wave")
+    ctx->opt_basis_wave = value != 0;
   else if (k == "coarse_krylov")
     ctx->opt_coarse_krylov = value != 0;
   else if (k == "coarse_cluster")

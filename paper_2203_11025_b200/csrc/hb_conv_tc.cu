@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __shared__ int4 sched[TC_MAX_CHUNKS];  // per K entry: {chunk-in-group | ty << 8 | tx << 16, chunk, kglob, kc}
   __shared__ int2 stg[TC_MAX_CHUNKS];    // per stage: {kb0 | kb1 << 16, group | last stage of group << 16}
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[240] = clock64();
   const int N = p.ntile;  // output channels of this CTA's work items; p.cout = row stride of out
   const int G = lay.G, kcmax = KC ? KC : lay.kcmax, nslots = lay.nslots, stages = lay.stages;
   const int CG = lay.CG, nhbuf = lay.nhbuf, nchunk = lay.nchunk;
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = tmem_slot;
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[241] = clock64();
 
   // work item -> (image, pixel box, output-channel block n0, K split: stages [s0, s1))
   int n0 = 0, ks = 0, s0 = 0, s1 = 0;
@@ -461,8 +463,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       ++tl;
     }
   }
+  if (p.trace && blockIdx.x == 0 && lane == 0 && warp >= 10) p.trace[242 + warp - 10] = clock64();
   tc_fence_before();
   __syncthreads();
+  if (p.trace && blockIdx.x == 0 && threadIdx.x == 0) p.trace[246] = clock64();
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
@@ -710,7 +714,9 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
             "prod cvt_in mma cvt_out\n",
             B, H, W, ca, cb, cw.cout, lay.G, lay.nslots, lay.nacc, lay.wres, lay.stages, lay.CG, lay.nhbuf,
             lay.box_bytes, ksplit);
-    const long long t0 = h[0] ? h[0] : h[2];
+    const long long t0 = h[240];
+    fprintf(stderr, "  setup %lld, epilogue done %lld %lld %lld %lld, exit %lld (cycles from entry)\n", h[241] - t0,
+            h[242] - t0, h[243] - t0, h[244] - t0, h[245] - t0, h[246] - t0);
     for (int i = 0; i < 64 && (h[i * 4] || h[i * 4 + 2]); ++i)
       fprintf(stderr, "  %2d %7lld %7lld %7lld %7lld\n", i, h[i * 4] - t0, h[i * 4 + 1] - t0, h[i * 4 + 2] - t0,
               h[i * 4 + 3] - t0);

@@ -815,14 +815,26 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
 
 // PDL launch with dynamic shared memory; opts in once per kernel (static +
 // dynamic shared memory may exceed the 48 KB default: adots_scalar stages 16 KB)
+// The grid is capped at one full wave: nblk_basis aims at 4 CTAs per SM, but
+// an instantiation whose registers allow only 3 would otherwise run 1.33
+// waves, the last third of the CTAs at a third of the occupancy (ncu, c0:
+// k_adots<5> at 68 registers, 592 CTAs).  The kernels grid-stride over the
+// column's nodes and size their partials by gridDim.x, so any nb works.
 template <typename... KArgs, typename... Args>
 static void launch_jm(Context& c, void (*k)(KArgs...), dim3 grid, size_t smem, Args&&... args) {
-  {
-    static std::vector<const void*> done;  // (per process; attributes are per function)
-    if (std::find(done.begin(), done.end(), reinterpret_cast<const void*>(k)) == done.end()) {
-      HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      done.push_back(reinterpret_cast<const void*>(k));
-    }
+  static std::vector<std::pair<const void*, int>> occ;  // (per process; attributes are per function)
+  int per_sm = 0;
+  for (const auto& e : occ)
+    if (e.first == reinterpret_cast<const void*>(k)) per_sm = e.second;
+  if (!per_sm) {
+    HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, KT, smem));
+    per_sm = std::max(1, per_sm);
+    occ.emplace_back(reinterpret_cast<const void*>(k), per_sm);
+  }
+  if (c.opt_basis_wave && grid.x > 1) {
+    const unsigned cap = std::max(1u, unsigned(per_sm * c.num_sms) / std::max(1u, grid.y));
+    grid.x = std::min(grid.x, cap);
   }
   launch_pdl(c, k, grid, dim3(KT), smem, std::forward<Args>(args)...);
 }

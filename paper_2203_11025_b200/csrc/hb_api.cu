@@ -298,7 +298,7 @@ static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const fl
       HB_CUDA(cudaEventRecord(c.ev_at_coarse, c.stream));
       c.ev_at_coarse = nullptr;
     }
-    coarsest_solve(c, B, c0, act, f, out);
+    if (!(c.dbg_skip & 4)) coarsest_solve(c, B, c0, act, f, out);
     return;
   }
   Level& L = *c.levels[size_t(l)];
@@ -316,12 +316,15 @@ static void vcycle_at(Context& c, int l, int B, int c0, const int* act, const fl
     // staged legs from e0 (level 0): the down leg stores the pre-smoothed iterate
     // into the level's v buffer and the up leg reads it back instead of e0
     float2* vpre = (e0 && c.opt_vpre && L.rows == L.ny) ? L.v.p + size_t(c0) * L.N() : nullptr;
-    if (stream)
+    const bool skip = c.dbg_skip & (l == 0 ? 1 : 2);
+    if (skip) {
+    } else if (stream)
       launch_down_stream(c, V, C.win(), w, offset, B, act, f, fscale, e0, Cf, vpre);
     else
       launch_down_fused(c, V, w, offset, B, act, f, fscale, e0, Cf);
     vcycle_at(c, l + 1, B, c0, act, Cf, nullptr, nullptr, Cx);
-    if (stream)
+    if (skip) {
+    } else if (stream)
       launch_up_stream(c, V, w, offset, C.nx, C.ny, C.win(), B, act, f, fscale, e0, Cx, out, vpre);
     else
       launch_up_fused(c, V, w, offset, C.nx, C.ny, B, act, f, fscale, e0, Cx, out);
@@ -503,12 +506,12 @@ static void fgmres_dev(Context& c, const hb_krylov_cfg* cfg, int kind, int B, co
       float2* Vj = c.kV.p + size_t(j) * BN;
       float2* Zj = c.kZ.p + size_t(j) * BN;
       precond_apply_dev(c, kind, B, c.kact.p, Vj, c.kscale.p, Zj);
-      launch_fg_adots(c, B, j, Zj, c.kW.p, c.kV.p);
+      if (!(c.dbg_skip & 8)) launch_fg_adots(c, B, j, Zj, c.kW.p, c.kV.p);
       launch_fg_update(c, B, j, m, c.kW.p, c.kV.p, cap, cfg->rel_tol, cfg->max_iters);
     }
     prof_active();
     if (flexible) {
-      launch_fg_finalize(c, B, m, c.kZ.p, dX);
+      if (!(c.dbg_skip & 16)) launch_fg_finalize(c, B, m, c.kZ.p, dX);
     } else {
       c.kfin.ensure(B);
       launch_fg_finalize_v(c, B, c.kV.p, c.kW.p, c.kfin.p);
@@ -1067,6 +1070,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_vpre = value != 0;
   else if (k == "staged_legs")
     ctx->opt_staged_legs = int(value);
+  else if (k == "debug_skip")
+    ctx->dbg_skip = int(value);
   else if (k == "stream_e0")
     ctx->opt_stream_e0 = value != 0;
   else

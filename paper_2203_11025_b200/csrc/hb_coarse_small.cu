@@ -11,56 +11,13 @@
 #include <cstdio>
 #include <cstdlib>
 
-#include "hb_common.cuh"
-#include "hb_internal.h"
+#include "hb_coarse_common.cuh"
 
 namespace hb {
 
 __device__ long long* g_coarse_trace = nullptr;
 
 namespace {
-
-constexpr int CS_MAXW = 32;
-constexpr int CS_SLOTS = 32;  // complex reduction slots: [0..15] dots, [16..31] Gram
-
-__device__ __forceinline__ double2 zmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
-}
-__device__ __forceinline__ double2 zconj(double2 a) { return make_double2(a.x, -a.y); }
-__device__ __forceinline__ double2 zsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 zscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-
-// warp reduce-scatter of 32 floats: on return lane l holds the warp sum of v[l] in v[0]
-__device__ __forceinline__ void warp_reduce_scatter32(float (&v)[32]) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int stage = 0; stage < 5; ++stage) {
-    const int half = 16 >> stage;
-    const int mask = 16 >> stage;
-    const bool upper = (lane & mask) != 0;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      if (k < half) {
-        const float send = upper ? v[k] : v[k + half];
-        const float keep = upper ? v[k + half] : v[k];
-        v[k] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
-      }
-    }
-  }
-}
-
-struct SmallSmem {
-  float part[CS_MAXW][2 * CS_SLOTS];  // [warp][float]: 0..31 dots (re,im), 32..63 Gram / norm
-  double2 H[kMaxCoarseIters + 1][kMaxCoarseIters + 1];  // H[col][row], col < k, row <= col+1
-  double2 G[kMaxCoarseIters][kMaxCoarseIters + 1];      // G[i][k] = <V_i, V_k>, k < i (padded: lane-per-row reads)
-  double2 y[kMaxCoarseIters];
-  double2 sn[kMaxCoarseIters], g[kMaxCoarseIters + 1];
-  double cs[kMaxCoarseIters];
-  double scale[kMaxCoarseIters + 2];                    // V_i = scale[i] * Vraw_i
-  float2 coef[kMaxCoarseIters + 1];
-  double beta0;
-  int k, stop;
-};
 
 // Per Arnoldi step j (two CTA barriers):
 //   w_raw = M D^-1 Vraw_j          (neighbours of Vraw_j read from shared memory)
@@ -314,69 +271,6 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_small(LevelView L, int m, cons
 // independent loads per node, no bounds branches).  Same arithmetic and
 // summation order as k_coarse_small (the MGS correction is fed from per-warp
 // smem broadcasts instead of double-precision shuffles).
-// Least squares min |beta0 e1 - H y| of the coarse GMRES on one warp
-// (krylov.hpp Givens + back substitution, same per-element operations as the
-// serial loop in k_coarse_small): lane j owns Hessenberg column j; rotation i
-// is generated by lane i once rotations 0..i-1 reached it and is broadcast to
-// lanes > i (depth k rotations instead of k(k+1)/2).  The triangle is then
-// transposed through smem so lane i owns row i for a column-sweep back
-// substitution.  Writes S.coef[i] = y_i * scale_i.
-template <int MAXK>
-__device__ __forceinline__ void coarse_lsq_warp(SmallSmem& S, int k, int lane) {
-  // rolled loops over smem-resident columns: this code runs once per launch,
-  // so its size (cold instruction fetch) matters more than its registers
-  double2 gi = make_double2(lane == 0 ? S.beta0 : 0.0, 0.0);  // lane i holds g[i]
-  double2 gcarry = make_double2(S.beta0, 0.0);                 // g[i] before rotation i (all lanes)
-  double2 dg = make_double2(1.0, 0.0);                         // this lane's final diagonal
-  double2* hc = S.H[lane < k ? lane : 0];
-#pragma unroll 1
-  for (int i = 0; i < k; ++i) {
-    double cs = 0.0;
-    double2 sn = make_double2(0.0, 0.0);
-    if (lane == i) {
-      const double2 a = hc[i];
-      const double hn = hc[i + 1].x;
-      const double a2 = a.x * a.x + a.y * a.y;
-      if (a2 + hn * hn == 0.0) {
-        cs = 1.0;
-      } else if (a2 == 0.0) {
-        sn = make_double2(1.0, 0.0);
-      } else {
-        const double ia = rsqrt(a2), ir = rsqrt(a2 + hn * hn);
-        cs = a2 * ia * ir;
-        sn = zscale(a, hn * ia * ir);
-      }
-      dg = dadd(zscale(a, cs), zmul(sn, hc[i + 1]));
-      hc[i] = dg;
-    }
-    cs = __shfl_sync(0xffffffffu, cs, i);
-    sn = make_double2(__shfl_sync(0xffffffffu, sn.x, i), __shfl_sync(0xffffffffu, sn.y, i));
-    if (lane > i && lane < k) {
-      const double2 h0 = hc[i], h1 = hc[i + 1];
-      hc[i] = dadd(zscale(h0, cs), zmul(sn, h1));
-      hc[i + 1] = dadd(zscale(zmul(zconj(sn), h0), -1.0), zscale(h1, cs));
-    }
-    const double2 gnext = zscale(zmul(zconj(sn), gcarry), -1.0);
-    if (lane == i) gi = zscale(gcarry, cs);
-    if (lane == i + 1) gi = gnext;
-    gcarry = gnext;
-  }
-  __syncwarp();
-  // column-sweep back substitution: lane i accumulates row i of R y
-  const double inv = 1.0 / (dg.x * dg.x + dg.y * dg.y);
-  double2 acc = gi, yl = make_double2(0.0, 0.0);
-#pragma unroll 1
-  for (int l = k - 1; l >= 0; --l) {
-    if (lane == l) yl = zscale(zmul(acc, zconj(dg)), inv);
-    const double2 y = make_double2(__shfl_sync(0xffffffffu, yl.x, l), __shfl_sync(0xffffffffu, yl.y, l));
-    if (lane < l) acc = zsub(acc, zmul(S.H[l][lane], y));
-  }
-  if (lane <= MAXK) {
-    const double2 c = lane < k ? zscale(yl, S.scale[lane]) : make_double2(0.0, 0.0);
-    S.coef[lane] = make_float2(float(c.x), float(c.y));  // zero beyond k: the x sum runs over all MAXK
-  }
-}
-
 template <int NT, int NPT, int MAXK>
 __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const int* act,
                                                        const float2* __restrict__ f, float2* __restrict__ x) {
@@ -476,99 +370,7 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
     if (tr && j < 16) tr[j * 8 + 3] = clock64();
     // scalar phase on warp 0 only (the fp64 work and its smem reads are not
     // repeated by every warp); results go through smem behind one barrier
-    if (warp == 0) {
-      double2 val = make_double2(0.0, 0.0);
-      {
-        // lane i < 16: <V_i, w>; lane 16 + i: Gram i (re at the odd slot)
-        const int f0 = lane < 16 ? 2 * lane : (one ? 0 : 32) + 30 - 2 * (lane - 16);
-        float px_[NT / 32], py_[NT / 32];  // fp32 pairwise fold of the per-warp sums, one conversion
-#pragma unroll
-        for (int w2 = 0; w2 < NT / 32; ++w2) {
-          const float2 pp = *reinterpret_cast<const float2*>(&S.part[w2][f0]);
-          px_[w2] = lane < 16 ? pp.x : pp.y;
-          py_[w2] = lane < 16 ? pp.y : pp.x;
-        }
-#pragma unroll
-        for (int st = 1; st < NT / 32; st *= 2)  // pairwise fold (depth log2 of the warp count)
-#pragma unroll
-          for (int w2 = 0; w2 + st < NT / 32; w2 += 2 * st) {
-            px_[w2] += px_[w2 + st];
-            py_[w2] += py_[w2 + st];
-          }
-        val = make_double2(px_[0], py_[0]);
-      }
-      if (tr && j < 16) tr[96 + j] = clock64();
-      const double nrm2 = __shfl_sync(0xffffffffu, val.x, 16 + j);
-      const double rnrm = nrm2 > 0.0 ? rsqrt(nrm2) : 0.0;
-      const double nrm = nrm2 * rnrm;
-      if (tr && j < 16) tr[112 + j] = clock64();
-      int stop = 0, kf = 0;
-      if (j == 0) {
-        if (lane == 0) S.beta0 = nrm;
-        if (nrm == 0.0) stop = 1;  // k = 0
-      } else {
-        const double hn = hn_prev * nrm;
-        if (lane == 0) S.H[j - 1][j] = make_double2(hn, 0.0);
-        if (hn <= 1e-14 * S.beta0) {
-          stop = 1;
-          kf = j;
-        }
-      }
-      const double sj = rnrm;
-      if (!stop) {
-        if (lane == 0) S.scale[j] = sj;
-        if (j == m) {
-          stop = 1;
-          kf = m;
-        }
-      }
-      if (!stop) {
-        hn_prev = sj;
-        const double si = (lane < j) ? S.scale[lane] : sj;
-        double2 hcgs = make_double2(0.0, 0.0);
-        if (lane <= j) hcgs = zscale(val, si * sj);
-        double2 gjk = make_double2(0.0, 0.0);
-        {
-          const double2 e = make_double2(__shfl_sync(0xffffffffu, val.x, (16 + lane) & 31),
-                                         __shfl_sync(0xffffffffu, val.y, (16 + lane) & 31));
-          if (lane < j) gjk = zscale(e, sj * S.scale[lane]);
-        }
-        if (tr && j < 16) tr[j * 8 + 7] = clock64();
-        // first-order MGS correction h_i -= sum_{k<i} hcgs_k G_ik (operands broadcast through smem)
-        if (lane <= MAXK) {
-          sHc[lane] = hcgs;
-          sGj[lane] = gjk;
-        }
-        __syncwarp();
-        double2 h = hcgs;
-        {
-          // branch-free: all products issued at once (masked), then a pairwise sum
-          const int row = lane < MAXK ? lane : MAXK - 1;
-          double2 pr[MAXK];
-#pragma unroll
-          for (int kk = 0; kk < MAXK; ++kk) {
-            const double2 hk = sHc[kk];
-            const double2 g1 = sGj[kk], g2 = S.G[row][kk];
-            const double2 p = zmul(hk, lane == j ? g1 : g2);
-            pr[kk] = (kk < lane && lane <= j) ? p : make_double2(0.0, 0.0);
-          }
-#pragma unroll
-          for (int st = 1; st < MAXK; st *= 2)
-#pragma unroll
-            for (int kk = 0; kk + st < MAXK; kk += 2 * st) pr[kk] = dadd(pr[kk], pr[kk + st]);
-          h = zsub(h, pr[0]);
-        }
-        if (lane <= j) S.H[j][lane] = h;
-        if (lane < j) S.G[j][lane] = gjk;
-        const double2 cc = zscale(h, si * nrm);  // si / sj
-        if (lane <= MAXK) S.coef[lane] = lane <= j ? make_float2(float(cc.x), float(cc.y)) : make_float2(0.f, 0.f);
-      }
-      if (lane == 0) {
-        S.stop = stop;
-        S.k = kf;
-      }
-      if (tr && j < 16) tr[j * 8 + 4] = clock64();
-    }
+    if (warp == 0) coarse_scalar_phase<NT / 32, MAXK>(S, sHc, sGj, j, m, one, hn_prev, lane);
     __syncthreads();
     if (S.stop) {
       k = S.k;

@@ -30,6 +30,13 @@ namespace hb {
 
 namespace {
 
+// row chunks per launch: halve the rows per warp while fewer than rpc_fill() x SMs x warps-per-CTA
+// warps would run (HB_RPC_FILL overrides; experiments)
+inline int rpc_fill() {
+  static const int v = getenv("HB_RPC_FILL") ? atoi(getenv("HB_RPC_FILL")) : 2;
+  return v;
+}
+
 constexpr int GW = 4;      // warps per CTA
 constexpr int ROWF = 68;   // float2 per staged fine row
 
@@ -473,7 +480,7 @@ void launch_down_staged(Context& c, const LevelView& L, const RowWin& cw, float 
   const int swout = e0 ? down_out<true>() : down_out<false>();
   static const int env_d = getenv("HB_RPC_DOWN") ? atoi(getenv("HB_RPC_DOWN")) : 0;
   int rpc = 8;
-  while (rpc > 4 && size_t((cnx + swout - 1) / swout) * ((cny + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * GW)
+  while (rpc > 4 && size_t((cnx + swout - 1) / swout) * ((cny + rpc - 1) / rpc) * B < size_t(rpc_fill()) * c.num_sms * GW)
     rpc /= 2;
   if (env_d) rpc = env_d;
   const int chunks = (cny + rpc - 1) / rpc;
@@ -502,7 +509,7 @@ void launch_up_staged(Context& c, const LevelView& L, float damping, int offset,
   static const int env_u = getenv("HB_RPC_UP") ? atoi(getenv("HB_RPC_UP")) : 0;
   const int nrows = L.w.hi - L.w.lo;
   int rpc = 16;
-  while (rpc > 8 && size_t((cnx + 29) / 30) * ((nrows + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * GW) rpc /= 2;
+  while (rpc > 8 && size_t((cnx + 29) / 30) * ((nrows + rpc - 1) / rpc) * B < size_t(rpc_fill()) * c.num_sms * GW) rpc /= 2;
   if (env_u) rpc = env_u;
   const int chunks = (nrows + rpc - 1) / rpc;
   const dim3 grid((cnx + 29) / 30, (chunks + GW - 1) / GW, B);

@@ -19,6 +19,13 @@ namespace hb {
 
 namespace {
 
+// row chunks per launch: halve the rows per warp while fewer than rpc_fill() x SMs x warps-per-CTA
+// warps would run (HB_RPC_FILL overrides; experiments)
+inline int rpc_fill() {
+  static const int v = getenv("HB_RPC_FILL") ? atoi(getenv("HB_RPC_FILL")) : 2;
+  return v;
+}
+
 constexpr int SW_OUT = 30;  // coarse columns emitted per warp
 constexpr int WARPS = 4;    // warps per CTA (independent row chunks)
 
@@ -620,7 +627,7 @@ void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float 
   // rows per warp: enough warps to fill the machine, >= 4 coarse rows to amortise the halo
   static const int env_d = getenv("HB_RPC_DOWN") ? atoi(getenv("HB_RPC_DOWN")) : 0;
   int rpc = 8;
-  while (rpc > 4 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((cny + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
+  while (rpc > 4 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((cny + rpc - 1) / rpc) * B < size_t(rpc_fill()) * c.num_sms * WARPS)
     rpc /= 2;
   if (env_d) rpc = env_d;
   const int chunks = (cny + rpc - 1) / rpc;
@@ -657,7 +664,7 @@ void launch_up_stream(Context& c, const LevelView& L, float damping, int offset,
   static const int env_u = getenv("HB_RPC_UP") ? atoi(getenv("HB_RPC_UP")) : 0;
   const int nrows = L.w.hi - L.w.lo;
   int rpc = 16;
-  while (rpc > 8 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((nrows + rpc - 1) / rpc) * B < size_t(8) * c.num_sms * WARPS)
+  while (rpc > 8 && size_t((cnx + SW_OUT - 1) / SW_OUT) * ((nrows + rpc - 1) / rpc) * B < size_t(rpc_fill()) * c.num_sms * WARPS)
     rpc /= 2;
   if (env_u) rpc = env_u;
   const int chunks = (nrows + rpc - 1) / rpc;

@@ -119,6 +119,11 @@ int hb_coarse_solve(hb_ctx* ctx, int batch, const double* f, double* x);
 #define HB_PC_JU 2 /* e1 = J_A(0, r); z = J_A(e1 + net(h^2 (r - A e1), kappa^2), r)  (M_JU,
                       inc/precond.hpp:104-139, JacobiUnetPreconditioner::apply with the A5 net) */
 int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* z);
+/* Same on device buffers: r, z are complex64 (interleaved float pairs)
+ * [batch][ny][nx] in device memory; enqueued on hb_stream(ctx), no host
+ * synchronisation (callers keeping their fields in HBM, e.g. a device-side
+ * outer Krylov loop).  r and z must not overlap. */
+int hb_precond_apply_device(hb_ctx* ctx, int kind, int batch, const void* r, void* z);
 /* name() and requires_flexible() of the reference plugin (inc/precond.hpp:14-27) */
 const char* hb_precond_name(int kind);
 int hb_precond_requires_flexible(hb_ctx* ctx, int kind);

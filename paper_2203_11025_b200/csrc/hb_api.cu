@@ -888,6 +888,19 @@ int hb_precond_apply(hb_ctx* ctx, int kind, int batch, const double* r, double* 
   HB_API_END
 }
 
+int hb_precond_apply_device(hb_ctx* ctx, int kind, int batch, const void* dr, void* dz) {
+  HB_API_BEGIN
+  require_whole(*ctx);
+  require_hier(*ctx);
+  if (batch < 1) throw HbError{HB_ERR_ARG, "batch must be >= 1"};
+  if (!dr || !dz) throw HbError{HB_ERR_ARG, "null device buffer"};
+  ensure_batch(*ctx, batch);
+  precond_apply_dev(*ctx, kind, batch, ctx->act_all.p, static_cast<const float2*>(dr), nullptr,
+                    static_cast<float2*>(dz));
+  HB_CUDA(cudaGetLastError());
+  HB_API_END
+}
+
 const char* hb_precond_name(int kind) { return precond_name(kind); }
 
 int hb_precond_requires_flexible(hb_ctx* ctx, int kind) { return !ctx || requires_flexible(*ctx, kind) ? 1 : 0; }

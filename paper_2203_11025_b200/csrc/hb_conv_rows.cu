@@ -111,10 +111,12 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
     y1 = min(p.H, y0 + p.rb);
   };
 
+  if (warp != 0) pdl_enter();  // the producer waits after issuing the weights
   if (warp == 0) {
     // ---------------- producer: weights once, then one row box per chunk and input row
     mbar_expect_tx_elect(&bar_w, uint32_t(p.nslice * nch * 3 * CR_WBLK));
     bulk_load_elect(wsm, p.wrow, uint32_t(p.nslice * nch * 3 * CR_WBLK), &bar_w);
+    pdl_enter();  // PDL: the weights above are constant; rows / act / outputs only after the predecessor
     int s = 0;
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       int b, x0, y0, y1;
@@ -363,7 +365,7 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
   if (c.prof_detail)
     c.prof_label = "conv_rows " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
-  k_conv_rows<<<grid, CR_THREADS, smem, c.stream>>>(mA, mB, p);
+  launch_pdl(c, k_conv_rows, dim3(grid), dim3(CR_THREADS), smem, mA, mB, p);
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());
   return true;

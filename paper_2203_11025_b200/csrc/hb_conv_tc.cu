@@ -217,6 +217,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     x0 = (tile % tiles_x) * p.bw;
   };
 
+  if (warp != 0) pdl_enter();  // the producer waits after issuing its resident weights
   if (warp == 0) {
     // ---------------- producer (whole warp, elected lane issues)
     int s = 0, it = 0, hb = 0, hit = 0;
@@ -233,6 +234,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tma_load_2d_elect(w + N * kc * 4, kc == 32 ? &mapWl32 : &mapWl16, &bar_w, e.z, 0);
       }
     }
+    pdl_enter();  // PDL: weights above are constant; activations / act / outputs only after the predecessor
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       int b, y0, x0;
       tile_coords(tile, b, y0, x0);
@@ -477,6 +479,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 __global__ void k_conv_ksum4(int ksplit, size_t n4, int cout4, size_t img4, const int* act,
                              const float4* __restrict__ ws, const float4* __restrict__ bias, int relu,
                              float4* __restrict__ out) {
+  pdl_enter();
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n4; i += size_t(gridDim.x) * blockDim.x) {
     if (act && !act[i / img4]) continue;  // frozen column: its partials were not written
     float4 a = __ldg(bias + (i % cout4));
@@ -496,6 +499,7 @@ __global__ void k_conv_ksum4(int ksplit, size_t n4, int cout4, size_t img4, cons
 // (deterministic); ws is dense over the tile grid, out follows the geometry
 __global__ void k_conv_ksum(int ksplit, int B, int H, int W, int cout, const int* act, const float* __restrict__ ws,
                             const float* __restrict__ bias, TcGeo geo, TcEpi epi, float* __restrict__ out) {
+  pdl_enter();
   const size_t n = size_t(B) * H * W * cout;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x) {
     const size_t pix = i / cout;
@@ -687,19 +691,20 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout) + " taps " +
                    std::to_string(NT) + " s" + std::to_string(geo.s);
   static const int dbg = getenv("HB_CONV_DEBUG") ? atoi(getenv("HB_CONV_DEBUG")) : 0;
-  kern<<<grid, TC_THREADS, smem, c.stream>>>(mA, mB, wh32, wl32, wh16, wl16, p, lay, dbg);
+  launch_pdl(c, kern, dim3(grid), dim3(TC_THREADS), smem, mA, mB, wh32, wl32, wh16, wl16, p, lay, dbg);
   if (ksplit > 1) {
     HB_CUDA(cudaGetLastError());
     const size_t n = size_t(B) * H * W * cw.cout;
     const bool dense = geo.os == 1 && geo.ldo == cw.cout && !t.epi.res && !t.epi.mu && t.epi.act != 2 && !t.epi.nco;
     if (dense) {
       const size_t n4 = n / 4;
-      k_conv_ksum4<<<int(std::min<size_t>((n4 + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
-          ksplit, n4, cw.cout / 4, size_t(H) * W * cw.cout / 4, t.act, reinterpret_cast<const float4*>(ws),
-          reinterpret_cast<const float4*>(cw.db.p), t.epi.act == 1, reinterpret_cast<float4*>(t.out));
+      launch_pdl(c, k_conv_ksum4, dim3(unsigned(std::min<size_t>((n4 + 255) / 256, size_t(c.num_sms) * 8))), dim3(256),
+                 0, ksplit, n4, cw.cout / 4, size_t(H) * W * cw.cout / 4, t.act, reinterpret_cast<const float4*>(ws),
+                 reinterpret_cast<const float4*>(cw.db.p), int(t.epi.act == 1), reinterpret_cast<float4*>(t.out));
     } else {
-      k_conv_ksum<<<int(std::min<size_t>((n + 255) / 256, size_t(c.num_sms) * 8)), 256, 0, c.stream>>>(
-          ksplit, B, H, W, cw.cout, t.act, ws, cw.db.p, geo, t.epi, t.out);
+      launch_pdl(c, k_conv_ksum, dim3(unsigned(std::min<size_t>((n + 255) / 256, size_t(c.num_sms) * 8))), dim3(256), 0,
+                 ksplit, B, H, W, int(cw.cout), t.act, static_cast<const float*>(ws), static_cast<const float*>(cw.db.p),
+                 geo, t.epi, t.out);
     }
   }
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout),

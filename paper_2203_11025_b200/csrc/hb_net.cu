@@ -41,6 +41,7 @@ struct ConvArgs {
 };
 
 __global__ void __launch_bounds__(256) k_conv3x3(ConvArgs p) {
+  pdl_enter();
   const int bz = blockIdx.z;
   if (p.act && !p.act[bz]) return;
   __shared__ float patch[PH * PW][CT_CI + 1];
@@ -124,6 +125,7 @@ constexpr int CS_TW = 32, CS_TH = 8, CS_PX = 1, CS_NT = CS_TW * CS_TH / CS_PX;
 
 template <int COUT>
 __global__ void __launch_bounds__(CS_NT) k_conv_small(ConvArgs p) {
+  pdl_enter();
   extern __shared__ __align__(16) float cs_sm[];
   const int bz = blockIdx.z;
   if (p.act && !p.act[bz]) return;
@@ -241,6 +243,7 @@ struct SmallW {
 
 template <int CIN, int COUT>
 __global__ void __launch_bounds__(CS_NT) k_conv_small_pw(ConvArgs p, const __grid_constant__ SmallW<CIN, COUT> wt) {
+  pdl_enter();
   extern __shared__ __align__(16) float cs_sm[];
   const int bz = blockIdx.z;
   if (p.act && !p.act[bz]) return;
@@ -323,7 +326,7 @@ bool conv_small_pw(Context& c, const ConvW& cw, const ConvArgs& p, dim3 g) {
       for (int tap = 0; tap < 9; ++tap) wt.w[(tap * CIN + ci) * COUT + co] = cw.w[(size_t(co) * CIN + ci) * 9 + tap];
   }
   const size_t smem = size_t(CS_TH + 2) * (CS_TW + 2) * size_t(CIN | 1) * sizeof(float);
-  k_conv_small_pw<CIN, COUT><<<g, CS_NT, smem, c.stream>>>(p, wt);
+  launch_pdl(c, k_conv_small_pw<CIN, COUT>, dim3(g), dim3(CS_NT), smem, p, wt);
   return true;
 }
 
@@ -331,6 +334,7 @@ bool conv_small_pw(Context& c, const ConvW& cw, const ConvArgs& p, dim3 g) {
 // one CTA per output row (grid (rows, B)), threads stride along the row
 __global__ void __launch_bounds__(256) k_maxpool2_v4(int H, int W, int C4, const float4* __restrict__ in,
                                                      float4* __restrict__ out, const int* act) {
+  pdl_enter();
   const int b = blockIdx.y, oy = blockIdx.x;
   if (act && !act[b]) return;
   const int Wo = W / 2, n = Wo * C4;
@@ -352,6 +356,7 @@ __global__ void __launch_bounds__(256) k_maxpool2_v4(int H, int W, int C4, const
 
 __global__ void k_maxpool2(int B, int H, int W, int C, const float* __restrict__ in, float* __restrict__ out,
                            const int* act) {
+  pdl_enter();
   const int Ho = H / 2, Wo = W / 2;
   const size_t total = size_t(Ho) * Wo * C;
   const int b = blockIdx.y;
@@ -380,6 +385,7 @@ __device__ __forceinline__ void up_taps(int o, int n, int* i0, int* i1, float* f
 
 __global__ void k_upsample2(int B, int H, int W, int C, const float* __restrict__ in, long long sin_,
                             float* __restrict__ out, const int* act) {
+  pdl_enter();
   const int Ho = 2 * H, Wo = 2 * W;
   const size_t total = size_t(Ho) * Wo * C;
   const int b = blockIdx.y;
@@ -401,6 +407,7 @@ __global__ void k_upsample2(int B, int H, int W, int C, const float* __restrict_
 
 __global__ void __launch_bounds__(256) k_upsample2_v4(int H, int W, int C4, const float4* __restrict__ in,
                                                       long long sin4, float4* __restrict__ out, const int* act) {
+  pdl_enter();
   const int b = blockIdx.y, oy = blockIdx.x;
   if (act && !act[b]) return;
   const int Wo = 2 * W, n = Wo * C4;
@@ -427,6 +434,7 @@ __global__ void __launch_bounds__(256) k_upsample2_v4(int H, int W, int C4, cons
 // [h^2 Re r, h^2 Im r, kappa^2] NHWC (inc/precond.hpp:74-83, gamma dropped)
 __global__ void k_pack(int N, float h2, const int* act, const float2* __restrict__ r, const float* rscale,
                        const float* __restrict__ k2, float* __restrict__ x) {
+  pdl_enter();
   const int b = blockIdx.y;
   if (act && !act[b]) return;
   const float s = h2 * (rscale ? rscale[b] : 1.0f);
@@ -440,6 +448,7 @@ __global__ void k_pack(int N, float h2, const int* act, const float2* __restrict
 }
 
 __global__ void k_unpack(int N, const int* act, const float* __restrict__ y, float2* __restrict__ e) {
+  pdl_enter();
   const int b = blockIdx.y;
   if (act && !act[b]) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
@@ -449,6 +458,7 @@ __global__ void k_unpack(int N, const int* act, const float* __restrict__ y, flo
 }
 
 __global__ void k_unpack_add(int N, const int* act, const float* __restrict__ y, const float2* base, float2* e) {
+  pdl_enter();
   const int b = blockIdx.y;
   if (act && !act[b]) return;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
@@ -517,9 +527,9 @@ static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int 
                                        conv_small_pw<8, 2>(c, cw, p, g));
     if (pw) {
     } else if (cw.cout == 16) {
-      k_conv_small<16><<<g, CS_NT, smem, c.stream>>>(p);
+      launch_pdl(c, k_conv_small<16>, dim3(g), dim3(CS_NT), smem, p);
     } else {
-      k_conv_small<2><<<g, CS_NT, smem, c.stream>>>(p);
+      launch_pdl(c, k_conv_small<2>, dim3(g), dim3(CS_NT), smem, p);
     }
     HB_CUDA(cudaGetLastError());
     return;
@@ -529,7 +539,7 @@ static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int 
   if (c.prof_detail)
     c.prof_label = "conv_simt " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
-  k_conv3x3<<<grid, 256, 0, c.stream>>>(p);
+  launch_pdl(c, k_conv3x3, dim3(grid), dim3(256), 0, p);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -537,12 +547,12 @@ static void maxpool(Context& c, int B, const int* act, int H, int W, int C, cons
   NScope ns(c, PC_NETIO);
   if (C % 4 == 0) {
     const int n = (W / 2) * (C / 4);
-    k_maxpool2_v4<<<dim3(H / 2, B), n >= 256 ? 256 : ((n + 31) / 32) * 32, 0, c.stream>>>(
+    launch_pdl(c, k_maxpool2_v4, dim3(H / 2, B), dim3(n >= 256 ? 256 : ((n + 31) / 32) * 32), 0,
         H, W, C / 4, reinterpret_cast<const float4*>(in), reinterpret_cast<float4*>(out), act);
     HB_CUDA(cudaGetLastError());
     return;
   }
-  k_maxpool2<<<dim3(grid1(size_t(H / 2) * (W / 2) * C), B), 256, 0, c.stream>>>(B, H, W, C, in, out, act);
+  launch_pdl(c, k_maxpool2, dim3(grid1(size_t(H / 2) * (W / 2) * C), B), dim3(256), 0, B, H, W, C, in, out, act);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -551,12 +561,12 @@ static void upsample(Context& c, int B, const int* act, int H, int W, int C, con
   NScope ns(c, PC_NETIO);
   if (C % 4 == 0 && sin_ % 4 == 0) {
     const int n = 2 * W * (C / 4);
-    k_upsample2_v4<<<dim3(2 * H, B), n >= 256 ? 256 : ((n + 31) / 32) * 32, 0, c.stream>>>(
+    launch_pdl(c, k_upsample2_v4, dim3(2 * H, B), dim3(n >= 256 ? 256 : ((n + 31) / 32) * 32), 0,
         H, W, C / 4, reinterpret_cast<const float4*>(in), sin_ / 4, reinterpret_cast<float4*>(out), act);
     HB_CUDA(cudaGetLastError());
     return;
   }
-  k_upsample2<<<dim3(grid1(size_t(4) * H * W * C), B), 256, 0, c.stream>>>(B, H, W, C, in, sin_, out, act);
+  launch_pdl(c, k_upsample2, dim3(grid1(size_t(4) * H * W * C), B), dim3(256), 0, B, H, W, C, in, sin_, out, act);
   HB_CUDA(cudaGetLastError());
 }
 
@@ -564,19 +574,19 @@ void launch_pack_input(Context& c, const LevelView& L, double h2, int B, const i
                        const float* rscale, float* x) {
   NScope ns(c, PC_NETIO);
   const int N = L.nx * L.ny;
-  k_pack<<<dim3(grid1(N), B), 256, 0, c.stream>>>(N, float(h2), act, r, rscale, L.k2f, x);
+  launch_pdl(c, k_pack, dim3(grid1(N), B), dim3(256), 0, N, float(h2), act, r, rscale, L.k2f, x);
   HB_CUDA(cudaGetLastError());
 }
 
 void launch_unpack_add(Context& c, int N, int B, const int* act, const float* y, const float2* base, float2* e) {
   NScope ns(c, PC_NETIO);
-  k_unpack_add<<<dim3(grid1(N), B), 256, 0, c.stream>>>(N, act, y, base, e);
+  launch_pdl(c, k_unpack_add, dim3(grid1(N), B), dim3(256), 0, N, act, y, base, e);
   HB_CUDA(cudaGetLastError());
 }
 
 void launch_unpack_output(Context& c, int N, int B, const int* act, const float* y, float2* e) {
   NScope ns(c, PC_NETIO);
-  k_unpack<<<dim3(grid1(N), B), 256, 0, c.stream>>>(N, act, y, e);
+  launch_pdl(c, k_unpack, dim3(grid1(N), B), dim3(256), 0, N, act, y, e);
   HB_CUDA(cudaGetLastError());
 }
 

@@ -25,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "hb_common.cuh"
 #include "hb_host.h"
 #include "hb_internal.h"
 #include "hb_paper.h"
@@ -319,6 +320,7 @@ struct PConv {
 // transpose (gather form of col2im, inc/autodiff.hpp:190-215)
 template <int CO>
 __global__ void __launch_bounds__(128) k_pconv(PConv a) {
+  pdl_enter();
   const long long npix = (long long)a.B * a.Ho * a.Wo;
   const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= npix) return;
@@ -398,6 +400,7 @@ constexpr int PC_T = 128, PC_CO = 16, PC_CI = 16;
 // so no work is spent on the 3/4 of the taps that miss.
 template <int P, bool VEC>  // VEC: cin % 4 == 0 and ldx % 4 == 0 (float4 input loads)
 __global__ void __launch_bounds__(PC_T) k_pconv_tiled(PConv a) {
+  pdl_enter();
   extern __shared__ float4 sw4[];  // [tap][ci_local][PC_CO] as float4 x 4
   float* sw = reinterpret_cast<float*>(sw4);
   const int t = threadIdx.x;
@@ -545,6 +548,7 @@ __global__ void __launch_bounds__(PC_T) k_pconv_tiled(PConv a) {
 // dst[pix][off + c] = src[pix (mod plane if bcast)][c]
 __global__ void k_copy_ch(long long npix, int plane, int bcast, int C, const float* __restrict__ src, int lds,
                           float* __restrict__ dst, int ldd) {
+  pdl_enter();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= npix * C) return;
   const long long p = i / C;
@@ -556,6 +560,7 @@ __global__ void k_copy_ch(long long npix, int plane, int bcast, int C, const flo
 // (h^2 Re r, h^2 Im r, kappa^2, gamma) NHWC (inc/precond.hpp:74-90)
 __global__ void k_pack4(int N, float h2, const int* act, const float2* __restrict__ r, const float* rscale,
                         const float* __restrict__ k2, const float* __restrict__ gam, float* __restrict__ x) {
+  pdl_enter();
   const int b = blockIdx.y;
   if (act && !act[b]) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -674,11 +679,11 @@ struct Exec {
         attr = true;
       }
       if (smem > 100 * 1024)
-        k_pconv<16><<<unsigned((npix + 127) / 128), 128, 0, c.stream>>>(a);
+        launch_pdl(c, k_pconv<16>, dim3(unsigned((npix + 127) / 128)), dim3(128), 0, a);
       else if (P == 4)
-        (vec ? k_pconv_tiled<4, true> : k_pconv_tiled<4, false>)<<<grid, PC_T, smem, c.stream>>>(a);
+        launch_pdl(c, (vec ? k_pconv_tiled<4, true> : k_pconv_tiled<4, false>), dim3(grid), dim3(PC_T), smem, a);
       else
-        (vec ? k_pconv_tiled<1, true> : k_pconv_tiled<1, false>)<<<grid, PC_T, smem, c.stream>>>(a);
+        launch_pdl(c, (vec ? k_pconv_tiled<1, true> : k_pconv_tiled<1, false>), dim3(grid), dim3(PC_T), smem, a);
     }
     HB_CUDA(cudaGetLastError());
     const double taps = D.transpose && stride == 2 ? double(D.k) * D.k / 4.0 : double(D.k) * D.k;
@@ -690,7 +695,7 @@ struct Exec {
     const long long npix = (long long)B * dst.H * dst.W;
     const long long n = npix * src.C;
     c.launches++;
-    k_copy_ch<<<unsigned((n + 255) / 256), 256, 0, c.stream>>>(npix, dst.H * dst.W, bcast ? 1 : 0, src.C, src.p,
+    launch_pdl(c, k_copy_ch, dim3(unsigned((n + 255) / 256)), dim3(256), 0, npix, dst.H * dst.W, bcast ? 1 : 0, src.C, src.p,
                                                                src.ld, dst.p, dst.ld);
     HB_CUDA(cudaGetLastError());
   }
@@ -843,7 +848,7 @@ void paper_infer(Context& c, int B, const int* act, const float2* r, const float
   P.io.ensure(np * 6);
   {
     const int tok = prof_begin(c, PC_NETIO);
-    k_pack4<<<dim3((N + 255) / 256, B), 256, 0, c.stream>>>(N, float(L.h * L.h), act, r, rscale, P.k2f.p, P.gamf.p,
+    launch_pdl(c, k_pack4, dim3((N + 255) / 256, B), dim3(256), 0, N, float(L.h * L.h), act, r, rscale, P.k2f.p, P.gamf.p,
                                                             P.io.p);
     HB_CUDA(cudaGetLastError());
     prof_end(c, PC_NETIO, tok, double(np) * (8 + 16) + double(N) * 8, 0);

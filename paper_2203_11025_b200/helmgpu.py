@@ -68,7 +68,8 @@ def lib():
         if not os.path.exists(LIB_PATH):
             raise ImportError(f"{LIB_PATH} missing: run `python -m paper_2203_11025_b200.build` "
                               "(the CUDA library is the only implementation; there is no CPU fallback)")
-        L = C.CDLL(LIB_PATH)
+        # HB_LIB_PATH: load another build of the same library (A/B timing, tools/abbuild.sh)
+        L = C.CDLL(os.environ.get("HB_LIB_PATH", LIB_PATH))
         L.hb_create.argtypes = [C.c_int, C.POINTER(_vp)]
         L.hb_destroy.argtypes = [_vp]
         L.hb_last_error.restype = C.c_char_p
@@ -94,6 +95,7 @@ def lib():
         L.hb_prolong.argtypes = [_vp, C.c_int, C.c_int, _dp, _dp]
         L.hb_coarse_solve.argtypes = [_vp, C.c_int, _dp, _dp]
         L.hb_precond_apply.argtypes = [_vp, C.c_int, C.c_int, _dp, _dp]
+        L.hb_precond_apply_device.argtypes = [_vp, C.c_int, C.c_int, _vp, _vp]
         L.hb_precond_name.restype = C.c_char_p
         L.hb_precond_name.argtypes = [C.c_int]
         L.hb_precond_requires_flexible.argtypes = [_vp, C.c_int]
@@ -476,6 +478,11 @@ class Context:
         z = np.zeros_like(r)
         self._check(lib().hb_precond_apply(self.h, HB_PC[kind], B, _p(r), _p(z)))
         return z
+
+    def precond_apply_device(self, kind, dr: int, dz: int, nb: int):
+        """r, z: device pointers to complex64 [nb][ny][nx] (e.g. torch.complex64
+        tensors' data_ptr()); enqueued on the library stream, no synchronisation."""
+        self._check(lib().hb_precond_apply_device(self.h, HB_PC[kind], nb, C.c_void_p(dr), C.c_void_p(dz)))
 
     def fgmres(self, kind, B, cfg: KrylovConfig, X0=None, out=None):
         """out: optional preallocated (e.g. pinned) c128 array receiving X."""

@@ -1071,8 +1071,6 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_lean_legs = value != 0;
   else if (k == "conv_rows")
     ctx->opt_conv_rows = value != 0;
-  else if (k == "conv_rows_ring")
-    ctx->conv_rows_ring = value == 3 ? 3 : 4;
   else if (k == "stream_vcycle")
     ctx->opt_stream = value != 0;
   else if (k == "wgrad_blk")

@@ -8,22 +8,33 @@
 //   D_r[x, (ky, co)] = sum_ci X[r, x + kx - 1, ci] W[co, ci, ky, kx]   (N = 3*16)
 // and output row y is assembled in the epilogue from three row accumulators,
 //   out[y, x, co] = sum_ky D_{y+ky-1}[x, (ky, co)] + bias,
-// so an input row costs 3 kx x 2 k-steps x 2 MMAs of N = 96 / 48 per
-// 16-channel chunk (12 MMAs) instead of 36 MMAs per output tile, and is loaded
-// and split into tf32 hi/lo once instead of three times.  3xTF32 as in
-// hb_conv_tc.cu: D[:, 0:96] += A_hi [W_hi | W_lo], D[:, 48:96] += A_lo W_hi.
+// so an input row is loaded and split into tf32 hi/lo once instead of three
+// times, at 12-18 MMAs per 16-channel chunk instead of 36 per output tile.
+// 3xTF32 (A = A_hi + A_lo, W = W_hi + W_lo, A_lo W_lo dropped) in two layouts:
+//  * one CTA per SM (512 TMEM columns; layers whose weights need > ~75 KB of
+//    shared memory): split accumulators, D[:, 0:96] += A_hi [W_hi | W_lo],
+//    D[:, 48:96] += A_lo W_hi (two MMAs of N = 96 / 48 per k-step), a 3-4 row
+//    D ring of 96 columns, two 16-channel chunks per step;
+//  * two CTAs per SM (256 TMEM columns each; the 16-output-channel layers):
+//    ONE 48-column accumulator per row, D += A_hi W_hi + A_hi W_lo + A_lo W_hi
+//    (three N = 48 MMAs per k-step), a 3-row ring and one A slot.  Each CTA's
+//    row pipeline (TMA -> A build -> MMA -> epilogue) is latency-bound --
+//    per-role clock64 traces showed the stages handing over at ~1840 cycles
+//    per input row with the tensor pipe ~30% busy -- so two independent
+//    pipelines per SM raise throughput (16 -> 16 at 512^2 x 16: 228 -> 180 us).
 //
-// Persistent CTA (one per SM), 14 warps: w0 TMA producer (input rows, a
-// 16-channel (130 px) box per chunk, out-of-range pixels read zeros = the
-// padding) | w1 MMA issuer | w2..w9 A build (smem row -> TMEM hi/lo, three kx
-// shifts) | w10..w13 epilogue.  Work item = (image, 128-column strip, block of
-// rb output rows); it streams rb + 2 input rows.  Row accumulators live in a
-// TMEM ring; a D slot is released once the last output row using it is out.
+// Persistent CTAs, warps: w0 TMA producer (input rows, a 16-channel (130 px)
+// box per chunk, out-of-range pixels read zeros = the padding) | w1 MMA issuer
+// | 8 (one CTA) or 4 (two CTAs) A-build warps (smem row -> TMEM hi/lo, three
+// kx shifts) | 4 epilogue warps.  Work item = (image, 128-column strip, block
+// of rb output rows); it streams rb + 2 input rows.  Row accumulators live in
+// a TMEM ring; a D slot is released once the last output row using it is out.
 #include "hb_common.cuh"
 #include "hb_internal.h"
 #include "hb_tc_ptx.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -33,11 +44,23 @@ namespace {
 
 using namespace tcx;
 
-constexpr int CR_THREADS = 448;
+// NCTA resident CTAs per SM: 1 -> 14 warps (8 A-build warps), 512 TMEM columns;
+// 2 -> 10 warps (4 A-build warps), 256 TMEM columns each: two independent row
+// pipelines share the SM's tensor pipe (the layer is latency-bound per CTA)
+template <int NCTA>
+struct CrShape {
+  static constexpr int NAB = NCTA == 1 ? 8 : 4;  // A-build warps
+  static constexpr int THREADS = 32 * (2 + NAB + 4);
+  static constexpr int TMEM = NCTA == 1 ? 512 : 256;
+  // one CTA: split accumulators [main 48 | correction 48] per row (two MMAs of N = 96 / 48 per k-step);
+  // two CTAs: ONE 48-column accumulator per row (three N = 48 MMAs) so a 3-row ring + an A slot fit 256 columns
+  static constexpr bool SPLIT = NCTA == 1;
+  static constexpr int DW = SPLIT ? 96 : 48;
+};
 constexpr int CR_RBUF = 4;              // input rows in flight (smem ring)
 constexpr int CR_BOX = 9216;            // one 16-channel row box: 130 px x 64 B = 8320 B, 1024-aligned
 constexpr int CR_WBLK = 96 * 64;        // one (chunk, kx) weight block: 96 rows x 16 ch fp32
-constexpr int CR_MAXRING = 4;
+constexpr int CR_MAXRING = 6;
 
 struct CrParams {
   int B, H, W, relu;
@@ -54,7 +77,8 @@ struct CrParams {
   const int* act;
 };
 
-__global__ void __launch_bounds__(CR_THREADS, 1)
+template <int NCTA>
+__global__ void __launch_bounds__(CrShape<NCTA>::THREADS, NCTA)
     k_conv_rows(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, CrParams p) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   __shared__ uint64_t bar_rfull[CR_RBUF], bar_rempty[CR_RBUF];
@@ -71,14 +95,15 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
   const int strips = p.W / 128, rblocks = (p.H + p.rb - 1) / p.rb;
   const int nitems = p.nslice * p.B * strips * rblocks;
   const int aw = gch * 3 * 32;   // TMEM columns of one A slot: (chunk, kx) x [hi 16 | lo 16]
-  const int a0 = ring * 96;      // first A-slot column (D ring first)
+  constexpr int DW = CrShape<NCTA>::DW;
+  const int a0 = ring * DW;      // first A-slot column (D ring first)
   if (threadIdx.x == 0) {
     for (int i = 0; i < CR_RBUF; ++i) {
       mbar_init(&bar_rfull[i], 1);
-      mbar_init(&bar_rempty[i], 256);
+      mbar_init(&bar_rempty[i], 32 * CrShape<NCTA>::NAB);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_afull[i], 256);
+      mbar_init(&bar_afull[i], 32 * CrShape<NCTA>::NAB);
       mbar_init(&bar_aempty[i], 1);
     }
     for (int i = 0; i < CR_MAXRING; ++i) {
@@ -90,7 +115,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
-                 "r"(512));
+                 "r"(CrShape<NCTA>::TMEM));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -157,7 +182,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
       for (int r = y0 - 1; r <= y1; ++r, ++rs) {
         const int ds = rs % ring;
         if (rs >= ring) mbar_wait(&bar_dempty[ds], ((rs / ring) - 1) & 1);  // epilogue released this slot
-        const uint32_t d = tbase + uint32_t(ds * 96);
+        const uint32_t d = tbase + uint32_t(ds * DW);
         uint32_t first = 0;
         for (int g = 0; g < ngrp; ++g, ++s) {
           const int as = s % na;
@@ -171,8 +196,14 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
               const uint32_t ta = tbase + uint32_t(a0 + as * aw + u * 32);
 #pragma unroll
               for (int kk = 0; kk < 2; ++kk) {
-                umma_ts(d, ta + 8 * kk, lw + 2 * kk, hi16, id96, first);            // A_hi [W_hi | W_lo]
-                umma_ts(d + 48, ta + 16 + 8 * kk, lw + 2 * kk, hi16, id48, 1u);   // A_lo W_hi -> correction
+                if (CrShape<NCTA>::SPLIT) {
+                  umma_ts(d, ta + 8 * kk, lw + 2 * kk, hi16, id96, first);            // A_hi [W_hi | W_lo]
+                  umma_ts(d + 48, ta + 16 + 8 * kk, lw + 2 * kk, hi16, id48, 1u);   // A_lo W_hi -> correction
+                } else {
+                  umma_ts(d, ta + 8 * kk, lw + 2 * kk, hi16, id48, first);                // A_hi W_hi
+                  umma_ts(d, ta + 8 * kk, lw + 2 * kk + (48 * 64 >> 4), hi16, id48, 1u);  // A_hi W_lo (rows 48..95)
+                  umma_ts(d, ta + 16 + 8 * kk, lw + 2 * kk, hi16, id48, 1u);             // A_lo W_hi
+                }
                 first = 1;
               }
             }
@@ -182,8 +213,9 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
         umma_commit_elect(&bar_dfull[ds]);
       }
     }
-  } else if (warp < 10) {
+  } else if (warp < 2 + CrShape<NCTA>::NAB) {
     // ---------------- A build: input row (3 kx shifts x chunks) -> TMEM [hi | lo]
+    constexpr int NG = CrShape<NCTA>::NAB / 4;  // A-build groups (4 warps = the TMEM lane quarters)
     const int q = warp & 3, half = (warp - 2) >> 2;
     const int pix = 32 * q + lane;
     int s = 0;
@@ -200,7 +232,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
         if (r >= 0 && r < p.H) {
           const uint32_t ta = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(a0 + as * aw);
           const int nu = (min(nch, (g + 1) * gch) - g * gch) * 3;
-          for (int u = half; u < nu; u += 2) {
+          for (int u = half; u < nu; u += NG) {
             const int ch = u / 3, kx = u - 3 * ch;  // chunk within this step's group
             const int hp = pix + kx;  // halo pixel (the box starts at x0 - 1)
             const unsigned char* row = base + rb_ * rowbuf + ch * CR_BOX + hp * 64;
@@ -247,17 +279,35 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
         float o[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) o[i] = __ldg(p.bias + sl * 16 + i);
+        if (CrShape<NCTA>::SPLIT) {
 #pragma unroll
-        for (int ky = 0; ky < 3; ++ky) {
-          const int rr = y + ky - 1;
-          if (rr < 0 || rr >= p.H) continue;  // zero padding row: no accumulator
-          const uint32_t dcol = uint32_t(((sb + j + ky) % ring) * 96 + ky * 16);
-          uint32_t v[16], u[16];
-          tmem_ld16(trow + dcol, v);
-          tmem_ld16(trow + dcol + 48, u);
+          for (int ky = 0; ky < 3; ++ky) {
+            const int rr = y + ky - 1;
+            if (rr < 0 || rr >= p.H) continue;  // zero padding row: no accumulator
+            const uint32_t dcol = uint32_t(((sb + j + ky) % ring) * DW + ky * 16);
+            uint32_t v[16], u[16];
+            tmem_ld16(trow + dcol, v);
+            tmem_ld16(trow + dcol + 48, u);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] += __uint_as_float(v[i]) + __uint_as_float(u[i]);
+          }
+        } else {
+          uint32_t v[3][16];
+#pragma unroll
+          for (int ky = 0; ky < 3; ++ky) {
+            const int rr = y + ky - 1;
+            if (rr < 0 || rr >= p.H) {  // zero padding row: no accumulator
+#pragma unroll
+              for (int i = 0; i < 16; ++i) v[ky][i] = 0u;
+              continue;
+            }
+            tmem_ld16(trow + uint32_t(((sb + j + ky) % ring) * DW + ky * 16), v[ky]);
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 16; ++i) o[i] += __uint_as_float(v[i]) + __uint_as_float(u[i]);
+          for (int i = 0; i < 16; ++i)
+            o[i] += __uint_as_float(v[0][i]) + __uint_as_float(v[1][i]) + __uint_as_float(v[2][i]);
         }
         if (p.relu) {
 #pragma unroll
@@ -280,7 +330,7 @@ __global__ void __launch_bounds__(CR_THREADS, 1)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(CrShape<NCTA>::TMEM));
   }
 }
 
@@ -337,35 +387,51 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
   p.b_is_ctx = b_ctx ? 1 : 0;
   p.nch = cw.cin / 16;
   p.nslice = cw.cout / 16;
-  p.gch = p.nch == 1 ? 1 : 2;
-  p.ring = p.gch == 1 ? c.conv_rows_ring : 3;
-  p.na = (p.ring * 96 + 2 * p.gch * 96 <= 512) ? 2 : 1;
+  const size_t wbytes = size_t(p.nslice) * p.nch * 3 * CR_WBLK;
+  // two CTAs per SM when both fit the shared memory (112 KB each): 256 TMEM
+  // columns each -> single accumulators, one chunk per step, one A slot, a
+  // 3-row D ring; else one CTA with split accumulators (HB_CR_NCTA: force)
+  static const int env_n = getenv("HB_CR_NCTA") ? atoi(getenv("HB_CR_NCTA")) : 0;
+  const bool two = env_n ? env_n == 2 : (size_t(3) * CR_BOX + wbytes + 1024 <= 112 * 1024);
+  if (two) {
+    p.gch = 1;
+    p.na = 1;
+    p.ring = 3;
+  } else {
+    p.gch = p.nch == 1 ? 1 : 2;
+    p.ring = p.gch == 1 ? 4 : 3;
+    p.na = (p.ring * 96 + 2 * p.gch * 96 <= 512) ? 2 : 1;
+  }
   const int strips = W / 128;
   // rows per work item: enough items for ~2 per SM, each >= 4 rows (halo: 2 extra input rows)
-  p.rb = std::max(4, std::min(32, (cw.cout / 16 * B * strips * H) / std::max(1, 2 * c.num_sms)));
+  p.rb = std::max(4, std::min(32, (cw.cout / 16 * B * strips * H) / std::max(1, (two ? 4 : 2) * c.num_sms)));
   p.wrow = cw.dwrow.p;
   p.bias = cw.db.p;
   p.out = out;
   p.act = act;
   const CUtensorMap mA = act_map(a, B, H, W, ca, 16, 130, 1);
   const CUtensorMap mB = cb ? act_map(bsrc, b_ctx ? 1 : B, H, W, cb, 16, 130, 1) : mA;
-  const size_t wbytes = size_t(p.nslice) * p.nch * 3 * CR_WBLK;
+  const size_t cap = two ? 112 * 1024 : 200 * 1024;
   p.rbuf = CR_RBUF;
-  while (p.rbuf > 2 && size_t(p.rbuf) * p.gch * CR_BOX + wbytes + 1024 > 200 * 1024) --p.rbuf;
+  while (p.rbuf > 2 && size_t(p.rbuf) * p.gch * CR_BOX + wbytes + 1024 > cap) --p.rbuf;
   const size_t smem = size_t(p.rbuf) * p.gch * CR_BOX + wbytes + 1024;
-  if (smem > 200 * 1024) return false;
+  if (smem > cap) return false;
   static int attr_dev = -1;
   if (attr_dev != c.device) {
-    HB_CUDA(cudaFuncSetAttribute(k_conv_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HB_CUDA(cudaFuncSetAttribute(k_conv_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    HB_CUDA(cudaFuncSetAttribute(k_conv_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 112 * 1024));
     attr_dev = c.device;
   }
   const int items = p.nslice * B * strips * ((H + p.rb - 1) / p.rb);
-  const int grid = std::min(items, c.num_sms);
+  const int grid = std::min(items, (two ? 2 : 1) * c.num_sms);
   const int tok = prof_begin(c, PC_CONV);
   if (c.prof_detail)
     c.prof_label = "conv_rows " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
-  launch_pdl(c, k_conv_rows, dim3(grid), dim3(CR_THREADS), smem, mA, mB, p);
+  if (two)
+    launch_pdl(c, k_conv_rows<2>, dim3(grid), dim3(CrShape<2>::THREADS), smem, mA, mB, p);
+  else
+    launch_pdl(c, k_conv_rows<1>, dim3(grid), dim3(CrShape<1>::THREADS), smem, mA, mB, p);
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());
   return true;

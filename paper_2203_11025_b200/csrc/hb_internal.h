@@ -351,7 +351,6 @@ struct Context {
   int dbg_skip = 0;  // diagnostics only (tools/debug/c0_marginal.py): skip kernel classes, results invalid
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size
   int opt_legs_wd = 2;  // Jacobi factor in the legs: 0 stored wD^-1, 1 from D, 2 by working-set size
-  int conv_rows_ring = 4;
   // captured FGMRES cycle graphs
   struct GraphEntry {
     unsigned long long gen;

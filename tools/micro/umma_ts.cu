@@ -65,9 +65,9 @@ int main() {
   long long* d; cudaMalloc(&d, 16);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   const char* names[3] = {"TS same-N", "TS ncat", "SS ncat"};
-  for (int aoff : {64, 128, 256})
-  for (int mode = 0; mode < 2; ++mode)
-    for (int n : {16, 64}) {
+  for (int aoff : {256})
+  for (int mode = 0; mode < 3; ++mode)
+    for (int n : {16, 48, 64, 128}) {
       const int iters = 512;
       long long h[2];
       for (int rep = 0; rep < 2; ++rep) {

@@ -622,6 +622,10 @@ __global__ void __launch_bounds__(KT) k_add_to_x(FineView F, const int* fin, con
 }
 
 // y = R^-1 g (back-substitution, inc/krylov.hpp:119-126); x += sum_i y_i Z_i
+// KM: the largest k of the instantiation; all k basis loads of a node are
+// issued before its fp64 FMAs (the rolled loop serialised one load round trip
+// per Z_i: 43% of HBM at c0)
+template <int KM>
 __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st, const float2* __restrict__ Z,
                                                  double2* __restrict__ x) {
   pdl_enter();
@@ -634,12 +638,17 @@ __global__ void __launch_bounds__(KT) k_finalize(FineView F, int B, ColState* st
   solve_small(S, k, sH, y);
   const size_t NS = F.ns(), N = F.nown(), OFF = F.off();
   const size_t BN = size_t(B) * NS;
+  const float2* zb = Z + b * NS + OFF;
   for (size_t p = size_t(blockIdx.x) * KT + threadIdx.x; p < N; p += size_t(gridDim.x) * KT) {
+    float2 z[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) z[i] = i < k ? ld(zb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
     double2 acc = x[b * NS + OFF + p];
-    for (int i = 0; i < k; ++i) {
-      const float2 z = ld(Z + size_t(i) * BN + b * NS + OFF, p);
-      acc.x += y[i].x * double(z.x) - y[i].y * double(z.y);
-      acc.y += y[i].x * double(z.y) + y[i].y * double(z.x);
+#pragma unroll
+    for (int i = 0; i < KM; ++i) {
+      if (i >= k) break;
+      acc.x += y[i].x * double(z[i].x) - y[i].y * double(z[i].y);
+      acc.y += y[i].x * double(z[i].y) + y[i].y * double(z[i].x);
     }
     x[b * NS + OFF + p] = acc;
   }
@@ -911,11 +920,16 @@ void launch_fg_update_finish(Context& c, int B, int j, int m, const double2* gsu
 }
 
 void launch_fg_finalize(Context& c, int B, int m, const float2* Z, double2* x) {
-  (void)m;
   const size_t N = owned_nodes(c);
   const int nb = std::max(1, std::min<int>(int((N + KT - 1) / KT), 4 * c.num_sms / std::max(1, B)));
   KScope ks(c, PC_KRYLOV_FINAL, double(B) * N * (32.0 + 8.0 * m));  // x (c128) in+out, Z_0..Z_{k-1} in (upper bound k = m)
-  launch_pdl(c, k_finalize, dim3(nb, B), dim3(KT), 0, fine_view(c), B, reinterpret_cast<ColState*>(c.kstate.p), Z, x);
+  auto* st = reinterpret_cast<ColState*>(c.kstate.p);
+  if (m <= 10)
+    launch_pdl(c, k_finalize<10>, dim3(nb, B), dim3(KT), 0, fine_view(c), B, st, Z, x);
+  else if (m <= 20)
+    launch_pdl(c, k_finalize<20>, dim3(nb, B), dim3(KT), 0, fine_view(c), B, st, Z, x);
+  else
+    launch_pdl(c, k_finalize<kMaxRestart>, dim3(nb, B), dim3(KT), 0, fine_view(c), B, st, Z, x);
   HB_CUDA(cudaGetLastError());
 }
 

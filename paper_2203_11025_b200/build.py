@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libhelmgpu.so")
-SOURCES = ["hb_api.cu", "hb_mg.cu", "hb_mg_fused.cu", "hb_mg_stream.cu", "hb_mg_staged.cu", "hb_coarse_small.cu", "hb_coarse_cluster.cu", "hb_krylov.cu", "hb_block.cu", "hb_net.cu",
+SOURCES = ["hb_api.cu", "hb_mg.cu", "hb_mg_fused.cu", "hb_mg_stream.cu", "hb_mg_staged.cu", "hb_mg_rowwarp.cu", "hb_coarse_small.cu", "hb_coarse_cluster.cu", "hb_krylov.cu", "hb_block.cu", "hb_net.cu",
            "hb_conv_tc.cu", "hb_conv_rows.cu", "hb_slab.cu", "hb_paper.cu", "hb_train.cu", "hb_datagen.cu", "hb_host.cpp"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-fvisibility=hidden", "-shared", "-ldl"]

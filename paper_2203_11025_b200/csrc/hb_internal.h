@@ -156,6 +156,11 @@ void launch_coarse_gmres(Context& c, const LevelView& L, int iters, int B, const
 // coarsest GMRES(iters) with D^-1 on the multi-CTA Krylov kernels (hb_krylov.cu), large coarse grids
 void coarse_krylov_solve(Context& c, const Level& L, int iters, int B, int slot, const float2* f, float2* x);
 // register-resident variant for <= 1024-node coarse grids, iters <= 10 (hb_coarse_small.cu); false if not applicable
+// full-row-warp V-cycle legs for 64 / 128-wide whole-grid levels (hb_mg_rowwarp.cu); false: not applicable
+bool launch_down_row(Context& c, const LevelView& L, float damping, int offset, int B, const int* act,
+                     const float2* f, const float* fscale, float2* fc);
+bool launch_up_row(Context& c, const LevelView& L, float damping, int offset, int B, const int* act, const float2* f,
+                   const float* fscale, const float2* vc, float2* z);
 bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const int* act, const float2* f,
                          float2* x);
 // fused down/up legs (nu1 = nu2 = 1)
@@ -346,7 +351,7 @@ struct Context {
   // options
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
-       opt_coarse_reg = true,
+       opt_coarse_reg = true, opt_row_legs = true,
        opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_coarse_cluster = true, opt_basis_wave = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
   int dbg_skip = 0;  // diagnostics only (tools/debug/c0_marginal.py): skip kernel classes, results invalid
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size

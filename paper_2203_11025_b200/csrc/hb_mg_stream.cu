@@ -632,7 +632,9 @@ void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float 
   if (env_d) rpc = env_d;
   const int chunks = (cny + rpc - 1) / rpc;
   const bool wd = legs_wd(c, L, B), even = (offset & 1) == 0;
-  if (staged) {
+  if (!e0 && !slab && launch_down_row(c, L, damping, offset, B, act, f, fscale, fc)) {
+    // full-row warps (hb_mg_rowwarp.cu: 64 / 128-wide levels)
+  } else if (staged) {
     launch_down_staged(c, L, cw, damping, offset, B, act, f, fscale, e0, wd, fc, vpre);
   } else if (e0) {
     const dim3 grid((cnx + SWE_DOWN - 1) / SWE_DOWN, (chunks + WARPS - 1) / WARPS, B);
@@ -671,7 +673,9 @@ void launch_up_stream(Context& c, const LevelView& L, float damping, int offset,
   const dim3 grid((cnx + SW_OUT - 1) / SW_OUT, (chunks + WARPS - 1) / WARPS, B);
   const bool slab = L.w.rows != L.ny || L.w.lo != 0 || L.w.hi != L.ny || cw.rows != cny || cw.row0 != 0;
   const bool wd = legs_wd(c, L, B), even = (offset & 1) == 0;
-  if (legs_staged(c, L, B)) {
+  if (!e0 && !slab && launch_up_row(c, L, damping, offset, B, act, f, fscale, vc, z)) {
+    // full-row warps (hb_mg_rowwarp.cu: 64 / 128-wide levels)
+  } else if (legs_staged(c, L, B)) {
     launch_up_staged(c, L, damping, offset, cnx, cny, cw, B, act, f, fscale, e0, vc, wd, z, vpre);
   } else if (e0 && slab) {
     throw HbError{HB_ERR_ARG, "register-prefetch legs from an initial guess run on whole grids only"};

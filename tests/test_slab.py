@@ -193,7 +193,7 @@ def test_slab_precond_equals_whole_c0(hgm, k, staged):
     from oracle import oracle as O
     n = 128
     k2, g, om = _problem(n)
-    opts = (("staged_legs", staged), ("legs_wd", staged % 2))
+    opts = (("staged_legs", staged), ("legs_wd", staged % 2), ("row_legs", 0))  # the strip legs on both sides
     whole = _ctx(hgm, k2, g, om, 3, "gmres", opts=opts)
     cs = _group(hgm, k2, g, om, 3, "gmres", k, opts=opts)
     assert cs[0].slab_rows() == (0, n)
@@ -247,8 +247,9 @@ def test_slab_c4_shape(hgm, coarse):
     n = 256
     k2, g, om = _problem(n)
     seed = 11 if coarse == "net" else None
-    whole = _ctx(hgm, k2, g, om, 4, coarse, net_seed=seed)
-    cs = _group(hgm, k2, g, om, 4, coarse, 2, net_seed=seed)
+    opts = (("row_legs", 0),)  # the strip legs on both sides (the full-row legs serve whole narrow grids only)
+    whole = _ctx(hgm, k2, g, om, 4, coarse, net_seed=seed, opts=opts)
+    cs = _group(hgm, k2, g, om, 4, coarse, 2, net_seed=seed, opts=opts)
     r = O.random_complex_normal(8, (1, n, n))
     zw = whole.precond_apply("v", r)
     zs = cs[0].precond_apply_slab("v", r)

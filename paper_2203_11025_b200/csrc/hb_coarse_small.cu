@@ -370,7 +370,10 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
     if (tr && j < 16) tr[j * 8 + 3] = clock64();
     // scalar phase on warp 0 only (the fp64 work and its smem reads are not
     // repeated by every warp); results go through smem behind one barrier
-    if (warp == 0) coarse_scalar_phase<NT / 32, MAXK>(S, sHc, sGj, j, m, one, hn_prev, lane);
+    if (warp == 0)
+      coarse_scalar_phase<NT / 32, MAXK>(S, sHc, sGj, j, m, one, hn_prev, lane);
+    else if (warp == NT / 32 - 1 && j >= 1)  // idle during the scalar phase: Givens of column j-1
+      coarse_givens_col<NT / 32>(S, j, one, lane);
     __syncthreads();
     if (S.stop) {
       k = S.k;
@@ -413,7 +416,7 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const 
   }
   __syncthreads();
   if (tr) tr[11 * 8 + 0] = clock64();
-  if (warp == 0) coarse_lsq_warp<MAXK>(S, k, lane);
+  if (warp == 0) coarse_backsub_warp<MAXK>(S, k, lane);
   if (t == 0) {
     if (tr) tr[11 * 8 + 1] = clock64();
   }
@@ -488,10 +491,7 @@ bool launch_coarse_small(Context& c, const LevelView& L, int iters, int B, const
                 h[j * 8 + 6] - h[j * 8]);
       fprintf(stderr, "  total %lld, least squares %lld, barrier %lld, x %lld (cycles)\n", h[88 + 2] - h[0],
               h[89] - h[88], h[91] - h[89], h[90] - h[91]);
-      for (int j = 0; j < iters && j < 16; ++j) fprintf(stderr, " %lld", h[j * 8 + 7] - h[j * 8 + 3]);
-      fprintf(stderr, " <- bar1 to pre-MGS\n");
-      for (int j = 0; j <= iters && j < 16; ++j) fprintf(stderr, " %lld/%lld", h[96 + j] - h[j * 8 + 3], h[112 + j] - h[j * 8 + 3]);
-      fprintf(stderr, " <- bar1 to fold done / rsqrt done\n");
+
     }
   }
   return true;

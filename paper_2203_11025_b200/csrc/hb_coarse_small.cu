@@ -13,6 +13,11 @@
 
 #include "hb_coarse_common.cuh"
 
+#ifndef HB_CREG_MINB
+#define HB_CREG_MINB 2  // resident CTAs per SM asked of k_coarse_reg: 2 (<= 128 registers; ~0.5 KB of spills,
+                        // measured 3% faster at c0 x 444 than one CTA at 228 registers)
+#endif
+
 namespace hb {
 
 __device__ long long* g_coarse_trace = nullptr;
@@ -272,7 +277,7 @@ __global__ void __launch_bounds__(NT, 1) k_coarse_small(LevelView L, int m, cons
 // summation order as k_coarse_small (the MGS correction is fed from per-warp
 // smem broadcasts instead of double-precision shuffles).
 template <int NT, int NPT, int MAXK>
-__global__ void __launch_bounds__(NT, 1) k_coarse_reg(LevelView L, int m, const int* act,
+__global__ void __launch_bounds__(NT, HB_CREG_MINB) k_coarse_reg(LevelView L, int m, const int* act,
                                                        const float2* __restrict__ f, float2* __restrict__ x) {
   pdl_enter();
   const int b = blockIdx.x;

@@ -77,6 +77,32 @@ struct FineView {
 // slab receives the same bits, so the replicated Hessenberg / Givens / flags
 // stay identical across slabs.
 
+// Fold the per-CTA partials of column b in its last CTA with every warp at
+// once: warp w takes values w, w + 8, ...; lane l sums CTAs l, l + 32, ... in
+// order (L2 loads, independent), then a fixed xor butterfly -- deterministic.
+// (A serial loop of nblk dependent L2 round trips per value cost ~150 us at
+// the end of every Krylov launch at c4, where one column has 592 CTAs.)
+__device__ __forceinline__ void fold_parts2(const double2* part, int b, int nblk, int nv, double2* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = warp; t < nv; t += KT / 32) {
+    double2 s = make_double2(0.0, 0.0);
+    for (int q = lane; q < nblk; q += 32) {
+      const double2 v = __ldcg(part + (size_t(b) * nblk + q) * KMAXV + t);
+      s.x += v.x;
+      s.y += v.y;
+    }
+    s = warp_sum2(s);
+    if (lane == 0) out[t] = s;
+  }
+}
+// the same for one double per CTA (part[b][nblk]); warp 0 only, result in lane 0 (all lanes)
+__device__ __forceinline__ double fold_parts1(const double* part, int b, int nblk) {
+  const int lane = threadIdx.x & 31;
+  double s = 0.0;
+  for (int q = lane; q < nblk; q += 32) s += __ldcg(part + size_t(b) * nblk + q);
+  return warp_sum(s);
+}
+
 // last CTA of column b? (classic threadfence + ticket pattern; resets the ticket)
 __device__ bool last_cta(unsigned* ticket, int b, int nblk) {
   __shared__ bool is_last;
@@ -143,9 +169,9 @@ __global__ void __launch_bounds__(KT) k_restart(FineView F, int B, ColState* st,
     part[size_t(b) * gridDim.x + blockIdx.x] = t;
   }
   if (!last_cta(ticket, b, gridDim.x)) return;
+  if (threadIdx.x >= 32) return;
+  const double t = fold_parts1(part, b, gridDim.x);
   if (threadIdx.x != 0) return;
-  double t = 0.0;
-  for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
   if (gsum) {
     gsum[size_t(b) * KMAXV] = make_double2(t, 0.0);
     return;
@@ -313,18 +339,12 @@ __global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState
   cta_reduce_acc(acc, 2 * nv, sred, reinterpret_cast<double*>(red));
   for (int t = threadIdx.x; t < nv; t += KT) part[(size_t(b) * gridDim.x + blockIdx.x) * KMAXV + t] = red[t];
   if (!last_cta(ticket, b, gridDim.x)) return;
-  for (int t = threadIdx.x; t < nv; t += KT) {
-    double2 s = make_double2(0.0, 0.0);
-    for (unsigned q = 0; q < gridDim.x; ++q) {
-      const volatile double2* pp = part + (size_t(b) * gridDim.x + q) * KMAXV + t;
-      s.x += pp->x;
-      s.y += pp->y;
-    }
-    red[t] = s;
-    if (gsum) gsum[size_t(b) * KMAXV + t] = s;
-  }
-  if (gsum) return;
+  fold_parts2(part, b, gridDim.x, nv, red);
   __syncthreads();
+  if (gsum) {
+    for (int t = threadIdx.x; t < nv; t += KT) gsum[size_t(b) * KMAXV + t] = red[t];
+    return;
+  }
   adots_scalar(st[b], j, red);
 }
 
@@ -444,18 +464,12 @@ __global__ void __launch_bounds__(KT) k_update(FineView F, int B, int j, int m, 
   }
   for (int t = threadIdx.x; t < ng; t += KT) myp[1 + t] = red[t];
   if (!last_cta(ticket, b, gridDim.x)) return;
-  for (int t = threadIdx.x; t <= ng; t += KT) {
-    double2 s2 = make_double2(0.0, 0.0);
-    for (unsigned q = 0; q < gridDim.x; ++q) {
-      const volatile double2* pp = part + (size_t(b) * gridDim.x + q) * KMAXV + t;
-      s2.x += pp->x;
-      s2.y += pp->y;
-    }
-    red[t] = s2;
-    if (gsum) gsum[size_t(b) * KMAXV + t] = s2;
-  }
-  if (gsum) return;
+  fold_parts2(part, b, gridDim.x, ng + 1, red);
   __syncthreads();
+  if (gsum) {
+    for (int t = threadIdx.x; t <= ng; t += KT) gsum[size_t(b) * KMAXV + t] = red[t];
+    return;
+  }
   if (threadIdx.x >= 32) return;
   update_scalar(S, b, j, m, red[0].x, gram ? red + 1 : nullptr, act, hist, hist_cap, rel_tol, max_iters, scale_out);
 }
@@ -679,9 +693,9 @@ __global__ void __launch_bounds__(KT) k_coarse_restart(FineView F, int B, ColSta
     part[size_t(b) * gridDim.x + blockIdx.x] = t;
   }
   if (!last_cta(ticket, b, gridDim.x)) return;
+  if (threadIdx.x >= 32) return;
+  const double t = fold_parts1(part, b, gridDim.x);
   if (threadIdx.x != 0) return;
-  double t = 0.0;
-  for (unsigned q = 0; q < gridDim.x; ++q) t += ((volatile double*)part)[size_t(b) * gridDim.x + q];
   restart_scalar(S, b, t, hist, hist_cap, 1e-300, max_iters, act, scale_out, count);
 }
 

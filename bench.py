@@ -929,7 +929,7 @@ def slab_budget(local, args, ws, rank):
            "rows_per_slab": hi - lo if ws > 1 else cfg["n"] // 2,
            "ms_per_iteration": (t2 - t1) / (b2 - b1), "iterations": [b1, b2],
            "rel_residual_end": round(float(rep.residual_history[0][-1] / rep.residual_history[0][0]), 6),
-           "note": "coarsest level all-gathered and solved replicated; 2 ghost rows per slab level"}
+           "note": "coarsest level all-gathered and solved replicated (NCCL ranks: every rank; in-process group on one GPU: once, solution copied to the other slabs); 2 ghost rows per slab level"}
     for c in ctxs:
         c.close()
     return out

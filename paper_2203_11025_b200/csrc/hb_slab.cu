@@ -249,7 +249,8 @@ static void halo(std::vector<Context*>& S, int l, int B, size_t esz, FieldFn fld
 }
 
 // whole coarsest-level field (B columns) on every slab from the owned rows
-static void gather_coarse(std::vector<Context*>& S, int B, FieldFn fld) {
+// (to0: in-process group, assemble it on slab 0 only -- see slab_vcycle)
+static void gather_coarse(std::vector<Context*>& S, int B, FieldFn fld, bool to0 = false) {
   SlabState& st = *S[0]->slab;
   const int l = int(S[0]->levels.size()) - 1;
   const Level& C = *S[0]->levels[size_t(l)];
@@ -261,7 +262,7 @@ static void gather_coarse(std::vector<Context*>& S, int B, FieldFn fld) {
       const Level& Ls = *src.levels[size_t(l)];
       const size_t width = size_t(Ls.hi - Ls.lo) * Ls.nx * esz;
       for (int t = 0; t < R; ++t) {
-        if (t == r) continue;
+        if (t == r || (to0 && t != 0)) continue;
         Context& dst = *S[size_t(t)];
         HB_CUDA(cudaMemcpy2DAsync(rowptr(dst, l, fld(dst, l, 0), esz, Ls.lo), cs,
                                   rowptr(src, l, fld(src, l, 0), esz, Ls.lo), cs, width, size_t(B),
@@ -324,12 +325,25 @@ static void slab_vcycle(std::vector<Context*>& S, int B, const std::vector<const
     if (l + 1 < nl - 1)
       halo(S, l + 1, B, sizeof(float2), f_level, 0);
     else
-      gather_coarse(S, B, f_level);
+      gather_coarse(S, B, f_level, S[0]->slab->group != nullptr);
   }
-  for (size_t s = 0; s < S.size(); ++s) {
-    Context& c = *S[s];
-    Level& C = *c.levels.back();
-    coarsest_solve(c, B, 0, act[s], C.f.p, C.x.p);
+  if (S[0]->slab->group != nullptr) {
+    // in-process group (all slabs on one device and stream): the replicated
+    // coarsest solve -- identical inputs, deterministic kernels, identical bits
+    // on every slab -- runs once on slab 0 and its solution is copied to the
+    // others (with one GPU per slab every rank solves it concurrently instead)
+    Context& c0 = *S[0];
+    Level& C0 = *c0.levels.back();
+    coarsest_solve(c0, B, 0, act[0], C0.f.p, C0.x.p);
+    for (size_t s = 1; s < S.size(); ++s)
+      HB_CUDA(cudaMemcpyAsync(S[s]->levels.back()->x.p, C0.x.p, sizeof(float2) * C0.N() * size_t(B),
+                              cudaMemcpyDeviceToDevice, c0.stream));
+  } else {
+    for (size_t s = 0; s < S.size(); ++s) {
+      Context& c = *S[s];
+      Level& C = *c.levels.back();
+      coarsest_solve(c, B, 0, act[s], C.f.p, C.x.p);
+    }
   }
   for (int l = nl - 2; l >= 0; --l) {
     if (l + 1 < nl - 1) halo(S, l + 1, B, sizeof(float2), x_level, 0);

@@ -64,6 +64,7 @@ constexpr int CR_MAXRING = 6;
 
 struct CrParams {
   int B, H, W, relu;
+  int ldo;               // output pixel stride (floats): the layer's cout (a launch may cover one 16-channel slice)
   int ca, cb, b_is_ctx;  // source channels (multiples of 16)
   int nch;               // (ca + cb) / 16 input chunks
   int nslice;            // cout / 16 output slices (one work item each)
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(CrShape<NCTA>::THREADS, NCTA)
     const int q = warp & 3;
     const int pix = 32 * q + lane;
     const uint32_t trow = tmem_base + (uint32_t(32 * q) << 16);
-    const int cout = p.nslice * 16;
+    const int cout = p.ldo;
     int sb = 0;  // step of the item's first input row
     for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
       int b, x0, y0, y1;
@@ -340,7 +341,7 @@ __global__ void __launch_bounds__(CrShape<NCTA>::THREADS, NCTA)
 // rows (part, ky, co), part 0 = W_hi, 1 = W_lo (tf32 round-to-nearest split),
 // stored pre-swizzled (SWIZZLE_64B) so a linear bulk copy lands in UMMA layout
 void conv_rows_prepare(ConvW& cw) {
-  if (cw.cout % 16 || cw.cout > 32 || cw.cin % 16 || cw.cin > 64) return;
+  if (cw.cout % 16 || cw.cout > 32 || cw.cin % 16 || cw.cin > 128) return;
   const int nch = cw.cin / 16, nsl = cw.cout / 16;
   std::vector<float> pk(size_t(nsl) * nch * 3 * 96 * 16, 0.f);
   auto tf32 = [](float x) {
@@ -375,7 +376,7 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
                       const float* bsrc, int cb, bool b_ctx, int relu, float* out) {
   if (!c.opt_conv_rows || !c.opt_tc_conv) return false;
   if (cw.cout % 16 || cw.cout > 32 || !cw.dwrow.p || W % 128 || ca % 16 || cb % 16 || ca + cb != cw.cin ||
-      cw.cin > 64)
+      cw.cin > 128)
     return false;
   CrParams p{};
   p.B = B;
@@ -386,8 +387,15 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
   p.cb = cb;
   p.b_is_ctx = b_ctx ? 1 : 0;
   p.nch = cw.cin / 16;
-  p.nslice = cw.cout / 16;
-  const size_t wbytes = size_t(p.nslice) * p.nch * 3 * CR_WBLK;
+  p.ldo = cw.cout;
+  const size_t wslice = size_t(p.nch) * 3 * CR_WBLK;  // weights of one 16-channel output slice
+  const int nsl_all = cw.cout / 16;
+  // all output slices in one launch when their weights fit beside the row ring;
+  // else (wide inputs, e.g. c3's 64 + 16 context -> 32) one launch per slice,
+  // each holding only its slice's weights
+  const bool per_slice = size_t(2) * CR_BOX * 2 + wslice * nsl_all + 1024 > 200 * 1024;
+  p.nslice = per_slice ? 1 : nsl_all;
+  const size_t wbytes = wslice * p.nslice;
   // two CTAs per SM when both fit the shared memory (112 KB each): 256 TMEM
   // columns each -> single accumulators, one chunk per step, one A slot, a
   // 3-row D ring; else one CTA with split accumulators (HB_CR_NCTA: force)
@@ -404,10 +412,7 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
   }
   const int strips = W / 128;
   // rows per work item: enough items for ~2 per SM, each >= 4 rows (halo: 2 extra input rows)
-  p.rb = std::max(4, std::min(32, (cw.cout / 16 * B * strips * H) / std::max(1, (two ? 4 : 2) * c.num_sms)));
-  p.wrow = cw.dwrow.p;
-  p.bias = cw.db.p;
-  p.out = out;
+  p.rb = std::max(4, std::min(32, (p.nslice * B * strips * H) / std::max(1, (two ? 4 : 2) * c.num_sms)));
   p.act = act;
   const CUtensorMap mA = act_map(a, B, H, W, ca, 16, 130, 1);
   const CUtensorMap mB = cb ? act_map(bsrc, b_ctx ? 1 : B, H, W, cb, 16, 130, 1) : mA;
@@ -428,10 +433,15 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
   if (c.prof_detail)
     c.prof_label = "conv_rows " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout);
-  if (two)
-    launch_pdl(c, k_conv_rows<2>, dim3(grid), dim3(CrShape<2>::THREADS), smem, mA, mB, p);
-  else
-    launch_pdl(c, k_conv_rows<1>, dim3(grid), dim3(CrShape<1>::THREADS), smem, mA, mB, p);
+  for (int s = 0; s < (per_slice ? nsl_all : 1); ++s) {
+    p.wrow = cw.dwrow.p + size_t(s) * wslice / sizeof(float);
+    p.bias = cw.db.p + 16 * s;
+    p.out = out + 16 * s;
+    if (two)
+      launch_pdl(c, k_conv_rows<2>, dim3(grid), dim3(CrShape<2>::THREADS), smem, mA, mB, p);
+    else
+      launch_pdl(c, k_conv_rows<1>, dim3(grid), dim3(CrShape<1>::THREADS), smem, mA, mB, p);
+  }
   prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
   HB_CUDA(cudaGetLastError());
   return true;

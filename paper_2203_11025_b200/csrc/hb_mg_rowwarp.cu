@@ -24,6 +24,9 @@ namespace hb {
 namespace {
 
 constexpr int RW_WARPS = 4;  // warps per CTA (independent row chunks)
+#ifndef HB_ROW_MINB
+#define HB_ROW_MINB 1
+#endif
 
 __device__ __forceinline__ float2 wfrom_d(float2 d, float damping) {  // damping / d (fast reciprocal)
   const float m = fmaf(d.x, d.x, d.y * d.y);
@@ -85,7 +88,7 @@ __device__ __forceinline__ void residual_row(const FRow<NPL>& u, const float2 (&
 // down leg: grid (ceil(coarse row chunks / RW_WARPS), B), block 32 x RW_WARPS;
 // warp = coarse rows [jy0, jy0 + rpc) of one column, all cnx = 16 NPL coarse columns
 template <int NPL, int O>
-__global__ void __launch_bounds__(32 * RW_WARPS) k_down_row(LevelView L, float damping, int rpc,
+__global__ void __launch_bounds__(32 * RW_WARPS, HB_ROW_MINB) k_down_row(LevelView L, float damping, int rpc,
                                                             const int* act, const float2* __restrict__ f,
                                                             const float* fscale, float2* __restrict__ fc) {
   constexpr int NC = NPL / 2;  // coarse columns per lane
@@ -219,7 +222,7 @@ __device__ __forceinline__ void up_v(const URow<NPL>& r, float damping, int lane
 
 // up leg: grid (ceil(fine row chunks / RW_WARPS), B); warp = fine rows [y0, y0 + rpc) of one column
 template <int NPL, int O>
-__global__ void __launch_bounds__(32 * RW_WARPS) k_up_row(LevelView L, float damping, int rpc,
+__global__ void __launch_bounds__(32 * RW_WARPS, HB_ROW_MINB) k_up_row(LevelView L, float damping, int rpc,
                                                           const int* act, const float2* __restrict__ f,
                                                           const float* fscale, const float2* __restrict__ vcoarse,
                                                           float2* __restrict__ z) {

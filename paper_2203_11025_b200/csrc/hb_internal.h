@@ -121,6 +121,12 @@ struct Net {
   std::vector<ConvW> convs;
   int enc1[8], enc2[8], up[8], dec1[8], dec2[8], head = -1;
   bool dirty = true;
+  // encoder-solver input layer split (hb_net.cu, net_forward_dev): the context
+  // channels are batch-broadcast, so their share of conv(concat(x, ctx)) is
+  // computed once per forward (pre_ctx, with the bias) and added per column to
+  // the in_ch-channel conv of x (pre_x)
+  ConvW pre_ctx, pre_x;
+  bool pre_split = false;
 };
 
 struct Prof {
@@ -351,7 +357,7 @@ struct Context {
   // options
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
-       opt_coarse_reg = true, opt_row_legs = true,
+       opt_coarse_reg = true, opt_row_legs = true, opt_ctx_pre = true,
        opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_coarse_cluster = true, opt_basis_wave = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
   int dbg_skip = 0;  // diagnostics only (tools/debug/c0_marginal.py): skip kernel classes, results invalid
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size

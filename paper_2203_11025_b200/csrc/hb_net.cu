@@ -38,6 +38,7 @@ struct ConvArgs {
   int relu;
   float* out;  // NHWC cout
   const int* act;
+  const float* pre = nullptr;  // per-pixel [H][W][cout] term replacing the bias, batch-broadcast (k_conv_small_pw)
 };
 
 __global__ void __launch_bounds__(256) k_conv3x3(ConvArgs p) {
@@ -284,8 +285,15 @@ __global__ void __launch_bounds__(CS_NT) k_conv_small_pw(ConvArgs p, const __gri
   __syncthreads();
   const int ty = t / CS_TW, tx = t % CS_TW;
   float acc[COUT];
+  if (p.pre) {  // batch-broadcast per-pixel term (the context channels' share, bias included)
+    const int yq = min(y0 + ty, p.H - 1), xq = min(x0 + tx, p.W - 1);
+    const float* pp = p.pre + (size_t(yq) * p.W + xq) * COUT;
 #pragma unroll
-  for (int co = 0; co < COUT; ++co) acc[co] = wt.b[co];
+    for (int co = 0; co < COUT; ++co) acc[co] = __ldg(pp + co);
+  } else {
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) acc[co] = wt.b[co];
+  }
 #pragma unroll
   for (int ky = 0; ky < 3; ++ky) {
     const float* rp = tile + ((ty + ky) * (CS_TW + 2) + tx) * cp;
@@ -627,7 +635,35 @@ static void build_topology(Net& n) {
 void net_upload(Context& c, int slot) {
   Net& n = c.nets[slot];
   if (!n.dirty) return;
-  for (auto& cw : n.convs) {
+  std::vector<ConvW*> up;
+  for (auto& cw : n.convs) up.push_back(&cw);
+  n.pre_split = false;
+  if (n.cfg.kind == HB_NET_SOLVER && n.cfg.ctx_ch > 0 && n.cfg.in_ch == 3 && n.cfg.ctx_ch == 16 && n.cfg.base == 16) {
+    // split the input layer's [x | ctx] weights: pre_ctx (16 -> 16, bias) and pre_x (3 -> 16, no bias)
+    const ConvW& full = n.convs[size_t(n.enc1[0])];
+    const int ci0 = n.cfg.in_ch, cc = n.cfg.ctx_ch, co = full.cout;
+    n.pre_ctx.cin = cc;
+    n.pre_x.cin = ci0;
+    n.pre_ctx.cout = n.pre_x.cout = co;
+    n.pre_ctx.w.assign(size_t(co) * cc * 9, 0.f);
+    n.pre_x.w.assign(size_t(co) * ci0 * 9, 0.f);
+    for (int o = 0; o < co; ++o)
+      for (int ci = 0; ci < full.cin; ++ci)
+        for (int t = 0; t < 9; ++t) {
+          const float v = full.w[(size_t(o) * full.cin + ci) * 9 + t];
+          if (ci < ci0)
+            n.pre_x.w[(size_t(o) * ci0 + ci) * 9 + t] = v;
+          else
+            n.pre_ctx.w[(size_t(o) * cc + (ci - ci0)) * 9 + t] = v;
+        }
+    n.pre_ctx.b = full.b;
+    n.pre_x.b.assign(size_t(co), 0.f);
+    up.push_back(&n.pre_ctx);
+    up.push_back(&n.pre_x);
+    n.pre_split = true;
+  }
+  for (ConvW* cwp : up) {
+    ConvW& cw = *cwp;
     std::vector<float> pk(size_t(9) * cw.cin * cw.cout);
     for (int co = 0; co < cw.cout; ++co)
       for (int ci = 0; ci < cw.cin; ++ci)
@@ -649,6 +685,7 @@ void net_upload(Context& c, int slot) {
 struct NetBuffers {
   int B = 0, H = 0, W = 0, slot = -1;
   std::vector<DBuf<float>> skip, tmp, pool, up, u;
+  DBuf<float> pre;  // the encoder-solver input layer's context share [H][W][16]
 };
 static thread_local NetBuffers g_nb[2];
 
@@ -681,6 +718,21 @@ static NetBuffers& buffers(Context& c, int slot, int B, int H, int W) {
 }
 
 // solver U-Net (A5, + A7 context concat); x NHWC in_ch -> y NHWC 2
+// the per-column part of the split input layer: 3 -> 16 narrow conv whose
+// accumulators start from the batch-broadcast context share pre (bias included)
+static void conv_pre(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, long long sa,
+                     int ca, const float* pre, int relu, float* out) {
+  ConvArgs p{B, H, W, a, sa, ca, nullptr, 0, 0, cw.dw.p, cw.db.p, cw.cout, relu, out, act};
+  p.pre = pre;
+  const dim3 g(((W + CS_TW - 1) / CS_TW) * ((H + CS_TH - 1) / CS_TH), 1, B);
+  NScope ns(c, PC_CONV, double(B) * H * W * 4.0 * (cw.cin + 2 * cw.cout), 2.0 * B * H * W * 9.0 * cw.cin * cw.cout);
+  if (c.prof_detail)
+    c.prof_label = "conv_small(pre) " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
+                   std::to_string(ca) + "->" + std::to_string(cw.cout);
+  if (!conv_small_pw<3, 16>(c, cw, p, g)) throw HbError{HB_ERR_STATE, "split input layer: no 3 -> 16 kernel"};
+  HB_CUDA(cudaGetLastError());
+}
+
 void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, const float* x, float* y) {
   Net& n = c.nets[slot];
   if (!n.set || n.cfg.kind != HB_NET_SOLVER) throw HbError{HB_ERR_STATE, "solver net not set"};
@@ -699,8 +751,17 @@ void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, 
       cur = nb.pool[size_t(l)].p;
     }
     const float* ctxp = es ? c.ctx_maps[size_t(2 * l)].p : nullptr;
-    conv(c, n.convs[size_t(n.enc1[l])], B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, ctxp, 0,
-         es ? n.cfg.ctx_ch : 0, 1, nb.tmp[size_t(l)].p);
+    if (l == 0 && es && n.pre_split && c.opt_small_pw && c.opt_ctx_pre) {
+      // conv(concat(x, ctx)) = conv_x(x) + conv_ctx(ctx): the context maps are the
+      // same for every column, so their share (with the bias) is computed once
+      // (B = 1) and the per-column kernel convolves only the 3 input channels
+      nb.pre.ensure(size_t(Hl) * Wl * n.pre_ctx.cout);
+      conv(c, n.pre_ctx, 1, nullptr, Hl, Wl, ctxp, 0, n.cfg.ctx_ch, nullptr, 0, 0, 0, nb.pre.p);
+      conv_pre(c, n.pre_x, B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, nb.pre.p, 1, nb.tmp[size_t(l)].p);
+    } else {
+      conv(c, n.convs[size_t(n.enc1[l])], B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, ctxp, 0,
+           es ? n.cfg.ctx_ch : 0, 1, nb.tmp[size_t(l)].p);
+    }
     conv(c, n.convs[size_t(n.enc2[l])], B, act, Hl, Wl, nb.tmp[size_t(l)].p, (long long)Hl * Wl * cl, cl, nullptr, 0,
          0, 1, nb.skip[size_t(l)].p);
     cur = nb.skip[size_t(l)].p;

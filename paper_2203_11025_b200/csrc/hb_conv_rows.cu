@@ -74,6 +74,7 @@ struct CrParams {
   int rbuf;              // input-row smem buffers (<= CR_RBUF)
   const float* wrow;     // [nslice][nch][3 kx][96 rows][16 ci] packed, SW64-swizzled
   const float* bias;
+  const float* pre;  // optional per-pixel [H][W][ldo] term replacing the bias, batch-broadcast (context share)
   float* out;
   const int* act;
 };
@@ -278,8 +279,20 @@ __global__ void __launch_bounds__(CrShape<NCTA>::THREADS, NCTA)
         mbar_wait(&bar_dfull[sn % ring], (sn / ring) & 1);
         tc_fence_after();
         float o[16];
+        if (p.pre) {  // the batch-broadcast context share of a split encoder-solver layer (bias included)
+          const float4* pp = reinterpret_cast<const float4*>(p.pre + (size_t(y) * p.W + x0 + pix) * cout + sl * 16);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) o[i] = __ldg(p.bias + sl * 16 + i);
+          for (int i = 0; i < 4; ++i) {
+            const float4 v = __ldg(pp + i);
+            o[4 * i] = v.x;
+            o[4 * i + 1] = v.y;
+            o[4 * i + 2] = v.z;
+            o[4 * i + 3] = v.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) o[i] = __ldg(p.bias + sl * 16 + i);
+        }
         if (CrShape<NCTA>::SPLIT) {
 #pragma unroll
           for (int ky = 0; ky < 3; ++ky) {
@@ -373,7 +386,7 @@ void conv_rows_prepare(ConvW& cw) {
 }
 
 bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
-                      const float* bsrc, int cb, bool b_ctx, int relu, float* out) {
+                      const float* bsrc, int cb, bool b_ctx, int relu, float* out, const float* pre) {
   if (!c.opt_conv_rows || !c.opt_tc_conv) return false;
   if (cw.cout % 16 || cw.cout > 32 || !cw.dwrow.p || W % 128 || ca % 16 || cb % 16 || ca + cb != cw.cin ||
       cw.cin > 128)
@@ -437,6 +450,7 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
     p.wrow = cw.dwrow.p + size_t(s) * wslice / sizeof(float);
     p.bias = cw.db.p + 16 * s;
     p.out = out + 16 * s;
+    p.pre = pre ? pre + 16 * s : nullptr;
     if (two)
       launch_pdl(c, k_conv_rows<2>, dim3(grid), dim3(CrShape<2>::THREADS), smem, mA, mB, p);
     else

@@ -127,6 +127,10 @@ struct Net {
   // the in_ch-channel conv of x (pre_x)
   ConvW pre_ctx, pre_x;
   bool pre_split = false;
+  // the same split for the other context-concat convs whose x part runs on
+  // k_conv_rows (Cout <= 32): conv index -> (context part, x part)
+  std::vector<int> split_of;
+  std::vector<ConvW> split_ctx, split_x;
 };
 
 struct Prof {
@@ -224,7 +228,8 @@ TcGeo conv_geo_3x3(int H, int W, int cout);
 void conv_tc_upload_packed(ConvW& cw, const std::vector<float>& packed);
 void conv_rows_prepare(ConvW& cw);
 bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
-                      const float* bsrc, int cb, bool b_ctx, int relu, float* out);
+                      const float* bsrc, int cb, bool b_ctx, int relu, float* out,
+                      const float* pre = nullptr);
 bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                     const float* bsrc, int cb, bool b_ctx, int relu, float* out);
 // row-streaming legs, zero initial guess (hb_mg_stream.cu)

@@ -662,6 +662,44 @@ void net_upload(Context& c, int slot) {
     up.push_back(&n.pre_x);
     n.pre_split = true;
   }
+  // the other context-concat convs (first conv of levels >= 1, the up-convs)
+  // whose x part fits k_conv_rows: [x | ctx] weights -> x part (no bias) +
+  // context part (bias); the forward computes the context share once (B = 1)
+  n.split_of.assign(n.convs.size(), -1);
+  n.split_ctx.clear();
+  n.split_x.clear();
+  if (n.cfg.kind == HB_NET_SOLVER && n.cfg.ctx_ch > 0 && n.cfg.ctx_ch % 16 == 0) {
+    std::vector<int> cands;
+    for (int l = 1; l < n.cfg.levels; ++l) cands.push_back(n.enc1[l]);
+    for (int l = 0; l + 1 < n.cfg.levels; ++l) cands.push_back(n.up[l]);
+    for (int idx : cands) {
+      const ConvW& full = n.convs[size_t(idx)];
+      const int cc = n.cfg.ctx_ch, cx = full.cin - cc, co = full.cout;
+      if (co % 16 || co > 32 || cx % 16 || cx <= 0) continue;  // x part must run on k_conv_rows
+      ConvW xc, cp;
+      xc.cin = cx;
+      cp.cin = cc;
+      xc.cout = cp.cout = co;
+      xc.w.assign(size_t(co) * cx * 9, 0.f);
+      cp.w.assign(size_t(co) * cc * 9, 0.f);
+      for (int o = 0; o < co; ++o)
+        for (int ci = 0; ci < full.cin; ++ci)
+          for (int t = 0; t < 9; ++t) {
+            const float v = full.w[(size_t(o) * full.cin + ci) * 9 + t];
+            if (ci < cx)
+              xc.w[(size_t(o) * cx + ci) * 9 + t] = v;
+            else
+              cp.w[(size_t(o) * cc + (ci - cx)) * 9 + t] = v;
+          }
+      cp.b = full.b;
+      xc.b.assign(size_t(co), 0.f);
+      n.split_of[size_t(idx)] = int(n.split_x.size());
+      n.split_x.push_back(std::move(xc));
+      n.split_ctx.push_back(std::move(cp));
+    }
+    for (auto& w : n.split_x) up.push_back(&w);
+    for (auto& w : n.split_ctx) up.push_back(&w);
+  }
   for (ConvW* cwp : up) {
     ConvW& cw = *cwp;
     std::vector<float> pk(size_t(9) * cw.cin * cw.cout);
@@ -718,6 +756,21 @@ static NetBuffers& buffers(Context& c, int slot, int B, int H, int W) {
 }
 
 // solver U-Net (A5, + A7 context concat); x NHWC in_ch -> y NHWC 2
+// a context-concat conv as x part (per column, k_conv_rows) + context share
+// (batch-broadcast ctx, once); false if the layer is not split / not eligible
+static bool conv_split(Context& c, Net& n, NetBuffers& nb, int idx, int B, const int* act, int H, int W,
+                       const float* x, int cx, const float* ctxp, int relu, float* out) {
+  if (!c.opt_ctx_pre || idx < 0 || size_t(idx) >= n.split_of.size() || n.split_of[size_t(idx)] < 0 || !ctxp)
+    return false;
+  const int si = n.split_of[size_t(idx)];
+  const ConvW& xc = n.split_x[size_t(si)];
+  const ConvW& cp = n.split_ctx[size_t(si)];
+  if (xc.cin != cx) return false;
+  nb.pre.ensure(size_t(H) * W * cp.cout);
+  conv(c, cp, 1, nullptr, H, W, ctxp, 0, cp.cin, nullptr, 0, 0, 0, nb.pre.p);
+  return launch_conv_rows(c, xc, B, act, H, W, x, cx, nullptr, 0, false, relu, out, nb.pre.p);
+}
+
 // the per-column part of the split input layer: 3 -> 16 narrow conv whose
 // accumulators start from the batch-broadcast context share pre (bias included)
 static void conv_pre(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, long long sa,
@@ -758,7 +811,7 @@ void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, 
       nb.pre.ensure(size_t(Hl) * Wl * n.pre_ctx.cout);
       conv(c, n.pre_ctx, 1, nullptr, Hl, Wl, ctxp, 0, n.cfg.ctx_ch, nullptr, 0, 0, 0, nb.pre.p);
       conv_pre(c, n.pre_x, B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, nb.pre.p, 1, nb.tmp[size_t(l)].p);
-    } else {
+    } else if (!(es && conv_split(c, n, nb, n.enc1[l], B, act, Hl, Wl, cur, curc, ctxp, 1, nb.tmp[size_t(l)].p))) {
       conv(c, n.convs[size_t(n.enc1[l])], B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, ctxp, 0,
            es ? n.cfg.ctx_ch : 0, 1, nb.tmp[size_t(l)].p);
     }
@@ -772,8 +825,9 @@ void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, 
     // concat(x, ctx_{l+1}) then upsample == [upsample(x) | upsample(ctx_{l+1})]; the latter is cached
     upsample(c, B, act, Hl / 2, Wl / 2, curc, cur, (long long)(Hl / 2) * (Wl / 2) * curc, nb.up[size_t(l)].p);
     const float* cup = es ? c.ctx_maps[size_t(2 * (l + 1) + 1)].p : nullptr;
-    conv(c, n.convs[size_t(n.up[l])], B, act, Hl, Wl, nb.up[size_t(l)].p, (long long)Hl * Wl * curc, curc, cup, 0,
-         es ? n.cfg.ctx_ch : 0, 0, nb.u[size_t(l)].p);
+    if (!(es && conv_split(c, n, nb, n.up[l], B, act, Hl, Wl, nb.up[size_t(l)].p, curc, cup, 0, nb.u[size_t(l)].p)))
+      conv(c, n.convs[size_t(n.up[l])], B, act, Hl, Wl, nb.up[size_t(l)].p, (long long)Hl * Wl * curc, curc, cup, 0,
+           es ? n.cfg.ctx_ch : 0, 0, nb.u[size_t(l)].p);
     conv(c, n.convs[size_t(n.dec1[l])], B, act, Hl, Wl, nb.u[size_t(l)].p, (long long)Hl * Wl * cl, cl,
          nb.skip[size_t(l)].p, (long long)Hl * Wl * cl, cl, 1, nb.tmp[size_t(l)].p);
     conv(c, n.convs[size_t(n.dec2[l])], B, act, Hl, Wl, nb.tmp[size_t(l)].p, (long long)Hl * Wl * cl, cl, nullptr, 0,

@@ -288,8 +288,19 @@ __global__ void __launch_bounds__(CS_NT) k_conv_small_pw(ConvArgs p, const __gri
   if (p.pre) {  // batch-broadcast per-pixel term (the context channels' share, bias included)
     const int yq = min(y0 + ty, p.H - 1), xq = min(x0 + tx, p.W - 1);
     const float* pp = p.pre + (size_t(yq) * p.W + xq) * COUT;
+    if constexpr (COUT % 4 == 0) {
 #pragma unroll
-    for (int co = 0; co < COUT; ++co) acc[co] = __ldg(pp + co);
+      for (int co = 0; co < COUT; co += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(pp + co));
+        acc[co] = v.x;
+        acc[co + 1] = v.y;
+        acc[co + 2] = v.z;
+        acc[co + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int co = 0; co < COUT; ++co) acc[co] = __ldg(pp + co);
+    }
   } else {
 #pragma unroll
     for (int co = 0; co < COUT; ++co) acc[co] = wt.b[co];

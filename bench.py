@@ -582,7 +582,10 @@ def fixed_budget(name, local, args, ws, rank):
     ctx, arr = problems.gpu_setup(cfg, device=local)
     Bh = np.ascontiguousarray(problems.rhs_block(arr)[cols])
     nb = Bh.shape[0]
-    budget = {"c3": max(2, args.budget // 5), "c2": max(2, args.budget // 2)}.get(name, args.budget)
+    # whole restart cycles: a budget that ends mid-cycle leaves the cycle's remaining inner
+    # steps launched as no-ops on frozen columns (their launches would inflate ms/iteration)
+    m = cfg["restart"]
+    budget = max(m, (args.budget // m) * m)
     kc = hg.KrylovConfig(restart=cfg["restart"], max_iters=budget, rel_tol=1e-6)
     dev = torch.device("cuda", local)
     dB = torch.from_numpy(Bh).to(dev)
@@ -981,7 +984,7 @@ def main():
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
                                                               "(0 = 3 per SM: one per SM in each of the 3 column groups)")
     ap.add_argument("--also", default="datagen,c1,c2,c3,c4,c4slab,mv512,paper_ju,train,block", help="comma list of configs measured on a fixed iteration budget "
-                                                       "(c2: budget/2, c3: budget/5 iterations)")
+                                                       "(rounded down to whole restart cycles, at least one)")
     ap.add_argument("--budget", type=int, default=20)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (hb_set_option)")
     ap.add_argument("--groups", type=int, default=3, help="independent column groups (solver contexts on their own "

@@ -131,6 +131,12 @@ struct Net {
   // k_conv_rows (Cout <= 32): conv index -> (context part, x part)
   std::vector<int> split_of;
   std::vector<ConvW> split_ctx, split_x;
+  // the context shares depend only on the weights and the context maps (fixed
+  // during a solve): cached per split layer (index split_x.size() = the input
+  // layer), recomputed when the key (encode / upload generations, H, W) changes
+  std::vector<DBuf<float>> pre_buf;
+  std::vector<char> pre_ok;
+  unsigned long long pre_key = ~0ull, upload_gen = 0;
 };
 
 struct Prof {
@@ -404,6 +410,7 @@ struct Context {
   std::shared_ptr<PaperState> paper;
   std::shared_ptr<TrainState> train;  // device parameters, tape and ADAM moments while training
   unsigned long long prob_gen = 0;  // bumped by hb_set_problem
+  unsigned long long ctx_gen = 0;   // bumped by every encoder forward (new context maps)
 };
 
 // Launch with programmatic dependent launch (PDL, sm_90+): the kernel may be

@@ -711,6 +711,9 @@ void net_upload(Context& c, int slot) {
     for (auto& w : n.split_x) up.push_back(&w);
     for (auto& w : n.split_ctx) up.push_back(&w);
   }
+  ++n.upload_gen;
+  n.pre_buf = std::vector<DBuf<float>>(n.split_x.size() + 1);
+  n.pre_ok.assign(n.split_x.size() + 1, 0);
   for (ConvW* cwp : up) {
     ConvW& cw = *cwp;
     std::vector<float> pk(size_t(9) * cw.cin * cw.cout);
@@ -734,7 +737,6 @@ void net_upload(Context& c, int slot) {
 struct NetBuffers {
   int B = 0, H = 0, W = 0, slot = -1;
   std::vector<DBuf<float>> skip, tmp, pool, up, u;
-  DBuf<float> pre;  // the encoder-solver input layer's context share [H][W][16]
 };
 static thread_local NetBuffers g_nb[2];
 
@@ -777,9 +779,13 @@ static bool conv_split(Context& c, Net& n, NetBuffers& nb, int idx, int B, const
   const ConvW& xc = n.split_x[size_t(si)];
   const ConvW& cp = n.split_ctx[size_t(si)];
   if (xc.cin != cx) return false;
-  nb.pre.ensure(size_t(H) * W * cp.cout);
-  conv(c, cp, 1, nullptr, H, W, ctxp, 0, cp.cin, nullptr, 0, 0, 0, nb.pre.p);
-  return launch_conv_rows(c, xc, B, act, H, W, x, cx, nullptr, 0, false, relu, out, nb.pre.p);
+  DBuf<float>& pre = n.pre_buf[size_t(si)];
+  if (!n.pre_ok[size_t(si)]) {  // the context share: once per (weights, context maps)
+    pre.ensure(size_t(H) * W * cp.cout);
+    conv(c, cp, 1, nullptr, H, W, ctxp, 0, cp.cin, nullptr, 0, 0, 0, pre.p);
+    n.pre_ok[size_t(si)] = 1;
+  }
+  return launch_conv_rows(c, xc, B, act, H, W, x, cx, nullptr, 0, false, relu, out, pre.p);
 }
 
 // the per-column part of the split input layer: 3 -> 16 narrow conv whose
@@ -806,6 +812,13 @@ void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, 
   if (es && !c.ctx_valid) throw HbError{HB_ERR_STATE, "encoder-solver net needs hb_encode first"};
   net_upload(c, slot);
   NetBuffers& nb = buffers(c, slot, B, H, W);
+  if (es) {  // cached context shares: valid for these weights, context maps and dims
+    const unsigned long long key = (c.ctx_gen << 40) ^ (n.upload_gen << 28) ^ (unsigned long long)(H) << 14 ^ W;
+    if (key != n.pre_key) {
+      n.pre_key = key;
+      n.pre_ok.assign(n.pre_ok.size(), 0);
+    }
+  }
   const float* cur = x;
   int curc = n.cfg.in_ch;
   for (int l = 0; l < L; ++l) {
@@ -819,9 +832,13 @@ void net_forward_dev(Context& c, int slot, int B, const int* act, int H, int W, 
       // conv(concat(x, ctx)) = conv_x(x) + conv_ctx(ctx): the context maps are the
       // same for every column, so their share (with the bias) is computed once
       // (B = 1) and the per-column kernel convolves only the 3 input channels
-      nb.pre.ensure(size_t(Hl) * Wl * n.pre_ctx.cout);
-      conv(c, n.pre_ctx, 1, nullptr, Hl, Wl, ctxp, 0, n.cfg.ctx_ch, nullptr, 0, 0, 0, nb.pre.p);
-      conv_pre(c, n.pre_x, B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, nb.pre.p, 1, nb.tmp[size_t(l)].p);
+      DBuf<float>& pre = n.pre_buf.back();
+      if (!n.pre_ok.back()) {
+        pre.ensure(size_t(Hl) * Wl * n.pre_ctx.cout);
+        conv(c, n.pre_ctx, 1, nullptr, Hl, Wl, ctxp, 0, n.cfg.ctx_ch, nullptr, 0, 0, 0, pre.p);
+        n.pre_ok.back() = 1;
+      }
+      conv_pre(c, n.pre_x, B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, pre.p, 1, nb.tmp[size_t(l)].p);
     } else if (!(es && conv_split(c, n, nb, n.enc1[l], B, act, Hl, Wl, cur, curc, ctxp, 1, nb.tmp[size_t(l)].p))) {
       conv(c, n.convs[size_t(n.enc1[l])], B, act, Hl, Wl, cur, (long long)Hl * Wl * curc, curc, ctxp, 0,
            es ? n.cfg.ctx_ch : 0, 1, nb.tmp[size_t(l)].p);
@@ -878,6 +895,7 @@ void encoder_forward_dev(Context& c, int H, int W, const float* k2f) {
     }
   }
   c.ctx_valid = true;
+  ++c.ctx_gen;
 }
 
 }  // namespace hb

@@ -271,7 +271,9 @@ __device__ __forceinline__ void cta_reduce_acc(const float (&acc)[NA], int nf, f
 __device__ void adots_scalar(ColState& S, int j, const double2* red);
 
 template <int JM, bool WIDE>
-__global__ void __launch_bounds__(KT) k_adots(FineView F, int B, int j, ColState* st, const int* act,
+// up to JM = 9 (c0's FGMRES(10)): <= 64 registers, 4 CTAs per SM (measured 2% on the c0 step);
+// the 20-32-vector instantiations would spill there
+__global__ void __launch_bounds__(KT, (JM <= 9 ? 4 : 1)) k_adots(FineView F, int B, int j, ColState* st, const int* act,
                                               const float2* __restrict__ Z, float2* __restrict__ W,
                                               const float2* __restrict__ V, double2* part, unsigned* ticket,
                                               double2* gsum) {

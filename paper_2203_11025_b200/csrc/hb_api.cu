@@ -1055,6 +1055,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_tc_conv = value != 0;
   else if (k == "conv_ksplit")
     ctx->opt_conv_ksplit = value != 0;
+  else if (k == "tconv_par4")
+    ctx->opt_tconv_par4 = value != 0;
   else if (k == "ctx_pre")
     ctx->opt_ctx_pre = value != 0;
   else if (k == "row_legs")

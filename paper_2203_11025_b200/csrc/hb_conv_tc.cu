@@ -440,6 +440,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const float* bias = p.bias + n0;
       const uint32_t trow = tmem_base + (uint32_t(32 * q) << 16) + uint32_t(acc * accw);
       for (int c0 = 0; c0 < ((dbg & 4) ? 0 : N); c0 += 16) {
+        int cq = n0 + c0;  // output channel of the chunk (par4: within its parity block)
+        if (GEN && p.geo.par4 && !part) {
+          const int qb = (n0 + c0) / p.geo.par4;
+          cq = (n0 + c0) - qb * p.geo.par4;
+          const size_t op = (size_t(b) * p.geo.Ho + (y0 + yy) * 2 + (qb >> 1)) * p.geo.Wo + (x0 + xx) * 2 + (qb & 1);
+          orow = p.out + op * p.geo.ldo + cq - c0;  // + c0 + i below
+          rrow = p.epi.res ? p.epi.res + op * p.epi.ldres + cq - c0 : nullptr;
+        }
         uint32_t v[16], u[16];
         tmem_ld16(trow + uint32_t(c0), v);
         tmem_ld16(trow + uint32_t(N + c0), u);
@@ -455,7 +463,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             o[i] = part ? x : p.relu ? fmaxf(y, 0.f) : y;
           }
         }
-        const int nvalid = GEN && p.epi.nco && !part ? p.epi.nco - (n0 + c0) : 16;  // padded output channels: not stored
+        const int nvalid = GEN && p.epi.nco && !part ? p.epi.nco - cq : 16;  // padded output channels: not stored
 #pragma unroll
         for (int i = 0; i < 16; i += 4)
           if (i < nvalid) *reinterpret_cast<float4*>(orow + c0 + i) = make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]);
@@ -509,9 +517,15 @@ __global__ void k_conv_ksum(int ksplit, int B, int H, int W, int cout, const int
     const int rem = int(pix - size_t(b) * H * W), y = rem / W, x = rem - y * W;
     float a = __ldg(bias + co);
     for (int s = 0; s < ksplit; ++s) a += __ldg(ws + size_t(s) * n + i);
-    if (epi.nco && co >= epi.nco) continue;  // padded output channel
-    const size_t opix = (size_t(b) * geo.Ho + y * geo.os + geo.py) * geo.Wo + x * geo.os + geo.px;
-    out[opix * geo.ldo + co] = tc_epilogue(epi, co, a, epi.res ? epi.res + opix * epi.ldres + co : nullptr);
+    int cq = co;
+    size_t opix = (size_t(b) * geo.Ho + y * geo.os + geo.py) * geo.Wo + x * geo.os + geo.px;
+    if (geo.par4) {  // the four parity classes of a transposed conv in one GEMM
+      const int qb = co / geo.par4;
+      cq = co - qb * geo.par4;
+      opix = (size_t(b) * geo.Ho + y * 2 + (qb >> 1)) * geo.Wo + x * 2 + (qb & 1);
+    }
+    if (epi.nco && cq >= epi.nco) continue;  // padded output channel
+    out[opix * geo.ldo + cq] = tc_epilogue(epi, co, a, epi.res ? epi.res + opix * epi.ldres + cq : nullptr);
   }
 }
 
@@ -671,7 +685,7 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
   // uniform chunk width as a template argument (fully unrolled issue loops);
   // mixed-width sources take the generic instantiation
   const bool uni = !cb || kca == kcb;
-  const bool gen = geo.s != 1 || geo.os != 1 || geo.ldo != cw.cout || t.epi.res || t.epi.mu || t.epi.act == 2 ||
+  const bool gen = geo.par4 || geo.s != 1 || geo.os != 1 || geo.ldo != cw.cout || t.epi.res || t.epi.mu || t.epi.act == 2 ||
                    t.epi.in_elu || t.epi.nco;
   void (*kern)(CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, CUtensorMap, TcParams, TcLayout, int) =
       gen ? (!uni ? k_conv_tc<0, true> : kcmax == 32 ? k_conv_tc<32, true> : k_conv_tc<16, true>)
@@ -689,7 +703,7 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
   if (c.prof_detail)
     c.prof_label = "conv_tc " + std::to_string(B) + "x" + std::to_string(H) + "x" + std::to_string(W) + " " +
                    std::to_string(ca) + "+" + std::to_string(cb) + "->" + std::to_string(cw.cout) + " taps " +
-                   std::to_string(NT) + " s" + std::to_string(geo.s);
+                   std::to_string(NT) + " s" + std::to_string(geo.s) + (geo.par4 ? " par4" : "");
   static const int dbg = getenv("HB_CONV_DEBUG") ? atoi(getenv("HB_CONV_DEBUG")) : 0;
   launch_pdl(c, kern, dim3(grid), dim3(TC_THREADS), smem, mA, mB, wh32, wl32, wh16, wl16, p, lay, dbg);
   if (ksplit > 1) {
@@ -707,8 +721,10 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
                  geo, t.epi, t.out);
     }
   }
-  prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout),
-           2.0 * B * H * W * double(NT) * cw.cin * cw.cout);
+  // useful flops: a 4-class transposed conv counts its k^2 real taps and real output channels
+  const double flops = geo.par4 ? 2.0 * B * H * W * double(geo.par4_kk) * cw.cin * (t.epi.nco ? t.epi.nco : geo.par4)
+                                : 2.0 * B * H * W * double(NT) * cw.cin * cw.cout;
+  prof_end(c, PC_CONV, tok, double(B) * H * W * 4.0 * (cw.cin + cw.cout), flops);
   HB_CUDA(cudaGetLastError());
   if (trace) {
     long long h[256];

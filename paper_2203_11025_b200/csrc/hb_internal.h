@@ -203,6 +203,11 @@ struct TcGeo {
   int ntaps, s, oy, ox, boxh, boxw;
   int os, py, px, Ho, Wo, ldo;
   int ty[TC_MAX_TAPS], tx[TC_MAX_TAPS];
+  // par4 > 0: the four output parity classes of a stride-2 transposed conv in one
+  // GEMM -- output channel block q = c / par4 (par4 channels each) is stored at
+  // output pixel (2y + (q >> 1), 2x + (q & 1)), channel c % par4 (os must be 2)
+  int par4 = 0;
+  int par4_kk = 0;  // par4: kernel taps k^2 of the transposed conv (useful flops: zero-weight taps not counted)
 };
 // epilogue: y = act(BN(x + bias [+ res])), BN in eval form ((t - mu) is) g + be
 // (inc/autodiff.hpp:289-296); act 0 none, 1 ReLU, 2 ELU; in_elu: ELU applied to
@@ -368,7 +373,7 @@ struct Context {
   // options
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
-       opt_coarse_reg = true, opt_row_legs = true, opt_ctx_pre = true,
+       opt_coarse_reg = true, opt_row_legs = true, opt_ctx_pre = true, opt_tconv_par4 = true,
        opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_coarse_cluster = true, opt_basis_wave = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
   int dbg_skip = 0;  // diagnostics only (tools/debug/c0_marginal.py): skip kernel classes, results invalid
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size

@@ -231,6 +231,45 @@ void upload_conv(PaperState& P, const std::string& kname, const std::string& bna
           off.push_back({ky - pad, kx - pad});
         }
       make(tk, off, 0, 0);
+    } else if (P.par4 && D.cin % 16 == 0 && 4 * coutp <= 128) {
+      // conv2d_transpose, stride 2 (:190-215), all four output parity classes in ONE
+      // implicit GEMM: output pixel 2o + p meets kernel taps k = p + pad - 2d at
+      // input o + d, d in {-1, 0, 1}^2 -- a 3x3 neighbourhood shared by the classes;
+      // N = 4 x coutp (class q = 2 py + px in channel block q, zero weights where a
+      // class has no tap) and the epilogue scatters block q to (2o_y + py, 2o_x + px):
+      // one launch of N = 64 MMAs instead of four launches of N = 16 (25 taps)
+      PaperTc T;
+      T.cw.cout = 4 * coutp;
+      T.cw.cin = D.cin;
+      std::vector<float> packed(size_t(4) * coutp * 9 * D.cin, 0.f);
+      for (int q = 0; q < 4; ++q) {
+        const int py = q >> 1, px = q & 1;
+        for (int t = 0; t < 9; ++t) {
+          const int dy = t / 3 - 1, dx = t % 3 - 1;
+          const int ky = py + pad - 2 * dy, kx = px + pad - 2 * dx;
+          if (ky < 0 || ky >= k || kx < 0 || kx >= k) continue;
+          for (int co = 0; co < D.cout; ++co)
+            for (int ci = 0; ci < D.cin; ++ci)
+              packed[(size_t(q * coutp + co) * 9 + t) * D.cin + ci] = w[(size_t(ky * k + kx) * D.cin + ci) * D.cout + co];
+        }
+      }
+      conv_tc_upload_packed(T.cw, packed);
+      std::vector<float> b4;
+      for (int q = 0; q < 4; ++q) {
+        const std::vector<float> bq = padv(Bq.v, 0.f);
+        b4.insert(b4.end(), bq.begin(), bq.end());
+      }
+      up(T.cw.db, b4);
+      T.geo = TcGeo{};
+      T.geo.ntaps = 9;
+      T.geo.oy = T.geo.ox = -1;
+      for (int t = 0; t < 9; ++t) {
+        T.geo.ty[t] = t / 3;
+        T.geo.tx[t] = t % 3;
+      }
+      T.geo.par4 = coutp;
+      T.geo.par4_kk = k * k;
+      D.tc.push_back(std::move(T));
     } else {  // conv2d_transpose, stride 2 (:190-215): output class (py, px) of pixel 2 o + p meets taps
       // k = p + pad (mod 2), input o + (p + pad - k) / 2
       for (int py = 0; py < 2; ++py)
@@ -262,10 +301,19 @@ void upload_conv(PaperState& P, const std::string& kname, const std::string& bna
       return o;
     };
     for (PaperTc& T : D.tc) {
-      up(T.mu, padv(param(P, bn + ".rmean").v, 0.f));
-      up(T.is, padv(is, 1.f));
-      up(T.g, padv(param(P, bn + ".scale").v, 1.f));
-      up(T.be, padv(param(P, bn + ".offset").v, 0.f));
+      const int rep = T.geo.par4 ? 4 : 1;  // one copy per parity-class channel block
+      auto padr = [&](const std::vector<float>& v, float fill) {
+        std::vector<float> o;
+        for (int r = 0; r < rep; ++r) {
+          const std::vector<float> b = padv(v, fill);
+          o.insert(o.end(), b.begin(), b.end());
+        }
+        return o;
+      };
+      up(T.mu, padr(param(P, bn + ".rmean").v, 0.f));
+      up(T.is, padr(is, 1.f));
+      up(T.g, padr(param(P, bn + ".scale").v, 1.f));
+      up(T.be, padr(param(P, bn + ".offset").v, 0.f));
     }
   }
 }
@@ -792,6 +840,10 @@ void paper_forward_dev(Context& c, int B, int H, int W, const float* in, float* 
   if (!P.active) throw HbError{HB_ERR_STATE, "paper net not set (hb_set_paper_net)"};
   const int q = 1 << P.cfg.levels;
   if (H % q || W % q) throw HbError{HB_ERR_ARG, "input dims must be divisible by 2^levels"};
+  if (P.par4 != c.opt_tconv_par4) {
+    P.par4 = c.opt_tconv_par4;
+    P.dirty = true;
+  }
   if (P.dirty) upload_all(P);
   const bool es = P.variant == 1;
   std::vector<TView> feats;

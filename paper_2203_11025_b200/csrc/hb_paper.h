@@ -40,6 +40,7 @@ struct PaperState {
   std::map<std::string, size_t> index;
   std::map<std::string, DevConv> dev;  // by kernel name
   bool dirty = true;
+  bool par4 = true;  // stride-2 transposed convs as ONE 4-parity-class GEMM (else four class launches)
   unsigned long long host_gen = 0;  // bumped when the host parameters change from outside training
   // encoder features (batch 1), per level
   std::vector<DBuf<float>> feat;

@@ -221,9 +221,12 @@ def test_paper_forward_tensor_core_sizes(hg):
     labels = [rec[0] for rec in c.prof_detail(False)]
     c.prof_enable(False)
     tc = [ln for ln in labels if ln.startswith("conv_tc")]
-    assert len(tc) >= 10, labels  # down1/2, 2 x 5 ResNets, 4 x up2/up1 classes ...
-    assert any("taps 25 s2" in ln for ln in tc) and any("taps 4 s1" in ln for ln in tc), tc
+    assert len(tc) >= 10, labels  # down1/2, 2 x 5 ResNets, up2/up1 (the four parity classes in one GEMM)
+    assert any("taps 25 s2" in ln for ln in tc) and any("par4" in ln for ln in tc), tc
     assert rel(y, g["y"]) < 1e-4, rel(y, g["y"])
+    c.set_option("tconv_par4", 0)  # the transposed convs as four per-class launches
+    y4 = c.paper_forward(x)
+    assert rel(y, y4) < 2e-6, rel(y, y4)
     c.set_option("tc_conv", 0)
     y2 = c.paper_forward(x)
     assert rel(y, y2) < 1e-5, rel(y, y2)

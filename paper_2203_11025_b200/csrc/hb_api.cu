@@ -1083,6 +1083,8 @@ int hb_set_option(hb_ctx* ctx, const char* key, int64_t value) {
     ctx->opt_wgrad_blk = value != 0;
   else if (k == "small_pw")
     ctx->opt_small_pw = value != 0;
+  else if (k == "conv_cols")
+    ctx->opt_conv_cols = value != 0;
   else if (k == "vpre")
     ctx->opt_vpre = value != 0;
   else if (k == "staged_legs")

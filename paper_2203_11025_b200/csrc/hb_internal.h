@@ -374,7 +374,7 @@ struct Context {
   double prof_scale = 1.0;  // active-column fraction while profiling (eager) FGMRES steps
   bool opt_fused = true, opt_graphs = true, opt_small_coarse = true, opt_split = true, opt_tc_conv = true, opt_stream = true, opt_conv_ksplit = true,
        opt_coarse_reg = true, opt_row_legs = true, opt_ctx_pre = true, opt_tconv_par4 = true,
-       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_coarse_cluster = true, opt_basis_wave = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true;
+       opt_conv_rows = true, opt_lean_legs = true, opt_coarse_krylov = true, opt_coarse_cluster = true, opt_basis_wave = true, opt_pdl = true, opt_stream_e0 = true, opt_vpre = true, opt_wgrad_blk = true, opt_small_pw = true, opt_conv_cols = true;
   int dbg_skip = 0;  // diagnostics only (tools/debug/c0_marginal.py): skip kernel classes, results invalid
   int opt_staged_legs = 2;  // cp.async-staged legs: 0 off, 1 on, 2 by working-set size
   int opt_legs_wd = 2;  // Jacobi factor in the legs: 0 stored wD^-1, 1 from D, 2 by working-set size

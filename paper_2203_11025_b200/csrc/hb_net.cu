@@ -349,6 +349,120 @@ bool conv_small_pw(Context& c, const ConvW& cw, const ConvArgs& p, dim3 g) {
   return true;
 }
 
+// Narrow-output head (Cin % 4 == 0 -> COUT <= 2, e.g. the U-Net's 16 -> 2):
+// one thread per output column, CC_R output rows slid down the column.  Input
+// rows stream through a CC_NS-slot shared-memory ring filled by coalesced
+// 16-byte cp.async (zero-filled outside the grid), pixel stride Cin + 4 words so
+// the per-thread float4 reads of 3 neighbouring pixels are conflict-free.  Each
+// input row is read once and feeds up to 3 output rows; no per-element halo
+// logic.  (Reading the rows straight from global memory instead spread every
+// 16-byte load over 32 L1 sectors and ran L1-bound.)  The accumulation order per
+// output (ky, ci, kx) is the tiled kernel's, so both give identical bits.
+constexpr int CC_R = 16, CC_NS = 4, CC_TW = 128;
+
+__device__ __forceinline__ void cc_cp16(float* dst, const float* src, bool ok) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src), "r"(ok ? 16 : 0) : "memory");
+}
+
+template <int CIN, int COUT>
+__global__ void __launch_bounds__(CC_TW) k_conv_cols(ConvArgs p, const __grid_constant__ SmallW<CIN, COUT> wt) {
+  static_assert(CIN % 4 == 0, "float4 rows");
+  constexpr int PS = CIN + 4, SEG = CC_TW + 2, NCH = SEG * (CIN / 4);
+  extern __shared__ __align__(16) float cc_sm[];  // [CC_NS][SEG][PS]
+  pdl_enter();
+  const int bz = blockIdx.z;
+  if (p.act && !p.act[bz]) return;
+  const int t = threadIdx.x, x0 = blockIdx.x * CC_TW, y0 = blockIdx.y * CC_R;
+  const float* A = p.a + bz * p.sa;
+  auto issue = [&](int r) {  // input row y0 + r - 1 -> slot r % CC_NS
+    const int y = y0 + r - 1;
+    const bool rok = r < CC_R + 2 && y >= 0 && y < p.H;
+    float* slot = cc_sm + (r % CC_NS) * SEG * PS;
+    for (int i = t; i < NCH; i += CC_TW) {
+      const int px = i / (CIN / 4), c4 = i % (CIN / 4), x = x0 - 1 + px;
+      const bool ok = rok && x >= 0 && x < p.W;
+      cc_cp16(slot + px * PS + 4 * c4, ok ? A + (size_t(y) * p.W + x) * CIN + 4 * c4 : A, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  float acc[CC_R][COUT];
+#pragma unroll
+  for (int o = 0; o < CC_R; ++o)
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) acc[o][co] = wt.b[co];
+#pragma unroll
+  for (int r = 0; r < CC_NS - 1; ++r) issue(r);
+#pragma unroll
+  for (int r = 0; r < CC_R + 2; ++r) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(CC_NS - 2) : "memory");
+    __syncthreads();  // row r visible to all; slot (r - 1) % CC_NS released by all
+    issue(r + CC_NS - 1);
+    const float* rp = cc_sm + (r % CC_NS) * SEG * PS + t * PS;
+#pragma unroll
+    for (int c4 = 0; c4 < CIN / 4; ++c4) {
+      float4 v[3];
+#pragma unroll
+      for (int kx = 0; kx < 3; ++kx) v[kx] = *reinterpret_cast<const float4*>(rp + kx * PS + 4 * c4);
+#pragma unroll
+      for (int ky = 0; ky < 3; ++ky) {
+        const int o = r - ky;  // input row y0 + r - 1 is tap ky of output row y0 + o
+        if (o < 0 || o >= CC_R) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int ci = 4 * c4 + j;
+#pragma unroll
+          for (int co = 0; co < COUT; ++co) {
+            const float a0 = j == 0 ? v[0].x : j == 1 ? v[0].y : j == 2 ? v[0].z : v[0].w;
+            const float a1 = j == 0 ? v[1].x : j == 1 ? v[1].y : j == 2 ? v[1].z : v[1].w;
+            const float a2 = j == 0 ? v[2].x : j == 1 ? v[2].y : j == 2 ? v[2].z : v[2].w;
+            acc[o][co] = fmaf(a0, wt.w[((ky * 3 + 0) * CIN + ci) * COUT + co], acc[o][co]);
+            acc[o][co] = fmaf(a1, wt.w[((ky * 3 + 1) * CIN + ci) * COUT + co], acc[o][co]);
+            acc[o][co] = fmaf(a2, wt.w[((ky * 3 + 2) * CIN + ci) * COUT + co], acc[o][co]);
+          }
+        }
+      }
+    }
+  }
+  const int x = x0 + t;
+  if (x >= p.W) return;
+#pragma unroll
+  for (int o = 0; o < CC_R; ++o) {
+    const int y = y0 + o;
+    if (y >= p.H) break;
+    float* O = p.out + ((size_t(bz) * p.H + y) * p.W + x) * COUT;
+    float r[COUT];
+#pragma unroll
+    for (int co = 0; co < COUT; ++co) r[co] = p.relu ? fmaxf(acc[o][co], 0.f) : acc[o][co];
+    if constexpr (COUT == 2) {
+      *reinterpret_cast<float2*>(O) = make_float2(r[0], r[1]);
+    } else {
+#pragma unroll
+      for (int co = 0; co < COUT; ++co) O[co] = r[co];
+    }
+  }
+}
+
+template <int CIN, int COUT>
+bool conv_cols(Context& c, const ConvW& cw, const ConvArgs& p) {
+  if (cw.cin != CIN || cw.cout != COUT || p.ca != CIN || p.cb != 0) return false;
+  SmallW<CIN, COUT> wt;
+  for (int co = 0; co < COUT; ++co) {
+    wt.b[co] = cw.b[size_t(co)];
+    for (int ci = 0; ci < CIN; ++ci)
+      for (int tap = 0; tap < 9; ++tap) wt.w[(tap * CIN + ci) * COUT + co] = cw.w[(size_t(co) * CIN + ci) * 9 + tap];
+  }
+  constexpr size_t smem = size_t(CC_NS) * (CC_TW + 2) * (CIN + 4) * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    HB_CUDA(cudaFuncSetAttribute(k_conv_cols<CIN, COUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    attr = true;
+  }
+  const dim3 g((p.W + CC_TW - 1) / CC_TW, (p.H + CC_R - 1) / CC_R, p.B);
+  launch_pdl(c, k_conv_cols<CIN, COUT>, g, dim3(CC_TW), smem, p, wt);
+  return true;
+}
+
 // 2x2 max-pool / x2 bilinear upsample, NHWC, 4 channels per thread (C % 4 == 0);
 // one CTA per output row (grid (rows, B)), threads stride along the row
 __global__ void __launch_bounds__(256) k_maxpool2_v4(int H, int W, int C4, const float4* __restrict__ in,
@@ -541,7 +655,8 @@ static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int 
       HB_CUDA(cudaFuncSetAttribute(k_conv_small<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
       attr = true;
     }
-    const bool pw = c.opt_small_pw && (conv_small_pw<3, 16>(c, cw, p, g) || conv_small_pw<19, 16>(c, cw, p, g) ||
+    const bool pw = c.opt_small_pw && ((c.opt_conv_cols && (conv_cols<16, 2>(c, cw, p) || conv_cols<8, 2>(c, cw, p))) ||
+                                       conv_small_pw<3, 16>(c, cw, p, g) || conv_small_pw<19, 16>(c, cw, p, g) ||
                                        conv_small_pw<1, 16>(c, cw, p, g) || conv_small_pw<16, 2>(c, cw, p, g) ||
                                        conv_small_pw<8, 2>(c, cw, p, g));
     if (pw) {

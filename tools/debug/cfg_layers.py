@@ -1,6 +1,6 @@
 """Per-launch device times (library profiler, eager) of one preconditioner apply
 of a BASELINE config's full RHS block, aggregated by label:
-   python tools/debug/cfg_layers.py c3 [B]"""
+   python tools/debug/cfg_layers.py c3 [B] [opt=v,opt=v]"""
 import collections
 import os
 import sys
@@ -14,8 +14,11 @@ from paper_2203_11025_b200 import problems  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 cfg = bench.config_for(name)
-B = int(sys.argv[2]) if len(sys.argv) > 2 else cfg["B"]
+B = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2] else cfg["B"]
 ctx, arr = problems.gpu_setup(cfg, device=0)
+for kv in (sys.argv[3].split(",") if len(sys.argv) > 3 else []):
+    k, v = kv.split("=")
+    ctx.set_option(k, int(v))
 n = cfg["n"]
 r = (np.random.default_rng(0).standard_normal((B, n, n)) + 0j).astype(np.complex64)
 dr = torch.from_numpy(r).cuda()

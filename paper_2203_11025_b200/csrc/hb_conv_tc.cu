@@ -365,7 +365,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int st = s0; st < s1; ++st, ++itc) {
         const int2 sg2 = stg[st];
         const int4 sg = make_int4(sg2.x & 0xffff, sg2.x >> 16, sg2.y & 0xffff, sg2.y >> 16);
-        if (sg.x == NT * sg.z * CG || st == s0) mbar_wait(&bar_hfull[hb], hph);
+        if (sg.x == NT * sg.z * CG || st == s0) {
+          mbar_wait(&bar_hfull[hb], hph);
+          if (GEN && p.epi.in_elu) {
+            // ELU of the input once per halo element, in place, by all 8 A-build
+            // warps (every tap reads each element; applying it per tap in the A build
+            // cost 9 expm1 per element and made the A build the pipeline's bottleneck)
+            float4* h4 = reinterpret_cast<float4*>(base + hb * hbuf_bytes);
+            for (int i = threadIdx.x - 64; i < hbuf_bytes / 16; i += 256) {
+              const float4 x = h4[i];
+              h4[i] = make_float4(elu_f(x.x), elu_f(x.y), elu_f(x.z), elu_f(x.w));
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the TMA refills this buffer
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+          }
+        }
         if (itc >= nslots) mbar_wait(&bar_aempty[j], aph ^ 1);
         tc_fence_after();
         if (p.trace && blockIdx.x == 0 && r == 0 && half == 0 && itc < 64) p.trace[itc * 4 + 1] = clock64();
@@ -385,8 +399,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             uint32_t vh[16], vl[16];
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              float4 x = *reinterpret_cast<const float4*>(row + (((4 * h + c) ^ f) << 4));
-              if (GEN && p.epi.in_elu) x = make_float4(elu_f(x.x), elu_f(x.y), elu_f(x.z), elu_f(x.w));
+              const float4 x = *reinterpret_cast<const float4*>(row + (((4 * h + c) ^ f) << 4));
               const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
               for (int u = 0; u < 4; ++u) {

@@ -436,24 +436,29 @@ __global__ void __launch_bounds__(128) k_pconv(PConv a) {
   }
 }
 
-// Register-tiled variant: a CTA owns 128*P output pixels x 16 output channels;
-// each thread P pixels (128 apart: coalesced stores) x 16 channels = 16P
-// accumulators.  Weights of a 16-input-channel chunk (all taps, 16 outputs,
-// zero-padded) are staged in shared memory and read as warp-uniform float4
-// broadcasts; inputs come from global (L1) as float4 over 4 channels.  Per
-// input channel and tap: 4 LDS.128 + P/4 LDG.128 for 16P FMAs.
-constexpr int PC_T = 128, PC_CO = 16, PC_CI = 16;
+// Register-tiled variant: a CTA owns 128*P output pixels x CO output channels
+// (CO = 16, or 4 for the narrow output layers); each thread P pixels (128
+// apart: coalesced stores) x CO channels = CO*P accumulators.  Weights of a
+// 16-input-channel chunk (all taps, CO outputs, zero-padded) are staged in
+// shared memory and read as warp-uniform float4 broadcasts; inputs come from
+// global (L1) as float4 over 4 channels.  At one pixel per thread (the small,
+// latency-bound layers) the input loads of a whole tap row (up to 5 taps) are
+// issued before its FMAs: one memory round trip per tap row, not per tap.
+constexpr int PC_T = 128, PC_CI = 16, PC_KMAX = 5;
 // Stride-2 transposed convolutions run per output parity class (blockIdx.z):
 // class (py, px) only meets taps ky = py + pad (mod 2), kx = px + pad (mod 2),
 // so no work is spent on the 3/4 of the taps that miss.
-template <int P, bool VEC>  // VEC: cin % 4 == 0 and ldx % 4 == 0 (float4 input loads)
+template <int P, bool VEC, int CO>  // VEC: cin % 4 == 0 and ldx % 4 == 0 (float4 input loads)
 __global__ void __launch_bounds__(PC_T) k_pconv_tiled(PConv a) {
+  // input loads batched ahead of their FMAs: KB taps of a row (registers allow it
+  // at P = 1) x CB float4 channel groups (more measured slower: occupancy)
+  constexpr int KB = P == 1 ? PC_KMAX : 1, CB = 1;
   pdl_enter();
-  extern __shared__ float4 sw4[];  // [tap][ci_local][PC_CO] as float4 x 4
+  extern __shared__ float4 sw4[];  // [tap][ci_local][CO] as float4 x CO/4
   float* sw = reinterpret_cast<float*>(sw4);
   const int t = threadIdx.x;
-  const int co0 = blockIdx.y * PC_CO;
-  const int nco = min(PC_CO, a.cout - co0);
+  const int co0 = blockIdx.y * CO;
+  const int nco = min(CO, a.cout - co0);
   const bool par = a.transpose && a.stride == 2;
   const int cls = blockIdx.z, py = cls >> 1, px = cls & 1;
   const int Hc = par ? (a.Ho - py + 1) / 2 : a.Ho, Wc = par ? (a.Wo - px + 1) / 2 : a.Wo;  // class grid
@@ -479,63 +484,105 @@ __global__ void __launch_bounds__(PC_T) k_pconv_tiled(PConv a) {
     pout[q] = ((long long)pb[q] * a.Ho + poy[q]) * a.Wo + pox[q];
     if (!a.xbatch) pb[q] = 0;
   }
-  float acc[P][PC_CO];
+  float acc[P][CO];
 #pragma unroll
   for (int q = 0; q < P; ++q)
 #pragma unroll
-    for (int j = 0; j < PC_CO; ++j) acc[q][j] = 0.f;
+    for (int j = 0; j < CO; ++j) acc[q][j] = 0.f;
   for (int ci0 = 0; ci0 < a.cin; ci0 += PC_CI) {
     const int nci = min(PC_CI, a.cin - ci0);
     __syncthreads();
-    for (int i = t; i < kk * PC_CI * PC_CO; i += PC_T) {
-      const int j = i % PC_CO, cl = (i / PC_CO) % PC_CI, tap = i / (PC_CO * PC_CI);
+    for (int i = t; i < kk * PC_CI * CO; i += PC_T) {
+      const int j = i % CO, cl = (i / CO) % PC_CI, tap = i / (CO * PC_CI);
       sw[i] = (j < nco && cl < nci) ? __ldg(a.w + (size_t(tap) * a.cin + ci0 + cl) * a.cout + co0 + j) : 0.f;
     }
     __syncthreads();
     for (int ky = ky0; ky < a.k; ky += kst)
-      for (int kx = kx0; kx < a.k; kx += kst) {
-        const float* xp[P];
-        bool ok[P];
+      for (int i0 = 0; i0 < PC_KMAX; i0 += KB) {
+        if (kx0 + i0 * kst >= a.k) break;
+        // input offsets of KB taps of this row (element index; -1 = outside / other class)
+        long long xo[KB][P];
 #pragma unroll
-        for (int q = 0; q < P; ++q) {
-          int iy, ix;
-          if (!a.transpose) {
-            iy = poy[q] * a.stride + ky - pad;
-            ix = pox[q] * a.stride + kx - pad;
-            ok[q] = pv[q];
-          } else {
-            iy = poy[q] + pad - ky;
-            ix = pox[q] + pad - kx;
-            ok[q] = pv[q];
-            if (a.stride == 2) {
-              ok[q] = ok[q] && !((iy | ix) & 1);
-              iy >>= 1;
-              ix >>= 1;
-            }
-          }
-          ok[q] = ok[q] && iy >= 0 && iy < a.Hin && ix >= 0 && ix < a.Win;
-          xp[q] = a.x + ((size_t(pb[q]) * a.Hin + (ok[q] ? iy : 0)) * a.Win + (ok[q] ? ix : 0)) * a.ldx + ci0;
-        }
-        const float4* wt = sw4 + (size_t(ky * a.k + kx) * PC_CI) * (PC_CO / 4);
-        if (VEC) {
-          for (int c4 = 0; c4 < nci; c4 += 4) {
-            float4 xv[P];
+        for (int i = 0; i < KB; ++i) {
+          const int kx = kx0 + (i0 + i) * kst;
 #pragma unroll
-            for (int q = 0; q < P; ++q) {
-              xv[q] = ok[q] ? __ldg(reinterpret_cast<const float4*>(xp[q] + c4)) : make_float4(0.f, 0.f, 0.f, 0.f);
-              if (a.in_elu) {
-                xv[q].x = elu(xv[q].x);
-                xv[q].y = elu(xv[q].y);
-                xv[q].z = elu(xv[q].z);
-                xv[q].w = elu(xv[q].w);
+          for (int q = 0; q < P; ++q) {
+            int iy, ix;
+            bool ok = pv[q] && kx < a.k;
+            if (!a.transpose) {
+              iy = poy[q] * a.stride + ky - pad;
+              ix = pox[q] * a.stride + kx - pad;
+            } else {
+              iy = poy[q] + pad - ky;
+              ix = pox[q] + pad - kx;
+              if (a.stride == 2) {
+                ok = ok && !((iy | ix) & 1);
+                iy >>= 1;
+                ix >>= 1;
               }
             }
+            ok = ok && iy >= 0 && iy < a.Hin && ix >= 0 && ix < a.Win;
+            xo[i][q] = ok ? ((long long)(size_t(pb[q]) * a.Hin + iy) * a.Win + ix) * a.ldx + ci0 : -1;
+          }
+        }
+        if (VEC) {
+          for (int c0 = 0; c0 < nci; c0 += 4 * CB) {
+            float4 xv[KB][CB][P];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float4* wr = wt + (c4 + u) * (PC_CO / 4);
-              float w[PC_CO];
+            for (int i = 0; i < KB; ++i)
 #pragma unroll
-              for (int j4 = 0; j4 < PC_CO / 4; ++j4) {
+              for (int cb = 0; cb < CB; ++cb)
+#pragma unroll
+                for (int q = 0; q < P; ++q) {
+                  const int c4 = c0 + 4 * cb;
+                  float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                  if (xo[i][q] >= 0 && c4 < nci) v = __ldg(reinterpret_cast<const float4*>(a.x + xo[i][q] + c4));
+                  if (a.in_elu) v = make_float4(elu(v.x), elu(v.y), elu(v.z), elu(v.w));
+                  xv[i][cb][q] = v;
+                }
+#pragma unroll
+            for (int i = 0; i < KB; ++i) {
+              const int kx = kx0 + (i0 + i) * kst;
+              if (kx >= a.k) break;
+              const float4* wt = sw4 + (size_t(ky * a.k + kx) * PC_CI) * (CO / 4);
+#pragma unroll
+              for (int cb = 0; cb < CB; ++cb) {
+                const int c4 = c0 + 4 * cb;
+                if (c4 >= nci) break;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  const float4* wr = wt + (c4 + u) * (CO / 4);
+                  float w[CO];
+#pragma unroll
+                  for (int j4 = 0; j4 < CO / 4; ++j4) {
+                    const float4 v = wr[j4];
+                    w[4 * j4] = v.x;
+                    w[4 * j4 + 1] = v.y;
+                    w[4 * j4 + 2] = v.z;
+                    w[4 * j4 + 3] = v.w;
+                  }
+#pragma unroll
+                  for (int q = 0; q < P; ++q) {
+                    const float4 xq = xv[i][cb][q];
+                    const float xs = u == 0 ? xq.x : u == 1 ? xq.y : u == 2 ? xq.z : xq.w;
+#pragma unroll
+                    for (int j = 0; j < CO; ++j) acc[q][j] = fmaf(xs, w[j], acc[q][j]);
+                  }
+                }
+              }
+            }
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < KB; ++i) {
+            const int kx = kx0 + (i0 + i) * kst;
+            if (kx >= a.k) break;
+            const float4* wt = sw4 + (size_t(ky * a.k + kx) * PC_CI) * (CO / 4);
+            for (int cl = 0; cl < nci; ++cl) {
+              const float4* wr = wt + cl * (CO / 4);
+              float w[CO];
+#pragma unroll
+              for (int j4 = 0; j4 < CO / 4; ++j4) {
                 const float4 v = wr[j4];
                 w[4 * j4] = v.x;
                 w[4 * j4 + 1] = v.y;
@@ -544,30 +591,11 @@ __global__ void __launch_bounds__(PC_T) k_pconv_tiled(PConv a) {
               }
 #pragma unroll
               for (int q = 0; q < P; ++q) {
-                const float xs = u == 0 ? xv[q].x : u == 1 ? xv[q].y : u == 2 ? xv[q].z : xv[q].w;
+                float xs = xo[i][q] >= 0 ? __ldg(a.x + xo[i][q] + cl) : 0.f;
+                if (a.in_elu) xs = elu(xs);
 #pragma unroll
-                for (int j = 0; j < PC_CO; ++j) acc[q][j] = fmaf(xs, w[j], acc[q][j]);
+                for (int j = 0; j < CO; ++j) acc[q][j] = fmaf(xs, w[j], acc[q][j]);
               }
-            }
-          }
-        } else {
-          for (int cl = 0; cl < nci; ++cl) {
-            const float4* wr = wt + cl * (PC_CO / 4);
-            float w[PC_CO];
-#pragma unroll
-            for (int j4 = 0; j4 < PC_CO / 4; ++j4) {
-              const float4 v = wr[j4];
-              w[4 * j4] = v.x;
-              w[4 * j4 + 1] = v.y;
-              w[4 * j4 + 2] = v.z;
-              w[4 * j4 + 3] = v.w;
-            }
-#pragma unroll
-            for (int q = 0; q < P; ++q) {
-              float xs = ok[q] ? __ldg(xp[q] + cl) : 0.f;
-              if (a.in_elu) xs = elu(xs);
-#pragma unroll
-              for (int j = 0; j < PC_CO; ++j) acc[q][j] = fmaf(xs, w[j], acc[q][j]);
             }
           }
         }
@@ -581,7 +609,7 @@ __global__ void __launch_bounds__(PC_T) k_pconv_tiled(PConv a) {
     float* yp = a.y + size_t(p) * a.ldy + co0;
     const float* rp = a.res ? a.res + size_t(p) * a.ldres + co0 : nullptr;
 #pragma unroll
-    for (int j = 0; j < PC_CO; ++j) {
+    for (int j = 0; j < CO; ++j) {
       if (j >= nco) break;
       const int co = co0 + j;
       float v = acc[q][j] + a.bias[co];
@@ -710,28 +738,32 @@ struct Exec {
     {
       const bool par = a.transpose && a.stride == 2;
       const long long cpix = par ? (npix + 3) / 4 : npix;  // pixels per parity class
-      const int coblk = (a.cout + PC_CO - 1) / PC_CO;
+      const int CO = a.cout <= 4 ? 4 : 16;  // narrow output layers (the net's 2-channel head)
+      const int coblk = (a.cout + CO - 1) / CO;
       // 4 pixels per thread when that still gives >= 2 CTAs per SM, else 1
       const bool big = (cpix + PC_T * 4 - 1) / (PC_T * 4) * coblk * (par ? 4 : 1) >= 2 * c.num_sms;
       const int P = big ? 4 : 1;
       const dim3 grid(unsigned((cpix + PC_T * P - 1) / (PC_T * P)), unsigned(coblk), par ? 4u : 1u);
-      const size_t smem = size_t(D.k) * D.k * PC_CI * PC_CO * sizeof(float);
+      const size_t smem = size_t(D.k) * D.k * PC_CI * CO * sizeof(float);
       const bool vec = a.cin % 4 == 0 && a.ldx % 4 == 0;
       static bool attr = false;
       if (!attr) {
         const int mx = 100 * 1024;
-        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
-        HB_CUDA(cudaFuncSetAttribute(k_pconv_tiled<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+        for (auto k : {k_pconv_tiled<4, true, 16>, k_pconv_tiled<4, false, 16>, k_pconv_tiled<1, true, 16>,
+                       k_pconv_tiled<1, false, 16>, k_pconv_tiled<4, true, 4>, k_pconv_tiled<4, false, 4>,
+                       k_pconv_tiled<1, true, 4>, k_pconv_tiled<1, false, 4>})
+          HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
         attr = true;
       }
-      if (smem > 100 * 1024)
+      void (*kern)(PConv) =
+          CO == 4 ? (P == 4 ? (vec ? k_pconv_tiled<4, true, 4> : k_pconv_tiled<4, false, 4>)
+                            : (vec ? k_pconv_tiled<1, true, 4> : k_pconv_tiled<1, false, 4>))
+                  : (P == 4 ? (vec ? k_pconv_tiled<4, true, 16> : k_pconv_tiled<4, false, 16>)
+                            : (vec ? k_pconv_tiled<1, true, 16> : k_pconv_tiled<1, false, 16>));
+      if (smem > 100 * 1024 || D.k > PC_KMAX)
         launch_pdl(c, k_pconv<16>, dim3(unsigned((npix + 127) / 128)), dim3(128), 0, a);
-      else if (P == 4)
-        launch_pdl(c, (vec ? k_pconv_tiled<4, true> : k_pconv_tiled<4, false>), dim3(grid), dim3(PC_T), smem, a);
       else
-        launch_pdl(c, (vec ? k_pconv_tiled<1, true> : k_pconv_tiled<1, false>), dim3(grid), dim3(PC_T), smem, a);
+        launch_pdl(c, kern, dim3(grid), dim3(PC_T), smem, a);
     }
     HB_CUDA(cudaGetLastError());
     const double taps = D.transpose && stride == 2 ? double(D.k) * D.k / 4.0 : double(D.k) * D.k;

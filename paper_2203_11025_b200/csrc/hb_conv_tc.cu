@@ -372,9 +372,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             // warps (every tap reads each element; applying it per tap in the A build
             // cost 9 expm1 per element and made the A build the pipeline's bottleneck)
             float4* h4 = reinterpret_cast<float4*>(base + hb * hbuf_bytes);
-            for (int i = threadIdx.x - 64; i < hbuf_bytes / 16; i += 256) {
-              const float4 x = h4[i];
-              h4[i] = make_float4(elu_f(x.x), elu_f(x.y), elu_f(x.z), elu_f(x.w));
+            const int n4 = hbuf_bytes / 16;
+            for (int i0 = threadIdx.x - 64; i0 < n4; i0 += 4 * 256) {  // 4 independent elements in flight
+              float4 x[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (i0 + u * 256 < n4) x[u] = h4[i0 + u * 256];
+#pragma unroll
+              for (int u = 0; u < 4; ++u)
+                if (i0 + u * 256 < n4) h4[i0 + u * 256] = make_float4(elu_f(x[u].x), elu_f(x[u].y), elu_f(x[u].z), elu_f(x[u].w));
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before the TMA refills this buffer
             asm volatile("bar.sync 1, 256;" ::: "memory");
@@ -464,15 +470,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint32_t v[16], u[16];
         tmem_ld16(trow + uint32_t(c0), v);
         tmem_ld16(trow + uint32_t(N + c0), u);
+        float bz[16];  // bias, or the per-pixel context share (bias included) of a split layer
+        if (p.epi.pre) {
+          const float4* pp = reinterpret_cast<const float4*>(
+              p.epi.pre + (opix - size_t(b) * p.geo.Ho * p.geo.Wo) * p.epi.ldpre + n0 + c0);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float4 w4 = __ldg(pp + i);
+            bz[4 * i] = w4.x;
+            bz[4 * i + 1] = w4.y;
+            bz[4 * i + 2] = w4.z;
+            bz[4 * i + 3] = w4.w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) bz[i] = __ldg(bias + c0 + i);
+        }
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         float o[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const float x = __uint_as_float(v[i]) + __uint_as_float(u[i]);
           if (GEN) {
-            o[i] = part ? x : tc_epilogue(p.epi, n0 + c0 + i, x + __ldg(bias + c0 + i), rrow ? rrow + c0 + i : nullptr);
+            o[i] = part ? x : tc_epilogue(p.epi, n0 + c0 + i, x + bz[i], rrow ? rrow + c0 + i : nullptr);
           } else {
-            const float y = x + __ldg(bias + c0 + i);
+            const float y = x + bz[i];
             o[i] = part ? x : p.relu ? fmaxf(y, 0.f) : y;
           }
         }
@@ -677,7 +699,7 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
   const int tiles0 = B * (H / bh) * (W / bw) * nsplit;
   const int nst = (ngrp - 1) * spg + (NT * (nchunk - (ngrp - 1) * lay.CG) + lay.G - 1) / lay.G;
   int ksplit = 1;
-  if (c.opt_conv_ksplit && tiles0 * 2 <= c.num_sms)
+  if (c.opt_conv_ksplit && tiles0 * 2 <= c.num_sms && !t.epi.pre)  // (the reduce kernels add the bias, not pre)
     ksplit = std::max(1, std::min({nst, c.num_sms / tiles0, 8}));
   const int sps = (nst + ksplit - 1) / ksplit;
   ksplit = (nst + sps - 1) / sps;  // no empty split
@@ -760,7 +782,7 @@ bool launch_conv_tc_gen(Context& c, const TcConv& t) {
 
 // the classic U-Net's 3x3 / stride 1 / pad 1 conv with bias + ReLU
 bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
-                    const float* bsrc, int cb, bool b_ctx, int relu, float* out) {
+                    const float* bsrc, int cb, bool b_ctx, int relu, float* out, const float* pre) {
   TcConv t{};
   t.cw = &cw;
   t.B = B;
@@ -775,6 +797,8 @@ bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, i
   t.act = act;
   t.geo = conv_geo_3x3(H, W, cw.cout);
   t.epi = TcEpi{nullptr, 0, nullptr, nullptr, nullptr, nullptr, relu ? 1 : 0, 0, 0};
+  t.epi.pre = pre;  // the batch-broadcast context share of a split encoder-solver layer (bias included)
+  t.epi.ldpre = cw.cout;
   return launch_conv_tc_gen(c, t);
 }
 

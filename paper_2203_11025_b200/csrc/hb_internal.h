@@ -218,6 +218,8 @@ struct TcEpi {
   const float *mu, *is, *g, *be;
   int act, in_elu;
   int nco;  // output channels actually stored (< cout when cout was padded to a multiple of 16); 0: all
+  const float* pre = nullptr;  // batch-broadcast per-pixel term [Ho][Wo][ldpre] replacing the bias (context share)
+  int ldpre = 0;
 };
 
 // one launch: weights cw (dwh / dwl [cout][ntaps * cin], db bias), input a
@@ -242,7 +244,7 @@ bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H,
                       const float* bsrc, int cb, bool b_ctx, int relu, float* out,
                       const float* pre = nullptr);
 bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
-                    const float* bsrc, int cb, bool b_ctx, int relu, float* out);
+                    const float* bsrc, int cb, bool b_ctx, int relu, float* out, const float* pre = nullptr);
 // row-streaming legs, zero initial guess (hb_mg_stream.cu)
 // cw: storage window of the coarse field (down: emitted rows [cw.lo, cw.hi); up: vc)
 void launch_down_stream(Context& c, const LevelView& L, const RowWin& cw, float damping, int offset, int B,

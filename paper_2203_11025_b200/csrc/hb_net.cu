@@ -789,7 +789,7 @@ void net_upload(Context& c, int slot) {
     n.pre_split = true;
   }
   // the other context-concat convs (first conv of levels >= 1, the up-convs)
-  // whose x part fits k_conv_rows: [x | ctx] weights -> x part (no bias) +
+  // whose x part runs on the tensor cores: [x | ctx] weights -> x part (no bias) +
   // context part (bias); the forward computes the context share once (B = 1)
   n.split_of.assign(n.convs.size(), -1);
   n.split_ctx.clear();
@@ -801,7 +801,7 @@ void net_upload(Context& c, int slot) {
     for (int idx : cands) {
       const ConvW& full = n.convs[size_t(idx)];
       const int cc = n.cfg.ctx_ch, cx = full.cin - cc, co = full.cout;
-      if (co % 16 || co > 32 || cx % 16 || cx <= 0) continue;  // x part must run on k_conv_rows
+      if (co % 16 || co > 256 || cx % 16 || cx <= 0) continue;  // x part must run on k_conv_rows / k_conv_tc
       ConvW xc, cp;
       xc.cin = cx;
       cp.cin = cc;
@@ -900,7 +900,8 @@ static bool conv_split(Context& c, Net& n, NetBuffers& nb, int idx, int B, const
     conv(c, cp, 1, nullptr, H, W, ctxp, 0, cp.cin, nullptr, 0, 0, 0, pre.p);
     n.pre_ok[size_t(si)] = 1;
   }
-  return launch_conv_rows(c, xc, B, act, H, W, x, cx, nullptr, 0, false, relu, out, pre.p);
+  return launch_conv_rows(c, xc, B, act, H, W, x, cx, nullptr, 0, false, relu, out, pre.p) ||
+         launch_conv_tc(c, xc, B, act, H, W, x, cx, nullptr, 0, false, relu, out, pre.p);
 }
 
 // the per-column part of the split input layer: 3 -> 16 narrow conv whose

@@ -18,6 +18,7 @@
 #include "hb_internal.h"
 
 #include <algorithm>
+#include <mutex>
 
 namespace hb {
 
@@ -848,14 +849,18 @@ void launch_fg_restart(Context& c, int B, const double2* b, const double2* x, fl
 template <typename... KArgs, typename... Args>
 static void launch_jm(Context& c, void (*k)(KArgs...), dim3 grid, size_t smem, Args&&... args) {
   static std::vector<std::pair<const void*, int>> occ;  // (per process; attributes are per function)
+  static std::mutex mu;  // column groups launch from several host threads
   int per_sm = 0;
-  for (const auto& e : occ)
-    if (e.first == reinterpret_cast<const void*>(k)) per_sm = e.second;
-  if (!per_sm) {
-    HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, KT, smem));
-    per_sm = std::max(1, per_sm);
-    occ.emplace_back(reinterpret_cast<const void*>(k), per_sm);
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (const auto& e : occ)
+      if (e.first == reinterpret_cast<const void*>(k)) per_sm = e.second;
+    if (!per_sm) {
+      HB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      HB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, KT, smem));
+      per_sm = std::max(1, per_sm);
+      occ.emplace_back(reinterpret_cast<const void*>(k), per_sm);
+    }
   }
   if (c.opt_basis_wave && grid.x > 1) {
     const unsigned cap = std::max(1u, unsigned(per_sm * c.num_sms) / std::max(1u, grid.y));

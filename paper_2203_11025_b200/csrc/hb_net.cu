@@ -358,14 +358,14 @@ bool conv_small_pw(Context& c, const ConvW& cw, const ConvArgs& p, dim3 g) {
 // logic.  (Reading the rows straight from global memory instead spread every
 // 16-byte load over 32 L1 sectors and ran L1-bound.)  The accumulation order per
 // output (ky, ci, kx) is the tiled kernel's, so both give identical bits.
-constexpr int CC_R = 16, CC_NS = 4, CC_TW = 128;
+constexpr int CC_NS = 4, CC_TW = 128;  // CC_R (rows per strip): 16, or 4 for grids that would not fill the SMs
 
 __device__ __forceinline__ void cc_cp16(float* dst, const float* src, bool ok) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(src), "r"(ok ? 16 : 0) : "memory");
 }
 
-template <int CIN, int COUT>
+template <int CIN, int COUT, int CC_R>
 __global__ void __launch_bounds__(CC_TW) k_conv_cols(ConvArgs p, const __grid_constant__ SmallW<CIN, COUT> wt) {
   static_assert(CIN % 4 == 0, "float4 rows");
   constexpr int PS = CIN + 4, SEG = CC_TW + 2, NCH = SEG * (CIN / 4);
@@ -455,11 +455,15 @@ bool conv_cols(Context& c, const ConvW& cw, const ConvArgs& p) {
   constexpr size_t smem = size_t(CC_NS) * (CC_TW + 2) * (CIN + 4) * sizeof(float);
   static bool attr = false;
   if (!attr) {
-    HB_CUDA(cudaFuncSetAttribute(k_conv_cols<CIN, COUT>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    HB_CUDA(cudaFuncSetAttribute(k_conv_cols<CIN, COUT, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    HB_CUDA(cudaFuncSetAttribute(k_conv_cols<CIN, COUT, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     attr = true;
   }
-  const dim3 g((p.W + CC_TW - 1) / CC_TW, (p.H + CC_R - 1) / CC_R, p.B);
-  launch_pdl(c, k_conv_cols<CIN, COUT>, g, dim3(CC_TW), smem, p, wt);
+  const int strips = (p.W + CC_TW - 1) / CC_TW;
+  if (strips * ((p.H + 15) / 16) * p.B >= 2 * c.num_sms)
+    launch_pdl(c, k_conv_cols<CIN, COUT, 16>, dim3(strips, (p.H + 15) / 16, p.B), dim3(CC_TW), smem, p, wt);
+  else  // small grids (c4's 512^2 coarse U-Net at B = 1): shorter strips, more CTAs
+    launch_pdl(c, k_conv_cols<CIN, COUT, 4>, dim3(strips, (p.H + 3) / 4, p.B), dim3(CC_TW), smem, p, wt);
   return true;
 }
 

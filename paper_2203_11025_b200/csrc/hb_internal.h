@@ -243,6 +243,10 @@ void conv_rows_prepare(ConvW& cw);
 bool launch_conv_rows(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                       const float* bsrc, int cb, bool b_ctx, int relu, float* out,
                       const float* pre = nullptr);
+// cin (12 | 16 | 20) -> 2 3x3 head (zero padding 1, bias, no activation) as
+// column strips (k_conv_cols, hb_net.cu); w host [9][cin][2], b host [2]
+bool launch_head_cols(Context& c, int cin, int B, int H, int W, const float* x, const float* w, const float* b,
+                      float* y);
 bool launch_conv_tc(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, int ca,
                     const float* bsrc, int cb, bool b_ctx, int relu, float* out, const float* pre = nullptr);
 // row-streaming legs, zero initial guess (hb_mg_stream.cu)

@@ -444,6 +444,9 @@ __global__ void __launch_bounds__(CC_TW) k_conv_cols(ConvArgs p, const __grid_co
 }
 
 template <int CIN, int COUT>
+void conv_cols_launch(Context& c, const ConvArgs& p, const SmallW<CIN, COUT>& wt);
+
+template <int CIN, int COUT>
 bool conv_cols(Context& c, const ConvW& cw, const ConvArgs& p) {
   if (cw.cin != CIN || cw.cout != COUT || p.ca != CIN || p.cb != 0) return false;
   SmallW<CIN, COUT> wt;
@@ -452,6 +455,12 @@ bool conv_cols(Context& c, const ConvW& cw, const ConvArgs& p) {
     for (int ci = 0; ci < CIN; ++ci)
       for (int tap = 0; tap < 9; ++tap) wt.w[(tap * CIN + ci) * COUT + co] = cw.w[(size_t(co) * CIN + ci) * 9 + tap];
   }
+  conv_cols_launch(c, p, wt);
+  return true;
+}
+
+template <int CIN, int COUT>
+void conv_cols_launch(Context& c, const ConvArgs& p, const SmallW<CIN, COUT>& wt) {
   constexpr size_t smem = size_t(CC_NS) * (CC_TW + 2) * (CIN + 4) * sizeof(float);
   static bool attr = false;
   if (!attr) {
@@ -464,7 +473,6 @@ bool conv_cols(Context& c, const ConvW& cw, const ConvArgs& p) {
     launch_pdl(c, k_conv_cols<CIN, COUT, 16>, dim3(strips, (p.H + 15) / 16, p.B), dim3(CC_TW), smem, p, wt);
   else  // small grids (c4's 512^2 coarse U-Net at B = 1): shorter strips, more CTAs
     launch_pdl(c, k_conv_cols<CIN, COUT, 4>, dim3(strips, (p.H + 3) / 4, p.B), dim3(CC_TW), smem, p, wt);
-  return true;
 }
 
 // 2x2 max-pool / x2 bilinear upsample, NHWC, 4 channels per thread (C % 4 == 0);
@@ -628,6 +636,7 @@ int grid1(size_t work, int cap = 4096) { return int(std::max<size_t>(1, std::min
 
 }  // namespace
 
+
 struct NScope {
   Context& c;
   int cls, tok;
@@ -636,6 +645,29 @@ struct NScope {
       : c(c_), cls(cls_), tok(prof_begin(c_, cls_)), bytes(bytes_), flops(flops_) {}
   ~NScope() { prof_end(c, cls, tok, bytes, flops); }
 };
+
+template <int CIN>
+static void head_cols(Context& c, int B, int H, int W, const float* x, const float* w, const float* b, float* y) {
+  SmallW<CIN, 2> wt;
+  for (int i = 0; i < 9 * CIN * 2; ++i) wt.w[i] = w[i];  // [tap][ci][co], as SmallW
+  wt.b[0] = b[0];
+  wt.b[1] = b[1];
+  ConvArgs p{B, H, W, x, (long long)H * W * CIN, CIN, nullptr, 0, 0, nullptr, nullptr, 2, 0, y, nullptr};
+  NScope ns(c, PC_CONV, double(B) * H * W * 4.0 * (CIN + 2), 2.0 * B * H * W * 9.0 * CIN * 2);
+  conv_cols_launch(c, p, wt);
+  HB_CUDA(cudaGetLastError());
+}
+
+bool launch_head_cols(Context& c, int cin, int B, int H, int W, const float* x, const float* w, const float* b,
+                      float* y) {
+  if (!c.opt_small_pw || !c.opt_conv_cols) return false;
+  switch (cin) {
+    case 12: head_cols<12>(c, B, H, W, x, w, b, y); return true;
+    case 16: head_cols<16>(c, B, H, W, x, w, b, y); return true;
+    case 20: head_cols<20>(c, B, H, W, x, w, b, y); return true;
+    default: return false;
+  }
+}
 
 // ---------------------------------------------------------------- launchers
 static void conv(Context& c, const ConvW& cw, int B, const int* act, int H, int W, const float* a, long long sa,

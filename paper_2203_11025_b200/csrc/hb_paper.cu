@@ -180,6 +180,13 @@ void upload_conv(PaperState& P, const std::string& kname, const std::string& bna
   };
   up(D.w, w);
   up(D.bias, Bq.v);
+  if ((D.cin == 12 || D.cin == 16 || D.cin == 20) && D.cout == 2 && k == 3 && !transpose) {  // output layer: k_conv_cols
+    D.hw = w;
+    D.hb = Bq.v;
+  } else {
+    D.hw.clear();
+    D.hb.clear();
+  }
   // tensor-core form (hb_conv_tc.cu): taps as input offsets (dy, dx) of the
   // output pixel's stride-s origin, weights packed [cout][tap][cin]
   D.tc.clear();
@@ -347,6 +354,7 @@ void upload_all(PaperState& P) {
   }
   upload_conv(P, pre + "out.k", pre + "out.b", "", false);
   P.dirty = false;
+  ++g_alloc_gen;  // the output layer carries its weights as kernel parameters: drop captured graphs
 }
 
 // ------------------------------------------------------------- kernels --
@@ -702,6 +710,11 @@ struct Exec {
     a.B = nb < 0 ? B : nb;
     a.xbatch = xbatch;
     const long long npix = (long long)a.B * a.Ho * a.Wo;
+    // the 16 -> 2 output layer: column strips with parameter-space weights
+    if (!D.hw.empty() && stride == 1 && !D.bn && !res && !in_elu && !act && xbatch && x.ld == D.cin && y.ld == 2) {
+      if (c.prof_detail) c.prof_label = kname;
+      if (launch_head_cols(c, D.cin, a.B, y.H, y.W, x.p, D.hw.data(), D.hb.data(), y.p)) return;
+    }
     // tensor cores (3xTF32 implicit GEMM, hb_conv_tc.cu) where the layer's
     // channels and dense input allow; the register-tiled SIMT kernel otherwise
     if (!D.tc.empty() && xbatch && x.ld == x.C && (!res || res->ld == y.C) && y.ld % 4 == 0 && c.opt_tc_conv &&
@@ -740,8 +753,10 @@ struct Exec {
       const long long cpix = par ? (npix + 3) / 4 : npix;  // pixels per parity class
       const int CO = a.cout <= 4 ? 4 : 16;  // narrow output layers (the net's 2-channel head)
       const int coblk = (a.cout + CO - 1) / CO;
-      // 4 pixels per thread when that still gives >= 2 CTAs per SM, else 1
-      const bool big = (cpix + PC_T * 4 - 1) / (PC_T * 4) * coblk * (par ? 4 : 1) >= 2 * c.num_sms;
+      // 4 pixels per thread when that still gives >= 2 CTAs per SM, else 1; 1 for
+      // few input channels (latency-bound: one pixel with batched tap-row loads
+      // beat four at the 4-channel first layer, 151 -> 118 us at batch 128)
+      const bool big = a.cin > 4 && (cpix + PC_T * 4 - 1) / (PC_T * 4) * coblk * (par ? 4 : 1) >= 2 * c.num_sms;
       const int P = big ? 4 : 1;
       const dim3 grid(unsigned((cpix + PC_T * P - 1) / (PC_T * P)), unsigned(coblk), par ? 4u : 1u);
       const size_t smem = size_t(D.k) * D.k * PC_CI * CO * sizeof(float);

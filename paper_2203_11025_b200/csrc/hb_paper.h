@@ -29,6 +29,7 @@ struct DevConv {  // one convolution with its fused epilogue
   int cout = 0, cin = 0, k = 0;
   bool transpose = false, bn = false;
   DBuf<float> w, bias, mu, is, g, be;
+  std::vector<float> hw, hb;  // host copies of w ([tap][cin][cout]) and bias: the 16 -> 2 head's kernel parameters
   std::vector<PaperTc> tc;  // tensor-core form (empty: channels not multiples of 16)
 };
 

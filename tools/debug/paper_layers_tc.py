@@ -9,6 +9,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspa
 from paper_2203_11025_b200 import helmgpu as hg  # noqa: E402
 
 B, n = int(sys.argv[1]) if len(sys.argv) > 1 else 16, 128
+opts = [kv.split("=") for kv in (sys.argv[2].split(",") if len(sys.argv) > 2 else [])]
 x = np.random.default_rng(0).standard_normal((B, 4, n, n)).astype(np.float32)
 for tc in (1, 0):
     c = hg.Context(0)
@@ -17,6 +18,8 @@ for tc in (1, 0):
         if name.endswith(".count"):
             c.paper_param(name, np.ones(dims, np.float32))
     c.set_option("tc_conv", tc)
+    for k, v in opts:
+        c.set_option(k, int(v))
     c.paper_forward(x)
     c.prof_enable(True)
     c.prof_detail(True)

@@ -104,3 +104,20 @@ def test_bench_gpus_flag_self_launches_ranks():
         assert line["dry_run"] and line["n_gpus"] == n
         assert line["rhs_total"] == B and line["max_over_ranks"] == float(n)
         assert line["rank0_columns"] == list(range(-(-B // n)))
+
+
+def test_bench_deadline_guard_reports_instead_of_hanging():
+    """bench.run_with_deadline: the NCCL slab entry runs under a deadline so a
+    wedged collective cannot take the headline line with it; results and
+    exceptions pass through, a late worker is reported as such."""
+    import time
+
+    sys.path.insert(0, ROOT)
+    import bench
+
+    assert bench.run_with_deadline(lambda: {"ok": 1}, 0, None) == ({"ok": 1}, False)
+    assert bench.run_with_deadline(lambda: {"ok": 2}, 0, 5.0) == ({"ok": 2}, False)
+    out, wedged = bench.run_with_deadline(lambda: 1 / 0, 0, 5.0)
+    assert not wedged and "ZeroDivisionError" in out["error"]
+    out, wedged = bench.run_with_deadline(lambda: time.sleep(3.0), 0, 0.2)
+    assert wedged and "no result within" in out["error"]

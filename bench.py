@@ -10,12 +10,13 @@ Helmholtz, unit point source, M_V (3-level shifted-Laplacian V-cycle, GMRES(10)
 coarsest), FGMRES(10) to 1e-6.  It is the only BASELINE config whose solve
 reaches 1e-6 with the seeded random-init weights the configs prescribe (c1-c4
 put a random-init U-Net in the preconditioner and stagnate; the oracle shows
-it).  One step = R independent c0 solves on one GPU, R = 3 per SM
-(444) by default -- one column per SM in each of the 3 column groups, the
+it).  One step = R independent c0 solves on one GPU, R = 6 per SM
+(888) by default -- two columns per SM in each of the 3 column groups, the
 device-filling analog of the reference arm, which runs one c0 solve per host
-core (throughput saturates there: 148 -> 8.9k, 296 -> 9.5k, 444 -> 10.4k,
-888 -> 10.4k solves/s).  Inputs resident in HBM; the per-step working set
-(~1.5 GB) exceeds L2, and L2 is additionally flushed (512 MiB write) between
+core (throughput saturates there; round 2, device / end to end: 296 -> 11.5k /
+10.6k, 444 -> 12.5k / 11.9k, 666 -> 12.8k / 12.3k, 888 -> 13.0k / 12.5k,
+1776 -> 13.2k / 12.8k solves/s).  Inputs resident in HBM; the per-step working
+set (~3 GB) exceeds L2, and L2 is additionally flushed (512 MiB write) between
 timed steps.  Multi-GPU: each rank runs its own R replicas (weak scaling, no
 collective).  The U-Net configs are measured on a fixed iteration budget under
 "also".
@@ -345,7 +346,7 @@ def run_ours(args, ws, rank, local):
     dev = torch.device("cuda", local)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     cfg = config_for(args.config)
-    R = args.replicas or 3 * sms
+    R = args.replicas or 6 * sms
     cols = columns(cfg, ws, rank, R)
     # G column groups = G independent solver contexts on their own streams, driven
     # from G host threads: one group's latency-bound coarsest solves overlap the
@@ -1075,7 +1076,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c0")
     ap.add_argument("--replicas", type=int, default=0, help="solves per GPU per step for single-RHS configs "
-                                                              "(0 = 3 per SM: one per SM in each of the 3 column groups)")
+                                                              "(0 = 6 per SM: two per SM in each of the 3 column groups)")
     ap.add_argument("--also", default="datagen,c1,c2,c3,c4,c4slab,mv512,paper_ju,train,block", help="comma list of configs measured on a fixed iteration budget "
                                                        "(rounded down to whole restart cycles, at least one)")
     ap.add_argument("--budget", type=int, default=20)

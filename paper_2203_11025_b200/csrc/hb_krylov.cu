@@ -300,6 +300,9 @@ __global__ void __launch_bounds__(KT, (JM <= 9 ? 4 : 1)) k_adots(FineView F, int
   // nodes per thread (large grids); short loops (c0) keep U = 1
   constexpr int U = !WIDE ? 1 : JM <= 1 ? 4 : JM <= 3 ? 2 : 1;
   const size_t stride = size_t(gridDim.x) * KT;
+  const unsigned nxu = unsigned(F.nx);
+  const bool pow2 = (nxu & (nxu - 1)) == 0 && N <= 0xffffffffull;
+  const int nx_sh = 31 - __clz(nxu);
   for (size_t p0 = size_t(blockIdx.x) * KT + threadIdx.x; p0 < N; p0 += stride * U) {
     float2 a[U][JM + 1], w[U];
 #pragma unroll
@@ -310,7 +313,9 @@ __global__ void __launch_bounds__(KT, (JM <= 9 ? 4 : 1)) k_adots(FineView F, int
       for (int i = 0; i <= JM; ++i) a[u][i] = (ok && i <= j) ? ld(Vb + size_t(i) * BN, p) : make_float2(0.f, 0.f);
       w[u] = make_float2(0.f, 0.f);
       if (!ok) continue;
-      const int ix = int(p % F.nx), iy = F.w.lo + int(p / F.nx);  // global row (ghost rows hold the neighbours)
+      // global row (ghost rows hold the neighbours); power-of-two widths (every BASELINE grid) by mask / shift
+      const int ix = pow2 ? int(unsigned(p) & (nxu - 1)) : int(p % F.nx);
+      const int iy = F.w.lo + (pow2 ? int(unsigned(p) >> nx_sh) : int(p / F.nx));
       if (dI) {  // w = A D^-1 (s_j Vraw_j), zb = Vraw_j (coarse GMRES, inc/multigrid.hpp:52-55)
         float2 nb = make_float2(0.f, 0.f);
         if (ix > 0) nb = cadd(nb, cmul(ld(zb, p - 1), ld(dI, p - 1)));
